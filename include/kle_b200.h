@@ -1,0 +1,150 @@
+/*
+ * kle_b200.h — C ABI of libkle_b200.so, the sm_100a implementation of the
+ * KLE-CGC data-parallel hot path (arXiv 2510.26180; reference package
+ * `pintuq`, /root/reference/pkg/src/pintuq).
+ *
+ * Conventions (all entry points):
+ *  - every array argument is a DEVICE pointer owned by the caller; fp64
+ *    throughout; sample-major C order exactly as the reference's per-sample
+ *    arrays stacked over samples: a trajectory block is [M][N][nx]
+ *    (CoarseTrajectory.states, pintuq/core.py:150-166), a tridiagonal
+ *    operator is dia[M][nx], off[M][nx] (off[s][i] couples rows i and i+1;
+ *    off[s][nx-1] is unused);
+ *  - `stream` is a cudaStream_t passed as void*; all work is stream ordered,
+ *    no implicit device synchronisation except where stated;
+ *  - return 0 on success, else a KLE_ERR_* code; kle_last_error() returns a
+ *    message for the calling thread's last failure. No exceptions cross the ABI;
+ *  - no hidden allocation: scratch/workspace is caller provided and sized by
+ *    the matching *_bytes query; no global mutable state beyond the
+ *    thread-local error string (reentrant on distinct streams).
+ *
+ * The reference has no FFI for this path (it is pure numpy/scipy); each entry
+ * point below names the reference function it replaces. INTEGRATION.md shows
+ * the Python (ctypes) binding the reference package would add.
+ */
+#ifndef KLE_B200_H
+#define KLE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KLE_ABI_VERSION 1
+
+/* status codes */
+#define KLE_OK 0
+#define KLE_ERR_INVALID 1
+#define KLE_ERR_CUDA 2
+#define KLE_ERR_UNSUPPORTED 3
+#define KLE_ERR_WORKSPACE 4
+
+/* per-sample status words written by kle_pcgc_solve_f64 / kle_cgc_update_f64 */
+#define KLE_SAMPLE_ACTIVE 0
+#define KLE_SAMPLE_CONVERGED 1   /* increment <= tol            (pintuq/pcgc.py:345-348) */
+#define KLE_SAMPLE_MAXITERS 2    /* MaxItersExceededError       (pintuq/pcgc.py:352-357) */
+#define KLE_SAMPLE_NONFINITE 3   /* CoarseTrajectory.assert_finite (pintuq/core.py:179-181) */
+
+int kle_abi_version(void);
+const char* kle_last_error(void);
+
+/* Chunking of the register-resident tridiagonal solver for a given nx:
+ * rows are padded to MR*P; the factor blob holds blob_doubles per sample. */
+int kle_fine_layout(int nx, int* MR, int* P, int* blob_doubles);
+
+/* LogNormalKL1D.linear_system (plugin contract pintuq/models.py:114-116):
+ * a(m_j) = exp(sum_k kl_table[k][j] xi[s][k]) on the nx+1 midpoints,
+ * dia = (a_j + a_{j+1}) inv_h2, off = -a_{j+1} inv_h2. xi is [M][d],
+ * kl_table is [d][nx+1]. */
+int kle_kl_tridiag_f64(const double* xi, int M, int d, const double* kl_table, int nx, double inv_h2,
+                       double* dia, double* off, void* stream);
+
+/* _linear_factor (pintuq/propagators.py:25-34): factor I + h*A for every
+ * sample into the solver blob (size M * blob_doubles); g0 is the constant
+ * source value (g(t) = g0 * ones). */
+int kle_fine_factor_f64(const double* dia, const double* off, int M, int nx, double h, double g0,
+                        double* blob, void* stream);
+
+/* propagate_fine / propagate_coarse / fine_reference / coarse_sweep_init
+ * (pintuq/propagators.py:121-176, pintuq/parareal.py:74-84):
+ * out[s][q][g] = (J backward-Euler steps of size h)^(g+1) applied to
+ * start[s][q], g = 0..nseg-1. start is [M][Q][nx], out is [M][Q][nseg][nx]. */
+int kle_sweep_f64(const double* start, double* out, const double* blob, int M, int Q, int nx, int J,
+                  int nseg, double h, double g0, void* stream);
+
+/* Fused fine sweep + CGC right-hand side of one PCGC iteration
+ * (pintuq/pcgc.py:321-330 fine sweeps; assemble_rhs_blocks :175-197;
+ *  cgc_correct rhs :233-237):
+ *   F_n   = F(from_n),  from = [u0, U_1..U_{N-1}]
+ *   R_n   = scaling_n * ((I + dT A) F_n - prev_n),  prev = [alpha U_N, U_1..U_{N-1}]
+ * which equals scaling_n * (dT (A b_n + g) + b_n) with b_n = F_n - G(prev_n).
+ * F_given (optional) skips the sweep; F_out (optional) stores F. status
+ * (optional) skips samples whose status word is not ACTIVE. */
+int kle_fgr_f64(const double* U, const double* u0, const double* F_given, double* F_out, double* R,
+                const double* fine_blob, const double* dia, const double* off, const double* scaling,
+                const int32_t* status, int M, int N, int nx, int J, double dt, double dT, double g0,
+                double alpha, void* stream);
+
+/* Scratch for the three-step solve (per-CTA slabs). */
+size_t kle_cgc_scratch_bytes(int M, int N, int nx);
+
+/* three_step_solve (pintuq/pcgc.py:148-172) over M samples:
+ *   u = diag(1/scaling) F (lambda I + dT A)^{-1} F* diag(scaling) r
+ * r, u are [M][N][nx]; lam is [N] interleaved complex (re, im) =
+ * build_alpha_circulant(N, alpha).eigenvalues (pintuq/pcgc.py:68-76),
+ * scaling / inv_scaling its scaling and 1/scaling; imag[M] (optional)
+ * receives max|Im u| per sample. */
+int kle_three_step_f64(const double* r, const double* scaling, const double* inv_scaling, const double* lam,
+                       const double* dia, const double* off, int M, int N, int nx, double dT, double* u,
+                       double* imag, void* scratch, size_t scratch_bytes, void* stream);
+
+/* CGC update of one PCGC iteration k (pintuq/pcgc.py:331-348): U <- three_step(R)
+ * in place, increment = max|U_new - U| per sample, stop test against tol,
+ * status/iters updated, inc_hist[s][k-1] and imag[s] recorded, and
+ * *active_count incremented once per still-active sample. R must already be
+ * alpha-scaled (kle_fgr_f64 output). */
+int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, const double* lam,
+                       const double* dia, const double* off, int M, int N, int nx, double dT, int k,
+                       int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
+                       double* imag, int32_t* active_count, void* scratch, size_t scratch_bytes,
+                       void* stream);
+
+/* Full outer loop of pcgc_solve (pintuq/pcgc.py:273-358) with
+ * stop_on="increment" for M samples at once, each frozen at its own
+ * iteration count. U: in = initial guess states [M][N][nx], out = final
+ * states. status/iters [M], inc_hist [M][max_iters] (NaN-initialised by the
+ * call), imag [M]. Synchronises the stream once per outer iteration (a
+ * 4-byte read of the active-sample count). */
+size_t kle_pcgc_workspace_bytes(int M, int N, int nx);
+int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const double* off,
+                       const double* fine_blob, const double* scaling, const double* inv_scaling,
+                       const double* lam, int M, int N, int nx, int J, double T, double alpha, double g0,
+                       double tol, int max_iters, int32_t* status, int32_t* iters, double* inc_hist,
+                       double* imag, void* workspace, size_t workspace_bytes, void* stream);
+
+/* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
+ * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);
+ * norms[degree+1] = 1/sqrt(k!). */
+int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
+                      const double* norms, double* Psi, void* stream);
+
+/* surrogate_predict batched (pintuq/surrogate.py:321-333):
+ * U0[M][L] = mean[L] + Psi[M][K] * C[K][L]  (FP64 tensor cores, DMMA). */
+int kle_gpc_eval_f64(const double* Psi, int M, int K, const double* C, const double* mean, int L, double* U0,
+                     void* stream);
+
+/* Moments (absent in the reference): out[l] = sum_s U[s][l]
+ * (center == NULL) or sum_s (U[s][l] - center[l])^2. Deterministic order. */
+size_t kle_col_sum_scratch_bytes(int M, int L);
+int kle_col_sum_f64(const double* U, int M, int L, const double* center, double* out, void* scratch,
+                    void* stream);
+
+/* out = a*x + b*y (n elements). */
+int kle_axpby_f64(const double* x, const double* y, double* out, double a, double b, size_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KLE_B200_H */

@@ -1,0 +1,34 @@
+"""B200-native KLE-CGC hot path (arXiv 2510.26180): the fine propagator, the
+diagonalised coarse-grid correction and the Hermite-gPC surrogate
+evaluation as sm_100a CUDA kernels behind a C ABI (``include/kle_b200.h``),
+with a host API mirroring the reference package ``pintuq``.
+"""
+from .core import (
+    CoarseTrajectory,
+    ConfigError,
+    DeviceError,
+    InitMode,
+    IterationRecord,
+    IterationTrace,
+    MaxItersExceededError,
+    NonConvergenceError,
+    ParameterSample,
+    PintuqError,
+    RankDeficientError,
+    RngStream,
+    SingularShiftError,
+    SnapshotError,
+    SolverConfig,
+    TimeGrid,
+    make_time_grid,
+)
+from .models import LinearModel, LogNormalKL1D, Model, ParameterMap, get_model
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CoarseTrajectory", "ConfigError", "DeviceError", "InitMode", "IterationRecord", "IterationTrace",
+    "LinearModel", "LogNormalKL1D", "MaxItersExceededError", "Model", "NonConvergenceError",
+    "ParameterMap", "ParameterSample", "PintuqError", "RankDeficientError", "RngStream",
+    "SingularShiftError", "SnapshotError", "SolverConfig", "TimeGrid", "get_model", "make_time_grid",
+]

@@ -1,0 +1,231 @@
+// extern "C" boundary of libkle_b200.so (declared in include/kle_b200.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/kle_b200.h"
+#include "kle_common.cuh"
+#include "kle_internal.h"
+
+namespace kle {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const char* msg) {
+  g_err = msg ? msg : "";
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    return set_error(KLE_ERR_CUDA, m.c_str());
+  }
+  return KLE_OK;
+}
+
+static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace kle
+
+using namespace kle;
+
+#define KLE_STREAM(s) (reinterpret_cast<cudaStream_t>(s))
+#define KLE_TRY(expr)            \
+  do {                           \
+    const int _rc = (expr);      \
+    if (_rc != KLE_OK) return _rc; \
+  } while (0)
+
+extern "C" {
+
+int kle_abi_version(void) { return KLE_ABI_VERSION; }
+
+const char* kle_last_error(void) { return g_err.c_str(); }
+
+int kle_fine_layout(int nx, int* MR, int* P, int* blob_doubles) {
+  const FineLayoutRT l = fine_layout(nx);
+  if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "nx exceeds the largest supported fine layout (1024)");
+  if (MR) *MR = l.MR;
+  if (P) *P = l.P;
+  if (blob_doubles) *blob_doubles = l.doubles;
+  return KLE_OK;
+}
+
+int kle_kl_tridiag_f64(const double* xi, int M, int d, const double* kl_table, int nx, double inv_h2,
+                       double* dia, double* off, void* stream) {
+  if (M < 0 || d < 1 || nx < 1) return set_error(KLE_ERR_INVALID, "kl_tridiag: bad dims");
+  return kl_tridiag(xi, M, d, kl_table, nx, inv_h2, dia, off, KLE_STREAM(stream));
+}
+
+int kle_fine_factor_f64(const double* dia, const double* off, int M, int nx, double h, double g0,
+                        double* blob, void* stream) {
+  if (M < 0 || nx < 1 || !(h > 0)) return set_error(KLE_ERR_INVALID, "fine_factor: bad arguments");
+  if (M == 0) return KLE_OK;
+  const FineLayoutRT l = fine_layout(nx);
+  if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: nx too large");
+  return fine_factor(l, dia, off, blob, M, nx, h, g0, KLE_STREAM(stream));
+}
+
+int kle_sweep_f64(const double* start, double* out, const double* blob, int M, int Q, int nx, int J,
+                  int nseg, double h, double g0, void* stream) {
+  if (M < 0 || Q < 0 || nx < 1 || J < 1 || nseg < 1) return set_error(KLE_ERR_INVALID, "sweep: bad dims");
+  if (M == 0 || Q == 0) return KLE_OK;
+  const FineLayoutRT l = fine_layout(nx);
+  if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "sweep: nx too large");
+  SweepArgs a{start, out, blob, M, Q, nx, J, nseg, h, g0};
+  return fine_sweep(l, a, KLE_STREAM(stream));
+}
+
+int kle_fgr_f64(const double* U, const double* u0, const double* F_given, double* F_out, double* R,
+                const double* fine_blob, const double* dia, const double* off, const double* scaling,
+                const int32_t* status, int M, int N, int nx, int J, double dt, double dT, double g0,
+                double alpha, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || J < 1) return set_error(KLE_ERR_INVALID, "fgr: bad dims");
+  if (M == 0) return KLE_OK;
+  const FineLayoutRT l = fine_layout(nx);
+  if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "fgr: nx too large");
+  FgrArgs a{U, u0, F_given, F_out, R, fine_blob, dia, off, scaling, status, M, N, nx, J, dt, dT, g0, alpha};
+  return fine_fgr(l, a, KLE_STREAM(stream));
+}
+
+size_t kle_cgc_scratch_bytes(int M, int N, int nx) {
+  if (M <= 0 || N <= 0 || nx <= 0) return 0;
+  return (size_t)cgc_grid(M, N, nx) * cgc_scratch_doubles_per_cta(N, nx) * sizeof(double);
+}
+
+int kle_three_step_f64(const double* r, const double* scaling, const double* inv_scaling, const double* lam,
+                       const double* dia, const double* off, int M, int N, int nx, double dT, double* u,
+                       double* imag, void* scratch, size_t scratch_bytes, void* stream) {
+  if (M < 0 || N < 1 || nx < 1) return set_error(KLE_ERR_INVALID, "three_step: bad dims");
+  if (M == 0) return KLE_OK;
+  if (scratch_bytes < kle_cgc_scratch_bytes(M, N, nx)) return set_error(KLE_ERR_WORKSPACE, "three_step: scratch too small");
+  if (imag) cudaMemsetAsync(imag, 0, sizeof(double) * M, KLE_STREAM(stream));
+  CgcArgs a{};
+  a.R = r;
+  a.load_scale = scaling;
+  a.U = nullptr;
+  a.Uout = u;
+  a.dia = dia;
+  a.off = off;
+  a.lam = lam;
+  a.inv_scaling = inv_scaling;
+  a.scratch = static_cast<double*>(scratch);
+  a.scratch_doubles_per_cta = cgc_scratch_doubles_per_cta(N, nx);
+  a.imag = imag;
+  a.M = M;
+  a.N = N;
+  a.nx = nx;
+  a.k = 1;
+  a.max_iters = 1;
+  a.dT = dT;
+  a.tol = 0.0;
+  return cgc_run(a, KLE_STREAM(stream));
+}
+
+int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, const double* lam,
+                       const double* dia, const double* off, int M, int N, int nx, double dT, int k,
+                       int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
+                       double* imag, int32_t* active_count, void* scratch, size_t scratch_bytes,
+                       void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || k < 1 || max_iters < k) return set_error(KLE_ERR_INVALID, "cgc_update: bad arguments");
+  if (M == 0) return KLE_OK;
+  if (scratch_bytes < kle_cgc_scratch_bytes(M, N, nx)) return set_error(KLE_ERR_WORKSPACE, "cgc_update: scratch too small");
+  CgcArgs a{};
+  a.R = R;
+  a.U = U;
+  a.dia = dia;
+  a.off = off;
+  a.lam = lam;
+  a.inv_scaling = inv_scaling;
+  a.scratch = static_cast<double*>(scratch);
+  a.scratch_doubles_per_cta = cgc_scratch_doubles_per_cta(N, nx);
+  a.status = status;
+  a.iters = iters;
+  a.inc_hist = inc_hist;
+  a.imag = imag;
+  a.active_count = active_count;
+  a.M = M;
+  a.N = N;
+  a.nx = nx;
+  a.k = k;
+  a.max_iters = max_iters;
+  a.dT = dT;
+  a.tol = tol;
+  return cgc_run(a, KLE_STREAM(stream));
+}
+
+size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
+  if (M <= 0 || N <= 0 || nx <= 0) return 0;
+  return align256((size_t)M * N * nx * sizeof(double)) + align256(kle_cgc_scratch_bytes(M, N, nx)) + 256;
+}
+
+int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const double* off,
+                       const double* fine_blob, const double* scaling, const double* inv_scaling,
+                       const double* lam, int M, int N, int nx, int J, double T, double alpha, double g0,
+                       double tol, int max_iters, int32_t* status, int32_t* iters, double* inc_hist,
+                       double* imag, void* workspace, size_t workspace_bytes, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || J < 1 || max_iters < 1 || !(T > 0) || !(alpha > 0 && alpha < 1))
+    return set_error(KLE_ERR_INVALID, "pcgc_solve: bad arguments");
+  if (M == 0) return KLE_OK;
+  if (workspace_bytes < kle_pcgc_workspace_bytes(M, N, nx))
+    return set_error(KLE_ERR_WORKSPACE, "pcgc_solve: workspace too small");
+  cudaStream_t st = KLE_STREAM(stream);
+  char* ws = static_cast<char*>(workspace);
+  double* R = reinterpret_cast<double*>(ws);
+  ws += align256((size_t)M * N * nx * sizeof(double));
+  const size_t scratch_bytes = kle_cgc_scratch_bytes(M, N, nx);
+  void* scratch = ws;
+  ws += align256(scratch_bytes);
+  int32_t* counter = reinterpret_cast<int32_t*>(ws);
+
+  const double dT = T / N, dt = dT / J;
+  cudaMemsetAsync(status, 0, sizeof(int32_t) * M, st);
+  cudaMemsetAsync(iters, 0, sizeof(int32_t) * M, st);
+  if (inc_hist) cudaMemsetAsync(inc_hist, 0xFF, sizeof(double) * (size_t)M * max_iters, st);
+  if (imag) cudaMemsetAsync(imag, 0, sizeof(double) * M, st);
+  KLE_TRY(check_launch("pcgc_solve: init"));
+  int32_t h_count = M;
+  for (int k = 1; k <= max_iters && h_count > 0; ++k) {
+    KLE_TRY(kle_fgr_f64(U, u0, nullptr, nullptr, R, fine_blob, dia, off, scaling, status, M, N, nx, J, dt, dT, g0,
+                        alpha, stream));
+    cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
+    KLE_TRY(kle_cgc_update_f64(R, U, inv_scaling, lam, dia, off, M, N, nx, dT, k, max_iters, tol, status, iters,
+                               inc_hist, imag, counter, scratch, scratch_bytes, stream));
+    cudaMemcpyAsync(&h_count, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(KLE_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return KLE_OK;
+}
+
+int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
+                      const double* norms, double* Psi, void* stream) {
+  if (M < 0 || d < 1 || P < 1) return set_error(KLE_ERR_INVALID, "gpc_basis: bad dims");
+  return gpc_basis(xi, M, d, degree, midx, P, norms, Psi, KLE_STREAM(stream));
+}
+
+int kle_gpc_eval_f64(const double* Psi, int M, int K, const double* C, const double* mean, int L, double* U0,
+                     void* stream) {
+  if (M < 0 || K < 1 || L < 1) return set_error(KLE_ERR_INVALID, "gpc_eval: bad dims");
+  return gemm_bias(Psi, C, mean, U0, M, K, L, KLE_STREAM(stream));
+}
+
+size_t kle_col_sum_scratch_bytes(int M, int L) {
+  if (L <= 0) return 0;
+  return col_sum_partial_doubles(M, L) * sizeof(double);
+}
+
+int kle_col_sum_f64(const double* U, int M, int L, const double* center, double* out, void* scratch,
+                    void* stream) {
+  if (M < 0 || L < 0) return set_error(KLE_ERR_INVALID, "col_sum: bad dims");
+  return col_sum(U, M, L, center, out, static_cast<double*>(scratch), KLE_STREAM(stream));
+}
+
+int kle_axpby_f64(const double* x, const double* y, double* out, double a, double b, size_t n, void* stream) {
+  return axpby(x, y, out, a, b, n, KLE_STREAM(stream));
+}
+
+}  // extern "C"

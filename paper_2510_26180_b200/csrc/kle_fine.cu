@@ -1,0 +1,307 @@
+// Fine propagator F, coarse propagator G and the fused "F + CGC right-hand
+// side" kernel for the 1D KL-coefficient diffusion operator.
+//
+// Reference counterparts:
+//   propagate_fine        pintuq/propagators.py:121-145  (J x splu.solve)
+//   propagate_coarse      pintuq/propagators.py:148-157
+//   assemble_rhs_blocks   pintuq/pcgc.py:175-197
+//   cgc_correct (rhs)     pintuq/pcgc.py:233-237
+//
+// The fused kernel uses the identity (G = (I + dT A)^{-1}(prev + dT g)):
+//   rhs_n = dT (A b_n + g) + b_n,  b_n = F_n - G(prev_n)
+//         = (I + dT A) F_n - prev_n
+// so the coarse solve of the reference collapses to one matvec.
+#include "kle_fine.cuh"
+#include "kle_internal.h"
+
+namespace kle {
+
+// ---------------------------------------------------------------------------
+// Factor kernel: one thread per sample, sequential LDL^T of T = I + h A and
+// the chunk/scan tables of the partitioned solve (layout: kle_common.cuh).
+// ---------------------------------------------------------------------------
+template <int MR, int P>
+__global__ void fine_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
+                                   double* __restrict__ blob, int M, int nx, double h, double g0) {
+  using L = FineLayout<MR, P>;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= M) return;
+  const double* d = dia + (size_t)s * nx;
+  const double* e = off + (size_t)s * nx;  // e[i] couples rows i, i+1; e[nx-1] unused
+  double* b = blob + (size_t)s * L::DOUBLES;
+  // pass 1: l_i and inv_i
+  double beta_prev = 1.0;
+  for (int row = 0; row < L::NXP; ++row) {
+    const int j = row % MR, k = row / MR;
+    double l = 0.0, inv = 1.0;
+    if (row < nx) {
+      const double D = fma(h, d[row], 1.0);
+      double beta = D;
+      if (row > 0) {
+        const double E = h * e[row - 1];
+        l = E / beta_prev;
+        beta = fma(-l, E, D);
+      }
+      inv = 1.0 / beta;
+      beta_prev = beta;
+    }
+    b[L::L_OFF + j * P + k] = l;
+    b[L::INV_OFF + j * P + k] = inv;
+  }
+  // pass 2: chunk products, kappa
+  const double hg = h * g0;
+  for (int k = 0; k < P; ++k) {
+    double pi = 1.0;
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      pi *= -b[L::L_OFF + j * P + k];
+      b[L::PIH_OFF + j * P + k] = pi * b[L::INV_OFF + j * P + k];
+      double lnext = 0.0;
+      if (row + 1 < L::NXP) lnext = b[L::L_OFF + ((row + 1) % MR) * P + (row + 1) / MR];
+      b[L::KAP_OFF + j * P + k] = (row < nx) ? hg * (1.0 + lnext) : 0.0;
+    }
+    double sg = 1.0;
+    for (int j = MR - 1; j >= 0; --j) {
+      const int row = k * MR + j;
+      double lnext = 0.0;
+      if (row + 1 < L::NXP) lnext = b[L::L_OFF + ((row + 1) % MR) * P + (row + 1) / MR];
+      sg *= -lnext;
+      b[L::SIG_OFF + j * P + k] = sg;
+    }
+  }
+  // pass 3: Kogge-Stone multipliers.  pie_k = pi at chunk end (before the
+  // inv scaling), sigs_k = sigma at chunk start.
+  double pie[P], sigs[P];
+  for (int k = 0; k < P; ++k) {
+    double pi = 1.0;
+    for (int j = 0; j < MR; ++j) pi *= -b[L::L_OFF + j * P + k];
+    pie[k] = pi;
+    sigs[k] = b[L::SIG_OFF + 0 * P + k];
+  }
+  for (int t = 0; t < L::LOGP; ++t) {
+    const int dd = 1 << t;
+    for (int k = 0; k < P; ++k) {
+      double af = 0.0, bb = 0.0;
+      if (k >= dd) {
+        af = 1.0;
+        for (int q = k - dd + 1; q <= k; ++q) af *= pie[q];
+      }
+      if (k + dd < P) {
+        bb = 1.0;
+        for (int q = k; q <= k + dd - 1; ++q) bb *= sigs[q];
+      }
+      b[L::AF_OFF + t * P + k] = af;
+      b[L::BB_OFF + t * P + k] = bb;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused F + rhs kernel. CTA = (group of subintervals, sample).
+// ---------------------------------------------------------------------------
+template <int MR, int P, int R, int NT>
+__global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
+  using L = FineLayout<MR, P>;
+  constexpr int SLOTS = 32 / P;
+  constexpr int NC = (NT / 32) * SLOTS * R;  // subintervals per CTA
+  extern __shared__ double sfac[];
+  const int s = blockIdx.y;
+  if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int k = lane % P, slot = lane / P;
+  const int nx = a.nx, N = a.N;
+  const size_t sbase = (size_t)s * N * nx;
+
+  int nr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) nr[r] = blockIdx.x * NC + (w * SLOTS + slot) * R + r;
+
+  double x[R][MR];
+  if (a.F_given == nullptr) {
+    const double* gb = a.ffac + (size_t)s * L::DOUBLES;
+    for (int i = tid; i < L::DOUBLES; i += NT) sfac[i] = gb[i];
+    const double hg = a.dt * a.g0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = k * MR + j;
+        double v = 0.0;
+        if (row < nx && nr[r] < N) {
+          const double st = (nr[r] == 0) ? a.u0[row] : a.U[sbase + (size_t)(nr[r] - 1) * nx + row];
+          v = st + hg;
+        }
+        x[r][j] = v;
+      }
+    }
+    __syncthreads();
+    for (int it = 0; it < a.J; ++it) be_solve<MR, P, R>(x, sfac, k);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < MR; ++j) x[r][j] = (k * MR + j < nx) ? x[r][j] - hg : 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = k * MR + j;
+        x[r][j] = (row < nx && nr[r] < N) ? a.F_given[sbase + (size_t)nr[r] * nx + row] : 0.0;
+      }
+  }
+  if (a.F_out) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = k * MR + j;
+        if (row < nx && nr[r] < N) a.F_out[sbase + (size_t)nr[r] * nx + row] = x[r][j];
+      }
+  }
+  // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n)
+  const double* dd = a.dia + (size_t)s * nx;
+  const double* ee = a.off + (size_t)s * nx;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double left = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
+    const double right = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
+    if (nr[r] >= N) continue;
+    const double sc = a.scaling[nr[r]];
+    const size_t prow = (nr[r] == 0) ? sbase + (size_t)(N - 1) * nx : sbase + (size_t)(nr[r] - 1) * nx;
+    const double pmul = (nr[r] == 0) ? a.alpha : 1.0;
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      if (row >= nx) continue;
+      const double xm = (j > 0) ? x[r][j - 1] : (k > 0 ? left : 0.0);
+      const double xp = (j < MR - 1) ? x[r][j + 1] : (k < P - 1 ? right : 0.0);
+      const double em = (row > 0) ? ee[row - 1] : 0.0;
+      const double ep = (row < nx - 1) ? ee[row] : 0.0;
+      const double Ax = fma(em, xm, fma(dd[row], x[r][j], ep * xp));
+      const double prev = pmul * a.U[prow + row];
+      const double rhs = fma(a.dT, Ax, x[r][j]) - prev;
+      a.Rout[sbase + (size_t)nr[r] * nx + row] = sc * rhs;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stand-alone sweep: out[s][q*nseg + g] = F^{(g+1)}(start[s][q]) where each
+// segment is J steps of size h (blob built for that h). nseg = 1 gives
+// propagate_fine / propagate_coarse (J=1, coarse blob); q = 1, nseg = N gives
+// fine_reference / coarse_sweep_init.
+// ---------------------------------------------------------------------------
+template <int MR, int P, int R, int NT>
+__global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
+  using L = FineLayout<MR, P>;
+  constexpr int SLOTS = 32 / P;
+  constexpr int NC = (NT / 32) * SLOTS * R;
+  extern __shared__ double sfac[];
+  const int s = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int k = lane % P, slot = lane / P;
+  const int nx = a.nx, Q = a.Q;
+  const double* gb = a.fac + (size_t)s * L::DOUBLES;
+  for (int i = tid; i < L::DOUBLES; i += NT) sfac[i] = gb[i];
+  int q[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) q[r] = blockIdx.x * NC + (w * SLOTS + slot) * R + r;
+  const double hg = a.h * a.g0;
+  double x[R][MR];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      x[r][j] = (row < nx && q[r] < Q) ? a.start[((size_t)s * Q + q[r]) * nx + row] + hg : 0.0;
+    }
+  __syncthreads();
+  for (int g = 0; g < a.nseg; ++g) {
+    for (int it = 0; it < a.J; ++it) be_solve<MR, P, R>(x, sfac, k);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (q[r] >= Q) continue;
+      double* o = a.out + (((size_t)s * Q + q[r]) * a.nseg + g) * nx;
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = k * MR + j;
+        if (row < nx) o[row] = x[r][j] - hg;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+// ---------------------------------------------------------------------------
+template <int MR, int P>
+struct FineInst {
+  static constexpr int R = (MR >= 32) ? 2 : (MR >= 8 ? 2 : 4);
+  static constexpr int NT = 128;
+  static constexpr int NC = (NT / 32) * (32 / P) * R;
+
+  static int factor(const double* dia, const double* off, double* blob, int M, int nx, double h,
+                    double g0, cudaStream_t st) {
+    fine_factor_kernel<MR, P><<<(M + 63) / 64, 64, 0, st>>>(dia, off, blob, M, nx, h, g0);
+    return check_launch("fine_factor_kernel");
+  }
+  static int fgr(const FgrArgs& a, cudaStream_t st) {
+    const size_t smem = (a.F_given ? 1 : FineLayout<MR, P>::DOUBLES) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    dim3 grid((a.N + NC - 1) / NC, a.M);
+    fgr_kernel<MR, P, R, NT><<<grid, NT, smem, st>>>(a);
+    return check_launch("fgr_kernel");
+  }
+  static int sweep(const SweepArgs& a, cudaStream_t st) {
+    const size_t smem = FineLayout<MR, P>::DOUBLES * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sweep_kernel<MR, P, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    dim3 grid((a.Q + NC - 1) / NC, a.M);
+    sweep_kernel<MR, P, R, NT><<<grid, NT, smem, st>>>(a);
+    return check_launch("sweep_kernel");
+  }
+};
+
+#define KLE_FINE_DISPATCH(MR_, P_, CALL) \
+  if (lay.MR == MR_ && lay.P == P_) return FineInst<MR_, P_>::CALL;
+
+#define KLE_FINE_ALL(CALL)            \
+  KLE_FINE_DISPATCH(1, 16, CALL)      \
+  KLE_FINE_DISPATCH(2, 16, CALL)      \
+  KLE_FINE_DISPATCH(4, 16, CALL)      \
+  KLE_FINE_DISPATCH(8, 16, CALL)      \
+  KLE_FINE_DISPATCH(16, 16, CALL)     \
+  KLE_FINE_DISPATCH(32, 16, CALL)     \
+  KLE_FINE_DISPATCH(32, 32, CALL)
+
+FineLayoutRT fine_layout(int nx) {
+  static const int cand[][2] = {{1, 16}, {2, 16}, {4, 16}, {8, 16}, {16, 16}, {32, 16}, {32, 32}};
+  for (auto& c : cand)
+    if (c[0] * c[1] >= nx) return {c[0], c[1], fine_blob_doubles(c[0], c[1])};
+  return {0, 0, 0};
+}
+
+int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,
+                double h, double g0, cudaStream_t st) {
+  KLE_FINE_ALL(factor(dia, off, blob, M, nx, h, g0, st))
+  return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: unsupported nx");
+}
+
+int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
+  KLE_FINE_ALL(fgr(a, st))
+  return set_error(KLE_ERR_UNSUPPORTED, "fgr: unsupported nx");
+}
+
+int fine_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st) {
+  KLE_FINE_ALL(sweep(a, st))
+  return set_error(KLE_ERR_UNSUPPORTED, "sweep: unsupported nx");
+}
+
+}  // namespace kle

@@ -1,0 +1,85 @@
+// Internal (C++) interfaces between the kernel translation units and the
+// C-ABI layer (kle_capi.cu). Not exported.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace kle {
+
+int set_error(int code, const char* msg);
+int check_launch(const char* what);
+
+struct FineLayoutRT {
+  int MR, P, doubles;
+};
+FineLayoutRT fine_layout(int nx);
+
+struct FgrArgs {
+  const double* U;        // [M][N][nx] current iterate (U_1..U_N)
+  const double* u0;       // [nx] initial state (shared by all samples)
+  const double* F_given;  // optional [M][N][nx]: skip the sweep, use these F ends
+  double* F_out;          // optional [M][N][nx]: also store the F ends
+  double* Rout;           // [M][N][nx] scaled CGC right-hand sides
+  const double* ffac;     // fine factor blobs [M][doubles]
+  const double* dia;      // [M][nx]
+  const double* off;      // [M][nx] (entry nx-1 unused)
+  const double* scaling;  // [N] alpha^(n/N)
+  const int32_t* active;  // [M] sample status (0 = active) or null
+  int M, N, nx, J;
+  double dt, dT, g0, alpha;
+};
+
+struct SweepArgs {
+  const double* start;  // [M][Q][nx]
+  double* out;          // [M][Q][nseg][nx]
+  const double* fac;    // blobs [M][doubles] for step h
+  int M, Q, nx, J, nseg;
+  double h, g0;
+};
+
+int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,
+                double h, double g0, cudaStream_t st);
+int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st);
+int fine_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st);
+
+struct CgcArgs {
+  const double* R;          // [M][N][nx] right-hand sides (already alpha-scaled unless load_scale)
+  const double* load_scale; // optional [N]: multiply R rows on load (stand-alone three-step)
+  double* U;                // [M][N][nx] in: U^k (for the increment), out: U^{k+1} (fused mode)
+  double* Uout;             // optional separate output (stand-alone mode); then U may be null
+  const double* dia;        // [M][nx]
+  const double* off;        // [M][nx]
+  const double* lam;        // [2*N] interleaved (re, im) eigenvalues of C_alpha
+  const double* inv_scaling;// [N] 1/alpha^(n/N)
+  double* scratch;          // per-CTA slabs
+  size_t scratch_doubles_per_cta;
+  int32_t* status;          // optional [M] sample status (fused mode)
+  int32_t* iters;           // optional [M]
+  double* inc;              // optional [M] increment of this iteration
+  double* inc_hist;         // optional [M][max_iters]
+  double* imag;             // optional [M] running max imaginary residue
+  int32_t* active_count;    // optional device counter of still-active samples
+  int M, N, nx, k, max_iters;
+  double dT, tol;
+};
+
+int cgc_grid(int M, int N, int nx);
+size_t cgc_scratch_doubles_per_cta(int N, int nx);
+int cgc_run(const CgcArgs& a, cudaStream_t st);
+
+int kl_tridiag(const double* xi, int M, int d, const double* table, int nx, double inv_h2, double* dia,
+               double* off, cudaStream_t st);
+
+int gpc_basis(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
+              const double* norms, double* Psi, cudaStream_t st);
+int gemm_bias(const double* A, const double* B, const double* bias, double* C, int M, int K, int L,
+              cudaStream_t st);
+
+int col_sum(const double* U, int M, int L, const double* center, double* out, double* partial,
+            cudaStream_t st);
+size_t col_sum_partial_doubles(int M, int L);
+
+int axpby(const double* x, const double* y, double* out, double a, double b, size_t n, cudaStream_t st);
+
+}  // namespace kle

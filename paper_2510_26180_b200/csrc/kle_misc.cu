@@ -1,0 +1,139 @@
+// Coefficient field, Hermite gPC basis, moments and small element-wise ops.
+#include "kle_common.cuh"
+#include "kle_internal.h"
+
+namespace kle {
+
+// a(m_j) = exp(sum_k table[k][j] xi_k) on the nx+1 midpoints, then the
+// tridiagonal A (models.py LogNormalKL1D.tridiagonal; the reference plugin
+// contract is pintuq/models.py:114-116). One CTA per sample.
+__global__ void kl_tridiag_kernel(const double* __restrict__ xi, int d, const double* __restrict__ table,
+                                  int nx, double inv_h2, double* __restrict__ dia, double* __restrict__ off) {
+  extern __shared__ double a[];
+  const int s = blockIdx.x;
+  const double* x = xi + (size_t)s * d;
+  for (int j = threadIdx.x; j <= nx; j += blockDim.x) {
+    double la = 0.0;
+    for (int k = 0; k < d; ++k) la = fma(table[(size_t)k * (nx + 1) + j], x[k], la);
+    a[j] = exp(la);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    dia[(size_t)s * nx + i] = (a[i] + a[i + 1]) * inv_h2;
+    off[(size_t)s * nx + i] = (i < nx - 1) ? -a[i + 1] * inv_h2 : 0.0;
+  }
+}
+
+int kl_tridiag(const double* xi, int M, int d, const double* table, int nx, double inv_h2, double* dia,
+               double* off, cudaStream_t st) {
+  if (M <= 0) return KLE_OK;
+  const size_t smem = (size_t)(nx + 1) * sizeof(double);
+  if (smem > 200 * 1024) return set_error(KLE_ERR_UNSUPPORTED, "kl_tridiag: nx too large");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kl_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  kl_tridiag_kernel<<<M, 256, smem, st>>>(xi, d, table, nx, inv_h2, dia, off);
+  return check_launch("kl_tridiag_kernel");
+}
+
+// Psi[s][col] = prod_d He~_{k_d}(xi_{s,d}) in gpc_multi_indices order, with
+// the same recurrence, normalisation and product order as
+// gpc_basis_matrix + _hermite_table (pintuq/surrogate.py:222-248).
+constexpr int GPC_MAXDEG = 8;
+constexpr int GPC_MAXDIM = 32;
+
+__global__ void gpc_basis_kernel(const double* __restrict__ xi, int M, int d, int degree,
+                                 const int32_t* __restrict__ midx, int P, const double* __restrict__ norms,
+                                 double* __restrict__ Psi) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= M) return;
+  double T[GPC_MAXDIM][GPC_MAXDEG + 1];
+  for (int k = 0; k < d; ++k) {
+    const double x = xi[(size_t)s * d + k];
+    T[k][0] = 1.0;
+    if (degree >= 1) T[k][1] = x;
+    // no FMA contraction: bit-identical to the numpy recurrence
+    for (int q = 1; q < degree; ++q) T[k][q + 1] = __dsub_rn(__dmul_rn(x, T[k][q]), __dmul_rn((double)q, T[k][q - 1]));
+    for (int q = 0; q <= degree; ++q) T[k][q] = __dmul_rn(T[k][q], norms[q]);
+  }
+  for (int col = 0; col < P; ++col) {
+    double b = 1.0;
+    for (int k = 0; k < d; ++k) {
+      const int kd = midx[col * d + k];
+      if (kd) b = __dmul_rn(b, T[k][kd]);
+    }
+    Psi[(size_t)s * P + col] = b;
+  }
+}
+
+int gpc_basis(const double* xi, int M, int d, int degree, const int32_t* midx, int P, const double* norms,
+              double* Psi, cudaStream_t st) {
+  if (d > GPC_MAXDIM || degree > GPC_MAXDEG || degree < 0)
+    return set_error(KLE_ERR_UNSUPPORTED, "gpc_basis: degree/dimension too large");
+  if (M <= 0) return KLE_OK;
+  gpc_basis_kernel<<<(M + 127) / 128, 128, 0, st>>>(xi, M, d, degree, midx, P, norms, Psi);
+  return check_launch("gpc_basis_kernel");
+}
+
+// Deterministic column sums over samples: out[l] = sum_s (U[s][l] - c[l])^p,
+// p = 1 without a center, p = 2 with one (two-pass variance).
+constexpr int CS_CHUNKS = 64;
+
+__global__ void col_sum_partial_kernel(const double* __restrict__ U, int M, int L,
+                                       const double* __restrict__ center, double* __restrict__ partial) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const int chunk = blockIdx.y, nch = gridDim.y;
+  const int s0 = (int)(((long long)M * chunk) / nch), s1 = (int)(((long long)M * (chunk + 1)) / nch);
+  double acc = 0.0;
+  if (center) {
+    const double c = center[l];
+    for (int s = s0; s < s1; ++s) {
+      const double v = U[(size_t)s * L + l] - c;
+      acc = fma(v, v, acc);
+    }
+  } else {
+    for (int s = s0; s < s1; ++s) acc += U[(size_t)s * L + l];
+  }
+  partial[(size_t)chunk * L + l] = acc;
+}
+
+__global__ void col_sum_final_kernel(const double* __restrict__ partial, int nch, int L, double* __restrict__ out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  double acc = 0.0;
+  for (int c = 0; c < nch; ++c) acc += partial[(size_t)c * L + l];
+  out[l] = acc;
+}
+
+size_t col_sum_partial_doubles(int M, int L) {
+  const int nch = M < CS_CHUNKS ? (M > 0 ? M : 1) : CS_CHUNKS;
+  return (size_t)nch * L;
+}
+
+int col_sum(const double* U, int M, int L, const double* center, double* out, double* partial, cudaStream_t st) {
+  if (L <= 0) return KLE_OK;
+  const int nch = M < CS_CHUNKS ? (M > 0 ? M : 1) : CS_CHUNKS;
+  dim3 g1((L + 255) / 256, nch);
+  col_sum_partial_kernel<<<g1, 256, 0, st>>>(U, M, L, center, partial);
+  col_sum_final_kernel<<<(L + 255) / 256, 256, 0, st>>>(partial, nch, L, out);
+  return check_launch("col_sum");
+}
+
+__global__ void axpby_kernel(const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ o,
+                             double a, double b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    o[i] = a * x[i] + b * y[i];
+}
+
+int axpby(const double* x, const double* y, double* out, double a, double b, size_t n, cudaStream_t st) {
+  if (n == 0) return KLE_OK;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  axpby_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, y, out, a, b, n);
+  return check_launch("axpby_kernel");
+}
+
+}  // namespace kle

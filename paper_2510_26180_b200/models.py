@@ -1,0 +1,215 @@
+"""Model plugins for the KLE-CGC hot path.
+
+The reference's plugin surface is ``LinearModel`` (``pintuq/models.py:109-125``):
+a model returns ``(A, g)`` with ``rhs(u, t) = -A u + g(t)``. The BASELINE
+configs need a *random-coefficient* diffusion model that the reference does
+not ship, so it is added here as a ``LinearModel`` subclass:
+
+``LogNormalKL1D``  u_t - (a(x, w) u_x)_x = f on (0, 1), zero Dirichlet,
+    u0 = sin(pi x), f = 1, nx interior nodes x_i = (i+1) h, h = 1/(nx+1);
+    log a = sum_k sqrt(lam_k) phi_k(x) xi_k, the d-term KL expansion of the
+    exponential covariance sigma^2 exp(-|x-y|/ell), xi_k iid N(0, 1).
+
+Discretisation (flux form, conservative): a is evaluated at the nx+1 cell
+midpoints m_j = (j + 1/2) h; A is tridiagonal with
+    A_ii     = (a_i + a_{i+1}) / h^2
+    A_i,i+1  = A_i+1,i = -a_{i+1} / h^2.
+A is a symmetric, strictly diagonally dominant M-matrix, so both
+(I + dt A) and (lambda_n I + dT A) (Re lambda_n > 0) admit pivot-free LU
+(this is what makes the device's no-pivot tridiagonal solvers exact
+restatements of SuperLU / LAPACK ?gbsv up to rounding).
+
+KL eigenpairs: Nystrom on the midpoint grid with uniform weight h,
+``eigh(sigma^2 exp(-|m_i - m_j|/ell) * h)``, eigenfunctions normalised to
+sum(phi^2) h = 1 and signed so that phi_k(m_0) > 0. Computed once per model
+on the host (the ``kl_table``), uploaded once, shared by all samples.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .core import ConfigError, ParameterSample, RngStream
+
+
+@dataclass(frozen=True)
+class ParameterMap:
+    """Coordinate map used by the surrogate fit (``pintuq/models.py:25-52``),
+    extended with ``identity`` for the Hermite (Gaussian) surrogates: the
+    reference's ``affine(-1, 1)`` is not bit-exact identity."""
+
+    kind: str
+    lo: float
+    hi: float
+
+    def apply(self, v):
+        v = np.asarray(v, dtype=float)
+        if self.kind == "identity":
+            return v.copy()
+        if self.kind == "affine":
+            return 2.0 * (v - self.lo) / (self.hi - self.lo) - 1.0
+        if self.kind == "cos2pi":
+            return np.cos(2.0 * np.pi * v)
+        raise ConfigError(f"unknown parameter map kind {self.kind!r}")
+
+    def to_dict(self) -> dict:
+        return {"kind": self.kind, "lo": self.lo, "hi": self.hi}
+
+    @staticmethod
+    def from_dict(d: dict) -> "ParameterMap":
+        return ParameterMap(str(d["kind"]), float(d["lo"]), float(d["hi"]))
+
+
+class Model:
+    """Interface shared by the models (``pintuq/models.py:61-106``)."""
+
+    name: str = ""
+    nx: int = 0
+    parameter_dim: int = 1
+    supports: tuple = ()
+    is_linear: bool = False
+
+    @property
+    def cell_volume(self) -> float:
+        raise NotImplementedError
+
+    def rhs(self, u, t, xi):
+        raise NotImplementedError
+
+    def jacobian(self, u, t, xi):
+        raise NotImplementedError
+
+    def initial_condition(self, xi):
+        raise NotImplementedError
+
+    def sample_parameters(self, count: int, rng: RngStream) -> list:
+        raise NotImplementedError
+
+    def fit_maps(self) -> list:
+        return [ParameterMap("affine", lo, hi) for lo, hi in self.supports]
+
+    def validate(self, xi: ParameterSample):
+        if xi.dim != self.parameter_dim:
+            raise ValueError(f"{self.name}: expected {self.parameter_dim} parameters, got {xi.dim}")
+        for v, (lo, hi) in zip(xi.values, self.supports):
+            if not lo <= v <= hi:
+                raise ValueError(f"{self.name}: parameter {v} outside support [{lo}, {hi}]")
+
+    def check_state(self, u):
+        u = np.asarray(u, dtype=float)
+        if u.shape != (self.nx,):
+            raise ValueError(f"{self.name}: state has shape {u.shape}, expected ({self.nx},)")
+        return u
+
+
+class LinearModel(Model):
+    """rhs(u, t) = -A u + g(t) (``pintuq/models.py:109-125``)."""
+
+    is_linear = True
+
+    def linear_system(self, xi: ParameterSample):
+        raise NotImplementedError
+
+    def rhs(self, u, t, xi):
+        u = self.check_state(u)
+        A, g = self.linear_system(xi)
+        return -(A @ u) + g(t)
+
+    def jacobian(self, u, t, xi):
+        A, _ = self.linear_system(xi)
+        return -A
+
+
+def exponential_kl_1d(points: np.ndarray, weight: float, sigma: float, ell: float, d: int):
+    """Nystrom KL of sigma^2 exp(-|x-y|/ell) on ``points`` with quadrature
+    ``weight``: returns (lam (d,), phi (d, len(points))) with sum(phi^2) w = 1
+    and phi_k[0] > 0."""
+    x = np.asarray(points, dtype=float)
+    K = (sigma * sigma) * np.exp(-np.abs(x[:, None] - x[None, :]) / ell) * weight
+    lam, vec = np.linalg.eigh(K)
+    order = np.argsort(lam)[::-1][:d]
+    lam = lam[order]
+    phi = vec[:, order].T / np.sqrt(weight)
+    phi *= np.where(phi[:, :1] < 0.0, -1.0, 1.0)
+    return lam, phi
+
+
+class LogNormalKL1D(LinearModel):
+    """1D log-normal random-coefficient diffusion (BASELINE configs 1, 2, 4, 5)."""
+
+    name = "lognormal-kl-1d"
+
+    def __init__(self, nx: int = 127, d: int = 4, sigma: float = 0.5, ell: float = 0.3,
+                 source: float = 1.0):
+        if nx < 1 or d < 1:
+            raise ConfigError("need nx >= 1 and d >= 1")
+        self.nx = int(nx)
+        self.parameter_dim = int(d)
+        self.supports = tuple((-np.inf, np.inf) for _ in range(self.parameter_dim))
+        self.h = 1.0 / (self.nx + 1)
+        self.sigma = float(sigma)
+        self.ell = float(ell)
+        self.source = float(source)
+        self.x = np.arange(1, self.nx + 1) * self.h
+        self.midpoints = (np.arange(self.nx + 1) + 0.5) * self.h
+        lam, phi = exponential_kl_1d(self.midpoints, self.h, self.sigma, self.ell, self.parameter_dim)
+        self.kl_eigenvalues = lam
+        self.kl_functions = phi
+        # row k: sqrt(lam_k) phi_k(m_j); log a(m_j) = kl_table.T @ xi
+        self.kl_table = np.ascontiguousarray(np.sqrt(lam)[:, None] * phi)
+        self._cache: dict = {}
+
+    @property
+    def cell_volume(self) -> float:
+        return self.h
+
+    def fit_maps(self):
+        return [ParameterMap("identity", lo, hi) for lo, hi in self.supports]
+
+    def log_coefficient(self, xi) -> np.ndarray:
+        v = np.asarray(getattr(xi, "values", xi), dtype=float)
+        return self.kl_table.T @ v
+
+    def coefficient(self, xi) -> np.ndarray:
+        """a at the nx+1 midpoints."""
+        return np.exp(self.log_coefficient(xi))
+
+    def tridiagonal(self, xi):
+        """(diag (nx,), off (nx-1,)) of A."""
+        a = self.coefficient(xi)
+        inv_h2 = 1.0 / (self.h * self.h)
+        return (a[:-1] + a[1:]) * inv_h2, -a[1:-1] * inv_h2
+
+    def linear_system(self, xi):
+        key = xi.key()
+        hit = self._cache.get(key)
+        if hit is not None:
+            return hit
+        import scipy.sparse as sp
+
+        dia, off = self.tridiagonal(xi)
+        A = sp.diags([off, dia, off], [-1, 0, 1], format="csc")
+        g = np.full(self.nx, self.source)
+        pair = (A, lambda t, g=g: g)
+        self._cache[key] = pair
+        return pair
+
+    def initial_condition(self, xi=None):
+        return np.sin(np.pi * self.x)
+
+    def sample_parameters(self, count, rng: RngStream) -> list:
+        draws = rng.normal(0.0, 1.0, size=(count, self.parameter_dim))
+        return [ParameterSample(row, id=i) for i, row in enumerate(draws)]
+
+
+_MODELS = {"lognormal-kl-1d": LogNormalKL1D}
+
+
+def get_model(name: str, **kwargs) -> Model:
+    """Registry lookup (``pintuq/models.py:400-413``)."""
+    try:
+        cls = _MODELS[name]
+    except KeyError:
+        raise ConfigError(f"unknown model {name!r}; known: {sorted(_MODELS)}") from None
+    return cls(**kwargs)

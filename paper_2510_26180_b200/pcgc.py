@@ -1,0 +1,273 @@
+"""Diagonalised parallel coarse-grid correction on the device — drop-in for
+``pintuq.pcgc`` (``/root/reference/pkg/src/pintuq/pcgc.py``).
+
+Same names, argument meaning and error behaviour as the reference:
+``build_alpha_circulant`` (:68-76), ``three_step_solve`` (:148-172),
+``assemble_rhs_blocks`` (:175-197), ``cgc_correct`` (:208-243, linear
+branch), ``pcgc_solve`` (:273-358). The per-sample functions run batches of
+one; ``pcgc_solve_batched`` is the production entry point (M samples, each
+frozen at its own iteration count, one C-ABI call).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    CoarseTrajectory,
+    IterationRecord,
+    IterationTrace,
+    MaxItersExceededError,
+    ParameterSample,
+    SolverConfig,
+    TimeGrid,
+)
+from .device import AlphaTables, DeviceOperator, empty, ptr, require_cuda, stream_ptr, to_dev, torch
+
+SAMPLE_ACTIVE, SAMPLE_CONVERGED, SAMPLE_MAXITERS, SAMPLE_NONFINITE = 0, 1, 2, 3
+
+
+@dataclass(frozen=True)
+class AlphaCirculantSpec:
+    """Eigenstructure of C_alpha (``pintuq/pcgc.py:35-65``)."""
+
+    n: int
+    alpha: float
+    eigenvalues: np.ndarray
+    scaling: np.ndarray
+
+    def dense_matrix(self) -> np.ndarray:
+        C = np.eye(self.n) - np.eye(self.n, k=-1)
+        C[0, self.n - 1] -= self.alpha
+        return C
+
+    def dft_matrix(self) -> np.ndarray:
+        jk = np.outer(np.arange(self.n), np.arange(self.n))
+        return np.exp(2j * np.pi * jk / self.n) / np.sqrt(self.n)
+
+    def eigenvector_matrix(self) -> np.ndarray:
+        return (1.0 / self.scaling)[:, None] * self.dft_matrix()
+
+    def inverse_eigenvector_matrix(self) -> np.ndarray:
+        return self.dft_matrix().conj().T * self.scaling[None, :]
+
+
+def build_alpha_circulant(n: int, alpha: float) -> AlphaCirculantSpec:
+    """lambda_n = 1 - alpha^{1/N} e^{-2 pi i n/N}, scaling_j = alpha^{j/N}."""
+    if n < 1:
+        raise ValueError(f"need at least one subinterval, got {n}")
+    if not 0.0 < alpha < 1.0:
+        raise ValueError(f"alpha must lie in (0, 1), got {alpha}")
+    root = alpha ** (1.0 / n)
+    eigenvalues = 1.0 - root * np.exp(-2j * np.pi * np.arange(n) / n)
+    scaling = alpha ** (np.arange(n) / n)
+    return AlphaCirculantSpec(int(n), float(alpha), eigenvalues, scaling)
+
+
+# ---------------------------------------------------------------------------
+def _cgc_scratch(M, N, nx):
+    nbytes = int(_lib.query("kle_cgc_scratch_bytes", M, N, nx))
+    return torch.empty(max(nbytes, 8), dtype=torch.uint8, device="cuda"), nbytes
+
+
+def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float, r, prescaled=False):
+    """u = V (Lambda (x) I + dT I (x) A)^{-1} V^{-1} r for every sample;
+    r: (M, N, nx) device tensor. Returns (u, imag (M,))."""
+    M, _, nx = r.shape
+    u = empty(M, N, nx)
+    imag = empty(M)
+    scratch, nbytes = _cgc_scratch(M, N, nx)
+    _lib.call("kle_three_step_f64", ptr(r.contiguous()), None if prescaled else ptr(tables.scaling),
+              ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia), ptr(op.off), M, N, nx, deltaT, ptr(u),
+              ptr(imag), ptr(scratch), nbytes, stream_ptr())
+    return u, imag
+
+
+def three_step_solve(spec: AlphaCirculantSpec, mean_jac, deltaT: float, r, solvers=None, executor=None):
+    """Solve (C_alpha (x) I - dT I (x) J) u = r (``pintuq/pcgc.py:148-172``)
+    for a symmetric tridiagonal J on the device. Returns (u, imag_residue)."""
+    import scipy.sparse as sp
+
+    r = np.asarray(r, dtype=float)
+    if r.shape[0] != spec.n:
+        raise ValueError(f"block count {r.shape[0]} does not match N={spec.n}")
+    require_cuda()
+    A = -sp.csr_matrix(np.atleast_2d(mean_jac) if not sp.issparse(mean_jac) else mean_jac)
+    nx = A.shape[0]
+    r2 = r.reshape(spec.n, nx)
+    dia = np.asarray(A.diagonal(0), dtype=float)
+    off = np.zeros(nx)
+    if nx > 1:
+        coo = A.tocoo()
+        if coo.nnz and np.max(np.abs(coo.row - coo.col)) > 1:
+            raise NotImplementedError("device three_step_solve supports tridiagonal Jacobians only")
+        if not np.array_equal(A.diagonal(-1), A.diagonal(1)):
+            raise NotImplementedError("device three_step_solve supports symmetric Jacobians only")
+        off[:-1] = A.diagonal(1)
+    op = DeviceOperator(to_dev(dia[None]), to_dev(off[None]), 0.0, to_dev(np.zeros(nx)))
+    u, imag = three_step_device(op, AlphaTables(spec), spec.n, deltaT, to_dev(r2[None]))
+    return u[0].cpu().numpy().reshape(r.shape), float(imag[0].item())
+
+
+def _grid_steps(grid: TimeGrid):
+    return grid.deltaT, grid.deltat
+
+
+def assemble_rhs_blocks(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, U_prev, fine_ends,
+                        executor=None):
+    """b_n = F_end_n - G(prev_n), prev = [alpha U_N, U_1..U_{N-1}]
+    (``pintuq/pcgc.py:175-197``)."""
+    op = DeviceOperator.from_model(model, [xi])
+    U = to_dev(np.asarray(U_prev, dtype=float))
+    prev = torch.cat([cfg.alpha * U[-1:], U[:-1]], dim=0) if U.shape[0] > 1 else cfg.alpha * U
+    G = op.sweep(prev[None].contiguous(), grid.deltaT, 1)[:, :, 0]
+    F = to_dev(np.asarray(fine_ends, dtype=float))[None]
+    b = empty(*F.shape)
+    _lib.call("kle_axpby_f64", ptr(F), ptr(G.contiguous()), ptr(b), 1.0, -1.0, F.numel(), stream_ptr())
+    return b[0].cpu().numpy()
+
+
+def _fgr(op, tables, U, R, J, grid, alpha, F_given=None, F_out=None, status=None):
+    M, N, nx = U.shape
+    dT, dt = _grid_steps(grid)
+    blob = op.blob(dt) if F_given is None else op.dia  # blob unused with F_given
+    _lib.call("kle_fgr_f64", ptr(U), ptr(op.u0), ptr(F_given), ptr(F_out), ptr(R), ptr(blob), ptr(op.dia),
+              ptr(op.off), ptr(tables.scaling), ptr(status), M, N, nx, J, dt, dT, op.g0, alpha, stream_ptr())
+
+
+def cgc_correct(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, U_prev: CoarseTrajectory,
+                fine_ends, spec=None, shifted_solvers=None, executor=None):
+    """One linear coarse-grid correction (``pintuq/pcgc.py:208-243``):
+    returns (CoarseTrajectory, {"inner_iters": 1, "imag_residue": ...})."""
+    if not getattr(model, "is_linear", False):
+        raise NotImplementedError("the device CGC covers linear models only")
+    N = grid.n_coarse
+    spec = spec or build_alpha_circulant(N, cfg.alpha)
+    op = DeviceOperator.from_model(model, [xi])
+    tables = AlphaTables(spec)
+    U = to_dev(U_prev.states)[None]
+    F = to_dev(np.asarray(fine_ends, dtype=float))[None]
+    R = empty(*U.shape)
+    _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha, F_given=F)
+    u, imag = three_step_device(op, tables, N, grid.deltaT, R, prescaled=True)
+    return CoarseTrajectory(U_prev.initial, u[0].cpu().numpy()), {"inner_iters": 1,
+                                                                   "imag_residue": float(imag[0].item())}
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class BatchResult:
+    """Outcome of ``pcgc_solve_batched`` (device tensors)."""
+
+    states: "torch.Tensor"      # (M, N, nx) final U
+    iters: "torch.Tensor"       # (M,) int32 iteration counts (len(records) - 1)
+    status: "torch.Tensor"      # (M,) int32 SAMPLE_* words
+    increments: "torch.Tensor"  # (M, max_iters) per-k increments, NaN past the stop
+    imag: "torch.Tensor"        # (M,) max imaginary residue
+
+
+def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, tables: AlphaTables = None,
+                      workspace=None) -> BatchResult:
+    """The production loop: U (M, N, nx) device tensor is overwritten with the
+    final states (``kle_pcgc_solve_f64``)."""
+    M, N, nx = U.shape
+    if N != grid.n_coarse or nx != op.nx or M != op.M:
+        raise ValueError("initial guess length does not match the time grid")
+    tables = tables or AlphaTables(build_alpha_circulant(N, cfg.alpha))
+    nbytes = int(_lib.query("kle_pcgc_workspace_bytes", M, N, nx))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(max(nbytes, 8), dtype=torch.uint8, device="cuda")
+    status = torch.empty(M, dtype=torch.int32, device="cuda")
+    iters = torch.empty(M, dtype=torch.int32, device="cuda")
+    inc = empty(M, cfg.max_outer_iters)
+    imag = empty(M)
+    _lib.call("kle_pcgc_solve_f64", ptr(U), ptr(op.u0), ptr(op.dia), ptr(op.off), ptr(op.blob(grid.deltat)),
+              ptr(tables.scaling), ptr(tables.inv_scaling), ptr(tables.lam), M, N, nx, grid.n_fine_per_coarse,
+              grid.t_final, cfg.alpha, op.g0, cfg.tol, cfg.max_outer_iters, ptr(status), ptr(iters), ptr(inc),
+              ptr(imag), ptr(workspace), nbytes, stream_ptr())
+    return BatchResult(U, iters, status, inc, imag)
+
+
+def pcgc_solve_batched(model, xis, grid: TimeGrid, cfg: SolverConfig, init_states) -> BatchResult:
+    """Batched ``pcgc_solve(stop_on="increment")`` over M samples."""
+    op = DeviceOperator.from_model(model, xis)
+    U = to_dev(init_states).clone()
+    return pcgc_solve_device(op, U, grid, cfg)
+
+
+def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, init: CoarseTrajectory,
+               reference: CoarseTrajectory | None = None, stop_on: str = "increment", store_states: bool = False,
+               executor=None, raise_on_max: bool = True, solver_name: str = "pcgc") -> IterationTrace:
+    """Single-sample drop-in for ``pintuq.pcgc.pcgc_solve`` (:273-358).
+
+    Each outer iteration is one fused F + rhs launch and one CGC launch; the
+    trace bookkeeping (errors vs the reference, stored states) is host side."""
+    if stop_on not in ("increment", "reference"):
+        raise ValueError(f"stop_on must be 'increment' or 'reference', not {stop_on!r}")
+    if stop_on == "reference" and reference is None:
+        raise ValueError("stop_on='reference' requires a reference trajectory")
+    if init.n_coarse != grid.n_coarse:
+        raise ValueError("initial guess length does not match the time grid")
+    model.validate(xi)
+    if not getattr(model, "is_linear", False):
+        raise NotImplementedError("the device PCGC covers linear models only")
+    N = grid.n_coarse
+    u0 = np.asarray(model.initial_condition(xi), dtype=float)
+    op = DeviceOperator.from_model(model, [xi])
+    tables = AlphaTables(build_alpha_circulant(N, cfg.alpha))
+    U = to_dev(init.states)[None].clone()
+    nx = U.shape[2]
+    R = empty(1, N, nx)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    iters = torch.zeros(1, dtype=torch.int32, device="cuda")
+    inc = empty(1, cfg.max_outer_iters).fill_(float("nan"))
+    imag = torch.zeros(1, dtype=torch.float64, device="cuda")
+    scratch, nbytes = _cgc_scratch(1, N, nx)
+
+    def err(states):
+        if reference is None:
+            return None, None
+        e = np.max(np.abs(states - reference.states), axis=1)
+        return e, float(np.max(e))
+
+    trace = IterationTrace(solver=solver_name, stop_on=stop_on)
+    trace.diagnostics["max_imag_residue"] = 0.0
+    host = np.asarray(init.states, dtype=float).copy()
+    ev, me = err(host)
+    trace.records.append(IterationRecord(0, None, ev, me, 0.0))
+    if store_states:
+        trace.states_history.append(host.copy())
+    if stop_on == "reference" and me is not None and me <= cfg.tol:
+        trace.converged = True
+        trace.trajectory = CoarseTrajectory(u0, host)
+        return trace
+    dT = grid.deltaT
+    for k in range(1, cfg.max_outer_iters + 1):
+        tic = time.perf_counter()
+        _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha)
+        # tol < 0 keeps the device from freezing the sample; the stop test is ours
+        _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
+                  ptr(op.off), 1, N, nx, dT, k, cfg.max_outer_iters, -1.0, None, None, ptr(inc), ptr(imag), None,
+                  ptr(scratch), nbytes, stream_ptr())
+        host = U[0].cpu().numpy()
+        increment = float(inc[0, k - 1].item())
+        wall_ms = 1e3 * (time.perf_counter() - tic)
+        ev, me = err(host)
+        trace.records.append(IterationRecord(k, increment, ev, me, wall_ms))
+        trace.diagnostics["max_imag_residue"] = float(imag[0].item())
+        if store_states:
+            trace.states_history.append(host.copy())
+        metric = increment if stop_on == "increment" else me
+        if metric <= cfg.tol:
+            trace.converged = True
+            break
+    trace.trajectory = CoarseTrajectory(u0, host)
+    trace.trajectory.assert_finite()
+    if not trace.converged and raise_on_max:
+        raise MaxItersExceededError(
+            f"{solver_name} did not reach tol {cfg.tol:.1e} within {cfg.max_outer_iters} iterations", trace=trace
+        )
+    return trace

@@ -1,0 +1,214 @@
+"""Generate the golden vectors by running the UNMODIFIED reference (pintuq)
+on the BASELINE log-normal KL model plugin.
+
+Run here (the reference tree exists only in the build container):
+
+    python tests/golden/make_golden.py            # writes tests/golden/*.npz
+
+The reference is imported read-only from /root/reference/pkg/src (pure-Python
+backend; the Cython extension only serves the nonlinear models). The model is
+plugged in through the reference's own plugin surface: a subclass of
+``pintuq.models.LinearModel`` (models.py:109-125) delegating to
+``paper_2510_26180_b200.models.LogNormalKL1D``. The Hermite surrogate is
+composed from the reference's lower-level functions exactly as SURVEY.md §0.2
+prescribes (collect_snapshots -> kl_build -> kl_coefficients ->
+gpc_fit(family="hermite") -> KLGpcSurrogate(family="hermite")).
+
+Outputs (np.savez_compressed):
+  c1.npz   config-1 pipeline: KL table, 3^4 Gauss-Hermite surrogate, the
+           first 16 of the 256 seeded eval samples: U0, iteration counts,
+           per-k increments, final fields, imag residue, moments; plus
+           single-call vectors for propagate_fine / propagate_coarse /
+           cgc_correct / three_step_solve / coarse_sweep_init.
+  c2.npz   config-2 shapes (nx=511, N=64, J=64, d=8): 3 samples from
+           coarse-sweep init: iteration counts, increments, final fields.
+  c5s.npz  config-5 analogue (nx=255, N=128, J=8), alpha in {1e-1,1e-2,1e-4}:
+           coarse-sweep init, iteration counts, increments, final fields.
+"""
+from __future__ import annotations
+
+import itertools
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+os.environ.setdefault("PINTUQ_PURE_PYTHON", "1")
+REF_SRC = "/root/reference/pkg/src"
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, str(ROOT))
+
+from pintuq import core as rcore  # noqa: E402
+from pintuq import models as rmodels  # noqa: E402
+from pintuq import parareal as rpar  # noqa: E402
+from pintuq import pcgc as rpcgc  # noqa: E402
+from pintuq import propagators as rprop  # noqa: E402
+from pintuq import surrogate as rsur  # noqa: E402
+
+from paper_2510_26180_b200.models import LogNormalKL1D, ParameterMap  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+class RefLogNormalKL1D(rmodels.LinearModel):
+    """Reference-side plugin: the reference's LinearModel interface over our
+    model definition (what a maintainer adds to pintuq.models._MODELS)."""
+
+    name = "lognormal-kl-1d"
+
+    def __init__(self, **kw):
+        self.inner = LogNormalKL1D(**kw)
+        self.nx = self.inner.nx
+        self.parameter_dim = self.inner.parameter_dim
+        self.supports = self.inner.supports
+        self._cache = {}
+
+    @property
+    def cell_volume(self):
+        return self.inner.cell_volume
+
+    def linear_system(self, xi):
+        key = xi.key()
+        if key not in self._cache:
+            self._cache[key] = self.inner.linear_system(rcore.ParameterSample(xi.values, id=xi.id))
+        return self._cache[key]
+
+    def initial_condition(self, xi):
+        return self.inner.initial_condition(xi)
+
+    def sample_parameters(self, count, rng):
+        draws = rng.normal(0.0, 1.0, size=(count, self.parameter_dim))
+        return [rcore.ParameterSample(r, id=i) for i, r in enumerate(draws)]
+
+    def fit_maps(self):
+        return [ParameterMap("identity", lo, hi) for lo, hi in self.supports]
+
+
+def hermite_surrogate(model, grid, cfg, training, degree, eps_kl=1e-10):
+    snap = rsur.collect_snapshots(model, grid, cfg, training, method="pcgc")
+    basis = rsur.kl_build(snap, eps_kl)
+    zeta = rsur.kl_coefficients(snap, basis)
+    points = np.array([xi.values for xi in training])
+    coeffs, resid, deg = rsur.gpc_fit(points, zeta, degree, family="hermite")
+    s = rsur.KLGpcSurrogate(
+        mean_field=snap.mean_field, eigenvalues=basis.retained.copy(), modes=basis.modes,
+        coeffs=coeffs, degree=deg, maps=model.fit_maps(), family="hermite",
+        cell_weight=snap.cell_weight,
+    )
+    return s, snap
+
+
+def solve_one(model, grid, cfg, xi, init_states):
+    init = rcore.CoarseTrajectory(model.initial_condition(xi), init_states)
+    tr = rpcgc.pcgc_solve(model, xi, grid, cfg, init, stop_on="increment")
+    incs = np.array([r.increment_inf for r in tr.records[1:]])
+    return tr.trajectory.states, tr.iterations, incs, tr.diagnostics["max_imag_residue"]
+
+
+def make_c1():
+    t0 = time.time()
+    model = RefLogNormalKL1D(nx=127, d=4, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 16, 32)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    train_rng, eval_rng, init_rng = rcore.RngStream(2718).split(3)
+    nodes, _ = np.polynomial.hermite_e.hermegauss(3)
+    grid_pts = np.array(list(itertools.product(nodes, repeat=4)))
+    training = [rcore.ParameterSample(p, id=i) for i, p in enumerate(grid_pts)]
+    s, snap = hermite_surrogate(model, grid, cfg, training, degree=2)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(256, 4))
+    M = 16
+    U0 = np.empty((M, 16, 127))
+    final = np.empty_like(U0)
+    iters = np.empty(M, np.int32)
+    incs = np.full((M, 60), np.nan)
+    imag = np.empty(M)
+    for i in range(M):
+        xi = rcore.ParameterSample(xi_all[i], id=i)
+        U0[i] = rsur.surrogate_predict(s, xi, model.initial_condition(xi)).states
+        st, it, inc, im = solve_one(model, grid, cfg, xi, U0[i])
+        final[i], iters[i], imag[i] = st, it, im
+        incs[i, : len(inc)] = inc
+    # single-call vectors on sample 0
+    xi0 = rcore.ParameterSample(xi_all[0], id=0)
+    u0 = model.initial_condition(xi0)
+    rng = np.random.default_rng(11)
+    u_rand = rng.normal(size=127)
+    pf_u0 = rprop.propagate_fine(model, u0, 0.0, grid.deltaT, grid, xi0, cfg)
+    pf_rand = rprop.propagate_fine(model, u_rand, 3 * grid.deltaT, 4 * grid.deltaT, grid, xi0, cfg)
+    pc_rand = rprop.propagate_coarse(model, u_rand, 0.0, grid.deltaT, xi0, cfg)
+    U_prev = rcore.CoarseTrajectory(u0, U0[0])
+    starts = np.vstack([u0, U0[0][:-1]])
+    F_ends = np.array([rprop.propagate_fine(model, starts[n], grid.coarse_point(n),
+                                            grid.coarse_point(n + 1), grid, xi0, cfg)
+                       for n in range(16)])
+    cgc_out, cgc_diag = rpcgc.cgc_correct(model, xi0, grid, cfg, U_prev, F_ends)
+    b_blocks = rpcgc.assemble_rhs_blocks(model, xi0, grid, cfg, U0[0], F_ends)
+    spec = rpcgc.build_alpha_circulant(16, 1e-3)
+    A, _ = model.linear_system(xi0)
+    r_rand = rng.normal(size=(16, 127))
+    ts_u, ts_imag = rpcgc.three_step_solve(spec, -A, grid.deltaT, r_rand)
+    cs = rpar.coarse_sweep_init(model, xi0, grid, cfg).states
+    cs_states, cs_iters, cs_incs, _ = solve_one(model, grid, cfg, xi0, cs)
+    np.savez_compressed(
+        OUT / "c1.npz",
+        kl_table=model.inner.kl_table, xi_all=xi_all, train_points=grid_pts,
+        mean_field=s.mean_field, eigenvalues=s.eigenvalues, modes=s.modes, coeffs=s.coeffs,
+        degree=s.degree, U0=U0, final=final, iters=iters, increments=incs, imag=imag,
+        mean=final.mean(axis=0), var=final.var(axis=0),
+        pf_u0=pf_u0, u_rand=u_rand, pf_rand=pf_rand, pc_rand=pc_rand, F_ends=F_ends,
+        b_blocks=b_blocks, cgc_states=cgc_out.states, cgc_imag=cgc_diag["imag_residue"],
+        r_rand=r_rand, ts_u=ts_u, ts_imag=ts_imag, lam=spec.eigenvalues, scaling=spec.scaling,
+        coarse_sweep=cs, cs_final=cs_states, cs_iters=cs_iters, cs_incs=cs_incs,
+        snapshots=snap.fields,
+    )
+    print(f"c1 done in {time.time() - t0:.1f}s; iters {iters.tolist()}; m_q {s.m_q}")
+
+
+def make_c2():
+    t0 = time.time()
+    model = RefLogNormalKL1D(nx=511, d=8, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 64, 64)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    _, eval_rng, _ = rcore.RngStream(2718).split(3)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(3, 8))
+    final = np.empty((3, 64, 511))
+    iters = np.empty(3, np.int32)
+    incs = np.full((3, 60), np.nan)
+    for i in range(3):
+        xi = rcore.ParameterSample(xi_all[i], id=i)
+        cs = rpar.coarse_sweep_init(model, xi, grid, cfg).states
+        st, it, inc, _ = solve_one(model, grid, cfg, xi, cs)
+        final[i], iters[i] = st, it
+        incs[i, : len(inc)] = inc
+    np.savez_compressed(OUT / "c2.npz", kl_table=model.inner.kl_table, xi=xi_all,
+                        final=final, iters=iters, increments=incs)
+    print(f"c2 done in {time.time() - t0:.1f}s; iters {iters.tolist()}")
+
+
+def make_c5s():
+    t0 = time.time()
+    model = RefLogNormalKL1D(nx=255, d=4, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 128, 8)
+    _, eval_rng, _ = rcore.RngStream(2718).split(3)
+    xi = rcore.ParameterSample(eval_rng.normal(0.0, 1.0, size=4), id=0)
+    out = {"kl_table": model.inner.kl_table, "xi": xi.values}
+    for alpha in (1e-1, 1e-2, 1e-4):
+        cfg = rcore.SolverConfig(alpha=alpha, tol=1e-8, max_outer_iters=60, seed=2718)
+        cs = rpar.coarse_sweep_init(model, xi, grid, cfg).states
+        st, it, inc, im = solve_one(model, grid, cfg, xi, cs)
+        tag = f"a{-int(round(np.log10(alpha)))}"
+        out[f"{tag}_final"] = st
+        out[f"{tag}_iters"] = it
+        out[f"{tag}_incs"] = inc
+        out[f"{tag}_imag"] = im
+    np.savez_compressed(OUT / "c5s.npz", **out)
+    print(f"c5s done in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c1", "c2", "c5s"]
+    for w in which:
+        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s}[w]()

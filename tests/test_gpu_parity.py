@@ -1,0 +1,290 @@
+"""Device parity: the CUDA path through the C ABI against the golden vectors
+of the unmodified reference and the pinned CPU oracle.
+
+Tolerances (BASELINE north star): parareal iteration counts exact; fields and
+moments within 1e-10 relative (max-norm, relative to the field's max); for
+alpha = 1e-4 at large N the reference's own round-off floor scales with
+cond(V) = alpha^{-(N-1)/N}, so rtol = max(1e-10, 1e-12 cond(V)) there.
+"""
+import numpy as np
+import pytest
+
+from oracle import batched, ref_port
+from tests.conftest import c1_config
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def test_library_exports_and_abi(cuda):
+    from paper_2510_26180_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.kle_abi_version() == 1
+    for name in _lib.EXPORTED:
+        assert hasattr(lib, name)
+
+
+def test_coefficient_field_matches_model(cuda, golden):
+    import torch
+    from paper_2510_26180_b200.device import DeviceOperator
+
+    model, _, _ = c1_config()
+    xi = golden("c1")["xi_all"]
+    op = DeviceOperator.from_model(model, xi)
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    assert rel(op.dia.cpu().numpy(), dia) <= 1e-14
+    assert rel(op.off.cpu().numpy()[:, :-1], off) <= 1e-14
+    assert torch.all(op.off[:, -1] == 0)
+
+
+def test_propagators_single_sample(cuda, golden):
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.propagators import (coarse_sweep_init, fine_reference, propagate_coarse,
+                                                   propagate_fine)
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    xi0 = ParameterSample(g["xi_all"][0], id=0)
+    u0 = model.initial_condition()
+    assert rel(propagate_fine(model, u0, 0.0, grid.deltaT, grid, xi0, cfg), g["pf_u0"]) <= 1e-13
+    assert rel(propagate_fine(model, g["u_rand"], 3 * grid.deltaT, 4 * grid.deltaT, grid, xi0, cfg),
+               g["pf_rand"]) <= 1e-13
+    assert rel(propagate_coarse(model, g["u_rand"], 0.0, grid.deltaT, xi0, cfg), g["pc_rand"]) <= 1e-13
+    assert rel(coarse_sweep_init(model, xi0, grid, cfg).states, g["coarse_sweep"]) <= 1e-13
+    op = ref_port.SampleOperator(*model.tridiagonal(xi0), np.full(model.nx, 1.0))
+    ref = ref_port.fine_reference(op, u0, 16, 32, grid.deltaT)
+    assert rel(fine_reference(model, xi0, grid, cfg).states, ref) <= 1e-12
+    with pytest.raises(ValueError):
+        propagate_fine(model, u0, 0.0, 2 * grid.deltaT, grid, xi0, cfg)
+
+
+def test_three_step_and_cgc_correct(cuda, golden):
+    from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample
+    from paper_2510_26180_b200.pcgc import assemble_rhs_blocks, build_alpha_circulant, cgc_correct, three_step_solve
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    xi0 = ParameterSample(g["xi_all"][0], id=0)
+    A, _ = model.linear_system(xi0)
+    u, imag = three_step_solve(build_alpha_circulant(16, 1e-3), -A, grid.deltaT, g["r_rand"])
+    assert rel(u, g["ts_u"]) <= RTOL
+    assert imag <= 1e-10 * max(np.abs(u).max(), 1.0)
+    U_prev = CoarseTrajectory(model.initial_condition(), g["U0"][0])
+    b = assemble_rhs_blocks(model, xi0, grid, cfg, g["U0"][0], g["F_ends"])
+    assert rel(b, g["b_blocks"]) <= 1e-12
+    out, diag = cgc_correct(model, xi0, grid, cfg, U_prev, g["F_ends"])
+    assert rel(out.states, g["cgc_states"]) <= RTOL
+    assert diag["inner_iters"] == 1
+    with pytest.raises(ValueError):
+        three_step_solve(build_alpha_circulant(4, 0.1), np.zeros((1, 1)), 0.1, np.zeros((3, 1)))
+
+
+def test_pcgc_solve_single_sample_matches_reference(cuda, golden):
+    from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample
+    from paper_2510_26180_b200.pcgc import pcgc_solve
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    for i in range(4):
+        xi = ParameterSample(g["xi_all"][i], id=i)
+        tr = pcgc_solve(model, xi, grid, cfg, CoarseTrajectory(model.initial_condition(), g["U0"][i]))
+        assert tr.iterations == int(g["iters"][i])
+        assert rel(tr.trajectory.states, g["final"][i]) <= RTOL
+        incs = np.array([r.increment_inf for r in tr.records[1:]])
+        # increments are differences of O(1) fields: compare at field round-off
+        np.testing.assert_allclose(incs, g["increments"][i, : tr.iterations], rtol=0, atol=1e-12)
+
+
+def test_kle_cgc_pipeline_c1_golden(cuda, golden):
+    """xi -> coefficient field -> Hermite surrogate U0 -> batched PCGC ->
+    moments, all on the device, against the reference's golden run."""
+    from paper_2510_26180_b200.engine import KleCgcSolver
+    from paper_2510_26180_b200.models import ParameterMap
+    from paper_2510_26180_b200.surrogate import KLGpcSurrogate
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], int(g["degree"]),
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+    solver = KleCgcSolver(model, grid, cfg, s)
+    M = len(g["iters"])
+    res = solver.solve(g["xi_all"][:M], keep_initial=True)
+    assert rel(res.U0.cpu().numpy(), g["U0"]) <= 1e-13
+    np.testing.assert_array_equal(res.batch.iters.cpu().numpy(), g["iters"])
+    assert np.all(res.batch.status.cpu().numpy() == 1)
+    assert rel(res.batch.states.cpu().numpy(), g["final"]) <= RTOL
+    mean, var = solver.moments(res)
+    assert rel(mean.cpu().numpy(), g["mean"]) <= RTOL
+    assert rel(var.cpu().numpy(), g["var"]) <= 1e-9
+    inc = res.batch.increments.cpu().numpy()
+    for i in range(M):
+        k = int(g["iters"][i])
+        np.testing.assert_allclose(inc[i, :k], g["increments"][i, :k], rtol=0, atol=1e-12)
+        assert np.all(np.isnan(inc[i, k:]))
+
+
+def test_kle_cgc_c1_full_batch_vs_oracle(cuda, golden):
+    """All 256 config-1 samples against the batched oracle."""
+    from paper_2510_26180_b200.engine import KleCgcSolver
+    from paper_2510_26180_b200.models import ParameterMap
+    from paper_2510_26180_b200.surrogate import KLGpcSurrogate
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2,
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+    xi = g["xi_all"]
+    res = KleCgcSolver(model, grid, cfg, s).solve(xi)
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    U0 = batched.hermite_predict(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2, xi)
+    out = batched.pcgc(dia, off, model.initial_condition(), U0, 16, 32, 1.0, 1e-3, 1e-8, 60)
+    np.testing.assert_array_equal(res.batch.iters.cpu().numpy(), out["iters"])
+    assert rel(res.batch.states.cpu().numpy(), out["states"]) <= RTOL
+
+
+def test_c2_shapes_match_reference(cuda, golden):
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    g = golden("c2")
+    model = LogNormalKL1D(nx=511, d=8)
+    grid = make_time_grid(1.0, 64, 64)
+    cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60)
+    op = DeviceOperator.from_model(model, g["xi"])
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), g["iters"])
+    assert rel(res.states.cpu().numpy(), g["final"]) <= RTOL
+
+
+@pytest.mark.parametrize("tag,alpha", [("a1", 1e-1), ("a2", 1e-2), ("a4", 1e-4)])
+def test_c5_analogue_alpha_sweep(cuda, golden, tag, alpha):
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    g = golden("c5s")
+    N = 128
+    model = LogNormalKL1D(nx=255, d=4)
+    grid = make_time_grid(1.0, N, 8)
+    cfg = SolverConfig(alpha=alpha, tol=1e-8, max_outer_iters=60)
+    op = DeviceOperator.from_model(model, g["xi"][None])
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    assert int(res.iters[0]) == int(g[f"{tag}_iters"])
+    rtol = max(RTOL, 1e-12 * alpha ** (-(N - 1) / N))
+    assert rel(res.states[0].cpu().numpy(), g[f"{tag}_final"]) <= rtol
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_three_step_vs_dense_randomized(cuda, trial):
+    """pintuq tests/test_pcgc.py:110-125 restated for the device operator
+    class (symmetric tridiagonal), incl. N = 1..8 (non powers of two)."""
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, three_step_solve
+
+    rng = np.random.default_rng(100 + trial)
+    n = int(rng.integers(1, 9))
+    nx = int(rng.integers(1, 17))
+    alpha = float(rng.uniform(0.02, 0.9))
+    dT = float(rng.uniform(0.01, 1.0))
+    spec = build_alpha_circulant(n, alpha)
+    off = -rng.uniform(0.1, 1.0, nx - 1) if nx > 1 else np.zeros(0)
+    dia = rng.uniform(0.5, 1.5, nx) + np.concatenate([[0.0], -off]) + np.concatenate([-off, [0.0]])
+    A = np.diag(dia) + np.diag(off, 1) + np.diag(off, -1)
+    r = rng.normal(size=(n, nx))
+    Mx = np.kron(spec.dense_matrix(), np.eye(nx)) + dT * np.kron(np.eye(n), A)
+    expected = np.linalg.solve(Mx, r.reshape(-1)).reshape(n, nx)
+    u, imag = three_step_solve(spec, -A, dT, r)
+    assert rel(u, expected) <= 1e-9
+    assert imag <= 1e-10 * max(np.abs(u).max(), 1.0)
+
+
+def test_three_step_hand_and_zero(cuda):
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, three_step_solve
+
+    u, imag = three_step_solve(build_alpha_circulant(2, 0.5), np.zeros((1, 1)), 0.3, np.array([[1.0], [0.0]]))
+    np.testing.assert_allclose(u, [[2.0], [2.0]], atol=1e-12)
+    u, _ = three_step_solve(build_alpha_circulant(5, 0.1), np.array([[-2.0]]), 0.1, np.zeros((5, 1)))
+    np.testing.assert_array_equal(u, np.zeros((5, 1)))
+
+
+def test_gpc_basis_bitwise_and_gemm(cuda, golden):
+    import torch
+    from paper_2510_26180_b200.models import ParameterMap
+    from paper_2510_26180_b200.surrogate import DeviceSurrogate, KLGpcSurrogate
+
+    g = golden("c1")
+    s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2,
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+    ds = DeviceSurrogate(s)
+    xi = g["xi_all"]
+    Psi = ds.basis(torch.as_tensor(xi, device="cuda")).cpu().numpy()
+    np.testing.assert_array_equal(Psi, ref_port.basis_matrix(xi, 2))
+    # degree-3 8-dim basis (config-2 surrogate shape) also bitwise
+    rng = np.random.default_rng(3)
+    xi8 = rng.normal(size=(300, 8))
+    s8 = KLGpcSurrogate(np.zeros((2, 3)), np.ones(1), np.ones((1, 2, 3)), np.ones((1, 165)), 3,
+                        [ParameterMap("identity", -np.inf, np.inf)] * 8)
+    Psi8 = DeviceSurrogate(s8).basis(torch.as_tensor(xi8, device="cuda")).cpu().numpy()
+    np.testing.assert_array_equal(Psi8, ref_port.basis_matrix(xi8, 3))
+
+
+def test_gpc_eval_factored_branch(cuda):
+    """m_q < P (config-2 shape: 132 < 165) uses the two-GEMM branch."""
+    import torch
+    from paper_2510_26180_b200.models import ParameterMap
+    from paper_2510_26180_b200.surrogate import DeviceSurrogate, KLGpcSurrogate
+
+    rng = np.random.default_rng(5)
+    m_q, P, N, nx = 20, 35, 4, 9  # d=4, p=3 -> P=35
+    s = KLGpcSurrogate(rng.normal(size=(N, nx)), rng.uniform(0.1, 1, m_q), rng.normal(size=(m_q, N, nx)),
+                       rng.normal(size=(m_q, P)), 3, [ParameterMap("identity", -np.inf, np.inf)] * 4)
+    ds = DeviceSurrogate(s)
+    assert ds.mode == "factored"
+    xi = rng.normal(size=(77, 4))
+    got = ds.predict(torch.as_tensor(xi, device="cuda")).cpu().numpy()
+    want = batched.hermite_predict(s.mean_field, s.eigenvalues, s.modes, s.coeffs, 3, xi)
+    assert rel(got, want) <= 1e-13
+
+
+def test_moments_match_numpy(cuda):
+    import torch
+    from paper_2510_26180_b200.moments import two_pass_moments
+
+    rng = np.random.default_rng(8)
+    U = rng.normal(1.0, 0.2, size=(1000, 3, 7))
+    mean, var = two_pass_moments(torch.as_tensor(U, device="cuda"), 1000)
+    assert rel(mean.cpu().numpy(), U.mean(axis=0)) <= 1e-13
+    assert rel(var.cpu().numpy(), U.var(axis=0)) <= 1e-12
+
+
+def test_determinism_bitwise(cuda, golden):
+    from paper_2510_26180_b200.engine import KleCgcSolver
+    from paper_2510_26180_b200.models import ParameterMap
+    from paper_2510_26180_b200.surrogate import KLGpcSurrogate
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2,
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+    solver = KleCgcSolver(model, grid, cfg, s)
+    a = solver.solve(g["xi_all"][:64]).batch.states.cpu().numpy()
+    b = solver.solve(g["xi_all"][:64]).batch.states.cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+
+
+def test_empty_batch_is_noop(cuda):
+    from paper_2510_26180_b200 import _lib
+
+    assert _lib.call("kle_fgr_f64", *([None] * 10), 0, 16, 127, 32, 0.1, 0.1, 1.0, 0.1, None) == 0
+    assert _lib.call("kle_sweep_f64", None, None, None, 0, 1, 127, 1, 1, 0.1, 1.0, None) == 0

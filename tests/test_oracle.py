@@ -1,0 +1,179 @@
+"""Pin the CPU oracle against the golden vectors produced by the unmodified
+reference (tests/golden/make_golden.py). CPU only."""
+import numpy as np
+import pytest
+
+from oracle import batched, ref_port
+from tests.conftest import c1_config
+
+
+def _op(model, xi):
+    dia, off = model.tridiagonal(xi)
+    full_off = off
+    return ref_port.SampleOperator(dia, full_off, np.full(model.nx, model.source))
+
+
+def test_kl_table_matches_golden(golden):
+    model, _, _ = c1_config()
+    g = golden("c1")
+    np.testing.assert_allclose(model.kl_table, g["kl_table"], rtol=0, atol=1e-13)
+
+
+def test_ref_port_single_calls_bitwise(golden):
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    xi0 = g["xi_all"][0]
+    op = _op(model, xi0)
+    u0 = model.initial_condition()
+    np.testing.assert_array_equal(ref_port.fine(op, u0, grid.n_fine_per_coarse, grid.deltat), g["pf_u0"])
+    np.testing.assert_array_equal(ref_port.fine(op, g["u_rand"], grid.n_fine_per_coarse, grid.deltat), g["pf_rand"])
+    np.testing.assert_array_equal(ref_port.coarse(op, g["u_rand"], grid.deltaT), g["pc_rand"])
+    lam, scaling = ref_port.alpha_circulant(16, 1e-3)
+    np.testing.assert_array_equal(lam, g["lam"])
+    np.testing.assert_array_equal(scaling, g["scaling"])
+    solvers = ref_port.shifted_solvers(op, lam, grid.deltaT)
+    u, imag = ref_port.three_step(lam, scaling, solvers, g["r_rand"])
+    np.testing.assert_array_equal(u, g["ts_u"])
+    assert imag == g["ts_imag"]
+    Un, im = ref_port.cgc(op, lam, scaling, solvers, cfg.alpha, grid.deltaT, g["U0"][0], g["F_ends"])
+    np.testing.assert_array_equal(Un, g["cgc_states"])
+    cs = ref_port.coarse_sweep(op, u0, 16, grid.deltaT)
+    np.testing.assert_array_equal(cs, g["coarse_sweep"])
+
+
+def test_ref_port_pcgc_reproduces_reference_c1(golden):
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    u0 = model.initial_condition()
+    for i in range(len(g["iters"])):
+        op = _op(model, g["xi_all"][i])
+        out = ref_port.pcgc(op, u0, g["U0"][i], 16, 32, 1.0, cfg.alpha, cfg.tol, cfg.max_outer_iters)
+        assert out["iters"] == g["iters"][i]
+        np.testing.assert_array_equal(out["states"], g["final"][i])
+        np.testing.assert_array_equal(out["increments"], g["increments"][i, : out["iters"]])
+
+
+def test_ref_port_surrogate_bitwise(golden):
+    g = golden("c1")
+    for i in range(len(g["iters"])):
+        pred = ref_port.surrogate_predict(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"],
+                                          int(g["degree"]), g["xi_all"][i])
+        np.testing.assert_array_equal(pred, g["U0"][i])
+
+
+def test_ref_port_kl_and_fit_from_snapshots(golden):
+    model, grid, _ = c1_config()
+    g = golden("c1")
+    w = model.cell_volume * grid.deltaT
+    mean, lam, modes, X = ref_port.kl_build(g["snapshots"], w, 1e-10)
+    np.testing.assert_array_equal(mean, g["mean_field"])
+    np.testing.assert_allclose(lam, g["eigenvalues"], rtol=1e-12)
+    assert modes.shape == g["modes"].shape
+    np.testing.assert_allclose(modes, g["modes"], rtol=0, atol=1e-9 * np.abs(g["modes"]).max())
+    zeta = ref_port.kl_coefficients(X, modes, lam, w)
+    coeffs = ref_port.gpc_fit(g["train_points"], zeta, 2)
+    np.testing.assert_allclose(coeffs, g["coeffs"], rtol=0, atol=1e-9 * np.abs(g["coeffs"]).max())
+
+
+def test_batched_oracle_matches_reference_c1(golden):
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    xi = g["xi_all"][: len(g["iters"])]
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    out = batched.pcgc(dia, off, model.initial_condition(), g["U0"], 16, 32, 1.0, cfg.alpha, cfg.tol,
+                       cfg.max_outer_iters)
+    np.testing.assert_array_equal(out["iters"], g["iters"])
+    scale = np.abs(g["final"]).max()
+    assert np.max(np.abs(out["states"] - g["final"])) / scale <= 1e-10
+    mean, var = batched.moments(out["states"])
+    np.testing.assert_allclose(mean, g["mean"], rtol=1e-11, atol=1e-14)
+    np.testing.assert_allclose(var, g["var"], rtol=1e-9, atol=1e-16)
+    U0 = batched.hermite_predict(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2, xi)
+    np.testing.assert_allclose(U0, g["U0"], rtol=0, atol=1e-14)
+
+
+def test_batched_oracle_c2_shapes(golden):
+    from paper_2510_26180_b200 import LogNormalKL1D
+
+    g = golden("c2")
+    model = LogNormalKL1D(nx=511, d=8)
+    np.testing.assert_allclose(model.kl_table, g["kl_table"], rtol=0, atol=1e-13)
+    dia, off = batched.tridiag_from_xi(g["xi"], model.kl_table, model.h)
+    init = batched.coarse_sweep(dia, off, model.initial_condition(), 64, 1.0 / 64)
+    out = batched.pcgc(dia, off, model.initial_condition(), init, 64, 64, 1.0, 1e-3, 1e-8, 60)
+    np.testing.assert_array_equal(out["iters"], g["iters"])
+    assert np.max(np.abs(out["states"] - g["final"])) / np.abs(g["final"]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("tag,alpha", [("a1", 1e-1), ("a2", 1e-2), ("a4", 1e-4)])
+def test_batched_oracle_c5_analogue(golden, tag, alpha):
+    from paper_2510_26180_b200 import LogNormalKL1D
+
+    g = golden("c5s")
+    model = LogNormalKL1D(nx=255, d=4)
+    dia, off = batched.tridiag_from_xi(g["xi"][None], model.kl_table, model.h)
+    N = 128
+    init = batched.coarse_sweep(dia, off, model.initial_condition(), N, 1.0 / N)
+    out = batched.pcgc(dia, off, model.initial_condition(), init, N, 8, 1.0, alpha, 1e-8, 60)
+    assert out["iters"][0] == int(g[f"{tag}_iters"])
+    cond = alpha ** (-(N - 1) / N)
+    rtol = max(1e-10, 1e-12 * cond)
+    assert np.max(np.abs(out["states"][0] - g[f"{tag}_final"])) / np.abs(g[f"{tag}_final"]).max() <= rtol
+
+
+# --- reference test pins restated on the oracle (pintuq tests/test_pcgc.py) ---
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("alpha", [0.05, 0.1, 0.5])
+def test_alpha_circulant_diagonalises(n, alpha):
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    spec = build_alpha_circulant(n, alpha)
+    V, Vinv = spec.eigenvector_matrix(), spec.inverse_eigenvector_matrix()
+    np.testing.assert_allclose(V @ Vinv, np.eye(n), atol=1e-12)
+    assert np.max(np.abs(V @ np.diag(spec.eigenvalues) @ Vinv - spec.dense_matrix())) <= 1e-12
+    lam, sc = ref_port.alpha_circulant(n, alpha)
+    np.testing.assert_array_equal(lam, spec.eigenvalues)
+    np.testing.assert_array_equal(sc, spec.scaling)
+
+
+def test_alpha_circulant_pins():
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    assert build_alpha_circulant(1, 0.5).eigenvalues[0] == pytest.approx(0.5, abs=1e-15)
+    np.testing.assert_allclose(np.sort(build_alpha_circulant(2, 0.25).eigenvalues.real), [0.5, 1.5], atol=1e-14)
+    assert np.prod(build_alpha_circulant(4, 0.1).eigenvalues) == pytest.approx(0.9, rel=1e-12)
+    for n in (2, 8, 33, 64):
+        cond = np.linalg.cond(build_alpha_circulant(n, 0.1).eigenvector_matrix())
+        assert cond == pytest.approx(0.1 ** (-(n - 1) / n), rel=1e-10)
+    for a in (0.0, 1.0, -0.2, 1.5):
+        with pytest.raises(ValueError):
+            build_alpha_circulant(4, a)
+
+
+def _dense_all_at_once(spec_dense, J, dT, r):
+    n, nx = r.shape
+    Mx = np.kron(spec_dense, np.eye(nx)) - dT * np.kron(np.eye(n), J)
+    return np.linalg.solve(Mx, r.reshape(-1)).reshape(n, nx)
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_oracle_three_step_vs_dense(trial):
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    rng = np.random.default_rng(100 + trial)
+    n = int(rng.integers(1, 9))
+    nx = int(rng.integers(1, 17))
+    alpha = float(rng.uniform(0.02, 0.9))
+    dT = float(rng.uniform(0.01, 1.0))
+    spec = build_alpha_circulant(n, alpha)
+    # symmetric diagonally dominant tridiagonal A (the device operator class)
+    off = -rng.uniform(0.1, 1.0, nx - 1) if nx > 1 else np.zeros(0)
+    dia = rng.uniform(0.5, 1.5, nx) + np.concatenate([[0.0], -off]) + np.concatenate([-off, [0.0]])
+    A = np.diag(dia) + np.diag(off, 1) + np.diag(off, -1)
+    r = rng.normal(size=(n, nx))
+    expected = _dense_all_at_once(spec.dense_matrix(), -A, dT, r)
+    op = ref_port.SampleOperator(dia, off, np.zeros(nx))
+    u, imag = ref_port.three_step(spec.eigenvalues, spec.scaling, ref_port.shifted_solvers(op, spec.eigenvalues, dT), r)
+    scale = max(np.abs(expected).max(), 1e-30)
+    assert np.abs(u - expected).max() / scale <= 1e-9
+    assert imag <= 1e-10 * max(np.abs(u).max(), 1.0)
