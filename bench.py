@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""Benchmark: KLE-CGC solves/s (and fine-step DOF-updates/s) on the
+BASELINE config-2 workload, one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2|c1|c4]
+
+A step = one complete batched KLE-CGC solve of the rank's sample shard with
+the inputs resident in HBM: coefficient field, factorisation, Hermite-gPC
+surrogate U0 (DMMA GEMM), the PCGC outer loop to tol with per-sample
+freezing, and the two-pass mean/variance (NCCL allreduce when N > 1).
+Weak scaling: every rank solves M samples (global ids rank*M ..).
+
+Rank 0 prints one JSON line.
+``--impl reference`` times the CPU reference path (the oracle's per-sample
+restatement of pintuq, scipy SuperLU/LAPACK/pocketfft — bit-identical to
+the reference) on the same config over all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # BASELINE.json configs[1]: the metric's workload on one B200
+    "c2": dict(nx=511, d=8, N=64, J=64, M=65536, degree=3, train="gauss2048", alpha=1e-3, tol=1e-8),
+    # configs[0] (CPU oracle config) and configs[3] (scaling sweep of config 1)
+    "c1": dict(nx=127, d=4, N=16, J=32, M=256, degree=2, train="gh3", alpha=1e-3, tol=1e-8),
+    "c4": dict(nx=127, d=4, N=16, J=32, M=131072, degree=2, train="gh3", alpha=1e-3, tol=1e-8),
+}
+METRIC = "fine-step DOF-updates/s and KLE-CGC solves/s at fixed tol, 1/2/4/8 B200"
+FLOPS_PER_DOF = 6.0   # rhs add 1, forward FMA 2, diagonal scale 1, back-substitution FMA 2
+SEED = 2718
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU work of the baseline sample")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def problem(cfgname):
+    from paper_2510_26180_b200 import LogNormalKL1D, RngStream, SolverConfig, make_time_grid
+
+    c = CONFIGS[cfgname]
+    model = LogNormalKL1D(nx=c["nx"], d=c["d"], sigma=0.5, ell=0.3)
+    grid = make_time_grid(1.0, c["N"], c["J"])
+    cfg = SolverConfig(alpha=c["alpha"], tol=c["tol"], max_outer_iters=60, seed=SEED)
+    train_rng, eval_rng, _ = RngStream(SEED).split(3)
+    if c["train"] == "gh3":
+        from paper_2510_26180_b200.engine import gauss_hermite_grid
+
+        train = gauss_hermite_grid(c["d"], 3)
+    else:
+        train = train_rng.normal(0.0, 1.0, size=(2048, c["d"]))
+    return c, model, grid, cfg, train, eval_rng
+
+
+def eval_samples(eval_rng, M_total, d):
+    return eval_rng.normal(0.0, 1.0, size=(M_total, d))
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                     "--format=csv,noheader,nounits", "-lms", "200"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        while not self._stop.is_set():
+            line = proc.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        proc.terminate()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        time.sleep(0.3)
+        self._stop.set()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4) if r[2 + i] == "Active"})
+        loaded = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_26180_b200 import _lib
+    from paper_2510_26180_b200.device import DeviceOperator, empty, ptr, stream_ptr
+    from paper_2510_26180_b200.engine import KleCgcSolver
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+    from paper_2510_26180_b200.surrogate import build_surrogate
+    from paper_2510_26180_b200.core import ParameterSample
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c, model, grid, cfg, train, eval_rng = problem(args.config)
+    M = c["M"]
+    t0 = time.time()
+    training = [ParameterSample(x, id=i) for i, x in enumerate(train)]
+    sur = build_surrogate(model, grid, cfg, training, eps_kl=1e-10, degree=c["degree"])
+    t_build = time.time() - t0
+    solver = KleCgcSolver(model, grid, cfg, sur)
+    xi_all = eval_samples(eval_rng, M * world, c["d"])
+    xi_host = np.ascontiguousarray(xi_all[rank * M:(rank + 1) * M])
+    xi_d = torch.as_tensor(xi_host, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(x):
+        res = solver.solve(x)
+        mean, var = solver.moments(res, M_total=M * world)
+        return res, mean, var
+
+    for _ in range(args.warmup):
+        res, mean, var = step(xi_d)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters_sum = 0
+    kmax = 0
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res, mean, var = step(xi_d)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    it = res.batch.iters
+    iters_sum = int(it.sum().item())
+    kmax = int(it.max().item())
+    status = res.batch.status.cpu().numpy()
+    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    it_t = torch.tensor([iters_sum], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+    ms_max = float(ms_t.item())
+    total_iters = float(it_t.item())
+    dof_per_iter = grid.n_coarse * grid.n_fine_per_coarse * model.nx
+    solves_per_s = M * world / (ms_max * 1e-3)
+    dof_per_s = total_iters * dof_per_iter / (ms_max * 1e-3)
+
+    # ---- kernel-level timing of the two hot kernels (all samples active) ----
+    op = DeviceOperator.from_model(model, xi_d)
+    U = solver.surrogate.predict(xi_d)
+    blob = op.blob(grid.deltat)
+    tables = solver.tables
+    R = empty(M, grid.n_coarse, model.nx)
+    st_ptr = stream_ptr()
+
+    def fgr():
+        _lib.call("kle_fgr_f64", ptr(U), ptr(op.u0), None, None, ptr(R), ptr(blob), ptr(op.dia), ptr(op.off),
+                  ptr(tables.scaling), None, M, grid.n_coarse, model.nx, grid.n_fine_per_coarse, grid.deltat,
+                  grid.deltaT, op.g0, cfg.alpha, st_ptr)
+
+    nbytes = int(_lib.query("kle_cgc_scratch_bytes", M, grid.n_coarse, model.nx))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    inc = empty(M)
+
+    def cgc():
+        _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
+                  ptr(op.off), M, grid.n_coarse, model.nx, grid.deltaT, 1, 1, -1.0, None, None, None, None, None,
+                  ptr(scratch), nbytes, st_ptr)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    fgr_ms = timed(fgr)
+    cgc_ms = timed(cgc)
+    gemm_ms = timed(lambda: solver.surrogate.predict(xi_d, out=U))
+    peaks = load_peaks()
+    fgr_flops = FLOPS_PER_DOF * M * dof_per_iter
+    fgr_tflops = fgr_flops / (fgr_ms * 1e-3) / 1e12
+    cgc_bytes = 24.0 * M * grid.n_coarse * model.nx   # read R, read U, write U (compulsory)
+    cgc_gbs = cgc_bytes / (cgc_ms * 1e-3) / 1e9
+    fgr_bytes = 16.0 * M * grid.n_coarse * model.nx   # read U, write R
+    K_g = solver.surrogate.inner_dim
+    gemm_tflops = 2.0 * M * K_g * grid.n_coarse * model.nx / (gemm_ms * 1e-3) / 1e12
+    avg_iters = total_iters / (M * world)
+    share_fgr = avg_iters * fgr_ms
+    share_cgc = avg_iters * cgc_ms
+
+    # ---- end to end through the public API: host xi -> device -> host moments ----
+    e2e = None
+    if world >= 1:
+        pinned = torch.from_numpy(xi_host).pin_memory()
+        host_mean = torch.empty(mean.numel(), dtype=torch.float64).pin_memory()
+        host_var = torch.empty_like(host_mean).pin_memory()
+        host_it = torch.empty(M, dtype=torch.int32).pin_memory()
+        host_st = torch.empty(M, dtype=torch.int32).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nrep = max(1, min(args.steps, 2))
+        for _ in range(nrep):
+            xd = pinned.to("cuda", non_blocking=True)
+            r2, m2, v2 = step(xd)
+            host_mean.copy_(m2.reshape(-1), non_blocking=True)
+            host_var.copy_(v2.reshape(-1), non_blocking=True)
+            host_it.copy_(r2.batch.iters, non_blocking=True)
+            host_st.copy_(r2.batch.status, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1) / nrep], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": M * world / (float(e2e_ms.item()) * 1e-3), "unit": "solves/s",
+               "h2d_bytes_per_step": int(xi_host.nbytes),
+               "d2h_bytes_per_step": int(host_mean.numel() * 16 + M * 8),
+               "ms_per_step": float(e2e_ms.item())}
+
+    launches_per_step = 1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 2 * kmax + 4 + 2
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_host)
+    if rank == 0:
+        fp64_peak = peaks.get("fp64_tflops")
+        line = {
+            "metric": METRIC,
+            "value": solves_per_s,
+            "unit": "KLE-CGC solves/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) KL coordinates, BASELINE configs; no dataset exists)",
+            "config": {"workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3}[args.config] }] ({args.config}): "
+                                   f"nx={model.nx}, N={grid.n_coarse}, J={grid.n_fine_per_coarse}, d={c['d']}, "
+                                   f"Hermite p={c['degree']}, alpha={cfg.alpha}, tol={cfg.tol}",
+                       "samples_per_gpu": M, "global_samples": M * world,
+                       "parallelism": f"sample-sharded x{world}",
+                       "l2": "inputs larger than L2 (state 8*M*N*nx bytes per rank)"},
+            "fine_dof_updates_per_s": dof_per_s,
+            "avg_outer_iters": avg_iters,
+            "max_outer_iters": kmax,
+            "all_converged": bool(np.all(status == 1)),
+            "surrogate_build_s": t_build,
+            "surrogate": {"m_q": sur.m_q, "P": solver.surrogate.P, "K_g": K_g, "mode": solver.surrogate.mode},
+            "roofline": {
+                "kernel": "fgr_kernel (fused J-step fine sweep + CGC rhs)",
+                "bound": "fp64",
+                "achieved": fgr_tflops,
+                "peak": fp64_peak,
+                "unit": "TFLOP/s",
+                "frac": (fgr_tflops / fp64_peak) if fp64_peak else None,
+                "traffic": None,
+                "peak_source": peaks.get("fp64_source"),
+                "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch",
+                "hbm_frac": (fgr_bytes / (fgr_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
+                "ms_per_launch": fgr_ms,
+            },
+            "kernels": {
+                "cgc_kernel": {"bound": "hbm", "achieved": cgc_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": cgc_gbs / peaks["hbm_gbs"], "ms_per_launch": cgc_ms,
+                               "algorithmic": "24 B per (n, i) per sample: read R, read U, write U"},
+                "gemm_bias_kernel": {"bound": "tensor(dmma)", "achieved": gemm_tflops,
+                                     "peak": peaks.get("dmma_tflops"), "unit": "TFLOP/s",
+                                     "frac": gemm_tflops / peaks["dmma_tflops"] if peaks.get("dmma_tflops") else None,
+                                     "ms_per_launch": gemm_ms},
+                "step_share": {"fgr": share_fgr / ms_max, "cgc": share_cgc / ms_max},
+            },
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def load_peaks():
+    out = {"hbm_gbs": 6537.0}
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        out["hbm_gbs"] = float(json.loads(p.read_text()).get("hbm_gbs", 6537.0))
+        out["hbm_source"] = "MEASURED_PEAKS.json"
+    else:
+        out["hbm_gbs"] = 6650.0
+        out["hbm_source"] = "fallback (B200_PROFILING.md)"
+    f = ROOT / "profiles" / "r01_fp64_peaks.jsonl"
+    if f.exists():
+        for line in f.read_text().splitlines():
+            try:
+                d = json.loads(line)
+            except ValueError:
+                continue
+            if d.get("what") == "dfma_tflops":
+                out["fp64_tflops"] = d["value"]
+                out["fp64_source"] = "measured DFMA peak, profiles/r01_fp64_peaks.jsonl (tools/fp64_peaks.cu)"
+            if d.get("what") == "dmma_tflops":
+                out["dmma_tflops"] = d["value"]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle/ref_port: bit-identical restatement of pintuq)
+# ---------------------------------------------------------------------------
+_W = {}
+
+
+def _cpu_init(payload):
+    _W.update(payload)
+
+
+def _cpu_solve(i):
+    from oracle import ref_port
+
+    w = _W
+    xi = w["xi"][i]
+    a = np.exp(xi @ w["kl_table"])
+    dia = (a[:-1] + a[1:]) * w["inv_h2"]
+    off = -a[1:-1] * w["inv_h2"]
+    op = ref_port.SampleOperator(dia, off, np.full(len(dia), 1.0))
+    U0 = ref_port.surrogate_predict(w["mean"], w["lam"], w["modes"], w["coeffs"], w["degree"], xi)
+    out = ref_port.pcgc(op, w["u0"], U0, w["N"], w["J"], 1.0, w["alpha"], w["tol"], 60)
+    return out["iters"]
+
+
+def cpu_baseline(args, c, model, grid, cfg, sur, xi_host):
+    """Time the reference CPU path on a bounded sample of the workload over
+    all host cores (ProcessPool, one sample per task)."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    cores = os.cpu_count() or 1
+    payload = dict(xi=xi_host, kl_table=model.kl_table,
+                   inv_h2=1.0 / (model.h * model.h), u0=model.initial_condition(), mean=sur.mean_field,
+                   lam=sur.eigenvalues, modes=sur.modes, coeffs=sur.coeffs, degree=sur.degree,
+                   N=grid.n_coarse, J=grid.n_fine_per_coarse, alpha=cfg.alpha, tol=cfg.tol)
+    # size the sample: one probe solve, then ~cpu_seconds of wall on `cores` workers
+    _cpu_init(payload)
+    t0 = time.time()
+    _cpu_solve(0)
+    per = time.time() - t0
+    n = int(max(cores, min(len(xi_host), cores * max(1.0, args.cpu_seconds / max(per, 1e-3)))))
+    n = min(n, len(xi_host))
+    import multiprocessing as mp
+
+    # fork: workers inherit the surrogate tables without pickling them
+    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+        list(ex.map(_cpu_solve, range(min(cores, n))))  # warm the workers
+        t0 = time.time()
+        its = list(ex.map(_cpu_solve, range(n)))
+        wall = time.time() - t0
+    dof = float(np.sum(its)) * grid.n_coarse * grid.n_fine_per_coarse * model.nx
+    return {"value": n / wall, "unit": "KLE-CGC solves/s", "cores": cores, "kind": "port",
+            "sample": f"first {n} of the {len(xi_host)} config samples, surrogate_predict + pcgc_solve "
+                      f"(oracle/ref_port = pintuq arithmetic, scipy SuperLU/LAPACK/pocketfft), "
+                      f"{cores} processes, {wall:.1f} s wall",
+            "fine_dof_updates_per_s": dof / wall, "single_core_s_per_solve": per}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    c, model, grid, cfg, train, eval_rng = problem(args.config)
+    from concurrent.futures import ProcessPoolExecutor
+
+    # the reference builds its surrogate on the CPU too (collect_snapshots ->
+    # kl_build -> gpc_fit); training solves run over all cores
+    t0 = time.time()
+    cores = os.cpu_count() or 1
+    sur = _cpu_build_surrogate(model, grid, cfg, train, c["degree"], cores)
+    t_build = time.time() - t0
+    xi_host = eval_samples(eval_rng, c["M"], c["d"])
+    vals = []
+    res = None
+    for s in range(args.warmup + args.steps):
+        res = cpu_baseline(args, c, model, grid, cfg, sur, xi_host)
+        if s >= args.warmup:
+            vals.append(res["value"])
+    v = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "KLE-CGC solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": {"workload": f"{args.config} (same as the b200 arm)", "samples_per_gpu": c["M"]},
+            "cpu_baseline": {**res, "value": v}, "surrogate_build_s": t_build,
+            "e2e": {"value": v, "unit": "KLE-CGC solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _snap_one(args):
+    from oracle import ref_port
+
+    xi, kl_table, inv_h2, u0, N, J, alpha, tol = args
+    a = np.exp(xi @ kl_table)
+    dia = (a[:-1] + a[1:]) * inv_h2
+    off = -a[1:-1] * inv_h2
+    op = ref_port.SampleOperator(dia, off, np.full(len(dia), 1.0))
+    init = ref_port.coarse_sweep(op, u0, N, 1.0 / N)
+    return ref_port.pcgc(op, u0, init, N, J, 1.0, alpha, tol, 60)["states"]
+
+
+def _cpu_build_surrogate(model, grid, cfg, train, degree, cores):
+    from concurrent.futures import ProcessPoolExecutor
+
+    from oracle import ref_port
+    from paper_2510_26180_b200.models import ParameterMap
+    from paper_2510_26180_b200.surrogate import KLGpcSurrogate
+
+    jobs = [(x, model.kl_table, 1.0 / (model.h * model.h), model.initial_condition(), grid.n_coarse,
+             grid.n_fine_per_coarse, cfg.alpha, cfg.tol) for x in train]
+    import multiprocessing as mp
+
+    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+        fields = np.array(list(ex.map(_snap_one, jobs, chunksize=4)))
+    w = model.cell_volume * grid.deltaT
+    mean, lam, modes, X = ref_port.kl_build(fields, w, 1e-10)
+    zeta = ref_port.kl_coefficients(X, modes, lam, w)
+    coeffs = ref_port.gpc_fit(train, zeta, degree)
+    return KLGpcSurrogate(mean, lam, modes, coeffs, degree, [ParameterMap("identity", -np.inf, np.inf)] * len(train[0]))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)

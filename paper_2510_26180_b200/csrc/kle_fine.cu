@@ -97,7 +97,8 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
 }
 
 // ---------------------------------------------------------------------------
-// Fused F + rhs kernel. CTA = (group of subintervals, sample).
+// Fused F + rhs kernel. CTA = (sample, group of subintervals); samples on
+// grid.x (grid.y is limited to 65535).
 // ---------------------------------------------------------------------------
 template <int MR, int P, int R, int NT>
 __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;  // subintervals per CTA
   extern __shared__ double sfac[];
-  const int s = blockIdx.y;
+  const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
 
   int nr[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) nr[r] = blockIdx.x * NC + (w * SLOTS + slot) * R + r;
+  for (int r = 0; r < R; ++r) nr[r] = blockIdx.y * NC + (w * SLOTS + slot) * R + r;
 
   double x[R][MR];
   if (a.F_given == nullptr) {
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;
   extern __shared__ double sfac[];
-  const int s = blockIdx.y;
+  const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
   const int nx = a.nx, Q = a.Q;
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
   for (int i = tid; i < L::DOUBLES; i += NT) sfac[i] = gb[i];
   int q[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) q[r] = blockIdx.x * NC + (w * SLOTS + slot) * R + r;
+  for (int r = 0; r < R; ++r) q[r] = blockIdx.y * NC + (w * SLOTS + slot) * R + r;
   const double hg = a.h * a.g0;
   double x[R][MR];
 #pragma unroll
@@ -252,7 +253,7 @@ struct FineInst {
       cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    dim3 grid((a.N + NC - 1) / NC, a.M);
+    dim3 grid(a.M, (a.N + NC - 1) / NC);
     fgr_kernel<MR, P, R, NT><<<grid, NT, smem, st>>>(a);
     return check_launch("fgr_kernel");
   }
@@ -263,7 +264,7 @@ struct FineInst {
       cudaFuncSetAttribute(sweep_kernel<MR, P, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    dim3 grid((a.Q + NC - 1) / NC, a.M);
+    dim3 grid(a.M, (a.Q + NC - 1) / NC);
     sweep_kernel<MR, P, R, NT><<<grid, NT, smem, st>>>(a);
     return check_launch("sweep_kernel");
   }
