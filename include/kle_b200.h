@@ -90,15 +90,27 @@ int kle_fgr_f64(const double* U, const double* u0, const double* F_given, double
 /* Scratch for the three-step solve (per-CTA slabs). */
 size_t kle_cgc_scratch_bytes(int M, int N, int nx);
 
+/* Pivots of the shifted systems (lambda_f I + dT A), f = 0..N/2, for every
+ * sample (factor_shifted, pintuq/pcgc.py:90-145; iteration invariant, so
+ * computed once per batch). Layout [M][N/2+1][nx] complex. Returns 0 bytes /
+ * KLE_ERR_UNSUPPORTED for shapes served by the on-the-fly path (N not a
+ * power of two, N > 64, nx > 1024). */
+size_t kle_shift_factor_bytes(int M, int N, int nx);
+int kle_shift_factor_f64(const double* dia, const double* off, const double* lam, int M, int N, int nx, double dT,
+                         double* sfac, void* stream);
+
 /* three_step_solve (pintuq/pcgc.py:148-172) over M samples:
  *   u = diag(1/scaling) F (lambda I + dT A)^{-1} F* diag(scaling) r
  * r, u are [M][N][nx]; lam is [N] interleaved complex (re, im) =
  * build_alpha_circulant(N, alpha).eigenvalues (pintuq/pcgc.py:68-76),
  * scaling / inv_scaling its scaling and 1/scaling; imag[M] (optional)
- * receives max|Im u| per sample. */
+ * receives max|Im u| per sample. sfac (optional, kle_shift_factor_f64)
+ * selects the cluster kernel; without it the pivots are formed on the fly
+ * and `scratch` (kle_cgc_scratch_bytes) is used. scaling == NULL means r is
+ * already alpha-scaled. */
 int kle_three_step_f64(const double* r, const double* scaling, const double* inv_scaling, const double* lam,
-                       const double* dia, const double* off, int M, int N, int nx, double dT, double* u,
-                       double* imag, void* scratch, size_t scratch_bytes, void* stream);
+                       const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
+                       double* u, double* imag, void* scratch, size_t scratch_bytes, void* stream);
 
 /* CGC update of one PCGC iteration k (pintuq/pcgc.py:331-348): U <- three_step(R)
  * in place, increment = max|U_new - U| per sample, stop test against tol,
@@ -106,8 +118,8 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
  * *active_count incremented once per still-active sample. R must already be
  * alpha-scaled (kle_fgr_f64 output). */
 int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, const double* lam,
-                       const double* dia, const double* off, int M, int N, int nx, double dT, int k,
-                       int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
+                       const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
+                       int k, int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
                        double* imag, int32_t* active_count, void* scratch, size_t scratch_bytes,
                        void* stream);
 

@@ -28,8 +28,11 @@ _SIGS = {
     "kle_sweep_f64": ([_p, _p, _p, _i, _i, _i, _i, _i, _d, _d, _p], _i),
     "kle_fgr_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _p], _i),
     "kle_cgc_scratch_bytes": ([_i, _i, _i], _z),
-    "kle_three_step_f64": ([_p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _p, _p, _p, _z, _p], _i),
-    "kle_cgc_update_f64": ([_p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z, _p], _i),
+    "kle_shift_factor_bytes": ([_i, _i, _i], _z),
+    "kle_shift_factor_f64": ([_p, _p, _p, _i, _i, _i, _d, _p, _p], _i),
+    "kle_three_step_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _p, _p, _p, _z, _p], _i),
+    "kle_cgc_update_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z,
+                            _p], _i),
     "kle_pcgc_workspace_bytes": ([_i, _i, _i], _z),
     "kle_pcgc_solve_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _i, _p, _p, _p, _p,
                             _p, _z, _p], _i),

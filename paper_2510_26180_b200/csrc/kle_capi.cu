@@ -96,12 +96,25 @@ size_t kle_cgc_scratch_bytes(int M, int N, int nx) {
   return (size_t)cgc_grid(M, N, nx) * cgc_scratch_doubles_per_cta(N, nx) * sizeof(double);
 }
 
+size_t kle_shift_factor_bytes(int M, int N, int nx) {
+  if (M <= 0 || N <= 0 || nx <= 0 || !cgc_cluster_supported(N, nx)) return 0;
+  return shift_factor_doubles(M, N, nx) * sizeof(double);
+}
+
+int kle_shift_factor_f64(const double* dia, const double* off, const double* lam, int M, int N, int nx, double dT,
+                         double* sfac, void* stream) {
+  if (M < 0 || N < 1 || nx < 1) return set_error(KLE_ERR_INVALID, "shift_factor: bad dims");
+  if (!cgc_cluster_supported(N, nx)) return set_error(KLE_ERR_UNSUPPORTED, "shift_factor: shape uses the on-the-fly path");
+  return shift_factor(dia, off, lam, M, N, nx, dT, sfac, KLE_STREAM(stream));
+}
+
 int kle_three_step_f64(const double* r, const double* scaling, const double* inv_scaling, const double* lam,
-                       const double* dia, const double* off, int M, int N, int nx, double dT, double* u,
-                       double* imag, void* scratch, size_t scratch_bytes, void* stream) {
+                       const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
+                       double* u, double* imag, void* scratch, size_t scratch_bytes, void* stream) {
   if (M < 0 || N < 1 || nx < 1) return set_error(KLE_ERR_INVALID, "three_step: bad dims");
   if (M == 0) return KLE_OK;
-  if (scratch_bytes < kle_cgc_scratch_bytes(M, N, nx)) return set_error(KLE_ERR_WORKSPACE, "three_step: scratch too small");
+  if (!sfac && scratch_bytes < kle_cgc_scratch_bytes(M, N, nx))
+    return set_error(KLE_ERR_WORKSPACE, "three_step: scratch too small");
   if (imag) cudaMemsetAsync(imag, 0, sizeof(double) * M, KLE_STREAM(stream));
   CgcArgs a{};
   a.R = r;
@@ -122,17 +135,19 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
   a.max_iters = 1;
   a.dT = dT;
   a.tol = 0.0;
+  if (sfac) return cgc_cluster_run(a, sfac, KLE_STREAM(stream));
   return cgc_run(a, KLE_STREAM(stream));
 }
 
 int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, const double* lam,
-                       const double* dia, const double* off, int M, int N, int nx, double dT, int k,
-                       int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
+                       const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
+                       int k, int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
                        double* imag, int32_t* active_count, void* scratch, size_t scratch_bytes,
                        void* stream) {
   if (M < 0 || N < 1 || nx < 1 || k < 1 || max_iters < k) return set_error(KLE_ERR_INVALID, "cgc_update: bad arguments");
   if (M == 0) return KLE_OK;
-  if (scratch_bytes < kle_cgc_scratch_bytes(M, N, nx)) return set_error(KLE_ERR_WORKSPACE, "cgc_update: scratch too small");
+  if (!sfac && scratch_bytes < kle_cgc_scratch_bytes(M, N, nx))
+    return set_error(KLE_ERR_WORKSPACE, "cgc_update: scratch too small");
   CgcArgs a{};
   a.R = R;
   a.U = U;
@@ -154,12 +169,17 @@ int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, co
   a.max_iters = max_iters;
   a.dT = dT;
   a.tol = tol;
+  if (sfac) return cgc_cluster_run(a, sfac, KLE_STREAM(stream));
   return cgc_run(a, KLE_STREAM(stream));
+}
+
+static size_t pcgc_scratch_part(int M, int N, int nx) {
+  return cgc_cluster_supported(N, nx) ? kle_shift_factor_bytes(M, N, nx) : kle_cgc_scratch_bytes(M, N, nx);
 }
 
 size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
   if (M <= 0 || N <= 0 || nx <= 0) return 0;
-  return align256((size_t)M * N * nx * sizeof(double)) + align256(kle_cgc_scratch_bytes(M, N, nx)) + 256;
+  return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256;
 }
 
 int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const double* off,
@@ -176,12 +196,15 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
   char* ws = static_cast<char*>(workspace);
   double* R = reinterpret_cast<double*>(ws);
   ws += align256((size_t)M * N * nx * sizeof(double));
-  const size_t scratch_bytes = kle_cgc_scratch_bytes(M, N, nx);
+  const bool clustered = cgc_cluster_supported(N, nx);
+  const size_t scratch_bytes = pcgc_scratch_part(M, N, nx);
   void* scratch = ws;
   ws += align256(scratch_bytes);
   int32_t* counter = reinterpret_cast<int32_t*>(ws);
+  double* sfac = clustered ? static_cast<double*>(scratch) : nullptr;
 
   const double dT = T / N, dt = dT / J;
+  if (clustered) KLE_TRY(shift_factor(dia, off, lam, M, N, nx, dT, sfac, st));
   cudaMemsetAsync(status, 0, sizeof(int32_t) * M, st);
   cudaMemsetAsync(iters, 0, sizeof(int32_t) * M, st);
   if (inc_hist) cudaMemsetAsync(inc_hist, 0xFF, sizeof(double) * (size_t)M * max_iters, st);
@@ -192,8 +215,8 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
     KLE_TRY(kle_fgr_f64(U, u0, nullptr, nullptr, R, fine_blob, dia, off, scaling, status, M, N, nx, J, dt, dT, g0,
                         alpha, stream));
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-    KLE_TRY(kle_cgc_update_f64(R, U, inv_scaling, lam, dia, off, M, N, nx, dT, k, max_iters, tol, status, iters,
-                               inc_hist, imag, counter, scratch, scratch_bytes, stream));
+    KLE_TRY(kle_cgc_update_f64(R, U, inv_scaling, lam, dia, off, sfac, M, N, nx, dT, k, max_iters, tol, status,
+                               iters, inc_hist, imag, counter, scratch, scratch_bytes, stream));
     cudaMemcpyAsync(&h_count, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return set_error(KLE_ERR_CUDA, cudaGetErrorString(e));

@@ -11,6 +11,8 @@
 //   rhs_n = dT (A b_n + g) + b_n,  b_n = F_n - G(prev_n)
 //         = (I + dT A) F_n - prev_n
 // so the coarse solve of the reference collapses to one matvec.
+#include <cstdlib>
+
 #include "kle_fine.cuh"
 #include "kle_internal.h"
 
@@ -29,10 +31,9 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
   const double* d = dia + (size_t)s * nx;
   const double* e = off + (size_t)s * nx;  // e[i] couples rows i, i+1; e[nx-1] unused
   double* b = blob + (size_t)s * L::DOUBLES;
-  // pass 1: l_i and inv_i
+  // LDL^T of I + hA: l_r (row r couples to r-1), inv_r = 1/beta_r; pad rows identity
   double beta_prev = 1.0;
   for (int row = 0; row < L::NXP; ++row) {
-    const int j = row % MR, k = row / MR;
     double l = 0.0, inv = 1.0;
     if (row < nx) {
       const double D = fma(h, d[row], 1.0);
@@ -45,38 +46,20 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
       inv = 1.0 / beta;
       beta_prev = beta;
     }
-    b[L::L_OFF + j * P + k] = l;
-    b[L::INV_OFF + j * P + k] = inv;
+    b[L::L_OFF + row] = l;
+    b[L::INV_OFF + row] = inv;
   }
-  // pass 2: chunk products, kappa
-  const double hg = h * g0;
-  for (int k = 0; k < P; ++k) {
-    double pi = 1.0;
-    for (int j = 0; j < MR; ++j) {
-      const int row = k * MR + j;
-      pi *= -b[L::L_OFF + j * P + k];
-      b[L::PIH_OFF + j * P + k] = pi * b[L::INV_OFF + j * P + k];
-      double lnext = 0.0;
-      if (row + 1 < L::NXP) lnext = b[L::L_OFF + ((row + 1) % MR) * P + (row + 1) / MR];
-      b[L::KAP_OFF + j * P + k] = (row < nx) ? hg * (1.0 + lnext) : 0.0;
-    }
-    double sg = 1.0;
-    for (int j = MR - 1; j >= 0; --j) {
-      const int row = k * MR + j;
-      double lnext = 0.0;
-      if (row + 1 < L::NXP) lnext = b[L::L_OFF + ((row + 1) % MR) * P + (row + 1) / MR];
-      sg *= -lnext;
-      b[L::SIG_OFF + j * P + k] = sg;
-    }
-  }
-  // pass 3: Kogge-Stone multipliers.  pie_k = pi at chunk end (before the
-  // inv scaling), sigs_k = sigma at chunk start.
+  // chunk products: pie_k = prod_j (-l_j) over chunk k, sigs_k = prod_j (-l_{j+1})
   double pie[P], sigs[P];
   for (int k = 0; k < P; ++k) {
-    double pi = 1.0;
-    for (int j = 0; j < MR; ++j) pi *= -b[L::L_OFF + j * P + k];
+    double pi = 1.0, sg = 1.0;
+    for (int j = 0; j < MR; ++j) pi *= -b[L::L_OFF + k * MR + j];
+    for (int j = MR - 1; j >= 0; --j) {
+      const int row = k * MR + j;
+      sg *= -((row + 1 < L::NXP) ? b[L::L_OFF + row + 1] : 0.0);
+    }
     pie[k] = pi;
-    sigs[k] = b[L::SIG_OFF + 0 * P + k];
+    sigs[k] = sg;
   }
   for (int t = 0; t < L::LOGP; ++t) {
     const int dd = 1 << t;
@@ -94,6 +77,7 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
       b[L::BB_OFF + t * P + k] = bb;
     }
   }
+  (void)g0;
 }
 
 // ---------------------------------------------------------------------------
@@ -105,7 +89,6 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
   using L = FineLayout<MR, P>;
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;  // subintervals per CTA
-  extern __shared__ double sfac[];
   const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -119,8 +102,8 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
 
   double x[R][MR];
   if (a.F_given == nullptr) {
-    const double* gb = a.ffac + (size_t)s * L::DOUBLES;
-    for (int i = tid; i < L::DOUBLES; i += NT) sfac[i] = gb[i];
+    LaneFactors<MR, P> fac;
+    fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
     const double hg = a.dt * a.g0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -135,8 +118,7 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
         x[r][j] = v;
       }
     }
-    __syncthreads();
-    for (int it = 0; it < a.J; ++it) be_solve<MR, P, R>(x, sfac, k);
+    be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -197,13 +179,12 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
   using L = FineLayout<MR, P>;
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;
-  extern __shared__ double sfac[];
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
   const int nx = a.nx, Q = a.Q;
-  const double* gb = a.fac + (size_t)s * L::DOUBLES;
-  for (int i = tid; i < L::DOUBLES; i += NT) sfac[i] = gb[i];
+  LaneFactors<MR, P> fac;
+  fac.load(a.fac + (size_t)s * L::DOUBLES, k, nx);
   int q[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) q[r] = blockIdx.y * NC + (w * SLOTS + slot) * R + r;
@@ -216,9 +197,8 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
       const int row = k * MR + j;
       x[r][j] = (row < nx && q[r] < Q) ? a.start[((size_t)s * Q + q[r]) * nx + row] + hg : 0.0;
     }
-  __syncthreads();
   for (int g = 0; g < a.nseg; ++g) {
-    for (int it = 0; it < a.J; ++it) be_solve<MR, P, R>(x, sfac, k);
+    be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (q[r] >= Q) continue;
@@ -235,9 +215,9 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
 // ---------------------------------------------------------------------------
 // host-side dispatch
 // ---------------------------------------------------------------------------
-template <int MR, int P>
+template <int MR, int P, int R_>
 struct FineInst {
-  static constexpr int R = (MR >= 32) ? 2 : (MR >= 8 ? 2 : 4);
+  static constexpr int R = R_;
   static constexpr int NT = 128;
   static constexpr int NC = (NT / 32) * (32 / P) * R;
 
@@ -247,46 +227,65 @@ struct FineInst {
     return check_launch("fine_factor_kernel");
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {
-    const size_t smem = (a.F_given ? 1 : FineLayout<MR, P>::DOUBLES) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
     dim3 grid(a.M, (a.N + NC - 1) / NC);
-    fgr_kernel<MR, P, R, NT><<<grid, NT, smem, st>>>(a);
+    fgr_kernel<MR, P, R, NT><<<grid, NT, 0, st>>>(a);
     return check_launch("fgr_kernel");
   }
   static int sweep(const SweepArgs& a, cudaStream_t st) {
-    const size_t smem = FineLayout<MR, P>::DOUBLES * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sweep_kernel<MR, P, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
     dim3 grid(a.M, (a.Q + NC - 1) / NC);
-    sweep_kernel<MR, P, R, NT><<<grid, NT, smem, st>>>(a);
+    sweep_kernel<MR, P, R, NT><<<grid, NT, 0, st>>>(a);
     return check_launch("sweep_kernel");
   }
 };
 
-#define KLE_FINE_DISPATCH(MR_, P_, CALL) \
-  if (lay.MR == MR_ && lay.P == P_) return FineInst<MR_, P_>::CALL;
+// (MR, P, R) variants; the first entry whose MR*P covers nx is the default,
+// KLE_FINE_VARIANT=<index> forces one (for tuning; blobs depend on MR, P).
+struct FineVariant {
+  int MR, P, R;
+};
+static const FineVariant kVariants[] = {
+    {1, 16, 4},  {2, 16, 4},  {4, 16, 4},  {8, 16, 4},  {16, 32, 4}, {32, 32, 2},  // defaults by size
+    {8, 16, 2},  {4, 32, 4},  {4, 32, 8},  {8, 16, 8},  {16, 16, 2}, {8, 32, 4},   // alternatives
+    {32, 16, 2}, {16, 32, 2}, {16, 32, 3}, {8, 32, 8},
+};
+static const int kNumDefaults = 6;
 
-#define KLE_FINE_ALL(CALL)            \
-  KLE_FINE_DISPATCH(1, 16, CALL)      \
-  KLE_FINE_DISPATCH(2, 16, CALL)      \
-  KLE_FINE_DISPATCH(4, 16, CALL)      \
-  KLE_FINE_DISPATCH(8, 16, CALL)      \
-  KLE_FINE_DISPATCH(16, 16, CALL)     \
-  KLE_FINE_DISPATCH(32, 16, CALL)     \
-  KLE_FINE_DISPATCH(32, 32, CALL)
+#define KLE_FINE_DISPATCH(MR_, P_, R_, CALL) \
+  if (lay.MR == MR_ && lay.P == P_ && lay.R == R_) return FineInst<MR_, P_, R_>::CALL;
+
+#define KLE_FINE_ALL(CALL)             \
+  KLE_FINE_DISPATCH(1, 16, 4, CALL)    \
+  KLE_FINE_DISPATCH(2, 16, 4, CALL)    \
+  KLE_FINE_DISPATCH(4, 16, 4, CALL)    \
+  KLE_FINE_DISPATCH(8, 16, 4, CALL)    \
+  KLE_FINE_DISPATCH(16, 32, 4, CALL)   \
+  KLE_FINE_DISPATCH(32, 32, 2, CALL)   \
+  KLE_FINE_DISPATCH(8, 16, 2, CALL)    \
+  KLE_FINE_DISPATCH(4, 32, 4, CALL)    \
+  KLE_FINE_DISPATCH(4, 32, 8, CALL)    \
+  KLE_FINE_DISPATCH(8, 16, 8, CALL)    \
+  KLE_FINE_DISPATCH(16, 16, 2, CALL)   \
+  KLE_FINE_DISPATCH(8, 32, 4, CALL)    \
+  KLE_FINE_DISPATCH(32, 16, 2, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 2, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 3, CALL)   \
+  KLE_FINE_DISPATCH(8, 32, 8, CALL)
 
 FineLayoutRT fine_layout(int nx) {
-  static const int cand[][2] = {{1, 16}, {2, 16}, {4, 16}, {8, 16}, {16, 16}, {32, 16}, {32, 32}};
-  for (auto& c : cand)
-    if (c[0] * c[1] >= nx) return {c[0], c[1], fine_blob_doubles(c[0], c[1])};
-  return {0, 0, 0};
+  const char* env = getenv("KLE_FINE_VARIANT");
+  if (env && *env) {
+    const int v = atoi(env);
+    const int nv = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
+    if (v >= 0 && v < nv && kVariants[v].MR * kVariants[v].P >= nx) {
+      const FineVariant& f = kVariants[v];
+      return {f.MR, f.P, f.R, fine_blob_doubles(f.MR, f.P)};
+    }
+  }
+  for (int i = 0; i < kNumDefaults; ++i) {
+    const FineVariant& f = kVariants[i];
+    if (f.MR * f.P >= nx) return {f.MR, f.P, f.R, fine_blob_doubles(f.MR, f.P)};
+  }
+  return {0, 0, 0, 0};
 }
 
 int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,

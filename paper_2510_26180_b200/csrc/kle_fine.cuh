@@ -14,88 +14,119 @@ template <int MR, int P>
 struct FineLayout {
   static constexpr int LOGP = ilog2c(P);
   static constexpr int NXP = MR * P;
-  static constexpr int L_OFF = 0;
-  static constexpr int INV_OFF = NXP;
-  static constexpr int PIH_OFF = 2 * NXP;
-  static constexpr int KAP_OFF = 3 * NXP;
-  static constexpr int SIG_OFF = 4 * NXP;
-  static constexpr int AF_OFF = 5 * NXP;
-  static constexpr int BB_OFF = 5 * NXP + LOGP * P;
-  static constexpr int DOUBLES = 5 * NXP + 2 * LOGP * P;
+  // chunk-major: lane k's MR values are contiguous (vector loads)
+  static constexpr int L_OFF = 0;        // l_r   (LDL^T sub-diagonal), [k][j]
+  static constexpr int INV_OFF = NXP;    // 1/beta_r,                 [k][j]
+  static constexpr int AF_OFF = 2 * NXP; // forward scan multipliers  [t][k]
+  static constexpr int BB_OFF = 2 * NXP + LOGP * P;  // backward scan multipliers
+  static constexpr int DOUBLES = 2 * NXP + 2 * LOGP * P;
 };
 
-// One backward-Euler solve (I + hA) x_new = x + h g0 on the x' = x + h g0
-// representation, for R right-hand sides held in registers.
-// `fac` points at the sample's blob (shared or global memory).
+// Per-lane register copy of the factor rows it owns.
+template <int MR, int P>
+struct LaneFactors {
+  double l[MR], inv[MR];
+  double af[FineLayout<MR, P>::LOGP], bb[FineLayout<MR, P>::LOGP];
+  double lnx;  // l of the next chunk's first row (0 for the last chunk)
+  int nreal;   // rows of this chunk that are real (< nx)
+
+  __device__ __forceinline__ void load(const double* __restrict__ blob, int k, int nx) {
+    using L = FineLayout<MR, P>;
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      l[j] = blob[L::L_OFF + k * MR + j];
+      inv[j] = blob[L::INV_OFF + k * MR + j];
+    }
+#pragma unroll
+    for (int t = 0; t < L::LOGP; ++t) {
+      af[t] = blob[L::AF_OFF + t * P + k];
+      bb[t] = blob[L::BB_OFF + t * P + k];
+    }
+    const double o = __shfl_down_sync(KLE_FULL_MASK, l[0], 1, P);
+    lnx = (k == P - 1) ? 0.0 : o;
+    nreal = min(MR, max(0, nx - k * MR));
+  }
+};
+
+// J backward-Euler solves (I + hA) x_new = x + h g0 on the x' = x + h g0
+// representation, R right-hand sides in registers, factors in registers.
+// Per step and row: five R-dependent FMAs
+//   yl_j = x_j - l_j yl_{j-1}            (local forward)
+//   y_j  = yl_j + pi_j Y                  (forward stitch, pi_j = prod -l)
+//   z'_j = y_j inv_j + kap_j              (kap_j = h g0 (1 + l_{j+1}))
+//   xl_j = z'_j - l_{j+1} xl_{j+1}        (local backward)
+//   x'_j = xl_j + sig_j X                 (backward stitch, sig_j = prod -l_{+1})
+// plus three R-independent products; Y, X come from P-lane carry scans.
 template <int MR, int P, int R>
-__device__ __forceinline__ void be_solve(double (&x)[R][MR], const double* __restrict__ fac, int k) {
+__device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, int J,
+                                         double hg) {
   using L = FineLayout<MR, P>;
-  // forward, chunk local
+  for (int it = 0; it < J; ++it) {
 #pragma unroll
-  for (int j = 1; j < MR; ++j) {
-    const double l = fac[L::L_OFF + j * P + k];
+    for (int j = 1; j < MR; ++j)
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[r][j] = fma(-l, x[r][j - 1], x[r][j]);
-  }
-  // forward carry scan across the P chunks
-  double Y[R];
+      for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+    double Y[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+    for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
 #pragma unroll
-  for (int t = 0; t < L::LOGP; ++t) {
-    const int d = 1 << t;
-    const double a = fac[L::AF_OFF + t * P + k];
+    for (int t = 0; t < L::LOGP; ++t) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t, P);
+        if (k >= (1 << t)) Y[r] = fma(f.af[t], o, Y[r]);
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], d, P);
-      if (k >= d) Y[r] = fma(a, o, Y[r]);
+      const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
+      Y[r] = (k == 0) ? 0.0 : o;
     }
-  }
+    {
+      double pi = 1.0;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
-    Y[r] = (k == 0) ? 0.0 : o;
-  }
-  // stitch + diagonal scale (+ source term absorbed in kap)
+      for (int j = 0; j < MR; ++j) {
+        pi *= -f.l[j];
 #pragma unroll
-  for (int j = 0; j < MR; ++j) {
-    const double inv = fac[L::INV_OFF + j * P + k];
-    const double ph = fac[L::PIH_OFF + j * P + k];
-    const double kp = fac[L::KAP_OFF + j * P + k];
+        for (int r = 0; r < R; ++r) x[r][j] = fma(pi, Y[r], x[r][j]);
+      }
+    }
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[r][j] = fma(x[r][j], inv, fma(ph, Y[r], kp));
-  }
-  // backward, chunk local
+    for (int j = MR - 1; j >= 0; --j) {
+      const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+      const double kap = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
 #pragma unroll
-  for (int j = MR - 2; j >= 0; --j) {
-    const double l = fac[L::L_OFF + (j + 1) * P + k];
+      for (int r = 0; r < R; ++r) {
+        double z = fma(x[r][j], f.inv[j], kap);
+        if (j + 1 < MR) z = fma(-ln, x[r][j + 1], z);
+        x[r][j] = z;
+      }
+    }
+    double X[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[r][j] = fma(-l, x[r][j + 1], x[r][j]);
-  }
-  // backward carry scan
-  double X[R];
+    for (int r = 0; r < R; ++r) X[r] = x[r][0];
 #pragma unroll
-  for (int r = 0; r < R; ++r) X[r] = x[r][0];
+    for (int t = 0; t < L::LOGP; ++t) {
 #pragma unroll
-  for (int t = 0; t < L::LOGP; ++t) {
-    const int d = 1 << t;
-    const double b = fac[L::BB_OFF + t * P + k];
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t, P);
+        if (k + (1 << t) < P) X[r] = fma(f.bb[t], o, X[r]);
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], d, P);
-      if (k + d < P) X[r] = fma(b, o, X[r]);
+      const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
+      X[r] = (k == P - 1) ? 0.0 : o;
     }
-  }
+    {
+      double sg = 1.0;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
-    X[r] = (k == P - 1) ? 0.0 : o;
-  }
+      for (int j = MR - 1; j >= 0; --j) {
+        sg *= -((j + 1 < MR) ? f.l[j + 1] : f.lnx);
 #pragma unroll
-  for (int j = 0; j < MR; ++j) {
-    const double sg = fac[L::SIG_OFF + j * P + k];
-#pragma unroll
-    for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
+        for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
+      }
+    }
   }
 }
 

@@ -11,7 +11,7 @@ int set_error(int code, const char* msg);
 int check_launch(const char* what);
 
 struct FineLayoutRT {
-  int MR, P, doubles;
+  int MR, P, R, doubles;
 };
 FineLayoutRT fine_layout(int nx);
 
@@ -63,6 +63,12 @@ struct CgcArgs {
   int M, N, nx, k, max_iters;
   double dT, tol;
 };
+
+bool cgc_cluster_supported(int N, int nx);
+size_t shift_factor_doubles(int M, int N, int nx);
+int shift_factor(const double* dia, const double* off, const double* lam, int M, int N, int nx, double dT,
+                 double* sfac, cudaStream_t st);
+int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st);
 
 int cgc_grid(int M, int N, int nx);
 size_t cgc_scratch_doubles_per_cta(int N, int nx);

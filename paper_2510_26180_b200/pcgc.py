@@ -73,16 +73,31 @@ def _cgc_scratch(M, N, nx):
     return torch.empty(max(nbytes, 8), dtype=torch.uint8, device="cuda"), nbytes
 
 
-def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float, r, prescaled=False):
+def shift_factors(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float):
+    """Pivots of (lambda_f I + dT A) for every sample (iteration invariant), or
+    None for shapes that form them on the fly (``kle_shift_factor_f64``)."""
+    nbytes = int(_lib.query("kle_shift_factor_bytes", op.M, N, op.nx))
+    if nbytes == 0:
+        return None
+    sfac = empty(nbytes // 8)
+    _lib.call("kle_shift_factor_f64", ptr(op.dia), ptr(op.off), ptr(tables.lam), op.M, N, op.nx, deltaT, ptr(sfac),
+              stream_ptr())
+    return sfac
+
+
+def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float, r, prescaled=False,
+                      sfac="auto"):
     """u = V (Lambda (x) I + dT I (x) A)^{-1} V^{-1} r for every sample;
     r: (M, N, nx) device tensor. Returns (u, imag (M,))."""
     M, _, nx = r.shape
     u = empty(M, N, nx)
     imag = empty(M)
-    scratch, nbytes = _cgc_scratch(M, N, nx)
+    if isinstance(sfac, str):
+        sfac = shift_factors(op, tables, N, deltaT)
+    scratch, nbytes = (None, 0) if sfac is not None else _cgc_scratch(M, N, nx)
     _lib.call("kle_three_step_f64", ptr(r.contiguous()), None if prescaled else ptr(tables.scaling),
-              ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia), ptr(op.off), M, N, nx, deltaT, ptr(u),
-              ptr(imag), ptr(scratch), nbytes, stream_ptr())
+              ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia), ptr(op.off), ptr(sfac), M, N, nx, deltaT,
+              ptr(u), ptr(imag), ptr(scratch), nbytes, stream_ptr())
     return u, imag
 
 
@@ -225,7 +240,8 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     iters = torch.zeros(1, dtype=torch.int32, device="cuda")
     inc = empty(1, cfg.max_outer_iters).fill_(float("nan"))
     imag = torch.zeros(1, dtype=torch.float64, device="cuda")
-    scratch, nbytes = _cgc_scratch(1, N, nx)
+    sfac = shift_factors(op, tables, N, grid.deltaT)
+    scratch, nbytes = (None, 0) if sfac is not None else _cgc_scratch(1, N, nx)
 
     def err(states):
         if reference is None:
@@ -250,8 +266,8 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
         _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha)
         # tol < 0 keeps the device from freezing the sample; the stop test is ours
         _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
-                  ptr(op.off), 1, N, nx, dT, k, cfg.max_outer_iters, -1.0, None, None, ptr(inc), ptr(imag), None,
-                  ptr(scratch), nbytes, stream_ptr())
+                  ptr(op.off), ptr(sfac), 1, N, nx, dT, k, cfg.max_outer_iters, -1.0, None, None, ptr(inc), ptr(imag),
+                  None, ptr(scratch), nbytes, stream_ptr())
         host = U[0].cpu().numpy()
         increment = float(inc[0, k - 1].item())
         wall_ms = 1e3 * (time.perf_counter() - tic)

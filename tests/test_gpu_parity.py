@@ -288,3 +288,52 @@ def test_empty_batch_is_noop(cuda):
 
     assert _lib.call("kle_fgr_f64", *([None] * 10), 0, 16, 127, 32, 0.1, 0.1, 1.0, 0.1, None) == 0
     assert _lib.call("kle_sweep_f64", None, None, None, 0, 1, 127, 1, 1, 0.1, 1.0, None) == 0
+
+
+@pytest.mark.parametrize("nx,N", [(127, 16), (511, 64), (255, 32), (1000, 8), (64, 2)])
+def test_cluster_and_on_the_fly_cgc_agree(cuda, nx, N):
+    """The cluster kernel (precomputed pivots, DSMEM stitching) and the
+    on-the-fly per-frequency kernel solve the same three-step system."""
+    from paper_2510_26180_b200 import LogNormalKL1D
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, three_step_device
+
+    rng = np.random.default_rng(nx + N)
+    M = 3
+    model = LogNormalKL1D(nx=nx, d=4)
+    xi = rng.normal(size=(M, 4))
+    op = DeviceOperator.from_model(model, xi)
+    spec = build_alpha_circulant(N, 1e-2)
+    tables = AlphaTables(spec)
+    r = rng.normal(size=(M, N, nx))
+    u1, im1 = three_step_device(op, tables, N, 1.0 / N, to_dev(r))
+    u2, im2 = three_step_device(op, tables, N, 1.0 / N, to_dev(r), sfac=None)
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    lam, sc = spec.eigenvalues, spec.scaling
+    p = np.fft.fft(sc[None, :, None] * r, axis=1, norm="ortho")
+    q = batched.thomas(lam[None, :, None] + dia[:, None, :] / N, (off / N)[:, None, :].astype(complex), p)
+    want = ((1.0 / sc)[None, :, None] * np.fft.ifft(q, axis=1, norm="ortho")).real
+    assert rel(u1.cpu().numpy(), want) <= 1e-10
+    assert rel(u2.cpu().numpy(), want) <= 1e-10
+    assert rel(u1.cpu().numpy(), u2.cpu().numpy()) <= 1e-11
+
+
+def test_non_power_of_two_N_pcgc(cuda):
+    """N = 12 (DFT fallback path) against the oracle."""
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    model = LogNormalKL1D(nx=63, d=4)
+    grid = make_time_grid(1.0, 12, 10)
+    cfg = SolverConfig(alpha=1e-2, tol=1e-9, max_outer_iters=60)
+    xi = np.random.default_rng(4).normal(size=(5, 4))
+    op = DeviceOperator.from_model(model, xi)
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    init = U.cpu().numpy()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    out = batched.pcgc(dia, off, model.initial_condition(), init, 12, 10, 1.0, 1e-2, 1e-9, 60)
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
+    assert rel(res.states.cpu().numpy(), out["states"]) <= RTOL
