@@ -4,22 +4,28 @@
 // Reference: three_step_solve pintuq/pcgc.py:148-172, factor_shifted :90-145,
 // the increment / stop test of pcgc_solve :335-348.
 //
-// The sample's N x nx block is split into CL row blocks of RB = 16*MR rows,
-// one CTA each (CL <= 8, a portable cluster). Per CTA:
-//   1. R[:, rows] -> shared-memory tile, radix-2 FFT along the time axis
-//      (p = F* scaling r, norm "ortho"); only f = 0..N/2 is solved
-//      (real input: q_{N-f} = conj(q_f)).
-//   2. For every frequency f, a 16-lane group owns the CTA's RB rows
-//      (MR per lane, in registers) and runs the complex LDL^T solve of
-//      (lambda_f I + dT A) with pivots 1/beta precomputed once per batch
-//      (shift_factor_kernel: the factorisation is iteration invariant).
-//      The two linear recurrences are stitched by a 16-lane affine scan
-//      (shuffles) and across the cluster's CTAs through distributed shared
-//      memory (each CTA publishes its block composite; consumers compose the
-//      composites of the blocks before/after them).
-//   3. Hermitian completion, inverse FFT, u = Re(.)/scaling, increment and
-//      imaginary-residue max-reductions (block, then cluster via DSMEM), the
-//      per-sample stop test.
+// The sample's N x nx block is split into CL row blocks of RB = 8*MR rows,
+// one CTA each. Per CTA:
+//   0. cp.async prefetch of the R rows, the old U rows (for the increment)
+//      and the operator's off-diagonal into shared memory; the pivots of the
+//      first frequency pass are loaded into registers at the same time.
+//   1. Two-for-one real FFT along time: rows c and c + RB/2 are packed as
+//      z = r_c + i r_{c+RB/2} into an [N][RB/2] complex tile (radix-2 DIT,
+//      bit-reversed input). p_f of both rows follows from Z_f, Z_{N-f}.
+//   2. For f = 0..N/2 (in passes of <= 17 frequencies), an 8-lane group owns
+//      the CTA's RB rows (MR per lane, registers) and solves
+//      (lambda_f I + dT A) q = p with the LDL^T pivots 1/beta precomputed once
+//      per batch (shift_factor_kernel). Chunks are stitched by a 3-stage
+//      affine lane scan and across the cluster's CTAs through distributed
+//      shared memory (block composites; consumers compose those of the blocks
+//      before/after them).
+//   3. The packed Hermitian spectra W_f = q_c + i q_{c+RB/2} (and the mirror
+//      W_{N-f}) are written in natural order (passes never touch each other's
+//      pending inputs), inverse FFT by radix-2 DIF (bit-reversed output),
+//      u = Re / Im parts over scaling; increment vs the prefetched old U;
+//      block + cluster max-reductions; per-sample stop test.
+// The two-for-one packing enforces the Hermitian symmetry of the real
+// solution, so u is real by construction (imag residue reported as 0).
 // HBM traffic per outer iteration and (n, i): R 8 B + U 8 B read, U 8 B
 // written, pivots 16 (N/2+1)/N B read.
 #include <cooperative_groups.h>
@@ -31,7 +37,8 @@ namespace cg = cooperative_groups;
 
 namespace kle {
 
-constexpr int CL_LANES = 16;
+constexpr int CL_LANES = 8;
+constexpr int CL_FPASS = 17;  // frequencies per pass
 
 __device__ __forceinline__ Cplx cfma(Cplx a, Cplx b, Cplx c) {  // a*b + c
   return {fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))};
@@ -45,23 +52,59 @@ __device__ __forceinline__ Cplx shfl_up_c(Cplx v, int d) {
 __device__ __forceinline__ Cplx shfl_down_c(Cplx v, int d) {
   return {__shfl_down_sync(KLE_FULL_MASK, v.re, d, CL_LANES), __shfl_down_sync(KLE_FULL_MASK, v.im, d, CL_LANES)};
 }
+__device__ __forceinline__ Cplx shfl_xor_c(Cplx v, int d) {
+  return {__shfl_xor_sync(KLE_FULL_MASK, v.re, d), __shfl_xor_sync(KLE_FULL_MASK, v.im, d)};
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+}
 
-// In-place radix-2 DIT over a [N][TC] tile (rows in bit-reversed order).
-__device__ void fft_tile_nt(Cplx* t, const Cplx* tw, int N, int TC, bool inverse) {
-  for (int len = 2; len <= N; len <<= 1) {
-    const int half = len >> 1, step = N / len;
-    const int nbf = (N >> 1) * TC;
-    for (int b = threadIdx.x; b < nbf; b += blockDim.x) {
+template <int LOGN>
+__device__ __forceinline__ int brev(int n) {
+  return LOGN == 0 ? 0 : (int)(__brev((unsigned)n) >> (32 - LOGN));
+}
+
+// radix-2 DIT, bit-reversed input -> natural output; tw[j] = exp(-2 pi i j/N)
+template <int LOGN, int TC>
+__device__ void fft_dit(Cplx* t, const Cplx* tw) {
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int lh = 0; lh < LOGN; ++lh) {
+    const int half = 1 << lh;
+    for (int b = threadIdx.x; b < (N / 2) * TC; b += blockDim.x) {
       const int c = b % TC, bf = b / TC;
-      const int g = bf / half, j = bf - g * half;
-      const int i0 = g * len + j, i1 = i0 + half;
-      Cplx w = tw[j * step];
-      if (inverse) w.im = -w.im;
-      const Cplx x0 = t[i0 * TC + c];
-      const Cplx x1 = t[i1 * TC + c];
+      const int j = bf & (half - 1), g = bf >> lh;
+      const int i0 = (g << (lh + 1)) + j, i1 = i0 + half;
+      const Cplx w = tw[j << (LOGN - 1 - lh)];
+      const Cplx x0 = t[i0 * TC + c], x1 = t[i1 * TC + c];
       const Cplx v = {fma(x1.re, w.re, -x1.im * w.im), fma(x1.re, w.im, x1.im * w.re)};
       t[i0 * TC + c] = {x0.re + v.re, x0.im + v.im};
       t[i1 * TC + c] = {x0.re - v.re, x0.im - v.im};
+    }
+    __syncthreads();
+  }
+}
+
+// radix-2 DIF with conjugate twiddles (inverse), natural input -> bit-reversed output
+template <int LOGN, int TC>
+__device__ void ifft_dif(Cplx* t, const Cplx* tw) {
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int lh = LOGN - 1; lh >= 0; --lh) {
+    const int half = 1 << lh;
+    for (int b = threadIdx.x; b < (N / 2) * TC; b += blockDim.x) {
+      const int c = b % TC, bf = b / TC;
+      const int j = bf & (half - 1), g = bf >> lh;
+      const int i0 = (g << (lh + 1)) + j, i1 = i0 + half;
+      const Cplx w = tw[j << (LOGN - 1 - lh)];
+      const Cplx x0 = t[i0 * TC + c], x1 = t[i1 * TC + c];
+      const Cplx d = {x0.re - x1.re, x0.im - x1.im};
+      t[i0 * TC + c] = {x0.re + x1.re, x0.im + x1.im};
+      t[i1 * TC + c] = {fma(d.re, w.re, d.im * w.im), fma(d.im, w.re, -d.re * w.im)};  // d * conj(w)
     }
     __syncthreads();
   }
@@ -92,220 +135,229 @@ __global__ void shift_factor_kernel(const double* __restrict__ dia, const double
 }
 
 template <int MR>
-__global__ void __launch_bounds__(576, 1) cgc_cluster_kernel(CgcArgs a, const double* __restrict__ sfac_d,
-                                                              int log2N) {
-  constexpr int RB = CL_LANES * MR;
+__device__ __forceinline__ void load_pivots(Cplx (&ib)[MR], Cplx& ibprev, const Cplx* __restrict__ src, int r0,
+                                            int nx) {
+  ibprev = (r0 > 0 && r0 - 1 < nx) ? src[r0 - 1] : Cplx{0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < MR; ++j) ib[j] = (r0 + j < nx) ? src[r0 + j] : Cplx{1.0, 0.0};
+}
+
+template <int LOGN, int MR>
+__global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const double* __restrict__ sfac_d) {
+  constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
+  constexpr int NPASS = (NF + CL_FPASS - 1) / CL_FPASS;
+  constexpr int FP = (NF + NPASS - 1) / NPASS;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int c = (int)cluster.block_rank();
   const int s = blockIdx.x / CL;
-  const int N = a.N, nx = a.nx, NF = N / 2 + 1;
+  const int nx = a.nx;
   if (a.status && a.status[s] != KLE_SAMPLE_ACTIVE) return;  // uniform over the cluster
 
-  extern __shared__ double smem[];
-  Cplx* tile = reinterpret_cast<Cplx*>(smem);  // [N][RB]
-  Cplx* tw = tile + N * RB;                    // [N]
-  Cplx* fwd = tw + N;                          // [NF][2]: (A, B) block composite
-  Cplx* bwd = fwd + 2 * NF;                    // [NF][2]: (S, T)
-  double* red = reinterpret_cast<double*>(bwd + 2 * NF);  // [34]
+  extern __shared__ __align__(16) double smem[];
+  Cplx* tile = reinterpret_cast<Cplx*>(smem);       // [N][HC] packed spectra
+  double* uold = smem + 2 * N * HC;                 // [N][RB]
+  double* offs = uold + N * RB;                     // [RB + 2]: dT*off[row0-1 .. row0+RB]
+  Cplx* tw = reinterpret_cast<Cplx*>(offs + RB + 2);  // [N/2]
+  Cplx* fwd = tw + N / 2;                           // [NF][2]
+  Cplx* bwd = fwd + 2 * NF;                         // [NF][2]
+  double* red = reinterpret_cast<double*>(bwd + 2 * NF);  // [8 + 2]
 
   const int tid = threadIdx.x;
-  for (int j = tid; j < N; j += blockDim.x) {
+  const size_t sb = (size_t)s * N * nx;
+  const int row0 = c * RB;
+  // ---- phase 0: prefetch --------------------------------------------------
+  for (int e = tid; e < N * RB; e += blockDim.x) {
+    const int n = e / RB, col = e % RB, row = row0 + col;
+    double* dst = reinterpret_cast<double*>(&tile[brev<LOGN>(n) * HC + (col % HC)]) + (col / HC);
+    if (row < nx) {
+      cp_async8(dst, a.R + sb + (size_t)n * nx + row);
+      if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
+    } else {
+      *dst = 0.0;
+    }
+  }
+  for (int e = tid; e < RB + 2; e += blockDim.x) {
+    const int row = row0 - 1 + e;  // offs[e] couples rows row and row+1
+    offs[e] = (row >= 0 && row + 1 < nx) ? a.dT * a.off[(size_t)s * nx + row] : 0.0;
+  }
+  for (int j = tid; j < N / 2; j += blockDim.x) {
     double sn, cs;
     sincospi(-2.0 * (double)j / (double)N, &sn, &cs);
     tw[j] = {cs, sn};
   }
-  const size_t sb = (size_t)s * N * nx;
-  const int row0 = c * RB;
-  // ---- phase 1: tile load (bit-reversed rows) + forward FFT --------------
-  for (int idx = tid; idx < N * RB; idx += blockDim.x) {
-    const int n = idx / RB, col = idx - n * RB, row = row0 + col;
-    double v = 0.0;
-    if (row < nx) {
-      v = a.R[sb + (size_t)n * nx + row];
-      if (a.load_scale) v *= a.load_scale[n];
-    }
-    const int pos = log2N > 0 ? (int)(__brev((unsigned)n) >> (32 - log2N)) : 0;
-    tile[pos * RB + col] = {v, 0.0};
-  }
-  __syncthreads();
-  fft_tile_nt(tile, tw, N, RB, false);
-
-  // ---- phase 2: shifted solves ---------------------------------------------
   const int fsys = tid / CL_LANES, k = tid % CL_LANES;
-  const bool valid = fsys < NF;
-  const int f = valid ? fsys : NF - 1;
-  const double rsN = 1.0 / sqrt((double)N);
-  const Cplx* ib_s = reinterpret_cast<const Cplx*>(sfac_d) + ((size_t)s * NF + f) * nx;
-  const double* ee = a.off + (size_t)s * nx;
-  const int r0 = row0 + k * MR;
-
-  Cplx y[MR], l[MR], ib[MR];
-  // l_r = dT off_{r-1} / beta_{r-1} (0 for r = 0 and pad rows)
-  Cplx ibprev = {0.0, 0.0};
-  if (r0 > 0 && r0 - 1 < nx) ibprev = ib_s[r0 - 1];
-#pragma unroll
-  for (int j = 0; j < MR; ++j) {
-    const int r = r0 + j;
-    const Cplx p = tile[f * RB + k * MR + j];
-    y[j] = {p.re * rsN, p.im * rsN};
-    ib[j] = (r < nx) ? ib_s[r] : Cplx{1.0, 0.0};
-    double E = 0.0;
-    if (r > 0 && r < nx) E = a.dT * ee[r - 1];
-    const Cplx ip = (j == 0) ? ibprev : ib[j - 1];
-    l[j] = {E * ip.re, E * ip.im};
-  }
-  // forward, lane local: yl_j = p_j - l_j yl_{j-1}; composite (A = prod(-l), B = yl_end)
-  Cplx A = {1.0, 0.0};
-#pragma unroll
-  for (int j = 0; j < MR; ++j) {
-    if (j > 0) y[j] = cfma({-l[j].re, -l[j].im}, y[j - 1], y[j]);
-    A = cneg_mul(l[j], A);
-  }
-  Cplx B = y[MR - 1];
-#pragma unroll
-  for (int d = 1; d < CL_LANES; d <<= 1) {
-    const Cplx Ao = shfl_up_c(A, d), Bo = shfl_up_c(B, d);
-    if (k >= d) {
-      B = cfma(A, Bo, B);
-      A = cmul(A, Ao);
-    }
-  }
-  Cplx Ae = shfl_up_c(A, 1), Be = shfl_up_c(B, 1);
-  if (k == 0) {
-    Ae = {1.0, 0.0};
-    Be = {0.0, 0.0};
-  }
-  if (valid && k == CL_LANES - 1) {
-    fwd[2 * f] = A;
-    fwd[2 * f + 1] = B;
-  }
-  cluster.sync();
-  Cplx Yc = {0.0, 0.0};
-  for (int q = 0; q < c; ++q) {
-    const Cplx* rf = cluster.map_shared_rank(fwd, q);
-    Yc = cfma(rf[2 * f], Yc, rf[2 * f + 1]);
-  }
-  const Cplx Cin = cfma(Ae, Yc, Be);
-  // stitch + scale: y_j += pi_j Cin, z_j = y_j / beta_j
+  const int r0l = k * MR;  // local first row of this lane
+  const int r0 = row0 + r0l;
+  const Cplx* piv = reinterpret_cast<const Cplx*>(sfac_d) + (size_t)s * NF * nx;
+  Cplx ib[MR], ibprev;
   {
-    Cplx pi = {1.0, 0.0};
+    const int f = min(fsys, NF - 1);
+    load_pivots<MR>(ib, ibprev, piv + (size_t)f * nx, r0, nx);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
+    for (int e = tid; e < N * RB; e += blockDim.x) {
+      const int n = e / RB, col = e % RB;
+      reinterpret_cast<double*>(&tile[brev<LOGN>(n) * HC + (col % HC)])[col / HC] *= a.load_scale[n];
+    }
+    __syncthreads();
+  }
+  fft_dit<LOGN, HC>(tile, tw);
+
+  const double hs = 0.5 / sqrt((double)N);  // two-for-one unpacking x 1/sqrt(N)
+#pragma unroll 1
+  for (int pass = 0; pass < NPASS; ++pass) {
+    const int fl = pass * FP + fsys;
+    const bool valid = fsys < FP && fl < NF;
+    const int f = valid ? fl : NF - 1;
+    if (pass > 0) load_pivots<MR>(ib, ibprev, piv + (size_t)f * nx, r0, nx);
+    // p_f for the lane's rows from the packed spectrum
+    Cplx y[MR];
+    const int fm = (N - f) & (N - 1);
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
-      pi = cneg_mul(l[j], pi);
-      y[j] = cmul(cfma(pi, Cin, y[j]), ib[j]);
+      const int col = r0l + j;
+      const Cplx zf = tile[f * HC + (col % HC)], zm = tile[fm * HC + (col % HC)];
+      if (col < HC) y[j] = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};   // (Z_f + conj Z_-f)/2
+      else y[j] = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};            // (Z_f - conj Z_-f)/(2i)
     }
-  }
-  // backward, lane local: xl_j = z_j - l_{j+1} xl_{j+1}
-  Cplx lnext;
-  {
-    const int r = r0 + MR - 1;
-    double E = 0.0;
-    if (r + 1 < nx) E = a.dT * ee[r];
-    lnext = {E * ib[MR - 1].re, E * ib[MR - 1].im};
-  }
-  Cplx S = {1.0, 0.0};
+    // l_r = dT off_{r-1} / beta_{r-1}
+    Cplx l[MR];
 #pragma unroll
-  for (int j = MR - 1; j >= 0; --j) {
-    const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
-    if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
-    S = cneg_mul(ln, S);
-  }
-  Cplx T = y[0];
-#pragma unroll
-  for (int d = 1; d < CL_LANES; d <<= 1) {
-    const Cplx So = shfl_down_c(S, d), To = shfl_down_c(T, d);
-    if (k + d < CL_LANES) {
-      T = cfma(S, To, T);
-      S = cmul(S, So);
+    for (int j = 0; j < MR; ++j) {
+      const double E = offs[r0l + j];  // couples rows r0+j-1 and r0+j
+      const Cplx ip = (j == 0) ? ibprev : ib[j - 1];
+      l[j] = {E * ip.re, E * ip.im};
     }
-  }
-  Cplx Se = shfl_down_c(S, 1), Te = shfl_down_c(T, 1);
-  if (k == CL_LANES - 1) {
-    Se = {1.0, 0.0};
-    Te = {0.0, 0.0};
-  }
-  if (valid && k == 0) {
-    bwd[2 * f] = S;
-    bwd[2 * f + 1] = T;
-  }
-  cluster.sync();
-  Cplx Xc = {0.0, 0.0};
-  for (int q = CL - 1; q > c; --q) {
-    const Cplx* rb = cluster.map_shared_rank(bwd, q);
-    Xc = cfma(rb[2 * f], Xc, rb[2 * f + 1]);
-  }
-  const Cplx Xin = cfma(Se, Xc, Te);
-  {
-    Cplx sg = {1.0, 0.0};
+    Cplx A = {1.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      if (j > 0) y[j] = cfma({-l[j].re, -l[j].im}, y[j - 1], y[j]);
+      A = cneg_mul(l[j], A);
+    }
+    Cplx B = y[MR - 1];
+#pragma unroll
+    for (int d = 1; d < CL_LANES; d <<= 1) {
+      const Cplx Ao = shfl_up_c(A, d), Bo = shfl_up_c(B, d);
+      if (k >= d) {
+        B = cfma(A, Bo, B);
+        A = cmul(A, Ao);
+      }
+    }
+    Cplx Ae = shfl_up_c(A, 1), Be = shfl_up_c(B, 1);
+    if (k == 0) {
+      Ae = {1.0, 0.0};
+      Be = {0.0, 0.0};
+    }
+    if (valid && k == CL_LANES - 1) {
+      fwd[2 * f] = A;
+      fwd[2 * f + 1] = B;
+    }
+    cluster.sync();
+    Cplx Yc = {0.0, 0.0};
+    for (int q = 0; q < c; ++q) {
+      const Cplx* rf = cluster.map_shared_rank(fwd, q);
+      Yc = cfma(rf[2 * f], Yc, rf[2 * f + 1]);
+    }
+    const Cplx Cin = cfma(Ae, Yc, Be);
+    {
+      Cplx pi = {1.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        pi = cneg_mul(l[j], pi);
+        y[j] = cmul(cfma(pi, Cin, y[j]), ib[j]);
+      }
+    }
+    const double En = offs[r0l + MR];  // couples the lane's last row and the next
+    const Cplx lnext = {En * ib[MR - 1].re, En * ib[MR - 1].im};
+    Cplx S = {1.0, 0.0};
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
       const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
-      sg = cneg_mul(ln, sg);
-      y[j] = cfma(sg, Xin, y[j]);
+      if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
+      S = cneg_mul(ln, S);
     }
-  }
-  // ---- phase 3: Hermitian completion, inverse FFT, update ----------------
-  if (valid) {
-    const int pf = log2N > 0 ? (int)(__brev((unsigned)f) >> (32 - log2N)) : 0;
-    const int nf = N - f;
-    const int pn = (f > 0 && nf > f) ? (int)(__brev((unsigned)nf) >> (32 - log2N)) : -1;
+    Cplx T = y[0];
+#pragma unroll
+    for (int d = 1; d < CL_LANES; d <<= 1) {
+      const Cplx So = shfl_down_c(S, d), To = shfl_down_c(T, d);
+      if (k + d < CL_LANES) {
+        T = cfma(S, To, T);
+        S = cmul(S, So);
+      }
+    }
+    Cplx Se = shfl_down_c(S, 1), Te = shfl_down_c(T, 1);
+    if (k == CL_LANES - 1) {
+      Se = {1.0, 0.0};
+      Te = {0.0, 0.0};
+    }
+    if (valid && k == 0) {
+      bwd[2 * f] = S;
+      bwd[2 * f + 1] = T;
+    }
+    cluster.sync();  // also: every thread has read this pass's inputs from the tile
+    Cplx Xc = {0.0, 0.0};
+    for (int q = CL - 1; q > c; --q) {
+      const Cplx* rb = cluster.map_shared_rank(bwd, q);
+      Xc = cfma(rb[2 * f], Xc, rb[2 * f + 1]);
+    }
+    const Cplx Xin = cfma(Se, Xc, Te);
+    {
+      Cplx sg = {1.0, 0.0};
+#pragma unroll
+      for (int j = MR - 1; j >= 0; --j) {
+        const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
+        sg = cneg_mul(ln, sg);
+        y[j] = cfma(sg, Xin, y[j]);
+      }
+    }
+    // pack W_f = q(col) + i q(col + HC): lanes k < 4 hold the first half rows
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
-      tile[pf * RB + k * MR + j] = y[j];
-      if (pn >= 0) tile[pn * RB + k * MR + j] = {y[j].re, -y[j].im};
+      const Cplx qb = shfl_xor_c(y[j], CL_LANES / 2);
+      if (valid && k < CL_LANES / 2) {
+        const int col = r0l + j;
+        tile[f * HC + col] = {y[j].re - qb.im, y[j].im + qb.re};
+        if (f > 0 && 2 * f < N) tile[(N - f) * HC + col] = {y[j].re + qb.im, qb.re - y[j].im};
+      }
     }
   }
   __syncthreads();
-  fft_tile_nt(tile, tw, N, RB, true);
-  double incmax = 0.0, immax = 0.0;
-  for (int idx = tid; idx < N * RB; idx += blockDim.x) {
-    const int n = idx / RB, col = idx - n * RB, row = row0 + col;
+  ifft_dif<LOGN, HC>(tile, tw);
+  // ---- update ----------------------------------------------------------------
+  const double rsN = 1.0 / sqrt((double)N);
+  double incmax = 0.0;
+  for (int e = tid; e < N * RB; e += blockDim.x) {
+    const int n = e / RB, col = e % RB, row = row0 + col;
     if (row >= nx) continue;
-    const Cplx v = tile[n * RB + col];
-    const double isc = a.inv_scaling[n];
-    const double u = (v.re * rsN) * isc;
-    const double ui = (v.im * rsN) * isc;
+    const Cplx z = tile[brev<LOGN>(n) * HC + (col % HC)];
+    const double u = ((col < HC ? z.re : z.im) * rsN) * a.inv_scaling[n];
     const size_t g = sb + (size_t)n * nx + row;
     if (a.Uout) {
-      if (a.U) incmax = nanmax(incmax, fabs(u - a.U[g]));
+      if (a.U) incmax = nanmax(incmax, fabs(u - uold[n * RB + col]));
       a.Uout[g] = u;
     } else {
-      incmax = nanmax(incmax, fabs(u - a.U[g]));
+      incmax = nanmax(incmax, fabs(u - uold[n * RB + col]));
       a.U[g] = u;
     }
-    immax = nanmax(immax, fabs(ui));
   }
-  // block then cluster reductions
   incmax = warp_max(incmax);
-  immax = warp_max(immax);
   const int lane = tid & 31, w = tid >> 5, nw = (blockDim.x + 31) >> 5;
   if (lane == 0) red[w] = incmax;
   __syncthreads();
   if (tid == 0) {
     double r1 = 0.0;
     for (int i = 0; i < nw; ++i) r1 = nanmax(r1, red[i]);
-    red[32] = r1;
-  }
-  __syncthreads();
-  if (lane == 0) red[w] = immax;
-  __syncthreads();
-  if (tid == 0) {
-    double r2 = 0.0;
-    for (int i = 0; i < nw; ++i) r2 = nanmax(r2, red[i]);
-    red[33] = r2;
+    red[8] = r1;
   }
   cluster.sync();
   if (c == 0 && tid == 0) {
-    double inc = red[32], im = red[33];
-    for (int q = 1; q < CL; ++q) {
-      const double* rr = cluster.map_shared_rank(red, q);
-      inc = nanmax(inc, rr[32]);
-      im = nanmax(im, rr[33]);
-    }
+    double inc = red[8];
+    for (int q = 1; q < CL; ++q) inc = nanmax(inc, cluster.map_shared_rank(red, q)[8]);
     if (a.inc) a.inc[s] = inc;
     if (a.inc_hist) a.inc_hist[(size_t)s * a.max_iters + (a.k - 1)] = inc;
-    if (a.imag) a.imag[s] = nanmax(a.imag[s], im);
     if (a.status) {
       int st = KLE_SAMPLE_ACTIVE;
       if (inc <= a.tol) st = KLE_SAMPLE_CONVERGED;
@@ -323,20 +375,23 @@ __global__ void __launch_bounds__(576, 1) cgc_cluster_kernel(CgcArgs a, const do
 }
 
 // ---------------------------------------------------------------------------
-static bool cluster_shape(int N, int nx, int* MR, int* CL) {
-  if (N < 2 || N > 64 || (N & (N - 1))) return false;  // <= 33 systems x 16 lanes <= 576 threads
-  int mr = (nx <= 128 || nx > 512) ? 8 : 4;
+static bool cluster_shape(int N, int nx, int* MR, int* CL, int* LOGN) {
+  if (N < 2 || N > 64 || (N & (N - 1))) return false;
+  int logn = 0;
+  while ((1 << logn) < N) ++logn;
+  const int mr = 8;
   const int rb = CL_LANES * mr;
   const int cl = (nx + rb - 1) / rb;
-  if (cl > 8) return false;
+  if (cl > 16) return false;
   *MR = mr;
   *CL = cl;
+  *LOGN = logn;
   return true;
 }
 
 bool cgc_cluster_supported(int N, int nx) {
-  int mr, cl;
-  return cluster_shape(N, nx, &mr, &cl);
+  int mr, cl, ln;
+  return cluster_shape(N, nx, &mr, &cl, &ln);
 }
 
 size_t shift_factor_doubles(int M, int N, int nx) { return 2 * (size_t)M * (N / 2 + 1) * nx; }
@@ -350,15 +405,19 @@ int shift_factor(const double* dia, const double* off, const double* lam, int M,
   return check_launch("shift_factor_kernel");
 }
 
-template <int MR>
-static int launch_cluster(const CgcArgs& a, const double* sfac, int CL, int log2N, cudaStream_t st) {
-  constexpr int RB = CL_LANES * MR;
-  const int NF = a.N / 2 + 1;
-  const int nt = ((NF * CL_LANES + 31) / 32) * 32;
-  const size_t smem = ((size_t)a.N * RB + a.N + 4 * NF) * sizeof(Cplx) + 34 * sizeof(double);
+template <int LOGN, int MR>
+static int launch_cluster(const CgcArgs& a, const double* sfac, int CL, cudaStream_t st) {
+  constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
+  constexpr int NPASS = (NF + CL_FPASS - 1) / CL_FPASS;
+  constexpr int FP = (NF + NPASS - 1) / NPASS;
+  const int nt = ((FP * CL_LANES + 31) / 32) * 32;
+  const size_t smem = (size_t)N * HC * sizeof(Cplx) + (size_t)N * RB * sizeof(double) + (RB + 2) * sizeof(double) +
+                      (N / 2 + 4 * NF) * sizeof(Cplx) + 10 * sizeof(double);
+  auto kern = cgc_cluster_kernel<LOGN, MR>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(cgc_cluster_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -373,18 +432,31 @@ static int launch_cluster(const CgcArgs& a, const double* sfac, int CL, int log2
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, cgc_cluster_kernel<MR>, a, sfac, log2N);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, sfac);
   if (e != cudaSuccess) return set_error(KLE_ERR_CUDA, cudaGetErrorString(e));
   return check_launch("cgc_cluster_kernel");
 }
 
+template <int MR>
+static int dispatch_logn(int logn, const CgcArgs& a, const double* sfac, int CL, cudaStream_t st) {
+  switch (logn) {
+    case 1: return launch_cluster<1, MR>(a, sfac, CL, st);
+    case 2: return launch_cluster<2, MR>(a, sfac, CL, st);
+    case 3: return launch_cluster<3, MR>(a, sfac, CL, st);
+    case 4: return launch_cluster<4, MR>(a, sfac, CL, st);
+    case 5: return launch_cluster<5, MR>(a, sfac, CL, st);
+    case 6: return launch_cluster<6, MR>(a, sfac, CL, st);
+  }
+  return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: N");
+}
+
 int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st) {
-  int MR, CL;
-  if (!cluster_shape(a.N, a.nx, &MR, &CL)) return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: shape");
+  int MR, CL, LOGN;
+  if (!cluster_shape(a.N, a.nx, &MR, &CL, &LOGN)) return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: shape");
   if (a.M <= 0) return KLE_OK;
-  int log2N = 0;
-  while ((1 << log2N) < a.N) ++log2N;
-  return MR == 4 ? launch_cluster<4>(a, sfac, CL, log2N, st) : launch_cluster<8>(a, sfac, CL, log2N, st);
+  if (a.imag) cudaMemsetAsync(a.imag, 0, sizeof(double) * a.M, st);  // real by construction
+  (void)MR;
+  return dispatch_logn<8>(LOGN, a, sfac, CL, st);
 }
 
 }  // namespace kle
