@@ -84,74 +84,130 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
 // Fused F + rhs kernel. CTA = (sample, group of subintervals); samples on
 // grid.x (grid.y is limited to 65535).
 // ---------------------------------------------------------------------------
-template <int MR, int P, int R, int NT>
-__global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
+// shared-memory staging of the fused kernel: start rows (which are also the
+// "prev" rows of the rhs for n >= 1), alpha-twisted prev row of n = 0, and
+// the operator diagonals, all fetched with cp.async before the sweep.
+template <int MR, int P, int NC>
+struct FgrSmem {
+  static constexpr int NXP = MR * P;
+  static constexpr size_t BYTES = ((size_t)(NC + 3) * NXP + 8) * sizeof(double);
+};
+
+template <int MR, int P, int R, int NT, bool PIPE>
+__global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs a) {
   using L = FineLayout<MR, P>;
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;  // subintervals per CTA
+  constexpr int NXP = MR * P;
   const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
   const int nx = a.nx, N = a.N;
   const size_t sbase = (size_t)s * N * nx;
+  const int n0 = blockIdx.y * NC;
 
-  int nr[R];
+  int nl[R];  // local subinterval index within the CTA
 #pragma unroll
-  for (int r = 0; r < R; ++r) nr[r] = blockIdx.y * NC + (w * SLOTS + slot) * R + r;
+  for (int r = 0; r < R; ++r) nl[r] = (w * SLOTS + slot) * R + r;
 
   double x[R][MR];
   if (a.F_given == nullptr) {
+    extern __shared__ __align__(16) double sm[];
+    double* st = sm;               // [NC][NXP]
+    double* p0 = st + NC * NXP;    // [NXP]
+    double* dd = p0 + NXP;         // [NXP]
+    double* ee = dd + NXP;         // [NXP + 1]: ee[i] couples rows i-1 and i
+    for (int e = tid; e < NC * nx; e += NT) {
+      const int ln = e / nx, row = e - ln * nx, n = n0 + ln;
+      if (n < N) cp_async8(st + ln * NXP + row, (n == 0) ? a.u0 + row : a.U + sbase + (size_t)(n - 1) * nx + row);
+    }
+    if (n0 == 0)
+      for (int row = tid; row < nx; row += NT) cp_async8(p0 + row, a.U + sbase + (size_t)(N - 1) * nx + row);
+    for (int row = tid; row < nx; row += NT) {
+      cp_async8(dd + row, a.dia + (size_t)s * nx + row);
+      if (row + 1 < nx) cp_async8(ee + row + 1, a.off + (size_t)s * nx + row);
+    }
+    if (tid == 0) {
+      ee[0] = 0.0;
+      ee[nx] = 0.0;
+    }
     LaneFactors<MR, P> fac;
     fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    __syncthreads();
     const double hg = a.dt * a.g0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
         const int row = k * MR + j;
-        double v = 0.0;
-        if (row < nx && nr[r] < N) {
-          const double st = (nr[r] == 0) ? a.u0[row] : a.U[sbase + (size_t)(nr[r] - 1) * nx + row];
-          v = st + hg;
-        }
-        x[r][j] = v;
+        x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * NXP + row] + hg : 0.0;
       }
-    }
-    be_steps<MR, P, R>(x, fac, k, a.J, hg);
+    if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
+    else be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int j = 0; j < MR; ++j) x[r][j] = (k * MR + j < nx) ? x[r][j] - hg : 0.0;
-  } else {
+    if (a.F_out) {
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < MR; ++j) {
+          const int row = k * MR + j;
+          if (row < nx && n0 + nl[r] < N) a.F_out[sbase + (size_t)(n0 + nl[r]) * nx + row] = x[r][j];
+        }
+    }
+    // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n), operands from shared memory
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double left = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
+      const double right = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
+      const int n = n0 + nl[r];
+      if (n >= N) continue;
+      const double sc = a.scaling[n];
+      const double* pv = (n == 0) ? p0 : st + nl[r] * NXP;
+      const double pmul = (n == 0) ? a.alpha : 1.0;
+      double* out = a.Rout + sbase + (size_t)n * nx;
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
         const int row = k * MR + j;
-        x[r][j] = (row < nx && nr[r] < N) ? a.F_given[sbase + (size_t)nr[r] * nx + row] : 0.0;
+        if (row >= nx) continue;
+        const double xm = (j > 0) ? x[r][j - 1] : (k > 0 ? left : 0.0);
+        const double xp = (j < MR - 1) ? x[r][j + 1] : (k < P - 1 ? right : 0.0);
+        const double Ax = fma(ee[row], xm, fma(dd[row], x[r][j], ee[row + 1] * xp));
+        const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[row];
+        out[row] = sc * rhs;
       }
+    }
+    return;
   }
-  if (a.F_out) {
+  // ---- F given (stand-alone cgc_correct): no sweep ----------------------------
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int j = 0; j < MR; ++j) {
-        const int row = k * MR + j;
-        if (row < nx && nr[r] < N) a.F_out[sbase + (size_t)nr[r] * nx + row] = x[r][j];
-      }
-  }
-  // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n)
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      const int n = n0 + nl[r];
+      x[r][j] = (row < nx && n < N) ? a.F_given[sbase + (size_t)n * nx + row] : 0.0;
+    }
   const double* dd = a.dia + (size_t)s * nx;
   const double* ee = a.off + (size_t)s * nx;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const double left = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
     const double right = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
-    if (nr[r] >= N) continue;
-    const double sc = a.scaling[nr[r]];
-    const size_t prow = (nr[r] == 0) ? sbase + (size_t)(N - 1) * nx : sbase + (size_t)(nr[r] - 1) * nx;
-    const double pmul = (nr[r] == 0) ? a.alpha : 1.0;
+    const int n = n0 + nl[r];
+    if (n >= N) continue;
+    const double sc = a.scaling[n];
+    const size_t prow = (n == 0) ? sbase + (size_t)(N - 1) * nx : sbase + (size_t)(n - 1) * nx;
+    const double pmul = (n == 0) ? a.alpha : 1.0;
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
       const int row = k * MR + j;
@@ -161,9 +217,8 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
       const double em = (row > 0) ? ee[row - 1] : 0.0;
       const double ep = (row < nx - 1) ? ee[row] : 0.0;
       const double Ax = fma(em, xm, fma(dd[row], x[r][j], ep * xp));
-      const double prev = pmul * a.U[prow + row];
-      const double rhs = fma(a.dT, Ax, x[r][j]) - prev;
-      a.Rout[sbase + (size_t)nr[r] * nx + row] = sc * rhs;
+      const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * a.U[prow + row];
+      a.Rout[sbase + (size_t)n * nx + row] = sc * rhs;
     }
   }
 }
@@ -174,7 +229,7 @@ __global__ void __launch_bounds__(NT) fgr_kernel(FgrArgs a) {
 // propagate_fine / propagate_coarse (J=1, coarse blob); q = 1, nseg = N gives
 // fine_reference / coarse_sweep_init.
 // ---------------------------------------------------------------------------
-template <int MR, int P, int R, int NT>
+template <int MR, int P, int R, int NT, bool PIPE>
 __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
   using L = FineLayout<MR, P>;
   constexpr int SLOTS = 32 / P;
@@ -198,7 +253,8 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
       x[r][j] = (row < nx && q[r] < Q) ? a.start[((size_t)s * Q + q[r]) * nx + row] + hg : 0.0;
     }
   for (int g = 0; g < a.nseg; ++g) {
-    be_steps<MR, P, R>(x, fac, k, a.J, hg);
+    if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
+    else be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (q[r] >= Q) continue;
@@ -215,7 +271,7 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
 // ---------------------------------------------------------------------------
 // host-side dispatch
 // ---------------------------------------------------------------------------
-template <int MR, int P, int R_>
+template <int MR, int P, int R_, bool PIPE = false>
 struct FineInst {
   static constexpr int R = R_;
   static constexpr int NT = 128;
@@ -228,12 +284,18 @@ struct FineInst {
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {
     dim3 grid(a.M, (a.N + NC - 1) / NC);
-    fgr_kernel<MR, P, R, NT><<<grid, NT, 0, st>>>(a);
+    const size_t smem = a.F_given ? 0 : FgrSmem<MR, P, NC>::BYTES;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    fgr_kernel<MR, P, R, NT, PIPE><<<grid, NT, smem, st>>>(a);
     return check_launch("fgr_kernel");
   }
   static int sweep(const SweepArgs& a, cudaStream_t st) {
     dim3 grid(a.M, (a.Q + NC - 1) / NC);
-    sweep_kernel<MR, P, R, NT><<<grid, NT, 0, st>>>(a);
+    sweep_kernel<MR, P, R, NT, PIPE><<<grid, NT, 0, st>>>(a);
     return check_launch("sweep_kernel");
   }
 };
@@ -241,35 +303,38 @@ struct FineInst {
 // (MR, P, R) variants; the first entry whose MR*P covers nx is the default,
 // KLE_FINE_VARIANT=<index> forces one (for tuning; blobs depend on MR, P).
 struct FineVariant {
-  int MR, P, R;
+  int MR, P, R, pipe;
 };
 static const FineVariant kVariants[] = {
-    {1, 16, 4},  {2, 16, 4},  {4, 16, 4},  {8, 16, 4},  {16, 32, 4}, {32, 32, 2},  // defaults by size
-    {8, 16, 2},  {4, 32, 4},  {4, 32, 8},  {8, 16, 8},  {16, 16, 2}, {8, 32, 4},   // alternatives
-    {32, 16, 2}, {16, 32, 2}, {16, 32, 3}, {8, 32, 8},
+    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {8, 16, 2, 0},  {16, 32, 3, 0}, {32, 32, 2, 0},  // defaults
+    {8, 16, 2, 1},  {4, 32, 4, 0},  {8, 16, 4, 1},  {8, 16, 4, 0},  {16, 16, 2, 0}, {8, 32, 4, 0},
+    {32, 16, 2, 0}, {16, 32, 2, 0}, {16, 32, 2, 1}, {16, 32, 4, 1}, {16, 32, 4, 0}, {4, 32, 4, 1},
 };
 static const int kNumDefaults = 6;
 
-#define KLE_FINE_DISPATCH(MR_, P_, R_, CALL) \
-  if (lay.MR == MR_ && lay.P == P_ && lay.R == R_) return FineInst<MR_, P_, R_>::CALL;
+#define KLE_FINE_DISPATCH(MR_, P_, R_, PI_, CALL) \
+  if (lay.MR == MR_ && lay.P == P_ && lay.R == R_ && lay.pipe == PI_) return FineInst<MR_, P_, R_, PI_>::CALL;
 
-#define KLE_FINE_ALL(CALL)             \
-  KLE_FINE_DISPATCH(1, 16, 4, CALL)    \
-  KLE_FINE_DISPATCH(2, 16, 4, CALL)    \
-  KLE_FINE_DISPATCH(4, 16, 4, CALL)    \
-  KLE_FINE_DISPATCH(8, 16, 4, CALL)    \
-  KLE_FINE_DISPATCH(16, 32, 4, CALL)   \
-  KLE_FINE_DISPATCH(32, 32, 2, CALL)   \
-  KLE_FINE_DISPATCH(8, 16, 2, CALL)    \
-  KLE_FINE_DISPATCH(4, 32, 4, CALL)    \
-  KLE_FINE_DISPATCH(4, 32, 8, CALL)    \
-  KLE_FINE_DISPATCH(8, 16, 8, CALL)    \
-  KLE_FINE_DISPATCH(16, 16, 2, CALL)   \
-  KLE_FINE_DISPATCH(8, 32, 4, CALL)    \
-  KLE_FINE_DISPATCH(32, 16, 2, CALL)   \
-  KLE_FINE_DISPATCH(16, 32, 2, CALL)   \
-  KLE_FINE_DISPATCH(16, 32, 3, CALL)   \
-  KLE_FINE_DISPATCH(8, 32, 8, CALL)
+#define KLE_FINE_ALL(CALL)                \
+  KLE_FINE_DISPATCH(1, 16, 4, 0, CALL)    \
+  KLE_FINE_DISPATCH(2, 16, 4, 0, CALL)    \
+  KLE_FINE_DISPATCH(4, 16, 4, 0, CALL)    \
+  KLE_FINE_DISPATCH(8, 16, 2, 0, CALL)    \
+  KLE_FINE_DISPATCH(16, 32, 3, 0, CALL)   \
+  KLE_FINE_DISPATCH(32, 32, 2, 0, CALL)   \
+  KLE_FINE_DISPATCH(8, 16, 2, 1, CALL)    \
+  KLE_FINE_DISPATCH(16, 32, 2, 1, CALL)   \
+  KLE_FINE_DISPATCH(4, 32, 4, 0, CALL)    \
+  KLE_FINE_DISPATCH(8, 16, 4, 1, CALL)    \
+  KLE_FINE_DISPATCH(8, 16, 4, 0, CALL)    \
+  KLE_FINE_DISPATCH(16, 16, 2, 0, CALL)   \
+  KLE_FINE_DISPATCH(8, 32, 4, 0, CALL)    \
+  KLE_FINE_DISPATCH(32, 16, 2, 0, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 2, 0, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 3, 0, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 4, 1, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 4, 0, CALL)   \
+  KLE_FINE_DISPATCH(4, 32, 4, 1, CALL)
 
 FineLayoutRT fine_layout(int nx) {
   const char* env = getenv("KLE_FINE_VARIANT");
@@ -278,14 +343,14 @@ FineLayoutRT fine_layout(int nx) {
     const int nv = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
     if (v >= 0 && v < nv && kVariants[v].MR * kVariants[v].P >= nx) {
       const FineVariant& f = kVariants[v];
-      return {f.MR, f.P, f.R, fine_blob_doubles(f.MR, f.P)};
+      return {f.MR, f.P, f.R, f.pipe, fine_blob_doubles(f.MR, f.P)};
     }
   }
   for (int i = 0; i < kNumDefaults; ++i) {
     const FineVariant& f = kVariants[i];
-    if (f.MR * f.P >= nx) return {f.MR, f.P, f.R, fine_blob_doubles(f.MR, f.P)};
+    if (f.MR * f.P >= nx) return {f.MR, f.P, f.R, f.pipe, fine_blob_doubles(f.MR, f.P)};
   }
-  return {0, 0, 0, 0};
+  return {0, 0, 0, 0, 0};
 }
 
 int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,

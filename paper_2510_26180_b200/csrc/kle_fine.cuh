@@ -130,4 +130,135 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
   }
 }
 
+// ---------------------------------------------------------------------------
+// Software-pipelined variant: the R right-hand sides form two groups A and B
+// (RG each) running half a step apart, so that every phase pairs one group's
+// latency-bound carry scan with the other group's row recurrence:
+//   S1 forward recurrence   S2 forward scan + stitch
+//   S3 backward recurrence  S4 backward scan + stitch
+//   schedule: B.S1 B.S2 | (A.S1,B.S3) (A.S2,B.S4) (A.S3,B.S1) (A.S4,B.S2) | ...
+// Same arithmetic per right-hand side as be_steps.
+template <int MR, int P, int RG>
+struct PipeGroup {
+  double x[RG][MR];
+  double Y[RG], X[RG];
+};
+
+template <int MR, int P, int RG>
+__device__ __forceinline__ void ph_s1(PipeGroup<MR, P, RG>& g, const LaneFactors<MR, P>& f) {
+#pragma unroll
+  for (int j = 1; j < MR; ++j)
+#pragma unroll
+    for (int r = 0; r < RG; ++r) g.x[r][j] = fma(-f.l[j], g.x[r][j - 1], g.x[r][j]);
+}
+
+template <int MR, int P, int RG>
+__device__ __forceinline__ void ph_s2(PipeGroup<MR, P, RG>& g, const LaneFactors<MR, P>& f, int k) {
+  using L = FineLayout<MR, P>;
+#pragma unroll
+  for (int r = 0; r < RG; ++r) g.Y[r] = g.x[r][MR - 1];
+#pragma unroll
+  for (int t = 0; t < L::LOGP; ++t)
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      const double o = __shfl_up_sync(KLE_FULL_MASK, g.Y[r], 1 << t, P);
+      if (k >= (1 << t)) g.Y[r] = fma(f.af[t], o, g.Y[r]);
+    }
+#pragma unroll
+  for (int r = 0; r < RG; ++r) {
+    const double o = __shfl_up_sync(KLE_FULL_MASK, g.Y[r], 1, P);
+    g.Y[r] = (k == 0) ? 0.0 : o;
+  }
+  double pi = 1.0;
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    pi *= -f.l[j];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) g.x[r][j] = fma(pi, g.Y[r], g.x[r][j]);
+  }
+}
+
+template <int MR, int P, int RG>
+__device__ __forceinline__ void ph_s3(PipeGroup<MR, P, RG>& g, const LaneFactors<MR, P>& f, double hg) {
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+    const double kap = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      double z = fma(g.x[r][j], f.inv[j], kap);
+      if (j + 1 < MR) z = fma(-ln, g.x[r][j + 1], z);
+      g.x[r][j] = z;
+    }
+  }
+}
+
+template <int MR, int P, int RG>
+__device__ __forceinline__ void ph_s4(PipeGroup<MR, P, RG>& g, const LaneFactors<MR, P>& f, int k) {
+  using L = FineLayout<MR, P>;
+#pragma unroll
+  for (int r = 0; r < RG; ++r) g.X[r] = g.x[r][0];
+#pragma unroll
+  for (int t = 0; t < L::LOGP; ++t)
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      const double o = __shfl_down_sync(KLE_FULL_MASK, g.X[r], 1 << t, P);
+      if (k + (1 << t) < P) g.X[r] = fma(f.bb[t], o, g.X[r]);
+    }
+#pragma unroll
+  for (int r = 0; r < RG; ++r) {
+    const double o = __shfl_down_sync(KLE_FULL_MASK, g.X[r], 1, P);
+    g.X[r] = (k == P - 1) ? 0.0 : o;
+  }
+  double sg = 1.0;
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    sg *= -((j + 1 < MR) ? f.l[j + 1] : f.lnx);
+#pragma unroll
+    for (int r = 0; r < RG; ++r) g.x[r][j] = fma(sg, g.X[r], g.x[r][j]);
+  }
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void be_steps_pipe(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, int J,
+                                              double hg) {
+  static_assert(R % 2 == 0, "pipelined solve needs an even number of right-hand sides");
+  constexpr int RG = R / 2;
+  PipeGroup<MR, P, RG> A, B;
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      A.x[r][j] = x[r][j];
+      B.x[r][j] = x[RG + r][j];
+    }
+  if (J > 0) {
+    ph_s1(B, f);
+    ph_s2(B, f, k);
+    for (int it = 0; it < J - 1; ++it) {
+      ph_s1(A, f);
+      ph_s3(B, f, hg);
+      ph_s2(A, f, k);
+      ph_s4(B, f, k);
+      ph_s3(A, f, hg);
+      ph_s1(B, f);
+      ph_s4(A, f, k);
+      ph_s2(B, f, k);
+    }
+    ph_s1(A, f);
+    ph_s3(B, f, hg);
+    ph_s2(A, f, k);
+    ph_s4(B, f, k);
+    ph_s3(A, f, hg);
+    ph_s4(A, f, k);
+  }
+#pragma unroll
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      x[r][j] = A.x[r][j];
+      x[RG + r][j] = B.x[r][j];
+    }
+}
+
 }  // namespace kle

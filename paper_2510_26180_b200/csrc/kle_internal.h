@@ -11,7 +11,7 @@ int set_error(int code, const char* msg);
 int check_launch(const char* what);
 
 struct FineLayoutRT {
-  int MR, P, R, doubles;
+  int MR, P, R, pipe, doubles;
 };
 FineLayoutRT fine_layout(int nx);
 
