@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU work of the baseline sample")
     return p.parse_args()
@@ -487,9 +487,80 @@ def _cpu_build_surrogate(model, grid, cfg, train, degree, cores):
     return KLGpcSurrogate(mean, lam, modes, coeffs, degree, [ParameterMap("identity", -np.inf, np.inf)] * len(train[0]))
 
 
+def run_c5(args):
+    """BASELINE configs[4]: diagonalised-CGC stress. nx = 4095, N = 1024, J = 8,
+    alpha in {1e-1, 1e-2, 1e-4}, 4096 samples (coarse-sweep initial guess),
+    processed in sample chunks (one state copy is 137 GB at M = 4096).
+    Reports iteration counts per alpha, end-to-end solves/s and the CGC
+    throughput (sample-iterations/s and compulsory GB/s of one CGC launch)."""
+    import torch
+
+    from paper_2510_26180_b200 import LogNormalKL1D, RngStream, SolverConfig, make_time_grid
+    from paper_2510_26180_b200 import _lib
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, empty, ptr, stream_ptr
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, pcgc_solve_device, shift_factors
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    nx, N, J, M, chunk = 4095, 1024, 8, int(os.environ.get("KLE_C5_M", "4096")), 256
+    model = LogNormalKL1D(nx=nx, d=4)
+    grid = make_time_grid(1.0, N, J)
+    _, eval_rng, _ = RngStream(SEED).split(3)
+    xi = eval_rng.normal(0.0, 1.0, size=(M, 4))
+    out = {"metric": "c5 CGC stress: iterations per alpha, CGC throughput", "config": {
+        "workload": "BASELINE configs[4]: nx=4095, N=1024, J=8, d=4, coarse-sweep init, tol=1e-8",
+        "samples": M, "chunk": chunk}, "alphas": {}}
+    for alpha in (1e-1, 1e-2, 1e-4):
+        cfg = SolverConfig(alpha=alpha, tol=1e-8, max_outer_iters=60, seed=SEED)
+        tables = AlphaTables(build_alpha_circulant(N, alpha))
+        iters = []
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for c0 in range(0, M, chunk):
+            op = DeviceOperator.from_model(model, xi[c0:c0 + chunk])
+            U = coarse_sweep_init_batched(op, grid).contiguous()
+            res = pcgc_solve_device(op, U, grid, cfg, tables)
+            iters.append(res.iters.cpu().numpy())
+            del U, res, op
+        ev1.record()
+        torch.cuda.synchronize()
+        wall_ms = ev0.elapsed_time(ev1)
+        it = np.concatenate(iters)
+        # one CGC launch on a full chunk (all samples active)
+        op = DeviceOperator.from_model(model, xi[:chunk])
+        U = coarse_sweep_init_batched(op, grid).contiguous()
+        R = empty(chunk, N, nx)
+        _lib.call("kle_fgr_f64", ptr(U), ptr(op.u0), None, None, ptr(R), ptr(op.blob(grid.deltat)), ptr(op.dia),
+                  ptr(op.off), ptr(tables.scaling), None, chunk, N, nx, J, grid.deltat, grid.deltaT, op.g0, alpha,
+                  stream_ptr())
+        sfac = shift_factors(op, tables, N, grid.deltaT)
+        nb = 0 if sfac is not None else int(_lib.query("kle_cgc_scratch_bytes", chunk, N, nx))
+        scratch = torch.empty(max(nb, 8), dtype=torch.uint8, device="cuda")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
+                  ptr(op.off), ptr(sfac), chunk, N, nx, grid.deltaT, 1, 1, -1.0, None, None, None, None, None,
+                  ptr(scratch), nb, stream_ptr())
+        b.record()
+        torch.cuda.synchronize()
+        cgc_ms = a.elapsed_time(b)
+        hist = {int(k): int(v) for k, v in zip(*np.unique(it, return_counts=True))}
+        out["alphas"][f"{alpha:g}"] = {
+            "iters_mean": float(it.mean()), "iters_hist": hist, "solves_per_s": M / (wall_ms * 1e-3),
+            "wall_s": wall_ms * 1e-3, "cgc_ms_per_launch": cgc_ms,
+            "cgc_sample_iterations_per_s": chunk / (cgc_ms * 1e-3),
+            "cgc_compulsory_gbs": 24.0 * chunk * N * nx / (cgc_ms * 1e-3) / 1e9,
+            "cgc_path": "cluster" if sfac is not None else "on-the-fly",
+        }
+        del U, R, op, scratch
+    print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    if a.config == "c5":
+        run_c5(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_b200(a)

@@ -47,7 +47,7 @@ const char* kle_last_error(void) { return g_err.c_str(); }
 
 int kle_fine_layout(int nx, int* MR, int* P, int* blob_doubles) {
   const FineLayoutRT l = fine_layout(nx);
-  if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "nx exceeds the largest supported fine layout (1024)");
+  if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "nx exceeds the largest supported fine layout (4096)");
   if (MR) *MR = l.MR;
   if (P) *P = l.P;
   if (blob_doubles) *blob_doubles = l.doubles;

@@ -350,21 +350,26 @@ FineLayoutRT fine_layout(int nx) {
     const FineVariant& f = kVariants[i];
     if (f.MR * f.P >= nx) return {f.MR, f.P, f.R, f.pipe, fine_blob_doubles(f.MR, f.P)};
   }
+  const int W = mw_warps(nx);
+  if (W) return {16, 32 * W, 1, 0, mw_blob_doubles(nx), W};
   return {0, 0, 0, 0, 0};
 }
 
 int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,
                 double h, double g0, cudaStream_t st) {
+  if (lay.W) return mw_factor(dia, off, blob, M, nx, h, st);
   KLE_FINE_ALL(factor(dia, off, blob, M, nx, h, g0, st))
   return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: unsupported nx");
 }
 
 int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
+  if (lay.W) return mw_fgr(a, st);
   KLE_FINE_ALL(fgr(a, st))
   return set_error(KLE_ERR_UNSUPPORTED, "fgr: unsupported nx");
 }
 
 int fine_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st) {
+  if (lay.W) return mw_sweep(a, st);
   KLE_FINE_ALL(sweep(a, st))
   return set_error(KLE_ERR_UNSUPPORTED, "sweep: unsupported nx");
 }

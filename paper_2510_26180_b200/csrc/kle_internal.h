@@ -12,6 +12,7 @@ int check_launch(const char* what);
 
 struct FineLayoutRT {
   int MR, P, R, pipe, doubles;
+  int W = 0;  // > 0: multi-warp system (kle_fine_mw.cu), P = 32 * W
 };
 FineLayoutRT fine_layout(int nx);
 
@@ -37,6 +38,12 @@ struct SweepArgs {
   int M, Q, nx, J, nseg;
   double h, g0;
 };
+
+int mw_warps(int nx);
+int mw_blob_doubles(int nx);
+int mw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, cudaStream_t st);
+int mw_fgr(const FgrArgs& a, cudaStream_t st);
+int mw_sweep(const SweepArgs& a, cudaStream_t st);
 
 int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,
                 double h, double g0, cudaStream_t st);

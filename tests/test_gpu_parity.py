@@ -337,3 +337,47 @@ def test_non_power_of_two_N_pcgc(cuda):
     out = batched.pcgc(dia, off, model.initial_condition(), init, 12, 10, 1.0, 1e-2, 1e-9, 60)
     np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
     assert rel(res.states.cpu().numpy(), out["states"]) <= RTOL
+
+
+@pytest.mark.parametrize("nx", [1500, 4095])
+def test_multiwarp_fine_solver_matches_oracle(cuda, nx):
+    """nx > 1024 uses the multi-warp layout (one CTA per system)."""
+    import torch
+    from paper_2510_26180_b200 import LogNormalKL1D
+    from paper_2510_26180_b200.device import DeviceOperator, to_dev
+
+    rng = np.random.default_rng(nx)
+    model = LogNormalKL1D(nx=nx, d=4)
+    xi = rng.normal(size=(2, 4))
+    op = DeviceOperator.from_model(model, xi)
+    assert op.layout[1] > 32  # multi-warp
+    starts = rng.normal(size=(2, 3, nx))
+    h, J = 1.0 / 1024 / 8, 8
+    got = op.sweep(to_dev(starts), h, J)[:, :, 0].cpu().numpy()
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    want = batched.be_steps(dia, off, starts, h, 1.0, J)
+    assert rel(got, want) <= 1e-12
+
+
+def test_c5_full_shape_alpha_1e4(cuda):
+    """Config 5 shape (nx = 4095, N = 1024, J = 8, alpha = 1e-4), one sample,
+    coarse-sweep initial guess: iteration count and fields vs the oracle."""
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    N, nx, alpha = 1024, 4095, 1e-4
+    model = LogNormalKL1D(nx=nx, d=4)
+    grid = make_time_grid(1.0, N, 8)
+    cfg = SolverConfig(alpha=alpha, tol=1e-8, max_outer_iters=60)
+    xi = np.random.default_rng(5).normal(size=(1, 4))
+    op = DeviceOperator.from_model(model, xi)
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    init = U.cpu().numpy()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    out = batched.pcgc(dia, off, model.initial_condition(), init, N, 8, 1.0, alpha, 1e-8, 60)
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
+    rtol = max(RTOL, 1e-12 * alpha ** (-(N - 1) / N))
+    assert rel(res.states.cpu().numpy(), out["states"]) <= rtol

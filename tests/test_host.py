@@ -51,6 +51,7 @@ def test_fine_layout_query():
     for nx in (1, 16, 127, 511, 1000):
         assert lib.kle_fine_layout(nx, ctypes.byref(MR), ctypes.byref(P), ctypes.byref(nd)) == 0
         assert MR.value * P.value >= nx
+    assert lib.kle_fine_layout(4095, ctypes.byref(MR), ctypes.byref(P), ctypes.byref(nd)) == 0 and P.value == 256
     assert lib.kle_fine_layout(5000, ctypes.byref(MR), ctypes.byref(P), ctypes.byref(nd)) != 0
     assert b"nx" in lib.kle_last_error()
 
