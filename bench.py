@@ -212,8 +212,8 @@ def run_b200(args):
     from paper_2510_26180_b200.pcgc import shift_factors
 
     sfac = shift_factors(op, tables, grid.n_coarse, grid.deltaT)
-    nbytes = 0 if sfac is not None else int(_lib.query("kle_cgc_scratch_bytes", M, grid.n_coarse, model.nx))
-    scratch = torch.empty(max(nbytes, 8), dtype=torch.uint8, device="cuda")
+    nbytes = 16 * M if sfac is not None else int(_lib.query("kle_cgc_scratch_bytes", M, grid.n_coarse, model.nx))
+    scratch = torch.zeros(max(nbytes, 8), dtype=torch.uint8, device="cuda")
 
     def cgc():
         _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
@@ -534,8 +534,8 @@ def run_c5(args):
                   ptr(op.off), ptr(tables.scaling), None, chunk, N, nx, J, grid.deltat, grid.deltaT, op.g0, alpha,
                   stream_ptr())
         sfac = shift_factors(op, tables, N, grid.deltaT)
-        nb = 0 if sfac is not None else int(_lib.query("kle_cgc_scratch_bytes", chunk, N, nx))
-        scratch = torch.empty(max(nb, 8), dtype=torch.uint8, device="cuda")
+        nb = 16 * chunk if sfac is not None else int(_lib.query("kle_cgc_scratch_bytes", chunk, N, nx))
+        scratch = torch.zeros(max(nb, 8), dtype=torch.uint8, device="cuda")
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),

@@ -93,7 +93,9 @@ int kle_fgr_f64(const double* U, const double* u0, const double* F_given, double
 
 size_t kle_cgc_scratch_bytes(int M, int N, int nx) {
   if (M <= 0 || N <= 0 || nx <= 0) return 0;
-  return (size_t)cgc_grid(M, N, nx) * cgc_scratch_doubles_per_cta(N, nx) * sizeof(double);
+  const size_t slab = (size_t)cgc_grid(M, N, nx) * cgc_scratch_doubles_per_cta(N, nx) * sizeof(double);
+  const size_t slots = (size_t)M * 2 * sizeof(unsigned long long);
+  return slab > slots ? slab : slots;
 }
 
 size_t kle_shift_factor_bytes(int M, int N, int nx) {
@@ -113,7 +115,7 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
                        double* u, double* imag, void* scratch, size_t scratch_bytes, void* stream) {
   if (M < 0 || N < 1 || nx < 1) return set_error(KLE_ERR_INVALID, "three_step: bad dims");
   if (M == 0) return KLE_OK;
-  if (!sfac && scratch_bytes < kle_cgc_scratch_bytes(M, N, nx))
+  if (scratch_bytes < (sfac ? (size_t)M * 16 : kle_cgc_scratch_bytes(M, N, nx)))
     return set_error(KLE_ERR_WORKSPACE, "three_step: scratch too small");
   if (imag) cudaMemsetAsync(imag, 0, sizeof(double) * M, KLE_STREAM(stream));
   CgcArgs a{};
@@ -135,7 +137,11 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
   a.max_iters = 1;
   a.dT = dT;
   a.tol = 0.0;
-  if (sfac) return cgc_cluster_run(a, sfac, KLE_STREAM(stream));
+  if (sfac) {
+    a.red_slots = static_cast<unsigned long long*>(scratch);
+    cudaMemsetAsync(scratch, 0, (size_t)M * 16, KLE_STREAM(stream));
+    return cgc_cluster_run(a, sfac, KLE_STREAM(stream));
+  }
   return cgc_run(a, KLE_STREAM(stream));
 }
 
@@ -146,7 +152,7 @@ int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, co
                        void* stream) {
   if (M < 0 || N < 1 || nx < 1 || k < 1 || max_iters < k) return set_error(KLE_ERR_INVALID, "cgc_update: bad arguments");
   if (M == 0) return KLE_OK;
-  if (!sfac && scratch_bytes < kle_cgc_scratch_bytes(M, N, nx))
+  if (scratch_bytes < (sfac ? (size_t)M * 16 : kle_cgc_scratch_bytes(M, N, nx)))
     return set_error(KLE_ERR_WORKSPACE, "cgc_update: scratch too small");
   CgcArgs a{};
   a.R = R;
@@ -169,12 +175,18 @@ int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, co
   a.max_iters = max_iters;
   a.dT = dT;
   a.tol = tol;
-  if (sfac) return cgc_cluster_run(a, sfac, KLE_STREAM(stream));
+  if (sfac) {
+    // the slots return to zero after every launch (last CTA resets the max; the
+    // ticket counts modulo the cluster size), so callers zero them once
+    a.red_slots = static_cast<unsigned long long*>(scratch);
+    return cgc_cluster_run(a, sfac, KLE_STREAM(stream));
+  }
   return cgc_run(a, KLE_STREAM(stream));
 }
 
 static size_t pcgc_scratch_part(int M, int N, int nx) {
-  return cgc_cluster_supported(N, nx) ? kle_shift_factor_bytes(M, N, nx) : kle_cgc_scratch_bytes(M, N, nx);
+  return cgc_cluster_supported(N, nx) ? align256(kle_shift_factor_bytes(M, N, nx)) + align256((size_t)M * 16)
+                                      : kle_cgc_scratch_bytes(M, N, nx);
 }
 
 size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
@@ -202,9 +214,15 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
   ws += align256(scratch_bytes);
   int32_t* counter = reinterpret_cast<int32_t*>(ws);
   double* sfac = clustered ? static_cast<double*>(scratch) : nullptr;
+  void* cgc_scratch = clustered ? static_cast<void*>(static_cast<char*>(scratch) + align256(kle_shift_factor_bytes(M, N, nx)))
+                                : scratch;
+  const size_t cgc_scratch_bytes = clustered ? (size_t)M * 16 : scratch_bytes;
 
   const double dT = T / N, dt = dT / J;
-  if (clustered) KLE_TRY(shift_factor(dia, off, lam, M, N, nx, dT, sfac, st));
+  if (clustered) {
+    KLE_TRY(shift_factor(dia, off, lam, M, N, nx, dT, sfac, st));
+    cudaMemsetAsync(cgc_scratch, 0, (size_t)M * 16, st);
+  }
   cudaMemsetAsync(status, 0, sizeof(int32_t) * M, st);
   cudaMemsetAsync(iters, 0, sizeof(int32_t) * M, st);
   if (inc_hist) cudaMemsetAsync(inc_hist, 0xFF, sizeof(double) * (size_t)M * max_iters, st);
@@ -216,7 +234,7 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
                         alpha, stream));
     cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
     KLE_TRY(kle_cgc_update_f64(R, U, inv_scaling, lam, dia, off, sfac, M, N, nx, dT, k, max_iters, tol, status,
-                               iters, inc_hist, imag, counter, scratch, scratch_bytes, stream));
+                               iters, inc_hist, imag, counter, cgc_scratch, cgc_scratch_bytes, stream));
     cudaMemcpyAsync(&h_count, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return set_error(KLE_ERR_CUDA, cudaGetErrorString(e));

@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
       }
     }
   }
+  asm volatile("barrier.cluster.arrive;\n" ::: "memory");
   __syncthreads();
   ifft_dif<LOGN, HC>(tile, tw);
   // ---- update ----------------------------------------------------------------
@@ -350,28 +351,35 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
   if (tid == 0) {
     double r1 = 0.0;
     for (int i = 0; i < nw; ++i) r1 = nanmax(r1, red[i]);
-    red[8] = r1;
-  }
-  cluster.sync();
-  if (c == 0 && tid == 0) {
-    double inc = red[8];
-    for (int q = 1; q < CL; ++q) inc = nanmax(inc, cluster.map_shared_rank(red, q)[8]);
-    if (a.inc) a.inc[s] = inc;
-    if (a.inc_hist) a.inc_hist[(size_t)s * a.max_iters + (a.k - 1)] = inc;
-    if (a.status) {
-      int st = KLE_SAMPLE_ACTIVE;
-      if (inc <= a.tol) st = KLE_SAMPLE_CONVERGED;
-      else if (!isfinite(inc)) st = KLE_SAMPLE_NONFINITE;
-      else if (a.k >= a.max_iters) st = KLE_SAMPLE_MAXITERS;
-      if (st != KLE_SAMPLE_ACTIVE) {
-        a.status[s] = st;
-        if (a.iters) a.iters[s] = a.k;
-      } else if (a.active_count) {
-        atomicAdd(a.active_count, 1);
+    // cluster-wide max through a global slot; the last CTA to arrive finishes
+    // the sample (no further cluster barrier needed). Non-negative doubles
+    // (and +NaN) order like their bit patterns.
+    unsigned long long* slot = a.red_slots + 2 * (size_t)s;
+    atomicMax(slot, (unsigned long long)__double_as_longlong(r1));
+    __threadfence();
+    const unsigned long long ticket = atomicAdd(slot + 1, 1ULL);
+    if ((ticket + 1) % (unsigned long long)CL == 0) {
+      __threadfence();
+      const double inc = __longlong_as_double((long long)atomicExch(slot, 0ULL));
+      if (a.inc) a.inc[s] = inc;
+      if (a.inc_hist) a.inc_hist[(size_t)s * a.max_iters + (a.k - 1)] = inc;
+      if (a.status) {
+        int st = KLE_SAMPLE_ACTIVE;
+        if (inc <= a.tol) st = KLE_SAMPLE_CONVERGED;
+        else if (!isfinite(inc)) st = KLE_SAMPLE_NONFINITE;
+        else if (a.k >= a.max_iters) st = KLE_SAMPLE_MAXITERS;
+        if (st != KLE_SAMPLE_ACTIVE) {
+          a.status[s] = st;
+          if (a.iters) a.iters[s] = a.k;
+        } else if (a.active_count) {
+          atomicAdd(a.active_count, 1);
+        }
       }
     }
   }
-  cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+  // every CTA arrived (after its last DSMEM read) before the update phase;
+  // wait here so no CTA's shared memory disappears under a remote reader
+  asm volatile("barrier.cluster.wait;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------

@@ -67,6 +67,7 @@ struct CgcArgs {
   double* inc_hist;         // optional [M][max_iters]
   double* imag;             // optional [M] running max imaginary residue
   int32_t* active_count;    // optional device counter of still-active samples
+  unsigned long long* red_slots;  // cluster path: [M][2] (max bits, arrival ticket), zero-initialised once
   int M, N, nx, k, max_iters;
   double dT, tol;
 };

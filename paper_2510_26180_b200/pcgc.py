@@ -94,7 +94,10 @@ def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: f
     imag = empty(M)
     if isinstance(sfac, str):
         sfac = shift_factors(op, tables, N, deltaT)
-    scratch, nbytes = (None, 0) if sfac is not None else _cgc_scratch(M, N, nx)
+    if sfac is not None:  # cluster path: per-sample reduction slots (zeroed by the call)
+        scratch, nbytes = torch.empty(16 * M, dtype=torch.uint8, device="cuda"), 16 * M
+    else:
+        scratch, nbytes = _cgc_scratch(M, N, nx)
     _lib.call("kle_three_step_f64", ptr(r.contiguous()), None if prescaled else ptr(tables.scaling),
               ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia), ptr(op.off), ptr(sfac), M, N, nx, deltaT,
               ptr(u), ptr(imag), ptr(scratch), nbytes, stream_ptr())
@@ -241,7 +244,10 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     inc = empty(1, cfg.max_outer_iters).fill_(float("nan"))
     imag = torch.zeros(1, dtype=torch.float64, device="cuda")
     sfac = shift_factors(op, tables, N, grid.deltaT)
-    scratch, nbytes = (None, 0) if sfac is not None else _cgc_scratch(1, N, nx)
+    if sfac is not None:  # cluster path: zero-initialised reduction slots
+        scratch, nbytes = torch.zeros(16, dtype=torch.uint8, device="cuda"), 16
+    else:
+        scratch, nbytes = _cgc_scratch(1, N, nx)
 
     def err(states):
         if reference is None:

@@ -29,7 +29,7 @@ def fgr():
 
 
 nb = int(_lib.query("kle_cgc_scratch_bytes", M, N, nx))
-scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+scratch = torch.zeros(nb, dtype=torch.uint8, device="cuda")
 
 
 def cgc(s):
