@@ -105,9 +105,10 @@ int kle_shift_factor_f64(const double* dia, const double* off, const double* lam
  * build_alpha_circulant(N, alpha).eigenvalues (pintuq/pcgc.py:68-76),
  * scaling / inv_scaling its scaling and 1/scaling; imag[M] (optional)
  * receives max|Im u| per sample. sfac (optional, kle_shift_factor_f64)
- * selects the cluster kernel; without it the pivots are formed on the fly
- * and `scratch` (kle_cgc_scratch_bytes) is used. scaling == NULL means r is
- * already alpha-scaled. */
+ * selects the cluster kernel; without it the pivots are formed on the fly.
+ * scratch: kle_cgc_scratch_bytes(M, N, nx) bytes (the cluster path needs
+ * 16*M bytes of per-sample reduction slots; the call zeroes them). scaling
+ * == NULL means r is already alpha-scaled. */
 int kle_three_step_f64(const double* r, const double* scaling, const double* inv_scaling, const double* lam,
                        const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
                        double* u, double* imag, void* scratch, size_t scratch_bytes, void* stream);
@@ -116,7 +117,9 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
  * in place, increment = max|U_new - U| per sample, stop test against tol,
  * status/iters updated, inc_hist[s][k-1] and imag[s] recorded, and
  * *active_count incremented once per still-active sample. R must already be
- * alpha-scaled (kle_fgr_f64 output). */
+ * alpha-scaled (kle_fgr_f64 output). With sfac (cluster path) `scratch` holds
+ * 16*M bytes of per-sample reduction slots that must be zero before the first
+ * call; every call leaves them zero again. */
 int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, const double* lam,
                        const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
                        int k, int max_iters, double tol, int32_t* status, int32_t* iters, double* inc_hist,
