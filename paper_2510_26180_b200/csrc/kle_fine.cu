@@ -303,12 +303,15 @@ struct FineInst {
 // (MR, P, R) variants; the first entry whose MR*P covers nx is the default,
 // KLE_FINE_VARIANT=<index> forces one (for tuning; blobs depend on MR, P).
 struct FineVariant {
-  int MR, P, R, pipe;
+  int MR, P, R, pipe, kind = 0;  // kind 1 (shared-memory factors): `pipe` is the min CTAs/SM bound
 };
 static const FineVariant kVariants[] = {
     {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {8, 16, 2, 0},  {16, 32, 3, 0}, {32, 32, 2, 0},  // defaults
     {8, 16, 2, 1},  {4, 32, 4, 0},  {8, 16, 4, 1},  {8, 16, 4, 0},  {16, 16, 2, 0}, {8, 32, 4, 0},
     {32, 16, 2, 0}, {16, 32, 2, 0}, {16, 32, 2, 1}, {16, 32, 4, 1}, {16, 32, 4, 0}, {4, 32, 4, 1},
+    {16, 32, 3, 4, 1}, {16, 32, 3, 3, 1}, {16, 32, 2, 4, 1}, {16, 32, 4, 3, 1},  // 18..21 shared-memory factors
+    {8, 16, 2, 4, 1},  {8, 16, 4, 4, 1},  {8, 32, 4, 4, 1},                     // 22..24
+    {32, 16, 2, 2, 1}, {32, 16, 1, 3, 1}, {16, 32, 3, 2, 1},                     // 25..27
 };
 static const int kNumDefaults = 6;
 
@@ -343,7 +346,9 @@ FineLayoutRT fine_layout(int nx) {
     const int nv = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
     if (v >= 0 && v < nv && kVariants[v].MR * kVariants[v].P >= nx) {
       const FineVariant& f = kVariants[v];
-      return {f.MR, f.P, f.R, f.pipe, fine_blob_doubles(f.MR, f.P)};
+      FineLayoutRT l{f.MR, f.P, f.R, f.pipe, f.kind ? sf_blob_doubles(f.MR, f.P) : fine_blob_doubles(f.MR, f.P)};
+      l.kind = f.kind;
+      return l;
     }
   }
   for (int i = 0; i < kNumDefaults; ++i) {
@@ -358,18 +363,26 @@ FineLayoutRT fine_layout(int nx) {
 int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx,
                 double h, double g0, cudaStream_t st) {
   if (lay.W) return mw_factor(dia, off, blob, M, nx, h, st);
+  if (lay.kind == 1) return sf_factor(lay, dia, off, blob, M, nx, h, g0, st);
   KLE_FINE_ALL(factor(dia, off, blob, M, nx, h, g0, st))
   return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: unsupported nx");
 }
 
 int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
   if (lay.W) return mw_fgr(a, st);
+  if (lay.kind == 1) {
+    if (!a.F_given) return sf_fgr(lay, a, st);
+    lay.kind = 0;  // F given: no sweep, any (MR, P) register variant serves the epilogue
+    lay.pipe = 0;
+    lay.R = (lay.MR == 16) ? 3 : (lay.P == 32 ? 4 : 2);
+  }
   KLE_FINE_ALL(fgr(a, st))
   return set_error(KLE_ERR_UNSUPPORTED, "fgr: unsupported nx");
 }
 
 int fine_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st) {
   if (lay.W) return mw_sweep(a, st);
+  if (lay.kind == 1) return sf_sweep(lay, a, st);
   KLE_FINE_ALL(sweep(a, st))
   return set_error(KLE_ERR_UNSUPPORTED, "sweep: unsupported nx");
 }

@@ -57,10 +57,13 @@ struct LaneFactors {
 //   xl_j = z'_j - l_{j+1} xl_{j+1}        (local backward)
 //   x'_j = xl_j + sig_j X                 (backward stitch, sig_j = prod -l_{+1})
 // plus three R-independent products; Y, X come from P-lane carry scans.
-template <int MR, int P, int R>
+// EXP (timing ablation only, wrong results): bit0 skips the carry scans,
+// bit1 skips the stitch loops.
+template <int MR, int P, int R, int EXP = 0>
 __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, int J,
                                          double hg) {
   using L = FineLayout<MR, P>;
+  constexpr bool SCAN = !(EXP & 1), STITCH = !(EXP & 2);
   for (int it = 0; it < J; ++it) {
 #pragma unroll
     for (int j = 1; j < MR; ++j)
@@ -69,6 +72,7 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
     double Y[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+    if constexpr (SCAN) {
 #pragma unroll
     for (int t = 0; t < L::LOGP; ++t) {
 #pragma unroll
@@ -82,7 +86,8 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
       const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
       Y[r] = (k == 0) ? 0.0 : o;
     }
-    {
+    }
+    if constexpr (STITCH) {
       double pi = 1.0;
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
@@ -105,6 +110,7 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
     double X[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) X[r] = x[r][0];
+    if constexpr (SCAN) {
 #pragma unroll
     for (int t = 0; t < L::LOGP; ++t) {
 #pragma unroll
@@ -118,7 +124,8 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
       const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
       X[r] = (k == P - 1) ? 0.0 : o;
     }
-    {
+    }
+    if constexpr (STITCH) {
       double sg = 1.0;
 #pragma unroll
       for (int j = MR - 1; j >= 0; --j) {

@@ -12,7 +12,8 @@ int check_launch(const char* what);
 
 struct FineLayoutRT {
   int MR, P, R, pipe, doubles;
-  int W = 0;  // > 0: multi-warp system (kle_fine_mw.cu), P = 32 * W
+  int W = 0;     // > 0: multi-warp system (kle_fine_mw.cu), P = 32 * W
+  int kind = 0;  // 0: factors in registers (kle_fine.cu); 1: factors in shared memory (kle_fine_sf.cu)
 };
 FineLayoutRT fine_layout(int nx);
 
@@ -39,6 +40,11 @@ struct SweepArgs {
   double h, g0;
 };
 
+int sf_blob_doubles(int MR, int P);
+int sf_factor(FineLayoutRT lay, const double* dia, const double* off, double* blob, int M, int nx, double h,
+              double g0, cudaStream_t st);
+int sf_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st);
+int sf_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st);
 int mw_warps(int nx);
 int mw_blob_doubles(int nx);
 int mw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, cudaStream_t st);
