@@ -381,3 +381,24 @@ def test_c5_full_shape_alpha_1e4(cuda):
     np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
     rtol = max(RTOL, 1e-12 * alpha ** (-(N - 1) / N))
     assert rel(res.states.cpu().numpy(), out["states"]) <= rtol
+
+
+def test_device_surrogate_build_matches_reference(cuda, golden):
+    """build_surrogate with device snapshots (3^4 Gauss-Hermite grid, the
+    config-1 recipe) against the surrogate the reference built."""
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.surrogate import build_surrogate, collect_snapshots
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    training = [ParameterSample(p, id=i) for i, p in enumerate(g["train_points"])]
+    snap = collect_snapshots(model, grid, cfg, training)
+    assert rel(snap.fields, g["snapshots"]) <= 1e-9  # PCGC to tol 1e-8 from the same init: O(1e-12)
+    s = build_surrogate(model, grid, cfg, training, eps_kl=1e-10, degree=2, snapshots=snap)
+    assert s.m_q == g["modes"].shape[0]
+    np.testing.assert_allclose(s.eigenvalues, g["eigenvalues"], rtol=1e-6, atol=1e-9 * g["eigenvalues"][0])
+    assert rel(s.mean_field, g["mean_field"]) <= 1e-10
+    # leading modes/coefficients (well separated eigenvalues) agree up to sign
+    for i in range(5):
+        sgn = np.sign(np.sum(s.modes[i] * g["modes"][i]))
+        assert rel(sgn * s.modes[i], g["modes"][i]) <= 1e-6
