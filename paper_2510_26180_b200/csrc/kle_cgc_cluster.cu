@@ -68,46 +68,109 @@ __device__ __forceinline__ int brev(int n) {
   return LOGN == 0 ? 0 : (int)(__brev((unsigned)n) >> (32 - LOGN));
 }
 
-// radix-2 DIT, bit-reversed input -> natural output; tw[j] = exp(-2 pi i j/N)
-template <int LOGN, int TC>
-__device__ void fft_dit(Cplx* t, const Cplx* tw) {
-  constexpr int N = 1 << LOGN;
-#pragma unroll 1
-  for (int lh = 0; lh < LOGN; ++lh) {
-    const int half = 1 << lh;
-    for (int b = threadIdx.x; b < (N / 2) * TC; b += blockDim.x) {
-      const int c = b % TC, bf = b / TC;
-      const int j = bf & (half - 1), g = bf >> lh;
-      const int i0 = (g << (lh + 1)) + j, i1 = i0 + half;
-      const Cplx w = tw[j << (LOGN - 1 - lh)];
-      const Cplx x0 = t[i0 * TC + c], x1 = t[i1 * TC + c];
-      const Cplx v = {fma(x1.re, w.re, -x1.im * w.im), fma(x1.re, w.im, x1.im * w.re)};
-      t[i0 * TC + c] = {x0.re + v.re, x0.im + v.im};
-      t[i1 * TC + c] = {x0.re - v.re, x0.im - v.im};
-    }
-    __syncthreads();
-  }
+// ---- four-step FFT over the columns of an [N][TC] tile (natural order in and
+// out). N = N1*N2: pass 1 does N2-point DFTs along stride-N1 subsequences and
+// the twiddle W_N^{n1 k2}; pass 2 does N1-point DFTs and writes X[k2 + N2 k1].
+// S = -1: forward (np.fft.fft sign), S = +1: inverse (unnormalised).
+template <int S>
+__device__ __forceinline__ Cplx mul_si(Cplx z) {  // z * (S i)
+  return S > 0 ? Cplx{-z.im, z.re} : Cplx{z.im, -z.re};
 }
+__device__ __forceinline__ Cplx cadd2(Cplx a, Cplx b) { return {a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ Cplx csub2(Cplx a, Cplx b) { return {a.re - b.re, a.im - b.im}; }
 
-// radix-2 DIF with conjugate twiddles (inverse), natural input -> bit-reversed output
-template <int LOGN, int TC>
-__device__ void ifft_dif(Cplx* t, const Cplx* tw) {
-  constexpr int N = 1 << LOGN;
-#pragma unroll 1
-  for (int lh = LOGN - 1; lh >= 0; --lh) {
-    const int half = 1 << lh;
-    for (int b = threadIdx.x; b < (N / 2) * TC; b += blockDim.x) {
-      const int c = b % TC, bf = b / TC;
-      const int j = bf & (half - 1), g = bf >> lh;
-      const int i0 = (g << (lh + 1)) + j, i1 = i0 + half;
-      const Cplx w = tw[j << (LOGN - 1 - lh)];
-      const Cplx x0 = t[i0 * TC + c], x1 = t[i1 * TC + c];
-      const Cplx d = {x0.re - x1.re, x0.im - x1.im};
-      t[i0 * TC + c] = {x0.re + x1.re, x0.im + x1.im};
-      t[i1 * TC + c] = {fma(d.re, w.re, d.im * w.im), fma(d.im, w.re, -d.re * w.im)};  // d * conj(w)
-    }
-    __syncthreads();
+template <int NS, int S>
+struct SmallDft;
+template <int S>
+struct SmallDft<1, S> {
+  __device__ __forceinline__ static void run(Cplx (&)[1]) {}
+};
+template <int S>
+struct SmallDft<2, S> {
+  __device__ __forceinline__ static void run(Cplx (&v)[2]) {
+    const Cplx a = v[0], b = v[1];
+    v[0] = cadd2(a, b);
+    v[1] = csub2(a, b);
   }
+};
+template <int S>
+struct SmallDft<4, S> {
+  __device__ __forceinline__ static void run(Cplx (&v)[4]) {
+    const Cplx s02 = cadd2(v[0], v[2]), d02 = csub2(v[0], v[2]);
+    const Cplx s13 = cadd2(v[1], v[3]), d13 = mul_si<S>(csub2(v[1], v[3]));
+    v[0] = cadd2(s02, s13);
+    v[2] = csub2(s02, s13);
+    v[1] = cadd2(d02, d13);
+    v[3] = csub2(d02, d13);
+  }
+};
+template <int S>
+struct SmallDft<8, S> {
+  __device__ __forceinline__ static void run(Cplx (&v)[8]) {
+    Cplx e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    SmallDft<4, S>::run(e);
+    SmallDft<4, S>::run(o);
+    constexpr double h = 0.70710678118654752440;
+    const Cplx w1 = {h, S * h}, w3 = {-h, S * h};
+    const Cplx t0 = o[0], t1 = cmul(o[1], w1), t2 = mul_si<S>(o[2]), t3 = cmul(o[3], w3);
+    v[0] = cadd2(e[0], t0);
+    v[4] = csub2(e[0], t0);
+    v[1] = cadd2(e[1], t1);
+    v[5] = csub2(e[1], t1);
+    v[2] = cadd2(e[2], t2);
+    v[6] = csub2(e[2], t2);
+    v[3] = cadd2(e[3], t3);
+    v[7] = csub2(e[3], t3);
+  }
+};
+
+// tw[j] = exp(-2 pi i j / N), j < N
+template <int LOGN, int TC, int S>
+__device__ void fft4step(Cplx* t, const Cplx* tw) {
+  constexpr int N = 1 << LOGN;
+  constexpr int N1 = 1 << ((LOGN + 1) / 2), N2 = N / N1;
+  // pass 1: tasks (n1, c)
+  for (int task = threadIdx.x; task < N1 * TC; task += blockDim.x) {
+    const int n1 = task / TC, c = task % TC;
+    Cplx v[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) v[n2] = t[(n1 + N1 * n2) * TC + c];
+    SmallDft<N2, S>::run(v);
+#pragma unroll
+    for (int k2 = 1; k2 < N2; ++k2) {
+      Cplx w = tw[(n1 * k2) & (N - 1)];
+      if (S > 0) w.im = -w.im;
+      v[k2] = cmul(v[k2], w);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) t[(n1 + N1 * k2) * TC + c] = v[k2];
+  }
+  __syncthreads();
+  // pass 2: tasks (k2, c); outputs go to natural positions after a barrier
+  constexpr int TASKS = N2 * TC;
+  constexpr int MAXR = 2;  // rounds held in registers (launcher guarantees blockDim * MAXR >= TASKS)
+  Cplx w[MAXR][N1];
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) {
+    const int task = threadIdx.x + r * blockDim.x;
+    if (task < TASKS) {
+      const int k2 = task / TC, c = task % TC;
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) w[r][n1] = t[(n1 + N1 * k2) * TC + c];
+      SmallDft<N1, S>::run(w[r]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) {
+    const int task = threadIdx.x + r * blockDim.x;
+    if (task < TASKS) {
+      const int k2 = task / TC, c = task % TC;
+#pragma unroll
+      for (int k1 = 0; k1 < N1; ++k1) t[(k2 + N2 * k1) * TC + c] = w[r][k1];
+    }
+  }
+  __syncthreads();
 }
 
 // pivots 1/beta_i of (lambda_f I + dT A), f = 0..N/2, layout [s][f][i]
@@ -158,8 +221,8 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
   Cplx* tile = reinterpret_cast<Cplx*>(smem);       // [N][HC] packed spectra
   double* uold = smem + 2 * N * HC;                 // [N][RB]
   double* offs = uold + N * RB;                     // [RB + 2]: dT*off[row0-1 .. row0+RB]
-  Cplx* tw = reinterpret_cast<Cplx*>(offs + RB + 2);  // [N/2]
-  Cplx* fwd = tw + N / 2;                           // [NF][2]
+  Cplx* tw = reinterpret_cast<Cplx*>(offs + RB + 2);  // [N]
+  Cplx* fwd = tw + N;                               // [NF][2]
   Cplx* bwd = fwd + 2 * NF;                         // [NF][2]
   double* red = reinterpret_cast<double*>(bwd + 2 * NF);  // [8 + 2]
 
@@ -169,7 +232,7 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
   // ---- phase 0: prefetch --------------------------------------------------
   for (int e = tid; e < N * RB; e += blockDim.x) {
     const int n = e / RB, col = e % RB, row = row0 + col;
-    double* dst = reinterpret_cast<double*>(&tile[brev<LOGN>(n) * HC + (col % HC)]) + (col / HC);
+    double* dst = reinterpret_cast<double*>(&tile[n * HC + (col % HC)]) + (col / HC);
     if (row < nx) {
       cp_async8(dst, a.R + sb + (size_t)n * nx + row);
       if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
@@ -181,7 +244,7 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
     const int row = row0 - 1 + e;  // offs[e] couples rows row and row+1
     offs[e] = (row >= 0 && row + 1 < nx) ? a.dT * a.off[(size_t)s * nx + row] : 0.0;
   }
-  for (int j = tid; j < N / 2; j += blockDim.x) {
+  for (int j = tid; j < N; j += blockDim.x) {
     double sn, cs;
     sincospi(-2.0 * (double)j / (double)N, &sn, &cs);
     tw[j] = {cs, sn};
@@ -200,11 +263,11 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
   if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
     for (int e = tid; e < N * RB; e += blockDim.x) {
       const int n = e / RB, col = e % RB;
-      reinterpret_cast<double*>(&tile[brev<LOGN>(n) * HC + (col % HC)])[col / HC] *= a.load_scale[n];
+      reinterpret_cast<double*>(&tile[n * HC + (col % HC)])[col / HC] *= a.load_scale[n];
     }
     __syncthreads();
   }
-  fft_dit<LOGN, HC>(tile, tw);
+  fft4step<LOGN, HC, -1>(tile, tw);
 
   const double hs = 0.5 / sqrt((double)N);  // two-for-one unpacking x 1/sqrt(N)
 #pragma unroll 1
@@ -326,24 +389,26 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
   }
   asm volatile("barrier.cluster.arrive;\n" ::: "memory");
   __syncthreads();
-  ifft_dif<LOGN, HC>(tile, tw);
+  fft4step<LOGN, HC, +1>(tile, tw);
   // ---- update ----------------------------------------------------------------
   const double rsN = 1.0 / sqrt((double)N);
   double incmax = 0.0;
+  bool bad = false;  // fmax drops NaN; remember it separately (a NaN increment must not converge)
+  double* __restrict__ out = a.Uout ? a.Uout : a.U;
+  const bool track = a.U != nullptr;
   for (int e = tid; e < N * RB; e += blockDim.x) {
     const int n = e / RB, col = e % RB, row = row0 + col;
     if (row >= nx) continue;
-    const Cplx z = tile[brev<LOGN>(n) * HC + (col % HC)];
+    const Cplx z = tile[n * HC + (col % HC)];
     const double u = ((col < HC ? z.re : z.im) * rsN) * a.inv_scaling[n];
-    const size_t g = sb + (size_t)n * nx + row;
-    if (a.Uout) {
-      if (a.U) incmax = nanmax(incmax, fabs(u - uold[n * RB + col]));
-      a.Uout[g] = u;
-    } else {
-      incmax = nanmax(incmax, fabs(u - uold[n * RB + col]));
-      a.U[g] = u;
+    if (track) {
+      const double d = fabs(u - uold[n * RB + col]);
+      incmax = fmax(incmax, d);
+      bad |= (d != d);
     }
+    out[sb + (size_t)n * nx + row] = u;
   }
+  if (__syncthreads_or(bad)) incmax = __longlong_as_double(0x7ff8000000000000LL);
   incmax = warp_max(incmax);
   const int lane = tid & 31, w = tid >> 5, nw = (blockDim.x + 31) >> 5;
   if (lane == 0) red[w] = incmax;
@@ -419,8 +484,10 @@ static int launch_cluster(const CgcArgs& a, const double* sfac, int CL, cudaStre
   constexpr int NPASS = (NF + CL_FPASS - 1) / CL_FPASS;
   constexpr int FP = (NF + NPASS - 1) / NPASS;
   const int nt = ((FP * CL_LANES + 31) / 32) * 32;
+  constexpr int N2 = N / (1 << ((LOGN + 1) / 2));
+  if (nt * 2 < N2 * HC) return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: FFT pass-2 tasks exceed 2 rounds");
   const size_t smem = (size_t)N * HC * sizeof(Cplx) + (size_t)N * RB * sizeof(double) + (RB + 2) * sizeof(double) +
-                      (N / 2 + 4 * NF) * sizeof(Cplx) + 10 * sizeof(double);
+                      (N + 4 * NF) * sizeof(Cplx) + 10 * sizeof(double);
   auto kern = cgc_cluster_kernel<LOGN, MR>;
   static bool attr = false;
   if (!attr) {
