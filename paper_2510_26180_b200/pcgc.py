@@ -186,6 +186,29 @@ class BatchResult:
     increments: "torch.Tensor"  # (M, max_iters) per-k increments, NaN past the stop
     imag: "torch.Tensor"        # (M,) max imaginary residue
 
+    def failures(self) -> dict:
+        """{sample index: exception} for every sample that did not converge,
+        mapped to the reference's error types (MaxItersExceededError,
+        pintuq/pcgc.py:352-357; non-finite trajectory ValueError,
+        pintuq/core.py:179-181)."""
+        st = self.status.cpu().numpy()
+        out = {}
+        for i in np.nonzero(st != SAMPLE_CONVERGED)[0]:
+            if st[i] == SAMPLE_MAXITERS:
+                out[int(i)] = MaxItersExceededError(f"sample {int(i)} did not reach tol")
+            elif st[i] == SAMPLE_NONFINITE:
+                out[int(i)] = ValueError(f"sample {int(i)}: trajectory contains non-finite entries")
+            else:
+                out[int(i)] = RuntimeError(f"sample {int(i)}: status {int(st[i])}")
+        return out
+
+    def raise_for_status(self):
+        """Raise the first per-sample failure (reference ``raise_on_max=True`` behaviour)."""
+        f = self.failures()
+        if f:
+            i = min(f)
+            raise f[i]
+
 
 def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, tables: AlphaTables = None,
                       workspace=None) -> BatchResult:

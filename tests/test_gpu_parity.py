@@ -402,3 +402,72 @@ def test_device_surrogate_build_matches_reference(cuda, golden):
     for i in range(5):
         sgn = np.sign(np.sum(s.modes[i] * g["modes"][i]))
         assert rel(sgn * s.modes[i], g["modes"][i]) <= 1e-6
+
+
+def test_batched_status_words_and_exceptions(cuda, golden):
+    """max_outer_iters too small -> MAXITERS status / MaxItersExceededError;
+    a non-finite initial guess -> NONFINITE status / ValueError; the other
+    samples are unaffected (per-sample failure isolation, experiments.py:236-257)."""
+    import torch
+    from paper_2510_26180_b200 import MaxItersExceededError, SolverConfig
+    from paper_2510_26180_b200.device import DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import SAMPLE_CONVERGED, SAMPLE_MAXITERS, SAMPLE_NONFINITE, pcgc_solve_device
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    op = DeviceOperator.from_model(model, g["xi_all"][:4])
+    U = to_dev(g["U0"][:4]).clone()
+    res = pcgc_solve_device(op, U, grid, SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=5))
+    assert np.all(res.status.cpu().numpy() == SAMPLE_MAXITERS)
+    assert np.all(res.iters.cpu().numpy() == 5)
+    with pytest.raises(MaxItersExceededError):
+        res.raise_for_status()
+    U = to_dev(g["U0"][:4]).clone()
+    U[2, 3, 7] = float("nan")
+    res = pcgc_solve_device(op, U, grid, cfg)
+    st = res.status.cpu().numpy()
+    assert st[2] == SAMPLE_NONFINITE and np.all(st[[0, 1, 3]] == SAMPLE_CONVERGED)
+    np.testing.assert_array_equal(res.iters.cpu().numpy()[[0, 1, 3]], g["iters"][[0, 1, 3]])
+    assert isinstance(res.failures()[2], ValueError)
+
+
+def test_pcgc_stop_on_reference_and_history(cuda, golden):
+    """stop_on='reference' with store_states (pintuq/pcgc.py:291-348)."""
+    from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample
+    from paper_2510_26180_b200.pcgc import pcgc_solve
+    from paper_2510_26180_b200.propagators import fine_reference
+
+    model, grid, cfg = c1_config()
+    g = golden("c1")
+    xi = ParameterSample(g["xi_all"][0], id=0)
+    ref = fine_reference(model, xi, grid, cfg)
+    tr = pcgc_solve(model, xi, grid, cfg, CoarseTrajectory(model.initial_condition(), g["U0"][0]),
+                    reference=ref, stop_on="reference", store_states=True)
+    assert tr.converged and tr.records[-1].max_err_vs_ref <= cfg.tol
+    assert len(tr.states_history) == tr.iterations + 1
+    errs = tr.max_errors()
+    assert errs[0] > errs[-1]
+    with pytest.raises(ValueError):
+        pcgc_solve(model, xi, grid, cfg, CoarseTrajectory(model.initial_condition(), g["U0"][0]), stop_on="reference")
+
+
+@pytest.mark.parametrize("nx,N,J", [(1, 4, 3), (2, 2, 2), (15, 1, 5), (33, 3, 2)])
+def test_degenerate_shapes(cuda, nx, N, J):
+    """Tiny / degenerate shapes (nx = 1, N = 1, odd N) against the oracle."""
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    model = LogNormalKL1D(nx=nx, d=2)
+    grid = make_time_grid(1.0, N, J)
+    cfg = SolverConfig(alpha=0.1, tol=1e-10, max_outer_iters=40)
+    xi = np.random.default_rng(nx * 10 + N).normal(size=(3, 2))
+    op = DeviceOperator.from_model(model, xi)
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    init = U.cpu().numpy()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    out = batched.pcgc(dia, off, model.initial_condition(), init, N, J, 1.0, 0.1, 1e-10, 40)
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
+    assert rel(res.states.cpu().numpy(), out["states"]) <= RTOL
