@@ -4,26 +4,30 @@
 // Reference: three_step_solve pintuq/pcgc.py:148-172, factor_shifted :90-145,
 // the increment / stop test of pcgc_solve :335-348.
 //
-// The sample's N x nx block is split into CL row blocks of RB = 8*MR rows,
-// one CTA each. Per CTA:
+// The sample's N x nx block is split into CL row blocks of RB = 8*MR rows
+// (MR = 8), one CTA each. Per CTA (NT = 8 (N/2+1) threads rounded to warps):
 //   0. cp.async prefetch of the R rows, the old U rows (for the increment)
-//      and the operator's off-diagonal into shared memory; the pivots of the
-//      first frequency pass are loaded into registers at the same time.
+//      and the operator's off-diagonal into shared memory; each thread keeps
+//      one column, so the address arithmetic is incremental. The pivots of
+//      the thread's frequency are loaded into registers at the same time.
 //   1. Two-for-one real FFT along time: rows c and c + RB/2 are packed as
-//      z = r_c + i r_{c+RB/2} into an [N][RB/2] complex tile (radix-2 DIT,
-//      bit-reversed input). p_f of both rows follows from Z_f, Z_{N-f}.
-//   2. For f = 0..N/2 (in passes of <= 17 frequencies), an 8-lane group owns
-//      the CTA's RB rows (MR per lane, registers) and solves
+//      z = r_c + i r_{c+RB/2} into an [N][RB/2] complex tile (four-step FFT,
+//      natural order; columns XOR-swizzled against bank conflicts).
+//      p_f of both rows follows from Z_f, Z_{N-f}.
+//   2. All frequencies f = 0..N/2 at once, one 8-lane group each: the group
+//      owns the CTA's RB rows (MR per lane, registers) and solves
 //      (lambda_f I + dT A) q = p with the LDL^T pivots 1/beta precomputed once
 //      per batch (shift_factor_kernel). Chunks are stitched by a 3-stage
 //      affine lane scan and across the cluster's CTAs through distributed
-//      shared memory (block composites; consumers compose those of the blocks
-//      before/after them).
+//      shared memory: every CTA publishes its block composite; a consumer
+//      loads those of the blocks before (after) it in parallel, one per lane,
+//      and composes them with a 3-stage lane butterfly. Two cluster barriers
+//      per iteration.
 //   3. The packed Hermitian spectra W_f = q_c + i q_{c+RB/2} (and the mirror
-//      W_{N-f}) are written in natural order (passes never touch each other's
-//      pending inputs), inverse FFT by radix-2 DIF (bit-reversed output),
+//      W_{N-f}) are written in natural order, inverse four-step FFT,
 //      u = Re / Im parts over scaling; increment vs the prefetched old U;
-//      block + cluster max-reductions; per-sample stop test.
+//      block max-reduction, cluster max through an atomic slot (the last CTA
+//      finishes the sample's stop test).
 // The two-for-one packing enforces the Hermitian symmetry of the real
 // solution, so u is real by construction (imag residue reported as 0).
 // HBM traffic per outer iteration and (n, i): R 8 B + U 8 B read, U 8 B
@@ -38,7 +42,6 @@ namespace cg = cooperative_groups;
 namespace kle {
 
 constexpr int CL_LANES = 8;
-constexpr int CL_FPASS = 17;  // frequencies per pass
 
 __device__ __forceinline__ Cplx cfma(Cplx a, Cplx b, Cplx c) {  // a*b + c
   return {fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))};
@@ -67,6 +70,18 @@ template <int LOGN>
 __device__ __forceinline__ int brev(int n) {
   return LOGN == 0 ? 0 : (int)(__brev((unsigned)n) >> (32 - LOGN));
 }
+
+// ---- tile layout: [N][HC] complex, the column index XOR-swizzled within
+// aligned groups of 8 (tswz) so that the 8-lane solver groups, whose lanes
+// read columns MR apart at 4 different frequency rows, spread over the banks;
+// consecutive columns of one row stay a permutation (conflict-free sweeps).
+template <int MR>
+__device__ __forceinline__ int tswz(int n, int c) {
+  if constexpr (MR == 8) return c ^ (((c >> 3) & 3) | ((n & 1) << 2));
+  else return c ^ (((c >> 3) & 1) | ((n & 3) << 1));
+}
+template <int MR, int HC>
+__device__ __forceinline__ int tix(int n, int c) { return n * HC + tswz<MR>(n, c); }
 
 // ---- four-step FFT over the columns of an [N][TC] tile (natural order in and
 // out). N = N1*N2: pass 1 does N2-point DFTs along stride-N1 subsequences and
@@ -125,7 +140,7 @@ struct SmallDft<8, S> {
 };
 
 // tw[j] = exp(-2 pi i j / N), j < N
-template <int LOGN, int TC, int S>
+template <int LOGN, int TC, int S, int MR>
 __device__ void fft4step(Cplx* t, const Cplx* tw) {
   constexpr int N = 1 << LOGN;
   constexpr int N1 = 1 << ((LOGN + 1) / 2), N2 = N / N1;
@@ -134,7 +149,7 @@ __device__ void fft4step(Cplx* t, const Cplx* tw) {
     const int n1 = task / TC, c = task % TC;
     Cplx v[N2];
 #pragma unroll
-    for (int n2 = 0; n2 < N2; ++n2) v[n2] = t[(n1 + N1 * n2) * TC + c];
+    for (int n2 = 0; n2 < N2; ++n2) v[n2] = t[tix<MR, TC>(n1 + N1 * n2, c)];
     SmallDft<N2, S>::run(v);
 #pragma unroll
     for (int k2 = 1; k2 < N2; ++k2) {
@@ -143,7 +158,7 @@ __device__ void fft4step(Cplx* t, const Cplx* tw) {
       v[k2] = cmul(v[k2], w);
     }
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) t[(n1 + N1 * k2) * TC + c] = v[k2];
+    for (int k2 = 0; k2 < N2; ++k2) t[tix<MR, TC>(n1 + N1 * k2, c)] = v[k2];
   }
   __syncthreads();
   // pass 2: tasks (k2, c); outputs go to natural positions after a barrier
@@ -156,7 +171,7 @@ __device__ void fft4step(Cplx* t, const Cplx* tw) {
     if (task < TASKS) {
       const int k2 = task / TC, c = task % TC;
 #pragma unroll
-      for (int n1 = 0; n1 < N1; ++n1) w[r][n1] = t[(n1 + N1 * k2) * TC + c];
+      for (int n1 = 0; n1 < N1; ++n1) w[r][n1] = t[tix<MR, TC>(n1 + N1 * k2, c)];
       SmallDft<N1, S>::run(w[r]);
     }
   }
@@ -167,7 +182,7 @@ __device__ void fft4step(Cplx* t, const Cplx* tw) {
     if (task < TASKS) {
       const int k2 = task / TC, c = task % TC;
 #pragma unroll
-      for (int k1 = 0; k1 < N1; ++k1) t[(k2 + N2 * k1) * TC + c] = w[r][k1];
+      for (int k1 = 0; k1 < N1; ++k1) t[tix<MR, TC>(k2 + N2 * k1, c)] = w[r][k1];
     }
   }
   __syncthreads();
@@ -205,11 +220,38 @@ __device__ __forceinline__ void load_pivots(Cplx (&ib)[MR], Cplx& ibprev, const 
   for (int j = 0; j < MR; ++j) ib[j] = (r0 + j < nx) ? src[r0 + j] : Cplx{1.0, 0.0};
 }
 
+// Composes the affine maps x -> A x + B held by the 8 lanes of a group
+// (butterfly; every lane ends with the ordered composite). OUTER_HIGH: the
+// higher lane's map is applied last.
+template <bool OUTER_HIGH>
+__device__ __forceinline__ void compose_lanes(Cplx& A, Cplx& B, int k) {
+#pragma unroll
+  for (int d = 1; d < CL_LANES; d <<= 1) {
+    const Cplx Ao = shfl_xor_c(A, d), Bo = shfl_xor_c(B, d);
+    const bool outer = OUTER_HIGH ? (k & d) != 0 : (k & d) == 0;
+    B = outer ? cfma(A, Bo, B) : cfma(Ao, B, Bo);
+    A = cmul(A, Ao);
+  }
+}
+
 template <int LOGN, int MR>
-__global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const double* __restrict__ sfac_d) {
-  constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
-  constexpr int NPASS = (NF + CL_FPASS - 1) / CL_FPASS;
-  constexpr int FP = (NF + NPASS - 1) / NPASS;
+struct ClShape {
+  static constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
+  static constexpr int NT = ((NF * CL_LANES + 31) / 32) * 32;  // one 8-lane group per frequency
+  static constexpr int NSTEP = NT / RB;                         // column-fixed sweeps (0: generic loop)
+#ifndef KLE_CGC_MINB
+#define KLE_CGC_MINB 2  // 288 threads: 2 CTAs/SM (measured; 1 CTA without spills is slower)
+#endif
+  static constexpr int MINB = NT <= 160 ? 3 : KLE_CGC_MINB;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * N * HC + (size_t)N * RB + RB + 2 + N + 2 * N +
+                                                   8 * NF + 16);
+};
+
+template <int LOGN, int MR>
+__global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB)
+    cgc_cluster_kernel(CgcArgs a, const double* __restrict__ sfac_d) {
+  using K = ClShape<LOGN, MR>;
+  constexpr int N = K::N, NF = K::NF, RB = K::RB, HC = K::HC, NT = K::NT, NSTEP = K::NSTEP;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int c = (int)cluster.block_rank();
@@ -218,204 +260,248 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
   if (a.status && a.status[s] != KLE_SAMPLE_ACTIVE) return;  // uniform over the cluster
 
   extern __shared__ __align__(16) double smem[];
-  Cplx* tile = reinterpret_cast<Cplx*>(smem);       // [N][HC] packed spectra
+  Cplx* tile = reinterpret_cast<Cplx*>(smem);       // [N][HC] packed spectra (swizzled columns)
   double* uold = smem + 2 * N * HC;                 // [N][RB]
   double* offs = uold + N * RB;                     // [RB + 2]: dT*off[row0-1 .. row0+RB]
-  Cplx* tw = reinterpret_cast<Cplx*>(offs + RB + 2);  // [N]
+  double* isc = offs + RB + 2;                      // [N]: inv_scaling
+  Cplx* tw = reinterpret_cast<Cplx*>(isc + N);      // [N]
   Cplx* fwd = tw + N;                               // [NF][2]
   Cplx* bwd = fwd + 2 * NF;                         // [NF][2]
-  double* red = reinterpret_cast<double*>(bwd + 2 * NF);  // [8 + 2]
+  double* red = reinterpret_cast<double*>(bwd + 2 * NF);  // [16]
 
   const int tid = threadIdx.x;
   const size_t sb = (size_t)s * N * nx;
   const int row0 = c * RB;
   // ---- phase 0: prefetch --------------------------------------------------
-  for (int e = tid; e < N * RB; e += blockDim.x) {
-    const int n = e / RB, col = e % RB, row = row0 + col;
-    double* dst = reinterpret_cast<double*>(&tile[n * HC + (col % HC)]) + (col / HC);
-    if (row < nx) {
-      cp_async8(dst, a.R + sb + (size_t)n * nx + row);
-      if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
-    } else {
-      *dst = 0.0;
+  if constexpr (NSTEP > 0) {  // each thread keeps one column; rows n = tid/RB + m*NSTEP
+    if (tid < NSTEP * RB) {
+      const int col = tid % RB, row = row0 + col, ci = col % HC, part = col / HC;
+      for (int n = tid / RB; n < N; n += NSTEP) {
+        double* dst = reinterpret_cast<double*>(&tile[tix<MR, HC>(n, ci)]) + part;
+        if (row < nx) {
+          cp_async8(dst, a.R + sb + (size_t)n * nx + row);
+          if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
+        } else {
+          *dst = 0.0;
+        }
+      }
+    }
+  } else {
+    for (int e = tid; e < N * RB; e += NT) {
+      const int n = e / RB, col = e % RB, row = row0 + col;
+      double* dst = reinterpret_cast<double*>(&tile[tix<MR, HC>(n, col % HC)]) + (col / HC);
+      if (row < nx) {
+        cp_async8(dst, a.R + sb + (size_t)n * nx + row);
+        if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
+      } else {
+        *dst = 0.0;
+      }
     }
   }
-  for (int e = tid; e < RB + 2; e += blockDim.x) {
+  for (int e = tid; e < RB + 2; e += NT) {
     const int row = row0 - 1 + e;  // offs[e] couples rows row and row+1
     offs[e] = (row >= 0 && row + 1 < nx) ? a.dT * a.off[(size_t)s * nx + row] : 0.0;
   }
-  for (int j = tid; j < N; j += blockDim.x) {
+  for (int j = tid; j < N; j += NT) {
     double sn, cs;
     sincospi(-2.0 * (double)j / (double)N, &sn, &cs);
     tw[j] = {cs, sn};
+    isc[j] = a.inv_scaling[j];
   }
   const int fsys = tid / CL_LANES, k = tid % CL_LANES;
+  const bool valid = fsys < NF;
+  const int f = valid ? fsys : NF - 1;
   const int r0l = k * MR;  // local first row of this lane
   const int r0 = row0 + r0l;
-  const Cplx* piv = reinterpret_cast<const Cplx*>(sfac_d) + (size_t)s * NF * nx;
   Cplx ib[MR], ibprev;
-  {
-    const int f = min(fsys, NF - 1);
-    load_pivots<MR>(ib, ibprev, piv + (size_t)f * nx, r0, nx);
-  }
+  load_pivots<MR>(ib, ibprev, reinterpret_cast<const Cplx*>(sfac_d) + ((size_t)s * NF + f) * nx, r0, nx);
   cp_async_wait_all();
   __syncthreads();
   if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
-    for (int e = tid; e < N * RB; e += blockDim.x) {
+    for (int e = tid; e < N * RB; e += NT) {
       const int n = e / RB, col = e % RB;
-      reinterpret_cast<double*>(&tile[n * HC + (col % HC)])[col / HC] *= a.load_scale[n];
+      reinterpret_cast<double*>(&tile[tix<MR, HC>(n, col % HC)])[col / HC] *= a.load_scale[n];
     }
     __syncthreads();
   }
-  fft4step<LOGN, HC, -1>(tile, tw);
+  fft4step<LOGN, HC, -1, MR>(tile, tw);
 
+  // ---- one frequency per 8-lane group: (lambda_f I + dT A) q = p_f ---------
   const double hs = 0.5 / sqrt((double)N);  // two-for-one unpacking x 1/sqrt(N)
-#pragma unroll 1
-  for (int pass = 0; pass < NPASS; ++pass) {
-    const int fl = pass * FP + fsys;
-    const bool valid = fsys < FP && fl < NF;
-    const int f = valid ? fl : NF - 1;
-    if (pass > 0) load_pivots<MR>(ib, ibprev, piv + (size_t)f * nx, r0, nx);
-    // p_f for the lane's rows from the packed spectrum
-    Cplx y[MR];
-    const int fm = (N - f) & (N - 1);
+  Cplx y[MR];
+  const int fm = (N - f) & (N - 1);
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const int col = r0l + j;
+    const Cplx zf = tile[tix<MR, HC>(f, col % HC)], zm = tile[tix<MR, HC>(fm, col % HC)];
+    if (col < HC) y[j] = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};   // (Z_f + conj Z_-f)/2
+    else y[j] = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};            // (Z_f - conj Z_-f)/(2i)
+  }
+  // l_r = dT off_{r-1} / beta_{r-1}
+  Cplx l[MR];
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const double E = offs[r0l + j];  // couples rows r0+j-1 and r0+j
+    const Cplx ip = (j == 0) ? ibprev : ib[j - 1];
+    l[j] = {E * ip.re, E * ip.im};
+  }
+  Cplx A = {1.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    if (j > 0) y[j] = cfma({-l[j].re, -l[j].im}, y[j - 1], y[j]);
+    A = cneg_mul(l[j], A);
+  }
+  Cplx B = y[MR - 1];
+#pragma unroll
+  for (int d = 1; d < CL_LANES; d <<= 1) {
+    const Cplx Ao = shfl_up_c(A, d), Bo = shfl_up_c(B, d);
+    if (k >= d) {
+      B = cfma(A, Bo, B);
+      A = cmul(A, Ao);
+    }
+  }
+  Cplx Ae = shfl_up_c(A, 1), Be = shfl_up_c(B, 1);
+  if (k == 0) {
+    Ae = {1.0, 0.0};
+    Be = {0.0, 0.0};
+  }
+  if (valid && k == CL_LANES - 1) {
+    fwd[2 * f] = A;
+    fwd[2 * f + 1] = B;
+  }
+  cluster.sync();
+  Cplx Yc;
+  {  // composite of the blocks q < c, q = k (+ 8) per lane, then a lane butterfly
+    Cplx A0 = {1.0, 0.0}, B0 = {0.0, 0.0}, A1 = {1.0, 0.0}, B1 = {0.0, 0.0};
+    if (k < c) {
+      const Cplx* rf = cluster.map_shared_rank(fwd, k);
+      A0 = rf[2 * f];
+      B0 = rf[2 * f + 1];
+    }
+    if (k + CL_LANES < c) {
+      const Cplx* rf = cluster.map_shared_rank(fwd, k + CL_LANES);
+      A1 = rf[2 * f];
+      B1 = rf[2 * f + 1];
+    }
+    compose_lanes<true>(A0, B0, k);
+    if (c > CL_LANES) compose_lanes<true>(A1, B1, k);
+    Yc = cfma(A1, B0, B1);
+  }
+  const Cplx Cin = cfma(Ae, Yc, Be);
+  {
+    Cplx pi = {1.0, 0.0};
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
-      const int col = r0l + j;
-      const Cplx zf = tile[f * HC + (col % HC)], zm = tile[fm * HC + (col % HC)];
-      if (col < HC) y[j] = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};   // (Z_f + conj Z_-f)/2
-      else y[j] = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};            // (Z_f - conj Z_-f)/(2i)
+      pi = cneg_mul(l[j], pi);
+      y[j] = cmul(cfma(pi, Cin, y[j]), ib[j]);
     }
-    // l_r = dT off_{r-1} / beta_{r-1}
-    Cplx l[MR];
+  }
+  const double En = offs[r0l + MR];  // couples the lane's last row and the next
+  const Cplx lnext = {En * ib[MR - 1].re, En * ib[MR - 1].im};
+  Cplx S = {1.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      const double E = offs[r0l + j];  // couples rows r0+j-1 and r0+j
-      const Cplx ip = (j == 0) ? ibprev : ib[j - 1];
-      l[j] = {E * ip.re, E * ip.im};
-    }
-    Cplx A = {1.0, 0.0};
+  for (int j = MR - 1; j >= 0; --j) {
+    const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
+    if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
+    S = cneg_mul(ln, S);
+  }
+  Cplx T = y[0];
 #pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      if (j > 0) y[j] = cfma({-l[j].re, -l[j].im}, y[j - 1], y[j]);
-      A = cneg_mul(l[j], A);
+  for (int d = 1; d < CL_LANES; d <<= 1) {
+    const Cplx So = shfl_down_c(S, d), To = shfl_down_c(T, d);
+    if (k + d < CL_LANES) {
+      T = cfma(S, To, T);
+      S = cmul(S, So);
     }
-    Cplx B = y[MR - 1];
-#pragma unroll
-    for (int d = 1; d < CL_LANES; d <<= 1) {
-      const Cplx Ao = shfl_up_c(A, d), Bo = shfl_up_c(B, d);
-      if (k >= d) {
-        B = cfma(A, Bo, B);
-        A = cmul(A, Ao);
-      }
+  }
+  Cplx Se = shfl_down_c(S, 1), Te = shfl_down_c(T, 1);
+  if (k == CL_LANES - 1) {
+    Se = {1.0, 0.0};
+    Te = {0.0, 0.0};
+  }
+  if (valid && k == 0) {
+    bwd[2 * f] = S;
+    bwd[2 * f + 1] = T;
+  }
+  cluster.sync();  // also: every thread has read its inputs from the tile
+  Cplx Xc;
+  {  // composite of the blocks q > c (the nearest block applied last)
+    Cplx A0 = {1.0, 0.0}, B0 = {0.0, 0.0}, A1 = {1.0, 0.0}, B1 = {0.0, 0.0};
+    if (c + 1 + k < CL) {
+      const Cplx* rb = cluster.map_shared_rank(bwd, c + 1 + k);
+      A0 = rb[2 * f];
+      B0 = rb[2 * f + 1];
     }
-    Cplx Ae = shfl_up_c(A, 1), Be = shfl_up_c(B, 1);
-    if (k == 0) {
-      Ae = {1.0, 0.0};
-      Be = {0.0, 0.0};
+    if (c + 1 + CL_LANES + k < CL) {
+      const Cplx* rb = cluster.map_shared_rank(bwd, c + 1 + CL_LANES + k);
+      A1 = rb[2 * f];
+      B1 = rb[2 * f + 1];
     }
-    if (valid && k == CL_LANES - 1) {
-      fwd[2 * f] = A;
-      fwd[2 * f + 1] = B;
-    }
-    cluster.sync();
-    Cplx Yc = {0.0, 0.0};
-    for (int q = 0; q < c; ++q) {
-      const Cplx* rf = cluster.map_shared_rank(fwd, q);
-      Yc = cfma(rf[2 * f], Yc, rf[2 * f + 1]);
-    }
-    const Cplx Cin = cfma(Ae, Yc, Be);
-    {
-      Cplx pi = {1.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < MR; ++j) {
-        pi = cneg_mul(l[j], pi);
-        y[j] = cmul(cfma(pi, Cin, y[j]), ib[j]);
-      }
-    }
-    const double En = offs[r0l + MR];  // couples the lane's last row and the next
-    const Cplx lnext = {En * ib[MR - 1].re, En * ib[MR - 1].im};
-    Cplx S = {1.0, 0.0};
+    compose_lanes<false>(A0, B0, k);
+    if (c + 1 + CL_LANES < CL) compose_lanes<false>(A1, B1, k);
+    Xc = cfma(A0, B1, B0);
+  }
+  const Cplx Xin = cfma(Se, Xc, Te);
+  {
+    Cplx sg = {1.0, 0.0};
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
       const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
-      if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
-      S = cneg_mul(ln, S);
-    }
-    Cplx T = y[0];
-#pragma unroll
-    for (int d = 1; d < CL_LANES; d <<= 1) {
-      const Cplx So = shfl_down_c(S, d), To = shfl_down_c(T, d);
-      if (k + d < CL_LANES) {
-        T = cfma(S, To, T);
-        S = cmul(S, So);
-      }
-    }
-    Cplx Se = shfl_down_c(S, 1), Te = shfl_down_c(T, 1);
-    if (k == CL_LANES - 1) {
-      Se = {1.0, 0.0};
-      Te = {0.0, 0.0};
-    }
-    if (valid && k == 0) {
-      bwd[2 * f] = S;
-      bwd[2 * f + 1] = T;
-    }
-    cluster.sync();  // also: every thread has read this pass's inputs from the tile
-    Cplx Xc = {0.0, 0.0};
-    for (int q = CL - 1; q > c; --q) {
-      const Cplx* rb = cluster.map_shared_rank(bwd, q);
-      Xc = cfma(rb[2 * f], Xc, rb[2 * f + 1]);
-    }
-    const Cplx Xin = cfma(Se, Xc, Te);
-    {
-      Cplx sg = {1.0, 0.0};
-#pragma unroll
-      for (int j = MR - 1; j >= 0; --j) {
-        const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
-        sg = cneg_mul(ln, sg);
-        y[j] = cfma(sg, Xin, y[j]);
-      }
-    }
-    // pack W_f = q(col) + i q(col + HC): lanes k < 4 hold the first half rows
-#pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      const Cplx qb = shfl_xor_c(y[j], CL_LANES / 2);
-      if (valid && k < CL_LANES / 2) {
-        const int col = r0l + j;
-        tile[f * HC + col] = {y[j].re - qb.im, y[j].im + qb.re};
-        if (f > 0 && 2 * f < N) tile[(N - f) * HC + col] = {y[j].re + qb.im, qb.re - y[j].im};
-      }
+      sg = cneg_mul(ln, sg);
+      y[j] = cfma(sg, Xin, y[j]);
     }
   }
+  // every CTA has done its last DSMEM read
   asm volatile("barrier.cluster.arrive;\n" ::: "memory");
+  // pack W_f = q(col) + i q(col + HC): lanes k < 4 hold the first half rows
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const Cplx qb = shfl_xor_c(y[j], CL_LANES / 2);
+    if (valid && k < CL_LANES / 2) {
+      const int col = r0l + j;
+      tile[tix<MR, HC>(f, col)] = {y[j].re - qb.im, y[j].im + qb.re};
+      if (f > 0 && 2 * f < N) tile[tix<MR, HC>(N - f, col)] = {y[j].re + qb.im, qb.re - y[j].im};
+    }
+  }
   __syncthreads();
-  fft4step<LOGN, HC, +1>(tile, tw);
+  fft4step<LOGN, HC, +1, MR>(tile, tw);
   // ---- update ----------------------------------------------------------------
   const double rsN = 1.0 / sqrt((double)N);
   double incmax = 0.0;
   bool bad = false;  // fmax drops NaN; remember it separately (a NaN increment must not converge)
   double* __restrict__ out = a.Uout ? a.Uout : a.U;
   const bool track = a.U != nullptr;
-  for (int e = tid; e < N * RB; e += blockDim.x) {
-    const int n = e / RB, col = e % RB, row = row0 + col;
-    if (row >= nx) continue;
-    const Cplx z = tile[n * HC + (col % HC)];
-    const double u = ((col < HC ? z.re : z.im) * rsN) * a.inv_scaling[n];
+  auto upd = [&](int n, int col, int row) {
+    const Cplx z = tile[tix<MR, HC>(n, col % HC)];
+    const double u = ((col < HC ? z.re : z.im) * rsN) * isc[n];
     if (track) {
       const double d = fabs(u - uold[n * RB + col]);
       incmax = fmax(incmax, d);
       bad |= (d != d);
     }
     out[sb + (size_t)n * nx + row] = u;
+  };
+  if constexpr (NSTEP > 0) {
+    if (tid < NSTEP * RB) {
+      const int col = tid % RB, row = row0 + col;
+      if (row < nx)
+        for (int n = tid / RB; n < N; n += NSTEP) upd(n, col, row);
+    }
+  } else {
+    for (int e = tid; e < N * RB; e += NT) {
+      const int n = e / RB, col = e % RB, row = row0 + col;
+      if (row < nx) upd(n, col, row);
+    }
   }
   if (__syncthreads_or(bad)) incmax = __longlong_as_double(0x7ff8000000000000LL);
   incmax = warp_max(incmax);
-  const int lane = tid & 31, w = tid >> 5, nw = (blockDim.x + 31) >> 5;
+  const int lane = tid & 31, w = tid >> 5;
+  constexpr int NW = NT / 32;
   if (lane == 0) red[w] = incmax;
   __syncthreads();
   if (tid == 0) {
     double r1 = 0.0;
-    for (int i = 0; i < nw; ++i) r1 = nanmax(r1, red[i]);
+    for (int i = 0; i < NW; ++i) r1 = nanmax(r1, red[i]);
     // cluster-wide max through a global slot; the last CTA to arrive finishes
     // the sample (no further cluster barrier needed). Non-negative doubles
     // (and +NaN) order like their bit patterns.
@@ -442,8 +528,8 @@ __global__ void __launch_bounds__(160, 3) cgc_cluster_kernel(CgcArgs a, const do
       }
     }
   }
-  // every CTA arrived (after its last DSMEM read) before the update phase;
-  // wait here so no CTA's shared memory disappears under a remote reader
+  // every CTA arrived (after its last DSMEM read) before the pack; wait here
+  // so no CTA's shared memory disappears under a remote reader
   asm volatile("barrier.cluster.wait;\n" ::: "memory");
 }
 
@@ -452,6 +538,8 @@ static bool cluster_shape(int N, int nx, int* MR, int* CL, int* LOGN) {
   if (N < 2 || N > 64 || (N & (N - 1))) return false;
   int logn = 0;
   while ((1 << logn) < N) ++logn;
+  // 64-row blocks: measured faster than 32-row blocks in clusters of up to 16
+  // (c2: 2.97 vs 4.34 ms per 4096 samples; fewer, fatter CTAs per sample)
   const int mr = 8;
   const int rb = CL_LANES * mr;
   const int cl = (nx + rb - 1) / rb;
@@ -480,25 +568,20 @@ int shift_factor(const double* dia, const double* off, const double* lam, int M,
 
 template <int LOGN, int MR>
 static int launch_cluster(const CgcArgs& a, const double* sfac, int CL, cudaStream_t st) {
-  constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
-  constexpr int NPASS = (NF + CL_FPASS - 1) / CL_FPASS;
-  constexpr int FP = (NF + NPASS - 1) / NPASS;
-  const int nt = ((FP * CL_LANES + 31) / 32) * 32;
-  constexpr int N2 = N / (1 << ((LOGN + 1) / 2));
-  if (nt * 2 < N2 * HC) return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: FFT pass-2 tasks exceed 2 rounds");
-  const size_t smem = (size_t)N * HC * sizeof(Cplx) + (size_t)N * RB * sizeof(double) + (RB + 2) * sizeof(double) +
-                      (N + 4 * NF) * sizeof(Cplx) + 10 * sizeof(double);
+  using K = ClShape<LOGN, MR>;
+  constexpr int N2 = K::N / (1 << ((LOGN + 1) / 2));
+  static_assert(K::NT * 2 >= N2 * K::HC, "cgc_cluster: FFT pass-2 tasks exceed 2 rounds");
   auto kern = cgc_cluster_kernel<LOGN, MR>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.M * CL), 1, 1);
-  cfg.blockDim = dim3((unsigned)nt, 1, 1);
-  cfg.dynamicSmemBytes = smem;
+  cfg.blockDim = dim3((unsigned)K::NT, 1, 1);
+  cfg.dynamicSmemBytes = K::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;

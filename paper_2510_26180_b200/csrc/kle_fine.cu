@@ -94,8 +94,14 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 // the operator diagonals, all fetched with cp.async before the sweep.
 template <int MR, int P, int NC>
 struct FgrSmem {
+  // rows are XOR-swizzled within their MR-row chunk (pidx), so that the P
+  // lanes of a system (stride MR rows) hit distinct banks; a permutation of
+  // each chunk, so no padding (ee needs one extra chunk for row nx)
   static constexpr int NXP = MR * P;
-  static constexpr size_t BYTES = ((size_t)(NC + 3) * NXP + 8) * sizeof(double);
+  static constexpr int LD = NXP;
+  static constexpr int SWZ = (MR < 16 ? MR : 16) - 1;
+  __device__ __forceinline__ static int pidx(int row) { return row ^ ((row / MR) & SWZ); }
+  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8) * sizeof(double);
 };
 
 template <int MR, int P, int R, int NT, bool PIPE>
@@ -119,23 +125,25 @@ __global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs 
   double x[R][MR];
   if (a.F_given == nullptr) {
     extern __shared__ __align__(16) double sm[];
-    double* st = sm;               // [NC][NXP]
-    double* p0 = st + NC * NXP;    // [NXP]
-    double* dd = p0 + NXP;         // [NXP]
-    double* ee = dd + NXP;         // [NXP + 1]: ee[i] couples rows i-1 and i
+    using SM = FgrSmem<MR, P, NC>;
+    constexpr int LD = SM::LD;
+    double* st = sm;              // [NC][LD]
+    double* p0 = st + NC * LD;    // [LD]
+    double* dd = p0 + LD;         // [LD]
+    double* ee = dd + LD;         // [LD + MR]: ee[pidx(i)] couples rows i-1 and i
     for (int e = tid; e < NC * nx; e += NT) {
       const int ln = e / nx, row = e - ln * nx, n = n0 + ln;
-      if (n < N) cp_async8(st + ln * NXP + row, (n == 0) ? a.u0 + row : a.U + sbase + (size_t)(n - 1) * nx + row);
+      if (n < N) cp_async8(st + ln * LD + SM::pidx(row), (n == 0) ? a.u0 + row : a.U + sbase + (size_t)(n - 1) * nx + row);
     }
     if (n0 == 0)
-      for (int row = tid; row < nx; row += NT) cp_async8(p0 + row, a.U + sbase + (size_t)(N - 1) * nx + row);
+      for (int row = tid; row < nx; row += NT) cp_async8(p0 + SM::pidx(row), a.U + sbase + (size_t)(N - 1) * nx + row);
     for (int row = tid; row < nx; row += NT) {
-      cp_async8(dd + row, a.dia + (size_t)s * nx + row);
-      if (row + 1 < nx) cp_async8(ee + row + 1, a.off + (size_t)s * nx + row);
+      cp_async8(dd + SM::pidx(row), a.dia + (size_t)s * nx + row);
+      if (row + 1 < nx) cp_async8(ee + SM::pidx(row + 1), a.off + (size_t)s * nx + row);
     }
     if (tid == 0) {
       ee[0] = 0.0;
-      ee[nx] = 0.0;
+      ee[SM::pidx(nx)] = 0.0;
     }
     LaneFactors<MR, P> fac;
     fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs 
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
         const int row = k * MR + j;
-        x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * NXP + row] + hg : 0.0;
+        x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * LD + SM::pidx(row)] + hg : 0.0;
       }
     if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
@@ -172,7 +180,7 @@ __global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs 
       const int n = n0 + nl[r];
       if (n >= N) continue;
       const double sc = a.scaling[n];
-      const double* pv = (n == 0) ? p0 : st + nl[r] * NXP;
+      const double* pv = (n == 0) ? p0 : st + nl[r] * LD;
       const double pmul = (n == 0) ? a.alpha : 1.0;
       double* out = a.Rout + sbase + (size_t)n * nx;
 #pragma unroll
@@ -181,8 +189,9 @@ __global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs 
         if (row >= nx) continue;
         const double xm = (j > 0) ? x[r][j - 1] : (k > 0 ? left : 0.0);
         const double xp = (j < MR - 1) ? x[r][j + 1] : (k < P - 1 ? right : 0.0);
-        const double Ax = fma(ee[row], xm, fma(dd[row], x[r][j], ee[row + 1] * xp));
-        const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[row];
+        const int pr = SM::pidx(row);
+        const double Ax = fma(ee[pr], xm, fma(dd[pr], x[r][j], ee[SM::pidx(row + 1)] * xp));
+        const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[pr];
         out[row] = sc * rhs;
       }
     }

@@ -1,5 +1,5 @@
 """Launch the hot kernels on config-2 shapes for ncu capture.
-usage: python tools/prof_kernels.py [M] [which: fgr,cgc,cgcfly,gemm]"""
+usage: python tools/prof_kernels.py [M] [which: fgr,cgc,cgcfly,gemm] [nx,N,J]"""
 import sys
 sys.path.insert(0, ".")
 import numpy as np
@@ -10,7 +10,7 @@ from paper_2510_26180_b200.pcgc import build_alpha_circulant, shift_factors
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["fgr", "cgc"]
-nx, N, J = 511, 64, 64
+nx, N, J = (int(v) for v in (sys.argv[3].split(",") if len(sys.argv) > 3 else (511, 64, 64)))
 model = LogNormalKL1D(nx=nx, d=8)
 grid = make_time_grid(1.0, N, J)
 xi = np.random.default_rng(0).normal(size=(M, 8))
