@@ -16,6 +16,10 @@
 #include "kle_fine.cuh"
 #include "kle_internal.h"
 
+#ifndef KLE_FINE_LAZY
+#define KLE_FINE_LAZY 0  // lazy-stitch step (kle_fine.cuh); measured slower, kept for A/B
+#endif
+
 namespace kle {
 
 // ---------------------------------------------------------------------------
@@ -77,6 +81,33 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
       b[L::BB_OFF + t * P + k] = bb;
     }
   }
+  // lazy-stitch vectors per chunk (be_steps_lazy)
+  for (int k = 0; k < P; ++k) {
+    const double* l = b + L::L_OFF + k * MR;
+    const double* inv = b + L::INV_OFF + k * MR;
+    double* phi = b + L::PHI_OFF + k * MR;
+    double* phi2 = b + L::PHI2_OFF + k * MR;
+    double* sg = b + L::SG_OFF + k * MR;
+    double* sg2 = b + L::SG2_OFF + k * MR;
+    const double lnx = (k + 1 < P) ? b[L::L_OFF + (k + 1) * MR] : 0.0;
+    double pi = 1.0;
+    for (int j = 0; j < MR; ++j) {
+      pi *= -l[j];
+      phi[j] = pi * inv[j];
+    }
+    for (int j = MR - 2; j >= 0; --j) phi[j] = fma(-l[j + 1], phi[j + 1], phi[j]);
+    double g = 1.0;
+    for (int j = MR - 1; j >= 0; --j) {
+      g *= -((j + 1 < MR) ? l[j + 1] : lnx);
+      sg[j] = g;
+    }
+    phi2[0] = phi[0];
+    sg2[0] = sg[0];
+    for (int j = 1; j < MR; ++j) {
+      phi2[j] = fma(-l[j], phi2[j - 1], phi[j]);
+      sg2[j] = fma(-l[j], sg2[j - 1], sg[j]);
+    }
+  }
   (void)g0;
 }
 
@@ -105,7 +136,12 @@ struct FgrSmem {
 };
 
 template <int MR, int P, int R, int NT, bool PIPE>
-__global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs a) {
+#ifdef KLE_FGR_MINB_ALL  // tuning override
+#define KLE_FGR_MINB(MR, R) KLE_FGR_MINB_ALL
+#else
+#define KLE_FGR_MINB(MR, R) ((MR) * (R) > 32 ? 2 : 3)
+#endif
+__global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a) {
   using L = FineLayout<MR, P>;
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;  // subintervals per CTA
@@ -158,6 +194,7 @@ __global__ void __launch_bounds__(NT, (MR * R > 32 ? 2 : 3)) fgr_kernel(FgrArgs 
         x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * LD + SM::pidx(row)] + hg : 0.0;
       }
     if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
+    else if constexpr (KLE_FINE_LAZY) be_steps_lazy<MR, P, R>(x, fac, a.ffac + (size_t)s * L::DOUBLES, k, a.J, hg);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -263,6 +300,7 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
     }
   for (int g = 0; g < a.nseg; ++g) {
     if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
+    else if constexpr (KLE_FINE_LAZY) be_steps_lazy<MR, P, R>(x, fac, a.fac + (size_t)s * L::DOUBLES, k, a.J, hg);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r) {

@@ -19,7 +19,12 @@ struct FineLayout {
   static constexpr int INV_OFF = NXP;    // 1/beta_r,                 [k][j]
   static constexpr int AF_OFF = 2 * NXP; // forward scan multipliers  [t][k]
   static constexpr int BB_OFF = 2 * NXP + LOGP * P;  // backward scan multipliers
-  static constexpr int DOUBLES = 2 * NXP + 2 * LOGP * P;
+  // lazy-stitch vectors (be_steps_lazy), chunk-major [k][j]
+  static constexpr int PHI_OFF = 2 * NXP + 2 * LOGP * P;  // phi  = Bwd0(pi * inv)
+  static constexpr int PHI2_OFF = PHI_OFF + NXP;          // phi2 = Fwd0(phi)
+  static constexpr int SG_OFF = PHI2_OFF + NXP;           // sg_j = prod_{i=j+1}^{MR} (-l_i)
+  static constexpr int SG2_OFF = SG_OFF + NXP;            // sg2  = Fwd0(sg)
+  static constexpr int DOUBLES = 6 * NXP + 2 * LOGP * P;
 };
 
 // Per-lane register copy of the factor rows it owns.
@@ -78,7 +83,7 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t, P);
-        if (k >= (1 << t)) Y[r] = fma(f.af[t], o, Y[r]);
+        Y[r] = fma(f.af[t], o, Y[r]);  // af = 0 for k < 2^t
       }
     }
 #pragma unroll
@@ -116,7 +121,7 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t, P);
-        if (k + (1 << t) < P) X[r] = fma(f.bb[t], o, X[r]);
+        X[r] = fma(f.bb[t], o, X[r]);  // bb = 0 for k + 2^t >= P
       }
     }
 #pragma unroll
@@ -134,6 +139,195 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
         for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Lazy-stitch form of the same step (default). With chunk-local recurrences
+//   Fwd0(v)_j = v_j - l_j Fwd0(v)_{j-1},  Bwd0(z)_j = z_j - l_{j+1} Bwd0(z)_{j+1}
+// (zero carries) one BE step of the partitioned solve is
+//   x' = Bwd0(Fwd0(x) inv + kap) + Y phi + X sg,   phi = Bwd0(pi inv)
+// with Y, X the forward / backward chunk carries. The state is kept as
+// yl = Fwd0(x), and the next step's forward pass is taken on the carry-free
+// part, Fwd0(x') = Fwd0(xl0) + Y phi2 + X sg2 (phi2 = Fwd0(phi), sg2 = Fwd0(sg)).
+// So neither carry scan waits for a stitch, and each scan runs concurrently
+// with an independent local pass:
+//   forward scan of last(yl)        ||  xl0 = Bwd0(yl inv + kap)
+//   backward scan of xl0_0 + Y phi0 ||  Fwd0(xl0)
+//   yl' = Fwd0(xl0) + Y phi2 + X sg2
+// Five R-dependent FMAs per row and step, as in be_steps; same arithmetic up
+// to the association of the carry terms.
+template <int MR, int P, int R>
+__device__ __forceinline__ void fwd_local(double (&x)[R][MR], const LaneFactors<MR, P>& f) {
+#pragma unroll
+  for (int j = 1; j < MR; ++j)
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void fwd_carry(const double (&x)[R][MR], const LaneFactors<MR, P>& f, int k,
+                                          double (&Y)[R]) {
+  using L = FineLayout<MR, P>;
+#pragma unroll
+  for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+#pragma unroll
+  for (int t = 0; t < L::LOGP; ++t)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t, P);
+      Y[r] = fma(f.af[t], o, Y[r]);  // af = 0 for k < 2^t
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
+    Y[r] = (k == 0) ? 0.0 : o;
+  }
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void bwd_local(double (&x)[R][MR], const LaneFactors<MR, P>& f, double hg) {
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+    const double kap = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double z = fma(x[r][j], f.inv[j], kap);
+      if (j + 1 < MR) z = fma(-ln, x[r][j + 1], z);
+      x[r][j] = z;
+    }
+  }
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void bwd_carry(const double (&x)[R][MR], const double (&Y)[R], double phi0,
+                                          const LaneFactors<MR, P>& f, int k, double (&X)[R]) {
+  using L = FineLayout<MR, P>;
+#pragma unroll
+  for (int r = 0; r < R; ++r) X[r] = fma(Y[r], phi0, x[r][0]);
+#pragma unroll
+  for (int t = 0; t < L::LOGP; ++t)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t, P);
+      X[r] = fma(f.bb[t], o, X[r]);  // bb = 0 for k + 2^t >= P
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
+    X[r] = (k == P - 1) ? 0.0 : o;
+  }
+}
+
+// The scans interleaved into the concurrent local pass in source order (one
+// shuffle round per segment of rows), so that each shuffle's latency is
+// covered by independent row FMAs.
+template <int MR, int P, int R>
+__device__ __forceinline__ void fwdscan_bwdlocal(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, double hg,
+                                                 double (&Y)[R]) {
+  using L = FineLayout<MR, P>;
+  constexpr int LOGP = L::LOGP, NS = LOGP + 1, SEG = (MR + NS - 1) / NS;
+  double o[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    Y[r] = x[r][MR - 1];
+    o[r] = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
+  }
+  auto step = [&](int st) {
+    if (st < LOGP) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        Y[r] = fma(f.af[st], o[r], Y[r]);
+        o[r] = __shfl_up_sync(KLE_FULL_MASK, Y[r], (st + 1 < LOGP) ? (1 << (st + 1)) : 1, P);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) Y[r] = (k == 0) ? 0.0 : o[r];
+    }
+  };
+#pragma unroll
+  for (int jj = 0; jj < MR; ++jj) {
+    const int j = MR - 1 - jj;
+    const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+    const double kap = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double z = fma(x[r][j], f.inv[j], kap);
+      if (j + 1 < MR) z = fma(-ln, x[r][j + 1], z);
+      x[r][j] = z;
+    }
+    if ((jj + 1) % SEG == 0 && (jj + 1) / SEG <= NS) step((jj + 1) / SEG - 1);
+  }
+#pragma unroll
+  for (int st = MR / SEG; st < NS; ++st) step(st);
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void bwdscan_fwdlocal(double (&x)[R][MR], const double (&Y)[R], double phi0,
+                                                 const LaneFactors<MR, P>& f, int k, double (&X)[R]) {
+  using L = FineLayout<MR, P>;
+  constexpr int LOGP = L::LOGP, NS = LOGP + 1, SEG = (MR - 1 + NS - 1) / NS;
+  double o[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    X[r] = fma(Y[r], phi0, x[r][0]);
+    o[r] = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
+  }
+  auto step = [&](int st) {
+    if (st < LOGP) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        X[r] = fma(f.bb[st], o[r], X[r]);
+        o[r] = __shfl_down_sync(KLE_FULL_MASK, X[r], (st + 1 < LOGP) ? (1 << (st + 1)) : 1, P);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) X[r] = (k == P - 1) ? 0.0 : o[r];
+    }
+  };
+#pragma unroll
+  for (int j = 1; j < MR; ++j) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+    if (SEG > 0 && j % SEG == 0 && j / SEG <= NS) step(j / SEG - 1);
+  }
+#pragma unroll
+  for (int st = (SEG > 0 ? (MR - 1) / SEG : 0); st < NS; ++st) step(st);
+}
+
+// x (materialised) -> J steps -> x (materialised). blob: this sample's factor
+// blob (the lazy vectors are read from it; the lane's l/inv/scan multipliers
+// come in f).
+template <int MR, int P, int R>
+__device__ __forceinline__ void be_steps_lazy(double (&x)[R][MR], const LaneFactors<MR, P>& f,
+                                              const double* __restrict__ blob, int k, int J, double hg) {
+  using L = FineLayout<MR, P>;
+  if (J <= 0) return;
+  double phi2[MR], sg2[MR];
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    phi2[j] = blob[L::PHI2_OFF + k * MR + j];
+    sg2[j] = blob[L::SG2_OFF + k * MR + j];
+  }
+  const double phi0 = blob[L::PHI_OFF + k * MR];
+  double Y[R], X[R];
+  fwd_local<MR, P, R>(x, f);
+  for (int it = 0; it < J - 1; ++it) {
+    fwdscan_bwdlocal<MR, P, R>(x, f, k, hg, Y);
+    bwdscan_fwdlocal<MR, P, R>(x, Y, phi0, f, k, X);
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(X[r], sg2[j], fma(Y[r], phi2[j], x[r][j]));
+  }
+  fwdscan_bwdlocal<MR, P, R>(x, f, k, hg, Y);
+  bwd_carry<MR, P, R>(x, Y, phi0, f, k, X);
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const double phi = blob[L::PHI_OFF + k * MR + j], sg = blob[L::SG_OFF + k * MR + j];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r][j] = fma(X[r], sg, fma(Y[r], phi, x[r][j]));
   }
 }
 
@@ -169,7 +363,7 @@ __device__ __forceinline__ void ph_s2(PipeGroup<MR, P, RG>& g, const LaneFactors
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
       const double o = __shfl_up_sync(KLE_FULL_MASK, g.Y[r], 1 << t, P);
-      if (k >= (1 << t)) g.Y[r] = fma(f.af[t], o, g.Y[r]);
+      g.Y[r] = fma(f.af[t], o, g.Y[r]);
     }
 #pragma unroll
   for (int r = 0; r < RG; ++r) {
@@ -210,7 +404,7 @@ __device__ __forceinline__ void ph_s4(PipeGroup<MR, P, RG>& g, const LaneFactors
 #pragma unroll
     for (int r = 0; r < RG; ++r) {
       const double o = __shfl_down_sync(KLE_FULL_MASK, g.X[r], 1 << t, P);
-      if (k + (1 << t) < P) g.X[r] = fma(f.bb[t], o, g.X[r]);
+      g.X[r] = fma(f.bb[t], o, g.X[r]);
     }
 #pragma unroll
   for (int r = 0; r < RG; ++r) {
