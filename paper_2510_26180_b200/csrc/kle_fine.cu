@@ -359,6 +359,7 @@ static const FineVariant kVariants[] = {
     {16, 32, 3, 4, 1}, {16, 32, 3, 3, 1}, {16, 32, 2, 4, 1}, {16, 32, 4, 3, 1},  // 18..21 shared-memory factors
     {8, 16, 2, 4, 1},  {8, 16, 4, 4, 1},  {8, 32, 4, 4, 1},                     // 22..24
     {32, 16, 2, 2, 1}, {32, 16, 1, 3, 1}, {16, 32, 3, 2, 1},                     // 25..27
+    {32, 16, 4, 3, 1}, {32, 16, 3, 3, 1}, {32, 16, 2, 4, 1}, {32, 16, 4, 2, 1},  // 28..31
 };
 static const int kNumDefaults = 6;
 

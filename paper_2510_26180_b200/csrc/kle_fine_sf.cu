@@ -6,8 +6,10 @@
 // R x MR state and the kernel can run 4 CTAs per SM: the carry-scan latency of
 // one warp is hidden behind the row recurrences of the others.
 //
-// Row record (6 doubles, 16-byte aligned pairs), per chunk row j of lane k:
-//   (sig_j, l_j) | (inv_j, pihat_j) | (kap_j, l_{j+1})
+// Row record (6 doubles) per chunk row j of lane k, stored as three planes of
+// 16-byte pairs, [plane][j][k] (consecutive lanes read consecutive pairs; the
+// two P = 16 systems of a warp read the same pair, a broadcast):
+//   plane 0 (sig_j, l_j) | plane 1 (inv_j, pihat_j) | plane 2 (kap_j, l_{j+1})
 // Per step: forward loop x_j += sig_j X (previous back-stitch), yl_j = x_j -
 // l_j yl_{j-1}; forward scan; backward loop z'_j = yl_j inv_j + pihat_j Y +
 // kap_j, xl_j = z'_j - l_{j+1} xl_{j+1}; backward scan. Five FMAs per row.
@@ -24,7 +26,7 @@ struct SfLayout {
   static constexpr int AF_OFF = ROW * NXP;
   static constexpr int BB_OFF = ROW * NXP + LOGP * P;
   static constexpr int DOUBLES = ROW * NXP + 2 * LOGP * P;
-  __host__ __device__ static constexpr int at(int j, int k) { return (j * P + k) * ROW; }
+  __host__ __device__ static constexpr int at(int q, int j, int k) { return ((q * MR + j) * P + k) * 2; }
 };
 
 template <int MR, int P>
@@ -36,7 +38,7 @@ __global__ void sf_factor_kernel(const double* __restrict__ dia, const double* _
   const double* d = dia + (size_t)s * nx;
   const double* e = off + (size_t)s * nx;
   double* b = blob + (size_t)s * L::DOUBLES;
-  auto el = [&](int row, int q) -> double& { return b[L::at(row % MR, row / MR) + q]; };
+  auto el = [&](int row, int q) -> double& { return b[L::at(q / 2, row % MR, row / MR) + (q % 2)]; };
   double beta_prev = 1.0;
   for (int row = 0; row < L::NXP; ++row) {
     double l = 0.0, inv = 1.0;
@@ -94,6 +96,15 @@ __global__ void sf_factor_kernel(const double* __restrict__ dia, const double* _
   }
 }
 
+// Shared-memory pair load through a 32-bit shared address (volatile: kept in
+// program order, never hoisted out of the step loop into registers, which
+// would spill; the row loops issue them a few rows ahead of use).
+__device__ __forceinline__ double2 lds2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 template <int MR, int P, int R>
 __device__ __forceinline__ void sf_steps(double (&x)[R][MR], const double* __restrict__ fac, int k, int J) {
   using L = SfLayout<MR, P>;
@@ -106,10 +117,13 @@ __device__ __forceinline__ void sf_steps(double (&x)[R][MR], const double* __res
   double X[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) X[r] = 0.0;
+  const unsigned fbase0 = (unsigned)__cvta_generic_to_shared(fac) + (unsigned)(k * 2 * sizeof(double));
   for (int it = 0; it < J; ++it) {
+    unsigned fb = fbase0;
+    asm volatile("" : "+r"(fb));
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
-      const double2 sl = *reinterpret_cast<const double2*>(fac + L::at(j, k));
+      const double2 sl = lds2(fb + (unsigned)(L::at(0, j, 0) * sizeof(double)));
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double v = fma(sl.x, X[r], x[r][j]);
@@ -125,7 +139,7 @@ __device__ __forceinline__ void sf_steps(double (&x)[R][MR], const double* __res
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t, P);
-        if (k >= (1 << t)) Y[r] = fma(af[t], o, Y[r]);
+        Y[r] = fma(af[t], o, Y[r]);  // af = 0 for k < 2^t
       }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -134,8 +148,8 @@ __device__ __forceinline__ void sf_steps(double (&x)[R][MR], const double* __res
     }
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
-      const double2 ip = *reinterpret_cast<const double2*>(fac + L::at(j, k) + 2);
-      const double2 kl = *reinterpret_cast<const double2*>(fac + L::at(j, k) + 4);
+      const double2 ip = lds2(fb + (unsigned)(L::at(1, j, 0) * sizeof(double)));
+      const double2 kl = lds2(fb + (unsigned)(L::at(2, j, 0) * sizeof(double)));
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double z = fma(x[r][j], ip.x, fma(ip.y, Y[r], kl.x));
@@ -150,7 +164,7 @@ __device__ __forceinline__ void sf_steps(double (&x)[R][MR], const double* __res
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t, P);
-        if (k + (1 << t) < P) X[r] = fma(bb[t], o, X[r]);
+        X[r] = fma(bb[t], o, X[r]);  // bb = 0 for k + 2^t >= P
       }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -160,7 +174,7 @@ __device__ __forceinline__ void sf_steps(double (&x)[R][MR], const double* __res
   }
 #pragma unroll
   for (int j = 0; j < MR; ++j) {
-    const double sg = fac[L::at(j, k)];
+    const double sg = fac[L::at(0, j, k)];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
   }
@@ -172,9 +186,7 @@ __global__ void __launch_bounds__(NT, MINB) fgr_sf_kernel(FgrArgs a) {
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;
   extern __shared__ __align__(16) double sm[];
-  double* fac = sm;                    // [DOUBLES]
-  double* dd = fac + L::DOUBLES;       // [NXP]
-  double* ee = dd + L::NXP;            // [NXP + 2]: ee[i] couples rows i-1, i
+  double* fac = sm;  // [DOUBLES]
   const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -186,12 +198,7 @@ __global__ void __launch_bounds__(NT, MINB) fgr_sf_kernel(FgrArgs a) {
   {
     const double* gb = a.ffac + (size_t)s * L::DOUBLES;
     for (int i = tid; i < L::DOUBLES / 2; i += NT)
-      reinterpret_cast<double2*>(fac)[i] = reinterpret_cast<const double2*>(gb)[i];
-    for (int row = tid; row < L::NXP; row += NT) {
-      dd[row] = (row < nx) ? a.dia[(size_t)s * nx + row] : 0.0;
-      ee[row + 1] = (row + 1 < nx) ? a.off[(size_t)s * nx + row] : 0.0;
-    }
-    if (tid == 0) ee[0] = 0.0;
+      reinterpret_cast<double2*>(fac)[i] = __ldg(reinterpret_cast<const double2*>(gb) + i);
   }
   int n[R];
 #pragma unroll
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(NT, MINB) fgr_sf_kernel(FgrArgs a) {
     for (int j = 0; j < MR; ++j) {
       const int row = k * MR + j;
       double v = 0.0;
-      if (row < nx && n[r] < N) v = ((n[r] == 0) ? a.u0[row] : U[sbase + (size_t)(n[r] - 1) * nx + row]) + hg;
+      if (row < nx && n[r] < N) v = __ldg((n[r] == 0) ? a.u0 + row : U + sbase + (size_t)(n[r] - 1) * nx + row) + hg;
       x[r][j] = v;
     }
   __syncthreads();
@@ -213,30 +220,42 @@ __global__ void __launch_bounds__(NT, MINB) fgr_sf_kernel(FgrArgs a) {
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int j = 0; j < MR; ++j) x[r][j] = (k * MR + j < nx) ? x[r][j] - hg : 0.0;
-  // epilogue: R_n = scaling_n ((I + dT A) F_n - prev_n); prev rows re-read (L2)
+  // epilogue: R_n = scaling_n ((I + dT A) F_n - prev_n); operator rows and the
+  // prev rows re-read through the read-only path (L2-resident), in batches of
+  // EB rows to bound the live registers
+  constexpr int EB = MR < 8 ? MR : 8;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const double left = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
     const double right = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
     if (n[r] >= N) continue;
     const double sc = a.scaling[n[r]];
-    const size_t prow = (n[r] == 0) ? sbase + (size_t)(N - 1) * nx : sbase + (size_t)(n[r] - 1) * nx;
+    const double* pvr = U + ((n[r] == 0) ? sbase + (size_t)(N - 1) * nx : sbase + (size_t)(n[r] - 1) * nx);
+    const double* dia = a.dia + (size_t)s * nx;
+    const double* off = a.off + (size_t)s * nx;
     const double pmul = (n[r] == 0) ? a.alpha : 1.0;
-    double pv[MR];
 #pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      const int row = k * MR + j;
-      pv[j] = (row < nx) ? U[prow + row] : 0.0;
-    }
+    for (int j0 = 0; j0 < MR; j0 += EB) {
+      double pv[EB], dd[EB], ee[EB + 1];
 #pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      const int row = k * MR + j;
-      if (row >= nx) continue;
-      const double xm = (j > 0) ? x[r][j - 1] : left;
-      const double xp = (j < MR - 1) ? x[r][j + 1] : right;
-      const double Ax = fma(ee[row], xm, fma(dd[row], x[r][j], ee[row + 1] * xp));
-      const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[j];
-      Rout[sbase + (size_t)n[r] * nx + row] = sc * rhs;
+      for (int jj = 0; jj <= EB; ++jj) {
+        const int row = k * MR + j0 + jj;
+        if (jj < EB) {
+          pv[jj] = (row < nx) ? __ldg(pvr + row) : 0.0;
+          dd[jj] = (row < nx) ? __ldg(dia + row) : 0.0;
+        }
+        ee[jj] = (row >= 1 && row < nx) ? __ldg(off + row - 1) : 0.0;  // couples rows row-1, row
+      }
+#pragma unroll
+      for (int jj = 0; jj < EB; ++jj) {
+        const int j = j0 + jj, row = k * MR + j;
+        if (row >= nx) continue;
+        const double xm = (j > 0) ? x[r][j - 1] : left;
+        const double xp = (j < MR - 1) ? x[r][j + 1] : right;
+        const double Ax = fma(ee[jj], xm, fma(dd[jj], x[r][j], ee[jj + 1] * xp));
+        const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[jj];
+        Rout[sbase + (size_t)n[r] * nx + row] = sc * rhs;
+      }
     }
   }
 }
@@ -297,7 +316,7 @@ struct SfInst {
   static int fgr(const FgrArgs& a, cudaStream_t st) {
     using L = SfLayout<MR, P>;
     if (a.F_given) return set_error(KLE_ERR_UNSUPPORTED, "sf fgr: F_given uses the register variant");
-    const size_t smem = ((size_t)L::DOUBLES + 2 * L::NXP + 2) * sizeof(double);
+    const size_t smem = (size_t)L::DOUBLES * sizeof(double);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(fgr_sf_kernel<MR, P, R, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -333,7 +352,11 @@ struct SfInst {
   KLE_SF_DISPATCH(8, 32, 4, 4, CALL)      \
   KLE_SF_DISPATCH(32, 16, 2, 2, CALL)     \
   KLE_SF_DISPATCH(32, 16, 1, 3, CALL)     \
-  KLE_SF_DISPATCH(16, 32, 3, 2, CALL)
+  KLE_SF_DISPATCH(16, 32, 3, 2, CALL)     \
+  KLE_SF_DISPATCH(32, 16, 4, 3, CALL)     \
+  KLE_SF_DISPATCH(32, 16, 3, 3, CALL)     \
+  KLE_SF_DISPATCH(32, 16, 2, 4, CALL)     \
+  KLE_SF_DISPATCH(32, 16, 4, 2, CALL)
 
 int sf_blob_doubles(int MR, int P) {
   int logp = 0;

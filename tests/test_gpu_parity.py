@@ -471,3 +471,31 @@ def test_degenerate_shapes(cuda, nx, N, J):
     out = batched.pcgc(dia, off, model.initial_condition(), init, N, J, 1.0, 0.1, 1e-10, 40)
     np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
     assert rel(res.states.cpu().numpy(), out["states"]) <= RTOL
+
+
+@pytest.mark.parametrize("variant", [4, 6, 13, 16, 18, 25, 27])
+def test_fine_variants_match_oracle(cuda, golden, monkeypatch, variant):
+    """Every tuning layout of the fine solver (register / pipelined / shared-memory
+    factors, KLE_FINE_VARIANT) gives the same sweep and the same PCGC iterates."""
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    monkeypatch.setenv("KLE_FINE_VARIANT", str(variant))
+    rng = np.random.default_rng(variant)
+    model = LogNormalKL1D(nx=511, d=8)
+    xi = rng.normal(size=(3, 8))
+    op = DeviceOperator.from_model(model, xi)
+    starts = rng.normal(size=(3, 5, 511))
+    h, J = 1.0 / 64 / 64, 64
+    got = op.sweep(to_dev(starts), h, J)[:, :, 0].cpu().numpy()
+    dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+    assert rel(got, batched.be_steps(dia, off, starts, h, 1.0, J)) <= 1e-12
+    g = golden("c2")
+    grid = make_time_grid(1.0, 64, 64)
+    op = DeviceOperator.from_model(model, g["xi"])
+    res = pcgc_solve_device(op, coarse_sweep_init_batched(op, grid).contiguous(), grid,
+                            SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60))
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), g["iters"])
+    assert rel(res.states.cpu().numpy(), g["final"]) <= RTOL
