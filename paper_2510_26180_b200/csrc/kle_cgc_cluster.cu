@@ -41,6 +41,23 @@ namespace cg = cooperative_groups;
 
 namespace kle {
 
+#ifdef KLE_CGC_TIMING
+// debug: per-CTA phase timestamps (globaltimer ns), first 4096 CTAs
+__device__ unsigned long long g_cgc_t[4096][10];
+#define CGC_T(i)                                                                          \
+  do {                                                                                    \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                          \
+      unsigned long long t_;                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+      g_cgc_t[blockIdx.x][i] = t_;                                                        \
+    }                                                                                     \
+  } while (0)
+#else
+#define CGC_T(i) \
+  do {           \
+  } while (0)
+#endif
+
 constexpr int CL_LANES = 8;
 
 __device__ __forceinline__ Cplx cfma(Cplx a, Cplx b, Cplx c) {  // a*b + c
@@ -272,6 +289,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   const int tid = threadIdx.x;
   const size_t sb = (size_t)s * N * nx;
   const int row0 = c * RB;
+  CGC_T(0);
   // ---- phase 0: prefetch --------------------------------------------------
   if constexpr (NSTEP > 0) {  // each thread keeps one column; rows n = tid/RB + m*NSTEP
     if (tid < NSTEP * RB) {
@@ -317,6 +335,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   load_pivots<MR>(ib, ibprev, reinterpret_cast<const Cplx*>(sfac_d) + ((size_t)s * NF + f) * nx, r0, nx);
   cp_async_wait_all();
   __syncthreads();
+  CGC_T(1);
   if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
     for (int e = tid; e < N * RB; e += NT) {
       const int n = e / RB, col = e % RB;
@@ -325,6 +344,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     __syncthreads();
   }
   fft4step<LOGN, HC, -1, MR>(tile, tw);
+  CGC_T(2);
 
   // ---- one frequency per 8-lane group: (lambda_f I + dT A) q = p_f ---------
   const double hs = 0.5 / sqrt((double)N);  // two-for-one unpacking x 1/sqrt(N)
@@ -369,7 +389,9 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     fwd[2 * f] = A;
     fwd[2 * f + 1] = B;
   }
+  CGC_T(3);
   cluster.sync();
+  CGC_T(4);
   Cplx Yc;
   {  // composite of the blocks q < c, q = k (+ 8) per lane, then a lane butterfly
     Cplx A0 = {1.0, 0.0}, B0 = {0.0, 0.0}, A1 = {1.0, 0.0}, B1 = {0.0, 0.0};
@@ -423,7 +445,9 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     bwd[2 * f] = S;
     bwd[2 * f + 1] = T;
   }
+  CGC_T(5);
   cluster.sync();  // also: every thread has read its inputs from the tile
+  CGC_T(6);
   Cplx Xc;
   {  // composite of the blocks q > c (the nearest block applied last)
     Cplx A0 = {1.0, 0.0}, B0 = {0.0, 0.0}, A1 = {1.0, 0.0}, B1 = {0.0, 0.0};
@@ -465,6 +489,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   }
   __syncthreads();
   fft4step<LOGN, HC, +1, MR>(tile, tw);
+  CGC_T(7);
   // ---- update ----------------------------------------------------------------
   const double rsN = 1.0 / sqrt((double)N);
   double incmax = 0.0;
@@ -494,6 +519,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     }
   }
   if (__syncthreads_or(bad)) incmax = __longlong_as_double(0x7ff8000000000000LL);
+  CGC_T(8);
   incmax = warp_max(incmax);
   const int lane = tid & 31, w = tid >> 5;
   constexpr int NW = NT / 32;
@@ -531,6 +557,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   // every CTA arrived (after its last DSMEM read) before the pack; wait here
   // so no CTA's shared memory disappears under a remote reader
   asm volatile("barrier.cluster.wait;\n" ::: "memory");
+  CGC_T(9);
 }
 
 // ---------------------------------------------------------------------------
@@ -607,6 +634,12 @@ static int dispatch_logn(int logn, const CgcArgs& a, const double* sfac, int CL,
   }
   return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: N");
 }
+
+#ifdef KLE_CGC_TIMING
+extern "C" int kle_debug_cgc_timing(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_cgc_t, sizeof(g_cgc_t));
+}
+#endif
 
 int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st) {
   int MR, CL, LOGN;

@@ -318,10 +318,13 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
 // ---------------------------------------------------------------------------
 // host-side dispatch
 // ---------------------------------------------------------------------------
-template <int MR, int P, int R_, bool PIPE = false>
+// PI: 0 = eager step, 128 threads; 1 = software-pipelined step; 2 = eager, 64
+// threads (finer CTA granularity: R = 3 wastes 2/66 instead of 8/72 slots at N = 64)
+template <int MR, int P, int R_, int PI = 0>
 struct FineInst {
+  static constexpr bool PIPE = PI == 1;
   static constexpr int R = R_;
-  static constexpr int NT = 128;
+  static constexpr int NT = PI == 2 ? 64 : 128;
   static constexpr int NC = (NT / 32) * (32 / P) * R;
 
   static int factor(const double* dia, const double* off, double* blob, int M, int nx, double h,
@@ -353,13 +356,14 @@ struct FineVariant {
   int MR, P, R, pipe, kind = 0;  // kind 1 (shared-memory factors): `pipe` is the min CTAs/SM bound
 };
 static const FineVariant kVariants[] = {
-    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {8, 16, 2, 0},  {16, 32, 3, 0}, {32, 32, 2, 0},  // defaults
+    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {8, 16, 2, 0},  {16, 32, 3, 2}, {32, 32, 2, 0},  // defaults
     {8, 16, 2, 1},  {4, 32, 4, 0},  {8, 16, 4, 1},  {8, 16, 4, 0},  {16, 16, 2, 0}, {8, 32, 4, 0},
     {32, 16, 2, 0}, {16, 32, 2, 0}, {16, 32, 2, 1}, {16, 32, 4, 1}, {16, 32, 4, 0}, {4, 32, 4, 1},
     {16, 32, 3, 4, 1}, {16, 32, 3, 3, 1}, {16, 32, 2, 4, 1}, {16, 32, 4, 3, 1},  // 18..21 shared-memory factors
     {8, 16, 2, 4, 1},  {8, 16, 4, 4, 1},  {8, 32, 4, 4, 1},                     // 22..24
     {32, 16, 2, 2, 1}, {32, 16, 1, 3, 1}, {16, 32, 3, 2, 1},                     // 25..27
     {32, 16, 4, 3, 1}, {32, 16, 3, 3, 1}, {32, 16, 2, 4, 1}, {32, 16, 4, 2, 1},  // 28..31
+    {16, 32, 3, 0}, {8, 16, 2, 2}, {16, 32, 2, 2},                                // 32..34
 };
 static const int kNumDefaults = 6;
 
@@ -372,6 +376,9 @@ static const int kNumDefaults = 6;
   KLE_FINE_DISPATCH(4, 16, 4, 0, CALL)    \
   KLE_FINE_DISPATCH(8, 16, 2, 0, CALL)    \
   KLE_FINE_DISPATCH(16, 32, 3, 0, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 3, 2, CALL)   \
+  KLE_FINE_DISPATCH(8, 16, 2, 2, CALL)    \
+  KLE_FINE_DISPATCH(16, 32, 2, 2, CALL)   \
   KLE_FINE_DISPATCH(32, 32, 2, 0, CALL)   \
   KLE_FINE_DISPATCH(8, 16, 2, 1, CALL)    \
   KLE_FINE_DISPATCH(16, 32, 2, 1, CALL)   \
