@@ -159,6 +159,64 @@ int kle_col_sum_f64(const double* U, int M, int L, const double* center, double*
 /* out = a*x + b*y (n elements). */
 int kle_axpby_f64(const double* x, const double* y, double* out, double a, double b, size_t n, void* stream);
 
+
+/* ===================== 2D 5-point path (BASELINE config 3) ==================
+ * DOF order x fastest on an n x n interior grid (nx = n*n <= 127*127); the
+ * operator is A = 5-point(dia, ex, ey): ex[i] = A[i][i+1], ey[i] = A[i][i+n]
+ * (zero across the grid edge). Implicit solves are direct, like the
+ * reference's SuperLU: banded L D L^T without pivoting, factored once per
+ * solve and reused by every outer iteration. */
+
+/* LinearModel.linear_system of the 2D KL plugin (pintuq/models.py:114-116;
+ * models.LogNormalKL2D): xi[M][d] -> dia/ex/ey[M][n*n]. kl_table [d][(n+1)^2]. */
+int kle_2d_kl5pt_f64(const double* xi, int M, int d, const double* kl_table, int n, double inv_h2, double* dia,
+                     double* ex, double* ey, void* stream);
+
+/* _linear_factor (pintuq/propagators.py:25-34) and factor_shifted
+ * (pintuq/pcgc.py:137-145) for bandwidth n. lam == NULL: B = shift*I + c*A,
+ * real, one matrix per sample: Lrow[M][nx][n] (L(i, i-n+t); caller zeroes it),
+ * Lt[M][nx][n] (L(i+1+t, i)), Dinv[M][nx]. lam != NULL (NF interleaved complex
+ * shifts): B = lam_f*I + c*A, complex, M*NF matrices, Lt[M*NF][nx][n] and
+ * Dinv[M*NF][nx] as interleaved complex; Lrow unused. */
+int kle_2d_factor_f64(const double* dia, const double* ex, const double* ey, int M, int n, const double* lam,
+                      int NF, double shift, double c, double* Lrow, double* Lt, double* Dinv, void* stream);
+
+/* Scratch (doubles) of kle_2d_fgr_f64 / kle_2d_sweep_f64 for M samples of N
+ * (or Q) right-hand sides. */
+size_t kle_2d_fine_work_doubles(int M, int N, int n);
+
+/* propagate_fine for all subintervals + assemble_rhs_blocks + the rhs of
+ * cgc_correct (pintuq/propagators.py:121-145, pcgc.py:175-197, 233-237):
+ * Rout[s][k] = scaling_k ((I + dT A) F_k - prev_k), F_k = J BE steps of dt from
+ * U_{k-1} (u0 for k = 0), prev_0 = alpha U_{N-1}. Real factor of I + dt A.
+ * F_given != NULL (stand-alone cgc_correct): no sweep, F_k = F_given[s][k]. */
+int kle_2d_fgr_f64(const double* U, const double* u0, const double* F_given, const double* dia, const double* ex,
+                   const double* ey, const double* Lrow, const double* Lt, const double* Dinv, const double* scaling,
+                   const int32_t* active, int M, int N, int n, int J, double dt, double dT, double g0,
+                   double alpha, double* work, size_t work_doubles, double* Rout, void* stream);
+
+/* propagate_fine / propagate_coarse / fine_reference (pintuq/propagators.py
+ * :121-176): out[s][q][g] = F^{(g+1)}(start[s][q]), segments of J steps of h. */
+int kle_2d_sweep_f64(const double* start, const double* dia, const double* ex, const double* ey,
+                     const double* Lrow, const double* Lt, const double* Dinv, int M, int Q, int n, int J,
+                     int nseg, double h, double g0, double* work, size_t work_doubles, double* out, void* stream);
+
+/* Scratch (doubles) of kle_2d_cgc_f64. */
+size_t kle_2d_cgc_work_doubles(int M, int N, int n);
+
+/* three_step_solve (pintuq/pcgc.py:148-172) + the increment / stop test of
+ * pcgc_solve (:335-348), N even: p = fft(r)/sqrt(N), q_f = B_f^{-1} p_f for
+ * f <= N/2 (complex factors from kle_2d_factor_f64), u = Re ifft(q) sqrt(N)^-1
+ * / scaling. R is alpha-scaled unless load_scale (stand-alone mode). With
+ * status != NULL and Uout == NULL, U is updated in place and the per-sample
+ * increment, status words, iteration counts and active count are written as
+ * in kle_cgc_update_f64; otherwise u goes to Uout (imag residue is 0: the
+ * Hermitian completion makes u real by construction). */
+int kle_2d_cgc_f64(const double* R, const double* load_scale, double* U, double* Uout, const double* Lt,
+                   const double* Dinv, const double* inv_scaling, int M, int N, int n, int k, int max_iters,
+                   double tol, int32_t* status, int32_t* iters, double* inc, double* inc_hist,
+                   int32_t* active_count, double* work, size_t work_doubles, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,9 +6,10 @@ so its output equals the reference's bit-for-bit (checked against the golden
 vectors generated from the unmodified reference: tests/golden/make_golden.py).
 
 Inputs are plain arrays: a sample is described by its tridiagonal operator
-``(dia, off)`` (A = tridiag(off, dia, off)) and a constant source vector ``g``
-(the linear_system contract, ``pintuq/models.py:114-116``, specialised to the
-time-independent sources of the BASELINE models).
+``(dia, off)`` (A = tridiag(off, dia, off)), or the 2D 5-point stencil
+``(dia, ex, ey)`` (``SampleOperator.from_stencil2d``), and a constant source
+vector ``g`` (the linear_system contract, ``pintuq/models.py:114-116``,
+specialised to the time-independent sources of the BASELINE models).
 """
 from __future__ import annotations
 
@@ -24,11 +25,18 @@ class SampleOperator:
     """A, g and the cached SuperLU factors of (I + h A) for one sample
     (``pintuq/propagators.py:17-34`` caches per (sample, step))."""
 
-    def __init__(self, dia, off, g):
-        self.nx = len(dia)
-        self.A = sp.diags([off, dia, off], [-1, 0, 1], format="csc")
+    def __init__(self, dia, off, g, A=None):
+        self.nx = len(dia) if A is None else A.shape[0]
+        self.A = sp.diags([off, dia, off], [-1, 0, 1], format="csc") if A is None else sp.csc_matrix(A)
         self.g = np.asarray(g, dtype=float)
         self._lu = {}
+
+    @classmethod
+    def from_stencil2d(cls, dia, ex, ey, n, g):
+        """2D 5-point operator (LogNormalKL2D.stencil layout): the wider-band
+        sample of the same plugin contract."""
+        A = sp.diags([ey[:-n], ex[:-1], dia, ex[:-1], ey[:-n]], [-n, -1, 0, 1, n], format="csc")
+        return cls(None, None, g, A=A)
 
     def lu(self, h):
         key = float(h)
@@ -70,6 +78,12 @@ def shifted_solvers(op: SampleOperator, lam, dT: float):
     if nx == 1:
         jval = complex(J[0, 0])
         return [lambda p, d=(l - dT * jval): p / d for l in lam]
+    coo = J.tocoo()
+    if int(np.max(np.abs(coo.row - coo.col))) > 1:
+        # wider band (2D): one complex SuperLU per eigenvalue (pcgc.py:137-145)
+        eye = sp.eye(nx, format="csc", dtype=complex)
+        shift = (dT * J.tocsc()).astype(complex)
+        return [spla.splu((l * eye - shift).tocsc()).solve for l in lam]
     sub = -dT * J.diagonal(-1)
     dia = dT * J.diagonal(0)
     sup = -dT * J.diagonal(1)

@@ -1,0 +1,621 @@
+// 2D (5-point) path of the KLE-CGC hot path: BASELINE config 3.
+//
+// Reference counterparts (the same plugin surface as the 1D path):
+//   LinearModel.linear_system     pintuq/models.py:114-116  (2D plugin: models.LogNormalKL2D)
+//   _linear_factor / BE step      pintuq/propagators.py:25-39  (SuperLU of I + dt A)
+//   propagate_fine / _coarse      pintuq/propagators.py:121-157
+//   assemble_rhs_blocks, rhs      pintuq/pcgc.py:175-197, 233-237
+//   factor_shifted (SuperLU / lambda, bandwidth > 1)  pintuq/pcgc.py:137-145
+//   three_step_solve              pintuq/pcgc.py:148-172
+//   pcgc_solve increment / stop   pintuq/pcgc.py:335-348
+//
+// The 5-point operator of an n x n grid (x fastest) has bandwidth n. Like the
+// reference (SuperLU), every implicit solve is direct: each sample's
+// T = I + dt A and the N/2+1 distinct shifted matrices B_f = lambda_f I + dT A
+// (B_{N-f} = conj B_f) are factored once per solve as banded L D L^T without
+// pivoting (T is SPD; B_f is complex symmetric with SPD real part, so no-pivot
+// LDL^T is stable) and reused by every outer iteration.
+//
+// Kernels:
+//   kl5pt_kernel       xi -> (dia, ex, ey) of A (cell-centre log a, face averages)
+//   band_factor_kernel one CTA per matrix: right-looking band LDL^T with the
+//                      (n+1) x (n+1) active window distributed over the CTA
+//                      (entry (row slot, diagonal offset) per thread, real parts
+//                      in shared memory, imaginary parts in registers); writes
+//                      L by columns (Lt, backward solves / column-form forward)
+//                      and, for the real factor, by rows (Lrow, dot-form forward)
+//   fine2d_kernel      one warp per (sample, 32 subintervals): J BE steps on 32
+//                      right-hand sides in the lanes (dot-form banded solves, the
+//                      last n solved rows in a shared-memory window), then the
+//                      CGC right-hand side rhs_n = scaling_n ((I + dT A) F_n - prev_n)
+//   dft_fwd_kernel     per (sample, DOF): p_f = fft(r)_f / sqrt(N), f <= N/2
+//   band_solve_cplx    one warp per (sample, f): B_f q = p (column-form forward
+//                      with a pending-update window, dot-form backward)
+//   dft_inv_update     per (sample, DOF): u = Re ifft(q) / sqrt(N) / scaling
+//                      (Hermitian completion), increment vs U, write U
+//   status2d_kernel    per sample: stop test, status words, active count
+#include <cmath>
+
+#include "kle_common.cuh"
+#include "kle_internal.h"
+
+namespace kle {
+
+// ---------------------------------------------------------------------------
+// scalar helpers for the real / complex instantiations
+// ---------------------------------------------------------------------------
+template <bool C>
+struct Sc;
+template <>
+struct Sc<false> {
+  using T = double;
+  __device__ static T mk(double r, double) { return r; }
+  __device__ static T mul(T a, T b) { return a * b; }
+  __device__ static T fms(T a, T b, T c) { return fma(-a, b, c); }  // c - a b
+  __device__ static T fma_(T a, T b, T c) { return fma(a, b, c); }
+  __device__ static T rcp(T a) { return 1.0 / a; }
+  __device__ static T sub(T a, T b) { return a - b; }
+  __device__ static T zero() { return 0.0; }
+  __device__ static double re(T a) { return a; }
+  __device__ static double im(T) { return 0.0; }
+  __device__ static T shfl_xor(T a, int o) { return __shfl_xor_sync(KLE_FULL_MASK, a, o); }
+  __device__ static T add(T a, T b) { return a + b; }
+};
+template <>
+struct Sc<true> {
+  using T = Cplx;
+  __device__ static T mk(double r, double i) { return {r, i}; }
+  __device__ static T mul(T a, T b) { return cmul(a, b); }
+  __device__ static T fms(T a, T b, T c) {
+    return {fma(-a.re, b.re, fma(a.im, b.im, c.re)), fma(-a.re, b.im, fma(-a.im, b.re, c.im))};
+  }
+  __device__ static T fma_(T a, T b, T c) {
+    return {fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))};
+  }
+  __device__ static T rcp(T a) { return crcp(a); }
+  __device__ static T sub(T a, T b) { return {a.re - b.re, a.im - b.im}; }
+  __device__ static T zero() { return {0.0, 0.0}; }
+  __device__ static double re(T a) { return a.re; }
+  __device__ static double im(T a) { return a.im; }
+  __device__ static T shfl_xor(T a, int o) {
+    return {__shfl_xor_sync(KLE_FULL_MASK, a.re, o), __shfl_xor_sync(KLE_FULL_MASK, a.im, o)};
+  }
+  __device__ static T add(T a, T b) { return {a.re + b.re, a.im + b.im}; }
+};
+
+// ---------------------------------------------------------------------------
+// xi -> 5-point stencil. log a at the cell centres (p + 1/2, r + 1/2) h,
+// p, r = 0..n, is kl_table^T xi (table [d][(n+1)^2], index r (n+1) + p);
+// face coefficients are the averages of the two centres a face separates
+// (models.LogNormalKL2D.stencil, same association of the sums).
+// ---------------------------------------------------------------------------
+__global__ void kl5pt_kernel(const double* __restrict__ xi, int M, int d, const double* __restrict__ table,
+                             int n, double inv_h2, double* __restrict__ dia, double* __restrict__ ex,
+                             double* __restrict__ ey) {
+  const int nx = n * n, nc = n + 1;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)M * nx) return;
+  const int s = (int)(t / nx), idx = (int)(t - (long long)s * nx);
+  const int i = idx % n + 1, j = idx / n + 1;  // node (i h, j h)
+  const double* v = xi + (size_t)s * d;
+  auto a_at = [&](int p, int r) {
+    const double* col = table + (size_t)r * nc + p;
+    double acc = 0.0;
+    for (int q = 0; q < d; ++q) acc = fma(col[(size_t)q * nc * nc], v[q], acc);
+    return exp(acc);
+  };
+  const double a00 = a_at(i - 1, j - 1), a10 = a_at(i, j - 1), a01 = a_at(i - 1, j), a11 = a_at(i, j);
+  const double axl = 0.5 * (a00 + a01), axr = 0.5 * (a10 + a11);
+  const double ayd = 0.5 * (a00 + a10), ayu = 0.5 * (a01 + a11);
+  const size_t o = (size_t)s * nx + idx;
+  dia[o] = (((axl + axr) + ayd) + ayu) * inv_h2;
+  ex[o] = (i < n) ? -axr * inv_h2 : 0.0;
+  ey[o] = (j < n) ? -ayu * inv_h2 : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Banded L D L^T of B = shift I + c A, one CTA (1024 threads) per matrix.
+// Window entry (rho, delta): row r with r = rho (mod n+1), r in [i, i+n], and
+// column r - delta. Thread t owns entries e = t + m * 1024 (rho = e / (n+1),
+// delta = e % (n+1)); real parts in shared memory, imaginary parts in registers.
+// Step i publishes column i (window position j = delta), eliminates, emits
+// Lt[i][t] = L(i+1+t, i), Dinv[i], and loads row i+n+1 into row i's slot.
+// ---------------------------------------------------------------------------
+constexpr int BF_NT = 1024;
+constexpr int BF_E = 16;  // (n+1)^2 <= BF_NT * BF_E  =>  n <= 127
+
+template <bool C>
+__global__ void __launch_bounds__(BF_NT, 1)
+    band_factor_kernel(const double* __restrict__ dia, const double* __restrict__ ex,
+                       const double* __restrict__ ey, int n, const double* __restrict__ lam, int NF,
+                       double shift_re, double c, double* __restrict__ Lrow, double* __restrict__ Lt,
+                       double* __restrict__ Dinv) {
+  using S = Sc<C>;
+  using T = typename S::T;
+  const int nx = n * n, W = n + 1;
+  const int phi = blockIdx.x, s = phi / NF, f = phi - s * NF;
+  const double* d_ = dia + (size_t)s * nx;
+  const double* ex_ = ex + (size_t)s * nx;
+  const double* ey_ = ey + (size_t)s * nx;
+  const T shift = C ? S::mk(lam[2 * f], lam[2 * f + 1]) : S::mk(shift_re, 0.0);
+  extern __shared__ __align__(16) double smem[];
+  double* wre = smem;                              // [BF_E][BF_NT]
+  T* col = reinterpret_cast<T*>(wre + BF_E * BF_NT);  // [2][W]
+  double wim[BF_E];
+  const int tid = threadIdx.x;
+  auto entryB = [&](int r, int delta) -> T {  // B(r, r - delta); identity padding beyond nx
+    if (r >= nx) return delta == 0 ? S::mk(1.0, 0.0) : S::zero();
+    if (r - delta < 0) return S::zero();
+    if (delta == 0) return S::add(shift, S::mk(c * d_[r], 0.0));
+    double v = 0.0;
+    if (delta == 1) v += c * ex_[r - 1];
+    if (delta == n) v += c * ey_[r - n];
+    return S::mk(v, 0.0);
+  };
+  // per entry: (delta << 8) | jpos, jpos = window position of the entry's row at
+  // step i; delta = 255 marks an unused entry (shared memory, to save registers)
+  int* dj = reinterpret_cast<int*>(col + 2 * W) + tid;  // [BF_E][BF_NT] in shared memory
+#pragma unroll
+  for (int m = 0; m < BF_E; ++m) {
+    const int e = tid + m * BF_NT;
+    T v = S::zero();
+    dj[m * BF_NT] = 255 << 8;
+    if (e < W * W) {
+      dj[m * BF_NT] = ((e % W) << 8) | (e / W);  // initial rows 0..n sit in slots 0..n
+      v = entryB(e / W, e % W);
+    }
+    wre[m * BF_NT + tid] = S::re(v);
+    wim[m] = S::im(v);
+  }
+  T* Lt_ = reinterpret_cast<T*>(Lt) + (size_t)phi * nx * n;
+  T* Di_ = reinterpret_cast<T*>(Dinv) + (size_t)phi * nx;
+  double* Lr_ = Lrow ? Lrow + (size_t)phi * nx * n : nullptr;
+  for (int i = 0; i < nx; ++i) {
+    T* cb = col + (i & 1) * W;
+#pragma unroll
+    for (int m = 0; m < BF_E; ++m) {
+      const int delta = dj[m * BF_NT] >> 8, jpos = dj[m * BF_NT] & 255;
+      if (delta == jpos) cb[jpos] = S::mk(wre[m * BF_NT + tid], wim[m]);
+    }
+    __syncthreads();
+    const T dinv = S::rcp(cb[0]);
+#pragma unroll
+    for (int m = 0; m < BF_E; ++m) {
+      const int delta = dj[m * BF_NT] >> 8, jpos = dj[m * BF_NT] & 255;
+      if (delta == 255) continue;
+      if (jpos >= 1 && delta < jpos) {
+        const T l = S::mul(cb[jpos], dinv);
+        const T w = S::fms(l, cb[jpos - delta], S::mk(wre[m * BF_NT + tid], wim[m]));
+        wre[m * BF_NT + tid] = S::re(w);
+        wim[m] = S::im(w);
+      } else if (jpos == 0) {  // row i leaves; row i + n + 1 enters its slot
+        const T v = entryB(i + W, delta);
+        wre[m * BF_NT + tid] = S::re(v);
+        wim[m] = S::im(v);
+      }
+      dj[m * BF_NT] = (delta << 8) | (jpos == 0 ? W - 1 : jpos - 1);
+    }
+    if (tid < n) {
+      const int r = i + 1 + tid;
+      const T l = (r < nx) ? S::mul(cb[tid + 1], dinv) : S::zero();
+      Lt_[(size_t)i * n + tid] = l;
+      if constexpr (!C) {
+        if (Lr_ && r < nx) Lr_[(size_t)r * n + (n - 1 - tid)] = l;  // L(r, i) = Lrow[r][i - r + n]
+      }
+    }
+    if (tid == 0) Di_[i] = dinv;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fine sweeps, one warp per (sample, group of 32 subintervals). Lanes are the
+// right-hand sides; each BE step is a forward (Lrow, dot form) and a backward
+// (Lt, dot form) banded substitution over the window of the last n solved
+// rows (shared memory, [W][33]). State X and scratch Z: [slot][nx][32].
+// ---------------------------------------------------------------------------
+struct Fine2dArgs {
+  const double* start;   // mode 0: U [M][N][nx]; mode 1: start rows [M][Q][nx]
+  const double* u0;      // mode 0: [nx]
+  const double* F_given; // mode 0, optional [M][N][nx]: skip the sweep, take these F ends
+  const double *dia, *ex, *ey;
+  const double *Lrow, *Lt, *Dinv;  // per sample: [nx][n], [nx][n], [nx]
+  const double* scaling;           // mode 0: [N]
+  const int32_t* active;           // mode 0: [M] or null
+  double* X;                       // [M * G][nx][32]
+  double* Z;                       // [M * G][nx][32]
+  double* out;                     // mode 0: R [M][N][nx]; mode 1: [M][Q][nseg][nx]
+  int M, N, n, J, nseg, mode;      // mode 0: fgr, mode 1: sweep (N = Q)
+  double dt, dT, g0, alpha;
+};
+
+__device__ __forceinline__ void fine2d_steps(const Fine2dArgs& a, int s, double* __restrict__ X,
+                                             double* __restrict__ Z, double* win, double* lrow, int lane) {
+  const int n = a.n, nx = n * n, W = n + 1;
+  const double* Lr = a.Lrow + (size_t)s * nx * n;
+  const double* Lt = a.Lt + (size_t)s * nx * n;
+  const double* Di = a.Dinv + (size_t)s * nx;
+  const double hg = a.dt * a.g0;
+  for (int step = 0; step < a.J; ++step) {
+    for (int q = lane; q < W * 33; q += 32) win[q] = 0.0;
+    __syncwarp();
+    for (int i = 0; i < nx; ++i) {  // forward: y_i = b_i - sum_k L(i,k) y_k
+      for (int t = lane; t < n; t += 32) lrow[t] = Lr[(size_t)i * n + t];
+      __syncwarp();
+      double acc = 0.0;
+      int slot = i % W;  // slot of k = i - n + t walks from (i+1) % W
+      for (int t = 0; t < n; ++t) {
+        if (++slot == W) slot = 0;
+        acc = fma(lrow[t], win[slot * 33 + lane], acc);
+      }
+      const double y = (X[(size_t)i * 32 + lane] + hg) - acc;
+      win[(i % W) * 33 + lane] = y;
+      Z[(size_t)i * 32 + lane] = y * Di[i];
+      __syncwarp();
+    }
+    for (int q = lane; q < W * 33; q += 32) win[q] = 0.0;
+    __syncwarp();
+    for (int i = nx - 1; i >= 0; --i) {  // backward: x_i = z_i - sum_t L(i+1+t, i) x_{i+1+t}
+      for (int t = lane; t < n; t += 32) lrow[t] = Lt[(size_t)i * n + t];
+      __syncwarp();
+      double acc = 0.0;
+      int slot = i % W;
+      for (int t = 0; t < n; ++t) {
+        if (++slot == W) slot = 0;
+        acc = fma(lrow[t], win[slot * 33 + lane], acc);
+      }
+      const double x = Z[(size_t)i * 32 + lane] - acc;
+      win[(i % W) * 33 + lane] = x;
+      X[(size_t)i * 32 + lane] = x;
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32) fine2d_kernel(Fine2dArgs a) {
+  const int n = a.n, nx = n * n, W = n + 1;
+  const int G = (a.N + 31) / 32;
+  const int s = blockIdx.x / G, g = blockIdx.x % G;
+  if (a.mode == 0 && a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
+  const int lane = threadIdx.x;
+  const int q = g * 32 + lane;  // subinterval (mode 0) / start row (mode 1)
+  const bool live = q < a.N;
+  extern __shared__ __align__(16) double sm2[];
+  double* win = sm2;             // [W][33]
+  double* lrow = win + W * 33;   // [n]
+  double* X = a.X + (size_t)blockIdx.x * nx * 32;
+  double* Z = a.Z + (size_t)blockIdx.x * nx * 32;
+  const double* src;
+  if (a.mode == 0) src = (q == 0 || !live) ? a.u0 : a.start + ((size_t)s * a.N + (q - 1)) * nx;
+  else src = a.start + ((size_t)s * a.N + (live ? q : 0)) * nx;
+  const double* x0 = (a.mode == 0 && a.F_given) ? a.F_given + ((size_t)s * a.N + (live ? q : 0)) * nx : src;
+  for (int i = 0; i < nx; ++i) X[(size_t)i * 32 + lane] = live ? x0[i] : 0.0;
+  __syncwarp();
+  if (a.mode == 1) {
+    for (int sg = 0; sg < a.nseg; ++sg) {
+      fine2d_steps(a, s, X, Z, win, lrow, lane);
+      if (live) {
+        double* o = a.out + (((size_t)s * a.N + q) * a.nseg + sg) * nx;
+        for (int i = 0; i < nx; ++i) o[i] = X[(size_t)i * 32 + lane];
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (!a.F_given) fine2d_steps(a, s, X, Z, win, lrow, lane);
+  __syncwarp();
+  if (!live) return;
+  // rhs_n = scaling_n ((I + dT A) F_n - prev_n); prev_0 = alpha U_{N-1}
+  const double* dd = a.dia + (size_t)s * nx;
+  const double* ex = a.ex + (size_t)s * nx;
+  const double* ey = a.ey + (size_t)s * nx;
+  const double* pv = (q == 0) ? a.start + ((size_t)s * a.N + (a.N - 1)) * nx : src;
+  const double pmul = (q == 0) ? a.alpha : 1.0;
+  const double sc = a.scaling[q];
+  double* o = a.out + ((size_t)s * a.N + q) * nx;
+  for (int i = 0; i < nx; ++i) {
+    const double x = X[(size_t)i * 32 + lane];
+    double Ax = dd[i] * x;
+    if (i + 1 < nx) Ax = fma(ex[i], X[(size_t)(i + 1) * 32 + lane], Ax);
+    if (i >= 1) Ax = fma(ex[i - 1], X[(size_t)(i - 1) * 32 + lane], Ax);
+    if (i + n < nx) Ax = fma(ey[i], X[(size_t)(i + n) * 32 + lane], Ax);
+    if (i >= n) Ax = fma(ey[i - n], X[(size_t)(i - n) * 32 + lane], Ax);
+    const double rhs = fma(a.dT, Ax, x) - pmul * pv[i];
+    o[i] = sc * rhs;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CGC: scaled DFT along time, per-frequency banded solves, inverse + update.
+// P layout: [M][NF][nx] complex.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load_twiddles(Cplx* tw, int N) {  // tw[j] = exp(-2 pi i j / N)
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double sn, cs;
+    sincospi(-2.0 * (double)j / (double)N, &sn, &cs);
+    tw[j] = {cs, sn};
+  }
+  __syncthreads();
+}
+
+__global__ void dft_fwd_kernel(const double* __restrict__ R, const double* __restrict__ load_scale,
+                               const int32_t* __restrict__ status, int M, int N, int nx,
+                               Cplx* __restrict__ P) {
+  __shared__ Cplx tw[1024];
+  load_twiddles(tw, N);
+  const int NF = N / 2 + 1;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)M * nx) return;
+  const int s = (int)(t / nx), i = (int)(t - (long long)s * nx);
+  if (status && status[s] != KLE_SAMPLE_ACTIVE) return;
+  const double* r = R + (size_t)s * N * nx + i;
+  const double rs = 1.0 / sqrt((double)N);
+  for (int f = 0; f < NF; ++f) {
+    double re = 0.0, im = 0.0;
+    int w = 0;  // (f k) mod N
+    for (int k = 0; k < N; ++k) {
+      double v = r[(size_t)k * nx];
+      if (load_scale) v *= load_scale[k];
+      re = fma(v, tw[w].re, re);
+      im = fma(v, tw[w].im, im);
+      w += f;
+      if (w >= N) w -= N;
+    }
+    P[((size_t)s * NF + f) * nx + i] = {re * rs, im * rs};
+  }
+}
+
+// one warp per (sample, frequency): B_f q = p in place
+__global__ void __launch_bounds__(32) band_solve_cplx_kernel(Cplx* __restrict__ P, const double* __restrict__ Lt,
+                                                             const double* __restrict__ Dinv,
+                                                             const int32_t* __restrict__ status, int NF, int n) {
+  const int nx = n * n, W = n + 1;
+  const int phi = blockIdx.x, s = phi / NF;
+  if (status && status[s] != KLE_SAMPLE_ACTIVE) return;
+  const int lane = threadIdx.x;
+  const Cplx* L = reinterpret_cast<const Cplx*>(Lt) + (size_t)phi * nx * n;
+  const Cplx* Di = reinterpret_cast<const Cplx*>(Dinv) + (size_t)phi * nx;
+  Cplx* p = P + (size_t)phi * nx;
+  __shared__ Cplx win[128];
+  for (int q = lane; q < W; q += 32) win[q] = {0.0, 0.0};
+  __syncwarp();
+  // forward, column form: pending updates acc[(r) % W] for rows r in (i, i+n]
+  for (int i = 0; i < nx; ++i) {
+    const int si = i % W;
+    const Cplx acc = win[si];
+    const Cplx pi = p[i];
+    const Cplx y = {pi.re - acc.re, pi.im - acc.im};
+    __syncwarp();
+    if (lane == 0) {
+      win[si] = {0.0, 0.0};
+      p[i] = cmul(y, Di[i]);  // z_i = y_i / D_i
+    }
+    __syncwarp();
+    for (int t = lane; t < n; t += 32) {
+      int sl = si + 1 + t;
+      if (sl >= W) sl -= W;
+      const Cplx l = L[(size_t)i * n + t];
+      Cplx w = win[sl];
+      w.re = fma(l.re, y.re, fma(-l.im, y.im, w.re));
+      w.im = fma(l.re, y.im, fma(l.im, y.re, w.im));
+      win[sl] = w;
+    }
+    __syncwarp();
+  }
+  for (int q = lane; q < W; q += 32) win[q] = {0.0, 0.0};
+  __syncwarp();
+  // backward, dot form: x_i = z_i - sum_t L(i+1+t, i) x_{i+1+t}
+  for (int i = nx - 1; i >= 0; --i) {
+    const int si = i % W;
+    double re = 0.0, im = 0.0;
+    for (int t = lane; t < n; t += 32) {
+      int sl = si + 1 + t;
+      if (sl >= W) sl -= W;
+      const Cplx l = L[(size_t)i * n + t];
+      const Cplx x = win[sl];
+      re = fma(l.re, x.re, fma(-l.im, x.im, re));
+      im = fma(l.re, x.im, fma(l.im, x.re, im));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(KLE_FULL_MASK, re, o);
+      im += __shfl_xor_sync(KLE_FULL_MASK, im, o);
+    }
+    const Cplx z = p[i];
+    const Cplx x = {z.re - re, z.im - im};
+    __syncwarp();
+    if (lane == 0) {
+      win[si] = x;
+      p[i] = x;
+    }
+    __syncwarp();
+  }
+}
+
+// u_k = Re(ifft(q))_k / sqrt(N) / scaling_k with q_{N-f} = conj(q_f); the
+// increment max |u - U| per sample into inc_bits (non-negative doubles and +NaN
+// order like their bit patterns).
+__global__ void dft_inv_update_kernel(const Cplx* __restrict__ P, const double* __restrict__ inv_scaling,
+                                      const int32_t* __restrict__ status, int M, int N, int nx,
+                                      double* __restrict__ U, double* __restrict__ Uout,
+                                      unsigned long long* __restrict__ inc_bits) {
+  __shared__ Cplx tw[1024];
+  load_twiddles(tw, N);
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool in = t < (long long)M * nx;
+  const int s = in ? (int)(t / nx) : 0, i = in ? (int)(t - (long long)s * nx) : 0;
+  const bool act = in && !(status && status[s] != KLE_SAMPLE_ACTIVE);
+  const int NF = N / 2 + 1;
+  double incmax = 0.0;
+  bool bad = false;
+  if (act) {
+    const Cplx* q = P + (size_t)s * NF * nx + i;
+    const double rs = 1.0 / sqrt((double)N);
+    double* out = (Uout ? Uout : U) + (size_t)s * N * nx + i;
+    const double* old = (inc_bits && U) ? U + (size_t)s * N * nx + i : nullptr;
+    for (int k = 0; k < N; ++k) {
+      double re = 0.0;
+      int w = 0;  // (f k) mod N; exp(+2 pi i f k / N) = conj tw
+      for (int f = 0; f < N; ++f) {
+        const int fe = f <= N / 2 ? f : N - f;
+        const Cplx v = q[(size_t)fe * nx];
+        const double vim = (f <= N / 2) ? v.im : -v.im;
+        re = fma(v.re, tw[w].re, fma(vim, tw[w].im, re));  // Re(v conj(tw))
+        w += k;
+        if (w >= N) w -= N;
+      }
+      const double u = (re * rs) * inv_scaling[k];
+      if (old) {
+        const double dlt = fabs(u - old[(size_t)k * nx]);
+        incmax = fmax(incmax, dlt);
+        bad |= (dlt != dlt);
+      }
+      out[(size_t)k * nx] = u;
+    }
+  }
+  if (inc_bits == nullptr) return;  // uniform
+  if (bad) incmax = __longlong_as_double(0x7ff8000000000000LL);
+  const int key = act ? s : -1;
+  const int k0 = __shfl_sync(KLE_FULL_MASK, key, 0);
+  if (__all_sync(KLE_FULL_MASK, key == k0)) {
+    if (k0 < 0) return;
+    double m = incmax;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_xor_sync(KLE_FULL_MASK, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(inc_bits + k0, (unsigned long long)__double_as_longlong(m));
+  } else if (act) {
+    atomicMax(inc_bits + s, (unsigned long long)__double_as_longlong(incmax));
+  }
+}
+
+__global__ void status2d_kernel(unsigned long long* __restrict__ inc_bits, int M, int k, int max_iters,
+                                double tol, int32_t* __restrict__ status, int32_t* __restrict__ iters,
+                                double* __restrict__ inc_out, double* __restrict__ inc_hist,
+                                int32_t* __restrict__ active_count) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= M) return;
+  if (status[s] != KLE_SAMPLE_ACTIVE) return;
+  const double inc = __longlong_as_double((long long)inc_bits[s]);
+  inc_bits[s] = 0ULL;
+  if (inc_out) inc_out[s] = inc;
+  if (inc_hist) inc_hist[(size_t)s * max_iters + (k - 1)] = inc;
+  int st = KLE_SAMPLE_ACTIVE;
+  if (inc <= tol) st = KLE_SAMPLE_CONVERGED;
+  else if (!isfinite(inc)) st = KLE_SAMPLE_NONFINITE;
+  else if (k >= max_iters) st = KLE_SAMPLE_MAXITERS;
+  if (st != KLE_SAMPLE_ACTIVE) {
+    status[s] = st;
+    if (iters) iters[s] = k;
+  } else if (active_count) {
+    atomicAdd(active_count, 1);
+  }
+}
+
+}  // namespace kle
+
+// ===========================================================================
+// C ABI (declared in include/kle_b200.h)
+// ===========================================================================
+using namespace kle;
+#define KLE2D_STREAM(s) (reinterpret_cast<cudaStream_t>(s))
+
+extern "C" int kle_2d_kl5pt_f64(const double* xi, int M, int d, const double* kl_table, int n, double inv_h2,
+                               double* dia, double* ex, double* ey, void* stream) {
+  if (M < 0 || d < 1 || n < 1) return set_error(KLE_ERR_INVALID, "kl5pt: bad dims");
+  const long long tot = (long long)M * n * n;
+  if (tot == 0) return KLE_OK;
+  kl5pt_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, KLE2D_STREAM(stream)>>>(xi, M, d, kl_table, n, inv_h2,
+                                                                                  dia, ex, ey);
+  return check_launch("kl5pt_kernel");
+}
+
+extern "C" int kle_2d_factor_f64(const double* dia, const double* ex, const double* ey, int M, int n,
+                                const double* lam, int NF, double shift, double c, double* Lrow, double* Lt,
+                                double* Dinv, void* stream) {
+  if (M < 0 || n < 1 || (n + 1) * (n + 1) > BF_NT * BF_E || (lam && NF < 1))
+    return set_error(KLE_ERR_INVALID, "factor2d: bad dims (n <= 127)");
+  if (M == 0) return KLE_OK;
+  const int W = n + 1;
+  if (lam) {
+    const size_t smem = sizeof(double) * BF_E * BF_NT + 2 * W * sizeof(Cplx) + sizeof(int) * BF_E * BF_NT;
+    cudaFuncSetAttribute(band_factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    band_factor_kernel<true><<<(unsigned)(M * NF), BF_NT, smem, KLE2D_STREAM(stream)>>>(
+        dia, ex, ey, n, lam, NF, 0.0, c, nullptr, Lt, Dinv);
+  } else {
+    const size_t smem = sizeof(double) * BF_E * BF_NT + 2 * W * sizeof(double) + sizeof(int) * BF_E * BF_NT;
+    cudaFuncSetAttribute(band_factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    band_factor_kernel<false><<<(unsigned)M, BF_NT, smem, KLE2D_STREAM(stream)>>>(dia, ex, ey, n, nullptr, 1, shift,
+                                                                                  c, Lrow, Lt, Dinv);
+  }
+  return check_launch("band_factor_kernel");
+}
+
+extern "C" size_t kle_2d_fine_work_doubles(int M, int N, int n) {
+  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 2 * (size_t)M * ((N + 31) / 32) * n * n * 32;
+}
+
+static int fine2d_launch(Fine2dArgs& a, void* stream) {
+  const int G = (a.N + 31) / 32;
+  const int W = a.n + 1;
+  const size_t smem = sizeof(double) * ((size_t)W * 33 + a.n);
+  fine2d_kernel<<<(unsigned)(a.M * G), 32, smem, KLE2D_STREAM(stream)>>>(a);
+  return check_launch("fine2d_kernel");
+}
+
+extern "C" int kle_2d_fgr_f64(const double* U, const double* u0, const double* F_given, const double* dia,
+                              const double* ex,
+                             const double* ey, const double* Lrow, const double* Lt, const double* Dinv,
+                             const double* scaling, const int32_t* active, int M, int N, int n, int J,
+                             double dt, double dT, double g0, double alpha, double* work, size_t work_doubles,
+                             double* Rout, void* stream) {
+  if (M < 0 || N < 1 || n < 1 || n > 127 || J < 1) return set_error(KLE_ERR_INVALID, "fgr2d: bad dims");
+  if (M == 0) return KLE_OK;
+  const size_t need = kle_2d_fine_work_doubles(M, N, n);
+  if (work_doubles < need) return set_error(KLE_ERR_WORKSPACE, "fgr2d: workspace too small");
+  Fine2dArgs a{U, u0, F_given, dia, ex, ey, Lrow, Lt, Dinv, scaling, active, work, work + need / 2, Rout,
+               M, N, n, J, 1, 0, dt, dT, g0, alpha};
+  return fine2d_launch(a, stream);
+}
+
+extern "C" int kle_2d_sweep_f64(const double* start, const double* dia, const double* ex, const double* ey,
+                               const double* Lrow, const double* Lt, const double* Dinv, int M, int Q, int n,
+                               int J, int nseg, double h, double g0, double* work, size_t work_doubles,
+                               double* out, void* stream) {
+  if (M < 0 || Q < 1 || n < 1 || n > 127 || J < 1 || nseg < 1) return set_error(KLE_ERR_INVALID, "sweep2d: bad dims");
+  if (M == 0) return KLE_OK;
+  const size_t need = kle_2d_fine_work_doubles(M, Q, n);
+  if (work_doubles < need) return set_error(KLE_ERR_WORKSPACE, "sweep2d: workspace too small");
+  Fine2dArgs a{start, nullptr, nullptr, dia, ex, ey, Lrow, Lt, Dinv, nullptr, nullptr, work, work + need / 2, out,
+               M, Q, n, J, nseg, 1, h, 0.0, g0, 0.0};
+  return fine2d_launch(a, stream);
+}
+
+extern "C" size_t kle_2d_cgc_work_doubles(int M, int N, int n) {
+  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 2 * (size_t)M * (N / 2 + 1) * n * n + (size_t)M;
+}
+
+extern "C" int kle_2d_cgc_f64(const double* R, const double* load_scale, double* U, double* Uout,
+                             const double* Lt, const double* Dinv, const double* inv_scaling, int M, int N, int n,
+                             int k, int max_iters, double tol, int32_t* status, int32_t* iters, double* inc,
+                             double* inc_hist, int32_t* active_count, double* work, size_t work_doubles,
+                             void* stream) {
+  if (M < 0 || N < 2 || (N & 1) || n < 1 || n > 127) return set_error(KLE_ERR_INVALID, "cgc2d: bad dims (N even)");
+  if (M == 0) return KLE_OK;
+  if (work_doubles < kle_2d_cgc_work_doubles(M, N, n)) return set_error(KLE_ERR_WORKSPACE, "cgc2d: workspace");
+  const int nx = n * n, NF = N / 2 + 1;
+  cudaStream_t st = KLE2D_STREAM(stream);
+  Cplx* P = reinterpret_cast<Cplx*>(work);
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(work + 2 * (size_t)M * NF * nx);
+  const long long tot = (long long)M * nx;
+  dft_fwd_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(R, load_scale, status, M, N, nx, P);
+  if (int e = check_launch("dft_fwd_kernel")) return e;
+  band_solve_cplx_kernel<<<(unsigned)(M * NF), 32, 0, st>>>(P, Lt, Dinv, status, NF, n);
+  if (int e = check_launch("band_solve_cplx_kernel")) return e;
+  const bool track = status != nullptr && U != nullptr && Uout == nullptr;
+  dft_inv_update_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(P, inv_scaling, status, M, N, nx, U, Uout,
+                                                                         track ? bits : nullptr);
+  if (int e = check_launch("dft_inv_update_kernel")) return e;
+  if (!track) return KLE_OK;
+  status2d_kernel<<<(unsigned)((M + 127) / 128), 128, 0, st>>>(bits, M, k, max_iters, tol, status, iters, inc,
+                                                                inc_hist, active_count);
+  return check_launch("status2d_kernel");
+}

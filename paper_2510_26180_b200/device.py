@@ -96,8 +96,13 @@ class DeviceOperator:
 
     @classmethod
     def from_model(cls, model, xis):
-        """xis: list of ParameterSample, an (M, d) array or a device tensor."""
+        """xis: list of ParameterSample, an (M, d) array or a device tensor.
+        5-point (2D) plugins get a ``twod.DeviceOperator2D``."""
         require_cuda()
+        from .twod import DeviceOperator2D, is_five_point
+
+        if is_five_point(model):
+            return DeviceOperator2D.from_model(model, xis)
         if isinstance(xis, ParameterSample):
             xis = [xis]
         kl_table = getattr(model, "kl_table", None)

@@ -203,7 +203,109 @@ class LogNormalKL1D(LinearModel):
         return [ParameterSample(row, id=i) for i, row in enumerate(draws)]
 
 
-_MODELS = {"lognormal-kl-1d": LogNormalKL1D}
+class LogNormalKL2D(LinearModel):
+    """2D log-normal random-coefficient diffusion on the unit square (BASELINE
+    config 3): n x n interior nodes of a 5-point finite-difference grid, zero
+    Dirichlet data, f = 1, u0 = sin(pi x) sin(pi y).
+
+    log a is the KL expansion of the separable covariance
+    sigma^2 exp(-|x1-x2|/ell) exp(-|y1-y2|/ell): the eigenpairs are products of
+    the 1D Nystrom pairs on the n+1 cell-centre coordinates (exponential_kl_1d
+    with sigma = 1), the d largest products kept (ties: lower (j, k) first).
+    log a is evaluated at the (n+1)^2 cell centres; face coefficients are the
+    arithmetic averages of the two cell centres a face separates. DOF order:
+    x fastest, idx = (j-1) n + (i-1) for node (i h, j h). The assembled operator
+    is symmetric, irreducibly diagonally dominant, bandwidth n.
+    """
+
+    name = "lognormal-kl-2d"
+
+    def __init__(self, n: int = 127, d: int = 10, sigma: float = 0.5, ell: float = 0.25,
+                 source: float = 1.0):
+        if n < 1 or d < 1:
+            raise ConfigError("need n >= 1 and d >= 1")
+        self.n = int(n)
+        self.nx = self.n * self.n
+        self.parameter_dim = int(d)
+        self.supports = tuple((-np.inf, np.inf) for _ in range(self.parameter_dim))
+        self.h = 1.0 / (self.n + 1)
+        self.sigma = float(sigma)
+        self.ell = float(ell)
+        self.source = float(source)
+        nc = self.n + 1
+        centres = (np.arange(nc) + 0.5) * self.h
+        m1 = min(nc, self.parameter_dim)
+        mu, phi = exponential_kl_1d(centres, self.h, 1.0, self.ell, m1)
+        jj, kk = np.meshgrid(np.arange(m1), np.arange(m1), indexing="ij")
+        jj, kk = jj.ravel(), kk.ravel()
+        lam_all = (self.sigma * self.sigma) * mu[jj] * mu[kk]
+        order = np.lexsort((kk, jj, -lam_all))[: self.parameter_dim]
+        if len(order) < self.parameter_dim:
+            raise ConfigError("d exceeds the number of product modes")
+        self.kl_eigenvalues = lam_all[order]
+        self.kl_pairs = np.stack([jj[order], kk[order]], axis=1)
+        # row q: sqrt(lam_q) phi_j(x_p) phi_k(y_r) at centre (p, r), flattened r*(n+1)+p
+        modes = np.stack([np.outer(phi[k], phi[j]).ravel() for j, k in self.kl_pairs])
+        self.kl_table = np.ascontiguousarray(np.sqrt(self.kl_eigenvalues)[:, None] * modes)
+        xs = np.arange(1, self.n + 1) * self.h
+        self.x = np.tile(xs, self.n)
+        self.y = np.repeat(xs, self.n)
+        self._cache: dict = {}
+
+    @property
+    def cell_volume(self) -> float:
+        return self.h * self.h
+
+    def fit_maps(self):
+        return [ParameterMap("identity", lo, hi) for lo, hi in self.supports]
+
+    def log_coefficient(self, xi) -> np.ndarray:
+        """log a at the cell centres, shape (n+1, n+1) indexed [r (y), p (x)]."""
+        v = np.asarray(getattr(xi, "values", xi), dtype=float)
+        return (self.kl_table.T @ v).reshape(self.n + 1, self.n + 1)
+
+    def faces(self, xi):
+        """(ax (n, n+1): x-faces [j-1][i], ay (n+1, n): y-faces [j][i-1])."""
+        a = np.exp(self.log_coefficient(xi))
+        ax = 0.5 * (a[:-1, :] + a[1:, :])   # face (i+1/2, j): centres (i, j-1), (i, j)
+        ay = 0.5 * (a[:, :-1] + a[:, 1:])   # face (i, j+1/2): centres (i-1, j), (i, j)
+        return ax, ay
+
+    def stencil(self, xi):
+        """(dia, ex, ey), each (nx,): A[i,i], A[i,i+1] (0 at the row end), A[i,i+n] (0 in the last row)."""
+        ax, ay = self.faces(xi)
+        n, inv_h2 = self.n, 1.0 / (self.h * self.h)
+        dia = (ax[:, :-1] + ax[:, 1:] + ay[:-1, :] + ay[1:, :]) * inv_h2
+        ex = -ax[:, 1:].copy() * inv_h2
+        ex[:, -1] = 0.0
+        ey = -ay[1:, :].copy() * inv_h2
+        ey[-1, :] = 0.0
+        return dia.ravel(), ex.ravel(), ey.ravel()
+
+    def linear_system(self, xi):
+        key = xi.key()
+        hit = self._cache.get(key)
+        if hit is not None:
+            return hit
+        import scipy.sparse as sp
+
+        dia, ex, ey = self.stencil(xi)
+        n = self.n
+        A = sp.diags([ey[:-n], ex[:-1], dia, ex[:-1], ey[:-n]], [-n, -1, 0, 1, n], format="csc")
+        g = np.full(self.nx, self.source)
+        pair = (A, lambda t, g=g: g)
+        self._cache[key] = pair
+        return pair
+
+    def initial_condition(self, xi=None):
+        return np.sin(np.pi * self.x) * np.sin(np.pi * self.y)
+
+    def sample_parameters(self, count, rng: RngStream) -> list:
+        draws = rng.normal(0.0, 1.0, size=(count, self.parameter_dim))
+        return [ParameterSample(row, id=i) for i, row in enumerate(draws)]
+
+
+_MODELS = {"lognormal-kl-1d": LogNormalKL1D, "lognormal-kl-2d": LogNormalKL2D}
 
 
 def get_model(name: str, **kwargs) -> Model:

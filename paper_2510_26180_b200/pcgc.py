@@ -116,6 +116,21 @@ def three_step_solve(spec: AlphaCirculantSpec, mean_jac, deltaT: float, r, solve
     A = -sp.csr_matrix(np.atleast_2d(mean_jac) if not sp.issparse(mean_jac) else mean_jac)
     nx = A.shape[0]
     r2 = r.reshape(spec.n, nx)
+    coo = A.tocoo()
+    bw = int(np.max(np.abs(coo.row - coo.col))) if coo.nnz else 0
+    if bw > 1:  # 5-point (2D) Jacobian of an n x n grid: bandwidth n
+        from .twod import DeviceOperator2D, three_step_device2d
+
+        n = bw
+        if n * n != nx or spec.n % 2:
+            raise NotImplementedError("device three_step_solve: 5-point operators on an n x n grid, N even")
+        ex, ey = np.zeros(nx), np.zeros(nx)
+        ex[:-1] = A.diagonal(1)
+        ey[:-n] = A.diagonal(n)
+        op = DeviceOperator2D(to_dev(A.diagonal(0)[None]), to_dev(ex[None]), to_dev(ey[None]), n, 0.0,
+                              to_dev(np.zeros(nx)))
+        u, imag = three_step_device2d(op, AlphaTables(spec), spec.n, deltaT, to_dev(r2[None]))
+        return u[0].cpu().numpy().reshape(r.shape), float(imag[0].item())
     dia = np.asarray(A.diagonal(0), dtype=float)
     off = np.zeros(nx)
     if nx > 1:
@@ -169,8 +184,14 @@ def cgc_correct(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, U
     U = to_dev(U_prev.states)[None]
     F = to_dev(np.asarray(fine_ends, dtype=float))[None]
     R = empty(*U.shape)
-    _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha, F_given=F)
-    u, imag = three_step_device(op, tables, N, grid.deltaT, R, prescaled=True)
+    from .twod import DeviceOperator2D, three_step_device2d
+
+    if isinstance(op, DeviceOperator2D):
+        op.fgr(U, tables, grid, cfg.alpha, R, F_given=F)
+        u, imag = three_step_device2d(op, tables, N, grid.deltaT, R, prescaled=True)
+    else:
+        _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha, F_given=F)
+        u, imag = three_step_device(op, tables, N, grid.deltaT, R, prescaled=True)
     return CoarseTrajectory(U_prev.initial, u[0].cpu().numpy()), {"inner_iters": 1,
                                                                    "imag_residue": float(imag[0].item())}
 
@@ -214,6 +235,10 @@ def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, 
                       workspace=None) -> BatchResult:
     """The production loop: U (M, N, nx) device tensor is overwritten with the
     final states (``kle_pcgc_solve_f64``)."""
+    from .twod import DeviceOperator2D, pcgc_solve_device2d
+
+    if isinstance(op, DeviceOperator2D):
+        return pcgc_solve_device2d(op, U, grid, cfg, tables)
     M, N, nx = U.shape
     if N != grid.n_coarse or nx != op.nx or M != op.M:
         raise ValueError("initial guess length does not match the time grid")
@@ -266,11 +291,21 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     iters = torch.zeros(1, dtype=torch.int32, device="cuda")
     inc = empty(1, cfg.max_outer_iters).fill_(float("nan"))
     imag = torch.zeros(1, dtype=torch.float64, device="cuda")
-    sfac = shift_factors(op, tables, N, grid.deltaT)
-    if sfac is not None:  # cluster path: zero-initialised reduction slots
-        scratch, nbytes = torch.zeros(16, dtype=torch.uint8, device="cuda"), 16
+    from .twod import DeviceOperator2D
+
+    is2d = isinstance(op, DeviceOperator2D)
+    if is2d:
+        if N % 2:
+            raise NotImplementedError("the 2D CGC needs an even number of subintervals")
+        fac2d = op.shifted_factors(tables, N, grid.deltaT)
+        nbytes = int(_lib.query("kle_2d_cgc_work_doubles", 1, N, op.n))
+        scratch = torch.zeros(max(nbytes, 1), dtype=torch.float64, device="cuda")
     else:
-        scratch, nbytes = _cgc_scratch(1, N, nx)
+        sfac = shift_factors(op, tables, N, grid.deltaT)
+        if sfac is not None:  # cluster path: zero-initialised reduction slots
+            scratch, nbytes = torch.zeros(16, dtype=torch.uint8, device="cuda"), 16
+        else:
+            scratch, nbytes = _cgc_scratch(1, N, nx)
 
     def err(states):
         if reference is None:
@@ -292,11 +327,17 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     dT = grid.deltaT
     for k in range(1, cfg.max_outer_iters + 1):
         tic = time.perf_counter()
-        _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha)
         # tol < 0 keeps the device from freezing the sample; the stop test is ours
-        _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
-                  ptr(op.off), ptr(sfac), 1, N, nx, dT, k, cfg.max_outer_iters, -1.0, None, None, ptr(inc), ptr(imag),
-                  None, ptr(scratch), nbytes, stream_ptr())
+        if is2d:
+            op.fgr(U, tables, grid, cfg.alpha, R, status=status)
+            _lib.call("kle_2d_cgc_f64", ptr(R), None, ptr(U), None, ptr(fac2d[0]), ptr(fac2d[1]),
+                      ptr(tables.inv_scaling), 1, N, op.n, k, cfg.max_outer_iters, -1.0, ptr(status), ptr(iters),
+                      None, ptr(inc), None, ptr(scratch), nbytes, stream_ptr())
+        else:
+            _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha)
+            _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
+                      ptr(op.off), ptr(sfac), 1, N, nx, dT, k, cfg.max_outer_iters, -1.0, None, None, ptr(inc),
+                      ptr(imag), None, ptr(scratch), nbytes, stream_ptr())
         host = U[0].cpu().numpy()
         increment = float(inc[0, k - 1].item())
         wall_ms = 1e3 * (time.perf_counter() - tic)

@@ -1,0 +1,216 @@
+"""2D (5-point) device path: BASELINE config 3 (``models.LogNormalKL2D``).
+
+Same plugin contract and entry points as the 1D path: ``DeviceOperator.from_model``
+returns a ``DeviceOperator2D`` for a 5-point operator, whose ``sweep`` serves
+``propagate_fine`` / ``propagate_coarse`` / ``fine_reference`` /
+``coarse_sweep_init``; ``pcgc.pcgc_solve_device`` dispatches here.
+
+All implicit solves are direct, like the reference's SuperLU
+(``pintuq/propagators.py:25-39``, ``pintuq/pcgc.py:137-145``): banded
+L D L^T factors of I + dt A (real) and of the N/2+1 distinct shifted matrices
+lambda_f I + dT A (complex) are built on the device once per solve
+(``kle_2d_factor_f64``) and reused by every outer iteration. Samples are
+processed in batches sized to the free device memory (the complex factors
+take 16 (N/2+1) n^3 bytes per sample).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .core import DeviceError, ParameterSample
+from .device import AlphaTables, empty, ptr, require_cuda, stream_ptr, to_dev
+
+try:
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+
+def stencil_of(model, xi):
+    """(dia, ex, ey, g0) of a 5-point plugin's operator via its own
+    ``linear_system`` (host-side model evaluation, as in the reference)."""
+    import scipy.sparse as sp
+
+    A, g = model.linear_system(xi)
+    A = sp.csr_matrix(A)
+    n = int(getattr(model, "n"))
+    nx = A.shape[0]
+    if nx != n * n:
+        raise NotImplementedError("5-point operator size must be n*n")
+    coo = A.tocoo()
+    off = np.setdiff1d(np.unique(np.abs(coo.row - coo.col)), [0, 1, n])
+    if off.size:
+        raise NotImplementedError("the 2D device path supports 5-point operators only")
+    if abs(A - A.T).max() if A.nnz else 0:
+        raise NotImplementedError("the 2D device path supports symmetric operators only")
+    dia = np.asarray(A.diagonal(0), dtype=float)
+    ex = np.zeros(nx)
+    ey = np.zeros(nx)
+    if nx > 1:
+        ex[:-1] = A.diagonal(1)
+    if nx > n:
+        ey[:-n] = A.diagonal(n)
+    g_a, g_b = np.asarray(g(0.0), dtype=float), np.asarray(g(1.0), dtype=float)
+    if not (np.array_equal(g_a, g_b) and np.all(g_a == g_a[0])):
+        raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
+    return dia, ex, ey, float(g_a[0])
+
+
+def is_five_point(model) -> bool:
+    """True for plugins on an n x n grid with a 5-point operator (bandwidth n)."""
+    n = getattr(model, "n", None)
+    return hasattr(model, "stencil") or (n is not None and n > 1 and getattr(model, "nx", None) == n * n)
+
+
+class DeviceOperator2D:
+    """Batch of M per-sample 5-point operators resident on the device."""
+
+    def __init__(self, dia, ex, ey, n: int, g0: float, u0):
+        require_cuda()
+        self.dia, self.ex, self.ey = dia, ex, ey
+        self.M, self.nx = dia.shape
+        self.n = int(n)
+        if self.n * self.n != self.nx or self.n > 127:
+            raise DeviceError("2D operator: need nx = n*n with n <= 127")
+        self.g0 = float(g0)
+        self.u0 = u0
+        self.layout = (0, 0, 0)
+        self._fine = {}
+
+    @classmethod
+    def from_model(cls, model, xis):
+        require_cuda()
+        if isinstance(xis, ParameterSample):
+            xis = [xis]
+        table = getattr(model, "kl_table", None)
+        n = int(model.n)
+        if table is not None and hasattr(model, "stencil"):
+            if isinstance(xis, (list, tuple)):
+                arr = np.array([np.asarray(x.values if isinstance(x, ParameterSample) else x, dtype=float)
+                                for x in xis])
+            else:
+                arr = xis
+            xi_d = to_dev(arr).reshape(-1, model.parameter_dim)
+            M = xi_d.shape[0]
+            dia, ex, ey = empty(M, n * n), empty(M, n * n), empty(M, n * n)
+            _lib.call("kle_2d_kl5pt_f64", ptr(xi_d), M, model.parameter_dim, ptr(to_dev(table)), n,
+                      1.0 / (model.h * model.h), ptr(dia), ptr(ex), ptr(ey), stream_ptr())
+            g0 = model.source
+        else:
+            rows = [stencil_of(model, x) for x in xis]
+            if len({r[3] for r in rows}) != 1:
+                raise NotImplementedError("all samples must share the source value g0")
+            dia, ex, ey = (to_dev(np.array([r[k] for r in rows])) for k in range(3))
+            g0 = rows[0][3]
+        first = xis[0] if isinstance(xis, (list, tuple)) else None
+        return cls(dia, ex, ey, n, g0, to_dev(model.initial_condition(first)))
+
+    def select(self, lo: int, hi: int) -> "DeviceOperator2D":
+        return DeviceOperator2D(self.dia[lo:hi], self.ex[lo:hi], self.ey[lo:hi], self.n, self.g0, self.u0)
+
+    # -- factors -------------------------------------------------------------
+    def fine_factor(self, h: float):
+        """(Lrow, Lt, Dinv) of I + h A for every sample (cached per h)."""
+        key = float(h)
+        f = self._fine.get(key)
+        if f is None:
+            M, nx, n = self.M, self.nx, self.n
+            Lrow = torch.zeros(M, nx, n, dtype=torch.float64, device="cuda")
+            Lt, Dinv = empty(M, nx, n), empty(M, nx)
+            _lib.call("kle_2d_factor_f64", ptr(self.dia), ptr(self.ex), ptr(self.ey), M, n, None, 1, 1.0, key,
+                      ptr(Lrow), ptr(Lt), ptr(Dinv), stream_ptr())
+            f = (Lrow, Lt, Dinv)
+            self._fine[key] = f
+        return f
+
+    def shifted_factors(self, tables: AlphaTables, N: int, deltaT: float):
+        """Complex (Lt, Dinv) of lambda_f I + dT A, f = 0..N/2 (B_{N-f} = conj B_f)."""
+        NF = N // 2 + 1
+        Lt = empty(self.M, NF, self.nx, self.n, 2)
+        Dinv = empty(self.M, NF, self.nx, 2)
+        _lib.call("kle_2d_factor_f64", ptr(self.dia), ptr(self.ex), ptr(self.ey), self.M, self.n,
+                  ptr(tables.lam), NF, 0.0, deltaT, None, ptr(Lt), ptr(Dinv), stream_ptr())
+        return Lt, Dinv
+
+    # -- propagators ---------------------------------------------------------
+    def sweep(self, start, h: float, J: int, nseg: int = 1):
+        """start: (M, Q, nx) device tensor -> (M, Q, nseg, nx)."""
+        M, Q, nx = start.shape
+        Lrow, Lt, Dinv = self.fine_factor(h)
+        out = empty(M, Q, nseg, nx)
+        nw = int(_lib.query("kle_2d_fine_work_doubles", M, Q, self.n))
+        work = empty(max(nw, 1))
+        _lib.call("kle_2d_sweep_f64", ptr(start.contiguous()), ptr(self.dia), ptr(self.ex), ptr(self.ey), ptr(Lrow),
+                  ptr(Lt), ptr(Dinv), M, Q, self.n, J, nseg, h, self.g0, ptr(work), nw, ptr(out), stream_ptr())
+        return out
+
+    def fgr(self, U, tables: AlphaTables, grid, alpha: float, R, status=None, F_given=None):
+        M, N, nx = U.shape
+        dT, dt = grid.deltaT, grid.deltat
+        Lrow, Lt, Dinv = self.fine_factor(dt)
+        nw = int(_lib.query("kle_2d_fine_work_doubles", M, N, self.n))
+        work = empty(max(nw, 1))
+        _lib.call("kle_2d_fgr_f64", ptr(U), ptr(self.u0), ptr(F_given), ptr(self.dia), ptr(self.ex), ptr(self.ey), ptr(Lrow),
+                  ptr(Lt), ptr(Dinv), ptr(tables.scaling), ptr(status), M, N, self.n, grid.n_fine_per_coarse,
+                  dt, dT, self.g0, alpha, ptr(work), nw, ptr(R), stream_ptr())
+
+
+def three_step_device2d(op: DeviceOperator2D, tables: AlphaTables, N: int, deltaT: float, r, prescaled=False,
+                        factors=None):
+    """u = V (Lambda (x) I + dT I (x) A)^{-1} V^{-1} r, r: (M, N, nx). Returns (u, imag)."""
+    M, _, nx = r.shape
+    Lt, Dinv = factors or op.shifted_factors(tables, N, deltaT)
+    u = empty(M, N, nx)
+    nw = int(_lib.query("kle_2d_cgc_work_doubles", M, N, op.n))
+    work = empty(max(nw, 1))
+    _lib.call("kle_2d_cgc_f64", ptr(r.contiguous()), None if prescaled else ptr(tables.scaling), None, ptr(u),
+              ptr(Lt), ptr(Dinv), ptr(tables.inv_scaling), M, N, op.n, 0, 1, 0.0, None, None, None, None, None,
+              ptr(work), nw, stream_ptr())
+    return u, torch.zeros(M, dtype=torch.float64, device="cuda")
+
+
+def _batch_size(op: DeviceOperator2D, N: int) -> int:
+    NF = N // 2 + 1
+    per = 8 * (2 * NF * op.nx * (op.n + 1) + 2 * op.nx * (op.n + 1) + 6 * N * op.nx + 2 * NF * op.nx)
+    free, _ = torch.cuda.mem_get_info()
+    return max(1, min(op.M, int(0.8 * free) // per))
+
+
+def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables = None, batch: int = None):
+    """Batched PCGC loop for the 2D operator (``pintuq/pcgc.py:273-358``,
+    stop_on="increment"); U (M, N, nx) is overwritten with the final states."""
+    from .pcgc import BatchResult, build_alpha_circulant
+
+    M, N, nx = U.shape
+    if N != grid.n_coarse or nx != op.nx or M != op.M:
+        raise ValueError("initial guess length does not match the time grid")
+    if N % 2:
+        raise NotImplementedError("the 2D CGC needs an even number of subintervals")
+    tables = tables or AlphaTables(build_alpha_circulant(N, cfg.alpha))
+    status = torch.zeros(M, dtype=torch.int32, device="cuda")
+    iters = torch.zeros(M, dtype=torch.int32, device="cuda")
+    inc = torch.full((M, cfg.max_outer_iters), float("nan"), dtype=torch.float64, device="cuda")
+    imag = torch.zeros(M, dtype=torch.float64, device="cuda")
+    B = batch or _batch_size(op, N)
+    active = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for lo in range(0, M, B):
+        hi = min(M, lo + B)
+        ob = op.select(lo, hi)
+        Ub = U[lo:hi]
+        Mb = hi - lo
+        Lt_c, Dinv_c = ob.shifted_factors(tables, N, grid.deltaT)
+        R = empty(Mb, N, nx)
+        nw = int(_lib.query("kle_2d_cgc_work_doubles", Mb, N, op.n))
+        work = torch.zeros(max(nw, 1), dtype=torch.float64, device="cuda")
+        st, it, ih = status[lo:hi], iters[lo:hi], inc[lo:hi]
+        for k in range(1, cfg.max_outer_iters + 1):
+            ob.fgr(Ub, tables, grid, cfg.alpha, R, status=st)
+            active.zero_()
+            _lib.call("kle_2d_cgc_f64", ptr(R), None, ptr(Ub), None, ptr(Lt_c), ptr(Dinv_c), ptr(tables.inv_scaling),
+                      Mb, N, op.n, k, cfg.max_outer_iters, cfg.tol, ptr(st), ptr(it), None, ptr(ih), ptr(active),
+                      ptr(work), nw, stream_ptr())
+            if int(active.item()) == 0:
+                break
+        del Lt_c, Dinv_c, R, work, ob
+    return BatchResult(U, iters, status, inc, imag)

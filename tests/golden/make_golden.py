@@ -24,6 +24,11 @@ Outputs (np.savez_compressed):
            coarse-sweep init: iteration counts, increments, final fields.
   c5s.npz  config-5 analogue (nx=255, N=128, J=8), alpha in {1e-1,1e-2,1e-4}:
            coarse-sweep init, iteration counts, increments, final fields.
+  c3s.npz  2D model (LogNormalKL2D) at small shapes (n=15, N=8, J=4, d=10):
+           3 samples from coarse-sweep init; propagate_fine / propagate_coarse /
+           three_step_solve / cgc_correct single-call vectors (SuperLU paths).
+  c3.npz   2D model at the config-3 shape (n=127, N=32, J=16, d=10): one
+           sample from coarse-sweep init (iteration count, increments, field).
 """
 from __future__ import annotations
 
@@ -48,7 +53,7 @@ from pintuq import pcgc as rpcgc  # noqa: E402
 from pintuq import propagators as rprop  # noqa: E402
 from pintuq import surrogate as rsur  # noqa: E402
 
-from paper_2510_26180_b200.models import LogNormalKL1D, ParameterMap  # noqa: E402
+from paper_2510_26180_b200.models import LogNormalKL1D, LogNormalKL2D, ParameterMap  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -58,9 +63,10 @@ class RefLogNormalKL1D(rmodels.LinearModel):
     model definition (what a maintainer adds to pintuq.models._MODELS)."""
 
     name = "lognormal-kl-1d"
+    inner_cls = LogNormalKL1D
 
     def __init__(self, **kw):
-        self.inner = LogNormalKL1D(**kw)
+        self.inner = self.inner_cls(**kw)
         self.nx = self.inner.nx
         self.parameter_dim = self.inner.parameter_dim
         self.supports = self.inner.supports
@@ -85,6 +91,11 @@ class RefLogNormalKL1D(rmodels.LinearModel):
 
     def fit_maps(self):
         return [ParameterMap("identity", lo, hi) for lo, hi in self.supports]
+
+
+class RefLogNormalKL2D(RefLogNormalKL1D):
+    name = "lognormal-kl-2d"
+    inner_cls = LogNormalKL2D
 
 
 def hermite_surrogate(model, grid, cfg, training, degree, eps_kl=1e-10):
@@ -208,7 +219,62 @@ def make_c5s():
     print(f"c5s done in {time.time() - t0:.1f}s")
 
 
+def make_c3s():
+    t0 = time.time()
+    n, N, J, d = 15, 8, 4, 10
+    model = RefLogNormalKL2D(n=n, d=d, sigma=0.5, ell=0.25)
+    grid = rcore.make_time_grid(1.0, N, J)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    _, eval_rng, _ = rcore.RngStream(2718).split(3)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(3, d))
+    final = np.empty((3, N, n * n))
+    iters = np.empty(3, np.int32)
+    incs = np.full((3, 60), np.nan)
+    cs_all = np.empty_like(final)
+    for i in range(3):
+        xi = rcore.ParameterSample(xi_all[i], id=i)
+        cs = rpar.coarse_sweep_init(model, xi, grid, cfg).states
+        st, it, inc, _ = solve_one(model, grid, cfg, xi, cs)
+        final[i], iters[i], cs_all[i] = st, it, cs
+        incs[i, : len(inc)] = inc
+    xi0 = rcore.ParameterSample(xi_all[0], id=0)
+    rng = np.random.default_rng(13)
+    u_rand = rng.normal(size=n * n)
+    pf_rand = rprop.propagate_fine(model, u_rand, 2 * grid.deltaT, 3 * grid.deltaT, grid, xi0, cfg)
+    pc_rand = rprop.propagate_coarse(model, u_rand, 0.0, grid.deltaT, xi0, cfg)
+    A, _ = model.linear_system(xi0)
+    spec = rpcgc.build_alpha_circulant(N, 1e-3)
+    r_rand = rng.normal(size=(N, n * n))
+    ts_u, ts_imag = rpcgc.three_step_solve(spec, -A, grid.deltaT, r_rand)
+    U_prev = rcore.CoarseTrajectory(model.initial_condition(xi0), cs_all[0])
+    starts = np.vstack([U_prev.initial, cs_all[0][:-1]])
+    F_ends = np.array([rprop.propagate_fine(model, starts[k], grid.coarse_point(k), grid.coarse_point(k + 1),
+                                            grid, xi0, cfg) for k in range(N)])
+    cgc_out, _ = rpcgc.cgc_correct(model, xi0, grid, cfg, U_prev, F_ends)
+    np.savez_compressed(OUT / "c3s.npz", kl_table=model.inner.kl_table, xi=xi_all, coarse_sweep=cs_all,
+                        final=final, iters=iters, increments=incs, u_rand=u_rand, pf_rand=pf_rand,
+                        pc_rand=pc_rand, r_rand=r_rand, ts_u=ts_u, ts_imag=ts_imag, F_ends=F_ends,
+                        cgc_states=cgc_out.states)
+    print(f"c3s done in {time.time() - t0:.1f}s; iters {iters.tolist()}")
+
+
+def make_c3():
+    t0 = time.time()
+    n, N, J, d = 127, 32, 16, 10
+    model = RefLogNormalKL2D(n=n, d=d, sigma=0.5, ell=0.25)
+    grid = rcore.make_time_grid(1.0, N, J)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    _, eval_rng, _ = rcore.RngStream(2718).split(3)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(1, d))
+    xi = rcore.ParameterSample(xi_all[0], id=0)
+    cs = rpar.coarse_sweep_init(model, xi, grid, cfg).states
+    st, it, inc, _ = solve_one(model, grid, cfg, xi, cs)
+    np.savez_compressed(OUT / "c3.npz", xi=xi_all, final=st[None], iters=np.array([it], np.int32),
+                        increments=inc[None])
+    print(f"c3 done in {time.time() - t0:.1f}s; iters {it}")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c5s"]
+    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3"]
     for w in which:
-        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s}[w]()
+        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3}[w]()

@@ -1,0 +1,114 @@
+"""Device parity for the 2D (5-point) path, BASELINE config 3, against the
+golden vectors of the unmodified reference (SuperLU paths) run on the
+``LogNormalKL2D`` plugin (tests/golden/make_golden.py c3s, c3).
+
+Tolerances as in test_gpu_parity: iteration counts exact, fields within 1e-10
+relative (max-norm over the field's max)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def small():
+    from paper_2510_26180_b200 import LogNormalKL2D, SolverConfig, make_time_grid
+
+    return (LogNormalKL2D(n=15, d=10, sigma=0.5, ell=0.25), make_time_grid(1.0, 8, 4),
+            SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60))
+
+
+def test_stencil_on_device_matches_model(cuda, golden):
+    from paper_2510_26180_b200.device import DeviceOperator
+
+    model, _, _ = small()
+    xi = golden("c3s")["xi"]
+    op = DeviceOperator.from_model(model, xi)
+    for s in range(len(xi)):
+        dia, ex, ey = model.stencil(xi[s])
+        assert rel(op.dia[s].cpu().numpy(), dia) <= 1e-14
+        assert rel(op.ex[s].cpu().numpy(), ex) <= 1e-14
+        assert rel(op.ey[s].cpu().numpy(), ey) <= 1e-14
+
+
+def test_propagators_2d(cuda, golden):
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.propagators import coarse_sweep_init, propagate_coarse, propagate_fine
+
+    model, grid, cfg = small()
+    g = golden("c3s")
+    xi0 = ParameterSample(g["xi"][0], id=0)
+    assert rel(propagate_fine(model, g["u_rand"], 2 * grid.deltaT, 3 * grid.deltaT, grid, xi0, cfg),
+               g["pf_rand"]) <= 1e-12
+    assert rel(propagate_coarse(model, g["u_rand"], 0.0, grid.deltaT, xi0, cfg), g["pc_rand"]) <= 1e-12
+    assert rel(coarse_sweep_init(model, xi0, grid, cfg).states, g["coarse_sweep"][0]) <= 1e-12
+
+
+def test_three_step_and_cgc_correct_2d(cuda, golden):
+    from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, cgc_correct, three_step_solve
+
+    model, grid, cfg = small()
+    g = golden("c3s")
+    xi0 = ParameterSample(g["xi"][0], id=0)
+    A, _ = model.linear_system(xi0)
+    u, imag = three_step_solve(build_alpha_circulant(8, 1e-3), -A, grid.deltaT, g["r_rand"])
+    assert rel(u, g["ts_u"]) <= 1e-11 and imag <= 1e-12
+    out, _ = cgc_correct(model, xi0, grid, cfg, CoarseTrajectory(model.initial_condition(), g["coarse_sweep"][0]),
+                         g["F_ends"])
+    assert rel(out.states, g["cgc_states"]) <= 1e-11
+
+
+def test_pcgc_batched_2d_small(cuda, golden):
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    model, grid, cfg = small()
+    g = golden("c3s")
+    op = DeviceOperator.from_model(model, g["xi"])
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    assert rel(U.cpu().numpy(), g["coarse_sweep"]) <= 1e-12
+    res = pcgc_solve_device(op, U, grid, cfg)
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), g["iters"])
+    assert rel(res.states.cpu().numpy(), g["final"]) <= RTOL
+    hist = res.increments.cpu().numpy()
+    for s in range(3):
+        k = int(g["iters"][s])
+        np.testing.assert_allclose(hist[s, :k], g["increments"][s, :k], rtol=1e-6, atol=1e-12)
+
+
+def test_pcgc_single_sample_dropin_2d(cuda, golden):
+    from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample
+    from paper_2510_26180_b200.pcgc import pcgc_solve
+
+    model, grid, cfg = small()
+    g = golden("c3s")
+    xi = ParameterSample(g["xi"][1], id=1)
+    tr = pcgc_solve(model, xi, grid, cfg, CoarseTrajectory(model.initial_condition(), g["coarse_sweep"][1]))
+    assert tr.iterations == int(g["iters"][1])
+    assert rel(tr.trajectory.states, g["final"][1]) <= RTOL
+
+
+def test_c3_full_shape_one_sample(cuda, golden):
+    """n = 127 (nx = 16,129), N = 32, J = 16, d = 10: the config-3 shape."""
+    from paper_2510_26180_b200 import LogNormalKL2D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import coarse_sweep_init_batched
+
+    g = golden("c3")
+    model = LogNormalKL2D(n=127, d=10, sigma=0.5, ell=0.25)
+    grid = make_time_grid(1.0, 32, 16)
+    cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60)
+    op = DeviceOperator.from_model(model, g["xi"])
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    np.testing.assert_array_equal(res.iters.cpu().numpy(), g["iters"])
+    assert rel(res.states.cpu().numpy(), g["final"]) <= RTOL

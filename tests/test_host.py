@@ -185,3 +185,23 @@ def test_host_kl_build_matches_golden(golden):
     coeffs, _, deg = gpc_fit(g["train_points"], zeta, 2, "hermite")
     assert deg == 2
     np.testing.assert_allclose(coeffs, g["coeffs"], atol=1e-9 * np.abs(g["coeffs"]).max())
+
+
+def test_model_2d_contract():
+    from paper_2510_26180_b200.models import LogNormalKL2D
+
+    m = get_model("lognormal-kl-2d", n=9, d=6)
+    assert isinstance(m, LogNormalKL2D) and m.nx == 81 and m.parameter_dim == 6
+    xi = ParameterSample(np.linspace(-1, 1, 6))
+    A, g = m.linear_system(xi)
+    Ad = A.toarray()
+    np.testing.assert_array_equal(Ad, Ad.T)
+    assert np.all(np.linalg.eigvalsh(Ad) > 0)
+    coo = A.tocoo()
+    assert set(np.unique(np.abs(coo.row - coo.col))) <= {0, 1, 9}
+    dia, ex, ey = m.stencil(xi)
+    assert np.all(ex.reshape(9, 9)[:, -1] == 0) and np.all(ey.reshape(9, 9)[-1] == 0)
+    np.testing.assert_allclose(m.kl_table @ m.kl_table.T * m.h ** 2, np.diag(m.kl_eigenvalues), atol=1e-12)
+    assert np.all(np.diff(m.kl_eigenvalues) <= 0)
+    u0 = m.initial_condition()
+    assert u0.shape == (81,) and abs(u0.max() - np.sin(np.pi * 0.5) ** 2) < 1e-12

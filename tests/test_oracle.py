@@ -177,3 +177,27 @@ def test_oracle_three_step_vs_dense(trial):
     scale = max(np.abs(expected).max(), 1e-30)
     assert np.abs(u - expected).max() / scale <= 1e-9
     assert imag <= 1e-10 * max(np.abs(u).max(), 1.0)
+
+
+def test_oracle_2d_matches_reference_goldens(golden):
+    """The per-sample restatement on the 5-point operator (SuperLU paths of
+    pcgc.py:137-145) reproduces the reference bit for bit."""
+    from oracle import ref_port
+    from paper_2510_26180_b200.models import LogNormalKL2D
+
+    g = golden("c3s")
+    m = LogNormalKL2D(n=15, d=10)
+    np.testing.assert_array_equal(m.kl_table, g["kl_table"])
+    for i in range(3):
+        dia, ex, ey = m.stencil(g["xi"][i])
+        op = ref_port.SampleOperator.from_stencil2d(dia, ex, ey, 15, np.ones(225))
+        np.testing.assert_array_equal(ref_port.coarse_sweep(op, m.initial_condition(), 8, 1 / 8), g["coarse_sweep"][i])
+        out = ref_port.pcgc(op, m.initial_condition(), g["coarse_sweep"][i], 8, 4, 1.0, 1e-3, 1e-8, 60)
+        assert out["iters"] == g["iters"][i]
+        np.testing.assert_array_equal(out["states"], g["final"][i])
+    dia, ex, ey = m.stencil(g["xi"][0])
+    op = ref_port.SampleOperator.from_stencil2d(dia, ex, ey, 15, np.ones(225))
+    np.testing.assert_array_equal(ref_port.fine(op, g["u_rand"], 4, 1 / 32), g["pf_rand"])
+    lam, sc = ref_port.alpha_circulant(8, 1e-3)
+    u, _ = ref_port.three_step(lam, sc, ref_port.shifted_solvers(op, lam, 1 / 8), g["r_rand"])
+    np.testing.assert_array_equal(u, g["ts_u"])
