@@ -173,13 +173,13 @@ int kle_2d_kl5pt_f64(const double* xi, int M, int d, const double* kl_table, int
                      double* ex, double* ey, void* stream);
 
 /* _linear_factor (pintuq/propagators.py:25-34) and factor_shifted
- * (pintuq/pcgc.py:137-145) for bandwidth n. lam == NULL: B = shift*I + c*A,
- * real, one matrix per sample: Lrow[M][nx][n] (L(i, i-n+t); caller zeroes it),
- * Lt[M][nx][n] (L(i+1+t, i)), Dinv[M][nx]. lam != NULL (NF interleaved complex
- * shifts): B = lam_f*I + c*A, complex, M*NF matrices, Lt[M*NF][nx][n] and
- * Dinv[M*NF][nx] as interleaved complex; Lrow unused. */
+ * (pintuq/pcgc.py:137-145) for bandwidth n: B = L D L^T, L stored by columns,
+ * Lt[i][t] = L(i+1+t, i), Dinv[i] = 1/D[i]. lam == NULL: B = shift*I + c*A,
+ * real, one matrix per sample (Lt[M][nx][n], Dinv[M][nx]). lam != NULL (NF
+ * interleaved complex shifts): B = lam_f*I + c*A, complex, M*NF matrices,
+ * Lt[M*NF][nx][n] and Dinv[M*NF][nx] as interleaved complex. */
 int kle_2d_factor_f64(const double* dia, const double* ex, const double* ey, int M, int n, const double* lam,
-                      int NF, double shift, double c, double* Lrow, double* Lt, double* Dinv, void* stream);
+                      int NF, double shift, double c, double* Lt, double* Dinv, void* stream);
 
 /* Scratch (doubles) of kle_2d_fgr_f64 / kle_2d_sweep_f64 for M samples of N
  * (or Q) right-hand sides. */
@@ -191,14 +191,14 @@ size_t kle_2d_fine_work_doubles(int M, int N, int n);
  * U_{k-1} (u0 for k = 0), prev_0 = alpha U_{N-1}. Real factor of I + dt A.
  * F_given != NULL (stand-alone cgc_correct): no sweep, F_k = F_given[s][k]. */
 int kle_2d_fgr_f64(const double* U, const double* u0, const double* F_given, const double* dia, const double* ex,
-                   const double* ey, const double* Lrow, const double* Lt, const double* Dinv, const double* scaling,
+                   const double* ey, const double* Lt, const double* Dinv, const double* scaling,
                    const int32_t* active, int M, int N, int n, int J, double dt, double dT, double g0,
                    double alpha, double* work, size_t work_doubles, double* Rout, void* stream);
 
 /* propagate_fine / propagate_coarse / fine_reference (pintuq/propagators.py
  * :121-176): out[s][q][g] = F^{(g+1)}(start[s][q]), segments of J steps of h. */
 int kle_2d_sweep_f64(const double* start, const double* dia, const double* ex, const double* ey,
-                     const double* Lrow, const double* Lt, const double* Dinv, int M, int Q, int n, int J,
+                     const double* Lt, const double* Dinv, int M, int Q, int n, int J,
                      int nseg, double h, double g0, double* work, size_t work_doubles, double* out, void* stream);
 
 /* Scratch (doubles) of kle_2d_cgc_f64. */

@@ -37,10 +37,10 @@ _SIGS = {
     "kle_pcgc_solve_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _i, _p, _p, _p, _p,
                             _p, _z, _p], _i),
     "kle_2d_kl5pt_f64": ([_p, _i, _i, _p, _i, _d, _p, _p, _p, _p], _i),
-    "kle_2d_factor_f64": ([_p, _p, _p, _i, _i, _p, _i, _d, _d, _p, _p, _p, _p], _i),
+    "kle_2d_factor_f64": ([_p, _p, _p, _i, _i, _p, _i, _d, _d, _p, _p, _p], _i),
     "kle_2d_fine_work_doubles": ([_i, _i, _i], _z),
-    "kle_2d_fgr_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _p, _z, _p, _p], _i),
-    "kle_2d_sweep_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _d, _p, _z, _p, _p], _i),
+    "kle_2d_fgr_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _p, _z, _p, _p], _i),
+    "kle_2d_sweep_f64": ([_p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _d, _p, _z, _p, _p], _i),
     "kle_2d_cgc_work_doubles": ([_i, _i, _i], _z),
     "kle_2d_cgc_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z, _p], _i),
     "kle_gpc_basis_f64": ([_p, _i, _i, _i, _p, _i, _p, _p, _p], _i),

@@ -22,8 +22,8 @@
 //                      (n+1) x (n+1) active window distributed over the CTA
 //                      (entry (row slot, diagonal offset) per thread, real parts
 //                      in shared memory, imaginary parts in registers); writes
-//                      L by columns (Lt, backward solves / column-form forward)
-//                      and, for the real factor, by rows (Lrow, dot-form forward)
+//                      L by columns (Lt[i][t] = L(i+1+t, i)), read by both
+//                      substitution directions
 //   fine2d_kernel      one warp per (sample, 32 subintervals): J BE steps on 32
 //                      right-hand sides in the lanes (dot-form banded solves, the
 //                      last n solved rows in a shared-memory window), then the
@@ -114,24 +114,30 @@ __global__ void kl5pt_kernel(const double* __restrict__ xi, int M, int d, const 
 }
 
 // ---------------------------------------------------------------------------
-// Banded L D L^T of B = shift I + c A, one CTA (1024 threads) per matrix.
-// Window entry (rho, delta): row r with r = rho (mod n+1), r in [i, i+n], and
-// column r - delta. Thread t owns entries e = t + m * 1024 (rho = e / (n+1),
-// delta = e % (n+1)); real parts in shared memory, imaginary parts in registers.
-// Step i publishes column i (window position j = delta), eliminates, emits
-// Lt[i][t] = L(i+1+t, i), Dinv[i], and loads row i+n+1 into row i's slot.
+// Banded L D L^T of B = shift I + c A, one CTA per matrix.
+// Window entry (rho, delta): row r with r = rho (mod W), W = n+1, r in
+// [i, i+n], column r - delta. Each thread owns two fixed diagonal offsets
+// (delta, W-1-delta) in a set of row slots, real parts in shared memory,
+// imaginary parts in registers. Step i:
+// publish column i (the entry with delta == window position j), one barrier,
+// eliminate W(r, c) -= (W(r,i) / d) W(c,i), emit Lt[i][t] = L(i+1+t, i) and
+// Dinv[i], and load row i+n+1 into row i's slot from a shared-memory ring of
+// operator values prefetched BF_AHEAD steps ahead (no global latency on the
+// per-step critical path).
 // ---------------------------------------------------------------------------
-constexpr int BF_NT = 1024;
-constexpr int BF_E = 16;  // (n+1)^2 <= BF_NT * BF_E  =>  n <= 127
+// NT threads per CTA, 16384 / NT window entries per thread (W <= 128); 1024
+// for both (512 threads for the complex factor measured slower)
+constexpr int BF_RING = 64;     // operator-row ring (rows i+W .. i+W+BF_AHEAD)
+constexpr int BF_AHEAD = 32;
 
-template <bool C>
-__global__ void __launch_bounds__(BF_NT, 1)
+template <bool C, int NT>
+__global__ void __launch_bounds__(NT, 1)
     band_factor_kernel(const double* __restrict__ dia, const double* __restrict__ ex,
                        const double* __restrict__ ey, int n, const double* __restrict__ lam, int NF,
-                       double shift_re, double c, double* __restrict__ Lrow, double* __restrict__ Lt,
-                       double* __restrict__ Dinv) {
+                       double shift_re, double c, double* __restrict__ Lt, double* __restrict__ Dinv) {
   using S = Sc<C>;
   using T = typename S::T;
+  constexpr int E = 16384 / NT;  // entries per thread (2 offsets x E/2 row slots)
   const int nx = n * n, W = n + 1;
   const int phi = blockIdx.x, s = phi / NF, f = phi - s * NF;
   const double* d_ = dia + (size_t)s * nx;
@@ -139,169 +145,299 @@ __global__ void __launch_bounds__(BF_NT, 1)
   const double* ey_ = ey + (size_t)s * nx;
   const T shift = C ? S::mk(lam[2 * f], lam[2 * f + 1]) : S::mk(shift_re, 0.0);
   extern __shared__ __align__(16) double smem[];
-  double* wre = smem;                              // [BF_E][BF_NT]
-  T* col = reinterpret_cast<T*>(wre + BF_E * BF_NT);  // [2][W]
-  double wim[BF_E];
+  double* wre = smem;                                   // [E][NT]
+  T* col = reinterpret_cast<T*>(wre + E * NT);    // [2][W]
+  double* ring = reinterpret_cast<double*>(col + 2 * W);  // [BF_RING][3]: c*dia[r], c*ex[r-1], c*ey[r-n]
   const int tid = threadIdx.x;
-  auto entryB = [&](int r, int delta) -> T {  // B(r, r - delta); identity padding beyond nx
-    if (r >= nx) return delta == 0 ? S::mk(1.0, 0.0) : S::zero();
-    if (r - delta < 0) return S::zero();
-    if (delta == 0) return S::add(shift, S::mk(c * d_[r], 0.0));
+  // balanced ownership: thread = (diagonal pair p, row group rho0); it holds the
+  // offsets delta_a = p and delta_b = W-1-p in the row slots rho0 + Qr m, so
+  // the active work per step (delta < window position) is even across threads
+  const int H = (W + 1) / 2, Qr = NT / H, E2 = (W + Qr - 1) / Qr;
+  const int pair = tid % H, rho0 = tid / H;
+  const int dl[2] = {pair, W - 1 - pair};
+  const bool two = dl[1] != dl[0];
+  auto load_row = [&](int r) {  // operator values of row r (identity padding beyond nx)
+    double* e = ring + 3 * (r % BF_RING);
+    e[0] = (r < nx) ? c * d_[r] : 0.0;
+    e[1] = (r < nx && r >= 1) ? c * ex_[r - 1] : 0.0;
+    e[2] = (r < nx && r >= n) ? c * ey_[r - n] : 0.0;
+  };
+  auto entryB = [&](int r, int dlt, const double* e) -> T {  // B(r, r - dlt) from ring values e
+    if (r >= nx) return dlt == 0 ? S::mk(1.0, 0.0) : S::zero();
+    if (r - dlt < 0) return S::zero();
+    if (dlt == 0) return S::add(shift, S::mk(e[0], 0.0));
     double v = 0.0;
-    if (delta == 1) v += c * ex_[r - 1];
-    if (delta == n) v += c * ey_[r - n];
+    if (dlt == 1) v += e[1];
+    if (dlt == n) v += e[2];
     return S::mk(v, 0.0);
   };
-  // per entry: (delta << 8) | jpos, jpos = window position of the entry's row at
-  // step i; delta = 255 marks an unused entry (shared memory, to save registers)
-  int* dj = reinterpret_cast<int*>(col + 2 * W) + tid;  // [BF_E][BF_NT] in shared memory
+  for (int k = W + tid; k < W + BF_AHEAD; k += NT) load_row(k);
+  double pre[3] = {0.0, 0.0, 0.0};  // thread NT-1: operator row in flight to the ring
+  double wim[E];
 #pragma unroll
-  for (int m = 0; m < BF_E; ++m) {
-    const int e = tid + m * BF_NT;
-    T v = S::zero();
-    dj[m * BF_NT] = 255 << 8;
-    if (e < W * W) {
-      dj[m * BF_NT] = ((e % W) << 8) | (e / W);  // initial rows 0..n sit in slots 0..n
-      v = entryB(e / W, e % W);
+  for (int m = 0; m < E / 2; ++m) {
+    const int rho = rho0 + Qr * m;
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      T v = S::zero();
+      if (m < E2 && rho < W && (w == 0 || two)) {  // rows 0..n in slots 0..n (operator from global memory)
+        const double e[3] = {rho < nx ? c * d_[rho] : 0.0, (rho < nx && rho >= 1) ? c * ex_[rho - 1] : 0.0,
+                             (rho < nx && rho >= n) ? c * ey_[rho - n] : 0.0};
+        v = entryB(rho, dl[w], e);
+      }
+      wre[(2 * m + w) * NT + tid] = S::re(v);
+      wim[2 * m + w] = S::im(v);
     }
-    wre[m * BF_NT + tid] = S::re(v);
-    wim[m] = S::im(v);
   }
+  __syncthreads();
   T* Lt_ = reinterpret_cast<T*>(Lt) + (size_t)phi * nx * n;
   T* Di_ = reinterpret_cast<T*>(Dinv) + (size_t)phi * nx;
-  double* Lr_ = Lrow ? Lrow + (size_t)phi * nx * n : nullptr;
   for (int i = 0; i < nx; ++i) {
     T* cb = col + (i & 1) * W;
+    const int ri = i % W;
 #pragma unroll
-    for (int m = 0; m < BF_E; ++m) {
-      const int delta = dj[m * BF_NT] >> 8, jpos = dj[m * BF_NT] & 255;
-      if (delta == jpos) cb[jpos] = S::mk(wre[m * BF_NT + tid], wim[m]);
+    for (int m = 0; m < E / 2; ++m) {
+      const int rho = rho0 + Qr * m;
+      if (m >= E2 || rho >= W) continue;
+      const int jpos = rho - ri + (rho < ri ? W : 0);
+#pragma unroll
+      for (int w = 0; w < 2; ++w)
+        if ((w == 0 || two) && dl[w] == jpos) cb[jpos] = S::mk(wre[(2 * m + w) * NT + tid], wim[2 * m + w]);
+    }
+    if (tid == NT - 1) {  // prefetch ring: store the row loaded last step, load the next one
+      if (i > 0) {
+        double* e = ring + 3 * ((i - 1 + W + BF_AHEAD) % BF_RING);
+        e[0] = pre[0];
+        e[1] = pre[1];
+        e[2] = pre[2];
+      }
+      const int r = i + W + BF_AHEAD;
+      pre[0] = (r < nx) ? c * d_[r] : 0.0;
+      pre[1] = (r < nx && r >= 1) ? c * ex_[r - 1] : 0.0;
+      pre[2] = (r < nx && r >= n) ? c * ey_[r - n] : 0.0;
     }
     __syncthreads();
     const T dinv = S::rcp(cb[0]);
+    const double* e = ring + 3 * ((i + W) % BF_RING);
 #pragma unroll
-    for (int m = 0; m < BF_E; ++m) {
-      const int delta = dj[m * BF_NT] >> 8, jpos = dj[m * BF_NT] & 255;
-      if (delta == 255) continue;
-      if (jpos >= 1 && delta < jpos) {
-        const T l = S::mul(cb[jpos], dinv);
-        const T w = S::fms(l, cb[jpos - delta], S::mk(wre[m * BF_NT + tid], wim[m]));
-        wre[m * BF_NT + tid] = S::re(w);
-        wim[m] = S::im(w);
-      } else if (jpos == 0) {  // row i leaves; row i + n + 1 enters its slot
-        const T v = entryB(i + W, delta);
-        wre[m * BF_NT + tid] = S::re(v);
-        wim[m] = S::im(v);
+    for (int m = 0; m < E / 2; ++m) {
+      const int rho = rho0 + Qr * m;
+      if (m >= E2 || rho >= W) continue;
+      const int jpos = rho - ri + (rho < ri ? W : 0);
+      if (jpos == 0) {  // row i leaves; row i + n + 1 enters its slot
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          if (w == 1 && !two) continue;
+          const T v = entryB(i + W, dl[w], e);
+          wre[(2 * m + w) * NT + tid] = S::re(v);
+          wim[2 * m + w] = S::im(v);
+        }
+        continue;
       }
-      dj[m * BF_NT] = (delta << 8) | (jpos == 0 ? W - 1 : jpos - 1);
+      if (dl[0] >= jpos && (!two || dl[1] >= jpos)) continue;
+      const T l = S::mul(cb[jpos], dinv);
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        if ((w == 1 && !two) || dl[w] >= jpos) continue;
+        const T v = S::fms(l, cb[jpos - dl[w]], S::mk(wre[(2 * m + w) * NT + tid], wim[2 * m + w]));
+        wre[(2 * m + w) * NT + tid] = S::re(v);
+        wim[2 * m + w] = S::im(v);
+      }
     }
     if (tid < n) {
       const int r = i + 1 + tid;
       const T l = (r < nx) ? S::mul(cb[tid + 1], dinv) : S::zero();
       Lt_[(size_t)i * n + tid] = l;
-      if constexpr (!C) {
-        if (Lr_ && r < nx) Lr_[(size_t)r * n + (n - 1 - tid)] = l;  // L(r, i) = Lrow[r][i - r + n]
-      }
     }
     if (tid == 0) Di_[i] = dinv;
   }
 }
 
 // ---------------------------------------------------------------------------
-// Fine sweeps, one warp per (sample, group of 32 subintervals). Lanes are the
-// right-hand sides; each BE step is a forward (Lrow, dot form) and a backward
-// (Lt, dot form) banded substitution over the window of the last n solved
-// rows (shared memory, [W][33]). State X and scratch Z: [slot][nx][32].
+// Fine sweeps, one warp per (sample, group of SB_R subintervals), the lanes
+// are the right-hand sides; each BE step is a forward and a backward banded
+// substitution (subst_pass), both reading the column-band factor Lt. State X and scratch Z: [slot][nx][SB_R].
 // ---------------------------------------------------------------------------
 struct Fine2dArgs {
   const double* start;   // mode 0: U [M][N][nx]; mode 1: start rows [M][Q][nx]
   const double* u0;      // mode 0: [nx]
   const double* F_given; // mode 0, optional [M][N][nx]: skip the sweep, take these F ends
   const double *dia, *ex, *ey;
-  const double *Lrow, *Lt, *Dinv;  // per sample: [nx][n], [nx][n], [nx]
+  const double *Lt, *Dinv;         // per sample: [nx][n] (L(i+1+t, i)), [nx]
   const double* scaling;           // mode 0: [N]
   const int32_t* active;           // mode 0: [M] or null
-  double* X;                       // [M * G][nx][32]
-  double* Z;                       // [M * G][nx][32]
+  double* X;                       // [M * G][nx][SB_R]
+  double* Z;                       // [M * G][nx][SB_R]
   double* out;                     // mode 0: R [M][N][nx]; mode 1: [M][Q][nseg][nx]
   int M, N, n, J, nseg, mode;      // mode 0: fgr, mode 1: sweep (N = Q)
   double dt, dT, g0, alpha;
 };
 
+// One banded substitution pass over the sequence positions p = 0..nx-1 (row
+// p forward, row nx-1-p backward), 32 right-hand sides in the lanes:
+//   v_p = b_p - sum_{q in [p-n, p)} c(p, q) v_q
+// forward  c = L(i, k)     = Lt[k][i - k - 1]
+// backward c = L(k, i)     = Lt[i][k - i - 1]   (k = row of position q)
+// Positions are processed in blocks of RB: the far part (q < p0) is one
+// register-blocked sweep over the window of the last n values (each window
+// load feeds RB FMAs; the block's coefficients are staged skewed in shared
+// memory, cst[qq][a] with qq = q - (p0 - n), straight from the registers the
+// next block's rows are prefetched into), the near part (p0 <= q < p) a small
+// triangular fix-up whose coefficients sit at cst[n + a2][a]. Window:
+// [WP][SB_R], WP = 2^ceil(log2(n+1)), slot = q & (WP-1), zero for q < 0.
+constexpr int SB_RB = 8;
+constexpr int SB_PF = 4;   // ceil(127 / 32): coefficient values per lane and row
+constexpr int SB_R = 32;   // right-hand sides per warp (16: the two lane halves split the window sweep;
+                           // measured slower at config 3: twice the coefficient traffic)
+constexpr int SB_H = 32 / SB_R;
+
+template <bool BACK>
+__device__ __forceinline__ void subst_pass(const double* __restrict__ Lc, const double* __restrict__ bsrc,
+                                           double badd, const double* __restrict__ Di, double* __restrict__ out,
+                                           double* win, double* cst, int n, int WP, int nx, int lane) {
+  constexpr int RB = SB_RB;
+  const int wm = WP - 1;
+  const int r = lane & (SB_R - 1), h = lane / SB_R;
+  for (int q = lane; q < WP * SB_R; q += 32) win[q] = 0.0;
+  for (int q = lane; q < (n + RB) * RB; q += 32) cst[q] = 0.0;
+  auto row_of = [&](int p) { return BACK ? nx - 1 - p : p; };
+  double pf[RB][SB_PF], pn = 0.0;
+  // forward: cst[u][a] = L(p0+a, p0-n+u) = Lt[p0-n+u][n-1-u+a] (a <= u), near
+  //          cst[n+a2][a] = L(p0+a, p0+a2) = Lt[p0+a2][a-a2-1] (a2 < a)
+  // backward: cst[a+n-1-u][a] = Lt[row(p0+a)][u] (covers the near part too)
+  auto fetch = [&](int p0) {
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int m = 0; m < SB_PF; ++m) {
+        const int u = lane + 32 * m;
+        if (BACK) {
+          pf[a][m] = (p0 + a < nx && u < n) ? __ldg(Lc + (size_t)row_of(p0 + a) * n + u) : 0.0;
+        } else {
+          const int k = p0 - n + u;
+          pf[a][m] = (u < n && a <= u && k >= 0 && p0 + a < nx) ? __ldg(Lc + (size_t)k * n + (n - 1 - u + a)) : 0.0;
+        }
+      }
+    if (!BACK) {
+      const int a2 = (lane & 63) / RB, a = lane % RB;  // lanes 0..31 cover a2 < 4; second pass below
+      pn = (a2 < a && p0 + a < nx) ? __ldg(Lc + (size_t)(p0 + a2) * n + (a - a2 - 1)) : 0.0;
+    }
+  };
+  double pn2 = 0.0;
+  auto fetch2 = [&](int p0) {  // forward near part, a2 >= 4
+    if (!BACK) {
+      const int a2 = 4 + lane / RB, a = lane % RB;
+      pn2 = (a2 < a && p0 + a < nx) ? __ldg(Lc + (size_t)(p0 + a2) * n + (a - a2 - 1)) : 0.0;
+    }
+  };
+  fetch(0);
+  fetch2(0);
+  for (int p0 = 0; p0 < nx; p0 += RB) {
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int m = 0; m < SB_PF; ++m) {
+        const int u = lane + 32 * m;
+        if (u < n) cst[(BACK ? a + n - 1 - u : u) * RB + a] = pf[a][m];
+      }
+    if (!BACK) {
+      cst[(n + lane / RB) * RB + lane % RB] = pn;
+      cst[(n + 4 + lane / RB) * RB + lane % RB] = pn2;
+    }
+    double bv[RB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) bv[a] = (p0 + a < nx) ? bsrc[(size_t)row_of(p0 + a) * SB_R + r] + badd : 0.0;
+    __syncwarp();
+    if (p0 + RB < nx) {  // in flight during the sweep
+      fetch(p0 + RB);
+      fetch2(p0 + RB);
+    }
+    double acc[RB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) acc[a] = 0.0;
+    const int q0 = p0 - n;
+#pragma unroll 4
+    for (int qq = h; qq < n; qq += SB_H) {
+      const double y = win[((q0 + qq) & wm) * SB_R + r];
+#pragma unroll
+      for (int a = 0; a < RB; a += 2) {
+        const double2 c = *reinterpret_cast<const double2*>(cst + qq * RB + a);
+        acc[a] = fma(c.x, y, acc[a]);
+        acc[a + 1] = fma(c.y, y, acc[a + 1]);
+      }
+    }
+    if constexpr (SB_H > 1) {
+#pragma unroll
+      for (int a = 0; a < RB; ++a) acc[a] += __shfl_xor_sync(KLE_FULL_MASK, acc[a], SB_R);
+    }
+    double yv[RB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) {
+      const int p = p0 + a;
+      double v = bv[a] - acc[a];
+#pragma unroll
+      for (int a2 = 0; a2 < a; ++a2) v = fma(-cst[(n + a2) * RB + a], yv[a2], v);
+      yv[a] = v;
+      if (p < nx && h == 0) {
+        const int i = row_of(p);
+        win[(p & wm) * SB_R + r] = v;
+        out[(size_t)i * SB_R + r] = Di ? v * Di[i] : v;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__host__ __device__ inline int win_pow2(int n) {
+  int w = 1;
+  while (w < n + 1) w <<= 1;
+  return w;
+}
+
 __device__ __forceinline__ void fine2d_steps(const Fine2dArgs& a, int s, double* __restrict__ X,
-                                             double* __restrict__ Z, double* win, double* lrow, int lane) {
-  const int n = a.n, nx = n * n, W = n + 1;
-  const double* Lr = a.Lrow + (size_t)s * nx * n;
+                                             double* __restrict__ Z, double* win, double* cst, int lane) {
+  const int n = a.n, nx = n * n, WP = win_pow2(n);
   const double* Lt = a.Lt + (size_t)s * nx * n;
   const double* Di = a.Dinv + (size_t)s * nx;
   const double hg = a.dt * a.g0;
   for (int step = 0; step < a.J; ++step) {
-    for (int q = lane; q < W * 33; q += 32) win[q] = 0.0;
-    __syncwarp();
-    for (int i = 0; i < nx; ++i) {  // forward: y_i = b_i - sum_k L(i,k) y_k
-      for (int t = lane; t < n; t += 32) lrow[t] = Lr[(size_t)i * n + t];
-      __syncwarp();
-      double acc = 0.0;
-      int slot = i % W;  // slot of k = i - n + t walks from (i+1) % W
-      for (int t = 0; t < n; ++t) {
-        if (++slot == W) slot = 0;
-        acc = fma(lrow[t], win[slot * 33 + lane], acc);
-      }
-      const double y = (X[(size_t)i * 32 + lane] + hg) - acc;
-      win[(i % W) * 33 + lane] = y;
-      Z[(size_t)i * 32 + lane] = y * Di[i];
-      __syncwarp();
-    }
-    for (int q = lane; q < W * 33; q += 32) win[q] = 0.0;
-    __syncwarp();
-    for (int i = nx - 1; i >= 0; --i) {  // backward: x_i = z_i - sum_t L(i+1+t, i) x_{i+1+t}
-      for (int t = lane; t < n; t += 32) lrow[t] = Lt[(size_t)i * n + t];
-      __syncwarp();
-      double acc = 0.0;
-      int slot = i % W;
-      for (int t = 0; t < n; ++t) {
-        if (++slot == W) slot = 0;
-        acc = fma(lrow[t], win[slot * 33 + lane], acc);
-      }
-      const double x = Z[(size_t)i * 32 + lane] - acc;
-      win[(i % W) * 33 + lane] = x;
-      X[(size_t)i * 32 + lane] = x;
-      __syncwarp();
-    }
+    subst_pass<false>(Lt, X, hg, Di, Z, win, cst, n, WP, nx, lane);   // y = L^{-1}(x + h g); Z = D^{-1} y
+    subst_pass<true>(Lt, Z, 0.0, nullptr, X, win, cst, n, WP, nx, lane);  // x = L^{-T} Z
   }
 }
 
-__global__ void __launch_bounds__(32) fine2d_kernel(Fine2dArgs a) {
-  const int n = a.n, nx = n * n, W = n + 1;
-  const int G = (a.N + 31) / 32;
+__global__ void __launch_bounds__(32, 5) fine2d_kernel(Fine2dArgs a) {
+  const int n = a.n, nx = n * n;
+  const int G = (a.N + SB_R - 1) / SB_R;
   const int s = blockIdx.x / G, g = blockIdx.x % G;
   if (a.mode == 0 && a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
-  const int lane = threadIdx.x;
-  const int q = g * 32 + lane;  // subinterval (mode 0) / start row (mode 1)
+  const int lane = threadIdx.x, rr = lane & (SB_R - 1), hh = lane / SB_R;
+  const int q = g * SB_R + rr;  // subinterval (mode 0) / start row (mode 1)
   const bool live = q < a.N;
   extern __shared__ __align__(16) double sm2[];
-  double* win = sm2;             // [W][33]
-  double* lrow = win + W * 33;   // [n]
-  double* X = a.X + (size_t)blockIdx.x * nx * 32;
-  double* Z = a.Z + (size_t)blockIdx.x * nx * 32;
+  double* win = sm2;                       // [WP][SB_R]
+  double* cst = win + win_pow2(n) * SB_R;  // [n + SB_RB][SB_RB]
+  double* X = a.X + (size_t)blockIdx.x * nx * SB_R;
+  double* Z = a.Z + (size_t)blockIdx.x * nx * SB_R;
   const double* src;
   if (a.mode == 0) src = (q == 0 || !live) ? a.u0 : a.start + ((size_t)s * a.N + (q - 1)) * nx;
   else src = a.start + ((size_t)s * a.N + (live ? q : 0)) * nx;
   const double* x0 = (a.mode == 0 && a.F_given) ? a.F_given + ((size_t)s * a.N + (live ? q : 0)) * nx : src;
-  for (int i = 0; i < nx; ++i) X[(size_t)i * 32 + lane] = live ? x0[i] : 0.0;
+  for (int i = hh; i < nx; i += SB_H) X[(size_t)i * SB_R + rr] = live ? x0[i] : 0.0;
   __syncwarp();
   if (a.mode == 1) {
     for (int sg = 0; sg < a.nseg; ++sg) {
-      fine2d_steps(a, s, X, Z, win, lrow, lane);
+      fine2d_steps(a, s, X, Z, win, cst, lane);
       if (live) {
         double* o = a.out + (((size_t)s * a.N + q) * a.nseg + sg) * nx;
-        for (int i = 0; i < nx; ++i) o[i] = X[(size_t)i * 32 + lane];
+        for (int i = hh; i < nx; i += SB_H) o[i] = X[(size_t)i * SB_R + rr];
       }
       __syncwarp();
     }
     return;
   }
-  if (!a.F_given) fine2d_steps(a, s, X, Z, win, lrow, lane);
+  if (!a.F_given) fine2d_steps(a, s, X, Z, win, cst, lane);
   __syncwarp();
   if (!live) return;
   // rhs_n = scaling_n ((I + dT A) F_n - prev_n); prev_0 = alpha U_{N-1}
@@ -312,13 +448,14 @@ __global__ void __launch_bounds__(32) fine2d_kernel(Fine2dArgs a) {
   const double pmul = (q == 0) ? a.alpha : 1.0;
   const double sc = a.scaling[q];
   double* o = a.out + ((size_t)s * a.N + q) * nx;
-  for (int i = 0; i < nx; ++i) {
-    const double x = X[(size_t)i * 32 + lane];
+  const double* Xq = X + rr;
+  for (int i = hh; i < nx; i += SB_H) {
+    const double x = Xq[(size_t)i * SB_R];
     double Ax = dd[i] * x;
-    if (i + 1 < nx) Ax = fma(ex[i], X[(size_t)(i + 1) * 32 + lane], Ax);
-    if (i >= 1) Ax = fma(ex[i - 1], X[(size_t)(i - 1) * 32 + lane], Ax);
-    if (i + n < nx) Ax = fma(ey[i], X[(size_t)(i + n) * 32 + lane], Ax);
-    if (i >= n) Ax = fma(ey[i - n], X[(size_t)(i - n) * 32 + lane], Ax);
+    if (i + 1 < nx) Ax = fma(ex[i], Xq[(size_t)(i + 1) * SB_R], Ax);
+    if (i >= 1) Ax = fma(ex[i - 1], Xq[(size_t)(i - 1) * SB_R], Ax);
+    if (i + n < nx) Ax = fma(ey[i], Xq[(size_t)(i + n) * SB_R], Ax);
+    if (i >= n) Ax = fma(ey[i - n], Xq[(size_t)(i - n) * SB_R], Ax);
     const double rhs = fma(a.dT, Ax, x) - pmul * pv[i];
     o[i] = sc * rhs;
   }
@@ -529,62 +666,61 @@ extern "C" int kle_2d_kl5pt_f64(const double* xi, int M, int d, const double* kl
 }
 
 extern "C" int kle_2d_factor_f64(const double* dia, const double* ex, const double* ey, int M, int n,
-                                const double* lam, int NF, double shift, double c, double* Lrow, double* Lt,
-                                double* Dinv, void* stream) {
-  if (M < 0 || n < 1 || (n + 1) * (n + 1) > BF_NT * BF_E || (lam && NF < 1))
+                                 const double* lam, int NF, double shift, double c, double* Lt, double* Dinv,
+                                 void* stream) {
+  if (M < 0 || n < 1 || n > 127 || (lam && NF < 1))
     return set_error(KLE_ERR_INVALID, "factor2d: bad dims (n <= 127)");
   if (M == 0) return KLE_OK;
   const int W = n + 1;
   if (lam) {
-    const size_t smem = sizeof(double) * BF_E * BF_NT + 2 * W * sizeof(Cplx) + sizeof(int) * BF_E * BF_NT;
-    cudaFuncSetAttribute(band_factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    band_factor_kernel<true><<<(unsigned)(M * NF), BF_NT, smem, KLE2D_STREAM(stream)>>>(
-        dia, ex, ey, n, lam, NF, 0.0, c, nullptr, Lt, Dinv);
+    const size_t smem = sizeof(double) * 16384 + 2 * W * sizeof(Cplx) + sizeof(double) * 3 * BF_RING;
+    cudaFuncSetAttribute(band_factor_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    band_factor_kernel<true, 1024><<<(unsigned)(M * NF), 1024, smem, KLE2D_STREAM(stream)>>>(
+        dia, ex, ey, n, lam, NF, 0.0, c, Lt, Dinv);
   } else {
-    const size_t smem = sizeof(double) * BF_E * BF_NT + 2 * W * sizeof(double) + sizeof(int) * BF_E * BF_NT;
-    cudaFuncSetAttribute(band_factor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    band_factor_kernel<false><<<(unsigned)M, BF_NT, smem, KLE2D_STREAM(stream)>>>(dia, ex, ey, n, nullptr, 1, shift,
-                                                                                  c, Lrow, Lt, Dinv);
+    const size_t smem = sizeof(double) * 16384 + 2 * W * sizeof(double) + sizeof(double) * 3 * BF_RING;
+    cudaFuncSetAttribute(band_factor_kernel<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    band_factor_kernel<false, 1024><<<(unsigned)M, 1024, smem, KLE2D_STREAM(stream)>>>(dia, ex, ey, n, nullptr, 1, shift,
+                                                                                  c, Lt, Dinv);
   }
   return check_launch("band_factor_kernel");
 }
 
 extern "C" size_t kle_2d_fine_work_doubles(int M, int N, int n) {
-  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 2 * (size_t)M * ((N + 31) / 32) * n * n * 32;
+  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 2 * (size_t)M * ((N + SB_R - 1) / SB_R) * n * n * SB_R;
 }
 
 static int fine2d_launch(Fine2dArgs& a, void* stream) {
-  const int G = (a.N + 31) / 32;
-  const int W = a.n + 1;
-  const size_t smem = sizeof(double) * ((size_t)W * 33 + a.n);
+  const int G = (a.N + SB_R - 1) / SB_R;
+  const size_t smem = sizeof(double) * ((size_t)win_pow2(a.n) * SB_R + (size_t)(a.n + SB_RB) * SB_RB);
+  cudaFuncSetAttribute(fine2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fine2d_kernel<<<(unsigned)(a.M * G), 32, smem, KLE2D_STREAM(stream)>>>(a);
   return check_launch("fine2d_kernel");
 }
 
 extern "C" int kle_2d_fgr_f64(const double* U, const double* u0, const double* F_given, const double* dia,
-                              const double* ex,
-                             const double* ey, const double* Lrow, const double* Lt, const double* Dinv,
-                             const double* scaling, const int32_t* active, int M, int N, int n, int J,
+                              const double* ex, const double* ey, const double* Lt, const double* Dinv,
+                              const double* scaling, const int32_t* active, int M, int N, int n, int J,
                              double dt, double dT, double g0, double alpha, double* work, size_t work_doubles,
                              double* Rout, void* stream) {
   if (M < 0 || N < 1 || n < 1 || n > 127 || J < 1) return set_error(KLE_ERR_INVALID, "fgr2d: bad dims");
   if (M == 0) return KLE_OK;
   const size_t need = kle_2d_fine_work_doubles(M, N, n);
   if (work_doubles < need) return set_error(KLE_ERR_WORKSPACE, "fgr2d: workspace too small");
-  Fine2dArgs a{U, u0, F_given, dia, ex, ey, Lrow, Lt, Dinv, scaling, active, work, work + need / 2, Rout,
+  Fine2dArgs a{U, u0, F_given, dia, ex, ey, Lt, Dinv, scaling, active, work, work + need / 2, Rout,
                M, N, n, J, 1, 0, dt, dT, g0, alpha};
   return fine2d_launch(a, stream);
 }
 
 extern "C" int kle_2d_sweep_f64(const double* start, const double* dia, const double* ex, const double* ey,
-                               const double* Lrow, const double* Lt, const double* Dinv, int M, int Q, int n,
+                                const double* Lt, const double* Dinv, int M, int Q, int n,
                                int J, int nseg, double h, double g0, double* work, size_t work_doubles,
                                double* out, void* stream) {
   if (M < 0 || Q < 1 || n < 1 || n > 127 || J < 1 || nseg < 1) return set_error(KLE_ERR_INVALID, "sweep2d: bad dims");
   if (M == 0) return KLE_OK;
   const size_t need = kle_2d_fine_work_doubles(M, Q, n);
   if (work_doubles < need) return set_error(KLE_ERR_WORKSPACE, "sweep2d: workspace too small");
-  Fine2dArgs a{start, nullptr, nullptr, dia, ex, ey, Lrow, Lt, Dinv, nullptr, nullptr, work, work + need / 2, out,
+  Fine2dArgs a{start, nullptr, nullptr, dia, ex, ey, Lt, Dinv, nullptr, nullptr, work, work + need / 2, out,
                M, Q, n, J, nseg, 1, h, 0.0, g0, 0.0};
   return fine2d_launch(a, stream);
 }

@@ -111,16 +111,15 @@ class DeviceOperator2D:
 
     # -- factors -------------------------------------------------------------
     def fine_factor(self, h: float):
-        """(Lrow, Lt, Dinv) of I + h A for every sample (cached per h)."""
+        """(Lt, Dinv) of I + h A for every sample (cached per h)."""
         key = float(h)
         f = self._fine.get(key)
         if f is None:
             M, nx, n = self.M, self.nx, self.n
-            Lrow = torch.zeros(M, nx, n, dtype=torch.float64, device="cuda")
             Lt, Dinv = empty(M, nx, n), empty(M, nx)
             _lib.call("kle_2d_factor_f64", ptr(self.dia), ptr(self.ex), ptr(self.ey), M, n, None, 1, 1.0, key,
-                      ptr(Lrow), ptr(Lt), ptr(Dinv), stream_ptr())
-            f = (Lrow, Lt, Dinv)
+                      ptr(Lt), ptr(Dinv), stream_ptr())
+            f = (Lt, Dinv)
             self._fine[key] = f
         return f
 
@@ -130,28 +129,28 @@ class DeviceOperator2D:
         Lt = empty(self.M, NF, self.nx, self.n, 2)
         Dinv = empty(self.M, NF, self.nx, 2)
         _lib.call("kle_2d_factor_f64", ptr(self.dia), ptr(self.ex), ptr(self.ey), self.M, self.n,
-                  ptr(tables.lam), NF, 0.0, deltaT, None, ptr(Lt), ptr(Dinv), stream_ptr())
+                  ptr(tables.lam), NF, 0.0, deltaT, ptr(Lt), ptr(Dinv), stream_ptr())
         return Lt, Dinv
 
     # -- propagators ---------------------------------------------------------
     def sweep(self, start, h: float, J: int, nseg: int = 1):
         """start: (M, Q, nx) device tensor -> (M, Q, nseg, nx)."""
         M, Q, nx = start.shape
-        Lrow, Lt, Dinv = self.fine_factor(h)
+        Lt, Dinv = self.fine_factor(h)
         out = empty(M, Q, nseg, nx)
         nw = int(_lib.query("kle_2d_fine_work_doubles", M, Q, self.n))
         work = empty(max(nw, 1))
-        _lib.call("kle_2d_sweep_f64", ptr(start.contiguous()), ptr(self.dia), ptr(self.ex), ptr(self.ey), ptr(Lrow),
-                  ptr(Lt), ptr(Dinv), M, Q, self.n, J, nseg, h, self.g0, ptr(work), nw, ptr(out), stream_ptr())
+        _lib.call("kle_2d_sweep_f64", ptr(start.contiguous()), ptr(self.dia), ptr(self.ex), ptr(self.ey), ptr(Lt),
+                  ptr(Dinv), M, Q, self.n, J, nseg, h, self.g0, ptr(work), nw, ptr(out), stream_ptr())
         return out
 
     def fgr(self, U, tables: AlphaTables, grid, alpha: float, R, status=None, F_given=None):
         M, N, nx = U.shape
         dT, dt = grid.deltaT, grid.deltat
-        Lrow, Lt, Dinv = self.fine_factor(dt)
+        Lt, Dinv = self.fine_factor(dt)
         nw = int(_lib.query("kle_2d_fine_work_doubles", M, N, self.n))
         work = empty(max(nw, 1))
-        _lib.call("kle_2d_fgr_f64", ptr(U), ptr(self.u0), ptr(F_given), ptr(self.dia), ptr(self.ex), ptr(self.ey), ptr(Lrow),
+        _lib.call("kle_2d_fgr_f64", ptr(U), ptr(self.u0), ptr(F_given), ptr(self.dia), ptr(self.ex), ptr(self.ey),
                   ptr(Lt), ptr(Dinv), ptr(tables.scaling), ptr(status), M, N, self.n, grid.n_fine_per_coarse,
                   dt, dT, self.g0, alpha, ptr(work), nw, ptr(R), stream_ptr())
 
