@@ -49,7 +49,9 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c3", "c5"])
+    p.add_argument("--samples", type=int, default=0, help="c3: evaluation samples (default 296 of the config's 4096)")
+    p.add_argument("--train", type=int, default=1024, help="c3: surrogate training samples (config: 1024)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU work of the baseline sample")
     return p.parse_args()
@@ -558,10 +560,123 @@ def run_c5(args):
     print(json.dumps(out), flush=True)
 
 
+def _cpu_solve2d(i):
+    from oracle import ref_port
+
+    w = _W
+    xi = w["xi"][i]
+    dia, ex, ey = w["model"].stencil(xi)
+    op = ref_port.SampleOperator.from_stencil2d(dia, ex, ey, w["n"], np.full(len(dia), 1.0))
+    U0 = ref_port.surrogate_predict(w["mean"], w["lam"], w["modes"], w["coeffs"], w["degree"], xi)
+    out = ref_port.pcgc(op, w["u0"], U0, w["N"], w["J"], 1.0, w["alpha"], w["tol"], 60)
+    return out["iters"]
+
+
+def run_c3(args):
+    """BASELINE configs[2]: 2D diffusion, 127 x 127 grid (nx = 16,129), N = 32,
+    J = 16, d = 10, Hermite p = 2 (66 terms) fitted on --train seeded samples,
+    alpha = 1e-3, tol = 1e-8. Timed step = U0 (gPC GEMM) + banded factors of
+    I + dt A and of the 17 shifted matrices + PCGC to tol + moments, on
+    --samples evaluation samples (the config's M = 4096 at ~0.1 s/sample is a
+    multi-minute step; the per-sample throughput does not depend on M beyond
+    filling the GPU). The CPU baseline is the oracle (SuperLU paths) on a
+    bounded sample over all host cores."""
+    import torch
+
+    from paper_2510_26180_b200 import LogNormalKL2D, ParameterSample, RngStream, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.engine import KleCgcSolver
+    from paper_2510_26180_b200.surrogate import build_surrogate
+
+    n, N, J, d = 127, 32, 16, 10
+    M = args.samples or 296
+    model = LogNormalKL2D(n=n, d=d, sigma=0.5, ell=0.25)
+    grid = make_time_grid(1.0, N, J)
+    cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=SEED)
+    train_rng, eval_rng, _ = RngStream(SEED).split(3)
+    train = train_rng.normal(0.0, 1.0, size=(args.train, d))
+    t0 = time.time()
+    sur = build_surrogate(model, grid, cfg, [ParameterSample(x, id=i) for i, x in enumerate(train)], eps_kl=1e-10,
+                          degree=2)
+    t_build = time.time() - t0
+    print(f"c3: surrogate built in {t_build:.1f} s (m_q={sur.m_q})", file=sys.stderr, flush=True)
+    solver = KleCgcSolver(model, grid, cfg, sur)
+    xi_host = eval_rng.normal(0.0, 1.0, size=(M, d))
+    xi_d = torch.as_tensor(xi_host, device="cuda")
+
+    def step(x):
+        res = solver.solve(x)
+        mean, var = solver.moments(res, M_total=M)
+        return res, mean, var
+
+    for _ in range(args.warmup):
+        tw = time.time()
+        res, mean, var = step(xi_d)
+        torch.cuda.synchronize()
+        print(f"c3: warm-up step {time.time() - tw:.1f} s", file=sys.stderr, flush=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clocks:
+        ev0.record()
+        for _ in range(args.steps):
+            res, mean, var = step(xi_d)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    it = res.batch.iters.cpu().numpy()
+    status = res.batch.status.cpu().numpy()
+    # end to end: pinned host xi -> device -> host moments
+    pinned = torch.from_numpy(xi_host).pin_memory()
+    hm = torch.empty(mean.numel(), dtype=torch.float64).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r2, m2, v2 = step(pinned.to("cuda", non_blocking=True))
+    hm.copy_(m2.reshape(-1), non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    dof = float(it.sum()) * N * J * model.nx
+    cpu = None
+    if not args.no_cpu_baseline:
+        from concurrent.futures import ProcessPoolExecutor
+        import multiprocessing as mp
+
+        cores = os.cpu_count() or 1
+        _cpu_init(dict(xi=xi_host, model=model, n=n, u0=model.initial_condition(), mean=sur.mean_field,
+                       lam=sur.eigenvalues, modes=sur.modes, coeffs=sur.coeffs, degree=sur.degree, N=N, J=J,
+                       alpha=cfg.alpha, tol=cfg.tol))
+        nb = min(M, cores)
+        print(f"c3: CPU baseline on {nb} samples", file=sys.stderr, flush=True)
+        with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+            t0 = time.time()
+            its = list(ex.map(_cpu_solve2d, range(nb)))
+            wall = time.time() - t0
+        cpu = {"value": nb / wall, "unit": "KLE-CGC solves/s", "cores": cores, "kind": "port",
+               "sample": f"first {nb} of the {M} evaluation samples, one per process, surrogate_predict + "
+                         f"pcgc_solve (oracle/ref_port: SuperLU of I + dt A and of each lambda_n I + dT A), "
+                         f"{wall:.1f} s wall",
+               "fine_dof_updates_per_s": float(np.sum(its)) * N * J * model.nx / wall}
+    line = {"metric": METRIC, "value": M / (ms * 1e-3), "unit": "KLE-CGC solves/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) KL coordinates; no dataset exists)",
+            "config": {"workload": f"BASELINE configs[2] (c3): 2D 127x127 5-point, N={N}, J={J}, d={d}, "
+                                   f"Hermite p=2 on {args.train} training samples, alpha={cfg.alpha}, tol={cfg.tol}; "
+                                   f"direct banded LDL^T solves (the reference's SuperLU semantics)",
+                       "samples": M, "l2": "state 8*M*N*nx bytes + factors 16*17*nx*n bytes per sample > L2"},
+            "fine_dof_updates_per_s": dof / (ms * 1e-3), "avg_outer_iters": float(it.mean()),
+            "max_outer_iters": int(it.max()), "all_converged": bool(np.all(status == 1)),
+            "surrogate_build_s": t_build, "surrogate": {"m_q": sur.m_q, "P": solver.surrogate.P},
+            "e2e": {"value": M / (e2e_ms * 1e-3), "unit": "solves/s", "h2d_bytes_per_step": int(xi_host.nbytes),
+                    "d2h_bytes_per_step": int(hm.numel() * 8), "ms_per_step": e2e_ms},
+            "clocks": clocks.summary(), "cpu_baseline": cpu}
+    print(json.dumps(line))
+
+
 if __name__ == "__main__":
     a = parse()
     if a.config == "c5":
         run_c5(a)
+    elif a.config == "c3" and a.impl == "b200":
+        run_c3(a)
     elif a.impl == "reference":
         run_reference(a)
     else:

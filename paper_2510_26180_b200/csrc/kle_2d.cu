@@ -287,15 +287,16 @@ struct Fine2dArgs {
 // [WP][SB_R], WP = 2^ceil(log2(n+1)), slot = q & (WP-1), zero for q < 0.
 constexpr int SB_RB = 8;
 constexpr int SB_PF = 4;   // ceil(127 / 32): coefficient values per lane and row
-constexpr int SB_R = 32;   // right-hand sides per warp (16: the two lane halves split the window sweep;
-                           // measured slower at config 3: twice the coefficient traffic)
-constexpr int SB_H = 32 / SB_R;
+// SB_R: right-hand sides per warp, 32 (lanes) or 16 (the two lane halves split
+// the window sweep: twice the coefficient traffic, twice the warps; chosen
+// when the batch is too small to fill the SMs with 32-wide warps).
 
-template <bool BACK>
+template <bool BACK, int SB_R>
 __device__ __forceinline__ void subst_pass(const double* __restrict__ Lc, const double* __restrict__ bsrc,
                                            double badd, const double* __restrict__ Di, double* __restrict__ out,
                                            double* win, double* cst, int n, int WP, int nx, int lane) {
   constexpr int RB = SB_RB;
+  constexpr int SB_H = 32 / SB_R;
   const int wm = WP - 1;
   const int r = lane & (SB_R - 1), h = lane / SB_R;
   for (int q = lane; q < WP * SB_R; q += 32) win[q] = 0.0;
@@ -345,9 +346,12 @@ __device__ __forceinline__ void subst_pass(const double* __restrict__ Lc, const 
       cst[(n + lane / RB) * RB + lane % RB] = pn;
       cst[(n + 4 + lane / RB) * RB + lane % RB] = pn2;
     }
-    double bv[RB];
+    double bv[RB], dv[RB];  // loads in flight during the sweep (consumed in the near part)
 #pragma unroll
-    for (int a = 0; a < RB; ++a) bv[a] = (p0 + a < nx) ? bsrc[(size_t)row_of(p0 + a) * SB_R + r] + badd : 0.0;
+    for (int a = 0; a < RB; ++a) {
+      bv[a] = (p0 + a < nx) ? bsrc[(size_t)row_of(p0 + a) * SB_R + r] : 0.0;
+      dv[a] = (Di && p0 + a < nx) ? __ldg(Di + row_of(p0 + a)) : 1.0;
+    }
     __syncwarp();
     if (p0 + RB < nx) {  // in flight during the sweep
       fetch(p0 + RB);
@@ -375,14 +379,14 @@ __device__ __forceinline__ void subst_pass(const double* __restrict__ Lc, const 
 #pragma unroll
     for (int a = 0; a < RB; ++a) {
       const int p = p0 + a;
-      double v = bv[a] - acc[a];
+      double v = (bv[a] + badd) - acc[a];
 #pragma unroll
       for (int a2 = 0; a2 < a; ++a2) v = fma(-cst[(n + a2) * RB + a], yv[a2], v);
       yv[a] = v;
       if (p < nx && h == 0) {
         const int i = row_of(p);
         win[(p & wm) * SB_R + r] = v;
-        out[(size_t)i * SB_R + r] = Di ? v * Di[i] : v;
+        out[(size_t)i * SB_R + r] = Di ? v * dv[a] : v;
       }
     }
   }
@@ -395,6 +399,7 @@ __host__ __device__ inline int win_pow2(int n) {
   return w;
 }
 
+template <int SB_R>
 __device__ __forceinline__ void fine2d_steps(const Fine2dArgs& a, int s, double* __restrict__ X,
                                              double* __restrict__ Z, double* win, double* cst, int lane) {
   const int n = a.n, nx = n * n, WP = win_pow2(n);
@@ -402,12 +407,14 @@ __device__ __forceinline__ void fine2d_steps(const Fine2dArgs& a, int s, double*
   const double* Di = a.Dinv + (size_t)s * nx;
   const double hg = a.dt * a.g0;
   for (int step = 0; step < a.J; ++step) {
-    subst_pass<false>(Lt, X, hg, Di, Z, win, cst, n, WP, nx, lane);   // y = L^{-1}(x + h g); Z = D^{-1} y
-    subst_pass<true>(Lt, Z, 0.0, nullptr, X, win, cst, n, WP, nx, lane);  // x = L^{-T} Z
+    subst_pass<false, SB_R>(Lt, X, hg, Di, Z, win, cst, n, WP, nx, lane);   // y = L^{-1}(x + h g); Z = D^{-1} y
+    subst_pass<true, SB_R>(Lt, Z, 0.0, nullptr, X, win, cst, n, WP, nx, lane);  // x = L^{-T} Z
   }
 }
 
+template <int SB_R>
 __global__ void __launch_bounds__(32, 5) fine2d_kernel(Fine2dArgs a) {
+  constexpr int SB_H = 32 / SB_R;
   const int n = a.n, nx = n * n;
   const int G = (a.N + SB_R - 1) / SB_R;
   const int s = blockIdx.x / G, g = blockIdx.x % G;
@@ -428,7 +435,7 @@ __global__ void __launch_bounds__(32, 5) fine2d_kernel(Fine2dArgs a) {
   __syncwarp();
   if (a.mode == 1) {
     for (int sg = 0; sg < a.nseg; ++sg) {
-      fine2d_steps(a, s, X, Z, win, cst, lane);
+      fine2d_steps<SB_R>(a, s, X, Z, win, cst, lane);
       if (live) {
         double* o = a.out + (((size_t)s * a.N + q) * a.nseg + sg) * nx;
         for (int i = hh; i < nx; i += SB_H) o[i] = X[(size_t)i * SB_R + rr];
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(32, 5) fine2d_kernel(Fine2dArgs a) {
     }
     return;
   }
-  if (!a.F_given) fine2d_steps(a, s, X, Z, win, cst, lane);
+  if (!a.F_given) fine2d_steps<SB_R>(a, s, X, Z, win, cst, lane);
   __syncwarp();
   if (!live) return;
   // rhs_n = scaling_n ((I + dT A) F_n - prev_n); prev_0 = alpha U_{N-1}
@@ -687,15 +694,29 @@ extern "C" int kle_2d_factor_f64(const double* dia, const double* ex, const doub
 }
 
 extern "C" size_t kle_2d_fine_work_doubles(int M, int N, int n) {
-  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 2 * (size_t)M * ((N + SB_R - 1) / SB_R) * n * n * SB_R;
+  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 2 * (size_t)M * ((N + 31) / 32) * n * n * 32;  // covers SB_R = 16
+}
+
+template <int SB_R>
+static int fine2d_launch_r(Fine2dArgs& a, void* stream) {
+  const int G = (a.N + SB_R - 1) / SB_R;
+  const size_t smem = sizeof(double) * ((size_t)win_pow2(a.n) * SB_R + (size_t)(a.n + SB_RB) * SB_RB);
+  cudaFuncSetAttribute(fine2d_kernel<SB_R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fine2d_kernel<SB_R><<<(unsigned)(a.M * G), 32, smem, KLE2D_STREAM(stream)>>>(a);
+  return check_launch("fine2d_kernel");
 }
 
 static int fine2d_launch(Fine2dArgs& a, void* stream) {
-  const int G = (a.N + SB_R - 1) / SB_R;
-  const size_t smem = sizeof(double) * ((size_t)win_pow2(a.n) * SB_R + (size_t)(a.n + SB_RB) * SB_RB);
-  cudaFuncSetAttribute(fine2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fine2d_kernel<<<(unsigned)(a.M * G), 32, smem, KLE2D_STREAM(stream)>>>(a);
-  return check_launch("fine2d_kernel");
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long warps32 = (long long)a.M * ((a.N + 31) / 32);
+  if (a.N > 16 && warps32 < 3LL * sms) return fine2d_launch_r<16>(a, stream);
+  return fine2d_launch_r<32>(a, stream);
 }
 
 extern "C" int kle_2d_fgr_f64(const double* U, const double* u0, const double* F_given, const double* dia,

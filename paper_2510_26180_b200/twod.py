@@ -173,7 +173,8 @@ def _batch_size(op: DeviceOperator2D, N: int) -> int:
     NF = N // 2 + 1
     per = 8 * (2 * NF * op.nx * (op.n + 1) + 2 * op.nx * (op.n + 1) + 6 * N * op.nx + 2 * NF * op.nx)
     free, _ = torch.cuda.mem_get_info()
-    return max(1, min(op.M, int(0.8 * free) // per))
+    free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()  # the caching allocator's idle blocks
+    return max(1, min(op.M, int(0.85 * free) // per))
 
 
 def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables = None, batch: int = None):
@@ -193,22 +194,41 @@ def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables 
     imag = torch.zeros(M, dtype=torch.float64, device="cuda")
     B = batch or _batch_size(op, N)
     active = torch.zeros(1, dtype=torch.int32, device="cuda")
+    import os
+    import time
+
+    prof = os.environ.get("KLE_2D_PROFILE") == "1"
+
+    def mark(msg, t0=[None]):
+        if prof:
+            torch.cuda.synchronize()
+            t = time.time()
+            if t0[0] is not None:
+                print(f"[2d] {msg}: {t - t0[0]:.3f} s", flush=True)
+            t0[0] = t
+
+    mark("start")
     for lo in range(0, M, B):
         hi = min(M, lo + B)
         ob = op.select(lo, hi)
         Ub = U[lo:hi]
         Mb = hi - lo
+        ob.fine_factor(grid.deltat)
+        mark(f"batch {lo}:{hi} real factor")
         Lt_c, Dinv_c = ob.shifted_factors(tables, N, grid.deltaT)
+        mark("complex factors")
         R = empty(Mb, N, nx)
         nw = int(_lib.query("kle_2d_cgc_work_doubles", Mb, N, op.n))
         work = torch.zeros(max(nw, 1), dtype=torch.float64, device="cuda")
         st, it, ih = status[lo:hi], iters[lo:hi], inc[lo:hi]
         for k in range(1, cfg.max_outer_iters + 1):
             ob.fgr(Ub, tables, grid, cfg.alpha, R, status=st)
+            mark(f"k={k} fgr")
             active.zero_()
             _lib.call("kle_2d_cgc_f64", ptr(R), None, ptr(Ub), None, ptr(Lt_c), ptr(Dinv_c), ptr(tables.inv_scaling),
                       Mb, N, op.n, k, cfg.max_outer_iters, cfg.tol, ptr(st), ptr(it), None, ptr(ih), ptr(active),
                       ptr(work), nw, stream_ptr())
+            mark(f"k={k} cgc")
             if int(active.item()) == 0:
                 break
         del Lt_c, Dinv_c, R, work, ob
