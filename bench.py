@@ -560,15 +560,13 @@ def run_c5(args):
     print(json.dumps(out), flush=True)
 
 
-def _cpu_solve2d(i):
+def _cpu_solve2d(task):
+    """One c3 sample on the oracle (SuperLU paths): task = (stencil, U0, u0, n, N, J, alpha, tol)."""
     from oracle import ref_port
 
-    w = _W
-    xi = w["xi"][i]
-    dia, ex, ey = w["model"].stencil(xi)
-    op = ref_port.SampleOperator.from_stencil2d(dia, ex, ey, w["n"], np.full(len(dia), 1.0))
-    U0 = ref_port.surrogate_predict(w["mean"], w["lam"], w["modes"], w["coeffs"], w["degree"], xi)
-    out = ref_port.pcgc(op, w["u0"], U0, w["N"], w["J"], 1.0, w["alpha"], w["tol"], 60)
+    (dia, ex, ey), U0, u0, n, N, J, alpha, tol = task
+    op = ref_port.SampleOperator.from_stencil2d(dia, ex, ey, n, np.full(len(dia), 1.0))
+    out = ref_port.pcgc(op, u0, U0, N, J, 1.0, alpha, tol, 60)
     return out["iters"]
 
 
@@ -640,19 +638,28 @@ def run_c3(args):
         import multiprocessing as mp
 
         cores = os.cpu_count() or 1
-        _cpu_init(dict(xi=xi_host, model=model, n=n, u0=model.initial_condition(), mean=sur.mean_field,
-                       lam=sur.eigenvalues, modes=sur.modes, coeffs=sur.coeffs, degree=sur.degree, N=N, J=J,
-                       alpha=cfg.alpha, tol=cfg.tol))
         nb = min(M, cores)
+        # spawned workers (a fork after the CUDA context and the BLAS thread pools
+        # of the surrogate build can deadlock); U0 = surrogate_predict on the host
+        from oracle import ref_port
+
+        tasks = [(model.stencil(xi_host[i]),
+                  ref_port.surrogate_predict(sur.mean_field, sur.eigenvalues, sur.modes, sur.coeffs, sur.degree,
+                                             xi_host[i]),
+                  model.initial_condition(), n, N, J, cfg.alpha, cfg.tol) for i in range(nb)]
         print(f"c3: CPU baseline on {nb} samples", file=sys.stderr, flush=True)
-        with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+        # one BLAS thread per worker (SuperLU calls BLAS; cores x cores threads thrash)
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"
+        with ProcessPoolExecutor(cores, mp_context=mp.get_context("spawn")) as ex:
+            list(ex.map(_cpu_solve2d, tasks[:1]))  # start the workers
             t0 = time.time()
-            its = list(ex.map(_cpu_solve2d, range(nb)))
+            its = list(ex.map(_cpu_solve2d, tasks))
             wall = time.time() - t0
         cpu = {"value": nb / wall, "unit": "KLE-CGC solves/s", "cores": cores, "kind": "port",
-               "sample": f"first {nb} of the {M} evaluation samples, one per process, surrogate_predict + "
-                         f"pcgc_solve (oracle/ref_port: SuperLU of I + dt A and of each lambda_n I + dT A), "
-                         f"{wall:.1f} s wall",
+               "sample": f"first {nb} of the {M} evaluation samples, one per process, pcgc_solve from the "
+                         f"host surrogate_predict U0 (oracle/ref_port: SuperLU of I + dt A and of each "
+                         f"lambda_n I + dT A), {wall:.1f} s wall",
                "fine_dof_updates_per_s": float(np.sum(its)) * N * J * model.nx / wall}
     line = {"metric": METRIC, "value": M / (ms * 1e-3), "unit": "KLE-CGC solves/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
