@@ -317,7 +317,10 @@ def run_b200(args):
                 "peak": fp64_peak,
                 "unit": "TFLOP/s",
                 "frac": (fgr_tflops / fp64_peak) if fp64_peak else None,
-                "traffic": None,
+                "traffic": (peaks["traffic"]["fgr_kernel"]["bytes_per_sample_iteration"] * M
+                            if "traffic" in peaks else None),
+                "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per sample-iteration "
+                                  "(profiles/r01_traffic.json) x samples per launch",
                 "peak_source": peaks.get("fp64_source"),
                 "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch",
                 "hbm_frac": (fgr_bytes / (fgr_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
@@ -328,7 +331,9 @@ def run_b200(args):
                                "frac": cgc_gbs / peaks["hbm_gbs"], "ms_per_launch": cgc_ms,
                                "algorithmic": "24 B per (n, i) per sample: read R, read U, write U "
                                               "(+ pivots 16 (N/2+1)/N B not counted)",
-                               "path": "cluster" if sfac is not None else "on-the-fly"},
+                               "path": "cluster" if sfac is not None else "on-the-fly",
+                               "traffic": (peaks["traffic"]["cgc_cluster_kernel"]["bytes_per_sample_iteration"] * M
+                                           if "traffic" in peaks and sfac is not None else None)},
                 "gemm_bias_kernel": {"bound": "tensor(dmma)", "achieved": gemm_tflops,
                                      "peak": peaks.get("dmma_tflops"), "unit": "TFLOP/s",
                                      "frac": gemm_tflops / peaks["dmma_tflops"] if peaks.get("dmma_tflops") else None,
@@ -367,6 +372,9 @@ def load_peaks():
                 out["fp64_source"] = "measured DFMA peak, profiles/r01_fp64_peaks.jsonl (tools/fp64_peaks.cu)"
             if d.get("what") == "dmma_tflops":
                 out["dmma_tflops"] = d["value"]
+    t = ROOT / "profiles" / "r01_traffic.json"
+    if t.exists():  # DRAM bytes per sample-iteration from one ncu --set full capture
+        out["traffic"] = json.loads(t.read_text())
     return out
 
 
