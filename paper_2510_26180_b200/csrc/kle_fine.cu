@@ -167,9 +167,11 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
     double* p0 = st + NC * LD;    // [LD]
     double* dd = p0 + LD;         // [LD]
     double* ee = dd + LD;         // [LD + MR]: ee[pidx(i)] couples rows i-1 and i
-    for (int e = tid; e < NC * nx; e += NT) {
-      const int ln = e / nx, row = e - ln * nx, n = n0 + ln;
-      if (n < N) cp_async8(st + ln * LD + SM::pidx(row), (n == 0) ? a.u0 + row : a.U + sbase + (size_t)(n - 1) * nx + row);
+    for (int ln = 0; ln < NC; ++ln) {  // no division in the index math
+      const int n = n0 + ln;
+      if (n >= N) break;
+      const double* src = (n == 0) ? a.u0 : a.U + sbase + (size_t)(n - 1) * nx;
+      for (int row = tid; row < nx; row += NT) cp_async8(st + ln * LD + SM::pidx(row), src + row);
     }
     if (n0 == 0)
       for (int row = tid; row < nx; row += NT) cp_async8(p0 + SM::pidx(row), a.U + sbase + (size_t)(N - 1) * nx + row);
