@@ -19,6 +19,9 @@
 #ifndef KLE_FINE_LAZY
 #define KLE_FINE_LAZY 0  // lazy-stitch step (kle_fine.cuh); measured slower, kept for A/B
 #endif
+#ifndef KLE_FINE_CS
+#define KLE_FINE_CS 0  // chunk products from shared memory (be_steps_cs): measured slower (5.79 vs 5.43 ms), A/B only
+#endif
 
 namespace kle {
 
@@ -132,7 +135,7 @@ struct FgrSmem {
   static constexpr int LD = NXP;
   static constexpr int SWZ = (MR < 16 ? MR : 16) - 1;
   __device__ __forceinline__ static int pidx(int row) { return row ^ ((row / MR) & SWZ); }
-  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8) * sizeof(double);
+  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8 + (KLE_FINE_CS ? 3 * NXP : 0)) * sizeof(double);
 };
 
 template <int MR, int P, int R, int NT, bool PIPE>
@@ -185,9 +188,13 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
     }
     LaneFactors<MR, P> fac;
     fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
+    const double hg = a.dt * a.g0;
+    double* cs = ee + LD + MR;  // [3][MR][P] chunk products (KLE_FINE_CS)
+    if constexpr (KLE_FINE_CS && !PIPE && !KLE_FINE_LAZY) {
+      if (w == 0 && slot == 0) chunk_products<MR, P>(cs, fac, k, hg);
+    }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
     __syncthreads();
-    const double hg = a.dt * a.g0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -197,6 +204,7 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
       }
     if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
     else if constexpr (KLE_FINE_LAZY) be_steps_lazy<MR, P, R>(x, fac, a.ffac + (size_t)s * L::DOUBLES, k, a.J, hg);
+    else if constexpr (KLE_FINE_CS) be_steps_cs<MR, P, R>(x, fac, k, a.J, cs);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r)

@@ -142,6 +142,102 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
   }
 }
 
+// Same step with the R-independent chunk products (pi_j, sig_j, kap_j) read
+// from shared memory (cs: [3][MR][P], written once per CTA) instead of being
+// recomputed every step: they leave the FP64 pipe for the LSU. The loads are
+// volatile so they are not hoisted into registers across the J loop.
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+template <int MR, int P>
+__device__ __forceinline__ void chunk_products(double* cs, const LaneFactors<MR, P>& f, int k, double hg) {
+  double pi = 1.0;
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    pi *= -f.l[j];
+    cs[(0 * MR + j) * P + k] = pi;
+  }
+  double sg = 1.0;
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+    sg *= -ln;
+    cs[(1 * MR + j) * P + k] = sg;
+    cs[(2 * MR + j) * P + k] = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
+  }
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, int J,
+                                            const double* cs) {
+  using L = FineLayout<MR, P>;
+  const unsigned base = (unsigned)__cvta_generic_to_shared(cs) + (unsigned)(k * sizeof(double));
+  for (int it = 0; it < J; ++it) {
+#pragma unroll
+    for (int j = 1; j < MR; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+    double Y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+#pragma unroll
+    for (int t = 0; t < L::LOGP; ++t) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t, P);
+        Y[r] = fma(f.af[t], o, Y[r]);  // af = 0 for k < 2^t
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
+      Y[r] = (k == 0) ? 0.0 : o;
+    }
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const double pi = lds_f64(base + (unsigned)((0 * MR + j) * P * sizeof(double)));
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(pi, Y[r], x[r][j]);
+    }
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j) {
+      const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+      const double kap = lds_f64(base + (unsigned)((2 * MR + j) * P * sizeof(double)));
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double z = fma(x[r][j], f.inv[j], kap);
+        if (j + 1 < MR) z = fma(-ln, x[r][j + 1], z);
+        x[r][j] = z;
+      }
+    }
+    double X[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) X[r] = x[r][0];
+#pragma unroll
+    for (int t = 0; t < L::LOGP; ++t) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t, P);
+        X[r] = fma(f.bb[t], o, X[r]);  // bb = 0 for k + 2^t >= P
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
+      X[r] = (k == P - 1) ? 0.0 : o;
+    }
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j) {
+      const double sg = lds_f64(base + (unsigned)((1 * MR + j) * P * sizeof(double)));
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Lazy-stitch form of the same step (default). With chunk-local recurrences
 //   Fwd0(v)_j = v_j - l_j Fwd0(v)_{j-1},  Bwd0(z)_j = z_j - l_{j+1} Bwd0(z)_{j+1}
