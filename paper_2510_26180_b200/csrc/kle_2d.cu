@@ -287,9 +287,11 @@ struct Fine2dArgs {
 // [WP][SB_R], WP = 2^ceil(log2(n+1)), slot = q & (WP-1), zero for q < 0.
 constexpr int SB_RB = 8;
 constexpr int SB_PF = 4;   // ceil(127 / 32): coefficient values per lane and row
-// SB_R: right-hand sides per warp, 32 (lanes) or 16 (the two lane halves split
-// the window sweep: twice the coefficient traffic, twice the warps; chosen
-// when the batch is too small to fill the SMs with 32-wide warps).
+// SB_R: right-hand sides per warp, 32 (lanes), 16 or 8 (the lane groups split
+// the window sweep: more coefficient traffic, more warps; chosen when the
+// batch is too small to fill the SMs with 32-wide warps). A cp.async
+// multi-stage pipeline for the coefficient / right-hand-side staging (instead
+// of the register prefetch) measured slower (0.42-0.51 vs 0.33 s per c3 step).
 
 template <bool BACK, int SB_R>
 __device__ __forceinline__ void subst_pass(const double* __restrict__ Lc, const double* __restrict__ bsrc,
@@ -371,10 +373,10 @@ __device__ __forceinline__ void subst_pass(const double* __restrict__ Lc, const 
         acc[a + 1] = fma(c.y, y, acc[a + 1]);
       }
     }
-    if constexpr (SB_H > 1) {
 #pragma unroll
-      for (int a = 0; a < RB; ++a) acc[a] += __shfl_xor_sync(KLE_FULL_MASK, acc[a], SB_R);
-    }
+    for (int o = SB_R; o < 32; o <<= 1)  // combine the lane groups' partial sweeps
+#pragma unroll
+      for (int a = 0; a < RB; ++a) acc[a] += __shfl_xor_sync(KLE_FULL_MASK, acc[a], o);
     double yv[RB];
 #pragma unroll
     for (int a = 0; a < RB; ++a) {
@@ -714,8 +716,13 @@ static int fine2d_launch(Fine2dArgs& a, void* stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const long long warps32 = (long long)a.M * ((a.N + 31) / 32);
-  if (a.N > 16 && warps32 < 3LL * sms) return fine2d_launch_r<16>(a, stream);
+  // narrowest warps (more warps per sample, more coefficient traffic) only as
+  // far as needed to put ~4 warps on every SM
+  const long long want = 4LL * sms;
+  if (a.N > 16 && (long long)a.M * ((a.N + 31) / 32) < want) {
+    if (a.N > 8 && (long long)a.M * ((a.N + 15) / 16) < want) return fine2d_launch_r<8>(a, stream);
+    return fine2d_launch_r<16>(a, stream);
+  }
   return fine2d_launch_r<32>(a, stream);
 }
 
