@@ -1,0 +1,127 @@
+"""The reference's own hot-path pins (test_propagators.py / test_pcgc.py
+of pintuq) replayed on the device path through the drop-in API, with a test-only
+plugin like the reference's ``ScalarDecay`` (conftest.py:14-34)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_2510_26180_b200 import (CoarseTrajectory, LinearModel, ParameterSample, SolverConfig,
+                                   make_time_grid)
+
+pytestmark = pytest.mark.gpu
+
+
+class ScalarDecay(LinearModel):
+    """u' = -lam u, nx = 1 (the reference's test plugin)."""
+
+    name = "scalar-decay"
+
+    def __init__(self, lam=1.0):
+        self.lam, self.nx, self.parameter_dim = float(lam), 1, 1
+        self.supports = ((-np.inf, np.inf),)
+
+    @property
+    def cell_volume(self):
+        return 1.0
+
+    def linear_system(self, xi):
+        return sp.csc_matrix([[self.lam]]), (lambda t: np.zeros(1))
+
+    def initial_condition(self, xi=None):
+        return np.ones(1)
+
+
+class Heat1D(LinearModel):
+    """Constant-coefficient heat equation without source (a generic tridiagonal plugin)."""
+
+    name = "heat-1d"
+
+    def __init__(self, nx=31):
+        self.nx, self.parameter_dim = nx, 1
+        self.supports = ((-np.inf, np.inf),)
+        self.h = 1.0 / (nx + 1)
+
+    @property
+    def cell_volume(self):
+        return self.h
+
+    def linear_system(self, xi):
+        k = 1.0 + 0.1 * float(xi.values[0])
+        main = np.full(self.nx, 2 * k / self.h ** 2)
+        off = np.full(self.nx - 1, -k / self.h ** 2)
+        return sp.diags([off, main, off], [-1, 0, 1], format="csc"), (lambda t: np.zeros(self.nx))
+
+    def initial_condition(self, xi=None):
+        return np.sin(np.pi * np.arange(1, self.nx + 1) * self.h)
+
+
+def test_backward_euler_scalar_and_power_oracle(cuda):
+    from paper_2510_26180_b200.propagators import backward_euler_step, propagate_fine
+
+    m, xi, cfg = ScalarDecay(2.0), ParameterSample(np.zeros(1)), SolverConfig()
+    v = backward_euler_step(m, np.ones(1), 0.0, 0.1, xi, cfg)
+    np.testing.assert_allclose(v, [1.0 / (1.0 + 2.0 * 0.1)], rtol=1e-14)
+    grid = make_time_grid(1.0, 1, 50)
+    f = propagate_fine(ScalarDecay(1.0), np.ones(1), 0.0, 1.0, grid, xi, cfg)
+    np.testing.assert_allclose(f, [(1.0 + 1.0 / 50) ** -50], rtol=1e-13)
+    assert abs(f[0] - 0.371528) < 1e-6
+
+
+def test_propagator_linearity_composition_and_errors(cuda):
+    from paper_2510_26180_b200.propagators import propagate_coarse, propagate_fine
+
+    m, xi, cfg = Heat1D(31), ParameterSample(np.array([0.7])), SolverConfig()
+    grid = make_time_grid(1.0, 4, 8)
+    rng = np.random.default_rng(3)
+    u, v = rng.normal(size=31), rng.normal(size=31)
+    fu = propagate_fine(m, u, 0.0, grid.deltaT, grid, xi, cfg)
+    fv = propagate_fine(m, v, 0.0, grid.deltaT, grid, xi, cfg)
+    fw = propagate_fine(m, 2.0 * u - 3.0 * v, 0.0, grid.deltaT, grid, xi, cfg)
+    np.testing.assert_allclose(fw, 2.0 * fu - 3.0 * fv, rtol=1e-12, atol=1e-12 * np.abs(fw).max())
+    # coarse step vs a dense solve
+    A, _ = m.linear_system(xi)
+    want = np.linalg.solve(np.eye(31) + grid.deltaT * A.toarray(), u)
+    np.testing.assert_allclose(propagate_coarse(m, u, 0.0, grid.deltaT, xi, cfg), want, rtol=1e-12,
+                               atol=1e-13 * np.abs(want).max())
+    # composition is bitwise: two calls of one interval = the same twice
+    a1 = propagate_fine(m, fu, grid.deltaT, 2 * grid.deltaT, grid, xi, cfg)
+    a2 = propagate_fine(m, propagate_fine(m, u, 0.0, grid.deltaT, grid, xi, cfg), grid.deltaT,
+                        2 * grid.deltaT, grid, xi, cfg)
+    np.testing.assert_array_equal(a1, a2)
+    u_copy = u.copy()
+    propagate_fine(m, u, 0.0, grid.deltaT, grid, xi, cfg)
+    np.testing.assert_array_equal(u, u_copy)  # the input is never mutated
+    with pytest.raises(ValueError):
+        propagate_fine(m, u, 0.0, 0.5 * grid.deltaT, grid, xi, cfg)
+
+
+def test_three_step_block_mismatch_and_cgc_fixed_point(cuda):
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, cgc_correct, three_step_solve
+    from paper_2510_26180_b200.propagators import fine_reference, propagate_fine
+
+    m, xi, cfg = Heat1D(15), ParameterSample(np.array([-0.4])), SolverConfig(alpha=1e-2)
+    grid = make_time_grid(1.0, 8, 6)
+    A, _ = m.linear_system(xi)
+    with pytest.raises(ValueError):
+        three_step_solve(build_alpha_circulant(8, 1e-2), -A, grid.deltaT, np.zeros((7, 15)))
+    # the serial fine trajectory is a fixed point of the CGC (pcgc.py:208-243)
+    ref = fine_reference(m, xi, grid, cfg)
+    starts = np.vstack([ref.initial, ref.states[:-1]])
+    F = np.array([propagate_fine(m, starts[n], n * grid.deltaT, (n + 1) * grid.deltaT, grid, xi, cfg)
+                  for n in range(8)])
+    out, diag = cgc_correct(m, xi, grid, cfg, CoarseTrajectory(ref.initial, ref.states), F)
+    np.testing.assert_allclose(out.states, ref.states, rtol=0, atol=1e-10 * np.abs(ref.states).max())
+    assert diag["imag_residue"] <= 1e-10
+
+
+def test_pcgc_converges_to_fine_reference(cuda):
+    from paper_2510_26180_b200.pcgc import pcgc_solve
+    from paper_2510_26180_b200.propagators import coarse_sweep_init, fine_reference
+
+    m, xi = Heat1D(31), ParameterSample(np.array([0.2]))
+    grid, cfg = make_time_grid(1.0, 16, 8), SolverConfig(alpha=1e-3, tol=1e-10, max_outer_iters=60)
+    ref = fine_reference(m, xi, grid, cfg)
+    tr = pcgc_solve(m, xi, grid, cfg, coarse_sweep_init(m, xi, grid, cfg))
+    assert tr.converged
+    assert np.max(np.abs(tr.trajectory.states - ref.states)) <= 10 * cfg.tol
+    assert tr.diagnostics["max_imag_residue"] <= 1e-10 * max(np.abs(tr.trajectory.states).max(), 1.0)
