@@ -357,19 +357,19 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     if (col < HC) y[j] = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};   // (Z_f + conj Z_-f)/2
     else y[j] = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};            // (Z_f - conj Z_-f)/(2i)
   }
-  // l_r = dT off_{r-1} / beta_{r-1}
-  Cplx l[MR];
-#pragma unroll
-  for (int j = 0; j < MR; ++j) {
+  // l_r = dT off_{r-1} / beta_{r-1}, formed where used (E from shared memory):
+  // keeping all MR of them live as well as the pivots spills registers
+  auto lj = [&](int j) -> Cplx {
     const double E = offs[r0l + j];  // couples rows r0+j-1 and r0+j
     const Cplx ip = (j == 0) ? ibprev : ib[j - 1];
-    l[j] = {E * ip.re, E * ip.im};
-  }
+    return {E * ip.re, E * ip.im};
+  };
   Cplx A = {1.0, 0.0};
 #pragma unroll
   for (int j = 0; j < MR; ++j) {
-    if (j > 0) y[j] = cfma({-l[j].re, -l[j].im}, y[j - 1], y[j]);
-    A = cneg_mul(l[j], A);
+    const Cplx l = lj(j);
+    if (j > 0) y[j] = cfma({-l.re, -l.im}, y[j - 1], y[j]);
+    A = cneg_mul(l, A);
   }
   Cplx B = y[MR - 1];
 #pragma unroll
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     Cplx pi = {1.0, 0.0};
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
-      pi = cneg_mul(l[j], pi);
+      pi = cneg_mul(lj(j), pi);
       y[j] = cmul(cfma(pi, Cin, y[j]), ib[j]);
     }
   }
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   Cplx S = {1.0, 0.0};
 #pragma unroll
   for (int j = MR - 1; j >= 0; --j) {
-    const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
+    const Cplx ln = (j == MR - 1) ? lnext : lj(j + 1);
     if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
     S = cneg_mul(ln, S);
   }
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     Cplx sg = {1.0, 0.0};
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
-      const Cplx ln = (j == MR - 1) ? lnext : l[j + 1];
+      const Cplx ln = (j == MR - 1) ? lnext : lj(j + 1);
       sg = cneg_mul(ln, sg);
       y[j] = cfma(sg, Xin, y[j]);
     }
