@@ -1,5 +1,6 @@
 // extern "C" boundary of libkle_b200.so (declared in include/kle_b200.h).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -228,18 +229,114 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
   if (inc_hist) cudaMemsetAsync(inc_hist, 0xFF, sizeof(double) * (size_t)M * max_iters, st);
   if (imag) cudaMemsetAsync(imag, 0, sizeof(double) * M, st);
   KLE_TRY(check_launch("pcgc_solve: init"));
-  int32_t h_count = M;
-  for (int k = 1; k <= max_iters && h_count > 0; ++k) {
-    KLE_TRY(kle_fgr_f64(U, u0, nullptr, nullptr, R, fine_blob, dia, off, scaling, status, M, N, nx, J, dt, dT, g0,
-                        alpha, stream));
-    cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
-    KLE_TRY(kle_cgc_update_f64(R, U, inv_scaling, lam, dia, off, sfac, M, N, nx, dT, k, max_iters, tol, status,
-                               iters, inc_hist, imag, counter, cgc_scratch, cgc_scratch_bytes, stream));
-    cudaMemcpyAsync(&h_count, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-    const cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return set_error(KLE_ERR_CUDA, cudaGetErrorString(e));
+  // Sample pipelines: the batch is split into `pipes` contiguous halves, each
+  // running its own outer loop on its own stream, started half an iteration
+  // apart, so the FP64-bound fine sweeps of one half share the SMs with the
+  // latency-bound CGC of the other. Results do not depend on the split (every
+  // sample's arithmetic is the same; only the launch grouping changes).
+  int pipes = (M >= 8192 && clustered) ? 2 : 1;
+  if (const char* e = getenv("KLE_PCGC_PIPES")) pipes = atoi(e) == 2 && M >= 2 && clustered ? 2 : 1;
+  const FineLayoutRT lay = fine_layout(nx);
+  struct Pipe {
+    int m0, M, k;
+    bool live;
+    cudaStream_t st, sc;  // fine sweeps (low priority), CGC (high priority)
+    cudaEvent_t done, fdone;
+    int32_t* count_d;
+  };
+  Pipe pp[2];
+  int32_t* h_count = nullptr;
+  if (cudaHostAlloc(&h_count, 2 * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess)
+    return set_error(KLE_ERR_CUDA, "pcgc_solve: pinned counter");
+  cudaEvent_t ready;
+  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  cudaEventRecord(ready, st);
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  for (int p = 0; p < pipes; ++p) {
+    pp[p].m0 = (int)((long long)M * p / pipes);
+    pp[p].M = (int)((long long)M * (p + 1) / pipes) - pp[p].m0;
+    pp[p].k = 0;
+    pp[p].live = pp[p].M > 0;
+    pp[p].count_d = counter + p;
+    h_count[p] = pp[p].M;
+    if (pipes == 1) {
+      pp[p].st = pp[p].sc = st;
+    } else {
+      cudaStreamCreateWithPriority(&pp[p].st, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&pp[p].sc, cudaStreamNonBlocking, hi);
+      cudaStreamWaitEvent(pp[p].st, ready, 0);
+    }
+    cudaEventCreateWithFlags(&pp[p].done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&pp[p].fdone, cudaEventDisableTiming);
   }
-  return KLE_OK;
+  auto enqueue = [&](Pipe& q) -> int {
+    const int k = ++q.k;
+    const size_t o = (size_t)q.m0;
+    double* Uq = U + o * N * nx;
+    const double* dq = dia + o * nx;
+    const double* eq = off + o * nx;
+    int32_t* sq = status + o;
+    KLE_TRY(kle_fgr_f64(Uq, u0, nullptr, nullptr, R + o * N * nx, fine_blob + o * lay.doubles, dq, eq, scaling, sq,
+                        q.M, N, nx, J, dt, dT, g0, alpha, q.st));
+    if (q.sc != q.st) {
+      cudaEventRecord(q.fdone, q.st);
+      cudaStreamWaitEvent(q.sc, q.fdone, 0);
+    }
+    cudaMemsetAsync(q.count_d, 0, sizeof(int32_t), q.sc);
+    const double* sf = clustered ? sfac + o * (shift_factor_doubles(1, N, nx)) : nullptr;
+    void* cs = clustered ? static_cast<void*>(static_cast<char*>(cgc_scratch) + o * 16) : cgc_scratch;
+    KLE_TRY(kle_cgc_update_f64(R + o * N * nx, Uq, inv_scaling, lam, dq, eq, sf, q.M, N, nx, dT, k, max_iters, tol,
+                               sq, iters + o, inc_hist ? inc_hist + o * max_iters : nullptr, imag ? imag + o : nullptr,
+                               q.count_d, cs, clustered ? (size_t)q.M * 16 : cgc_scratch_bytes, q.sc));
+    cudaMemcpyAsync(&h_count[&q - pp], q.count_d, sizeof(int32_t), cudaMemcpyDeviceToHost, q.sc);
+    cudaEventRecord(q.done, q.sc);
+    if (q.sc != q.st) cudaStreamWaitEvent(q.st, q.done, 0);
+    return KLE_OK;
+  };
+  int rc = KLE_OK;
+  for (int p = 0; p < pipes && rc == KLE_OK; ++p) {
+    if (!pp[p].live) continue;
+    rc = enqueue(pp[p]);
+    if (p == 0 && pipes == 2)  // the second half starts after the first half's first fine sweep
+      cudaStreamWaitEvent(pp[1].st, pp[0].fdone, 0);
+  }
+  for (bool any = true; any && rc == KLE_OK;) {
+    any = false;
+    for (int p = 0; p < pipes && rc == KLE_OK; ++p) {
+      Pipe& q = pp[p];
+      if (!q.live) continue;
+      const cudaError_t e = cudaEventSynchronize(q.done);
+      if (e != cudaSuccess) {
+        rc = set_error(KLE_ERR_CUDA, cudaGetErrorString(e));
+        break;
+      }
+      if (h_count[p] == 0 || q.k >= max_iters) {
+        q.live = false;
+        continue;
+      }
+      any = true;
+      rc = enqueue(q);
+    }
+  }
+  if (pipes == 2) {  // join: later work on `st` sees both halves
+    for (int p = 0; p < pipes; ++p) {
+      cudaEventRecord(pp[p].done, pp[p].sc);
+      cudaStreamWaitEvent(st, pp[p].done, 0);
+    }
+  }
+  for (int p = 0; p < pipes; ++p) {
+    if (pipes == 2) {
+      cudaStreamDestroy(pp[p].st);
+      cudaStreamDestroy(pp[p].sc);
+    }
+    cudaEventDestroy(pp[p].done);
+    cudaEventDestroy(pp[p].fdone);
+  }
+  cudaEventDestroy(ready);
+  cudaStreamSynchronize(st);
+  cudaFreeHost(h_count);
+  return rc;
 }
 
 int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
