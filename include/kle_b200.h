@@ -139,6 +139,32 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
                        double tol, int max_iters, int32_t* status, int32_t* iters, double* inc_hist,
                        double* imag, void* workspace, size_t workspace_bytes, void* stream);
 
+/* pcgc_solve with a reference trajectory (pintuq/pcgc.py:273-358 with
+ * `reference=`): ref [M][N][nx] is the serial fine solution (fine_reference,
+ * pintuq/propagators.py:160-176). Records err_hist [M][max_iters+1][N]
+ * (_error_record, pintuq/parareal.py:87-91; k = 0 is the initial guess,
+ * NaN-initialised) and max_err [M] (the last recorded max error); both
+ * optional. stop_on_reference != 0 is stop_on="reference": a sample stops
+ * at the first k whose max error is <= tol (k = 0 included, iters = 0);
+ * otherwise the increment stops it as in kle_pcgc_solve_f64. */
+int kle_pcgc_solve_ref_f64(double* U, const double* u0, const double* dia, const double* off,
+                           const double* fine_blob, const double* scaling, const double* inv_scaling,
+                           const double* lam, int M, int N, int nx, int J, double T, double alpha, double g0,
+                           double tol, int max_iters, const double* ref, int stop_on_reference, int32_t* status,
+                           int32_t* iters, double* inc_hist, double* err_hist, double* max_err, double* imag,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* One error record of the iterate U against ref (pintuq/parareal.py:87-91)
+ * for the samples active at iteration k (status ACTIVE or iters == k; all at
+ * k = 0), written to err_hist[s][k][:] ([M][max_iters+1][N], optional) and
+ * max_err[s] (optional). With stop_on_reference, samples whose max error is
+ * <= tol are marked CONVERGED with iters = k (active_count decremented for
+ * k > 0; at k = 0 it counts the samples left active). Used by the batched
+ * loops (1D and 2D). */
+int kle_err_ref_f64(const double* U, const double* ref, int M, int N, int nx, int k, int max_iters, double tol,
+                    int stop_on_reference, int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist,
+                    double* max_err, void* stream);
+
 /* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
  * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);
  * norms[degree+1] = 1/sqrt(k!). */

@@ -138,18 +138,33 @@ def fine_reference(op: SampleOperator, u0, N: int, J: int, dT: float):
 
 
 def pcgc(op: SampleOperator, u0, init_states, N, J, T, alpha, tol, max_iters,
-         keep_history=False):
-    """Outer PCGC loop with increment stopping (``pintuq/pcgc.py:273-358``).
+         keep_history=False, reference=None, stop_on="increment"):
+    """Outer PCGC loop (``pintuq/pcgc.py:273-358``): increment stopping, or
+    with ``reference`` (N, nx) the error records of ``_error_record``
+    (``pintuq/parareal.py:87-91``) and, for stop_on="reference", stopping at
+    the first record (k = 0 included, ``pcgc.py:312-316``) with max error <= tol.
 
-    Returns dict(states, iters, converged, increments, imag, history)."""
+    Returns dict(states, iters, converged, increments, imag, history, err, max_err)."""
     dT = T / N
     dt = dT / J
     lam, scaling = alpha_circulant(N, alpha)
     solvers = shifted_solvers(op, lam, dT)
     U = np.array(init_states, dtype=float, copy=True)
     increments, hist = [], [U.copy()] if keep_history else []
+    errs = []
+
+    def record(V):
+        if reference is not None:
+            errs.append(np.max(np.abs(V - reference), axis=1))
+            return float(np.max(errs[-1]))
+        return None
+
     imag = 0.0
     converged = False
+    me = record(U)
+    if stop_on == "reference" and me is not None and me <= tol:
+        converged = True
+        max_iters = 0
     for _k in range(1, max_iters + 1):
         starts = np.vstack([u0, U[:-1]])
         F_ends = np.array([fine(op, starts[n], J, dt) for n in range(N)])
@@ -158,13 +173,17 @@ def pcgc(op: SampleOperator, u0, init_states, N, J, T, alpha, tol, max_iters,
         U = U_new
         imag = max(imag, im)
         increments.append(inc)
+        me = record(U)
         if keep_history:
             hist.append(U.copy())
-        if inc <= tol:
+        metric = inc if stop_on == "increment" else me
+        if metric <= tol:
             converged = True
             break
+    err = np.array(errs) if reference is not None else None
     return dict(states=U, iters=len(increments), converged=converged,
-                increments=np.array(increments), imag=imag, history=hist)
+                increments=np.array(increments), imag=imag, history=hist, err=err,
+                max_err=None if err is None else err.max(axis=1))
 
 
 # ---------------------------------------------------------------------------

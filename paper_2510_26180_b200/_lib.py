@@ -36,6 +36,9 @@ _SIGS = {
     "kle_pcgc_workspace_bytes": ([_i, _i, _i], _z),
     "kle_pcgc_solve_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _i, _p, _p, _p, _p,
                             _p, _z, _p], _i),
+    "kle_pcgc_solve_ref_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _i, _p, _i, _p,
+                                _p, _p, _p, _p, _p, _p, _z, _p], _i),
+    "kle_err_ref_f64": ([_p, _p, _i, _i, _i, _i, _i, _d, _i, _p, _p, _p, _p, _p, _p], _i),
     "kle_2d_kl5pt_f64": ([_p, _i, _i, _p, _i, _d, _p, _p, _p, _p], _i),
     "kle_2d_factor_f64": ([_p, _p, _p, _i, _i, _p, _i, _d, _d, _p, _p, _p], _i),
     "kle_2d_fine_work_doubles": ([_i, _i, _i], _z),

@@ -195,11 +195,11 @@ size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
   return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256;
 }
 
-int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const double* off,
-                       const double* fine_blob, const double* scaling, const double* inv_scaling,
-                       const double* lam, int M, int N, int nx, int J, double T, double alpha, double g0,
-                       double tol, int max_iters, int32_t* status, int32_t* iters, double* inc_hist,
-                       double* imag, void* workspace, size_t workspace_bytes, void* stream) {
+static int pcgc_loop(double* U, const double* u0, const double* dia, const double* off, const double* fine_blob,
+                     const double* scaling, const double* inv_scaling, const double* lam, int M, int N, int nx, int J,
+                     double T, double alpha, double g0, double tol, int max_iters, int32_t* status, int32_t* iters,
+                     double* inc_hist, double* imag, const double* ref, int stop_ref, double* err_hist,
+                     double* max_err, void* workspace, size_t workspace_bytes, void* stream) {
   if (M < 0 || N < 1 || nx < 1 || J < 1 || max_iters < 1 || !(T > 0) || !(alpha > 0 && alpha < 1))
     return set_error(KLE_ERR_INVALID, "pcgc_solve: bad arguments");
   if (M == 0) return KLE_OK;
@@ -228,7 +228,12 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
   cudaMemsetAsync(iters, 0, sizeof(int32_t) * M, st);
   if (inc_hist) cudaMemsetAsync(inc_hist, 0xFF, sizeof(double) * (size_t)M * max_iters, st);
   if (imag) cudaMemsetAsync(imag, 0, sizeof(double) * M, st);
+  if (err_hist) cudaMemsetAsync(err_hist, 0xFF, sizeof(double) * (size_t)M * (max_iters + 1) * N, st);
   KLE_TRY(check_launch("pcgc_solve: init"));
+  if (ref)  // record k = 0 (the initial guess) and, for stop_on="reference", its stop test
+    KLE_TRY(err_ref(U, ref, M, N, nx, 0, max_iters, tol, stop_ref, status, iters, nullptr, err_hist, max_err, st));
+  // with stop_on="reference" the increment never stops a sample (tol < 0); err_ref_kernel does
+  const double cgc_tol = (ref && stop_ref) ? -1.0 : tol;
   // Sample pipelines: the batch is split into `pipes` contiguous halves, each
   // running its own outer loop on its own stream, started half an iteration
   // apart, so the FP64-bound fine sweeps of one half share the SMs with the
@@ -286,9 +291,14 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
     cudaMemsetAsync(q.count_d, 0, sizeof(int32_t), q.sc);
     const double* sf = clustered ? sfac + o * (shift_factor_doubles(1, N, nx)) : nullptr;
     void* cs = clustered ? static_cast<void*>(static_cast<char*>(cgc_scratch) + o * 16) : cgc_scratch;
-    KLE_TRY(kle_cgc_update_f64(R + o * N * nx, Uq, inv_scaling, lam, dq, eq, sf, q.M, N, nx, dT, k, max_iters, tol,
-                               sq, iters + o, inc_hist ? inc_hist + o * max_iters : nullptr, imag ? imag + o : nullptr,
-                               q.count_d, cs, clustered ? (size_t)q.M * 16 : cgc_scratch_bytes, q.sc));
+    KLE_TRY(kle_cgc_update_f64(R + o * N * nx, Uq, inv_scaling, lam, dq, eq, sf, q.M, N, nx, dT, k, max_iters,
+                               cgc_tol, sq, iters + o, inc_hist ? inc_hist + o * max_iters : nullptr,
+                               imag ? imag + o : nullptr, q.count_d, cs,
+                               clustered ? (size_t)q.M * 16 : cgc_scratch_bytes, q.sc));
+    if (ref)
+      KLE_TRY(err_ref(Uq, ref + o * N * nx, q.M, N, nx, k, max_iters, tol, stop_ref, sq, iters + o, q.count_d,
+                      err_hist ? err_hist + o * (size_t)(max_iters + 1) * N : nullptr, max_err ? max_err + o : nullptr,
+                      q.sc));
     cudaMemcpyAsync(&h_count[&q - pp], q.count_d, sizeof(int32_t), cudaMemcpyDeviceToHost, q.sc);
     cudaEventRecord(q.done, q.sc);
     if (q.sc != q.st) cudaStreamWaitEvent(q.st, q.done, 0);
@@ -337,6 +347,36 @@ int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const dou
   cudaStreamSynchronize(st);
   cudaFreeHost(h_count);
   return rc;
+}
+
+int kle_pcgc_solve_f64(double* U, const double* u0, const double* dia, const double* off,
+                       const double* fine_blob, const double* scaling, const double* inv_scaling,
+                       const double* lam, int M, int N, int nx, int J, double T, double alpha, double g0,
+                       double tol, int max_iters, int32_t* status, int32_t* iters, double* inc_hist,
+                       double* imag, void* workspace, size_t workspace_bytes, void* stream) {
+  return pcgc_loop(U, u0, dia, off, fine_blob, scaling, inv_scaling, lam, M, N, nx, J, T, alpha, g0, tol, max_iters,
+                   status, iters, inc_hist, imag, nullptr, 0, nullptr, nullptr, workspace, workspace_bytes, stream);
+}
+
+int kle_pcgc_solve_ref_f64(double* U, const double* u0, const double* dia, const double* off,
+                           const double* fine_blob, const double* scaling, const double* inv_scaling,
+                           const double* lam, int M, int N, int nx, int J, double T, double alpha, double g0,
+                           double tol, int max_iters, const double* ref, int stop_on_reference, int32_t* status,
+                           int32_t* iters, double* inc_hist, double* err_hist, double* max_err, double* imag,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (!ref) return set_error(KLE_ERR_INVALID, "pcgc_solve_ref: reference trajectory required");
+  return pcgc_loop(U, u0, dia, off, fine_blob, scaling, inv_scaling, lam, M, N, nx, J, T, alpha, g0, tol, max_iters,
+                   status, iters, inc_hist, imag, ref, stop_on_reference, err_hist, max_err, workspace,
+                   workspace_bytes, stream);
+}
+
+int kle_err_ref_f64(const double* U, const double* ref, int M, int N, int nx, int k, int max_iters, double tol,
+                    int stop_on_reference, int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist,
+                    double* max_err, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || k < 0 || max_iters < k) return set_error(KLE_ERR_INVALID, "err_ref: bad arguments");
+  if (!status || !iters) return set_error(KLE_ERR_INVALID, "err_ref: status and iters are required");
+  return err_ref(U, ref, M, N, nx, k, max_iters, tol, stop_on_reference, status, iters, active_count, err_hist,
+                 max_err, KLE_STREAM(stream));
 }
 
 int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,

@@ -100,6 +100,10 @@ int col_sum(const double* U, int M, int L, const double* center, double* out, do
             cudaStream_t st);
 size_t col_sum_partial_doubles(int M, int L);
 
+int err_ref(const double* U, const double* ref, int M, int N, int nx, int k, int max_iters, double tol, int stop_ref,
+            int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist, double* max_err,
+            cudaStream_t st);
+
 int axpby(const double* x, const double* y, double* out, double a, double b, size_t n, cudaStream_t st);
 
 }  // namespace kle

@@ -136,4 +136,63 @@ int axpby(const double* x, const double* y, double* out, double a, double b, siz
   return check_launch("axpby_kernel");
 }
 
+// Error of the iterate against the serial fine reference, per subinterval
+// (_error_record, pintuq/parareal.py:87-91: err_n = max_x |U_n - ref_n|,
+// max_err = max_n err_n), and the stop_on="reference" test of pcgc_solve
+// (pintuq/pcgc.py:312-316 for k = 0, :343-348 for k >= 1). One CTA per
+// sample. A sample takes part at iteration k if it was active during it:
+// status ACTIVE, or it terminated at this k (iters == k). With stop_ref the
+// CGC ran with tol < 0 (the increment never stops a sample), and this kernel
+// converges the samples whose max_err <= tol (fixing the active count).
+__global__ void err_ref_kernel(const double* __restrict__ U, const double* __restrict__ ref, int N, int nx, int k,
+                               int max_iters, double tol, int stop_ref, int32_t* __restrict__ status,
+                               int32_t* __restrict__ iters, int32_t* __restrict__ active_count,
+                               double* __restrict__ err_hist, double* __restrict__ max_err) {
+  const int s = blockIdx.x;
+  const int st0 = status[s];
+  if (k > 0 && st0 != KLE_SAMPLE_ACTIVE && iters[s] != k) return;
+  __shared__ double wmax[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const size_t base = (size_t)s * N * nx;
+  double mine = 0.0;
+  for (int n = w; n < N; n += nw) {
+    const double* u = U + base + (size_t)n * nx;
+    const double* r = ref + base + (size_t)n * nx;
+    double e = 0.0;
+    for (int i = lane; i < nx; i += 32) e = nanmax(e, fabs(__ldg(u + i) - __ldg(r + i)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = nanmax(e, __shfl_xor_sync(KLE_FULL_MASK, e, o));
+    if (lane == 0 && err_hist) err_hist[((size_t)s * (max_iters + 1) + k) * N + n] = e;
+    mine = nanmax(mine, e);
+  }
+  if (lane == 0) wmax[w] = mine;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double me = 0.0;
+  for (int i = 0; i < nw; ++i) me = nanmax(me, wmax[i]);
+  if (max_err) max_err[s] = me;
+  if (!stop_ref) return;
+  if (me <= tol) {  // NaN compares false
+    status[s] = KLE_SAMPLE_CONVERGED;
+    iters[s] = k;
+    if (k > 0 && st0 == KLE_SAMPLE_ACTIVE && active_count) atomicSub(active_count, 1);
+  } else if (k == 0) {
+    if (me != me) {
+      status[s] = KLE_SAMPLE_NONFINITE;
+      iters[s] = 0;
+    } else if (active_count) {
+      atomicAdd(active_count, 1);
+    }
+  }
+}
+
+int err_ref(const double* U, const double* ref, int M, int N, int nx, int k, int max_iters, double tol, int stop_ref,
+            int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist, double* max_err,
+            cudaStream_t st) {
+  if (M <= 0) return KLE_OK;
+  err_ref_kernel<<<M, 256, 0, st>>>(U, ref, N, nx, k, max_iters, tol, stop_ref, status, iters, active_count,
+                                    err_hist, max_err);
+  return check_launch("err_ref_kernel");
+}
+
 }  // namespace kle

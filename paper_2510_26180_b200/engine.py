@@ -40,10 +40,22 @@ class KleCgcSolver:
         self.tables = AlphaTables(build_alpha_circulant(grid.n_coarse, cfg.alpha))
         self._ws = None
 
-    def solve(self, xi, keep_initial: bool = False) -> KleCgcResult:
-        """xi: (M, d) host array or device tensor."""
+    def solve(self, xi, keep_initial: bool = False, stop_on: str = "increment",
+              with_reference: bool = False) -> KleCgcResult:
+        """xi: (M, d) host array or device tensor.
+
+        ``stop_on="reference"`` (or ``with_reference``) computes the serial fine
+        reference of every sample on the device and records the per-iteration
+        errors against it, as the reference harness does for every solve
+        (``_run_one_sample``, ``pintuq/experiments.py:212-235``: ``fine_reference``
+        then ``pcgc_solve(..., reference=, stop_on="reference")``)."""
         xi_d = to_dev(xi).reshape(-1, self.model.parameter_dim)
         op = DeviceOperator.from_model(self.model, xi_d)
+        reference = None
+        if stop_on == "reference" or with_reference:
+            from .propagators import fine_reference_batched
+
+            reference = fine_reference_batched(op, self.grid)
         U = self.surrogate.predict(xi_d)
         U0 = U.clone() if keep_initial else None
         if self._ws is None:
@@ -53,7 +65,8 @@ class KleCgcSolver:
         need = int(_lib.query("kle_pcgc_workspace_bytes", op.M, self.grid.n_coarse, self.model.nx))
         if self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
-        res = pcgc_solve_device(op, U, self.grid, self.cfg, self.tables, self._ws)
+        res = pcgc_solve_device(op, U, self.grid, self.cfg, self.tables, self._ws, reference=reference,
+                                stop_on=stop_on)
         return KleCgcResult(res, U0)
 
     @staticmethod

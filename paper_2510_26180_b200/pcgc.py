@@ -206,6 +206,18 @@ class BatchResult:
     status: "torch.Tensor"      # (M,) int32 SAMPLE_* words
     increments: "torch.Tensor"  # (M, max_iters) per-k increments, NaN past the stop
     imag: "torch.Tensor"        # (M,) max imaginary residue
+    err_vs_ref: "torch.Tensor | None" = None  # (M, max_iters+1, N) err_n of record k (k = 0: guess), NaN past the stop
+    max_err: "torch.Tensor | None" = None     # (M,) max error of the last record
+
+    def iters_to_tol(self, tol: float):
+        """Per sample, the first k whose max error vs the reference is <= tol
+        (IterationTrace.iters_to_tol, pintuq/parareal.py:49-54); -1 if none."""
+        if self.err_vs_ref is None:
+            raise ValueError("no reference errors were recorded")
+        me = self.err_vs_ref.amax(dim=2)  # NaN rows (past the stop) stay NaN
+        ok = me <= tol
+        first = torch.where(ok.any(dim=1), ok.int().argmax(dim=1), torch.full_like(ok[:, 0], -1, dtype=torch.int64))
+        return first
 
     def failures(self) -> dict:
         """{sample index: exception} for every sample that did not converge,
@@ -232,13 +244,20 @@ class BatchResult:
 
 
 def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, tables: AlphaTables = None,
-                      workspace=None) -> BatchResult:
+                      workspace=None, reference=None, stop_on: str = "increment") -> BatchResult:
     """The production loop: U (M, N, nx) device tensor is overwritten with the
-    final states (``kle_pcgc_solve_f64``)."""
+    final states (``kle_pcgc_solve_f64``). ``reference`` (M, N, nx), e.g.
+    ``fine_reference_batched``, adds the per-iteration error records of
+    ``pcgc_solve(reference=...)``; ``stop_on="reference"`` stops each sample
+    at its first record with max error <= tol (``kle_pcgc_solve_ref_f64``)."""
     from .twod import DeviceOperator2D, pcgc_solve_device2d
 
+    if stop_on not in ("increment", "reference"):
+        raise ValueError(f"stop_on must be 'increment' or 'reference', not {stop_on!r}")
+    if stop_on == "reference" and reference is None:
+        raise ValueError("stop_on='reference' requires a reference trajectory")
     if isinstance(op, DeviceOperator2D):
-        return pcgc_solve_device2d(op, U, grid, cfg, tables)
+        return pcgc_solve_device2d(op, U, grid, cfg, tables, reference=reference, stop_on=stop_on)
     M, N, nx = U.shape
     if N != grid.n_coarse or nx != op.nx or M != op.M:
         raise ValueError("initial guess length does not match the time grid")
@@ -250,18 +269,34 @@ def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, 
     iters = torch.empty(M, dtype=torch.int32, device="cuda")
     inc = empty(M, cfg.max_outer_iters)
     imag = empty(M)
-    _lib.call("kle_pcgc_solve_f64", ptr(U), ptr(op.u0), ptr(op.dia), ptr(op.off), ptr(op.blob(grid.deltat)),
-              ptr(tables.scaling), ptr(tables.inv_scaling), ptr(tables.lam), M, N, nx, grid.n_fine_per_coarse,
-              grid.t_final, cfg.alpha, op.g0, cfg.tol, cfg.max_outer_iters, ptr(status), ptr(iters), ptr(inc),
-              ptr(imag), ptr(workspace), nbytes, stream_ptr())
-    return BatchResult(U, iters, status, inc, imag)
+    common = (ptr(U), ptr(op.u0), ptr(op.dia), ptr(op.off), ptr(op.blob(grid.deltat)), ptr(tables.scaling),
+              ptr(tables.inv_scaling), ptr(tables.lam), M, N, nx, grid.n_fine_per_coarse, grid.t_final, cfg.alpha,
+              op.g0, cfg.tol, cfg.max_outer_iters)
+    if reference is None:
+        _lib.call("kle_pcgc_solve_f64", *common, ptr(status), ptr(iters), ptr(inc), ptr(imag), ptr(workspace),
+                  nbytes, stream_ptr())
+        return BatchResult(U, iters, status, inc, imag)
+    ref = to_dev(reference).contiguous()
+    if tuple(ref.shape) != (M, N, nx):
+        raise ValueError("reference trajectory shape does not match the initial guess")
+    err = empty(M, cfg.max_outer_iters + 1, N)
+    me = empty(M)
+    _lib.call("kle_pcgc_solve_ref_f64", *common, ptr(ref), int(stop_on == "reference"), ptr(status), ptr(iters),
+              ptr(inc), ptr(err), ptr(me), ptr(imag), ptr(workspace), nbytes, stream_ptr())
+    return BatchResult(U, iters, status, inc, imag, err, me)
 
 
-def pcgc_solve_batched(model, xis, grid: TimeGrid, cfg: SolverConfig, init_states) -> BatchResult:
-    """Batched ``pcgc_solve(stop_on="increment")`` over M samples."""
+def pcgc_solve_batched(model, xis, grid: TimeGrid, cfg: SolverConfig, init_states, reference=None,
+                       stop_on: str = "increment") -> BatchResult:
+    """Batched ``pcgc_solve`` over M samples (``reference``: (M, N, nx) or
+    ``"fine"`` for the batched serial fine reference of every sample)."""
     op = DeviceOperator.from_model(model, xis)
     U = to_dev(init_states).clone()
-    return pcgc_solve_device(op, U, grid, cfg)
+    if isinstance(reference, str) and reference == "fine":
+        from .propagators import fine_reference_batched
+
+        reference = fine_reference_batched(op, grid)
+    return pcgc_solve_device(op, U, grid, cfg, reference=reference, stop_on=stop_on)
 
 
 def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, init: CoarseTrajectory,

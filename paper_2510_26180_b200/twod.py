@@ -177,9 +177,12 @@ def _batch_size(op: DeviceOperator2D, N: int) -> int:
     return max(1, min(op.M, int(0.85 * free) // per))
 
 
-def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables = None, batch: int = None):
-    """Batched PCGC loop for the 2D operator (``pintuq/pcgc.py:273-358``,
-    stop_on="increment"); U (M, N, nx) is overwritten with the final states."""
+def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables = None, batch: int = None,
+                        reference=None, stop_on: str = "increment"):
+    """Batched PCGC loop for the 2D operator (``pintuq/pcgc.py:273-358``);
+    U (M, N, nx) is overwritten with the final states. ``reference`` (M, N,
+    nx) adds the error records; ``stop_on="reference"`` stops on them
+    (``kle_err_ref_f64`` after every correction)."""
     from .pcgc import BatchResult, build_alpha_circulant
 
     M, N, nx = U.shape
@@ -194,6 +197,19 @@ def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables 
     imag = torch.zeros(M, dtype=torch.float64, device="cuda")
     B = batch or _batch_size(op, N)
     active = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ref = err = me = None
+    stop_ref = int(stop_on == "reference")
+    if reference is not None:
+        ref = reference.contiguous()
+        if tuple(ref.shape) != (M, N, nx):
+            raise ValueError("reference trajectory shape does not match the initial guess")
+        err = torch.full((M, cfg.max_outer_iters + 1, N), float("nan"), dtype=torch.float64, device="cuda")
+        me = empty(M)
+    cgc_tol = -1.0 if (ref is not None and stop_ref) else cfg.tol
+
+    def record(Ub, lo, Mb, k, st, it):
+        _lib.call("kle_err_ref_f64", ptr(Ub), ptr(ref[lo:lo + Mb]), Mb, N, nx, k, cfg.max_outer_iters, cfg.tol,
+                  stop_ref, ptr(st), ptr(it), ptr(active), ptr(err[lo:lo + Mb]), ptr(me[lo:lo + Mb]), stream_ptr())
     import os
     import time
 
@@ -221,15 +237,23 @@ def pcgc_solve_device2d(op: DeviceOperator2D, U, grid, cfg, tables: AlphaTables 
         nw = int(_lib.query("kle_2d_cgc_work_doubles", Mb, N, op.n))
         work = torch.zeros(max(nw, 1), dtype=torch.float64, device="cuda")
         st, it, ih = status[lo:hi], iters[lo:hi], inc[lo:hi]
+        if ref is not None:
+            active.zero_()
+            record(Ub, lo, Mb, 0, st, it)
+            if stop_ref and int(active.item()) == 0:
+                del Lt_c, Dinv_c, R, work, ob
+                continue
         for k in range(1, cfg.max_outer_iters + 1):
             ob.fgr(Ub, tables, grid, cfg.alpha, R, status=st)
             mark(f"k={k} fgr")
             active.zero_()
             _lib.call("kle_2d_cgc_f64", ptr(R), None, ptr(Ub), None, ptr(Lt_c), ptr(Dinv_c), ptr(tables.inv_scaling),
-                      Mb, N, op.n, k, cfg.max_outer_iters, cfg.tol, ptr(st), ptr(it), None, ptr(ih), ptr(active),
+                      Mb, N, op.n, k, cfg.max_outer_iters, cgc_tol, ptr(st), ptr(it), None, ptr(ih), ptr(active),
                       ptr(work), nw, stream_ptr())
+            if ref is not None:
+                record(Ub, lo, Mb, k, st, it)
             mark(f"k={k} cgc")
             if int(active.item()) == 0:
                 break
         del Lt_c, Dinv_c, R, work, ob
-    return BatchResult(U, iters, status, inc, imag)
+    return BatchResult(U, iters, status, inc, imag, err, me)

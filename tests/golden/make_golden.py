@@ -27,6 +27,12 @@ Outputs (np.savez_compressed):
   c3s.npz  2D model (LogNormalKL2D) at small shapes (n=15, N=8, J=4, d=10):
            3 samples from coarse-sweep init; propagate_fine / propagate_coarse /
            three_step_solve / cgc_correct single-call vectors (SuperLU paths).
+  ref.npz  stop_on="reference" (the harness composition, pintuq/experiments.py:
+           212-257): c1 samples 0..7 from their surrogate U0 (kle-pcgc) and
+           samples 0..3 from random_guess_init (pcgc), plus c3s samples 0..2,
+           each against fine_reference: per-record error vectors, max errors,
+           increments, iteration counts, final fields; one c1 sample with
+           reference= but stop_on="increment".
   c3.npz   2D model at the config-3 shape (n=127, N=32, J=16, d=10): one
            sample from coarse-sweep init (iteration count, increments, field).
 """
@@ -274,7 +280,65 @@ def make_c3():
     print(f"c3 done in {time.time() - t0:.1f}s; iters {it}")
 
 
+def _ref_trace(model, grid, cfg, xi, init_states, stop_on="reference"):
+    reference = rprop.fine_reference(model, xi, grid, cfg)
+    init = rcore.CoarseTrajectory(model.initial_condition(xi), init_states)
+    tr = rpcgc.pcgc_solve(model, xi, grid, cfg, init, reference=reference, stop_on=stop_on, raise_on_max=False)
+    incs = np.array([np.nan] + [r.increment_inf for r in tr.records[1:]])
+    return dict(ref=reference.states, err=tr.error_vectors(), max_err=tr.max_errors(), incs=incs,
+                iters=tr.iterations, to_tol=tr.iters_to_tol(cfg.tol), final=tr.trajectory.states,
+                converged=tr.converged)
+
+
+def _pack(out, tag, runs, N, nx, K=61):
+    M = len(runs)
+    out[f"{tag}_ref"] = np.array([r["ref"] for r in runs])
+    out[f"{tag}_final"] = np.array([r["final"] for r in runs])
+    out[f"{tag}_iters"] = np.array([r["iters"] for r in runs], np.int32)
+    out[f"{tag}_to_tol"] = np.array([-1 if r["to_tol"] is None else r["to_tol"] for r in runs], np.int32)
+    err = np.full((M, K, N), np.nan)
+    me = np.full((M, K), np.nan)
+    inc = np.full((M, K), np.nan)
+    for i, r in enumerate(runs):
+        err[i, : len(r["err"])] = r["err"]
+        me[i, : len(r["max_err"])] = r["max_err"]
+        inc[i, : len(r["incs"])] = r["incs"]
+    out[f"{tag}_err"], out[f"{tag}_max_err"], out[f"{tag}_incs"] = err, me, inc
+
+
+def make_ref():
+    t0 = time.time()
+    out = {}
+    g1 = np.load(OUT / "c1.npz")
+    model = RefLogNormalKL1D(nx=127, d=4, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 16, 32)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    xs = g1["xi_all"]
+    kle = [_ref_trace(model, grid, cfg, rcore.ParameterSample(xs[i], id=i), g1["U0"][i]) for i in range(8)]
+    _pack(out, "kle", kle, 16, 127)
+    _, _, init_rng = rcore.RngStream(2718).split(3)
+    rnd_init, rnd = [], []
+    for i in range(4):
+        xi = rcore.ParameterSample(xs[i], id=i)
+        init = rpar.random_guess_init(model, xi, grid, init_rng).states
+        rnd_init.append(init)
+        rnd.append(_ref_trace(model, grid, cfg, xi, init))
+    _pack(out, "rnd", rnd, 16, 127)
+    out["rnd_init"] = np.array(rnd_init)
+    inc = [_ref_trace(model, grid, cfg, rcore.ParameterSample(xs[0], id=0), g1["U0"][0], stop_on="increment")]
+    _pack(out, "inc", inc, 16, 127)
+    g3 = np.load(OUT / "c3s.npz")
+    m2 = RefLogNormalKL2D(n=15, d=10, sigma=0.5, ell=0.25)
+    grid2 = rcore.make_time_grid(1.0, 8, 4)
+    c3 = [_ref_trace(m2, grid2, cfg, rcore.ParameterSample(g3["xi"][i], id=i), g3["coarse_sweep"][i])
+          for i in range(3)]
+    _pack(out, "c3s", c3, 8, 225)
+    np.savez_compressed(OUT / "ref.npz", **out)
+    print(f"ref done in {time.time() - t0:.1f}s; kle iters {out['kle_iters'].tolist()} "
+          f"rnd iters {out['rnd_iters'].tolist()} c3s iters {out['c3s_iters'].tolist()}")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3"]
+    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref"]
     for w in which:
-        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3}[w]()
+        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3, "ref": make_ref}[w]()

@@ -201,3 +201,59 @@ def test_oracle_2d_matches_reference_goldens(golden):
     lam, sc = ref_port.alpha_circulant(8, 1e-3)
     u, _ = ref_port.three_step(lam, sc, ref_port.shifted_solvers(op, lam, 1 / 8), g["r_rand"])
     np.testing.assert_array_equal(u, g["ts_u"])
+
+
+def _check_ref_run(out, g, tag, i):
+    K = out["iters"] + 1
+    assert out["iters"] == g[f"{tag}_iters"][i]
+    np.testing.assert_array_equal(out["states"], g[f"{tag}_final"][i])
+    np.testing.assert_array_equal(out["err"], g[f"{tag}_err"][i, :K])
+    np.testing.assert_array_equal(out["max_err"], g[f"{tag}_max_err"][i, :K])
+    np.testing.assert_array_equal(out["increments"], g[f"{tag}_incs"][i, 1:K])
+
+
+def test_ref_port_stop_on_reference_bitwise(golden):
+    """stop_on="reference" with the serial fine reference (the harness
+    composition, pintuq/experiments.py:212-235): kle-pcgc from the surrogate
+    U0, pcgc from random_guess_init, and reference= with increment stopping."""
+    model, grid, cfg = c1_config()
+    g1, g = golden("c1"), golden("ref")
+    u0 = model.initial_condition()
+    for tag, inits, stop in (("kle", g1["U0"], "reference"), ("rnd", g["rnd_init"], "reference"),
+                             ("inc", g1["U0"], "increment")):
+        for i in range(len(g[f"{tag}_iters"])):
+            op = _op(model, g1["xi_all"][i])
+            ref = ref_port.fine_reference(op, u0, 16, 32, grid.deltaT)
+            np.testing.assert_array_equal(ref, g[f"{tag}_ref"][i])
+            out = ref_port.pcgc(op, u0, inits[i], 16, 32, 1.0, cfg.alpha, cfg.tol, cfg.max_outer_iters,
+                                reference=ref, stop_on=stop)
+            _check_ref_run(out, g, tag, i)
+
+
+def test_random_guess_init_matches_reference(golden):
+    """random_guess_init draws (pintuq/parareal.py:63-71) from the harness's
+    init stream are reproduced by the drop-in (same PCG64 derivation)."""
+    from paper_2510_26180_b200 import ParameterSample, RngStream
+    from paper_2510_26180_b200.propagators import random_guess_init
+
+    model, grid, cfg = c1_config()
+    g1, g = golden("c1"), golden("ref")
+    _, _, init_rng = RngStream(2718).split(3)
+    for i in range(4):
+        tr = random_guess_init(model, ParameterSample(g1["xi_all"][i], id=i), grid, init_rng)
+        np.testing.assert_array_equal(tr.states, g["rnd_init"][i])
+
+
+def test_oracle_2d_stop_on_reference(golden):
+    from paper_2510_26180_b200.models import LogNormalKL2D
+
+    g3, g = golden("c3s"), golden("ref")
+    m = LogNormalKL2D(n=15, d=10)
+    for i in range(3):
+        dia, ex, ey = m.stencil(g3["xi"][i])
+        op = ref_port.SampleOperator.from_stencil2d(dia, ex, ey, 15, np.ones(225))
+        ref = ref_port.fine_reference(op, m.initial_condition(), 8, 4, 1 / 8)
+        np.testing.assert_array_equal(ref, g["c3s_ref"][i])
+        out = ref_port.pcgc(op, m.initial_condition(), g3["coarse_sweep"][i], 8, 4, 1.0, 1e-3, 1e-8, 60,
+                            reference=ref, stop_on="reference")
+        _check_ref_run(out, g, "c3s", i)
