@@ -165,6 +165,28 @@ int kle_err_ref_f64(const double* U, const double* ref, int M, int N, int nx, in
                     int stop_on_reference, int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist,
                     double* max_err, void* stream);
 
+/* Classical parareal, the paper's comparison baseline (parareal_solve,
+ * pintuq/parareal.py:100-191), for the tridiagonal models:
+ *   U_n^{k+1} = G(U_{n-1}^{k+1}) + F(U_{n-1}^k) - G(U_{n-1}^k),  U_{-1} = u0,
+ * G one backward-Euler step of dT (coarse_blob = kle_fine_factor_f64 with
+ * h = dT), F J steps of dt (fine_blob). init: Gprev[s][n] = G(start_n) with
+ * start = [u0, U_0 .. U_{N-2}] (:153-155). step: the sequential correction
+ * of one outer iteration given F[s][n] = F(start_n) (:170-176), increment
+ * and stop test (:181-190), per-sample status as kle_cgc_update_f64.
+ * solve: the whole loop (ref / err_hist / max_err / stop_on_reference as
+ * kle_pcgc_solve_ref_f64; ref may be NULL). nx <= 1024. */
+int kle_parareal_init_f64(const double* U, const double* u0, const double* coarse_blob, int M, int N, int nx,
+                          double dT, double g0, double* Gprev, void* stream);
+int kle_parareal_step_f64(double* U, const double* u0, const double* F, double* Gprev, const double* coarse_blob,
+                          int M, int N, int nx, double dT, double g0, int k, int max_iters, double tol,
+                          int32_t* status, int32_t* iters, double* inc_hist, int32_t* active_count, void* stream);
+size_t kle_parareal_workspace_bytes(int M, int N, int nx);
+int kle_parareal_solve_f64(double* U, const double* u0, const double* dia, const double* off,
+                           const double* fine_blob, const double* coarse_blob, int M, int N, int nx, int J, double T,
+                           double g0, double tol, int max_iters, const double* ref, int stop_on_reference,
+                           int32_t* status, int32_t* iters, double* inc_hist, double* err_hist, double* max_err,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
 /* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
  * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);
  * norms[degree+1] = 1/sqrt(k!). */

@@ -88,6 +88,8 @@ int kle_fgr_f64(const double* U, const double* u0, const double* F_given, double
   if (M == 0) return KLE_OK;
   const FineLayoutRT l = fine_layout(nx);
   if (l.MR == 0) return set_error(KLE_ERR_UNSUPPORTED, "fgr: nx too large");
+  if (!R && (F_given || !F_out || l.W || l.kind))
+    return set_error(KLE_ERR_UNSUPPORTED, "fgr: F ends only (R = NULL) needs F_out and a register layout");
   FgrArgs a{U, u0, F_given, F_out, R, fine_blob, dia, off, scaling, status, M, N, nx, J, dt, dT, g0, alpha};
   return fine_fgr(l, a, KLE_STREAM(stream));
 }
@@ -377,6 +379,84 @@ int kle_err_ref_f64(const double* U, const double* ref, int M, int N, int nx, in
   if (!status || !iters) return set_error(KLE_ERR_INVALID, "err_ref: status and iters are required");
   return err_ref(U, ref, M, N, nx, k, max_iters, tol, stop_on_reference, status, iters, active_count, err_hist,
                  max_err, KLE_STREAM(stream));
+}
+
+// ---- classical parareal (pintuq/parareal.py:100-191) ------------------------
+int kle_parareal_init_f64(const double* U, const double* u0, const double* coarse_blob, int M, int N, int nx,
+                          double dT, double g0, double* Gprev, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || !(dT > 0)) return set_error(KLE_ERR_INVALID, "parareal_init: bad arguments");
+  PararealArgs a{};
+  a.U = const_cast<double*>(U);
+  a.u0 = u0;
+  a.Gprev = Gprev;
+  a.gfac = coarse_blob;
+  a.M = M;
+  a.N = N;
+  a.nx = nx;
+  a.mode = 0;
+  a.dT = dT;
+  a.g0 = g0;
+  return parareal_run(fine_layout(nx), a, KLE_STREAM(stream));
+}
+
+int kle_parareal_step_f64(double* U, const double* u0, const double* F, double* Gprev, const double* coarse_blob,
+                          int M, int N, int nx, double dT, double g0, int k, int max_iters, double tol,
+                          int32_t* status, int32_t* iters, double* inc_hist, int32_t* active_count, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || k < 1 || max_iters < k || !(dT > 0))
+    return set_error(KLE_ERR_INVALID, "parareal_step: bad arguments");
+  PararealArgs a{U, u0, F, Gprev, coarse_blob, status, iters, inc_hist, active_count, M, N, nx, k, max_iters, 1,
+                 dT, g0, tol};
+  return parareal_run(fine_layout(nx), a, KLE_STREAM(stream));
+}
+
+size_t kle_parareal_workspace_bytes(int M, int N, int nx) {
+  if (M <= 0 || N <= 0 || nx <= 0) return 0;
+  return 2 * align256((size_t)M * N * nx * sizeof(double)) + 256;
+}
+
+int kle_parareal_solve_f64(double* U, const double* u0, const double* dia, const double* off,
+                           const double* fine_blob, const double* coarse_blob, int M, int N, int nx, int J, double T,
+                           double g0, double tol, int max_iters, const double* ref, int stop_on_reference,
+                           int32_t* status, int32_t* iters, double* inc_hist, double* err_hist, double* max_err,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || J < 1 || max_iters < 1 || !(T > 0))
+    return set_error(KLE_ERR_INVALID, "parareal_solve: bad arguments");
+  if (M == 0) return KLE_OK;
+  if (workspace_bytes < kle_parareal_workspace_bytes(M, N, nx))
+    return set_error(KLE_ERR_WORKSPACE, "parareal_solve: workspace too small");
+  const FineLayoutRT lay = fine_layout(nx);
+  if (lay.W != 0 || lay.kind != 0) return set_error(KLE_ERR_UNSUPPORTED, "parareal_solve: nx > 1024");
+  cudaStream_t st = KLE_STREAM(stream);
+  char* ws = static_cast<char*>(workspace);
+  double* F = reinterpret_cast<double*>(ws);
+  ws += align256((size_t)M * N * nx * sizeof(double));
+  double* G = reinterpret_cast<double*>(ws);
+  ws += align256((size_t)M * N * nx * sizeof(double));
+  int32_t* counter = reinterpret_cast<int32_t*>(ws);
+  const double dT = T / N, dt = dT / J;
+  cudaMemsetAsync(status, 0, sizeof(int32_t) * M, st);
+  cudaMemsetAsync(iters, 0, sizeof(int32_t) * M, st);
+  if (inc_hist) cudaMemsetAsync(inc_hist, 0xFF, sizeof(double) * (size_t)M * max_iters, st);
+  if (err_hist) cudaMemsetAsync(err_hist, 0xFF, sizeof(double) * (size_t)M * (max_iters + 1) * N, st);
+  KLE_TRY(check_launch("parareal_solve: init"));
+  if (ref) KLE_TRY(err_ref(U, ref, M, N, nx, 0, max_iters, tol, stop_on_reference, status, iters, nullptr, err_hist,
+                           max_err, st));
+  const double step_tol = (ref && stop_on_reference) ? -1.0 : tol;
+  KLE_TRY(kle_parareal_init_f64(U, u0, coarse_blob, M, N, nx, dT, g0, G, stream));
+  int32_t h_count = M;
+  for (int k = 1; k <= max_iters && h_count > 0; ++k) {
+    FgrArgs fa{U, u0, nullptr, F, nullptr, fine_blob, dia, off, nullptr, status, M, N, nx, J, dt, dT, g0, 0.0};
+    KLE_TRY(fine_fgr(lay, fa, st));
+    cudaMemsetAsync(counter, 0, sizeof(int32_t), st);
+    KLE_TRY(kle_parareal_step_f64(U, u0, F, G, coarse_blob, M, N, nx, dT, g0, k, max_iters, step_tol, status, iters,
+                                  inc_hist, counter, stream));
+    if (ref) KLE_TRY(err_ref(U, ref, M, N, nx, k, max_iters, tol, stop_on_reference, status, iters, counter,
+                             err_hist, max_err, st));
+    cudaMemcpyAsync(&h_count, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(KLE_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return KLE_OK;
 }
 
 int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
           if (row < nx && n0 + nl[r] < N) a.F_out[sbase + (size_t)(n0 + nl[r]) * nx + row] = x[r][j];
         }
     }
+    if (a.Rout == nullptr) return;  // F ends only (classical parareal)
     // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n), operands from shared memory
 #pragma unroll
     for (int r = 0; r < R; ++r) {

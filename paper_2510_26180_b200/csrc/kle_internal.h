@@ -32,6 +32,21 @@ struct FgrArgs {
   double dt, dT, g0, alpha;
 };
 
+struct PararealArgs {
+  double* U;              // [M][N][nx] in: U^k, out: U^{k+1} (mode 1); read-only in mode 0
+  const double* u0;       // [nx]
+  const double* F;        // [M][N][nx] fine ends F(U_n^k) (mode 1)
+  double* Gprev;          // [M][N][nx] G(U_n^k): written (mode 0) / read and replaced (mode 1)
+  const double* gfac;     // coarse factor blobs [M][doubles] of I + dT A
+  int32_t* status;        // optional [M]
+  int32_t* iters;         // optional [M]
+  double* inc_hist;       // optional [M][max_iters]
+  int32_t* active_count;  // optional
+  int M, N, nx, k, max_iters, mode;
+  double dT, g0, tol;
+};
+int parareal_run(FineLayoutRT lay, const PararealArgs& a, cudaStream_t st);
+
 struct SweepArgs {
   const double* start;  // [M][Q][nx]
   double* out;          // [M][Q][nseg][nx]

@@ -33,6 +33,11 @@ Outputs (np.savez_compressed):
            each against fine_reference: per-record error vectors, max errors,
            increments, iteration counts, final fields; one c1 sample with
            reference= but stop_on="increment".
+  para.npz classical parareal_solve (pintuq/parareal.py:100-191), the
+           paper's baseline: c1 samples 0..3 from coarse_sweep_init
+           (increment stop) and from random_guess_init against
+           fine_reference (reference stop, the harness's "parareal" solver),
+           c3s samples 0..2 (increment stop).
   c3.npz   2D model at the config-3 shape (n=127, N=32, J=16, d=10): one
            sample from coarse-sweep init (iteration count, increments, field).
 """
@@ -338,7 +343,56 @@ def make_ref():
           f"rnd iters {out['rnd_iters'].tolist()} c3s iters {out['c3s_iters'].tolist()}")
 
 
+def _para_trace(model, grid, cfg, xi, init_states, reference=None, stop_on="increment"):
+    init = rcore.CoarseTrajectory(model.initial_condition(xi), init_states)
+    tr = rpar.parareal_solve(model, xi, grid, cfg, init, reference=reference, stop_on=stop_on,
+                             raise_on_max=False)
+    incs = np.array([np.nan] + [r.increment_inf for r in tr.records[1:]])
+    out = dict(ref=None if reference is None else reference.states, iters=tr.iterations,
+               to_tol=tr.iters_to_tol(cfg.tol), final=tr.trajectory.states, incs=incs, converged=tr.converged)
+    if reference is not None:
+        out.update(err=tr.error_vectors(), max_err=tr.max_errors())
+    else:
+        out.update(err=np.zeros((0, grid.n_coarse)), max_err=np.zeros(0), ref=np.zeros((grid.n_coarse, model.nx)))
+    return out
+
+
+def make_para():
+    t0 = time.time()
+    out = {}
+    g1 = np.load(OUT / "c1.npz")
+    model = RefLogNormalKL1D(nx=127, d=4, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 16, 32)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    xs = g1["xi_all"]
+    cs_runs, cs_init = [], []
+    for i in range(4):
+        xi = rcore.ParameterSample(xs[i], id=i)
+        cs = rpar.coarse_sweep_init(model, xi, grid, cfg).states
+        cs_init.append(cs)
+        cs_runs.append(_para_trace(model, grid, cfg, xi, cs))
+    _pack(out, "cs", cs_runs, 16, 127)
+    out["cs_init"] = np.array(cs_init)
+    rnd = []
+    g = np.load(OUT / "ref.npz")
+    for i in range(4):
+        xi = rcore.ParameterSample(xs[i], id=i)
+        ref = rprop.fine_reference(model, xi, grid, cfg)
+        rnd.append(_para_trace(model, grid, cfg, xi, g["rnd_init"][i], reference=ref, stop_on="reference"))
+    _pack(out, "rnd", rnd, 16, 127)
+    g3 = np.load(OUT / "c3s.npz")
+    m2 = RefLogNormalKL2D(n=15, d=10, sigma=0.5, ell=0.25)
+    grid2 = rcore.make_time_grid(1.0, 8, 4)
+    c3 = [_para_trace(m2, grid2, cfg, rcore.ParameterSample(g3["xi"][i], id=i), g3["coarse_sweep"][i])
+          for i in range(3)]
+    _pack(out, "c3s", c3, 8, 225)
+    np.savez_compressed(OUT / "para.npz", **out)
+    print(f"para done in {time.time() - t0:.1f}s; cs iters {out['cs_iters'].tolist()} "
+          f"rnd iters {out['rnd_iters'].tolist()} c3s iters {out['c3s_iters'].tolist()}")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref"]
+    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para"]
     for w in which:
-        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3, "ref": make_ref}[w]()
+        {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3, "ref": make_ref,
+         "para": make_para}[w]()

@@ -257,3 +257,32 @@ def test_oracle_2d_stop_on_reference(golden):
         out = ref_port.pcgc(op, m.initial_condition(), g3["coarse_sweep"][i], 8, 4, 1.0, 1e-3, 1e-8, 60,
                             reference=ref, stop_on="reference")
         _check_ref_run(out, g, "c3s", i)
+
+
+def test_ref_port_parareal_bitwise(golden):
+    """Classical parareal restatement (pintuq/parareal.py:100-191) against the
+    reference: coarse-sweep init with increment stop, random init with the
+    reference stop (1D), and the 2D plugin."""
+    from paper_2510_26180_b200.models import LogNormalKL2D
+
+    model, grid, cfg = c1_config()
+    g1, gr, g = golden("c1"), golden("ref"), golden("para")
+    u0 = model.initial_condition()
+    for i in range(4):
+        op = _op(model, g1["xi_all"][i])
+        np.testing.assert_array_equal(ref_port.coarse_sweep(op, u0, 16, grid.deltaT), g["cs_init"][i])
+        out = ref_port.parareal(op, u0, g["cs_init"][i], 16, 32, 1.0, cfg.tol, cfg.max_outer_iters)
+        assert out["iters"] == g["cs_iters"][i]
+        np.testing.assert_array_equal(out["states"], g["cs_final"][i])
+        np.testing.assert_array_equal(out["increments"], g["cs_incs"][i, 1:out["iters"] + 1])
+        ref = ref_port.fine_reference(op, u0, 16, 32, grid.deltaT)
+        out = ref_port.parareal(op, u0, gr["rnd_init"][i], 16, 32, 1.0, cfg.tol, cfg.max_outer_iters,
+                                reference=ref, stop_on="reference")
+        _check_ref_run(out, g, "rnd", i)
+    g3 = golden("c3s")
+    m = LogNormalKL2D(n=15, d=10)
+    for i in range(3):
+        op = ref_port.SampleOperator.from_stencil2d(*m.stencil(g3["xi"][i]), 15, np.ones(225))
+        out = ref_port.parareal(op, m.initial_condition(), g3["coarse_sweep"][i], 8, 4, 1.0, 1e-8, 60)
+        assert out["iters"] == g["c3s_iters"][i]
+        np.testing.assert_array_equal(out["states"], g["c3s_final"][i])
