@@ -98,7 +98,12 @@ size_t kle_cgc_scratch_bytes(int M, int N, int nx) {
   if (M <= 0 || N <= 0 || nx <= 0) return 0;
   const size_t slab = (size_t)cgc_grid(M, N, nx) * cgc_scratch_doubles_per_cta(N, nx) * sizeof(double);
   const size_t slots = (size_t)M * 2 * sizeof(unsigned long long);
-  return slab > slots ? slab : slots;
+  size_t b = slab > slots ? slab : slots;
+  if (cgc_large_supported(N, nx)) {
+    const size_t l = cgc_large_scratch_bytes(M, N, nx);
+    if (l > b) b = l;
+  }
+  return b;
 }
 
 size_t kle_shift_factor_bytes(int M, int N, int nx) {

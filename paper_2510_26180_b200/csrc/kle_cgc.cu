@@ -18,6 +18,7 @@
 //   phase 3  u = diag(1/scaling) F(q) (Hermitian completion), U^{k+1} = Re u,
 //            increment / imaginary-residue reductions, per-sample stop test.
 #include <cmath>
+#include <cstdlib>
 
 #include "kle_common.cuh"
 #include "kle_internal.h"
@@ -237,6 +238,11 @@ int cgc_grid(int M, int N, int nx) {
   return M < g ? (M > 0 ? M : 1) : g;
 }
 
+static bool use_large(int N, int nx) {
+  static const char* env = getenv("KLE_CGC_LARGE");  // 0: on-the-fly kernel (A/B)
+  return cgc_large_supported(N, nx) && !(env && env[0] == '0');
+}
+
 size_t cgc_scratch_doubles_per_cta(int N, int nx) {
   const size_t NF = (size_t)N / 2 + 1;
   return 4 * (size_t)nx * NF;  // p/y/q (complex) + inverse pivots (complex)
@@ -244,6 +250,7 @@ size_t cgc_scratch_doubles_per_cta(int N, int nx) {
 
 int cgc_run(const CgcArgs& a, cudaStream_t st) {
   if (a.N < 1 || a.nx < 1) return set_error(KLE_ERR_INVALID, "cgc: bad dims");
+  if (use_large(a.N, a.nx)) return cgc_large_run(a, st);
   int log2N = -1;
   if ((a.N & (a.N - 1)) == 0) {
     log2N = 0;

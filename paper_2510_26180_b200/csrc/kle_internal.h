@@ -102,6 +102,10 @@ int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st);
 int cgc_grid(int M, int N, int nx);
 size_t cgc_scratch_doubles_per_cta(int N, int nx);
 int cgc_run(const CgcArgs& a, cudaStream_t st);
+// large blocks (power-of-two N <= 1024, any nx): streaming FFT / solve / FFT kernels
+bool cgc_large_supported(int N, int nx);
+size_t cgc_large_scratch_bytes(int M, int N, int nx);
+int cgc_large_run(const CgcArgs& a, cudaStream_t st);
 
 int kl_tridiag(const double* xi, int M, int d, const double* table, int nx, double inv_h2, double* dia,
                double* off, cudaStream_t st);
