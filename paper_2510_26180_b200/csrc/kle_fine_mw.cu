@@ -15,6 +15,8 @@
 //   aex    product of the chunk-end forward multipliers of the lanes before
 //          this one in its warp;  sex  same for the backward, lanes after
 //   aw/sw  whole-warp products
+#include <cstdlib>
+
 #include "kle_fine.cuh"
 #include "kle_internal.h"
 
@@ -296,6 +298,229 @@ __global__ void __launch_bounds__(256, 2) sweep_mw_kernel(SweepArgs a, int W) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused F + CGC rhs, persistent over subintervals: CTA = (sample, group of G
+// subintervals), R subintervals in flight per lane (R right-hand sides share
+// the factor registers, the scans and the barriers), factors loaded once per
+// CTA, the next group's start rows prefetched into shared memory (cp.async)
+// while the current group sweeps; prev_n (= start_n for n >= 1) re-read from
+// L2 in the epilogue.
+// cfw[w][q] = prod_{q<p<w} aw[p] (q < w), cbw[w][q] = prod_{w<p<q} sw[p] (q > w):
+// the weights of the warp composites, so each warp sums them in parallel
+template <int MR, int R>
+__device__ void mw_steps_r(double (&x)[R][MR], const MwLane<MR>& f, const double* __restrict__ cfw,
+                           const double* __restrict__ cbw, double (*fw)[16], double (*bw)[16], int W, int J,
+                           double hg) {
+  const int k = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int it = 0; it < J; ++it) {
+#pragma unroll
+    for (int j = 1; j < MR; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+    double Y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t);
+        Y[r] = fma(f.af[t], o, Y[r]);  // af = 0 for k < 2^t
+      }
+    if (k == 31)
+#pragma unroll
+      for (int r = 0; r < R; ++r) fw[r][w] = Y[r];
+    __syncthreads();
+    double Cin[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      // Yw = sum_{q<w} cfw[w][q] fw[q]: independent products, no serial chain
+      double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; q += 2) {
+        if (q < w) y0 = fma(cfw[w * 16 + q], fw[r][q], y0);
+        if (q + 1 < w) y1 = fma(cfw[w * 16 + q + 1], fw[r][q + 1], y1);
+      }
+      double Yex = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1);
+      if (k == 0) Yex = 0.0;
+      Cin[r] = fma(f.aex, y0 + y1, Yex);
+    }
+    double pi = 1.0;
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      pi *= -f.l[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(pi, Cin[r], x[r][j]);
+    }
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j) {
+      const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+      const double kap = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double z = fma(x[r][j], f.inv[j], kap);
+        if (j + 1 < MR) z = fma(-ln, x[r][j + 1], z);
+        x[r][j] = z;
+      }
+    }
+    double X[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) X[r] = x[r][0];
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t);
+        X[r] = fma(f.bb[t], o, X[r]);  // bb = 0 for k + 2^t >= 32
+      }
+    if (k == 0)
+#pragma unroll
+      for (int r = 0; r < R; ++r) bw[r][w] = X[r];
+    __syncthreads();
+    double Xin[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; q += 2) {
+        if (q > w && q < W) x0 = fma(cbw[w * 16 + q], bw[r][q], x0);
+        if (q + 1 > w && q + 1 < W) x1 = fma(cbw[w * 16 + q + 1], bw[r][q + 1], x1);
+      }
+      double Xex = __shfl_down_sync(KLE_FULL_MASK, X[r], 1);
+      if (k == 31) Xex = 0.0;
+      Xin[r] = fma(f.sex, x0 + x1, Xex);
+    }
+    double sg = 1.0;
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j) {
+      sg *= -((j + 1 < MR) ? f.l[j + 1] : f.lnx);
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(sg, Xin[r], x[r][j]);
+    }
+  }
+}
+
+__device__ __forceinline__ void mw_cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
+// padded shared-memory row index: lane-owned MR-row chunks (stride MR + 1,
+// odd) so the 32 lanes of a warp hit distinct banks
+template <int MR>
+__device__ __forceinline__ int mw_pidx(int row) { return row + row / MR; }
+
+template <int MR, int R>
+__global__ void __launch_bounds__(256, 1) fgr_mw2_kernel(FgrArgs a, int W, int G) {
+  const MwLayout<MR> L(W);
+  const int s = blockIdx.x;
+  if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
+  const int LD = L.nxp + L.nxp / MR + 2;  // padded row length (+ guard for row nx)
+  extern __shared__ __align__(16) double sm[];
+  // [2][R][LD] start rows (double-buffered: the current group's rows are also
+  // its prev rows in the epilogue), [R][LD] F ends
+  double* ob = sm + 2 * R * LD;
+  __shared__ double fw[R][16], bw[R][16], cfw[16 * 16], cbw[16 * 16];
+  const int lane = threadIdx.x, tid = threadIdx.x;
+  const int nx = a.nx, N = a.N, NT = 32 * W;
+  const int nbeg = blockIdx.y * G, nend = min(N, nbeg + G);
+  const size_t sbase = (size_t)s * N * nx;
+  const double* blob = a.ffac + (size_t)s * L.doubles();
+  if (tid < W) {  // composite weights of warp tid
+    const int w = tid;
+    double p = 1.0;
+    for (int q = w - 1; q >= 0; --q) {
+      cfw[w * 16 + q] = p;
+      p *= blob[L.aw_off() + q];
+    }
+    p = 1.0;
+    for (int q = w + 1; q < W; ++q) {
+      cbw[w * 16 + q] = p;
+      p *= blob[L.sw_off() + q];
+    }
+  }
+  auto prefetch = [&](int n0, double* dst) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int n = n0 + r;
+      if (n >= nend) break;
+      const double* src = (n == 0) ? a.u0 : a.U + sbase + (size_t)(n - 1) * nx;
+      for (int row = tid; row < nx; row += NT) mw_cp_async8(dst + r * LD + mw_pidx<MR>(row), src + row);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  prefetch(nbeg, sm);
+  MwLane<MR> f;
+  mw_load<MR>(f, blob, L, lane, nx);
+  const double hg = a.dt * a.g0;
+  const double* dd = a.dia + (size_t)s * nx;
+  const double* ee = a.off + (size_t)s * nx;
+  int cur = 0;
+  for (int n0 = nbeg; n0 < nend; n0 += R, cur ^= 1) {
+    double* buf = sm + cur * R * LD;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    if (n0 + R < nend) prefetch(n0 + R, sm + (cur ^ 1) * R * LD);
+    double x[R][MR];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = lane * MR + j;
+        x[r][j] = (row < nx && n0 + r < nend) ? buf[r * LD + mw_pidx<MR>(row)] + hg : 0.0;
+      }
+    mw_steps_r<MR, R>(x, f, cfw, cbw, fw, bw, W, a.J, hg);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = lane * MR + j;
+        ob[r * LD + mw_pidx<MR>(row)] = (row < nx) ? x[r][j] - hg : 0.0;
+      }
+    if (tid == 0)
+#pragma unroll
+      for (int r = 0; r < R; ++r) ob[r * LD + mw_pidx<MR>(nx)] = 0.0;  // F_{nx} = 0 (Dirichlet)
+    __syncthreads();
+    // epilogue, rows strided over the threads (coalesced): R_n = scaling_n ((I + dT A) F_n - prev_n);
+    // prev_n = start_n (buf) for n >= 1, alpha U_{N-1} for n = 0
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int n = n0 + r;
+      if (n >= nend) break;
+      const double* F = ob + r * LD;
+      const double* pv = buf + r * LD;
+      if (a.F_out)
+        for (int row = tid; row < nx; row += NT) a.F_out[sbase + (size_t)n * nx + row] = F[mw_pidx<MR>(row)];
+      if (!a.Rout) continue;
+      const double sc = a.scaling[n];
+      const double* p0 = a.U + sbase + (size_t)(N - 1) * nx;
+      constexpr int EB = 8;
+      for (int r0 = tid; r0 < nx; r0 += EB * NT) {
+        double em[EB], dg[EB], ep[EB], pr[EB];
+#pragma unroll
+        for (int b = 0; b < EB; ++b) {
+          const int row = r0 + b * NT;
+          const bool in = row < nx;
+          em[b] = (in && row > 0) ? __ldg(ee + row - 1) : 0.0;
+          ep[b] = (in && row < nx - 1) ? __ldg(ee + row) : 0.0;
+          dg[b] = in ? __ldg(dd + row) : 0.0;
+          pr[b] = in ? ((n == 0) ? a.alpha * __ldg(p0 + row) : pv[mw_pidx<MR>(row)]) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < EB; ++b) {
+          const int row = r0 + b * NT;
+          if (row >= nx) break;
+          const double Fc = F[mw_pidx<MR>(row)];
+          const double Fm = row > 0 ? F[mw_pidx<MR>(row - 1)] : 0.0;
+          const double Fp = F[mw_pidx<MR>(row + 1)];
+          const double Ax = fma(em[b], Fm, fma(dg[b], Fc, ep[b] * Fp));
+          a.Rout[sbase + (size_t)n * nx + row] = sc * (fma(a.dT, Ax, Fc) - pr[b]);
+        }
+      }
+    }
+  }
+}
+
 int mw_warps(int nx) {
   const int W = (nx + 32 * MW_MR - 1) / (32 * MW_MR);
   return (W >= 1 && W <= 8) ? W : 0;
@@ -313,10 +538,28 @@ int mw_factor(const double* dia, const double* off, double* blob, int M, int nx,
   return check_launch("mw_factor_kernel");
 }
 
+template <int R>
+static int launch_mw2(const FgrArgs& a, int W, cudaStream_t st) {
+  const MwLayout<MW_MR> L(W);
+  const int G = 16 * R;  // subintervals per CTA
+  const size_t smem = sizeof(double) * 3 * R * (size_t)(L.nxp + L.nxp / MW_MR + 2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fgr_mw2_kernel<MW_MR, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  fgr_mw2_kernel<MW_MR, R><<<dim3(a.M, (a.N + G - 1) / G), 32 * W, smem, st>>>(a, W, G);
+  return check_launch("fgr_mw2_kernel");
+}
+
 int mw_fgr(const FgrArgs& a, cudaStream_t st) {
   const int W = mw_warps(a.nx);
   if (!W) return set_error(KLE_ERR_UNSUPPORTED, "fgr (multi-warp): nx too large");
   if (a.N > 65535) return set_error(KLE_ERR_UNSUPPORTED, "fgr (multi-warp): N too large");
+  static const char* env = getenv("KLE_FINE_MW");  // 0: one CTA per subinterval (A/B); 1/2: R
+  const int v = (env && *env) ? atoi(env) : 1;
+  if (!a.F_given && v == 1) return launch_mw2<1>(a, W, st);
+  if (!a.F_given && v == 2) return launch_mw2<2>(a, W, st);
   fgr_mw_kernel<MW_MR><<<dim3(a.M, a.N), 32 * W, 0, st>>>(a, W);
   return check_launch("fgr_mw_kernel");
 }
