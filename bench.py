@@ -521,6 +521,12 @@ def run_c5(args):
     out = {"metric": "c5 CGC stress: iterations per alpha, CGC throughput", "config": {
         "workload": "BASELINE configs[4]: nx=4095, N=1024, J=8, d=4, coarse-sweep init, tol=1e-8",
         "samples": M, "chunk": chunk}, "alphas": {}}
+    # warm-up (untimed): one small chunk through the whole path (kernel attributes, allocator)
+    op = DeviceOperator.from_model(model, xi[:8])
+    U = coarse_sweep_init_batched(op, grid).contiguous()
+    pcgc_solve_device(op, U, grid, SolverConfig(alpha=1e-1, tol=1e-8, max_outer_iters=60, seed=SEED))
+    torch.cuda.synchronize()
+    del U, op
     for alpha in (1e-1, 1e-2, 1e-4):
         cfg = SolverConfig(alpha=alpha, tol=1e-8, max_outer_iters=60, seed=SEED)
         tables = AlphaTables(build_alpha_circulant(N, alpha))
@@ -542,9 +548,15 @@ def run_c5(args):
         op = DeviceOperator.from_model(model, xi[:chunk])
         U = coarse_sweep_init_batched(op, grid).contiguous()
         R = empty(chunk, N, nx)
-        _lib.call("kle_fgr_f64", ptr(U), ptr(op.u0), None, None, ptr(R), ptr(op.blob(grid.deltat)), ptr(op.dia),
+        blob = op.blob(grid.deltat)
+        fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fa.record()
+        _lib.call("kle_fgr_f64", ptr(U), ptr(op.u0), None, None, ptr(R), ptr(blob), ptr(op.dia),
                   ptr(op.off), ptr(tables.scaling), None, chunk, N, nx, J, grid.deltat, grid.deltaT, op.g0, alpha,
                   stream_ptr())
+        fb.record()
+        torch.cuda.synchronize()
+        fgr_ms = fa.elapsed_time(fb)
         sfac = shift_factors(op, tables, N, grid.deltaT)
         nb = 16 * chunk if sfac is not None else int(_lib.query("kle_cgc_scratch_bytes", chunk, N, nx))
         scratch = torch.zeros(max(nb, 8), dtype=torch.uint8, device="cuda")
@@ -562,7 +574,11 @@ def run_c5(args):
             "wall_s": wall_ms * 1e-3, "cgc_ms_per_launch": cgc_ms,
             "cgc_sample_iterations_per_s": chunk / (cgc_ms * 1e-3),
             "cgc_compulsory_gbs": 24.0 * chunk * N * nx / (cgc_ms * 1e-3) / 1e9,
-            "cgc_path": "cluster" if sfac is not None else "on-the-fly",
+            "cgc_hbm_frac": 24.0 * chunk * N * nx / (cgc_ms * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
+            "cgc_path": "cluster" if sfac is not None else "large (FFT / per-frequency solve / inverse FFT kernels)",
+            "fgr_ms_per_launch": fgr_ms,
+            "fgr_dof_updates_per_s": chunk * N * J * nx / (fgr_ms * 1e-3),
+            "fgr_tflops_alg": FLOPS_PER_DOF * chunk * N * J * nx / (fgr_ms * 1e-3) / 1e12,
         }
         del U, R, op, scratch
     print(json.dumps(out), flush=True)

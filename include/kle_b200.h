@@ -198,6 +198,15 @@ int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t*
 int kle_gpc_eval_f64(const double* Psi, int M, int K, const double* C, const double* mean, int L, double* U0,
                      void* stream);
 
+/* Surrogate build on the device (pintuq/surrogate.py:144-184):
+ * C[M][L] = bias[L] (optional) + A[M][K] * B, B = [K][L] row-major, or
+ * B^T with B = [L][K] row-major when trans_b != 0 (the Gram matrix X X^T of
+ * kl_build :153 and the projections X G^T of kl_coefficients :183), DMMA. */
+int kle_gemm_f64(const double* A, const double* B, const double* bias, double* C, int M, int K, int L, int trans_b,
+                 void* stream);
+/* out[s][l] = X[s][l] - v[l]: snapshot fluctuations about the mean (:63). */
+int kle_sub_row_f64(const double* X, const double* v, double* out, int M, int L, void* stream);
+
 /* Moments (absent in the reference): out[l] = sum_s U[s][l]
  * (center == NULL) or sum_s (U[s][l] - center[l])^2. Deterministic order. */
 size_t kle_col_sum_scratch_bytes(int M, int L);

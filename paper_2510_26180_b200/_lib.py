@@ -53,6 +53,8 @@ _SIGS = {
     "kle_2d_cgc_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z, _p], _i),
     "kle_gpc_basis_f64": ([_p, _i, _i, _i, _p, _i, _p, _p, _p], _i),
     "kle_gpc_eval_f64": ([_p, _i, _i, _p, _p, _i, _p, _p], _i),
+    "kle_gemm_f64": ([_p, _p, _p, _p, _i, _i, _i, _i, _p], _i),
+    "kle_sub_row_f64": ([_p, _p, _p, _i, _i, _p], _i),
     "kle_col_sum_scratch_bytes": ([_i, _i], _z),
     "kle_col_sum_f64": ([_p, _i, _i, _p, _p, _p, _p], _i),
     "kle_axpby_f64": ([_p, _p, _p, _d, _d, _z, _p], _i),

@@ -202,6 +202,38 @@ size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
   return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256;
 }
 
+struct PipeResources {
+  cudaStream_t sf[2], sc[2];  // per pipeline: fine sweeps (low priority), CGC (high priority)
+  cudaEvent_t done[2], fdone[2], ready;
+  int32_t* h_count;  // pinned [2]
+};
+
+// one set per host thread and device, created on first use, never freed
+// (process lifetime; a handful of streams/events and 8 pinned bytes)
+static PipeResources* pipe_resources() {
+  static thread_local PipeResources* per_dev[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (per_dev[dev]) return per_dev[dev];
+  auto* r = new PipeResources{};
+  int lo = 0, hi = 0;
+  bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess;
+  for (int p = 0; p < 2 && ok; ++p) {
+    ok = ok && cudaStreamCreateWithPriority(&r->sf[p], cudaStreamNonBlocking, lo) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithPriority(&r->sc[p], cudaStreamNonBlocking, hi) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&r->done[p], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&r->fdone[p], cudaEventDisableTiming) == cudaSuccess;
+  }
+  ok = ok && cudaEventCreateWithFlags(&r->ready, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaHostAlloc(&r->h_count, 2 * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
+  if (!ok) {
+    delete r;
+    return nullptr;
+  }
+  per_dev[dev] = r;
+  return r;
+}
+
 static int pcgc_loop(double* U, const double* u0, const double* dia, const double* off, const double* fine_blob,
                      const double* scaling, const double* inv_scaling, const double* lam, int M, int N, int nx, int J,
                      double T, double alpha, double g0, double tol, int max_iters, int32_t* status, int32_t* iters,
@@ -257,14 +289,15 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
     int32_t* count_d;
   };
   Pipe pp[2];
-  int32_t* h_count = nullptr;
-  if (cudaHostAlloc(&h_count, 2 * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess)
-    return set_error(KLE_ERR_CUDA, "pcgc_solve: pinned counter");
-  cudaEvent_t ready;
-  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  // streams, events and the pinned counters are created once per host thread
+  // and device and reused: driver resource calls inside a solve serialise with
+  // other driver clients (e.g. an nvidia-smi poll) and cost more than a short
+  // solve
+  PipeResources* res = pipe_resources();
+  if (!res) return set_error(KLE_ERR_CUDA, "pcgc_solve: stream/event/pinned-buffer creation failed");
+  int32_t* h_count = res->h_count;
+  cudaEvent_t ready = res->ready;
   cudaEventRecord(ready, st);
-  int lo = 0, hi = 0;
-  cudaDeviceGetStreamPriorityRange(&lo, &hi);
   for (int p = 0; p < pipes; ++p) {
     pp[p].m0 = (int)((long long)M * p / pipes);
     pp[p].M = (int)((long long)M * (p + 1) / pipes) - pp[p].m0;
@@ -275,12 +308,12 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
     if (pipes == 1) {
       pp[p].st = pp[p].sc = st;
     } else {
-      cudaStreamCreateWithPriority(&pp[p].st, cudaStreamNonBlocking, lo);
-      cudaStreamCreateWithPriority(&pp[p].sc, cudaStreamNonBlocking, hi);
+      pp[p].st = res->sf[p];
+      pp[p].sc = res->sc[p];
       cudaStreamWaitEvent(pp[p].st, ready, 0);
     }
-    cudaEventCreateWithFlags(&pp[p].done, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&pp[p].fdone, cudaEventDisableTiming);
+    pp[p].done = res->done[p];
+    pp[p].fdone = res->fdone[p];
   }
   auto enqueue = [&](Pipe& q) -> int {
     const int k = ++q.k;
@@ -342,17 +375,7 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
       cudaStreamWaitEvent(st, pp[p].done, 0);
     }
   }
-  for (int p = 0; p < pipes; ++p) {
-    if (pipes == 2) {
-      cudaStreamDestroy(pp[p].st);
-      cudaStreamDestroy(pp[p].sc);
-    }
-    cudaEventDestroy(pp[p].done);
-    cudaEventDestroy(pp[p].fdone);
-  }
-  cudaEventDestroy(ready);
   cudaStreamSynchronize(st);
-  cudaFreeHost(h_count);
   return rc;
 }
 
@@ -474,6 +497,17 @@ int kle_gpc_eval_f64(const double* Psi, int M, int K, const double* C, const dou
                      void* stream) {
   if (M < 0 || K < 1 || L < 1) return set_error(KLE_ERR_INVALID, "gpc_eval: bad dims");
   return gemm_bias(Psi, C, mean, U0, M, K, L, KLE_STREAM(stream));
+}
+
+int kle_gemm_f64(const double* A, const double* B, const double* bias, double* C, int M, int K, int L, int trans_b,
+                 void* stream) {
+  if (M < 0 || K < 1 || L < 0) return set_error(KLE_ERR_INVALID, "gemm: bad dims");
+  return gemm_bias(A, B, bias, C, M, K, L, KLE_STREAM(stream), trans_b != 0);
+}
+
+int kle_sub_row_f64(const double* X, const double* v, double* out, int M, int L, void* stream) {
+  if (M < 0 || L < 0) return set_error(KLE_ERR_INVALID, "sub_row: bad dims");
+  return sub_row(X, v, out, M, L, KLE_STREAM(stream));
 }
 
 size_t kle_col_sum_scratch_bytes(int M, int L) {

@@ -29,6 +29,9 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// TB: B is given transposed, [L][K] row-major (C = bias + A B^T: Gram and
+// projection products of the surrogate build, pintuq/surrogate.py:153, 183)
+template <bool TB>
 __global__ void __launch_bounds__(G_NT) gemm_bias_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                          const double* __restrict__ bias, double* __restrict__ C,
                                                          int M, int K, int L) {
@@ -48,10 +51,11 @@ __global__ void __launch_bounds__(G_NT) gemm_bias_kernel(const double* __restric
       cp_async8(&As[stage][kk][m], A + (ok ? (size_t)gm * K + gk : 0), ok);
     }
     for (int idx = tid; idx < GB_K * GB_N; idx += G_NT) {
-      const int kk = idx / GB_N, n = idx % GB_N;
+      const int kk = TB ? idx % GB_K : idx / GB_N, n = TB ? idx / GB_K : idx % GB_N;
       const int gk = k0 + kk, gn = n0 + n;
       const bool ok = gk < K && gn < L;
-      cp_async8(&Bs[stage][kk][n], B + (ok ? (size_t)gk * L + gn : 0), ok);
+      const size_t off = TB ? (size_t)gn * K + gk : (size_t)gk * L + gn;
+      cp_async8(&Bs[stage][kk][n], B + (ok ? off : 0), ok);
     }
     cp_async_commit();
   };
@@ -98,13 +102,30 @@ __global__ void __launch_bounds__(G_NT) gemm_bias_kernel(const double* __restric
 }
 
 int gemm_bias(const double* A, const double* B, const double* bias, double* C, int M, int K, int L,
-              cudaStream_t st) {
+              cudaStream_t st, bool trans_b) {
   if (M <= 0 || L <= 0) return KLE_OK;
   if (K <= 0) return set_error(KLE_ERR_INVALID, "gemm: K must be > 0");
   dim3 grid((L + GB_N - 1) / GB_N, (M + GB_M - 1) / GB_M);
   if (grid.y > 65535) return set_error(KLE_ERR_UNSUPPORTED, "gemm: M too large for one launch");
-  gemm_bias_kernel<<<grid, G_NT, 0, st>>>(A, B, bias, C, M, K, L);
+  if (trans_b) gemm_bias_kernel<true><<<grid, G_NT, 0, st>>>(A, B, bias, C, M, K, L);
+  else gemm_bias_kernel<false><<<grid, G_NT, 0, st>>>(A, B, bias, C, M, K, L);
   return check_launch("gemm_bias_kernel");
+}
+
+// out[s][l] = X[s][l] - v[l] (snapshot fluctuations, pintuq/surrogate.py:63)
+__global__ void sub_row_kernel(const double* __restrict__ X, const double* __restrict__ v, double* __restrict__ out,
+                               int M, int L) {
+  const size_t n = (size_t)M * L;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = X[i] - v[i % L];
+}
+
+int sub_row(const double* X, const double* v, double* out, int M, int L, cudaStream_t st) {
+  if (M <= 0 || L <= 0) return KLE_OK;
+  size_t blocks = ((size_t)M * L + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  sub_row_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, v, out, M, L);
+  return check_launch("sub_row_kernel");
 }
 
 }  // namespace kle

@@ -113,7 +113,8 @@ int kl_tridiag(const double* xi, int M, int d, const double* table, int nx, doub
 int gpc_basis(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
               const double* norms, double* Psi, cudaStream_t st);
 int gemm_bias(const double* A, const double* B, const double* bias, double* C, int M, int K, int L,
-              cudaStream_t st);
+              cudaStream_t st, bool trans_b = false);
+int sub_row(const double* X, const double* v, double* out, int M, int L, cudaStream_t st);
 
 int col_sum(const double* U, int M, int L, const double* center, double* out, double* partial,
             cudaStream_t st);

@@ -8,11 +8,13 @@ and one FP64 tensor-core GEMM forms ``U0 = mean + Psi C`` with the
 precontracted ``C = H^T diag(sqrt(lam)) G`` (inner dimension P), or
 ``U0 = mean + (Psi H^T diag(sqrt lam)) G`` when m_q < P (inner dimension m_q).
 
-The offline build (``build_surrogate`` :336-393) is a one-time host step as in
-the reference, except that the snapshot library is produced by the batched
-device PCGC solver (``collect_snapshots`` :67-117); the snapshot-method KL
-(``kl_build`` :144-171), the coefficients (:174-184) and the least-squares
-fit (:264-288) are small dense LAPACK problems solved on the host.
+The offline build (``build_surrogate`` :336-393): the snapshot library is
+produced by the batched device PCGC solver (``collect_snapshots`` :67-117);
+with the snapshots on the device, the snapshot-method KL runs its three
+large products there (``kl_build_device``: the Gram matrix X X^T :153 and
+the modes E^T X :167 as DMMA GEMMs, the coefficients X G^T :183), leaving
+the n_t x n_t ``eigh`` and the least-squares fit (:264-288) — small dense
+LAPACK problems — on the host, exactly as the reference solves them.
 """
 from __future__ import annotations
 
@@ -111,6 +113,7 @@ class SnapshotSet:
     mean_field: np.ndarray
     fluctuations: np.ndarray
     cell_weight: float
+    device_fields: object = None  # (n_t, N, nx) device tensor when collected on the device
 
     @property
     def n_train(self) -> int:
@@ -155,7 +158,9 @@ def collect_snapshots(model, grid: TimeGrid, cfg: SolverConfig, training: list, 
                 {training[i].id: RuntimeError(f"status {int(st[i])}") for i in bad},
             )
         fields = res.states
-    return make_snapshot_set(training, fields.cpu().numpy(), model.cell_volume * grid.deltaT)
+    snap = make_snapshot_set(training, fields.cpu().numpy(), model.cell_volume * grid.deltaT)
+    snap.device_fields = fields
+    return snap
 
 
 @dataclass
@@ -191,6 +196,51 @@ def kl_build(snap: SnapshotSet, eps_kl: float) -> KLBasis:
     m_q = min(int(np.searchsorted(ratios, 1.0 - eps_kl) + 1), int(np.sum(lam > _EIGENVALUE_FLOOR_REL * lam[0])))
     modes = ((1.0 / np.sqrt(lam[:m_q] * n_t))[:, None] * (E[:, :m_q].T @ X)).reshape((m_q,) + snap.fields.shape[1:])
     return KLBasis(lam, modes, m_q, snap.cell_weight, float(ratios[m_q - 1]))
+
+
+def _gemm(A, B, trans_b=False, bias=None):
+    from .device import empty, ptr, stream_ptr
+
+    M, K = A.shape
+    L = B.shape[0] if trans_b else B.shape[1]
+    C = empty(M, L)
+    _lib.call("kle_gemm_f64", ptr(A.contiguous()), ptr(B.contiguous()), ptr(bias), ptr(C), M, K, L, int(trans_b),
+              stream_ptr())
+    return C
+
+
+def kl_build_device(snap: SnapshotSet, eps_kl: float):
+    """``kl_build`` + ``kl_coefficients`` (pintuq/surrogate.py:144-184) with
+    the snapshot products on the device. Returns (KLBasis, zeta). The
+    eigendecomposition of the n_t x n_t covariance is the reference's own
+    host ``eigh``; mode selection is identical."""
+    from .device import empty, ptr, stream_ptr, to_dev
+    from .moments import device_col_sum, device_scale
+
+    if not 0.0 < eps_kl < 1.0:
+        raise ValueError(f"eps_kl must lie in (0, 1), got {eps_kl}")
+    F = snap.device_fields
+    n_t = snap.n_train
+    F2 = F.reshape(n_t, -1)
+    L = F2.shape[1]
+    mean = device_scale(device_col_sum(F2), 1.0 / n_t)
+    X = empty(n_t, L)
+    _lib.call("kle_sub_row_f64", ptr(F2.contiguous()), ptr(mean), ptr(X), n_t, L, stream_ptr())
+    gram = _gemm(X, X, trans_b=True).cpu().numpy()
+    lam, E = np.linalg.eigh((snap.cell_weight / n_t) * gram)
+    lam = np.clip(lam[::-1], 0.0, None)
+    E = E[:, ::-1]
+    total = float(np.sum(lam))
+    mean_energy = snap.cell_weight * float(np.sum(snap.mean_field ** 2))
+    if total <= _ZERO_VARIANCE_REL * max(mean_energy, 1.0):
+        return KLBasis(lam, np.empty((0,) + snap.fields.shape[1:]), 0, snap.cell_weight, 1.0), np.empty((n_t, 0))
+    ratios = np.cumsum(lam) / total
+    m_q = min(int(np.searchsorted(ratios, 1.0 - eps_kl) + 1), int(np.sum(lam > _EIGENVALUE_FLOOR_REL * lam[0])))
+    scale = 1.0 / np.sqrt(lam[:m_q] * n_t)
+    G = _gemm(to_dev(np.ascontiguousarray(scale[:, None] * E[:, :m_q].T)), X)  # (m_q, L) modes
+    zeta = snap.cell_weight * _gemm(X, G, trans_b=True).cpu().numpy() / np.sqrt(lam[:m_q])[None, :]
+    modes = G.cpu().numpy().reshape((m_q,) + snap.fields.shape[1:])
+    return KLBasis(lam, modes, m_q, snap.cell_weight, float(ratios[m_q - 1])), zeta
 
 
 def kl_coefficients(snap: SnapshotSet, basis: KLBasis) -> np.ndarray:
@@ -328,12 +378,17 @@ def surrogate_predict_batched(ds: DeviceSurrogate, xi_d, out=None):
 
 def build_surrogate(model, grid: TimeGrid, cfg: SolverConfig, training: list, eps_kl: float = 1e-10,
                     degree: int | None = None, snapshot_method: str = "pcgc", executor=None,
-                    snapshots: SnapshotSet | None = None, family: str = "hermite") -> KLGpcSurrogate:
-    """Snapshots (device) -> KL -> least-squares Hermite fit (host)."""
+                    snapshots: SnapshotSet | None = None, family: str = "hermite",
+                    kl_on_device: bool = True) -> KLGpcSurrogate:
+    """Snapshots (device) -> KL (device products, host eigh) -> least-squares
+    Hermite fit (host). ``kl_on_device=False`` runs the KL on the host."""
     if snapshots is None:
         snapshots = collect_snapshots(model, grid, cfg, training, snapshot_method, executor)
-    basis = kl_build(snapshots, eps_kl)
-    zeta = kl_coefficients(snapshots, basis)
+    if kl_on_device and snapshots.device_fields is not None:
+        basis, zeta = kl_build_device(snapshots, eps_kl)
+    else:
+        basis = kl_build(snapshots, eps_kl)
+        zeta = kl_coefficients(snapshots, basis)
     maps = model.fit_maps()
     points = np.column_stack([m.apply([xi.values[d] for xi in snapshots.samples]) for d, m in enumerate(maps)])
     if degree is None:
