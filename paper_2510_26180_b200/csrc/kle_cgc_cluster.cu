@@ -237,6 +237,38 @@ __device__ __forceinline__ void load_pivots(Cplx (&ib)[MR], Cplx& ibprev, const 
   for (int j = 0; j < MR; ++j) ib[j] = (r0 + j < nx) ? src[r0 + j] : Cplx{1.0, 0.0};
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// The lane's pivots 1/beta (rows r0 .. r0+MR-1 of its frequency, plus row
+// r0-1): in registers (SP = false) or read from the CTA's shared-memory copy
+// where used (SP = true: 32 fewer registers, 3 CTAs/SM).
+template <int MR, bool SP>
+struct PivSrc;
+template <int MR>
+struct PivSrc<MR, false> {
+  Cplx v[MR], pv;
+  __device__ __forceinline__ void init(const Cplx* g, const Cplx*, int, int r0, int nx) { load_pivots<MR>(v, pv, g, r0, nx); }
+  __device__ __forceinline__ Cplx operator[](int j) const { return v[j]; }
+  __device__ __forceinline__ Cplx prev(int j) const { return j == 0 ? pv : v[j - 1]; }
+};
+template <int MR>
+struct PivSrc<MR, true> {
+  const Cplx* sp;  // this frequency's [RB] row slice (swizzled)
+  int r0l;
+  Cplx pv;         // row r0 - 1
+  __device__ __forceinline__ void init(const Cplx* g, const Cplx* s, int rl, int r0, int nx) {
+    sp = s;
+    r0l = rl;
+    if (rl == 0) pv = (r0 > 0 && r0 - 1 < nx) ? g[r0 - 1] : Cplx{0.0, 0.0};
+  }
+  __device__ __forceinline__ Cplx at(int r) const { return sp[r ^ ((r >> 3) & 7)]; }
+  __device__ __forceinline__ Cplx operator[](int j) const { return at(r0l + j); }
+  __device__ __forceinline__ Cplx prev(int j) const { return (j == 0 && r0l == 0) ? pv : at(r0l + j - 1); }
+};
+
 // Composes the affine maps x -> A x + B held by the 8 lanes of a group
 // (butterfly; every lane ends with the ordered composite). OUTER_HIGH: the
 // higher lane's map is applied last.
@@ -256,11 +288,17 @@ struct ClShape {
   static constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
   static constexpr int NT = ((NF * CL_LANES + 31) / 32) * 32;  // one 8-lane group per frequency
   static constexpr int NSTEP = NT / RB;                         // column-fixed sweeps (0: generic loop)
-#ifndef KLE_CGC_MINB
-#define KLE_CGC_MINB 2  // 288 threads: 2 CTAs/SM (measured; 1 CTA without spills is slower)
+#ifndef KLE_CGC_SP
+#define KLE_CGC_SP 1  // pivots in shared memory, old U re-read from global: 3 CTAs/SM at 288 threads
 #endif
-  static constexpr int MINB = NT <= 160 ? 3 : KLE_CGC_MINB;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * N * HC + (size_t)N * RB + RB + 2 + N + 2 * N +
+  static constexpr bool SP = KLE_CGC_SP != 0;
+#ifndef KLE_CGC_MINB
+#define KLE_CGC_MINB 2  // 288 threads, pivots in registers: 2 CTAs/SM (measured; 1 CTA without spills is slower)
+#endif
+  static constexpr int MINB = (NT <= 160 || SP) ? 3 : KLE_CGC_MINB;
+  static constexpr size_t UOLD = SP ? 0 : (size_t)N * RB;           // doubles
+  static constexpr size_t PIV = SP ? (size_t)2 * NF * RB : 0;       // doubles: [NF][RB] complex, swizzled rows
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * N * HC + UOLD + PIV + RB + 2 + N + 2 * N +
                                                    8 * NF + 16);
 };
 
@@ -278,8 +316,9 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
 
   extern __shared__ __align__(16) double smem[];
   Cplx* tile = reinterpret_cast<Cplx*>(smem);       // [N][HC] packed spectra (swizzled columns)
-  double* uold = smem + 2 * N * HC;                 // [N][RB]
-  double* offs = uold + N * RB;                     // [RB + 2]: dT*off[row0-1 .. row0+RB]
+  double* uold = smem + 2 * N * HC;                 // [N][RB] (pivots in registers only)
+  Cplx* piv = reinterpret_cast<Cplx*>(uold + K::UOLD);  // [NF][RB] pivots (SP), row r at r ^ ((r >> 3) & 7)
+  double* offs = uold + K::UOLD + K::PIV;           // [RB + 2]: dT*off[row0-1 .. row0+RB]
   double* isc = offs + RB + 2;                      // [N]: inv_scaling
   Cplx* tw = reinterpret_cast<Cplx*>(isc + N);      // [N]
   Cplx* fwd = tw + N;                               // [NF][2]
@@ -298,7 +337,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
         double* dst = reinterpret_cast<double*>(&tile[tix<MR, HC>(n, ci)]) + part;
         if (row < nx) {
           cp_async8(dst, a.R + sb + (size_t)n * nx + row);
-          if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
+          if (!K::SP && a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
         } else {
           *dst = 0.0;
         }
@@ -310,10 +349,19 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
       double* dst = reinterpret_cast<double*>(&tile[tix<MR, HC>(n, col % HC)]) + (col / HC);
       if (row < nx) {
         cp_async8(dst, a.R + sb + (size_t)n * nx + row);
-        if (a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
+        if (!K::SP && a.U) cp_async8(uold + n * RB + col, a.U + sb + (size_t)n * nx + row);
       } else {
         *dst = 0.0;
       }
+    }
+  }
+  if constexpr (K::SP) {  // the CTA's rows of every frequency's pivots, 16-byte copies
+    const Cplx* src = reinterpret_cast<const Cplx*>(sfac_d) + (size_t)s * NF * nx;
+    for (int e = tid; e < NF * RB; e += NT) {
+      const int ff = e / RB, r = e % RB, row = row0 + r;
+      Cplx* dst = &piv[ff * RB + (r ^ ((r >> 3) & 7))];
+      if (row < nx) cp_async16(dst, src + (size_t)ff * nx + row);
+      else *dst = {1.0, 0.0};
     }
   }
   for (int e = tid; e < RB + 2; e += NT) {
@@ -331,8 +379,8 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   const int f = valid ? fsys : NF - 1;
   const int r0l = k * MR;  // local first row of this lane
   const int r0 = row0 + r0l;
-  Cplx ib[MR], ibprev;
-  load_pivots<MR>(ib, ibprev, reinterpret_cast<const Cplx*>(sfac_d) + ((size_t)s * NF + f) * nx, r0, nx);
+  PivSrc<MR, K::SP> ib;
+  ib.init(reinterpret_cast<const Cplx*>(sfac_d) + ((size_t)s * NF + f) * nx, piv + f * RB, r0l, r0, nx);
   cp_async_wait_all();
   __syncthreads();
   CGC_T(1);
@@ -361,7 +409,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   // keeping all MR of them live as well as the pivots spills registers
   auto lj = [&](int j) -> Cplx {
     const double E = offs[r0l + j];  // couples rows r0+j-1 and r0+j
-    const Cplx ip = (j == 0) ? ibprev : ib[j - 1];
+    const Cplx ip = ib.prev(j);
     return {E * ip.re, E * ip.im};
   };
   Cplx A = {1.0, 0.0};
@@ -496,11 +544,11 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   bool bad = false;  // fmax drops NaN; remember it separately (a NaN increment must not converge)
   double* __restrict__ out = a.Uout ? a.Uout : a.U;
   const bool track = a.U != nullptr;
-  auto upd = [&](int n, int col, int row) {
+  auto upd = [&](int n, int col, int row, double uo) {
     const Cplx z = tile[tix<MR, HC>(n, col % HC)];
     const double u = ((col < HC ? z.re : z.im) * rsN) * isc[n];
     if (track) {
-      const double d = fabs(u - uold[n * RB + col]);
+      const double d = fabs(u - uo);
       incmax = fmax(incmax, d);
       bad |= (d != d);
     }
@@ -509,13 +557,34 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   if constexpr (NSTEP > 0) {
     if (tid < NSTEP * RB) {
       const int col = tid % RB, row = row0 + col;
-      if (row < nx)
-        for (int n = tid / RB; n < N; n += NSTEP) upd(n, col, row);
+      if (row < nx) {
+        if constexpr (K::SP) {
+          // the column's old values, all loads issued before the stores (out may alias U)
+          constexpr int NR = (N + NSTEP - 1) / NSTEP;
+          constexpr int UB = NR < 8 ? NR : 8;  // loads in flight per batch
+#pragma unroll
+          for (int m0 = 0; m0 < NR; m0 += UB) {
+            double uo[UB];
+#pragma unroll
+            for (int m = 0; m < UB; ++m) {
+              const int n = tid / RB + (m0 + m) * NSTEP;
+              uo[m] = (track && m0 + m < NR && n < N) ? a.U[sb + (size_t)n * nx + row] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < UB; ++m) {
+              const int n = tid / RB + (m0 + m) * NSTEP;
+              if (m0 + m < NR && n < N) upd(n, col, row, uo[m]);
+            }
+          }
+        } else {
+          for (int n = tid / RB; n < N; n += NSTEP) upd(n, col, row, track ? uold[n * RB + col] : 0.0);
+        }
+      }
     }
   } else {
     for (int e = tid; e < N * RB; e += NT) {
       const int n = e / RB, col = e % RB, row = row0 + col;
-      if (row < nx) upd(n, col, row);
+      if (row < nx) upd(n, col, row, track ? (K::SP ? a.U[sb + (size_t)n * nx + row] : uold[n * RB + col]) : 0.0);
     }
   }
   if (__syncthreads_or(bad)) incmax = __longlong_as_double(0x7ff8000000000000LL);
