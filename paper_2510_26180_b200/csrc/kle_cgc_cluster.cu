@@ -205,27 +205,45 @@ __device__ void fft4step(Cplx* t, const Cplx* tw) {
   __syncthreads();
 }
 
-// pivots 1/beta_i of (lambda_f I + dT A), f = 0..N/2, layout [s][f][i]
-__global__ void shift_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
-                                    const double* __restrict__ lam, int M, int NF, int nx, double dT,
-                                    double* __restrict__ sfac) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= (long long)M * NF) return;
-  const int s = (int)(t / NF), f = (int)(t - (long long)s * NF);
+// pivots 1/beta_i of (lambda_f I + dT A), f = 0..N/2, layout [s][f][i].
+// One CTA per sample: thread f runs the sequential complex recurrence
+// (factor_shifted, pintuq/pcgc.py:112-135) over the rows in chunks of SF_CH,
+// staging each chunk in shared memory so the whole CTA stores it coalesced
+// (rows contiguous per frequency).
+constexpr int SF_CH = 64;
+__global__ void __launch_bounds__(128) shift_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
+                                                           const double* __restrict__ lam, int M, int NF, int nx,
+                                                           double dT, double* __restrict__ sfac) {
+  extern __shared__ __align__(16) Cplx stage[];  // [NF][SF_CH + 1]
+  const int s = blockIdx.x;
+  const int f = threadIdx.x;
   const double* d = dia + (size_t)s * nx;
   const double* e = off + (size_t)s * nx;
-  Cplx* out = reinterpret_cast<Cplx*>(sfac) + ((size_t)s * NF + f) * nx;
-  const Cplx lm = {lam[2 * f], lam[2 * f + 1]};
+  Cplx* out = reinterpret_cast<Cplx*>(sfac) + (size_t)s * NF * nx;
+  const bool act = f < NF;
+  const Cplx lm = act ? Cplx{lam[2 * f], lam[2 * f + 1]} : Cplx{1.0, 0.0};
   Cplx ib = {0.0, 0.0};
-  for (int i = 0; i < nx; ++i) {
-    Cplx beta = {fma(dT, d[i], lm.re), lm.im};
-    if (i > 0) {
-      const double E = dT * e[i - 1];
-      beta.re = fma(-E * E, ib.re, beta.re);
-      beta.im = fma(-E * E, ib.im, beta.im);
+  for (int i0 = 0; i0 < nx; i0 += SF_CH) {
+    const int nr = min(SF_CH, nx - i0);
+    if (act) {
+      for (int r = 0; r < nr; ++r) {
+        const int i = i0 + r;
+        Cplx beta = {fma(dT, __ldg(d + i), lm.re), lm.im};
+        if (i > 0) {
+          const double E = dT * __ldg(e + i - 1);
+          beta.re = fma(-E * E, ib.re, beta.re);
+          beta.im = fma(-E * E, ib.im, beta.im);
+        }
+        ib = crcp(beta);
+        stage[f * (SF_CH + 1) + r] = ib;
+      }
     }
-    ib = crcp(beta);
-    out[i] = ib;
+    __syncthreads();
+    for (int q = threadIdx.x; q < NF * nr; q += blockDim.x) {
+      const int ff = q / nr, r = q % nr;
+      out[(size_t)ff * nx + i0 + r] = stage[ff * (SF_CH + 1) + r];
+    }
+    __syncthreads();
   }
 }
 
@@ -658,7 +676,9 @@ int shift_factor(const double* dia, const double* off, const double* lam, int M,
   const int NF = N / 2 + 1;
   const long long nth = (long long)M * NF;
   if (nth == 0) return KLE_OK;
-  shift_factor_kernel<<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(dia, off, lam, M, NF, nx, dT, sfac);
+  if (NF > 128) return set_error(KLE_ERR_UNSUPPORTED, "shift_factor: N > 254");
+  const size_t smem = sizeof(Cplx) * (size_t)NF * (SF_CH + 1);
+  shift_factor_kernel<<<(unsigned)M, NF <= 64 ? 64 : 128, smem, st>>>(dia, off, lam, M, NF, nx, dT, sfac);
   return check_launch("shift_factor_kernel");
 }
 
