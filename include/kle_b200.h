@@ -187,6 +187,27 @@ int kle_parareal_solve_f64(double* U, const double* u0, const double* dia, const
                            int32_t* status, int32_t* iters, double* inc_hist, double* err_hist, double* max_err,
                            void* workspace, size_t workspace_bytes, void* stream);
 
+/* Nonlinear tridiagonal models (Burgers kind 0, Allen-Cahn kind 1): fused
+ * backward-Euler sweeps with a damped Newton iteration per step, the
+ * compiled kernels of the reference (pintuq/_kernels.pyx:100-163,
+ * be_sweep_burgers / be_sweep_allencahn; propagators.py:82-99). For every
+ * sample s and start q: out[s][q][g] = state after (g+1)*J steps of size h
+ * from start[s][q]; p0[s] = nu (Burgers) or eps (Allen-Cahn); bc_lo/bc_hi the
+ * Allen-Cahn boundary values. status[s][q] (optional) = 1-based index of the
+ * first step whose Newton iteration missed newton_tol within max_newton
+ * iterations (0 = success), as the reference's kernel status. */
+size_t kle_newton_work_bytes(int M, int Q, int nx);
+int kle_newton_sweep_f64(int kind, const double* start, double* out, const double* p0, int M, int Q, int nx, int J,
+                         int nseg, double h, double dx, double bc_lo, double bc_hi, double newton_tol, int max_newton,
+                         const int32_t* active, int32_t* status, void* work, size_t work_bytes, void* stream);
+
+/* The parareal correction of subinterval n (pintuq/parareal.py:174-176) for
+ * the samples with status ACTIVE (or all, status = NULL):
+ * U[s][n] = (Gn[s] + F[s][n]) - Gprev[s][n]; Gprev[s][n] = Gn[s]. Used by the
+ * nonlinear-model parareal loop, whose coarse steps are Newton sweeps. */
+int kle_para_combine_f64(double* U, const double* Gn, const double* F, double* Gprev, const int32_t* status, int M,
+                         int N, int nx, int n, void* stream);
+
 /* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
  * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);
  * norms[degree+1] = 1/sqrt(k!). */

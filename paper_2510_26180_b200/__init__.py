@@ -22,12 +22,13 @@ from .core import (
     TimeGrid,
     make_time_grid,
 )
-from .models import LinearModel, LogNormalKL1D, LogNormalKL2D, Model, ParameterMap, get_model
+from .models import (AllenCahn1D, Burgers1D, LinearModel, LogNormalKL1D, LogNormalKL2D, Model, ParameterMap,
+                     get_model)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "CoarseTrajectory", "ConfigError", "DeviceError", "InitMode", "IterationRecord", "IterationTrace",
+    "AllenCahn1D", "Burgers1D", "CoarseTrajectory", "ConfigError", "DeviceError", "InitMode", "IterationRecord", "IterationTrace",
     "LinearModel", "LogNormalKL1D", "LogNormalKL2D", "MaxItersExceededError", "Model", "NonConvergenceError",
     "ParameterMap", "ParameterSample", "PintuqError", "RankDeficientError", "RngStream",
     "SingularShiftError", "SnapshotError", "SolverConfig", "TimeGrid", "get_model", "make_time_grid",

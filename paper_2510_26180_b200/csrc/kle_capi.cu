@@ -487,6 +487,30 @@ int kle_parareal_solve_f64(double* U, const double* u0, const double* dia, const
   return KLE_OK;
 }
 
+// ---- nonlinear models: fused Newton backward-Euler sweeps (pintuq/_kernels.pyx) ----
+size_t kle_newton_work_bytes(int M, int Q, int nx) {
+  if (M <= 0 || Q <= 0 || nx <= 0) return 0;
+  return newton_work_doubles(M, Q, nx) * sizeof(double);
+}
+
+int kle_newton_sweep_f64(int kind, const double* start, double* out, const double* p0, int M, int Q, int nx, int J,
+                         int nseg, double h, double dx, double bc_lo, double bc_hi, double newton_tol, int max_newton,
+                         const int32_t* active, int32_t* status, void* work, size_t work_bytes, void* stream) {
+  if (kind < 0 || kind > 1 || M < 0 || Q < 0 || nx < 1 || J < 1 || nseg < 1 || max_newton < 0 || !(h > 0) ||
+      !(dx > 0))
+    return set_error(KLE_ERR_INVALID, "newton_sweep: bad arguments");
+  if (M == 0 || Q == 0) return KLE_OK;
+  if (work_bytes < kle_newton_work_bytes(M, Q, nx)) return set_error(KLE_ERR_WORKSPACE, "newton_sweep: work too small");
+  NewtonArgs a{start, out, p0, active, status, M, Q, nx, J, nseg, kind, max_newton, h, dx, bc_lo, bc_hi, newton_tol};
+  return newton_sweep(a, static_cast<double*>(work), KLE_STREAM(stream));
+}
+
+int kle_para_combine_f64(double* U, const double* Gn, const double* F, double* Gprev, const int32_t* status, int M,
+                         int N, int nx, int n, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || n < 0 || n >= N) return set_error(KLE_ERR_INVALID, "para_combine: bad arguments");
+  return para_combine(U, Gn, F, Gprev, status, M, N, nx, n, KLE_STREAM(stream));
+}
+
 int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
                       const double* norms, double* Psi, void* stream) {
   if (M < 0 || d < 1 || P < 1) return set_error(KLE_ERR_INVALID, "gpc_basis: bad dims");

@@ -47,6 +47,20 @@ struct PararealArgs {
 };
 int parareal_run(FineLayoutRT lay, const PararealArgs& a, cudaStream_t st);
 
+struct NewtonArgs {
+  const double* start;    // [M][Q][nx]
+  double* out;            // [M][Q][nseg][nx]
+  const double* p0;       // [M] nu (Burgers) or eps (Allen-Cahn)
+  const int32_t* active;  // optional [M]
+  int32_t* status;        // optional [M][Q]: first failing step (1-based), 0 = ok
+  int M, Q, nx, J, nseg, kind, max_newton;
+  double h, dx, bc_lo, bc_hi, newton_tol;
+};
+size_t newton_work_doubles(int M, int Q, int nx);
+int newton_sweep(const NewtonArgs& a, double* work, cudaStream_t st);
+int para_combine(double* U, const double* Gn, const double* F, double* Gp, const int32_t* status, int M, int N,
+                 int nx, int n, cudaStream_t st);
+
 struct SweepArgs {
   const double* start;  // [M][Q][nx]
   double* out;          // [M][Q][nseg][nx]

@@ -305,7 +305,136 @@ class LogNormalKL2D(LinearModel):
         return [ParameterSample(row, id=i) for i, row in enumerate(draws)]
 
 
-_MODELS = {"lognormal-kl-1d": LogNormalKL1D, "lognormal-kl-2d": LogNormalKL2D}
+# ---------------------------------------------------------------------------
+# Nonlinear tridiagonal models (pintuq/models.py:269-379): the reference's
+# fused Newton sweeps (_kernels.pyx) run on the device (kle_newton_sweep_f64).
+# ---------------------------------------------------------------------------
+class Burgers1D(Model):
+    """Viscous Burgers u_t + u u_x = nu u_xx on (0, 1), zero Dirichlet, upwind
+    convection switched on sign(u_i), nu = xi / 50, xi ~ U[1, 3]
+    (``pintuq/models.py:269-323``)."""
+
+    name = "burgers"
+    parameter_dim = 1
+    supports = ((1.0, 3.0),)
+    sweep_kind = 0
+
+    def __init__(self, dx: float = 1.0 / 100.0):
+        self.dx = float(dx)
+        self.m = round(1.0 / self.dx) - 1
+        self.nx = self.m
+        self.x = np.arange(1, self.m + 1) * self.dx
+
+    @property
+    def cell_volume(self) -> float:
+        return self.dx
+
+    @staticmethod
+    def viscosity(xi_value: float) -> float:
+        return xi_value / 50.0
+
+    def rhs(self, u, t, xi):
+        u = self.check_state(u)
+        nu, dx = self.viscosity(xi.values[0]), self.dx
+        left = np.concatenate(([0.0], u[:-1]))
+        right = np.concatenate((u[1:], [0.0]))
+        dudx = np.where(u >= 0.0, (u - left) / dx, (right - u) / dx)
+        return -u * dudx + nu * (left - 2.0 * u + right) / dx**2
+
+    def jacobian(self, u, t, xi):
+        import scipy.sparse as sp
+
+        u = self.check_state(u)
+        nu, dx = self.viscosity(xi.values[0]), self.dx
+        left = np.concatenate(([0.0], u[:-1]))
+        right = np.concatenate((u[1:], [0.0]))
+        up = u >= 0.0
+        diag = np.where(up, -(2.0 * u - left) / dx, -(right - 2.0 * u) / dx) - 2.0 * nu / dx**2
+        sub = np.where(up[1:], u[1:] / dx, 0.0) + nu / dx**2
+        sup = np.where(up[:-1], 0.0, -u[:-1] / dx) + nu / dx**2
+        return sp.diags([sub, diag, sup], [-1, 0, 1], format="csr")
+
+    def initial_condition(self, xi=None):
+        return np.sin(2.0 * np.pi * self.x)
+
+    def sample_parameters(self, count, rng: RngStream) -> list:
+        from .core import sample_uniform
+
+        return sample_uniform(*self.supports[0], count, rng)
+
+    def sweep_args(self, xi: ParameterSample) -> tuple:
+        """(kernel kind, parameters) of the fused implicit sweeps (``models.py:320-323``)."""
+        return "burgers", (self.viscosity(xi.values[0]), self.dx)
+
+    def sweep_params(self, xi) -> tuple:
+        """Device sweep parameters (p0 per sample; dx, bc_lo, bc_hi shared)."""
+        return self.viscosity(float(np.asarray(xi.values if isinstance(xi, ParameterSample) else xi)[0])), \
+            self.dx, 0.0, 0.0
+
+
+class AllenCahn1D(Model):
+    """Allen-Cahn u_t = eps u_xx - (u^3 - u) on (-1, 1), u(-1) = -1, u(1) = 1,
+    eps a truncated Gaussian on [0.06, 1] (``pintuq/models.py:326-379``)."""
+
+    name = "allen-cahn"
+    parameter_dim = 1
+    supports = ((0.06, 1.0),)
+    bc = (-1.0, 1.0)
+    gaussian = (0.53, 0.15)
+    sweep_kind = 1
+
+    def __init__(self, dx: float = 1.0 / 128.0):
+        self.dx = float(dx)
+        self.m = round(2.0 / self.dx) - 1
+        self.nx = self.m
+        self.x = -1.0 + np.arange(1, self.m + 1) * self.dx
+        self._lift = np.zeros(self.m)
+        self._lift[0] = self.bc[0] / self.dx**2
+        self._lift[-1] = self.bc[1] / self.dx**2
+
+    @property
+    def cell_volume(self) -> float:
+        return self.dx
+
+    def rhs(self, u, t, xi):
+        u = self.check_state(u)
+        eps = xi.values[0]
+        left = np.concatenate(([0.0], u[:-1]))
+        right = np.concatenate((u[1:], [0.0]))
+        d2 = (left - 2.0 * u + right) / self.dx**2 + self._lift
+        return eps * d2 - (u**3 - u)
+
+    def jacobian(self, u, t, xi):
+        import scipy.sparse as sp
+
+        u = self.check_state(u)
+        eps = xi.values[0]
+        m = self.m
+        band = sp.diags([np.ones(m - 1), -2.0 * np.ones(m), np.ones(m - 1)], [-1, 0, 1], format="csr") / self.dx**2
+        return eps * band - sp.diags(3.0 * u**2 - 1.0)
+
+    def initial_condition(self, xi=None):
+        return 0.53 * self.x + 0.47 * np.sin(-1.5 * np.pi * self.x)
+
+    def sample_parameters(self, count, rng: RngStream) -> list:
+        from .core import sample_truncated_gaussian
+
+        mu, sigma = self.gaussian
+        return sample_truncated_gaussian(mu, sigma, *self.supports[0], count, rng)
+
+    def with_boundaries(self, u: np.ndarray) -> np.ndarray:
+        return np.concatenate(([self.bc[0]], np.asarray(u, float), [self.bc[1]]))
+
+    def sweep_args(self, xi: ParameterSample) -> tuple:
+        return "allen-cahn", (xi.values[0], self.dx, self.bc[0], self.bc[1])
+
+    def sweep_params(self, xi) -> tuple:
+        return float(np.asarray(xi.values if isinstance(xi, ParameterSample) else xi)[0]), self.dx, \
+            self.bc[0], self.bc[1]
+
+
+_MODELS = {"lognormal-kl-1d": LogNormalKL1D, "lognormal-kl-2d": LogNormalKL2D, "burgers": Burgers1D,
+           "allen-cahn": AllenCahn1D}
 
 
 def get_model(name: str, **kwargs) -> Model:

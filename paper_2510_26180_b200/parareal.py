@@ -34,7 +34,12 @@ def _check_1d(op):
 def parareal_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, reference=None,
                           stop_on: str = "increment") -> BatchResult:
     """Batched ``parareal_solve`` for the M samples of ``op``: U (M, N, nx)
-    (the initial guesses) is overwritten with the final states."""
+    (the initial guesses) is overwritten with the final states. ``op`` may be
+    a ``nonlinear.NewtonOperator`` (Burgers, Allen-Cahn)."""
+    from .nonlinear import NewtonOperator, parareal_solve_newton
+
+    if isinstance(op, NewtonOperator):
+        return parareal_solve_newton(op, U, grid, cfg, reference, stop_on)
     if stop_on not in ("increment", "reference"):
         raise ValueError(f"stop_on must be 'increment' or 'reference', not {stop_on!r}")
     if stop_on == "reference" and reference is None:
@@ -73,8 +78,12 @@ def parareal_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig
     if init.n_coarse != grid.n_coarse:
         raise ValueError("initial guess length does not match the time grid")
     model.validate(xi)
+    from .nonlinear import NewtonOperator, is_newton_model
+
+    if is_newton_model(model):
+        return _parareal_newton_trace(model, xi, grid, cfg, init, reference, stop_on, raise_on_max)
     if not getattr(model, "is_linear", False):
-        raise NotImplementedError("the device parareal covers linear models only")
+        raise NotImplementedError("the device parareal covers linear and tridiagonal Newton models only")
     N = grid.n_coarse
     u0 = np.asarray(model.initial_condition(xi), dtype=float)
     op = DeviceOperator.from_model(model, [xi])
@@ -124,6 +133,36 @@ def parareal_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig
             break
     trace.trajectory = CoarseTrajectory(u0, host)
     trace.trajectory.assert_finite()
+    if not trace.converged and raise_on_max:
+        raise MaxItersExceededError(
+            f"parareal did not reach tol {cfg.tol:.1e} within {cfg.max_outer_iters} iterations", trace=trace
+        )
+    return trace
+
+
+def _parareal_newton_trace(model, xi, grid, cfg, init, reference, stop_on, raise_on_max):
+    """parareal_solve for one sample of a nonlinear model: the batched device
+    loop with M = 1, the trace rebuilt from its records."""
+    from .nonlinear import NewtonOperator, parareal_solve_newton
+
+    u0 = np.asarray(model.initial_condition(xi), dtype=float)
+    op = NewtonOperator.from_model(model, [xi], cfg)
+    U = to_dev(init.states)[None].clone()
+    ref = None if reference is None else to_dev(reference.states)[None]
+    res = parareal_solve_newton(op, U, grid, cfg, ref, stop_on)
+    k = int(res.iters[0].item())
+    trace = IterationTrace(solver="parareal", stop_on=stop_on)
+    errs = res.err_vs_ref[0].cpu().numpy() if res.err_vs_ref is not None else None
+    incs = res.increments[0].cpu().numpy()
+    for j in range(k + 1):
+        ev = None if errs is None else errs[j]
+        me = None if ev is None else float(np.max(ev))
+        trace.records.append(IterationRecord(j, None if j == 0 else float(incs[j - 1]), ev, me, 0.0))
+    trace.trajectory = CoarseTrajectory(u0, res.states[0].cpu().numpy())
+    st = int(res.status[0].item())
+    trace.converged = st == 1
+    if st == 3:
+        trace.trajectory.assert_finite()
     if not trace.converged and raise_on_max:
         raise MaxItersExceededError(
             f"parareal did not reach tol {cfg.tol:.1e} within {cfg.max_outer_iters} iterations", trace=trace

@@ -20,14 +20,27 @@ def _linear_only(model):
         raise NotImplementedError("the device propagators cover linear models only")
 
 
+def _sweep1(model, xi, cfg, u, h, J, nseg=1):
+    """One sample: (nseg, nx) states after J, 2J, ... steps of size h from u.
+    Linear models: partitioned LDL^T sweeps; the nonlinear tridiagonal models
+    (Burgers, Allen-Cahn): the fused Newton sweeps (pintuq/propagators.py:82-99)."""
+    from .nonlinear import NewtonOperator, is_newton_model
+
+    if is_newton_model(model):
+        op = NewtonOperator.from_model(model, [xi], cfg)
+        out, _ = op.sweep(to_dev(u)[None, None], h, J, nseg)
+        return out[0, 0].cpu().numpy()
+    _linear_only(model)
+    op = DeviceOperator.from_model(model, [xi])
+    return op.sweep(to_dev(u)[None, None], h, J, nseg=nseg)[0, 0].cpu().numpy()
+
+
 def backward_euler_step(model, u, t_from: float, dt: float, xi: ParameterSample, cfg: SolverConfig):
     """One implicit Euler step (``pintuq/propagators.py:102-118``)."""
     if dt <= 0:
         raise ValueError(f"step size must be positive, got {dt}")
     u = model.check_state(u)
-    _linear_only(model)
-    op = DeviceOperator.from_model(model, [xi])
-    return op.sweep(to_dev(u)[None, None], dt, 1)[0, 0, 0].cpu().numpy()
+    return _sweep1(model, xi, cfg, u, dt, 1)[0]
 
 
 def propagate_fine(model, u, t_from: float, t_to: float, grid: TimeGrid, xi: ParameterSample,
@@ -39,9 +52,7 @@ def propagate_fine(model, u, t_from: float, t_to: float, grid: TimeGrid, xi: Par
             f"fine propagation interval [{t_from}, {t_to}] does not span one coarse step {grid.deltaT}"
         )
     u = model.check_state(u)
-    _linear_only(model)
-    op = DeviceOperator.from_model(model, [xi])
-    return op.sweep(to_dev(u)[None, None], grid.deltat, grid.n_fine_per_coarse)[0, 0, 0].cpu().numpy()
+    return _sweep1(model, xi, cfg, u, grid.deltat, grid.n_fine_per_coarse)[0]
 
 
 def propagate_coarse(model, u, t_from: float, t_to: float, xi: ParameterSample, cfg: SolverConfig):
@@ -51,22 +62,16 @@ def propagate_coarse(model, u, t_from: float, t_to: float, xi: ParameterSample, 
 
 def fine_reference(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig) -> CoarseTrajectory:
     """Serial F trajectory at the coarse points (``pintuq/propagators.py:160-176``)."""
-    _linear_only(model)
     u0 = np.asarray(model.initial_condition(xi), dtype=float)
-    op = DeviceOperator.from_model(model, [xi])
-    out = op.sweep(to_dev(u0)[None, None], grid.deltat, grid.n_fine_per_coarse, nseg=grid.n_coarse)
-    traj = CoarseTrajectory(u0, out[0, 0].cpu().numpy())
+    traj = CoarseTrajectory(u0, _sweep1(model, xi, cfg, u0, grid.deltat, grid.n_fine_per_coarse, grid.n_coarse))
     traj.assert_finite()
     return traj
 
 
 def coarse_sweep_init(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig) -> CoarseTrajectory:
     """N serial coarse steps from u0 (``pintuq/parareal.py:74-84``)."""
-    _linear_only(model)
     u0 = np.asarray(model.initial_condition(xi), dtype=float)
-    op = DeviceOperator.from_model(model, [xi])
-    out = op.sweep(to_dev(u0)[None, None], grid.deltaT, 1, nseg=grid.n_coarse)
-    return CoarseTrajectory(u0, out[0, 0].cpu().numpy())
+    return CoarseTrajectory(u0, _sweep1(model, xi, cfg, u0, grid.deltaT, 1, grid.n_coarse))
 
 
 def random_guess_init(model, xi: ParameterSample, grid: TimeGrid, rng: RngStream) -> CoarseTrajectory:

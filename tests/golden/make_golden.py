@@ -38,6 +38,14 @@ Outputs (np.savez_compressed):
            (increment stop) and from random_guess_init against
            fine_reference (reference stop, the harness's "parareal" solver),
            c3s samples 0..2 (increment stop).
+  nl.npz   nonlinear models at the reference harness settings (BENCHMARK_DEFAULTS,
+           pintuq/experiments.py:33-38): Burgers1D (dx 1/100, T 2, N 25,
+           J 40) and AllenCahn1D (dx 1/128, N 30, J 48, T 3: at the harness's
+           T 30 the coarse Newton step from u0 fails, which the file records as
+           ac_fail_status), samples from
+           the models' own samplers: propagate_fine / propagate_coarse /
+           fine_reference single calls and classical parareal_solve from
+           coarse_sweep_init (increment stop, tol 1e-8).
   c3.npz   2D model at the config-3 shape (n=127, N=32, J=16, d=10): one
            sample from coarse-sweep init (iteration count, increments, field).
 """
@@ -391,8 +399,52 @@ def make_para():
           f"rnd iters {out['rnd_iters'].tolist()} c3s iters {out['c3s_iters'].tolist()}")
 
 
+def make_nl():
+    t0 = time.time()
+    out = {}
+    for tag, model, T, N, J, ns in (("bu", rmodels.Burgers1D(dx=1 / 100), 2.0, 25, 40, 3),
+                                    ("ac", rmodels.AllenCahn1D(dx=1 / 128), 3.0, 30, 48, 2)):
+        grid = rcore.make_time_grid(T, N, J)
+        cfg = rcore.SolverConfig(alpha=0.1, tol=1e-8, max_outer_iters=60, seed=2718)
+        xis = model.sample_parameters(ns, rcore.RngStream(2718).split(3)[1])
+        out[f"{tag}_xi"] = np.array([x.values for x in xis])
+        xi0 = xis[0]
+        u0 = model.initial_condition(xi0)
+        out[f"{tag}_pf"] = rprop.propagate_fine(model, u0, 0.0, grid.deltaT, grid, xi0, cfg)
+        out[f"{tag}_pc"] = rprop.propagate_coarse(model, u0, 0.0, grid.deltaT, xi0, cfg)
+        out[f"{tag}_ref"] = rprop.fine_reference(model, xi0, grid, cfg).states
+        out[f"{tag}_rhs0"] = model.rhs(u0, 0.0, xi0)
+        out[f"{tag}_jac0"] = model.jacobian(u0, 0.0, xi0).toarray()
+        finals, iters, incs, inits = [], [], np.full((ns, 61), np.nan), []
+        for i, xi in enumerate(xis):
+            cs = rpar.coarse_sweep_init(model, xi, grid, cfg)
+            tr = rpar.parareal_solve(model, xi, grid, cfg, cs)
+            inits.append(cs.states)
+            finals.append(tr.trajectory.states)
+            iters.append(tr.iterations)
+            inc = [r.increment_inf for r in tr.records[1:]]
+            incs[i, 1:len(inc) + 1] = inc
+        out[f"{tag}_init"] = np.array(inits)
+        out[f"{tag}_final"] = np.array(finals)
+        out[f"{tag}_iters"] = np.array(iters, np.int32)
+        out[f"{tag}_incs"] = incs
+        print(f"  {tag}: iters {iters} ({time.time() - t0:.1f}s)", flush=True)
+    # the harness's Allen-Cahn coarse step (dT = 1) from u0: Newton fails at step 1
+    ac = rmodels.AllenCahn1D(dx=1 / 128)
+    xi0 = rcore.ParameterSample(out["ac_xi"][0], id=0)
+    try:
+        rprop.propagate_coarse(ac, ac.initial_condition(xi0), 0.0, 1.0, xi0,
+                               rcore.SolverConfig(alpha=0.1, tol=1e-8, max_outer_iters=60))
+        out["ac_fail_status"] = np.int32(0)
+    except rcore.NonConvergenceError as exc:
+        out["ac_fail_status"] = np.int32(int(str(exc).split("step ")[1].split("/")[0]))
+        out["ac_fail_last"] = exc.last_iterate
+    np.savez_compressed(OUT / "nl.npz", **out)
+    print(f"nl done in {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para"]
+    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para", "nl"]
     for w in which:
         {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3, "ref": make_ref,
-         "para": make_para}[w]()
+         "para": make_para, "nl": make_nl}[w]()

@@ -286,3 +286,19 @@ def test_ref_port_parareal_bitwise(golden):
         out = ref_port.parareal(op, m.initial_condition(), g3["coarse_sweep"][i], 8, 4, 1.0, 1e-8, 60)
         assert out["iters"] == g["c3s_iters"][i]
         np.testing.assert_array_equal(out["states"], g["c3s_final"][i])
+
+
+def test_nonlinear_models_match_reference(golden):
+    """Burgers1D / AllenCahn1D host definitions (rhs, Jacobian, samplers,
+    initial states) against the reference's (pintuq/models.py:269-379)."""
+    from paper_2510_26180_b200 import AllenCahn1D, Burgers1D, ParameterSample, RngStream
+
+    g = golden("nl")
+    for tag, model, ns in (("bu", Burgers1D(dx=1 / 100), 3), ("ac", AllenCahn1D(dx=1 / 128), 2)):
+        xis = model.sample_parameters(ns, RngStream(2718).split(3)[1])
+        np.testing.assert_array_equal(np.array([x.values for x in xis]), g[f"{tag}_xi"])
+        xi0 = ParameterSample(g[f"{tag}_xi"][0], id=0)
+        u0 = model.initial_condition(xi0)
+        np.testing.assert_array_equal(model.rhs(u0, 0.0, xi0), g[f"{tag}_rhs0"])
+        np.testing.assert_array_equal(model.jacobian(u0, 0.0, xi0).toarray(), g[f"{tag}_jac0"])
+        assert model.nx == g[f"{tag}_ref"].shape[1]
