@@ -46,6 +46,7 @@ extern "C" {
 #define KLE_SAMPLE_CONVERGED 1   /* increment <= tol            (pintuq/pcgc.py:345-348) */
 #define KLE_SAMPLE_MAXITERS 2    /* MaxItersExceededError       (pintuq/pcgc.py:352-357) */
 #define KLE_SAMPLE_NONFINITE 3   /* CoarseTrajectory.assert_finite (pintuq/core.py:179-181) */
+#define KLE_SAMPLE_NEWTON 4      /* NonConvergenceError of the simplified Newton CGC (pintuq/pcgc.py:264-269) */
 
 int kle_abi_version(void);
 const char* kle_last_error(void);
@@ -207,6 +208,17 @@ int kle_newton_sweep_f64(int kind, const double* start, double* out, const doubl
  * nonlinear-model parareal loop, whose coarse steps are Newton sweeps. */
 int kle_para_combine_f64(double* U, const double* Gn, const double* F, double* Gprev, const int32_t* status, int M,
                          int N, int nx, int n, void* stream);
+
+/* cgc_correct for the nonlinear tridiagonal models (pintuq/pcgc.py:245-270):
+ * the simplified Newton iteration with the averaged Jacobian, each inner step
+ * a diagonalised three-step solve of (C_alpha (x) I - dT I (x) mean_jac),
+ * until max|u_next - u_l| <= newton_tol (at most 150 inner steps; then the
+ * sample's status becomes KLE_SAMPLE_NEWTON). One CTA per active sample:
+ * U [M][N][nx] the previous iterate, b = F_end - G(prev) (assemble_rhs_blocks),
+ * Uout the correction; inner[s] = inner iterations. N * nx <= ~9000. */
+int kle_newton_cgc_f64(int kind, const double* U, const double* b, double* Uout, const double* p0, const double* lam,
+                       const double* scaling, const double* inv_scaling, int M, int N, int nx, double dT, double dx,
+                       double bc_lo, double bc_hi, double newton_tol, int32_t* status, int32_t* inner, void* stream);
 
 /* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
  * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);

@@ -47,6 +47,7 @@ _SIGS = {
     "kle_newton_work_bytes": ([_i, _i, _i], _z),
     "kle_newton_sweep_f64": ([_i, _p, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _d, _d, _i, _p, _p, _p, _z, _p], _i),
     "kle_para_combine_f64": ([_p, _p, _p, _p, _p, _i, _i, _i, _i, _p], _i),
+    "kle_newton_cgc_f64": ([_i, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _d, _d, _d, _d, _p, _p, _p], _i),
     "kle_2d_kl5pt_f64": ([_p, _i, _i, _p, _i, _d, _p, _p, _p, _p], _i),
     "kle_2d_factor_f64": ([_p, _p, _p, _i, _i, _p, _i, _d, _d, _p, _p, _p], _i),
     "kle_2d_fine_work_doubles": ([_i, _i, _i], _z),

@@ -511,6 +511,16 @@ int kle_para_combine_f64(double* U, const double* Gn, const double* F, double* G
   return para_combine(U, Gn, F, Gprev, status, M, N, nx, n, KLE_STREAM(stream));
 }
 
+int kle_newton_cgc_f64(int kind, const double* U, const double* b, double* Uout, const double* p0, const double* lam,
+                       const double* scaling, const double* inv_scaling, int M, int N, int nx, double dT, double dx,
+                       double bc_lo, double bc_hi, double newton_tol, int32_t* status, int32_t* inner, void* stream) {
+  if (kind < 0 || kind > 1 || M < 0 || N < 1 || nx < 1 || !(dT > 0) || !(dx > 0))
+    return set_error(KLE_ERR_INVALID, "newton_cgc: bad arguments");
+  NewtonCgcArgs a{U, b, Uout, p0, lam, scaling, inv_scaling, status, inner, M, N, nx, kind, dT, dx, bc_lo, bc_hi,
+                  newton_tol};
+  return newton_cgc(a, KLE_STREAM(stream));
+}
+
 int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
                       const double* norms, double* Psi, void* stream) {
   if (M < 0 || d < 1 || P < 1) return set_error(KLE_ERR_INVALID, "gpc_basis: bad dims");

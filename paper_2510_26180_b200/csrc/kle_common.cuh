@@ -79,3 +79,6 @@ __device__ __forceinline__ double nanmax(double a, double b) {
 #define KLE_SAMPLE_MAXITERS 2
 #define KLE_SAMPLE_NONFINITE 3
 #endif
+#ifndef KLE_SAMPLE_NEWTON
+#define KLE_SAMPLE_NEWTON 4
+#endif

@@ -57,6 +57,20 @@ struct NewtonArgs {
   double h, dx, bc_lo, bc_hi, newton_tol;
 };
 size_t newton_work_doubles(int M, int Q, int nx);
+struct NewtonCgcArgs {
+  const double* U;            // [M][N][nx] U^k
+  const double* b;            // [M][N][nx] F - G(prev)
+  double* Uout;               // [M][N][nx] U^{k+1}
+  const double* p0;           // [M]
+  const double* lam;          // [2N]
+  const double* scaling;      // [N]
+  const double* inv_scaling;  // [N]
+  int32_t* status;            // optional [M]: skip non-active, NEWTON on failure
+  int32_t* inner;             // optional [M]: simplified-Newton iterations
+  int M, N, nx, kind;
+  double dT, dx, bc_lo, bc_hi, newton_tol;
+};
+int newton_cgc(const NewtonCgcArgs& a, cudaStream_t st);
 int newton_sweep(const NewtonArgs& a, double* work, cudaStream_t st);
 int para_combine(double* U, const double* Gn, const double* F, double* Gp, const int32_t* status, int M, int N,
                  int nx, int n, cudaStream_t st);

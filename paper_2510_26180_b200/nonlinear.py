@@ -140,3 +140,76 @@ def parareal_solve_newton(op: NewtonOperator, U, grid: TimeGrid, cfg: SolverConf
     iters.copy_(torch.as_tensor(it))
     return BatchResult(U, iters, status, inc_km.t().contiguous(), torch.zeros(M, dtype=torch.float64, device="cuda"),
                        err, me)
+
+
+# ---------------------------------------------------------------------------
+# PCGC for the nonlinear models (batched): Newton fine / coarse sweeps and the
+# simplified-Newton diagonalised CGC (pintuq/pcgc.py:245-270)
+# ---------------------------------------------------------------------------
+def pcgc_solve_newton(op: NewtonOperator, U, grid: TimeGrid, cfg: SolverConfig, reference=None,
+                      stop_on: str = "increment"):
+    """Batched ``pcgc_solve`` (``pintuq/pcgc.py:273-358``) for the M samples
+    of a nonlinear model; U (M, N, nx) initial guesses, overwritten. Per outer
+    iteration: the N fine Newton sweeps, the N coarse Newton steps of
+    ``assemble_rhs_blocks`` (b = F - G(prev), prev = [alpha U_N, U_1..]),
+    then ``kle_newton_cgc_f64`` (one CTA per sample runs the whole simplified
+    Newton loop). ``BatchResult.imag`` carries the per-sample inner iteration
+    count of the last correction (the reference's ``diag["inner_iters"]``)."""
+    from .device import AlphaTables
+    from .pcgc import BatchResult, build_alpha_circulant
+
+    if stop_on not in ("increment", "reference"):
+        raise ValueError(f"stop_on must be 'increment' or 'reference', not {stop_on!r}")
+    if stop_on == "reference" and reference is None:
+        raise ValueError("stop_on='reference' requires a reference trajectory")
+    M, N, nx = U.shape
+    if N != grid.n_coarse or nx != op.nx or M != op.M:
+        raise ValueError("initial guess length does not match the time grid")
+    K = cfg.max_outer_iters
+    tables = AlphaTables(build_alpha_circulant(N, cfg.alpha))
+    status = torch.zeros(M, dtype=torch.int32, device="cuda")
+    iters = torch.zeros(M, dtype=torch.int32, device="cuda")
+    inner = torch.zeros(M, dtype=torch.int32, device="cuda")
+    inc_km = torch.full((K, M), float("nan"), dtype=torch.float64, device="cuda")
+    inc_rec = torch.full((M, K + 1, N), float("nan"), dtype=torch.float64, device="cuda")
+    ref = err = me = None
+    stop_ref = int(stop_on == "reference")
+    if reference is not None:
+        ref = to_dev(reference).contiguous()
+        err = torch.full((M, K + 1, N), float("nan"), dtype=torch.float64, device="cuda")
+        me = empty(M)
+        _lib.call("kle_err_ref_f64", ptr(U), ptr(ref), M, N, nx, 0, K, cfg.tol, stop_ref, ptr(status), ptr(iters),
+                  None, ptr(err), ptr(me), stream_ptr())
+    u0b = op.u0[None, None].expand(M, 1, nx).contiguous()
+    b = empty(M, N, nx)
+    k_done = 0
+    for k in range(1, K + 1):
+        if int(np.count_nonzero(status.cpu().numpy() == 0)) == 0:
+            break
+        k_done = k
+        U_old = U.clone()
+        F, _ = op.sweep(torch.cat([u0b, U_old[:, :-1]], dim=1).contiguous(), grid.deltat, grid.n_fine_per_coarse,
+                        active=status)
+        last = empty(M, 1, nx)
+        _lib.call("kle_axpby_f64", ptr(U_old[:, -1:].contiguous()), ptr(U_old[:, -1:].contiguous()), ptr(last),
+                  cfg.alpha, 0.0, M * nx, stream_ptr())
+        G, _ = op.sweep(torch.cat([last, U_old[:, :-1]], dim=1).contiguous(), grid.deltaT, 1, active=status)
+        _lib.call("kle_axpby_f64", ptr(F[:, :, 0].contiguous()), ptr(G[:, :, 0].contiguous()), ptr(b), 1.0, -1.0,
+                  M * N * nx, stream_ptr())
+        _lib.call("kle_newton_cgc_f64", op.kind, ptr(U_old), ptr(b), ptr(U), ptr(op.p0), ptr(tables.lam),
+                  ptr(tables.scaling), ptr(tables.inv_scaling), M, N, nx, grid.deltaT, op.dx, op.bc_lo, op.bc_hi,
+                  op.newton_tol, ptr(status), ptr(inner), stream_ptr())
+        _lib.call("kle_err_ref_f64", ptr(U), ptr(U_old), M, N, nx, k, K, cfg.tol, 1 - stop_ref, ptr(status),
+                  ptr(iters), None, ptr(inc_rec), ptr(inc_km[k - 1]), stream_ptr())
+        if ref is not None:
+            _lib.call("kle_err_ref_f64", ptr(U), ptr(ref), M, N, nx, k, K, cfg.tol, stop_ref, ptr(status),
+                      ptr(iters), None, ptr(err), ptr(me), stream_ptr())
+    st, it = status.cpu().numpy(), iters.cpu().numpy()
+    lastinc = inc_km[max(k_done - 1, 0)].cpu().numpy()
+    still = st == 0
+    st[still & ~np.isfinite(lastinc)] = 3
+    st[still & np.isfinite(lastinc)] = 2
+    it[still | (st == 4)] = np.where(it[still | (st == 4)] > 0, it[still | (st == 4)], k_done)
+    status.copy_(torch.as_tensor(st))
+    iters.copy_(torch.as_tensor(it))
+    return BatchResult(U, iters, status, inc_km.t().contiguous(), inner.to(torch.float64), err, me)

@@ -17,6 +17,7 @@ import numpy as np
 
 from . import _lib
 from .core import (
+    NonConvergenceError,
     CoarseTrajectory,
     IterationRecord,
     IterationTrace,
@@ -27,7 +28,7 @@ from .core import (
 )
 from .device import AlphaTables, DeviceOperator, empty, ptr, require_cuda, stream_ptr, to_dev, torch
 
-SAMPLE_ACTIVE, SAMPLE_CONVERGED, SAMPLE_MAXITERS, SAMPLE_NONFINITE = 0, 1, 2, 3
+SAMPLE_ACTIVE, SAMPLE_CONVERGED, SAMPLE_MAXITERS, SAMPLE_NONFINITE, SAMPLE_NEWTON = 0, 1, 2, 3, 4
 
 
 @dataclass(frozen=True)
@@ -229,6 +230,8 @@ class BatchResult:
         for i in np.nonzero(st != SAMPLE_CONVERGED)[0]:
             if st[i] == SAMPLE_MAXITERS:
                 out[int(i)] = MaxItersExceededError(f"sample {int(i)} did not reach tol")
+            elif st[i] == SAMPLE_NEWTON:
+                out[int(i)] = NonConvergenceError(f"sample {int(i)}: simplified Newton CGC stalled")
             elif st[i] == SAMPLE_NONFINITE:
                 out[int(i)] = ValueError(f"sample {int(i)}: trajectory contains non-finite entries")
             else:
@@ -258,6 +261,10 @@ def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, 
         raise ValueError("stop_on='reference' requires a reference trajectory")
     if isinstance(op, DeviceOperator2D):
         return pcgc_solve_device2d(op, U, grid, cfg, tables, reference=reference, stop_on=stop_on)
+    from .nonlinear import NewtonOperator, pcgc_solve_newton
+
+    if isinstance(op, NewtonOperator):
+        return pcgc_solve_newton(op, U, grid, cfg, reference=reference, stop_on=stop_on)
     M, N, nx = U.shape
     if N != grid.n_coarse or nx != op.nx or M != op.M:
         raise ValueError("initial guess length does not match the time grid")
@@ -313,8 +320,12 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     if init.n_coarse != grid.n_coarse:
         raise ValueError("initial guess length does not match the time grid")
     model.validate(xi)
+    from .nonlinear import is_newton_model
+
+    if is_newton_model(model):
+        return _pcgc_newton_trace(model, xi, grid, cfg, init, reference, stop_on, raise_on_max, solver_name)
     if not getattr(model, "is_linear", False):
-        raise NotImplementedError("the device PCGC covers linear models only")
+        raise NotImplementedError("the device PCGC covers linear and tridiagonal Newton models only")
     N = grid.n_coarse
     u0 = np.asarray(model.initial_condition(xi), dtype=float)
     op = DeviceOperator.from_model(model, [xi])
@@ -386,6 +397,41 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
             trace.converged = True
             break
     trace.trajectory = CoarseTrajectory(u0, host)
+    trace.trajectory.assert_finite()
+    if not trace.converged and raise_on_max:
+        raise MaxItersExceededError(
+            f"{solver_name} did not reach tol {cfg.tol:.1e} within {cfg.max_outer_iters} iterations", trace=trace
+        )
+    return trace
+
+
+def _pcgc_newton_trace(model, xi, grid, cfg, init, reference, stop_on, raise_on_max, solver_name):
+    """pcgc_solve for one sample of a nonlinear model: the batched device loop
+    with M = 1 (simplified-Newton CGC, pcgc.py:245-270), trace rebuilt from its
+    records."""
+    from .core import NonConvergenceError
+    from .nonlinear import NewtonOperator, pcgc_solve_newton
+
+    u0 = np.asarray(model.initial_condition(xi), dtype=float)
+    op = NewtonOperator.from_model(model, [xi], cfg)
+    U = to_dev(init.states)[None].clone()
+    ref = None if reference is None else to_dev(reference.states)[None]
+    res = pcgc_solve_newton(op, U, grid, cfg, ref, stop_on)
+    st = int(res.status[0].item())
+    if st == 4:
+        raise NonConvergenceError("simplified Newton stalled after 150 diagonalized solves",
+                                  last_iterate=res.states[0].cpu().numpy())
+    k = int(res.iters[0].item())
+    trace = IterationTrace(solver=solver_name, stop_on=stop_on)
+    trace.diagnostics["max_imag_residue"] = 0.0
+    errs = res.err_vs_ref[0].cpu().numpy() if res.err_vs_ref is not None else None
+    incs = res.increments[0].cpu().numpy()
+    for j in range(k + 1):
+        ev = None if errs is None else errs[j]
+        trace.records.append(IterationRecord(j, None if j == 0 else float(incs[j - 1]), ev,
+                                             None if ev is None else float(np.max(ev)), 0.0))
+    trace.trajectory = CoarseTrajectory(u0, res.states[0].cpu().numpy())
+    trace.converged = st == 1
     trace.trajectory.assert_finite()
     if not trace.converged and raise_on_max:
         raise MaxItersExceededError(

@@ -425,10 +425,33 @@ def make_nl():
             inc = [r.increment_inf for r in tr.records[1:]]
             incs[i, 1:len(inc) + 1] = inc
         out[f"{tag}_init"] = np.array(inits)
+        # PCGC with the simplified-Newton CGC (pcgc.py:245-270) from the same initial guesses
+        pf, pi_, pinc = [], [], np.full((ns, 61), np.nan)
+        for i, xi in enumerate(xis):
+            cs = rcore.CoarseTrajectory(model.initial_condition(xi), inits[i])
+            tr = rpcgc.pcgc_solve(model, xi, grid, cfg, cs)
+            pf.append(tr.trajectory.states)
+            pi_.append(tr.iterations)
+            inc = [r.increment_inf for r in tr.records[1:]]
+            pinc[i, 1:len(inc) + 1] = inc
+        out[f"{tag}_pcgc_final"] = np.array(pf)
+        out[f"{tag}_pcgc_iters"] = np.array(pi_, np.int32)
+        out[f"{tag}_pcgc_incs"] = pinc
+        # one cgc_correct call: inner iteration count and result
+        xi0 = xis[0]
+        cs = rcore.CoarseTrajectory(model.initial_condition(xi0), inits[0])
+        starts = np.vstack([cs.initial, cs.states[:-1]])
+        fe = np.array([rprop.propagate_fine(model, starts[n], grid.coarse_point(n), grid.coarse_point(n + 1), grid,
+                                            xi0, cfg) for n in range(N)])
+        cc, diag = rpcgc.cgc_correct(model, xi0, grid, cfg, cs, fe)
+        out[f"{tag}_cgc_F"] = fe
+        out[f"{tag}_cgc_out"] = cc.states
+        out[f"{tag}_cgc_inner"] = np.int32(diag["inner_iters"])
         out[f"{tag}_final"] = np.array(finals)
         out[f"{tag}_iters"] = np.array(iters, np.int32)
         out[f"{tag}_incs"] = incs
-        print(f"  {tag}: iters {iters} ({time.time() - t0:.1f}s)", flush=True)
+        print(f"  {tag}: parareal iters {iters}, pcgc iters {pi_}, cgc inner {diag['inner_iters']} "
+              f"({time.time() - t0:.1f}s)", flush=True)
     # the harness's Allen-Cahn coarse step (dT = 1) from u0: Newton fails at step 1
     ac = rmodels.AllenCahn1D(dx=1 / 128)
     xi0 = rcore.ParameterSample(out["ac_xi"][0], id=0)

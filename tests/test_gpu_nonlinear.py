@@ -90,3 +90,56 @@ def test_newton_parareal_dropin_and_failure_status(cuda, golden):
         propagate_coarse(ac, ac.initial_condition(xa), 0.0, 1.0, xa, SolverConfig(alpha=0.1, tol=1e-8))
     assert f"step {int(g['ac_fail_status'])}/1" in str(ei.value)
     assert ei.value.last_iterate.shape == (ac.nx,)
+
+
+@pytest.mark.parametrize("tag", ["bu", "ac"])
+def test_newton_pcgc_matches_reference(cuda, golden, tag):
+    """pcgc_solve with the simplified-Newton averaged-Jacobian CGC
+    (pintuq/pcgc.py:245-270) for the nonlinear models, batched."""
+    import torch
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.nonlinear import NewtonOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+
+    g = golden("nl")
+    model, grid, cfg = _setup(tag)
+    xis = [ParameterSample(v, id=i) for i, v in enumerate(g[f"{tag}_xi"])]
+    op = NewtonOperator.from_model(model, xis, cfg)
+    U = torch.as_tensor(g[f"{tag}_init"], device="cuda").clone()
+    res = pcgc_solve_device(op, U, grid, cfg)
+    iters = res.iters.cpu().numpy()
+    np.testing.assert_array_equal(iters, g[f"{tag}_pcgc_iters"])
+    assert np.all(res.status.cpu().numpy() == 1)
+    assert rel(res.states.cpu().numpy(), g[f"{tag}_pcgc_final"]) <= RT
+    inc = res.increments.cpu().numpy()
+    for i, k in enumerate(iters):
+        np.testing.assert_allclose(inc[i, :k], g[f"{tag}_pcgc_incs"][i, 1:k + 1], rtol=0, atol=1e-10)
+
+
+@pytest.mark.parametrize("tag", ["bu", "ac"])
+def test_newton_cgc_single_correction(cuda, golden, tag):
+    """One simplified-Newton correction (cgc_correct, pcgc.py:245-270) from
+    the reference's fine ends: result and inner iteration count."""
+    import torch
+    from paper_2510_26180_b200 import ParameterSample, _lib
+    from paper_2510_26180_b200.device import AlphaTables, empty, ptr, stream_ptr
+    from paper_2510_26180_b200.nonlinear import NewtonOperator
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    g = golden("nl")
+    model, grid, cfg = _setup(tag)
+    N, nx = grid.n_coarse, model.nx
+    xi0 = ParameterSample(g[f"{tag}_xi"][0], id=0)
+    op = NewtonOperator.from_model(model, [xi0], cfg)
+    U = torch.as_tensor(g[f"{tag}_init"][:1], device="cuda").contiguous()
+    prev = np.vstack([cfg.alpha * g[f"{tag}_init"][0][-1:], g[f"{tag}_init"][0][:-1]])
+    G, _ = op.sweep(torch.as_tensor(prev[None], device="cuda"), grid.deltaT, 1)
+    b = torch.as_tensor(g[f"{tag}_cgc_F"][None], device="cuda") - G[:, :, 0]
+    tables = AlphaTables(build_alpha_circulant(N, cfg.alpha))
+    out = empty(1, N, nx)
+    inner = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("kle_newton_cgc_f64", op.kind, ptr(U), ptr(b.contiguous()), ptr(out), ptr(op.p0), ptr(tables.lam),
+              ptr(tables.scaling), ptr(tables.inv_scaling), 1, N, nx, grid.deltaT, op.dx, op.bc_lo, op.bc_hi,
+              op.newton_tol, None, ptr(inner), stream_ptr())
+    assert rel(out[0].cpu().numpy(), g[f"{tag}_cgc_out"]) <= RT
+    assert abs(int(inner.item()) - int(g[f"{tag}_cgc_inner"])) <= 1  # the 1e-12 inner stop may flip by one step
