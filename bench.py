@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c3", "c5"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c3", "c5", "burgers", "allen-cahn"])
     p.add_argument("--samples", type=int, default=0, help="c3: evaluation samples (default 296 of the config's 4096)")
     p.add_argument("--train", type=int, default=1024, help="c3: surrogate training samples (config: 1024)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -704,9 +704,93 @@ def run_c3(args):
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------------------
+# nonlinear models: PCGC with the simplified-Newton CGC and the
+# classical parareal baseline, batched, at the reference harness settings
+# ---------------------------------------------------------------------------
+NL_CASES = {
+    # pintuq/experiments.py:33-38 (BENCHMARK_DEFAULTS); Allen-Cahn at T = 3 instead of 30: with dT = 1 the
+    # reference's own coarse Newton step from u0 fails (recorded in tests/golden/nl.npz)
+    "burgers": dict(T=2.0, N=25, J=40),
+    "allen-cahn": dict(T=3.0, N=30, J=48),
+}
+
+
+def _cpu_nl(task):
+    from oracle import nonlinear_port as nlp
+
+    m, u0, init, N, J, T = task
+    return nlp.pcgc_newton(m, u0, init, N, J, T, 0.1, 1e-8, 60)["iters"]
+
+
+def run_nonlinear(args):
+    """Batched PCGC (and classical parareal) for Burgers1D / AllenCahn1D on the
+    device from coarse-sweep initial guesses; CPU oracle (the reference's
+    pure-Python path, bit-identical) on a bounded sample beside it."""
+    import torch
+    from concurrent.futures import ProcessPoolExecutor
+
+    from paper_2510_26180_b200 import AllenCahn1D, Burgers1D, RngStream, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.nonlinear import NewtonOperator
+    from paper_2510_26180_b200.parareal import parareal_solve_device
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+
+    c = NL_CASES[args.config]
+    model = Burgers1D(dx=1 / 100) if args.config == "burgers" else AllenCahn1D(dx=1 / 128)
+    grid = make_time_grid(c["T"], c["N"], c["J"])
+    cfg = SolverConfig(alpha=0.1, tol=1e-8, max_outer_iters=60, seed=SEED)
+    M = args.samples or 4096
+    xis = model.sample_parameters(M, RngStream(SEED).split(3)[1])
+    op = NewtonOperator.from_model(model, xis, cfg)
+    u0 = op.u0[None, None].expand(M, 1, model.nx).contiguous()
+
+    def init():
+        return op.sweep(u0, grid.deltaT, 1, nseg=grid.n_coarse)[0][:, 0].contiguous()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        torch.cuda.synchronize()
+        return r, a.elapsed_time(b)
+
+    for _ in range(max(1, args.warmup)):
+        pcgc_solve_device(op, init(), grid, cfg)
+    res, ms_pcgc = timed(lambda: pcgc_solve_device(op, init(), grid, cfg))
+    res_p, ms_par = timed(lambda: parareal_solve_device(op, init(), grid, cfg))
+    it, itp = res.iters.cpu().numpy(), res_p.iters.cpu().numpy()
+    # CPU oracle: bounded sample over all cores
+    cores = os.cpu_count() or 1
+    U0 = init().cpu().numpy()
+    n_cpu = min(M, max(cores, 2 * cores if args.config == "burgers" else cores))
+    tasks = [((model.sweep_kind,) + model.sweep_params(xis[i].values), model.initial_condition(), U0[i],
+              grid.n_coarse, grid.n_fine_per_coarse, grid.t_final) for i in range(n_cpu)]
+    t0 = time.time()
+    with ProcessPoolExecutor(cores) as ex:
+        cpu_it = list(ex.map(_cpu_nl, tasks))
+    cpu_s = time.time() - t0
+    line = {"metric": f"PCGC solves/s, nonlinear model ({model.name})", "value": M / (ms_pcgc * 1e-3),
+            "unit": "PCGC solves/s", "n_gpus": 1, "higher_is_better": True, "dtype": "f64",
+            "config": {"workload": f"{model.name}: nx={model.nx}, T={grid.t_final}, N={grid.n_coarse}, "
+                                   f"J={grid.n_fine_per_coarse}, alpha=0.1, tol=1e-8, coarse-sweep init",
+                       "samples": M},
+            "pcgc": {"ms": ms_pcgc, "iters_mean": float(it.mean()), "all_converged": bool(np.all(
+                res.status.cpu().numpy() == 1)), "inner_iters_last_mean": float(res.imag.cpu().numpy().mean())},
+            "parareal": {"ms": ms_par, "solves_per_s": M / (ms_par * 1e-3), "iters_mean": float(itp.mean())},
+            "cpu_baseline": {"value": n_cpu / cpu_s, "unit": "PCGC solves/s", "cores": cores, "kind": "port",
+                             "sample": f"first {n_cpu} samples, oracle/nonlinear_port.pcgc_newton (the reference's "
+                                       f"pure-Python path, bit-identical), {cores} processes, {cpu_s:.1f} s wall",
+                             "iters_match": bool(np.array_equal(np.array(cpu_it), it[:n_cpu]))}}
+    print(json.dumps(line), flush=True)
+
+
 if __name__ == "__main__":
     a = parse()
-    if a.config == "c5":
+    if a.config in NL_CASES:
+        run_nonlinear(a)
+    elif a.config == "c5":
         run_c5(a)
     elif a.config == "c3" and a.impl == "b200":
         run_c3(a)

@@ -5,7 +5,7 @@
 // Per inner iteration (u_l = current iterate, b = F - G(prev) from
 // assemble_rhs_blocks, pcgc.py:175-197):
 //   shifted_i = u_l[i] - b[i];  F_l[i] = f(shifted_i);  J_i = f'(shifted_i)
-//   mean_jac = (J_0 + ... + J_{N-1}) / N                  (tridiagonal)
+//   mean_jac = (J_0 + ... + J_{N-1}) * (1/N)              (tridiagonal)
 //   rhs = dT (F_l - mean_jac u_l) + b
 //   u_next = three_step_solve(spec, mean_jac, dT, rhs)      (pcgc.py:148-172:
 //            scaled DFT along time, N shifted solves (lambda_n I - dT mean_jac)
@@ -105,9 +105,10 @@ __global__ void __launch_bounds__(256) newton_cgc_kernel(NewtonCgcArgs a) {
         }
         rh[(size_t)n * m + i] = f;  // F_l, completed to the rhs below
       }
-      jb[i] = i > 0 ? sl / N : 0.0;  // J[i][i-1]
-      jb[m + i] = sd / N;
-      jb[2 * m + i] = i < m - 1 ? su / N : 0.0;  // J[i][i+1]
+      const double invN = 1.0 / N;  // mean_jac / N is a sparse scalar product with 1/N in scipy
+      jb[i] = i > 0 ? sl * invN : 0.0;  // J[i][i-1]
+      jb[m + i] = sd * invN;
+      jb[2 * m + i] = i < m - 1 ? su * invN : 0.0;  // J[i][i+1]
     }
     __syncthreads();
     // rhs = dT (F_l - mean_jac u_l) + b, alpha-scaled for the DFT

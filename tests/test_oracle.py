@@ -302,3 +302,35 @@ def test_nonlinear_models_match_reference(golden):
         np.testing.assert_array_equal(model.rhs(u0, 0.0, xi0), g[f"{tag}_rhs0"])
         np.testing.assert_array_equal(model.jacobian(u0, 0.0, xi0).toarray(), g[f"{tag}_jac0"])
         assert model.nx == g[f"{tag}_ref"].shape[1]
+
+
+def test_nonlinear_port_bitwise(golden):
+    """The nonlinear restatement (Newton sweeps, simplified-Newton CGC,
+    parareal and PCGC loops) reproduces the reference bit for bit at the
+    harness settings (tests/golden/nl.npz, pure-Python backend)."""
+    from oracle import nonlinear_port as nlp
+    from paper_2510_26180_b200 import AllenCahn1D, Burgers1D
+
+    g = golden("nl")
+    for tag, model, T, N, J in (("bu", Burgers1D(dx=1 / 100), 2.0, 25, 40), ("ac", AllenCahn1D(dx=1 / 128), 3.0, 30, 48)):
+        xs = g[f"{tag}_xi"]
+        m0 = (model.sweep_kind,) + model.sweep_params(xs[0])
+        u0 = model.initial_condition()
+        dT = T / N
+        np.testing.assert_array_equal(nlp.sweep(m0, u0, dT / J, J)[0], g[f"{tag}_pf"])
+        np.testing.assert_array_equal(nlp.sweep(m0, u0, dT, 1)[0], g[f"{tag}_pc"])
+        lam, sc = ref_port.alpha_circulant(N, 0.1)
+        U = g[f"{tag}_init"][0]
+        prev = np.vstack([0.1 * U[-1:], U[:-1]])
+        G = np.array([nlp.sweep(m0, prev[n], nlp.coarse_dt(T, N, n), 1)[0] for n in range(N)])
+        out, inner = nlp.cgc_newton(m0, lam, sc, N, dT, U, g[f"{tag}_cgc_F"] - G, 1e-12)
+        np.testing.assert_array_equal(out, g[f"{tag}_cgc_out"])
+        assert inner == g[f"{tag}_cgc_inner"]
+        i = len(xs) - 1  # one full loop of each kind per model (the longest runs are the GPU tests' job)
+        mi = (model.sweep_kind,) + model.sweep_params(xs[i])
+        pc = nlp.pcgc_newton(mi, u0, g[f"{tag}_init"][i], N, J, T, 0.1, 1e-8, 60)
+        assert pc["iters"] == g[f"{tag}_pcgc_iters"][i]
+        np.testing.assert_array_equal(pc["states"], g[f"{tag}_pcgc_final"][i])
+        pa = nlp.parareal_newton(mi, u0, g[f"{tag}_init"][i], N, J, T, 1e-8, 60)
+        assert pa["iters"] == g[f"{tag}_iters"][i]
+        np.testing.assert_array_equal(pa["states"], g[f"{tag}_final"][i])
