@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
         }
     }
     if (a.Rout == nullptr) return;  // F ends only (classical parareal)
-    // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n), operands from shared memory
+    // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n), operands from shared memory;
+    // each rhs row replaces its (consumed) prev row in st, then the CTA stores st coalesced
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const double left = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
@@ -229,8 +230,8 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
       if (n >= N) continue;
       const double sc = a.scaling[n];
       const double* pv = (n == 0) ? p0 : st + nl[r] * LD;
+      double* rs = st + nl[r] * LD;
       const double pmul = (n == 0) ? a.alpha : 1.0;
-      double* out = a.Rout + sbase + (size_t)n * nx;
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
         const int row = k * MR + j;
@@ -240,8 +241,16 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
         const int pr = SM::pidx(row);
         const double Ax = fma(ee[pr], xm, fma(dd[pr], x[r][j], ee[SM::pidx(row + 1)] * xp));
         const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[pr];
-        out[row] = sc * rhs;
+        rs[pr] = sc * rhs;
       }
+    }
+    __syncthreads();
+    for (int ln = 0; ln < NC; ++ln) {
+      const int n = n0 + ln;
+      if (n >= N) break;
+      double* out = a.Rout + sbase + (size_t)n * nx;
+      const double* rs = st + ln * LD;
+      for (int row = tid; row < nx; row += NT) out[row] = rs[SM::pidx(row)];
     }
     return;
   }
