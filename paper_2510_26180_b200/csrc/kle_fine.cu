@@ -376,7 +376,7 @@ struct FineVariant {
   int MR, P, R, pipe, kind = 0;  // kind 1 (shared-memory factors): `pipe` is the min CTAs/SM bound
 };
 static const FineVariant kVariants[] = {
-    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {8, 16, 2, 0},  {16, 32, 3, 2}, {32, 32, 2, 0},  // defaults
+    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {16, 8, 2, 2},  {16, 32, 3, 2}, {32, 32, 2, 0},  // defaults
     {8, 16, 2, 1},  {4, 32, 4, 0},  {8, 16, 4, 1},  {8, 16, 4, 0},  {16, 16, 2, 0}, {8, 32, 4, 0},
     {32, 16, 2, 0}, {16, 32, 2, 0}, {16, 32, 2, 1}, {16, 32, 4, 1}, {16, 32, 4, 0}, {4, 32, 4, 1},
     {16, 32, 3, 4, 1}, {16, 32, 3, 3, 1}, {16, 32, 2, 4, 1}, {16, 32, 4, 3, 1},  // 18..21 shared-memory factors
@@ -384,6 +384,7 @@ static const FineVariant kVariants[] = {
     {32, 16, 2, 2, 1}, {32, 16, 1, 3, 1}, {16, 32, 3, 2, 1},                     // 25..27
     {32, 16, 4, 3, 1}, {32, 16, 3, 3, 1}, {32, 16, 2, 4, 1}, {32, 16, 4, 2, 1},  // 28..31
     {16, 32, 3, 0}, {8, 16, 2, 2}, {16, 32, 2, 2},                                // 32..34
+    {16, 8, 2, 0},  {16, 8, 3, 0},  {16, 8, 2, 2},  {16, 8, 3, 2},  {8, 8, 4, 0},   // 35..39 (nx <= 128)
 };
 static const int kNumDefaults = 6;
 
@@ -412,7 +413,12 @@ static const int kNumDefaults = 6;
   KLE_FINE_DISPATCH(16, 32, 3, 0, CALL)   \
   KLE_FINE_DISPATCH(16, 32, 4, 1, CALL)   \
   KLE_FINE_DISPATCH(16, 32, 4, 0, CALL)   \
-  KLE_FINE_DISPATCH(4, 32, 4, 1, CALL)
+  KLE_FINE_DISPATCH(4, 32, 4, 1, CALL)    \
+  KLE_FINE_DISPATCH(16, 8, 2, 0, CALL)    \
+  KLE_FINE_DISPATCH(16, 8, 3, 0, CALL)    \
+  KLE_FINE_DISPATCH(16, 8, 2, 2, CALL)    \
+  KLE_FINE_DISPATCH(16, 8, 3, 2, CALL)    \
+  KLE_FINE_DISPATCH(8, 8, 4, 0, CALL)
 
 FineLayoutRT fine_layout(int nx) {
   const char* env = getenv("KLE_FINE_VARIANT");

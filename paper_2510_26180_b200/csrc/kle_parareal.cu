@@ -103,6 +103,7 @@ int parareal_run(FineLayoutRT lay, const PararealArgs& a, cudaStream_t st) {
   if (lay.MR == 2 && lay.P == 16) return launch_parareal<2, 16>(a, st);
   if (lay.MR == 4 && lay.P == 16) return launch_parareal<4, 16>(a, st);
   if (lay.MR == 8 && lay.P == 16) return launch_parareal<8, 16>(a, st);
+  if (lay.MR == 16 && lay.P == 8) return launch_parareal<16, 8>(a, st);
   if (lay.MR == 16 && lay.P == 32) return launch_parareal<16, 32>(a, st);
   if (lay.MR == 32 && lay.P == 32) return launch_parareal<32, 32>(a, st);
   return set_error(KLE_ERR_UNSUPPORTED, "parareal: fine layout");
