@@ -38,7 +38,10 @@ namespace kle {
 
 namespace {
 
-constexpr int CL_CP = 4;       // complex columns per FFT tile (8 real columns)
+#ifndef KLE_CGCL_CP
+#define KLE_CGCL_CP 4
+#endif
+constexpr int CL_CP = KLE_CGCL_CP;  // complex columns per FFT tile (2 CP real columns)
 constexpr int CL_RC = 2 * CL_CP;
 
 __device__ __forceinline__ Cplx ca(Cplx a, Cplx b) { return {a.re + b.re, a.im + b.im}; }
