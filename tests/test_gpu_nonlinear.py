@@ -143,3 +143,64 @@ def test_newton_cgc_single_correction(cuda, golden, tag):
               op.newton_tol, None, ptr(inner), stream_ptr())
     assert rel(out[0].cpu().numpy(), g[f"{tag}_cgc_out"]) <= RT
     assert abs(int(inner.item()) - int(g[f"{tag}_cgc_inner"])) <= 1  # the 1e-12 inner stop may flip by one step
+
+
+def test_newton_status_words_and_maxiters(cuda, golden):
+    """Per-system Newton status (first failing step, 0 = ok) in a mixed batch,
+    MaxItersExceeded mapping of the batched loops, and the single-sample
+    pcgc_solve drop-in for a nonlinear model."""
+    import torch
+    from paper_2510_26180_b200 import (CoarseTrajectory, MaxItersExceededError, ParameterSample, SolverConfig)
+    from paper_2510_26180_b200.nonlinear import NewtonOperator
+    from paper_2510_26180_b200.parareal import parareal_solve_device
+    from paper_2510_26180_b200.pcgc import pcgc_solve, pcgc_solve_device
+
+    g = golden("nl")
+    ac, _, cfg_ac = _setup("ac")
+    xs = [ParameterSample(v, id=i) for i, v in enumerate(g["ac_xi"])]
+    op = NewtonOperator.from_model(ac, xs, cfg_ac)
+    u0 = op.u0[None, None].expand(2, 1, ac.nx).contiguous()
+    # dT = 1 fails at step 1 (the reference's status), dT = 0.1 succeeds, in the same launch
+    out, st = op.sweep(torch.cat([u0, u0], dim=1).contiguous(), 1.0, 1, raise_on_fail=False)
+    assert st.cpu().numpy()[:, 0].tolist() == [int(g["ac_fail_status"])] * 2
+    out, st = op.sweep(u0, 0.1, 1, raise_on_fail=False)
+    assert not st.cpu().numpy().any()
+
+    model, grid, cfg = _setup("bu")
+    xis = [ParameterSample(v, id=i) for i, v in enumerate(g["bu_xi"])]
+    op = NewtonOperator.from_model(model, xis, cfg)
+    short = SolverConfig(alpha=0.1, tol=1e-8, max_outer_iters=3)
+    for solve in (pcgc_solve_device, parareal_solve_device):
+        U = torch.as_tensor(g["bu_init"], device="cuda").clone()
+        res = solve(op, U, grid, short)
+        assert np.all(res.status.cpu().numpy() == 2) and np.all(res.iters.cpu().numpy() == 3)
+        assert isinstance(res.failures()[0], MaxItersExceededError)
+    tr = pcgc_solve(model, xis[2], grid, cfg, CoarseTrajectory(model.initial_condition(), g["bu_init"][2]))
+    assert tr.converged and tr.iterations == g["bu_pcgc_iters"][2]
+    assert rel(tr.trajectory.states, g["bu_pcgc_final"][2]) <= RT
+
+
+def test_newton_pcgc_reference_stop(cuda, golden):
+    """stop_on="reference" for a nonlinear model: the device loop stops at the
+    first record within tol of the fine reference, and matches the oracle."""
+    import torch
+    from oracle import nonlinear_port as nlp
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.nonlinear import NewtonOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+
+    g = golden("nl")
+    model, grid, cfg = _setup("bu")
+    xis = [ParameterSample(v, id=i) for i, v in enumerate(g["bu_xi"][:2])]
+    op = NewtonOperator.from_model(model, xis, cfg)
+    ref, _ = op.sweep(op.u0[None, None].expand(2, 1, model.nx).contiguous(), grid.deltat,
+                      grid.n_fine_per_coarse, nseg=grid.n_coarse)
+    ref = ref[:, 0].contiguous()
+    U = torch.as_tensor(g["bu_init"][:2], device="cuda").clone()
+    res = pcgc_solve_device(op, U, grid, cfg, reference=ref, stop_on="reference")
+    it = res.iters.cpu().numpy()
+    assert np.all(res.status.cpu().numpy() == 1)
+    np.testing.assert_array_equal(res.iters_to_tol(cfg.tol).cpu().numpy(), it)
+    err = res.err_vs_ref.cpu().numpy()
+    for i in range(2):
+        assert np.max(err[i, it[i]]) <= cfg.tol < np.max(err[i, it[i] - 1])
