@@ -30,6 +30,7 @@
 // p written once and read twice, y/q written twice, pivots written and read
 // once (96 B per (f, i), f <= N/2, i.e. ~48 B per (n, i)).
 #include <cmath>
+#include <cstdlib>
 
 #include "kle_common.cuh"
 #include "kle_internal.h"
@@ -414,12 +415,38 @@ static int run_large(const CgcArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(cgcl_inv_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  for (int m0 = 0; m0 < a.M; m0 += MB) {
-    const int mb = a.M - m0 < MB ? a.M - m0 : MB;
-    cgcl_fwd_kernel<LOGN><<<dim3(tiles, mb), K::NT, smem, st>>>(a, m0, tw, P);
+  // two sub-batch streams over the two halves of the scratch: one half's FFT
+  // kernels overlap the other half's per-frequency solves
+  static thread_local cudaStream_t ss[2] = {nullptr, nullptr};
+  static thread_local cudaEvent_t ev[3];
+  static const char* env = getenv("KLE_CGCL_STREAMS");
+  const bool two = !(env && env[0] == '1') && MB >= 2;
+  if (two && !ss[0]) {
+    for (int q = 0; q < 2; ++q) cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking);
+    for (int q = 0; q < 3; ++q) cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
+  }
+  const int HB = two ? MB / 2 : MB;  // samples per sub-batch
+  if (two) {
+    cudaEventRecord(ev[2], st);
+    for (int q = 0; q < 2; ++q) cudaStreamWaitEvent(ss[q], ev[2], 0);
+  }
+  int j = 0;
+  for (int m0 = 0; m0 < a.M; m0 += HB, ++j) {
+    const int mb = a.M - m0 < HB ? a.M - m0 : HB;
+    const int h = two ? (j & 1) : 0;
+    cudaStream_t sq = two ? ss[h] : st;
+    Cplx* Ph = P + (size_t)h * HB * a.nx * NF;
+    Cplx* IBh = IB + (size_t)h * HB * a.nx * NF;
+    cgcl_fwd_kernel<LOGN><<<dim3(tiles, mb), K::NT, smem, sq>>>(a, m0, tw, Ph);
     const long long nth = (long long)mb * NF;
-    cgcl_solve_kernel<<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(a, m0, mb, NF, P, IB);
-    cgcl_inv_kernel<LOGN><<<dim3(tiles, mb), K::NT, smem, st>>>(a, m0, tw, P, a.U ? bits : nullptr);
+    cgcl_solve_kernel<<<(unsigned)((nth + 127) / 128), 128, 0, sq>>>(a, m0, mb, NF, Ph, IBh);
+    cgcl_inv_kernel<LOGN><<<dim3(tiles, mb), K::NT, smem, sq>>>(a, m0, tw, Ph, a.U ? bits : nullptr);
+  }
+  if (two) {
+    for (int q = 0; q < 2; ++q) {
+      cudaEventRecord(ev[q], ss[q]);
+      cudaStreamWaitEvent(st, ev[q], 0);
+    }
   }
   if (a.U) cgcl_status_kernel<<<(a.M + 127) / 128, 128, 0, st>>>(a, bits);
   return check_launch("cgc_large");
