@@ -199,6 +199,12 @@ def pcgc_solve_newton(op: NewtonOperator, U, grid: TimeGrid, cfg: SolverConfig, 
         _lib.call("kle_newton_cgc_f64", op.kind, ptr(U_old), ptr(b), ptr(U), ptr(op.p0), ptr(tables.lam),
                   ptr(tables.scaling), ptr(tables.inv_scaling), M, N, nx, grid.deltaT, op.dx, op.bc_lo, op.bc_hi,
                   op.newton_tol, ptr(status), ptr(inner), stream_ptr())
+        st_h = status.cpu().numpy()
+        failed = (st_h == 4) & (iters.cpu().numpy() == 0)
+        if failed.any():  # the simplified Newton stalled in this iteration (pcgc.py:264-269)
+            it_h = iters.cpu().numpy()
+            it_h[failed] = k
+            iters.copy_(torch.as_tensor(it_h))
         _lib.call("kle_err_ref_f64", ptr(U), ptr(U_old), M, N, nx, k, K, cfg.tol, 1 - stop_ref, ptr(status),
                   ptr(iters), None, ptr(inc_rec), ptr(inc_km[k - 1]), stream_ptr())
         if ref is not None:
@@ -209,7 +215,7 @@ def pcgc_solve_newton(op: NewtonOperator, U, grid: TimeGrid, cfg: SolverConfig, 
     still = st == 0
     st[still & ~np.isfinite(lastinc)] = 3
     st[still & np.isfinite(lastinc)] = 2
-    it[still | (st == 4)] = np.where(it[still | (st == 4)] > 0, it[still | (st == 4)], k_done)
+    it[still] = k_done
     status.copy_(torch.as_tensor(st))
     iters.copy_(torch.as_tensor(it))
     return BatchResult(U, iters, status, inc_km.t().contiguous(), inner.to(torch.float64), err, me)
