@@ -192,14 +192,17 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   T* Lt_ = reinterpret_cast<T*>(Lt) + (size_t)phi * nx * n;
   T* Di_ = reinterpret_cast<T*>(Dinv) + (size_t)phi * nx;
+  // window position of each owned row slot, (rho - i) mod W, advanced incrementally per row
+  int jp[E / 2];
+#pragma unroll
+  for (int m = 0; m < E / 2; ++m) jp[m] = rho0 + Qr * m;
   for (int i = 0; i < nx; ++i) {
     T* cb = col + (i & 1) * W;
-    const int ri = i % W;
 #pragma unroll
     for (int m = 0; m < E / 2; ++m) {
       const int rho = rho0 + Qr * m;
       if (m >= E2 || rho >= W) continue;
-      const int jpos = rho - ri + (rho < ri ? W : 0);
+      const int jpos = jp[m];
 #pragma unroll
       for (int w = 0; w < 2; ++w)
         if ((w == 0 || two) && dl[w] == jpos) cb[jpos] = S::mk(wre[(2 * m + w) * NT + tid], wim[2 * m + w]);
@@ -223,7 +226,8 @@ __global__ void __launch_bounds__(NT, 1)
     for (int m = 0; m < E / 2; ++m) {
       const int rho = rho0 + Qr * m;
       if (m >= E2 || rho >= W) continue;
-      const int jpos = rho - ri + (rho < ri ? W : 0);
+      const int jpos = jp[m];
+      jp[m] = jpos == 0 ? W - 1 : jpos - 1;  // position at row i + 1
       if (jpos == 0) {  // row i leaves; row i + n + 1 enters its slot
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
