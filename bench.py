@@ -588,7 +588,33 @@ def run_c5(args):
             "fgr_tflops_alg": FLOPS_PER_DOF * chunk * N * J * nx / (fgr_ms * 1e-3) / 1e12,
         }
         del U, R, op, scratch
+    if not args.no_cpu_baseline:  # the reference path (SuperLU / LAPACK / pocketfft) on the host cores
+        from concurrent.futures import ProcessPoolExecutor
+
+        cores = os.cpu_count() or 1
+        model_np = model
+        tasks = []
+        for i in range(cores):
+            dia, off = model_np.tridiagonal(xi[i])
+            tasks.append((dia, off, model_np.initial_condition(), N, J, 1e-1))
+        t0 = time.time()
+        with ProcessPoolExecutor(cores) as ex:
+            cpu_it = list(ex.map(_cpu_c5, tasks))
+        wall = time.time() - t0
+        out["cpu_baseline"] = {"value": cores / wall, "unit": "KLE-CGC solves/s", "cores": cores, "kind": "port",
+                               "sample": f"first {cores} samples at alpha = 0.1, coarse-sweep init, one per process "
+                                         f"(oracle/ref_port: SuperLU, solve_banded, np.fft), {wall:.1f} s wall",
+                               "iters": cpu_it}
     print(json.dumps(out), flush=True)
+
+
+def _cpu_c5(task):
+    from oracle import ref_port
+
+    dia, off, u0, N, J, alpha = task
+    op = ref_port.SampleOperator(dia, off, np.ones(len(dia)))
+    init = ref_port.coarse_sweep(op, u0, N, 1.0 / N)
+    return ref_port.pcgc(op, u0, init, N, J, 1.0, alpha, 1e-8, 60)["iters"]
 
 
 def _cpu_solve2d(task):
