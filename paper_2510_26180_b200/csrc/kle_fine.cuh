@@ -37,10 +37,23 @@ struct LaneFactors {
 
   __device__ __forceinline__ void load(const double* __restrict__ blob, int k, int nx) {
     using L = FineLayout<MR, P>;
+    if constexpr (MR % 2 == 0 && (L::DOUBLES % 2) == 0) {  // 16-byte loads (blob rows are 16-byte aligned)
+      const double2* lp = reinterpret_cast<const double2*>(blob + L::L_OFF + k * MR);
+      const double2* ip = reinterpret_cast<const double2*>(blob + L::INV_OFF + k * MR);
 #pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      l[j] = blob[L::L_OFF + k * MR + j];
-      inv[j] = blob[L::INV_OFF + k * MR + j];
+      for (int j = 0; j < MR / 2; ++j) {
+        const double2 a = __ldg(lp + j), b = __ldg(ip + j);
+        l[2 * j] = a.x;
+        l[2 * j + 1] = a.y;
+        inv[2 * j] = b.x;
+        inv[2 * j + 1] = b.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        l[j] = blob[L::L_OFF + k * MR + j];
+        inv[j] = blob[L::INV_OFF + k * MR + j];
+      }
     }
 #pragma unroll
     for (int t = 0; t < L::LOGP; ++t) {
