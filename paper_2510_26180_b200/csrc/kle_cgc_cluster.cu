@@ -33,6 +33,7 @@
 // HBM traffic per outer iteration and (n, i): R 8 B + U 8 B read, U 8 B
 // written, pivots 16 (N/2+1)/N B read.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "kle_common.cuh"
 #include "kle_internal.h"
@@ -654,7 +655,8 @@ static bool cluster_shape(int N, int nx, int* MR, int* CL, int* LOGN) {
   while ((1 << logn) < N) ++logn;
   // 64-row blocks: measured faster than 32-row blocks in clusters of up to 16
   // (c2: 2.97 vs 4.34 ms per 4096 samples; fewer, fatter CTAs per sample)
-  const int mr = 8;
+  static const char* env = getenv("KLE_CGC_MR");  // 4: 32-row blocks (A/B)
+  const int mr = (env && atoi(env) == 4) ? 4 : 8;
   const int rb = CL_LANES * mr;
   const int cl = (nx + rb - 1) / rb;
   if (cl > 16) return false;
@@ -735,7 +737,7 @@ int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st) {
   if (!cluster_shape(a.N, a.nx, &MR, &CL, &LOGN)) return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: shape");
   if (a.M <= 0) return KLE_OK;
   if (a.imag) cudaMemsetAsync(a.imag, 0, sizeof(double) * a.M, st);  // real by construction
-  (void)MR;
+  if (MR == 4) return dispatch_logn<4>(LOGN, a, sfac, CL, st);
   return dispatch_logn<8>(LOGN, a, sfac, CL, st);
 }
 
