@@ -220,6 +220,20 @@ int kle_newton_cgc_f64(int kind, const double* U, const double* b, double* Uout,
                        const double* scaling, const double* inv_scaling, int M, int N, int nx, double dT, double dx,
                        double bc_lo, double bc_hi, double newton_tol, int32_t* status, int32_t* inner, void* stream);
 
+/* forward_dft / inverse_dft (pintuq/pcgc.py:79-87): out[k][l] = sum_n in[n][l]
+ * exp(sign 2 pi i n k / N) / sqrt(N) on [N][L] complex (interleaved re, im)
+ * arrays; sign = +1 is F (x) I (np.fft.ifft, ortho), -1 is F* (x) I (np.fft.fft). */
+int kle_block_dft_f64(const double* in, double* out, int N, int L, int sign, void* stream);
+
+/* One shifted solver of factor_shifted (pintuq/pcgc.py:112-135):
+ * (lam I - dT J) q = p for nrhs complex right-hand sides p [nrhs][nx], J =
+ * tridiag(sub [nx-1] = J[i+1][i], dia [nx], sup [nx-1] = J[i][i+1]), real;
+ * cwork [nrhs][nx] complex scratch; status [nrhs] = 1 on a zero pivot
+ * (SingularShiftError). */
+int kle_shifted_tridiag_solve_f64(const double* sub, const double* dia, const double* sup, double lam_re,
+                                  double lam_im, double dT, const double* p, double* q, double* cwork, int nx,
+                                  int nrhs, int32_t* status, void* stream);
+
 /* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
  * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);
  * norms[degree+1] = 1/sqrt(k!). */

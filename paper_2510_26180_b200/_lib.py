@@ -48,6 +48,8 @@ _SIGS = {
     "kle_newton_sweep_f64": ([_i, _p, _p, _p, _i, _i, _i, _i, _i, _d, _d, _d, _d, _d, _i, _p, _p, _p, _z, _p], _i),
     "kle_para_combine_f64": ([_p, _p, _p, _p, _p, _i, _i, _i, _i, _p], _i),
     "kle_newton_cgc_f64": ([_i, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _d, _d, _d, _d, _p, _p, _p], _i),
+    "kle_block_dft_f64": ([_p, _p, _i, _i, _i, _p], _i),
+    "kle_shifted_tridiag_solve_f64": ([_p, _p, _p, _d, _d, _d, _p, _p, _p, _i, _i, _p, _p], _i),
     "kle_2d_kl5pt_f64": ([_p, _i, _i, _p, _i, _d, _p, _p, _p, _p], _i),
     "kle_2d_factor_f64": ([_p, _p, _p, _i, _i, _p, _i, _d, _d, _p, _p, _p], _i),
     "kle_2d_fine_work_doubles": ([_i, _i, _i], _z),

@@ -521,6 +521,18 @@ int kle_newton_cgc_f64(int kind, const double* U, const double* b, double* Uout,
   return newton_cgc(a, KLE_STREAM(stream));
 }
 
+int kle_block_dft_f64(const double* in, double* out, int N, int L, int sign, void* stream) {
+  if (N < 1 || L < 0 || (sign != 1 && sign != -1)) return set_error(KLE_ERR_INVALID, "block_dft: bad arguments");
+  return block_dft(in, out, N, L, sign, KLE_STREAM(stream));
+}
+
+int kle_shifted_tridiag_solve_f64(const double* sub, const double* dia, const double* sup, double lam_re,
+                                  double lam_im, double dT, const double* p, double* q, double* cwork, int nx,
+                                  int nrhs, int32_t* status, void* stream) {
+  if (nx < 1 || nrhs < 0) return set_error(KLE_ERR_INVALID, "shifted_tridiag: bad arguments");
+  return shifted_tridiag(sub, dia, sup, lam_re, lam_im, dT, p, q, cwork, nx, nrhs, status, KLE_STREAM(stream));
+}
+
 int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
                       const double* norms, double* Psi, void* stream) {
   if (M < 0 || d < 1 || P < 1) return set_error(KLE_ERR_INVALID, "gpc_basis: bad dims");

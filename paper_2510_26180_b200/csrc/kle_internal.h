@@ -152,6 +152,10 @@ int err_ref(const double* U, const double* ref, int M, int N, int nx, int k, int
             int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist, double* max_err,
             cudaStream_t st);
 
+int block_dft(const double* in, double* out, int N, int L, int sign, cudaStream_t st);
+int shifted_tridiag(const double* sub, const double* dia, const double* sup, double lre, double lim, double dT,
+                    const double* p, double* q, double* cwork, int nx, int nrhs, int32_t* status, cudaStream_t st);
+
 int axpby(const double* x, const double* y, double* out, double a, double b, size_t n, cudaStream_t st);
 
 }  // namespace kle

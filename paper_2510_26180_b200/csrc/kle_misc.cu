@@ -195,4 +195,82 @@ int err_ref(const double* U, const double* ref, int M, int N, int nx, int k, int
   return check_launch("err_ref_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Block DFT along the first axis (forward_dft / inverse_dft, pintuq/pcgc.py:
+// 79-87): out[k][l] = sum_n in[n][l] exp(sign 2 pi i n k / N) / sqrt(N),
+// sign = +1 for F (x) I (np.fft.ifft, norm="ortho"), -1 for F* (x) I
+// (np.fft.fft). Direct O(N^2) per column (API utility, not the hot path:
+// the CGC kernels fuse their own FFTs).
+__global__ void block_dft_kernel(const Cplx* __restrict__ in, Cplx* __restrict__ out, int N, int L, int sign) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= (size_t)N * L) return;
+  const int k = (int)(t / L), l = (int)(t - (size_t)k * L);
+  double re = 0.0, im = 0.0;
+  for (int n = 0; n < N; ++n) {
+    double sn, cs;
+    sincospi((double)sign * 2.0 * (double)(((long long)n * k) % N) / (double)N, &sn, &cs);
+    const Cplx v = in[(size_t)n * L + l];
+    re += v.re * cs - v.im * sn;
+    im += v.re * sn + v.im * cs;
+  }
+  const double r = 1.0 / sqrt((double)N);
+  out[t] = {re * r, im * r};
+}
+
+int block_dft(const double* in, double* out, int N, int L, int sign, cudaStream_t st) {
+  const size_t tot = (size_t)N * L;
+  if (tot == 0) return KLE_OK;
+  block_dft_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(reinterpret_cast<const Cplx*>(in),
+                                                                  reinterpret_cast<Cplx*>(out), N, L, sign);
+  return check_launch("block_dft_kernel");
+}
+
+// (lam I - dT J) q = p for nrhs right-hand sides, J = tridiag(sub, dia, sup)
+// real (sub[i] = J[i+1][i], sup[i] = J[i][i+1]): the banded shifted solvers of
+// factor_shifted (pintuq/pcgc.py:112-135), pivot-free complex Thomas, one
+// thread per right-hand side. status[r] = 1 for a zero or non-finite pivot
+// (the reference's SingularShiftError).
+__global__ void shifted_tridiag_kernel(const double* __restrict__ sub, const double* __restrict__ dia,
+                                       const double* __restrict__ sup, double lre, double lim, double dT,
+                                       const Cplx* __restrict__ p, Cplx* __restrict__ q, Cplx* __restrict__ cwork,
+                                       int nx, int nrhs, int32_t* __restrict__ status) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrhs) return;
+  const Cplx* pr = p + (size_t)r * nx;
+  Cplx* qr = q + (size_t)r * nx;
+  Cplx* cp = cwork + (size_t)r * nx;
+  bool bad = false;
+  Cplx cprev = {0.0, 0.0}, dprev = {0.0, 0.0};
+  for (int i = 0; i < nx; ++i) {
+    const double a = i > 0 ? -dT * sub[i - 1] : 0.0;  // coupling to row i-1
+    const double c = i < nx - 1 ? -dT * sup[i] : 0.0;  // coupling to row i+1
+    const Cplx den = {lre - dT * dia[i] - a * cprev.re, lim - a * cprev.im};
+    const double m2 = den.re * den.re + den.im * den.im;
+    if (!(m2 > 0.0) || !isfinite(m2)) bad = true;
+    const Cplx iden = crcp(den);
+    const Cplx num = {pr[i].re - a * dprev.re, pr[i].im - a * dprev.im};
+    dprev = cmul(num, iden);
+    cprev = {c * iden.re, c * iden.im};
+    cp[i] = cprev;
+    qr[i] = dprev;
+  }
+  Cplx x = qr[nx - 1];
+  for (int i = nx - 2; i >= 0; --i) {
+    const Cplx cc = cp[i];
+    x = {qr[i].re - (cc.re * x.re - cc.im * x.im), qr[i].im - (cc.re * x.im + cc.im * x.re)};
+    qr[i] = x;
+  }
+  if (status) status[r] = bad ? 1 : 0;
+}
+
+int shifted_tridiag(const double* sub, const double* dia, const double* sup, double lre, double lim, double dT,
+                    const double* p, double* q, double* cwork, int nx, int nrhs, int32_t* status, cudaStream_t st) {
+  if (nx <= 0 || nrhs <= 0) return KLE_OK;
+  shifted_tridiag_kernel<<<(nrhs + 127) / 128, 128, 0, st>>>(sub, dia, sup, lre, lim, dT,
+                                                             reinterpret_cast<const Cplx*>(p),
+                                                             reinterpret_cast<Cplx*>(q),
+                                                             reinterpret_cast<Cplx*>(cwork), nx, nrhs, status);
+  return check_launch("shifted_tridiag_kernel");
+}
+
 }  // namespace kle

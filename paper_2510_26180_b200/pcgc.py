@@ -105,6 +105,67 @@ def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: f
     return u, imag
 
 
+def _block_dft(v, sign: int) -> np.ndarray:
+    require_cuda()
+    v = np.asarray(v)
+    shape = v.shape
+    c = np.ascontiguousarray(v.reshape(shape[0], -1), dtype=np.complex128)
+    src = torch.as_tensor(c.view(np.float64), device="cuda")
+    out = torch.empty_like(src)
+    _lib.call("kle_block_dft_f64", ptr(src), ptr(out), shape[0], c.shape[1], sign, stream_ptr())
+    return out.cpu().numpy().view(np.complex128).reshape(shape)
+
+
+def forward_dft(v) -> np.ndarray:
+    """F (x) I on a block vector of shape (N, ...), entries omega^(jk)/sqrt(N),
+    omega = exp(+2 pi i / N) (``pintuq/pcgc.py:79-82``); on the device."""
+    return _block_dft(v, +1)
+
+
+def inverse_dft(v) -> np.ndarray:
+    """F* (x) I, the inverse of :func:`forward_dft` (``pintuq/pcgc.py:85-87``)."""
+    return _block_dft(v, -1)
+
+
+def factor_shifted(spec: AlphaCirculantSpec, mean_jac, deltaT: float) -> list:
+    """Solver callables for the N shifted systems (lambda_n I - deltaT J)
+    (``pintuq/pcgc.py:90-145``) for a tridiagonal J (nx = 1 included); each
+    callable solves one right-hand side (or a stack, last axis nx) on the
+    device and raises ``SingularShiftError`` on a zero pivot. Wider
+    Jacobians: the batched 2D path (``three_step_solve``) factors them."""
+    import scipy.sparse as sp
+
+    from .core import SingularShiftError
+
+    J = sp.csr_matrix(np.atleast_2d(mean_jac) if not sp.issparse(mean_jac) else mean_jac)
+    nx = J.shape[0]
+    coo = J.tocoo()
+    if coo.nnz and int(np.max(np.abs(coo.row - coo.col))) > 1:
+        raise NotImplementedError("device factor_shifted covers tridiagonal Jacobians")
+    require_cuda()
+    sub = to_dev(np.asarray(J.diagonal(-1), dtype=float) if nx > 1 else np.zeros(1))
+    dia = to_dev(np.asarray(J.diagonal(0), dtype=float))
+    sup = to_dev(np.asarray(J.diagonal(1), dtype=float) if nx > 1 else np.zeros(1))
+
+    def make(lam):
+        def solve(p):
+            p = np.asarray(p)
+            c = np.ascontiguousarray(p.reshape(-1, nx), dtype=np.complex128)
+            src = torch.as_tensor(c.view(np.float64), device="cuda")
+            q = torch.empty_like(src)
+            work = torch.empty_like(src)
+            st = torch.zeros(c.shape[0], dtype=torch.int32, device="cuda")
+            _lib.call("kle_shifted_tridiag_solve_f64", ptr(sub), ptr(dia), ptr(sup), float(lam.real), float(lam.imag),
+                      float(deltaT), ptr(src), ptr(q), ptr(work), nx, c.shape[0], ptr(st), stream_ptr())
+            if bool(st.any().item()):
+                raise SingularShiftError(f"shifted system at lambda={lam} is singular")
+            return q.cpu().numpy().view(np.complex128).reshape(p.shape)
+
+        return solve
+
+    return [make(complex(lam)) for lam in spec.eigenvalues]
+
+
 def three_step_solve(spec: AlphaCirculantSpec, mean_jac, deltaT: float, r, solvers=None, executor=None):
     """Solve (C_alpha (x) I - dT I (x) J) u = r (``pintuq/pcgc.py:148-172``)
     for a symmetric tridiagonal J on the device. Returns (u, imag_residue)."""

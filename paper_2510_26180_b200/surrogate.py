@@ -96,6 +96,13 @@ def gpc_basis_matrix(points, degree: int, family: str = "hermite") -> np.ndarray
     return B
 
 
+def gpc_eval_basis(xi_mapped, degree: int, family: str = "legendre") -> np.ndarray:
+    """All total-order basis functions at one mapped point, length P
+    (``pintuq/surrogate.py:251-253``; host table, the batched evaluation of
+    the hot path is ``DeviceSurrogate.basis``)."""
+    return gpc_basis_matrix(np.atleast_2d(xi_mapped), degree, family)[0]
+
+
 def default_degree(n_train: int, dim: int, cap: int = 6) -> int:
     p = 0
     while p < cap and gpc_basis_count(p + 1, dim) <= max(1, n_train // 2):

@@ -125,3 +125,35 @@ def test_pcgc_converges_to_fine_reference(cuda):
     assert tr.converged
     assert np.max(np.abs(tr.trajectory.states - ref.states)) <= 10 * cfg.tol
     assert tr.diagnostics["max_imag_residue"] <= 1e-10 * max(np.abs(tr.trajectory.states).max(), 1.0)
+
+
+def test_block_dft_and_factor_shifted_api(cuda):
+    """forward_dft / inverse_dft against np.fft and the naive DFT matrix
+    (pintuq tests: test_pcgc.py:65-86 pins at 1e-13), and factor_shifted's
+    solvers against dense solves; zero pivots raise SingularShiftError."""
+    import scipy.sparse as sp
+    from paper_2510_26180_b200 import SingularShiftError
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, factor_shifted, forward_dft, inverse_dft
+
+    rng = np.random.default_rng(4)
+    for N in (1, 2, 5, 8, 33):
+        v = rng.normal(size=(N, 7)) + 1j * rng.normal(size=(N, 7))
+        np.testing.assert_allclose(forward_dft(v), np.fft.ifft(v, axis=0, norm="ortho"), rtol=0, atol=1e-13)
+        np.testing.assert_allclose(inverse_dft(v), np.fft.fft(v, axis=0, norm="ortho"), rtol=0, atol=1e-13)
+        np.testing.assert_allclose(inverse_dft(forward_dft(v)), v, rtol=0, atol=1e-13)
+        w = np.exp(2j * np.pi * np.outer(np.arange(N), np.arange(N)) / N) / np.sqrt(N)
+        np.testing.assert_allclose(forward_dft(v), w @ v, rtol=0, atol=1e-12)
+    nx, dT = 12, 0.05
+    J = sp.diags([rng.uniform(1, 2, nx - 1), -rng.uniform(4, 6, nx), rng.uniform(1, 2, nx - 1)], [-1, 0, 1])
+    spec = build_alpha_circulant(6, 0.1)
+    solvers = factor_shifted(spec, J, dT)
+    for lam, solve in zip(spec.eigenvalues, solvers):
+        p = rng.normal(size=nx) + 1j * rng.normal(size=nx)
+        q = solve(p)
+        dense = lam * np.eye(nx) - dT * J.toarray()
+        np.testing.assert_allclose(dense @ q, p, rtol=0, atol=1e-12)
+    scalar = factor_shifted(spec, np.array([[2.0]]), dT)
+    np.testing.assert_allclose(scalar[1](np.array([1.0 + 0j])), 1.0 / (spec.eigenvalues[1] - dT * 2.0), rtol=1e-14)
+    sing = factor_shifted(build_alpha_circulant(1, 0.5), np.array([[1.0]]), 0.5)  # lambda = 0.5 = dT J
+    with pytest.raises(SingularShiftError):
+        sing[0](np.array([1.0 + 0j]))
