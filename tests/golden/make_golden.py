@@ -466,8 +466,28 @@ def make_nl():
     print(f"nl done in {time.time() - t0:.1f}s")
 
 
+def make_models():
+    """The reference's own linear models at one parameter value (operator,
+    source, initial state) and a Diffusion1D PCGC run (coarse-sweep init)."""
+    out = {}
+    xi = rcore.ParameterSample(np.array([1.3]), id=0)
+    for tag, model in (("d1", rmodels.Diffusion1D()), ("ad", rmodels.AdvectionDiffusion2D())):
+        A, g = model.linear_system(xi)
+        out[f"{tag}_A"] = A.toarray()
+        out[f"{tag}_g"] = g(0.3)
+        out[f"{tag}_u0"] = model.initial_condition(xi)
+    d1 = rmodels.Diffusion1D()
+    grid = rcore.make_time_grid(1.0, 16, 32)
+    cfg = rcore.SolverConfig(alpha=0.1, tol=1e-10, max_outer_iters=60, seed=2718)
+    cs = rpar.coarse_sweep_init(d1, xi, grid, cfg).states
+    st, it, inc, _ = solve_one(d1, grid, cfg, xi, cs)
+    out.update(d1_init=cs, d1_final=st, d1_iters=np.int32(it), d1_incs=inc)
+    np.savez_compressed(OUT / "models.npz", **out)
+    print(f"models done; diffusion-1d pcgc iters {it}")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para", "nl"]
+    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para", "nl", "models"]
     for w in which:
         {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3, "ref": make_ref,
-         "para": make_para, "nl": make_nl}[w]()
+         "para": make_para, "nl": make_nl, "models": make_models}[w]()

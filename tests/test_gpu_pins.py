@@ -157,3 +157,23 @@ def test_block_dft_and_factor_shifted_api(cuda):
     sing = factor_shifted(build_alpha_circulant(1, 0.5), np.array([[1.0]]), 0.5)  # lambda = 0.5 = dT J
     with pytest.raises(SingularShiftError):
         sing[0](np.array([1.0 + 0j]))
+
+
+def test_reference_diffusion1d_model_on_device(cuda, golden):
+    """The reference's Diffusion1D plugin (symmetric tridiagonal, zero source)
+    runs through the generic plugin path: pcgc_solve matches the reference."""
+    from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.models import AdvectionDiffusion2D, Diffusion1D
+    from paper_2510_26180_b200.pcgc import pcgc_solve
+
+    g = golden("models")
+    model, xi = Diffusion1D(), ParameterSample(np.array([1.3]), id=0)
+    grid = make_time_grid(1.0, 16, 32)
+    cfg = SolverConfig(alpha=0.1, tol=1e-10, max_outer_iters=60)
+    tr = pcgc_solve(model, xi, grid, cfg, CoarseTrajectory(model.initial_condition(), g["d1_init"]))
+    assert tr.iterations == int(g["d1_iters"])
+    assert np.max(np.abs(tr.trajectory.states - g["d1_final"])) <= 1e-10 * np.max(np.abs(g["d1_final"]))
+    ad = AdvectionDiffusion2D()
+    with pytest.raises(NotImplementedError):
+        pcgc_solve(ad, ParameterSample(np.array([3.0]), id=0), make_time_grid(1.0, 8, 4), cfg,
+                   CoarseTrajectory(ad.initial_condition(), np.zeros((8, ad.nx))))

@@ -334,3 +334,18 @@ def test_nonlinear_port_bitwise(golden):
         pa = nlp.parareal_newton(mi, u0, g[f"{tag}_init"][i], N, J, T, 1e-8, 60)
         assert pa["iters"] == g[f"{tag}_iters"][i]
         np.testing.assert_array_equal(pa["states"], g[f"{tag}_final"][i])
+
+
+def test_reference_linear_models_match(golden):
+    """Diffusion1D / AdvectionDiffusion2D host definitions equal the
+    reference's (pintuq/models.py:128-266) bit for bit."""
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.models import AdvectionDiffusion2D, Diffusion1D
+
+    g = golden("models")
+    xi = ParameterSample(np.array([1.3]), id=0)
+    for tag, model in (("d1", Diffusion1D()), ("ad", AdvectionDiffusion2D())):
+        A, src = model.linear_system(xi)
+        np.testing.assert_array_equal(A.toarray(), g[f"{tag}_A"])
+        np.testing.assert_array_equal(src(0.3), g[f"{tag}_g"])
+        np.testing.assert_array_equal(model.initial_condition(xi), g[f"{tag}_u0"])
