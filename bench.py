@@ -286,7 +286,12 @@ def run_b200(args):
                "d2h_bytes_per_step": int(host_mean.numel() * 16 + M * 8),
                "ms_per_step": float(e2e_ms.item())}
 
-    launches_per_step = 1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 2 * kmax + 4 + 2
+    # per step: kl_tridiag, fine_factor, gpc basis + 1-2 GEMMs, shift_factor, then per outer iteration and
+    # sample pipeline (two when the batch is large, kle_capi.cu) one fgr and one CGC launch (an upper bound:
+    # a pipeline stops as soon as its own samples have converged), and 2 x (2 col-sum + 1 scale) for the moments
+    pipes = 2 if (M >= 8192 and sfac is not None and os.environ.get("KLE_PCGC_PIPES", "2") != "1") else 1
+    launches_per_step = (1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 1
+                         + 2 * pipes * kmax + 6)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_host)
