@@ -305,6 +305,25 @@ int kle_2d_sweep_f64(const double* start, const double* dia, const double* ex, c
                      const double* Lt, const double* Dinv, int M, int Q, int n, int J,
                      int nseg, double h, double g0, double* work, size_t work_doubles, double* out, void* stream);
 
+/* The real factor (Lt, Dinv from kle_2d_factor_f64) restaged for the TMA
+ * sweeps: per sample, direction (forward, backward) and block of 8 rows, one
+ * contiguous chunk of (n + 9) * 8 doubles holding the block's band
+ * coefficients in the order the sweep reads them and D^{-1} of its rows.
+ * Built once per solve; kle_2d_fgr_staged_f64 / kle_2d_sweep_staged_f64 stream
+ * one chunk per block with cp.async.bulk (pintuq/propagators.py:25-39: the
+ * factor is computed once and reused by every BE step, as SuperLU's is). */
+size_t kle_2d_fine_stage_doubles(int M, int n);
+int kle_2d_fine_stage_f64(const double* Lt, const double* Dinv, int M, int n, double* stage, void* stream);
+
+/* kle_2d_fgr_f64 / kle_2d_sweep_f64 on the staged factor (same outputs, same
+ * workspace size; one CTA per sample and 32 right-hand sides). */
+int kle_2d_fgr_staged_f64(const double* U, const double* u0, const double* F_given, const double* dia,
+                          const double* ex, const double* ey, const double* stage, const double* scaling,
+                          const int32_t* active, int M, int N, int n, int J, double dt, double dT, double g0,
+                          double alpha, double* work, size_t work_doubles, double* Rout, void* stream);
+int kle_2d_sweep_staged_f64(const double* start, const double* stage, int M, int Q, int n, int J, int nseg,
+                            double h, double g0, double* work, size_t work_doubles, double* out, void* stream);
+
 /* Scratch (doubles) of kle_2d_cgc_f64. */
 size_t kle_2d_cgc_work_doubles(int M, int N, int n);
 

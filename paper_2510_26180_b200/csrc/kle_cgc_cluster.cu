@@ -76,6 +76,10 @@ __device__ __forceinline__ Cplx shfl_down_c(Cplx v, int d) {
 __device__ __forceinline__ Cplx shfl_xor_c(Cplx v, int d) {
   return {__shfl_xor_sync(KLE_FULL_MASK, v.re, d), __shfl_xor_sync(KLE_FULL_MASK, v.im, d)};
 }
+#ifndef KLE_CGC_UPRE
+#define KLE_CGC_UPRE 1  // prefetch the old U columns into the dead pivot space during the inverse FFT
+#endif
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
@@ -555,6 +559,16 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     }
   }
   __syncthreads();
+  // the pivots are dead now: stream the column's old values into their space
+  // while the inverse FFT runs (each thread loads exactly what it reads later)
+  constexpr bool UPRE = K::SP && NSTEP > 0 && KLE_CGC_UPRE;
+  double* uold_p = reinterpret_cast<double*>(piv);  // [N][RB]
+  if constexpr (UPRE) {
+    if (a.U && tid < NSTEP * RB && row0 + tid % RB < nx) {
+      const int col = tid % RB;
+      for (int n = tid / RB; n < N; n += NSTEP) cp_async8(uold_p + n * RB + col, a.U + sb + (size_t)n * nx + row0 + col);
+    }
+  }
   fft4step<LOGN, HC, +1, MR>(tile, tw);
   CGC_T(7);
   // ---- update ----------------------------------------------------------------
@@ -577,7 +591,10 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     if (tid < NSTEP * RB) {
       const int col = tid % RB, row = row0 + col;
       if (row < nx) {
-        if constexpr (K::SP) {
+        if constexpr (UPRE) {
+          cp_async_wait_all();
+          for (int n = tid / RB; n < N; n += NSTEP) upd(n, col, row, track ? uold_p[n * RB + col] : 0.0);
+        } else if constexpr (K::SP) {
           // the column's old values, all loads issued before the stores (out may alias U)
           constexpr int NR = (N + NSTEP - 1) / NSTEP;
           constexpr int UB = NR < 8 ? NR : 8;  // loads in flight per batch

@@ -15,6 +15,8 @@ take 16 (N/2+1) n^3 bytes per sample).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -25,6 +27,11 @@ try:
     import torch
 except ImportError:  # pragma: no cover
     torch = None
+
+
+# the TMA-staged fine sweeps (kle_2d_tma.cu); KLE_2D_TMA=0 selects the
+# per-warp sweeps of kle_2d.cu (A/B measurements)
+_USE_TMA = os.environ.get("KLE_2D_TMA", "1") != "0"
 
 
 def stencil_of(model, xi):
@@ -77,6 +84,7 @@ class DeviceOperator2D:
         self.u0 = u0
         self.layout = (0, 0, 0)
         self._fine = {}
+        self._stage = {}
 
     @classmethod
     def from_model(cls, model, xis):
@@ -123,6 +131,23 @@ class DeviceOperator2D:
             self._fine[key] = f
         return f
 
+    def fine_stage(self, h: float):
+        """The factor of I + h A restaged for the TMA sweeps
+        (``kle_2d_fine_stage_f64``: per row block, the skewed coefficient
+        chunks of both substitution directions and D^{-1}), cached per h. The
+        column-form factor is dropped unless ``fine_factor`` cached it."""
+        key = float(h)
+        st = self._stage.get(key)
+        if st is None:
+            cached = key in self._fine
+            Lt, Dinv = self.fine_factor(key)
+            st = empty(int(_lib.query("kle_2d_fine_stage_doubles", self.M, self.n)))
+            _lib.call("kle_2d_fine_stage_f64", ptr(Lt), ptr(Dinv), self.M, self.n, ptr(st), stream_ptr())
+            if not cached:
+                del self._fine[key]
+            self._stage[key] = st
+        return st
+
     def shifted_factors(self, tables: AlphaTables, N: int, deltaT: float):
         """Complex (Lt, Dinv) of lambda_f I + dT A, f = 0..N/2 (B_{N-f} = conj B_f)."""
         NF = N // 2 + 1
@@ -136,10 +161,15 @@ class DeviceOperator2D:
     def sweep(self, start, h: float, J: int, nseg: int = 1):
         """start: (M, Q, nx) device tensor -> (M, Q, nseg, nx)."""
         M, Q, nx = start.shape
-        Lt, Dinv = self.fine_factor(h)
         out = empty(M, Q, nseg, nx)
         nw = int(_lib.query("kle_2d_fine_work_doubles", M, Q, self.n))
         work = empty(max(nw, 1))
+        if _USE_TMA:
+            st = self.fine_stage(h)
+            _lib.call("kle_2d_sweep_staged_f64", ptr(start.contiguous()), ptr(st), M, Q, self.n, J, nseg, h, self.g0,
+                      ptr(work), nw, ptr(out), stream_ptr())
+            return out
+        Lt, Dinv = self.fine_factor(h)
         _lib.call("kle_2d_sweep_f64", ptr(start.contiguous()), ptr(self.dia), ptr(self.ex), ptr(self.ey), ptr(Lt),
                   ptr(Dinv), M, Q, self.n, J, nseg, h, self.g0, ptr(work), nw, ptr(out), stream_ptr())
         return out
@@ -147,9 +177,15 @@ class DeviceOperator2D:
     def fgr(self, U, tables: AlphaTables, grid, alpha: float, R, status=None, F_given=None):
         M, N, nx = U.shape
         dT, dt = grid.deltaT, grid.deltat
-        Lt, Dinv = self.fine_factor(dt)
         nw = int(_lib.query("kle_2d_fine_work_doubles", M, N, self.n))
         work = empty(max(nw, 1))
+        if _USE_TMA:
+            st = self.fine_stage(dt)
+            _lib.call("kle_2d_fgr_staged_f64", ptr(U), ptr(self.u0), ptr(F_given), ptr(self.dia), ptr(self.ex),
+                      ptr(self.ey), ptr(st), ptr(tables.scaling), ptr(status), M, N, self.n,
+                      grid.n_fine_per_coarse, dt, dT, self.g0, alpha, ptr(work), nw, ptr(R), stream_ptr())
+            return
+        Lt, Dinv = self.fine_factor(dt)
         _lib.call("kle_2d_fgr_f64", ptr(U), ptr(self.u0), ptr(F_given), ptr(self.dia), ptr(self.ex), ptr(self.ey),
                   ptr(Lt), ptr(Dinv), ptr(tables.scaling), ptr(status), M, N, self.n, grid.n_fine_per_coarse,
                   dt, dT, self.g0, alpha, ptr(work), nw, ptr(R), stream_ptr())
@@ -171,9 +207,14 @@ def three_step_device2d(op: DeviceOperator2D, tables: AlphaTables, N: int, delta
 
 def _batch_size(op: DeviceOperator2D, N: int) -> int:
     NF = N // 2 + 1
-    per = 8 * (2 * NF * op.nx * (op.n + 1) + 2 * op.nx * (op.n + 1) + 6 * N * op.nx + 2 * NF * op.nx)
+    nblk = (op.nx + 7) // 8
+    per = 8 * (2 * NF * op.nx * (op.n + 1) + 2 * op.nx * (op.n + 1) + 6 * N * op.nx + 2 * NF * op.nx
+               + 2 * nblk * (op.n + 9) * 8)
+    # the per-batch factors are single allocations of tens of GB: hand the
+    # caching allocator's idle (possibly fragmented) blocks back first, so the
+    # free figure is what one allocation can actually get
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
-    free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()  # the caching allocator's idle blocks
     return max(1, min(op.M, int(0.85 * free) // per))
 
 

@@ -44,6 +44,8 @@ fac = None if SKIP_C else timed("factor complex (17 shifts)", lambda: op.shifted
 U = coarse_sweep_init_batched(op, grid).contiguous()
 R = empty(M, N, n * n)
 status = torch.zeros(M, dtype=torch.int32, device="cuda")
+if hasattr(op, "fine_stage"):
+    timed("restage (TMA chunks)", lambda: op.fine_stage(grid.deltat))
 timed("fgr2d (J steps, N rhs)", lambda: op.fgr(U, tables, grid, 1e-3, R, status=status))
 if SKIP_C:
     sys.exit(0)
