@@ -58,13 +58,20 @@ class KleCgcSolver:
             reference = fine_reference_batched(op, self.grid)
         U = self.surrogate.predict(xi_d)
         U0 = U.clone() if keep_initial else None
-        if self._ws is None:
-            self._ws = torch.empty(0, dtype=torch.uint8, device="cuda")
-        from . import _lib
+        from .twod import DeviceOperator2D
 
-        need = int(_lib.query("kle_pcgc_workspace_bytes", op.M, self.grid.n_coarse, self.model.nx))
-        if self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        if isinstance(op, DeviceOperator2D):
+            # the 2D loop sizes its own per-batch buffers from the free memory:
+            # a 1D workspace here would only shrink its batches
+            self._ws = None
+        else:
+            from . import _lib
+
+            if self._ws is None:
+                self._ws = torch.empty(0, dtype=torch.uint8, device="cuda")
+            need = int(_lib.query("kle_pcgc_workspace_bytes", op.M, self.grid.n_coarse, self.model.nx))
+            if self._ws.numel() < need:
+                self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
         res = pcgc_solve_device(op, U, self.grid, self.cfg, self.tables, self._ws, reference=reference,
                                 stop_on=stop_on)
         return KleCgcResult(res, U0)
