@@ -637,10 +637,10 @@ def run_c3(args):
     J = 16, d = 10, Hermite p = 2 (66 terms) fitted on --train seeded samples,
     alpha = 1e-3, tol = 1e-8. Timed step = U0 (gPC GEMM) + banded factors of
     I + dt A and of the 17 shifted matrices + PCGC to tol + moments, on
-    --samples evaluation samples (the config's M = 4096 at ~0.1 s/sample is a
-    multi-minute step; the per-sample throughput does not depend on M beyond
-    filling the GPU). The CPU baseline is the oracle (SuperLU paths) on a
-    bounded sample over all host cores."""
+    --samples evaluation samples (default: the config's M = 4,096, a ~80 s
+    step; the samples go through in batches sized to the free HBM, ~193).
+    The CPU baseline is the oracle (SuperLU paths) on a bounded sample over
+    all host cores."""
     import torch
 
     from paper_2510_26180_b200 import LogNormalKL2D, ParameterSample, RngStream, SolverConfig, make_time_grid
@@ -648,7 +648,7 @@ def run_c3(args):
     from paper_2510_26180_b200.surrogate import build_surrogate
 
     n, N, J, d = 127, 32, 16, 10
-    M = args.samples or 296
+    M = args.samples or 4096
     model = LogNormalKL2D(n=n, d=d, sigma=0.5, ell=0.25)
     grid = make_time_grid(1.0, N, J)
     cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=SEED)
