@@ -112,3 +112,59 @@ def test_c3_full_shape_one_sample(cuda, golden):
     res = pcgc_solve_device(op, U, grid, cfg)
     np.testing.assert_array_equal(res.iters.cpu().numpy(), g["iters"])
     assert rel(res.states.cpu().numpy(), g["final"]) <= RTOL
+
+
+def _dense_ops(op):
+    """Dense I-free operator A (M, nx, nx) of a DeviceOperator2D batch (fp64,
+    for small n only)."""
+    import torch
+
+    n = op.n
+    A = torch.diag_embed(op.dia)
+    A = A + torch.diag_embed(op.ex[:, :-1], 1) + torch.diag_embed(op.ex[:, :-1], -1)
+    A = A + torch.diag_embed(op.ey[:, :-n], n) + torch.diag_embed(op.ey[:, :-n], -n)
+    return A
+
+
+@pytest.mark.parametrize("M,N", [(20, 32), (150, 32), (300, 32), (300, 40), (7, 5)])
+def test_tma_sweeps_match_dense_solves(cuda, M, N):
+    """kle_2d_fgr_staged_f64 / kle_2d_sweep_staged_f64 (the TMA + DMMA sweeps,
+    8, 16 and 32 right-hand sides per CTA as the batch size selects them, and
+    ragged subinterval counts) against dense fp64 solves of the same BE steps
+    and the same CGC right-hand side (pintuq/propagators.py:37-39,121-145,
+    pcgc.py:175-197,233-237)."""
+    import torch
+
+    from paper_2510_26180_b200 import LogNormalKL2D, make_time_grid
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, empty
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    n, J, alpha = 15, 3, 1e-3
+    model = LogNormalKL2D(n=n, d=10, sigma=0.5, ell=0.25)
+    grid = make_time_grid(1.0, N, J)
+    xi = np.random.default_rng(M + N).normal(size=(M, 10))
+    op = DeviceOperator.from_model(model, xi)
+    nx = n * n
+    U = torch.as_tensor(np.random.default_rng(1).uniform(0.0, 1.0, size=(M, N, nx)), device="cuda")
+    tables = AlphaTables(build_alpha_circulant(N, alpha))
+    R = empty(M, N, nx)
+    op.fgr(U, tables, grid, alpha, R)
+    A = _dense_ops(op)
+    eye = torch.eye(nx, dtype=torch.float64, device="cuda")
+    T = eye + grid.deltat * A
+    starts = torch.cat([op.u0.view(1, 1, nx).expand(M, 1, nx), U[:, :-1]], dim=1)
+    x = starts.transpose(1, 2)  # (M, nx, N)
+    for _ in range(J):
+        x = torch.linalg.solve(T, x + grid.deltat * op.g0)
+    F = x.transpose(1, 2)
+    prev = torch.cat([alpha * U[:, -1:], U[:, :-1]], dim=1)
+    AF = torch.einsum("sij,snj->sni", A, F)
+    ref = tables.scaling.view(1, N, 1) * (F + grid.deltaT * AF - prev)
+    assert rel(R.cpu().numpy(), ref.cpu().numpy()) <= 1e-12
+    # the sweep entry (propagate_fine / fine_reference): two segments of J steps
+    out = op.sweep(U.contiguous(), grid.deltat, J, nseg=2)
+    x = U.transpose(1, 2)
+    for seg in range(2):
+        for _ in range(J):
+            x = torch.linalg.solve(T, x + grid.deltat * op.g0)
+        assert rel(out[:, :, seg].cpu().numpy(), x.transpose(1, 2).cpu().numpy()) <= 1e-12
