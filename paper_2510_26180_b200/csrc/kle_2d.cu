@@ -35,6 +35,7 @@
 //                      (Hermitian completion), increment vs U, write U
 //   status2d_kernel    per sample: stop test, status words, active count
 #include <cmath>
+#include <cstdlib>
 
 #include "kle_common.cuh"
 #include "kle_internal.h"
@@ -254,6 +255,182 @@ __global__ void __launch_bounds__(NT, 1)
       Lt_[(size_t)i * n + tid] = l;
     }
     if (tid == 0) Di_[i] = dinv;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Panel (rank-PF_B) banded L D L^T of B = lam I + c A (complex shifts), one
+// 512-thread CTA per matrix. The active window (rows i0 .. i0+n+PF_B-1, all
+// columns >= i0 of the band) is kept complex in shared memory as diagonal
+// rings: diagonal d (entries (r, r-d)) is a FIFO of NB - d entries, NB = n +
+// PF_B, entry of column cc at roff(d) + cc mod (NB - d); eliminated columns
+// free exactly the slots the rows entering next need. Per panel:
+//   1. the first 160 threads (one window row each) factor the panel's PF_B
+//      columns with one named barrier per column (rows' entries in registers,
+//      the column's pivot rows published through shared memory), writing
+//      PA[k][x] = W(x,k)/d_k and PB[k][x] = W(x,k); the other threads load the
+//      PF_B operator rows that enter for the next panel;
+//   2. all threads apply the rank-PF_B update W(r,c) -= sum_k PA[k][r] PB[k][c]
+//      to the trailing triangle (rows r and n-1-r folded into one list of n+1
+//      entries per thread group, 16 entries per thread, columns strided over
+//      the group's 8 threads so PB reads are conflict-free).
+// Each window entry is read and written once per PF_B rows instead of once
+// per row (band_factor_kernel: ~4,400 shared-memory wavefronts per row).
+// ---------------------------------------------------------------------------
+constexpr int PF_B = 8;
+constexpr int PF_NT = 512;
+constexpr int PF_PT = 160;  // panel threads (>= n + PF_B, a multiple of 32)
+constexpr int PF_M = 16;    // trailing entries per thread (8 threads per folded row pair)
+
+__host__ __device__ inline int pf_roff(int d, int NB) { return d * NB - d * (d - 1) / 2; }
+__host__ inline size_t pf_smem_bytes(int n) {
+  const int NB = n + PF_B;
+  return sizeof(Cplx) * ((size_t)pf_roff(n + 1, NB) + 2 * (size_t)PF_B * NB + 2 * PF_B);
+}
+
+__global__ void __launch_bounds__(PF_NT, 1)
+    band_factor_panel_kernel(const double* __restrict__ dia, const double* __restrict__ ex,
+                             const double* __restrict__ ey, int n, const double* __restrict__ lam, int NF, double c,
+                             double* __restrict__ Lt, double* __restrict__ Dinv) {
+  using S = Sc<true>;
+  using T = Cplx;
+  constexpr int B = PF_B;
+  const int nx = n * n, NB = n + B;
+  const int phi = blockIdx.x, s = phi / NF, f = phi - s * NF;
+  const double* d_ = dia + (size_t)s * nx;
+  const double* ex_ = ex + (size_t)s * nx;
+  const double* ey_ = ey + (size_t)s * nx;
+  const T shift = S::mk(lam[2 * f], lam[2 * f + 1]);
+  extern __shared__ __align__(16) double smem[];
+  T* ring = reinterpret_cast<T*>(smem);
+  T* PA = ring + pf_roff(n + 1, NB);  // [B][NB]
+  T* PB = PA + B * NB;                // [B][NB]
+  T* pub = PB + B * NB;               // [2][B]
+  const int tid = threadIdx.x;
+  auto opB = [&](int r, int dd) -> T {  // B(r, r - dd): the operator (identity beyond nx)
+    if (r >= nx) return dd == 0 ? S::mk(1.0, 0.0) : S::zero();
+    if (r - dd < 0) return S::zero();
+    if (dd == 0) return S::add(shift, S::mk(c * d_[r], 0.0));
+    double v = 0.0;
+    if (dd == 1) v += c * ex_[r - 1];
+    if (dd == n) v += c * ey_[r - n];
+    return S::mk(v, 0.0);
+  };
+  // initial window: rows 0 .. NB-1, column cc of ring d at index cc
+  for (int dd = 0; dd <= n; ++dd)
+    for (int idx = tid; idx < NB - dd; idx += PF_NT) ring[pf_roff(dd, NB) + idx] = opB(idx + dd, dd);
+  // panel-thread state: row x, entries k with 0 <= x - k <= n; ring index of column i0 + k
+  const int x = tid;
+  int psl[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    const int dd = x - k;
+    psl[k] = (dd >= 0 && dd <= n) ? k % (NB - dd) : 0;
+  }
+  // trailing-thread state: folded pair p (rows p and n-1-p), lane g of 8; entry m: list index j = g + 8m
+  const int p = tid >> 3, g = tid & 7;
+  const int R1 = p, R2 = n - 1 - p;
+  const bool pair_ok = R1 <= R2;
+  int tix[PF_M];
+#pragma unroll
+  for (int m = 0; m < PF_M; ++m) {
+    const int j = g + 8 * m;
+    int R = -1, C = 0;
+    if (pair_ok && j <= n) {
+      if (j <= R1) { R = R1; C = j; }
+      else if (R2 != R1) { R = R2; C = j - R1 - 1; }
+    }
+    const int dd = R - C;
+    tix[m] = (R >= 0) ? (B + C) % (NB - dd) : 0;
+  }
+  __syncthreads();
+  T* Lt_ = reinterpret_cast<T*>(Lt) + (size_t)phi * nx * n;
+  T* Di_ = reinterpret_cast<T*>(Dinv) + (size_t)phi * nx;
+  for (int i0 = 0; i0 < nx; i0 += B) {
+    // ---- 1. panel: load the rows' panel entries, then factor the PF_B columns
+    T e[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int dd = x - k;
+      e[k] = (x < NB && dd >= 0 && dd <= n) ? ring[pf_roff(dd, NB) + psl[k]] : S::zero();
+    }
+    __syncthreads();  // the panel columns' slots are free from here on
+    if (tid < PF_PT) {
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        T* pb = pub + (k & 1) * B;
+        if (x >= k && x < B) pb[x] = e[k];
+        asm volatile("bar.sync 1, %0;\n" ::"r"(PF_PT) : "memory");
+        const T di = S::rcp(pb[k]);
+        if (x < NB) {
+          const T ek = e[k];
+          const T l = (x > k) ? S::mul(ek, di) : S::zero();
+          PB[k * NB + x] = ek;
+          PA[k * NB + x] = l;
+#pragma unroll
+          for (int k2 = k + 1; k2 < B; ++k2)
+            if (x >= k2 && x - k2 <= n) e[k2] = S::fms(l, pb[k2], e[k2]);
+          if (x == k && i0 + k < nx) Di_[i0 + k] = di;
+        }
+      }
+    } else {  // rows entering for the next panel: i0+NB .. i0+NB+B-1 (operator values)
+      for (int q = tid - PF_PT; q < B * (n + 1); q += PF_NT - PF_PT) {
+        const int r = i0 + NB + q / (n + 1), dd = q % (n + 1), cc = r - dd;
+        ring[pf_roff(dd, NB) + cc % (NB - dd)] = opB(r, dd);
+      }
+    }
+    __syncthreads();
+    for (int q = tid; q < B * n; q += PF_NT) {  // Lt[i][t] = L(i+1+t, i), i = i0 + k
+      const int k = q / n, t = q - k * n, i = i0 + k;
+      if (i < nx) Lt_[(size_t)i * n + t] = (i + 1 + t < nx) ? PA[k * NB + k + 1 + t] : S::zero();
+    }
+    // ---- 2. trailing rank-B update of rows/columns i0+B .. i0+NB-1
+    if (pair_ok) {
+      T acc[PF_M];
+#pragma unroll
+      for (int m = 0; m < PF_M; ++m) {
+        const int j = g + 8 * m;
+        const int R = (j <= R1) ? R1 : R2, C = (j <= R1) ? j : j - R1 - 1;
+        const bool ok = j <= n && (j <= R1 || R2 != R1);
+        acc[m] = ok ? ring[pf_roff(R - C, NB) + tix[m]] : S::zero();
+      }
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const T a1 = PA[k * NB + B + R1], a2 = PA[k * NB + B + R2];
+#pragma unroll
+        for (int m = 0; m < PF_M; ++m) {
+          const int j = g + 8 * m;
+          const int C = (j <= R1) ? j : j - R1 - 1;
+          if (j <= n) acc[m] = S::fms((j <= R1) ? a1 : a2, PB[k * NB + B + C], acc[m]);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < PF_M; ++m) {
+        const int j = g + 8 * m;
+        const int R = (j <= R1) ? R1 : R2, C = (j <= R1) ? j : j - R1 - 1;
+        if (j <= n && (j <= R1 || R2 != R1)) ring[pf_roff(R - C, NB) + tix[m]] = acc[m];
+      }
+    }
+    __syncthreads();
+    // ---- advance the ring indices by one panel
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int dd = x - k;
+      if (dd >= 0 && dd <= n) {
+        psl[k] += B;
+        if (psl[k] >= NB - dd) psl[k] -= NB - dd;
+      }
+    }
+    if (pair_ok) {
+#pragma unroll
+      for (int m = 0; m < PF_M; ++m) {
+        const int j = g + 8 * m;
+        const int R = (j <= R1) ? R1 : R2, C = (j <= R1) ? j : j - R1 - 1;
+        const int L = NB - (R - C);
+        tix[m] += B;
+        if (tix[m] >= L) tix[m] -= L;
+      }
+    }
   }
 }
 
@@ -685,6 +862,17 @@ extern "C" int kle_2d_factor_f64(const double* dia, const double* ex, const doub
     return set_error(KLE_ERR_INVALID, "factor2d: bad dims (n <= 127)");
   if (M == 0) return KLE_OK;
   const int W = n + 1;
+  static const bool panel = [] {
+    const char* e = getenv("KLE_2D_FACTOR_PANEL");
+    return !(e && e[0] == '0');
+  }();
+  if (lam && panel && (n + 1) / 2 * 8 <= PF_NT && n + PF_B <= PF_PT && n + 1 <= 8 * PF_M) {
+    const size_t smem = pf_smem_bytes(n);
+    cudaFuncSetAttribute(band_factor_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    band_factor_panel_kernel<<<(unsigned)(M * NF), PF_NT, smem, KLE2D_STREAM(stream)>>>(dia, ex, ey, n, lam, NF, c,
+                                                                                       Lt, Dinv);
+    return check_launch("band_factor_panel_kernel");
+  }
   if (lam) {
     const size_t smem = sizeof(double) * 16384 + 2 * W * sizeof(Cplx) + sizeof(double) * 3 * BF_RING;
     cudaFuncSetAttribute(band_factor_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -168,3 +168,38 @@ def test_tma_sweeps_match_dense_solves(cuda, M, N):
         for _ in range(J):
             x = torch.linalg.solve(T, x + grid.deltat * op.g0)
         assert rel(out[:, :, seg].cpu().numpy(), x.transpose(1, 2).cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [15, 40, 127])
+def test_complex_band_factors_reconstruct(cuda, n):
+    """kle_2d_factor_f64 with complex shifts (the panel L D L^T): L D L^T
+    rebuilt densely equals lambda_f I + dT A for every frequency (complex
+    symmetric, pintuq/pcgc.py:137-145 factors the same matrices with SuperLU)."""
+    import torch
+
+    from paper_2510_26180_b200 import LogNormalKL2D
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    N, dT = 8, 1.0 / 8
+    model = LogNormalKL2D(n=n, d=10, sigma=0.5, ell=0.25)
+    xi = np.random.default_rng(n).normal(size=(2, 10))
+    op = DeviceOperator.from_model(model, xi)
+    tables = AlphaTables(build_alpha_circulant(N, 1e-3))
+    Lt, Dinv = op.shifted_factors(tables, N, dT)
+    nx, NF = n * n, N // 2 + 1
+    Lc = torch.view_as_complex(Lt.reshape(2, NF, nx, n, 2))
+    Dc = torch.view_as_complex(Dinv.reshape(2, NF, nx, 2))
+    A = _dense_ops(op).to(torch.complex128)
+    lam = torch.view_as_complex(tables.lam.reshape(N, 2))
+    rows = torch.arange(nx, device="cuda")
+    for s_ in range(2):
+        for f in (0, 1, NF - 1):
+            L = torch.eye(nx, dtype=torch.complex128, device="cuda")
+            for t in range(n):
+                r = rows[: nx - 1 - t]
+                L[r + 1 + t, r] = Lc[s_, f, : nx - 1 - t, t]
+            D = torch.diag(1.0 / Dc[s_, f])
+            Bf = lam[f] * torch.eye(nx, dtype=torch.complex128, device="cuda") + dT * A[s_]
+            err = (L @ D @ L.T - Bf).abs().max() / Bf.abs().max()
+            assert float(err) <= 1e-13, (s_, f, float(err))
