@@ -271,9 +271,8 @@ __global__ void __launch_bounds__(NT, 1)
 //      PA[k][x] = W(x,k)/d_k and PB[k][x] = W(x,k); the other threads load the
 //      PF_B operator rows that enter for the next panel;
 //   2. all threads apply the rank-PF_B update W(r,c) -= sum_k PA[k][r] PB[k][c]
-//      to the trailing triangle (rows r and n-1-r folded into one list of n+1
-//      entries per thread group, 16 entries per thread, columns strided over
-//      the group's 8 threads so PB reads are conflict-free).
+//      to the trailing triangle: 8 threads per folded row pair (r, n-1-r),
+//      columns strided over them, each PB read feeding both rows.
 // Each window entry is read and written once per PF_B rows instead of once
 // per row (band_factor_kernel: ~4,400 shared-memory wavefronts per row).
 // ---------------------------------------------------------------------------
@@ -285,7 +284,7 @@ constexpr int PF_M = 16;    // trailing entries per thread (8 threads per folded
 __host__ __device__ inline int pf_roff(int d, int NB) { return d * NB - d * (d - 1) / 2; }
 __host__ inline size_t pf_smem_bytes(int n) {
   const int NB = n + PF_B;
-  return sizeof(Cplx) * ((size_t)pf_roff(n + 1, NB) + 2 * (size_t)PF_B * NB + 2 * PF_B);
+  return sizeof(Cplx) * ((size_t)pf_roff(n + 1, NB) + 2 * (size_t)PF_B * NB + 2 * PF_B) + sizeof(int) * (n + 1);
 }
 
 __global__ void __launch_bounds__(PF_NT, 1)
@@ -306,6 +305,7 @@ __global__ void __launch_bounds__(PF_NT, 1)
   T* PA = ring + pf_roff(n + 1, NB);  // [B][NB]
   T* PB = PA + B * NB;                // [B][NB]
   T* pub = PB + B * NB;               // [2][B]
+  int* rb = reinterpret_cast<int*>(pub + 2 * B);  // [n+1]: ring index of column i0+B on diagonal d
   const int tid = threadIdx.x;
   auto opB = [&](int r, int dd) -> T {  // B(r, r - dd): the operator (identity beyond nx)
     if (r >= nx) return dd == 0 ? S::mk(1.0, 0.0) : S::zero();
@@ -327,22 +327,10 @@ __global__ void __launch_bounds__(PF_NT, 1)
     const int dd = x - k;
     psl[k] = (dd >= 0 && dd <= n) ? k % (NB - dd) : 0;
   }
-  // trailing-thread state: folded pair p (rows p and n-1-p), lane g of 8; entry m: list index j = g + 8m
+  // trailing-thread state: folded pair p (rows p and n-1-p of the trailing triangle), lane g of 8
   const int p = tid >> 3, g = tid & 7;
   const int R1 = p, R2 = n - 1 - p;
   const bool pair_ok = R1 <= R2;
-  int tix[PF_M];
-#pragma unroll
-  for (int m = 0; m < PF_M; ++m) {
-    const int j = g + 8 * m;
-    int R = -1, C = 0;
-    if (pair_ok && j <= n) {
-      if (j <= R1) { R = R1; C = j; }
-      else if (R2 != R1) { R = R2; C = j - R1 - 1; }
-    }
-    const int dd = R - C;
-    tix[m] = (R >= 0) ? (B + C) % (NB - dd) : 0;
-  }
   __syncthreads();
   T* Lt_ = reinterpret_cast<T*>(Lt) + (size_t)phi * nx * n;
   T* Di_ = reinterpret_cast<T*>(Dinv) + (size_t)phi * nx;
@@ -374,6 +362,7 @@ __global__ void __launch_bounds__(PF_NT, 1)
         }
       }
     } else {  // rows entering for the next panel: i0+NB .. i0+NB+B-1 (operator values)
+      for (int dd = tid - PF_PT; dd <= n; dd += PF_NT - PF_PT) rb[dd] = (i0 + B) % (NB - dd);
       for (int q = tid - PF_PT; q < B * (n + 1); q += PF_NT - PF_PT) {
         const int r = i0 + NB + q / (n + 1), dd = q % (n + 1), cc = r - dd;
         ring[pf_roff(dd, NB) + cc % (NB - dd)] = opB(r, dd);
@@ -386,29 +375,54 @@ __global__ void __launch_bounds__(PF_NT, 1)
     }
     // ---- 2. trailing rank-B update of rows/columns i0+B .. i0+NB-1
     if (pair_ok) {
-      T acc[PF_M];
+      // columns C = g + 8 (4q + u) of both rows of the pair: the 8 lanes of a
+      // pair read 8 consecutive PB entries and the warp's 4 pairs the same
+      // ones (one wavefront); each PB value feeds both rows
+#pragma unroll 1
+      for (int q = 0; q < PF_M / 4; ++q) {
+        const int c0 = g + 32 * q;
+        if (c0 > R2) break;
+        const bool do1 = c0 <= R1 && R1 != R2;
+        T a1c[4], a2c[4];
+        int w1[4], w2[4], C[4];
 #pragma unroll
-      for (int m = 0; m < PF_M; ++m) {
-        const int j = g + 8 * m;
-        const int R = (j <= R1) ? R1 : R2, C = (j <= R1) ? j : j - R1 - 1;
-        const bool ok = j <= n && (j <= R1 || R2 != R1);
-        acc[m] = ok ? ring[pf_roff(R - C, NB) + tix[m]] : S::zero();
-      }
-#pragma unroll
-      for (int k = 0; k < B; ++k) {
-        const T a1 = PA[k * NB + B + R1], a2 = PA[k * NB + B + R2];
-#pragma unroll
-        for (int m = 0; m < PF_M; ++m) {
-          const int j = g + 8 * m;
-          const int C = (j <= R1) ? j : j - R1 - 1;
-          if (j <= n) acc[m] = S::fms((j <= R1) ? a1 : a2, PB[k * NB + B + C], acc[m]);
+        for (int u = 0; u < 4; ++u) {
+          C[u] = c0 + 8 * u;
+          const int d2 = R2 - C[u], d1 = R1 - C[u];
+          const int e2 = max(d2, 0), e1 = max(d1, 0);
+          int i2 = rb[e2] + C[u];
+          if (i2 >= NB - e2) i2 -= NB - e2;
+          int i1 = rb[e1] + C[u];
+          if (i1 >= NB - e1) i1 -= NB - e1;
+          w2[u] = pf_roff(e2, NB) + i2;
+          w1[u] = pf_roff(e1, NB) + i1;
+          a2c[u] = d2 >= 0 ? ring[w2[u]] : S::zero();
+          a1c[u] = (do1 && d1 >= 0) ? ring[w1[u]] : S::zero();
         }
-      }
+        if (do1) {
 #pragma unroll
-      for (int m = 0; m < PF_M; ++m) {
-        const int j = g + 8 * m;
-        const int R = (j <= R1) ? R1 : R2, C = (j <= R1) ? j : j - R1 - 1;
-        if (j <= n && (j <= R1 || R2 != R1)) ring[pf_roff(R - C, NB) + tix[m]] = acc[m];
+          for (int k = 0; k < B; ++k) {
+            const T x1 = PA[k * NB + B + R1], x2 = PA[k * NB + B + R2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const T pbv = PB[k * NB + B + C[u]];
+              a2c[u] = S::fms(x2, pbv, a2c[u]);
+              a1c[u] = S::fms(x1, pbv, a1c[u]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            const T x2 = PA[k * NB + B + R2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a2c[u] = S::fms(x2, PB[k * NB + B + C[u]], a2c[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (C[u] <= R2) ring[w2[u]] = a2c[u];
+          if (do1 && C[u] <= R1) ring[w1[u]] = a1c[u];
+        }
       }
     }
     __syncthreads();
@@ -419,16 +433,6 @@ __global__ void __launch_bounds__(PF_NT, 1)
       if (dd >= 0 && dd <= n) {
         psl[k] += B;
         if (psl[k] >= NB - dd) psl[k] -= NB - dd;
-      }
-    }
-    if (pair_ok) {
-#pragma unroll
-      for (int m = 0; m < PF_M; ++m) {
-        const int j = g + 8 * m;
-        const int R = (j <= R1) ? R1 : R2, C = (j <= R1) ? j : j - R1 - 1;
-        const int L = NB - (R - C);
-        tix[m] += B;
-        if (tix[m] >= L) tix[m] -= L;
       }
     }
   }
