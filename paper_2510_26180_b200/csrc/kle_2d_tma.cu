@@ -238,7 +238,7 @@ __device__ __forceinline__ void tma_pass(const double* __restrict__ chunks, cons
 }
 
 __device__ __forceinline__ void dmma_acc(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
@@ -290,19 +290,26 @@ __device__ __forceinline__ void tma_pass_mma(const double* __restrict__ chunks, 
 #pragma unroll
       for (int a2 = 0; a2 < a; ++a2, ++t) nc[t] = cst[(n + a2) * RB + a];
     const int q0 = p0 - n;
-    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-#pragma unroll 4
-    for (int ks = 0; ks < KS; ks += 2) {
-      const int qa = 4 * ks + fk, qb = qa + 4;
+    // four independent accumulators (8-deep DMMA chains at n = 127)
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0}, c3[2] = {0.0, 0.0};
+#pragma unroll 2
+    for (int ks = 0; ks < KS; ks += 4) {
+      const int qa = 4 * ks + fk, qb = qa + 4, qc = qa + 8, qd = qa + 12;
       const double A0 = qa < n ? cst[qa * RB + fa] : 0.0;
       const double B0 = win[((q0 + qa) & wm) * 8 + fa];
       const double A1 = qb < n ? cst[qb * RB + fa] : 0.0;
       const double B1 = win[((q0 + qb) & wm) * 8 + fa];
+      const double A2 = qc < n ? cst[qc * RB + fa] : 0.0;
+      const double B2 = win[((q0 + qc) & wm) * 8 + fa];
+      const double A3 = qd < n ? cst[qd * RB + fa] : 0.0;
+      const double B3 = win[((q0 + qd) & wm) * 8 + fa];
       dmma_acc(c0, A0, B0);
       dmma_acc(c1, A1, B1);
+      dmma_acc(c2, A2, B2);
+      dmma_acc(c3, A3, B3);
     }
-    xs[fa * 8 + 2 * fk] = c0[0] + c1[0];
-    xs[fa * 8 + 2 * fk + 1] = c0[1] + c1[1];
+    xs[fa * 8 + 2 * fk] = (c0[0] + c1[0]) + (c2[0] + c3[0]);
+    xs[fa * 8 + 2 * fk + 1] = (c0[1] + c1[1]) + (c2[1] + c3[1]);
     __syncwarp();
     if (lane < 8) {
       double yv[RB];
