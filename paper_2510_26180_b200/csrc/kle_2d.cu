@@ -696,9 +696,15 @@ __global__ void dft_fwd_kernel(const double* __restrict__ R, const double* __res
 }
 
 // one warp per (sample, frequency): B_f q = p in place
+// The factor rows are streamed PD rows ahead in registers (4 complex per lane
+// and row for n <= 128) together with p_i and D_i^{-1}: the row recurrence
+// only waits on shared memory, HBM latency is hidden PD rows deep.
+constexpr int BS_PD = 4;
+
 __global__ void __launch_bounds__(32) band_solve_cplx_kernel(Cplx* __restrict__ P, const double* __restrict__ Lt,
                                                              const double* __restrict__ Dinv,
                                                              const int32_t* __restrict__ status, int NF, int n) {
+  constexpr int PD = BS_PD;
   const int nx = n * n, W = n + 1;
   const int phi = blockIdx.x, s = phi / NF;
   if (status && status[s] != KLE_SAMPLE_ACTIVE) return;
@@ -707,58 +713,93 @@ __global__ void __launch_bounds__(32) band_solve_cplx_kernel(Cplx* __restrict__ 
   const Cplx* Di = reinterpret_cast<const Cplx*>(Dinv) + (size_t)phi * nx;
   Cplx* p = P + (size_t)phi * nx;
   __shared__ Cplx win[128];
+  Cplx lr[PD][4], pr[PD], dr[PD];
+  auto fetch = [&](int u, int i, bool with_d) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int t = lane + 32 * m;
+      lr[u][m] = (i >= 0 && i < nx && t < n) ? L[(size_t)i * n + t] : Cplx{0.0, 0.0};
+    }
+    pr[u] = (i >= 0 && i < nx) ? p[i] : Cplx{0.0, 0.0};
+    if (with_d) dr[u] = (i >= 0 && i < nx) ? Di[i] : Cplx{0.0, 0.0};
+  };
   for (int q = lane; q < W; q += 32) win[q] = {0.0, 0.0};
+#pragma unroll
+  for (int u = 0; u < PD; ++u) fetch(u, u, true);
   __syncwarp();
   // forward, column form: pending updates acc[(r) % W] for rows r in (i, i+n]
-  for (int i = 0; i < nx; ++i) {
-    const int si = i % W;
-    const Cplx acc = win[si];
-    const Cplx pi = p[i];
-    const Cplx y = {pi.re - acc.re, pi.im - acc.im};
-    __syncwarp();
-    if (lane == 0) {
-      win[si] = {0.0, 0.0};
-      p[i] = cmul(y, Di[i]);  // z_i = y_i / D_i
+  for (int i0 = 0; i0 < nx; i0 += PD) {
+#pragma unroll
+    for (int u = 0; u < PD; ++u) {
+      const int i = i0 + u;
+      if (i < nx) {
+        const int si = i % W;
+        const Cplx acc = win[si];
+        const Cplx y = {pr[u].re - acc.re, pr[u].im - acc.im};
+        __syncwarp();
+        if (lane == 0) {
+          win[si] = {0.0, 0.0};
+          p[i] = cmul(y, dr[u]);  // z_i = y_i / D_i
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int t = lane + 32 * m;
+          if (t < n) {
+            int sl = si + 1 + t;
+            if (sl >= W) sl -= W;
+            const Cplx l = lr[u][m];
+            Cplx w = win[sl];
+            w.re = fma(l.re, y.re, fma(-l.im, y.im, w.re));
+            w.im = fma(l.re, y.im, fma(l.im, y.re, w.im));
+            win[sl] = w;
+          }
+        }
+        __syncwarp();
+      }
+      fetch(u, i + PD, true);
     }
-    __syncwarp();
-    for (int t = lane; t < n; t += 32) {
-      int sl = si + 1 + t;
-      if (sl >= W) sl -= W;
-      const Cplx l = L[(size_t)i * n + t];
-      Cplx w = win[sl];
-      w.re = fma(l.re, y.re, fma(-l.im, y.im, w.re));
-      w.im = fma(l.re, y.im, fma(l.im, y.re, w.im));
-      win[sl] = w;
-    }
-    __syncwarp();
   }
   for (int q = lane; q < W; q += 32) win[q] = {0.0, 0.0};
-  __syncwarp();
-  // backward, dot form: x_i = z_i - sum_t L(i+1+t, i) x_{i+1+t}
-  for (int i = nx - 1; i >= 0; --i) {
-    const int si = i % W;
-    double re = 0.0, im = 0.0;
-    for (int t = lane; t < n; t += 32) {
-      int sl = si + 1 + t;
-      if (sl >= W) sl -= W;
-      const Cplx l = L[(size_t)i * n + t];
-      const Cplx x = win[sl];
-      re = fma(l.re, x.re, fma(-l.im, x.im, re));
-      im = fma(l.re, x.im, fma(l.im, x.re, im));
-    }
+  __syncwarp();  // also orders the forward pass's p[] stores before the reloads below
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      re += __shfl_xor_sync(KLE_FULL_MASK, re, o);
-      im += __shfl_xor_sync(KLE_FULL_MASK, im, o);
+  for (int u = 0; u < PD; ++u) fetch(u, nx - 1 - u, false);
+  // backward, dot form: x_i = z_i - sum_t L(i+1+t, i) x_{i+1+t}
+  for (int i0 = nx - 1; i0 >= 0; i0 -= PD) {
+#pragma unroll
+    for (int u = 0; u < PD; ++u) {
+      const int i = i0 - u;
+      if (i >= 0) {
+        const int si = i % W;
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int t = lane + 32 * m;
+          if (t < n) {
+            int sl = si + 1 + t;
+            if (sl >= W) sl -= W;
+            const Cplx l = lr[u][m];
+            const Cplx x = win[sl];
+            re = fma(l.re, x.re, fma(-l.im, x.im, re));
+            im = fma(l.re, x.im, fma(l.im, x.re, im));
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(KLE_FULL_MASK, re, o);
+          im += __shfl_xor_sync(KLE_FULL_MASK, im, o);
+        }
+        const Cplx z = pr[u];
+        const Cplx x = {z.re - re, z.im - im};
+        __syncwarp();
+        if (lane == 0) {
+          win[si] = x;
+          p[i] = x;
+        }
+        __syncwarp();
+      }
+      fetch(u, i - PD, false);
     }
-    const Cplx z = p[i];
-    const Cplx x = {z.re - re, z.im - im};
-    __syncwarp();
-    if (lane == 0) {
-      win[si] = x;
-      p[i] = x;
-    }
-    __syncwarp();
   }
 }
 
