@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(32 * NW) fine2d_tma_kernel(Fine2dTmaArgs a) {
   constexpr int NT = 32 * NW, RW = 32 / NW;
   constexpr int RPC = MMA ? 8 * NW : 32;  // right-hand sides per CTA (one 8-wide DMMA tile per warp)
   constexpr int WW = MMA ? 8 : RW;        // window columns per warp
+  static_assert(NT % RPC == 0, "the start-state load maps threads to right-hand sides");
   const int n = a.n, nx = n * n;
   const int G = (a.N + RPC - 1) / RPC;
   const int s = blockIdx.x / G, g = blockIdx.x % G;
@@ -372,8 +373,11 @@ __global__ void __launch_bounds__(32 * NW) fine2d_tma_kernel(Fine2dTmaArgs a) {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   double* X = a.X + (size_t)blockIdx.x * nx * RPC;
   double* Z = a.Z + (size_t)blockIdx.x * nx * RPC;
-  // load the start states, X[i][jj] (32 right-hand sides; dead ones zero)
-  for (int jj = 0; jj < RPC; ++jj) {
+  // load the start states, X[i][jj] (RPC right-hand sides; dead ones zero):
+  // consecutive threads write consecutive X entries (rows of RPC doubles)
+  {
+    // thread tid always handles the same right-hand side jj = tid % RPC (NT is a multiple of RPC)
+    const int jj = tid % RPC;
     const int q = g * RPC + jj;
     const bool live = q < a.N;
     const double* src;
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(32 * NW) fine2d_tma_kernel(Fine2dTmaArgs a) {
     } else {
       src = a.start + ((size_t)s * a.N + (live ? q : 0)) * nx;
     }
-    for (int i = tid; i < nx; i += NT) X[(size_t)i * RPC + jj] = live ? src[i] : 0.0;
+    for (int i = tid / RPC; i < nx; i += NT / RPC) X[(size_t)i * RPC + jj] = live ? src[i] : 0.0;
   }
   fence_async_global();
   __syncthreads();
@@ -391,11 +395,12 @@ __global__ void __launch_bounds__(32 * NW) fine2d_tma_kernel(Fine2dTmaArgs a) {
   if (a.mode == 1) {
     for (int sg = 0; sg < a.nseg; ++sg) {
       tma_steps<NW, MMA>(a, s, X, Z, stg, full, win, xs, it);
-      for (int jj = 0; jj < RPC; ++jj) {
-        const int q = g * RPC + jj;
-        if (q >= a.N) break;
-        double* o = a.out + (((size_t)s * a.N + q) * a.nseg + sg) * nx;
-        for (int i = tid; i < nx; i += NT) o[i] = X[(size_t)i * RPC + jj];
+      {
+        const int jj = tid % RPC, q = g * RPC + jj;
+        if (q < a.N) {
+          double* o = a.out + (((size_t)s * a.N + q) * a.nseg + sg) * nx;
+          for (int i = tid / RPC; i < nx; i += NT / RPC) o[i] = X[(size_t)i * RPC + jj];
+        }
       }
       __syncthreads();
     }
@@ -406,24 +411,27 @@ __global__ void __launch_bounds__(32 * NW) fine2d_tma_kernel(Fine2dTmaArgs a) {
   const double* dd = a.dia + (size_t)s * nx;
   const double* ex = a.ex + (size_t)s * nx;
   const double* ey = a.ey + (size_t)s * nx;
-  for (int jj = 0; jj < RPC; ++jj) {
+  {
+    // thread tid keeps right-hand side jj = tid % RPC: X rows are read contiguously
+    const int jj = tid % RPC;
     const int q = g * RPC + jj;
-    if (q >= a.N) break;
-    const double* pv = (q == 0) ? a.start + ((size_t)s * a.N + (a.N - 1)) * nx
-                                : a.start + ((size_t)s * a.N + (q - 1)) * nx;
-    const double pmul = (q == 0) ? a.alpha : 1.0;
-    const double sc = a.scaling[q];
-    double* o = a.out + ((size_t)s * a.N + q) * nx;
-    const double* Xq = X + jj;
-    for (int i = tid; i < nx; i += NT) {
-      const double x = Xq[(size_t)i * RPC];
-      double Ax = dd[i] * x;
-      if (i + 1 < nx) Ax = fma(ex[i], Xq[(size_t)(i + 1) * RPC], Ax);
-      if (i >= 1) Ax = fma(ex[i - 1], Xq[(size_t)(i - 1) * RPC], Ax);
-      if (i + n < nx) Ax = fma(ey[i], Xq[(size_t)(i + n) * RPC], Ax);
-      if (i >= n) Ax = fma(ey[i - n], Xq[(size_t)(i - n) * RPC], Ax);
-      const double rhs = fma(a.dT, Ax, x) - pmul * pv[i];
-      o[i] = sc * rhs;
+    if (q < a.N) {
+      const double* pv = (q == 0) ? a.start + ((size_t)s * a.N + (a.N - 1)) * nx
+                                  : a.start + ((size_t)s * a.N + (q - 1)) * nx;
+      const double pmul = (q == 0) ? a.alpha : 1.0;
+      const double sc = a.scaling[q];
+      double* o = a.out + ((size_t)s * a.N + q) * nx;
+      const double* Xq = X + jj;
+      for (int i = tid / RPC; i < nx; i += NT / RPC) {
+        const double x = Xq[(size_t)i * RPC];
+        double Ax = dd[i] * x;
+        if (i + 1 < nx) Ax = fma(ex[i], Xq[(size_t)(i + 1) * RPC], Ax);
+        if (i >= 1) Ax = fma(ex[i - 1], Xq[(size_t)(i - 1) * RPC], Ax);
+        if (i + n < nx) Ax = fma(ey[i], Xq[(size_t)(i + n) * RPC], Ax);
+        if (i >= n) Ax = fma(ey[i - n], Xq[(size_t)(i - n) * RPC], Ax);
+        const double rhs = fma(a.dT, Ax, x) - pmul * pv[i];
+        o[i] = sc * rhs;
+      }
     }
   }
 }
