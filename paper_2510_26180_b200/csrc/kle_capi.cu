@@ -202,10 +202,11 @@ size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
   return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256;
 }
 
+constexpr int kMaxPipes = 4;
 struct PipeResources {
-  cudaStream_t sf[2], sc[2];  // per pipeline: fine sweeps (low priority), CGC (high priority)
-  cudaEvent_t done[2], fdone[2], ready;
-  int32_t* h_count;  // pinned [2]
+  cudaStream_t sf[kMaxPipes], sc[kMaxPipes];  // per pipeline: fine sweeps (low priority), CGC (high priority)
+  cudaEvent_t done[kMaxPipes], fdone[kMaxPipes], ready;
+  int32_t* h_count;  // pinned [kMaxPipes]
 };
 
 // one set per host thread and device, created on first use, never freed
@@ -218,14 +219,14 @@ static PipeResources* pipe_resources() {
   auto* r = new PipeResources{};
   int lo = 0, hi = 0;
   bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess;
-  for (int p = 0; p < 2 && ok; ++p) {
+  for (int p = 0; p < kMaxPipes && ok; ++p) {
     ok = ok && cudaStreamCreateWithPriority(&r->sf[p], cudaStreamNonBlocking, lo) == cudaSuccess;
     ok = ok && cudaStreamCreateWithPriority(&r->sc[p], cudaStreamNonBlocking, hi) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&r->done[p], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&r->fdone[p], cudaEventDisableTiming) == cudaSuccess;
   }
   ok = ok && cudaEventCreateWithFlags(&r->ready, cudaEventDisableTiming) == cudaSuccess;
-  ok = ok && cudaHostAlloc(&r->h_count, 2 * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
+  ok = ok && cudaHostAlloc(&r->h_count, kMaxPipes * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
   if (!ok) {
     delete r;
     return nullptr;
@@ -279,7 +280,11 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
   // latency-bound CGC of the other. Results do not depend on the split (every
   // sample's arithmetic is the same; only the launch grouping changes).
   int pipes = (M >= 8192 && clustered) ? 2 : 1;
-  if (const char* e = getenv("KLE_PCGC_PIPES")) pipes = atoi(e) == 2 && M >= 2 && clustered ? 2 : 1;
+  if (const char* e = getenv("KLE_PCGC_PIPES")) {
+    pipes = clustered ? atoi(e) : 1;
+    pipes = pipes < 1 ? 1 : (pipes > kMaxPipes ? kMaxPipes : pipes);
+    if (pipes > M) pipes = M > 0 ? M : 1;
+  }
   const FineLayoutRT lay = fine_layout(nx);
   struct Pipe {
     int m0, M, k;
@@ -288,7 +293,7 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
     cudaEvent_t done, fdone;
     int32_t* count_d;
   };
-  Pipe pp[2];
+  Pipe pp[kMaxPipes];
   // streams, events and the pinned counters are created once per host thread
   // and device and reused: driver resource calls inside a solve serialise with
   // other driver clients (e.g. an nvidia-smi poll) and cost more than a short
@@ -348,8 +353,8 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
   for (int p = 0; p < pipes && rc == KLE_OK; ++p) {
     if (!pp[p].live) continue;
     rc = enqueue(pp[p]);
-    if (p == 0 && pipes == 2)  // the second half starts after the first half's first fine sweep
-      cudaStreamWaitEvent(pp[1].st, pp[0].fdone, 0);
+    if (p + 1 < pipes)  // each part starts after the previous part's first fine sweep
+      cudaStreamWaitEvent(pp[p + 1].st, pp[p].fdone, 0);
   }
   for (bool any = true; any && rc == KLE_OK;) {
     any = false;
@@ -369,7 +374,7 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
       rc = enqueue(q);
     }
   }
-  if (pipes == 2) {  // join: later work on `st` sees both halves
+  if (pipes > 1) {  // join: later work on `st` sees every part
     for (int p = 0; p < pipes; ++p) {
       cudaEventRecord(pp[p].done, pp[p].sc);
       cudaStreamWaitEvent(st, pp[p].done, 0);
