@@ -177,3 +177,29 @@ def test_reference_diffusion1d_model_on_device(cuda, golden):
     with pytest.raises(NotImplementedError):
         pcgc_solve(ad, ParameterSample(np.array([3.0]), id=0), make_time_grid(1.0, 8, 4), cfg,
                    CoarseTrajectory(ad.initial_condition(), np.zeros((8, ad.nx))))
+
+
+@pytest.mark.parametrize("pipes", [2, 3, 4])
+def test_sample_pipelines_do_not_change_results(cuda, pipes, monkeypatch):
+    """The batched loop's staggered sample pipelines (KLE_PCGC_PIPES) only
+    regroup launches: states, iteration counts and increments are bitwise the
+    single-pipeline ones (scheduling independence)."""
+    import torch
+
+    from paper_2510_26180_b200 import LogNormalKL1D
+    from paper_2510_26180_b200.pcgc import pcgc_solve_batched
+
+    model = LogNormalKL1D(nx=127, d=4)
+    grid = make_time_grid(1.0, 16, 32)
+    cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60)
+    M = 301
+    xi = np.random.default_rng(7).normal(size=(M, 4))
+    U0 = np.random.default_rng(8).uniform(0.0, 1.0, size=(M, 16, 127))
+    monkeypatch.setenv("KLE_PCGC_PIPES", "1")
+    one = pcgc_solve_batched(model, xi, grid, cfg, U0)
+    monkeypatch.setenv("KLE_PCGC_PIPES", str(pipes))
+    many = pcgc_solve_batched(model, xi, grid, cfg, U0)
+    assert torch.equal(one.iters, many.iters)
+    assert torch.equal(one.status, many.status)
+    assert torch.equal(one.states, many.states)
+    assert torch.equal(torch.nan_to_num(one.increments, nan=-1.0), torch.nan_to_num(many.increments, nan=-1.0))
