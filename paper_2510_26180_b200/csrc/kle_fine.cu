@@ -221,27 +221,47 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
     }
     if (a.Rout == nullptr) return;  // F ends only (classical parareal)
     // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n), operands from shared memory;
-    // each rhs row replaces its (consumed) prev row in st, then the CTA stores st coalesced
+    // each rhs row replaces its (consumed) prev row in st, then the CTA stores st coalesced.
+    // Row-major over j with the R right-hand sides inner: the operator values of a row are
+    // read once, every shared load precedes every store (no alias barriers between them),
+    // and the rhs values overwrite x in place (the left neighbour is carried in xl).
+    double left[R], right[R], sc[R], pmul[R];
+    const double* pv[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double left = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
-      const double right = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
+      left[r] = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
+      right[r] = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
       const int n = n0 + nl[r];
-      if (n >= N) continue;
-      const double sc = a.scaling[n];
-      const double* pv = (n == 0) ? p0 : st + nl[r] * LD;
+      sc[r] = (n < N) ? a.scaling[n] : 0.0;
+      pmul[r] = (n == 0) ? a.alpha : 1.0;
+      pv[r] = (n == 0) ? p0 : st + nl[r] * LD;
+    }
+    double xl[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) xl[r] = k > 0 ? left[r] : 0.0;
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      const int pr = SM::pidx(row);
+      const double dj = dd[pr], em = ee[pr], ep = ee[SM::pidx(row + 1)];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double xc = x[r][j];
+        const double xp = (j < MR - 1) ? x[r][j + 1] : (k < P - 1 ? right[r] : 0.0);
+        const double Ax = fma(em, xl[r], fma(dj, xc, ep * xp));
+        const double rhs = fma(a.dT, Ax, xc) - pmul[r] * pv[r][pr];
+        xl[r] = xc;
+        x[r][j] = sc[r] * rhs;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (n0 + nl[r] >= N) continue;
       double* rs = st + nl[r] * LD;
-      const double pmul = (n == 0) ? a.alpha : 1.0;
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
         const int row = k * MR + j;
-        if (row >= nx) continue;
-        const double xm = (j > 0) ? x[r][j - 1] : (k > 0 ? left : 0.0);
-        const double xp = (j < MR - 1) ? x[r][j + 1] : (k < P - 1 ? right : 0.0);
-        const int pr = SM::pidx(row);
-        const double Ax = fma(ee[pr], xm, fma(dd[pr], x[r][j], ee[SM::pidx(row + 1)] * xp));
-        const double rhs = fma(a.dT, Ax, x[r][j]) - pmul * pv[pr];
-        rs[pr] = sc * rhs;
+        if (row < nx) rs[SM::pidx(row)] = x[r][j];
       }
     }
     __syncthreads();
