@@ -176,12 +176,14 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
       const double* src = (n == 0) ? a.u0 : a.U + sbase + (size_t)(n - 1) * nx;
       for (int row = tid; row < nx; row += NT) cp_async8(st + ln * LD + SM::pidx(row), src + row);
     }
+    asm volatile("cp.async.commit_group;\n" ::);  // group 1: the start rows (needed first)
     if (n0 == 0)
       for (int row = tid; row < nx; row += NT) cp_async8(p0 + SM::pidx(row), a.U + sbase + (size_t)(N - 1) * nx + row);
     for (int row = tid; row < nx; row += NT) {
       cp_async8(dd + SM::pidx(row), a.dia + (size_t)s * nx + row);
       if (row + 1 < nx) cp_async8(ee + SM::pidx(row + 1), a.off + (size_t)s * nx + row);
     }
+    asm volatile("cp.async.commit_group;\n" ::);  // group 2: epilogue operands
     if (tid == 0) {
       ee[0] = 0.0;
       ee[SM::pidx(nx)] = 0.0;
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
     if constexpr (KLE_FINE_CS && !PIPE && !KLE_FINE_LAZY) {
       if (w == 0 && slot == 0) chunk_products<MR, P>(cs, fac, k, hg);
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -219,7 +221,9 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
           if (row < nx && n0 + nl[r] < N) a.F_out[sbase + (size_t)(n0 + nl[r]) * nx + row] = x[r][j];
         }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
     if (a.Rout == nullptr) return;  // F ends only (classical parareal)
+    __syncthreads();  // the epilogue operands (group 2) of every thread have landed
     // epilogue: rhs_n = scaling_n * ((I + dT A) F_n - prev_n), operands from shared memory;
     // each rhs row replaces its (consumed) prev row in st, then the CTA stores st coalesced.
     // Row-major over j with the R right-hand sides inner: the operator values of a row are
