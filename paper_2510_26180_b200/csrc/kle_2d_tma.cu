@@ -44,7 +44,10 @@ __host__ __device__ inline int tb_wp(int n) {
   while (w < n + 1) w <<= 1;
   return w;
 }
-__host__ __device__ inline int tb_ch(int n) { return (n + TB_RB + 1) * TB_RB; }  // doubles per chunk
+// far rows padded to KP = 16 ceil(n/16) (zero rows n..KP-1: the DMMA loop runs whole groups of four
+// 4-row k-steps with no bounds test), then 8 near rows and D^{-1}
+__host__ __device__ inline int tb_kp(int n) { return (n + 15) / 16 * 16; }
+__host__ __device__ inline int tb_ch(int n) { return (tb_kp(n) + TB_RB + 1) * TB_RB; }  // doubles per chunk
 __host__ __device__ inline int tb_nblk(int n) { return (n * n + TB_RB - 1) / TB_RB; }
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -76,7 +79,8 @@ __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Restage: chunk e of block blk (p0 = 8 blk), forward (dir 0):
+// Restage: chunk e of block blk (p0 = 8 blk) in the unpadded row numbering u
+// (far rows u < n, then rows KP.. hold u = n.., zero rows between), forward (dir 0):
 //   e = u*8 + a, u < n:       L(p0+a, p0-n+u) = Lt[p0-n+u][n-1-u+a]   (a <= u)
 //   e = (n+a2)*8 + a:         L(p0+a, p0+a2)  = Lt[p0+a2][a-a2-1]      (a2 < a)
 //   e = (n+8)*8 + a:          Dinv[p0+a]
@@ -97,10 +101,14 @@ __global__ void fine2d_stage_kernel(const double* __restrict__ Lt, const double*
   r -= (long long)dir * nb * CH;
   const int blk = (int)(r / CH), e = (int)(r - (long long)blk * CH);
   const double* L = Lt + (size_t)s * nx * n;
-  const int p0 = blk * TB_RB, a = e % TB_RB, u = e / TB_RB;
+  const int p0 = blk * TB_RB, a = e % TB_RB, up = e / TB_RB, KP = tb_kp(n);
+  // chunk row up -> row u of the unpadded layout (far rows < n, near rows n..n+7, D^{-1} at n+8)
+  const int u = up < n ? up : (up >= KP ? up - KP + n : -1);
   const int p = p0 + a;
   double v = 0.0;
-  if (u == n + TB_RB) {
+  if (u < 0) {
+    v = 0.0;
+  } else if (u == n + TB_RB) {
     v = (dir == 0 && p < nx) ? Dinv[(size_t)s * nx + p] : 1.0;
   } else if (p < nx) {
     if (dir == 0) {
@@ -143,6 +151,7 @@ __device__ __forceinline__ void tma_pass(const double* __restrict__ chunks, cons
                                          double* win, int n, int& it) {
   constexpr int RB = TB_RB, RW = 32 / NW;
   const int nx = n * n, CH = tb_ch(n), SZ = CH + RB * 32, nb = tb_nblk(n), WP = tb_wp(n), wm = WP - 1;
+  const int KP = tb_kp(n);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int r = lane % RW, h = lane / RW, j = w * RW + r;
   auto issue = [&](int b, int st) {
@@ -168,14 +177,14 @@ __device__ __forceinline__ void tma_pass(const double* __restrict__ chunks, cons
 #pragma unroll
     for (int a = 0; a < RB; ++a) {
       bv[a] = (a < cnt) ? bvs[(BACK ? cnt - 1 - a : a) * 32 + j] : 0.0;
-      dv[a] = BACK ? 1.0 : cst[(n + RB) * RB + a];
+      dv[a] = BACK ? 1.0 : cst[(KP + RB) * RB + a];
     }
     // near-part coefficients, loaded now (off the chain of the triangular fix-up)
     double nc[RB * (RB - 1) / 2];
 #pragma unroll
     for (int a = 1, t = 0; a < RB; ++a)
 #pragma unroll
-      for (int a2 = 0; a2 < a; ++a2, ++t) nc[t] = cst[(n + a2) * RB + a];
+      for (int a2 = 0; a2 < a; ++a2, ++t) nc[t] = cst[(KP + a2) * RB + a];
     // far part: this lane's window positions qq = h + NW m, m < nq, in chunks
     // of TB_U with the next chunk's shared-memory loads in flight (one warp per
     // SM sub-partition: nothing else hides their latency)
@@ -257,9 +266,10 @@ __device__ __forceinline__ void tma_pass_mma(const double* __restrict__ chunks, 
                                              double* win, double* xs, int n, int& it) {
   constexpr int RB = TB_RB;
   const int nx = n * n, CH = tb_ch(n), SZ = CH + RB * RPC, nb = tb_nblk(n), WP = tb_wp(n), wm = WP - 1;
+  const int KP = tb_kp(n);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int fa = lane >> 2, fk = lane & 3, rl = lane & 7, j = w * 8 + rl;
-  const int KS = (n + 3) / 4;
+  const int KS = KP / 4;  // a multiple of 4
   auto issue = [&](int b, int st) {
     const int p0 = b * RB, cnt = min(RB, nx - p0);
     double* dst = stg + (size_t)st * SZ;
@@ -283,26 +293,26 @@ __device__ __forceinline__ void tma_pass_mma(const double* __restrict__ chunks, 
 #pragma unroll
     for (int a = 0; a < RB; ++a) {
       bv[a] = (a < cnt) ? bvs[(BACK ? cnt - 1 - a : a) * RPC + j] : 0.0;
-      dv[a] = BACK ? 1.0 : cst[(n + RB) * RB + a];
+      dv[a] = BACK ? 1.0 : cst[(KP + RB) * RB + a];
     }
 #pragma unroll
     for (int a = 1, t = 0; a < RB; ++a)
 #pragma unroll
-      for (int a2 = 0; a2 < a; ++a2, ++t) nc[t] = cst[(n + a2) * RB + a];
+      for (int a2 = 0; a2 < a; ++a2, ++t) nc[t] = cst[(KP + a2) * RB + a];
     const int q0 = p0 - n;
-    // four independent accumulators (8-deep DMMA chains at n = 127)
+    // four independent accumulators (8-deep DMMA chains at n = 127). A fragments at immediate
+    // offsets (rows >= n of the chunk are zero); B fragment slot (q0 + 4 ks + fk) & wm advanced
+    // by 4 per k-step on a pre-scaled index
     double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0}, c3[2] = {0.0, 0.0};
+    const double* ap = cst + fk * RB + fa;
+    const int bmask = WP * 8 - 1;
+    const int bb = ((q0 + fk) * 8 + fa) & bmask;
 #pragma unroll 2
     for (int ks = 0; ks < KS; ks += 4) {
-      const int qa = 4 * ks + fk, qb = qa + 4, qc = qa + 8, qd = qa + 12;
-      const double A0 = qa < n ? cst[qa * RB + fa] : 0.0;
-      const double B0 = win[((q0 + qa) & wm) * 8 + fa];
-      const double A1 = qb < n ? cst[qb * RB + fa] : 0.0;
-      const double B1 = win[((q0 + qb) & wm) * 8 + fa];
-      const double A2 = qc < n ? cst[qc * RB + fa] : 0.0;
-      const double B2 = win[((q0 + qc) & wm) * 8 + fa];
-      const double A3 = qd < n ? cst[qd * RB + fa] : 0.0;
-      const double B3 = win[((q0 + qd) & wm) * 8 + fa];
+      const double A0 = ap[(4 * ks) * RB], A1 = ap[(4 * ks + 4) * RB];
+      const double A2 = ap[(4 * ks + 8) * RB], A3 = ap[(4 * ks + 12) * RB];
+      const double B0 = win[(bb + 32 * ks) & bmask], B1 = win[(bb + 32 * ks + 32) & bmask];
+      const double B2 = win[(bb + 32 * ks + 64) & bmask], B3 = win[(bb + 32 * ks + 96) & bmask];
       dmma_acc(c0, A0, B0);
       dmma_acc(c1, A1, B1);
       dmma_acc(c2, A2, B2);
