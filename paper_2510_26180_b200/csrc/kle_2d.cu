@@ -276,7 +276,10 @@ __global__ void __launch_bounds__(NT, 1)
 // Each window entry is read and written once per PF_B rows instead of once
 // per row (band_factor_kernel: ~4,400 shared-memory wavefronts per row).
 // ---------------------------------------------------------------------------
-constexpr int PF_B = 8;
+#ifndef KLE_PF_B
+#define KLE_PF_B 12
+#endif
+constexpr int PF_B = KLE_PF_B;  // panel width (columns per rank-PF_B update)
 constexpr int PF_NT = 512;
 constexpr int PF_PT = 160;  // panel threads (>= n + PF_B, a multiple of 32)
 constexpr int PF_M = 16;    // trailing entries per thread (8 threads per folded row pair)
