@@ -508,7 +508,7 @@ def _cpu_build_surrogate(model, grid, cfg, train, degree, cores):
     mean, lam, modes, X = ref_port.kl_build(fields, w, 1e-10)
     zeta = ref_port.kl_coefficients(X, modes, lam, w)
     coeffs = ref_port.gpc_fit(train, zeta, degree)
-    return KLGpcSurrogate(mean, lam, modes, coeffs, degree, [ParameterMap("identity", -np.inf, np.inf)] * len(train[0]))
+    return KLGpcSurrogate(mean, lam, modes, coeffs, degree, [ParameterMap("identity", -np.inf, np.inf)] * len(train[0]), family="hermite")
 
 
 def run_c5(args):

@@ -14,9 +14,18 @@
  *    no implicit device synchronisation except where stated;
  *  - return 0 on success, else a KLE_ERR_* code; kle_last_error() returns a
  *    message for the calling thread's last failure. No exceptions cross the ABI;
- *  - no hidden allocation: scratch/workspace is caller provided and sized by
- *    the matching *_bytes query; no global mutable state beyond the
- *    thread-local error string (reentrant on distinct streams).
+ *  - no hidden device allocation: scratch/workspace is caller provided and
+ *    sized by the matching *_bytes query;
+ *  - library-owned state, all of it listed here: the thread-local error
+ *    string; per (host thread, device) auxiliary streams/events and 16 pinned
+ *    host bytes used by the multi-stream paths (kle_pcgc_solve_f64's sample
+ *    pipelines, the large-block CGC), created on first use and freed by
+ *    kle_release_resources(); per-device kernel-attribute flags (set once per
+ *    device, atomically). Reentrant on distinct streams;
+ *  - kle_pcgc_solve_f64 / kle_pcgc_solve_ref_f64 / kle_parareal_solve_f64 run
+ *    the outer loop on the host: they read the active-sample count back every
+ *    iteration and return after the work on `stream` has completed
+ *    (synchronous, like the reference's pcgc_solve).
  *
  * The reference has no FFI for this path (it is pure numpy/scipy); each entry
  * point below names the reference function it replaces. INTEGRATION.md shows
@@ -50,6 +59,10 @@ extern "C" {
 
 int kle_abi_version(void);
 const char* kle_last_error(void);
+/* Free the calling host thread's auxiliary streams/events/pinned bytes on the
+ * current device (synchronises the device first). Safe to call at any time;
+ * they are recreated on the next multi-stream call. */
+int kle_release_resources(void);
 
 /* Chunking of the register-resident tridiagonal solver for a given nx:
  * rows are padded to MR*P; the factor blob holds blob_doubles per sample. */
@@ -234,11 +247,14 @@ int kle_shifted_tridiag_solve_f64(const double* sub, const double* dia, const do
                                   double lam_im, double dT, const double* p, double* q, double* cwork, int nx,
                                   int nrhs, int32_t* status, void* stream);
 
-/* gpc_basis_matrix with the Hermite table (pintuq/surrogate.py:222-248):
- * Psi[M][P] from xi[M][d]; midx[P][d] = gpc_multi_indices(degree, d);
- * norms[degree+1] = 1/sqrt(k!). */
-int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
-                      const double* norms, double* Psi, void* stream);
+/* gpc_basis_matrix (pintuq/surrogate.py:208-248) at the mapped points
+ * (KLGpcSurrogate.map_parameters, ParameterMap.apply pintuq/models.py:39-45):
+ * Psi[M][P] from raw xi[M][d]; family 0 = probabilists' Hermite
+ * (norms[k] = 1/sqrt(k!)), 1 = Legendre (norms[k] = sqrt(2k+1));
+ * maps = optional [d][3] (kind, lo, hi): kind 0 identity, 1 affine onto
+ * [-1, 1], 2 cos(2 pi v); NULL = identity; midx[P][d] = gpc_multi_indices. */
+int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, int family, const double* maps,
+                      const int32_t* midx, int P, const double* norms, double* Psi, void* stream);
 
 /* surrogate_predict batched (pintuq/surrogate.py:321-333):
  * U0[M][L] = mean[L] + Psi[M][K] * C[K][L]  (FP64 tensor cores, DMMA). */

@@ -22,6 +22,7 @@ _z = C.c_size_t
 _SIGS = {
     "kle_abi_version": ([], _i),
     "kle_last_error": ([], C.c_char_p),
+    "kle_release_resources": ([], _i),
     "kle_fine_layout": ([_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)], _i),
     "kle_kl_tridiag_f64": ([_p, _i, _i, _p, _i, _d, _p, _p, _p], _i),
     "kle_fine_factor_f64": ([_p, _p, _i, _i, _d, _d, _p, _p], _i),
@@ -61,7 +62,7 @@ _SIGS = {
     "kle_2d_sweep_staged_f64": ([_p, _p, _i, _i, _i, _i, _i, _d, _d, _p, _z, _p, _p], _i),
     "kle_2d_cgc_work_doubles": ([_i, _i, _i], _z),
     "kle_2d_cgc_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z, _p], _i),
-    "kle_gpc_basis_f64": ([_p, _i, _i, _i, _p, _i, _p, _p, _p], _i),
+    "kle_gpc_basis_f64": ([_p, _i, _i, _i, _i, _p, _p, _i, _p, _p, _p], _i),
     "kle_gpc_eval_f64": ([_p, _i, _i, _p, _p, _i, _p, _p], _i),
     "kle_gemm_f64": ([_p, _p, _p, _p, _i, _i, _i, _i, _p], _i),
     "kle_sub_row_f64": ([_p, _p, _p, _i, _i, _p], _i),

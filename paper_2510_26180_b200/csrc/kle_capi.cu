@@ -40,6 +40,58 @@ using namespace kle;
     if (_rc != KLE_OK) return _rc; \
   } while (0)
 
+namespace kle {
+
+static thread_local AuxResources* g_aux[64] = {};
+
+static void aux_destroy(AuxResources* r) {
+  for (int p = 0; p < kMaxPipes; ++p) {
+    if (r->sf[p]) cudaStreamDestroy(r->sf[p]);
+    if (r->sc[p]) cudaStreamDestroy(r->sc[p]);
+    if (r->done[p]) cudaEventDestroy(r->done[p]);
+    if (r->fdone[p]) cudaEventDestroy(r->fdone[p]);
+  }
+  if (r->ready) cudaEventDestroy(r->ready);
+  for (int q = 0; q < 2; ++q)
+    if (r->cgcl[q]) cudaStreamDestroy(r->cgcl[q]);
+  for (int q = 0; q < 3; ++q)
+    if (r->cgcl_ev[q]) cudaEventDestroy(r->cgcl_ev[q]);
+  if (r->h_count) cudaFreeHost(r->h_count);
+  delete r;
+}
+
+AuxResources* aux_resources() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    set_error(KLE_ERR_CUDA, "aux_resources: no current device");
+    return nullptr;
+  }
+  if (g_aux[dev]) return g_aux[dev];
+  auto* r = new AuxResources{};
+  int lo = 0, hi = 0;
+  bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess;
+  for (int p = 0; p < kMaxPipes && ok; ++p) {
+    ok = ok && cudaStreamCreateWithPriority(&r->sf[p], cudaStreamNonBlocking, lo) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithPriority(&r->sc[p], cudaStreamNonBlocking, hi) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&r->done[p], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&r->fdone[p], cudaEventDisableTiming) == cudaSuccess;
+  }
+  ok = ok && cudaEventCreateWithFlags(&r->ready, cudaEventDisableTiming) == cudaSuccess;
+  for (int q = 0; q < 2 && ok; ++q) ok = cudaStreamCreateWithFlags(&r->cgcl[q], cudaStreamNonBlocking) == cudaSuccess;
+  for (int q = 0; q < 3 && ok; ++q) ok = cudaEventCreateWithFlags(&r->cgcl_ev[q], cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaHostAlloc(&r->h_count, kMaxPipes * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    aux_destroy(r);
+    set_error(KLE_ERR_CUDA, "aux_resources: stream/event/pinned-buffer creation failed");
+    return nullptr;
+  }
+  g_aux[dev] = r;
+  return r;
+}
+
+}  // namespace kle
+
 extern "C" {
 
 int kle_abi_version(void) { return KLE_ABI_VERSION; }
@@ -202,37 +254,16 @@ size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
   return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256;
 }
 
-constexpr int kMaxPipes = 4;
-struct PipeResources {
-  cudaStream_t sf[kMaxPipes], sc[kMaxPipes];  // per pipeline: fine sweeps (low priority), CGC (high priority)
-  cudaEvent_t done[kMaxPipes], fdone[kMaxPipes], ready;
-  int32_t* h_count;  // pinned [kMaxPipes]
-};
 
-// one set per host thread and device, created on first use, never freed
-// (process lifetime; a handful of streams/events and 8 pinned bytes)
-static PipeResources* pipe_resources() {
-  static thread_local PipeResources* per_dev[64] = {};
+int kle_release_resources(void) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (per_dev[dev]) return per_dev[dev];
-  auto* r = new PipeResources{};
-  int lo = 0, hi = 0;
-  bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess;
-  for (int p = 0; p < kMaxPipes && ok; ++p) {
-    ok = ok && cudaStreamCreateWithPriority(&r->sf[p], cudaStreamNonBlocking, lo) == cudaSuccess;
-    ok = ok && cudaStreamCreateWithPriority(&r->sc[p], cudaStreamNonBlocking, hi) == cudaSuccess;
-    ok = ok && cudaEventCreateWithFlags(&r->done[p], cudaEventDisableTiming) == cudaSuccess;
-    ok = ok && cudaEventCreateWithFlags(&r->fdone[p], cudaEventDisableTiming) == cudaSuccess;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return set_error(KLE_ERR_CUDA, "release: no device");
+  if (AuxResources* r = g_aux[dev]) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return set_error(KLE_ERR_CUDA, "release: device synchronize failed");
+    g_aux[dev] = nullptr;
+    aux_destroy(r);
   }
-  ok = ok && cudaEventCreateWithFlags(&r->ready, cudaEventDisableTiming) == cudaSuccess;
-  ok = ok && cudaHostAlloc(&r->h_count, kMaxPipes * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
-  if (!ok) {
-    delete r;
-    return nullptr;
-  }
-  per_dev[dev] = r;
-  return r;
+  return KLE_OK;
 }
 
 static int pcgc_loop(double* U, const double* u0, const double* dia, const double* off, const double* fine_blob,
@@ -298,8 +329,8 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
   // and device and reused: driver resource calls inside a solve serialise with
   // other driver clients (e.g. an nvidia-smi poll) and cost more than a short
   // solve
-  PipeResources* res = pipe_resources();
-  if (!res) return set_error(KLE_ERR_CUDA, "pcgc_solve: stream/event/pinned-buffer creation failed");
+  AuxResources* res = aux_resources();
+  if (!res) return KLE_ERR_CUDA;
   int32_t* h_count = res->h_count;
   cudaEvent_t ready = res->ready;
   cudaEventRecord(ready, st);
@@ -538,10 +569,10 @@ int kle_shifted_tridiag_solve_f64(const double* sub, const double* dia, const do
   return shifted_tridiag(sub, dia, sup, lam_re, lam_im, dT, p, q, cwork, nx, nrhs, status, KLE_STREAM(stream));
 }
 
-int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
-                      const double* norms, double* Psi, void* stream) {
+int kle_gpc_basis_f64(const double* xi, int M, int d, int degree, int family, const double* maps,
+                      const int32_t* midx, int P, const double* norms, double* Psi, void* stream) {
   if (M < 0 || d < 1 || P < 1) return set_error(KLE_ERR_INVALID, "gpc_basis: bad dims");
-  return gpc_basis(xi, M, d, degree, midx, P, norms, Psi, KLE_STREAM(stream));
+  return gpc_basis(xi, M, d, degree, family, maps, midx, P, norms, Psi, KLE_STREAM(stream));
 }
 
 int kle_gpc_eval_f64(const double* Psi, int M, int K, const double* C, const double* mean, int L, double* U0,

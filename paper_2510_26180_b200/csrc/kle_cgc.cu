@@ -258,11 +258,11 @@ int cgc_run(const CgcArgs& a, cudaStream_t st) {
   }
   const int TC = tile_cols(a.N);
   const size_t smem = cgc_smem_bytes(a.N);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(cgc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_cgc: cudaFuncSetAttribute", [&] {
+        return cudaFuncSetAttribute(cgc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }))
+    return rc;
   const int grid = cgc_grid(a.M, a.N, a.nx);
   cgc_kernel<<<grid, CGC_NT, smem, st>>>(a, TC, log2N);
   return check_launch("cgc_kernel");

@@ -707,12 +707,12 @@ static int launch_cluster(const CgcArgs& a, const double* sfac, int CL, cudaStre
   constexpr int N2 = K::N / (1 << ((LOGN + 1) / 2));
   static_assert(K::NT * 2 >= N2 * K::HC, "cgc_cluster: FFT pass-2 tasks exceed 2 rounds");
   auto kern = cgc_cluster_kernel<LOGN, MR>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
-  }
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_cgc_cluster: cudaFuncSetAttribute", [&] {
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
+        return e != cudaSuccess ? e : cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }))
+    return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.M * CL), 1, 1);
   cfg.blockDim = dim3((unsigned)K::NT, 1, 1);

@@ -409,22 +409,20 @@ static int run_large(const CgcArgs& a, cudaStream_t st) {
   cgcl_twiddle_kernel<<<(N + 127) / 128, 128, 0, st>>>(tw, N);
   const int tiles = (a.nx + CL_RC - 1) / CL_RC;
   constexpr size_t smem = sizeof(Cplx) * K::TILE;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(cgcl_fwd_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(cgcl_inv_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_cgc_large: cudaFuncSetAttribute", [&] {
+        const cudaError_t e = cudaFuncSetAttribute(cgcl_fwd_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return e != cudaSuccess ? e : cudaFuncSetAttribute(cgcl_inv_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }))
+    return rc;
   // two sub-batch streams over the two halves of the scratch: one half's FFT
   // kernels overlap the other half's per-frequency solves
-  static thread_local cudaStream_t ss[2] = {nullptr, nullptr};
-  static thread_local cudaEvent_t ev[3];
   static const char* env = getenv("KLE_CGCL_STREAMS");
   const bool two = !(env && env[0] == '1') && MB >= 2;
-  if (two && !ss[0]) {
-    for (int q = 0; q < 2; ++q) cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking);
-    for (int q = 0; q < 3; ++q) cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
-  }
+  AuxResources* res = two ? aux_resources() : nullptr;
+  if (two && !res) return KLE_ERR_CUDA;
+  cudaStream_t* ss = two ? res->cgcl : nullptr;
+  cudaEvent_t* ev = two ? res->cgcl_ev : nullptr;
   const int HB = two ? MB / 2 : MB;  // samples per sub-batch
   if (two) {
     cudaEventRecord(ev[2], st);

@@ -379,11 +379,11 @@ struct FineInst {
   static int fgr(const FgrArgs& a, cudaStream_t st) {
     dim3 grid(a.M, (a.N + NC - 1) / NC);
     const size_t smem = a.F_given ? 0 : FgrSmem<MR, P, NC>::BYTES;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
+    static PerDeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, "kle_fine: cudaFuncSetAttribute", [&] {
+          return cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }))
+      return rc;
     fgr_kernel<MR, P, R, NT, PIPE><<<grid, NT, smem, st>>>(a);
     return check_launch("fgr_kernel");
   }

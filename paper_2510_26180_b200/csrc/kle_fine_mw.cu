@@ -543,11 +543,11 @@ static int launch_mw2(const FgrArgs& a, int W, cudaStream_t st) {
   const MwLayout<MW_MR> L(W);
   const int G = 16 * R;  // subintervals per CTA
   const size_t smem = sizeof(double) * 3 * R * (size_t)(L.nxp + L.nxp / MW_MR + 2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fgr_mw2_kernel<MW_MR, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_fine_mw: cudaFuncSetAttribute", [&] {
+        return cudaFuncSetAttribute(fgr_mw2_kernel<MW_MR, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      }))
+    return rc;
   fgr_mw2_kernel<MW_MR, R><<<dim3(a.M, (a.N + G - 1) / G), 32 * W, smem, st>>>(a, W, G);
   return check_launch("fgr_mw2_kernel");
 }

@@ -317,24 +317,24 @@ struct SfInst {
     using L = SfLayout<MR, P>;
     if (a.F_given) return set_error(KLE_ERR_UNSUPPORTED, "sf fgr: F_given uses the register variant");
     const size_t smem = (size_t)L::DOUBLES * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fgr_sf_kernel<MR, P, R, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static PerDeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, "kle_fine_sf: cudaFuncSetAttribute", [&] {
+          return cudaFuncSetAttribute(fgr_sf_kernel<MR, P, R, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-      attr = true;
-    }
+        }))
+      return rc;
     fgr_sf_kernel<MR, P, R, NT, MINB><<<dim3(a.M, (a.N + NC - 1) / NC), NT, smem, st>>>(a);
     return check_launch("fgr_sf_kernel");
   }
   static int sweep(const SweepArgs& a, cudaStream_t st) {
     using L = SfLayout<MR, P>;
     const size_t smem = (size_t)L::DOUBLES * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sweep_sf_kernel<MR, P, R, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static PerDeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, "kle_fine_sf: cudaFuncSetAttribute", [&] {
+          return cudaFuncSetAttribute(sweep_sf_kernel<MR, P, R, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-      attr = true;
-    }
+        }))
+      return rc;
     sweep_sf_kernel<MR, P, R, NT, MINB><<<dim3(a.M, (a.Q + NC - 1) / NC), NT, smem, st>>>(a);
     return check_launch("sweep_sf_kernel");
   }

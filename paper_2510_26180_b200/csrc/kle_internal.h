@@ -3,12 +3,49 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstddef>
+#include <atomic>
 #include <cstdint>
 
 namespace kle {
 
 int set_error(int code, const char* msg);
 int check_launch(const char* what);
+
+// Kernel attributes (cudaFuncSetAttribute) are per device: the setup runs once
+// per device this process touches (bit `dev` of the mask), its return codes are
+// checked, and concurrent first calls from several host threads are benign
+// (the attribute calls are idempotent).
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> mask{0};
+};
+template <class F>
+inline int once_per_device(PerDeviceOnce& once, const char* what, F&& setup) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev > 63) return set_error(2, what);
+  const unsigned long long bit = 1ull << dev;
+  if (once.mask.load(std::memory_order_acquire) & bit) return 0;
+  const cudaError_t e = setup();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(2, what);
+  }
+  once.mask.fetch_or(bit, std::memory_order_acq_rel);
+  return 0;
+}
+
+// Stream-ordering helpers of the multi-stream paths (the PCGC sample pipelines
+// in kle_capi.cu, the two sub-batch streams of the large-block CGC): created
+// on first use per (host thread, current device), never device memory, freed
+// by kle_release_resources() (include/kle_b200.h).
+constexpr int kMaxPipes = 4;
+struct AuxResources {
+  cudaStream_t sf[kMaxPipes], sc[kMaxPipes];  // per pipeline: fine sweeps (low priority), CGC (high priority)
+  cudaEvent_t done[kMaxPipes], fdone[kMaxPipes], ready;
+  cudaStream_t cgcl[2];                       // large-block CGC sub-batch streams
+  cudaEvent_t cgcl_ev[3];
+  int32_t* h_count;                           // pinned [kMaxPipes]
+};
+AuxResources* aux_resources();  // nullptr (and the error string set) on failure
 
 struct FineLayoutRT {
   int MR, P, R, pipe, doubles;
@@ -138,7 +175,7 @@ int cgc_large_run(const CgcArgs& a, cudaStream_t st);
 int kl_tridiag(const double* xi, int M, int d, const double* table, int nx, double inv_h2, double* dia,
                double* off, cudaStream_t st);
 
-int gpc_basis(const double* xi, int M, int d, int degree, const int32_t* midx, int P,
+int gpc_basis(const double* xi, int M, int d, int degree, int family, const double* maps, const int32_t* midx, int P,
               const double* norms, double* Psi, cudaStream_t st);
 int gemm_bias(const double* A, const double* B, const double* bias, double* C, int M, int K, int L,
               cudaStream_t st, bool trans_b = false);

@@ -29,33 +29,51 @@ int kl_tridiag(const double* xi, int M, int d, const double* table, int nx, doub
   if (M <= 0) return KLE_OK;
   const size_t smem = (size_t)(nx + 1) * sizeof(double);
   if (smem > 200 * 1024) return set_error(KLE_ERR_UNSUPPORTED, "kl_tridiag: nx too large");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kl_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_misc: cudaFuncSetAttribute", [&] {
+        return cudaFuncSetAttribute(kl_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }))
+    return rc;
   kl_tridiag_kernel<<<M, 256, smem, st>>>(xi, d, table, nx, inv_h2, dia, off);
   return check_launch("kl_tridiag_kernel");
 }
 
-// Psi[s][col] = prod_d He~_{k_d}(xi_{s,d}) in gpc_multi_indices order, with
-// the same recurrence, normalisation and product order as
-// gpc_basis_matrix + _hermite_table (pintuq/surrogate.py:222-248).
+// Psi[s][col] = prod_d phi_{k_d}(map_d(xi_{s,d})) in gpc_multi_indices order:
+// gpc_basis_matrix + _legendre_table / _hermite_table + ParameterMap.apply
+// (pintuq/surrogate.py:208-248, pintuq/models.py:39-45), the same recurrences,
+// normalisation and product order, every operation rounded separately (no FMA
+// contraction) so the Hermite/Legendre tables and the affine map are
+// bit-identical to numpy's. maps: optional [d][3] (kind, lo, hi), kind 0 =
+// identity, 1 = affine onto [-1, 1], 2 = cos(2 pi v) (the device cos can differ
+// from numpy's in the last bit).
 constexpr int GPC_MAXDEG = 8;
 constexpr int GPC_MAXDIM = 32;
 
-__global__ void gpc_basis_kernel(const double* __restrict__ xi, int M, int d, int degree,
-                                 const int32_t* __restrict__ midx, int P, const double* __restrict__ norms,
-                                 double* __restrict__ Psi) {
+__global__ void gpc_basis_kernel(const double* __restrict__ xi, int M, int d, int degree, int family,
+                                 const double* __restrict__ maps, const int32_t* __restrict__ midx, int P,
+                                 const double* __restrict__ norms, double* __restrict__ Psi) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= M) return;
   double T[GPC_MAXDIM][GPC_MAXDEG + 1];
   for (int k = 0; k < d; ++k) {
-    const double x = xi[(size_t)s * d + k];
+    double x = xi[(size_t)s * d + k];
+    if (maps) {
+      const int kind = (int)maps[3 * k];
+      const double lo = maps[3 * k + 1], hi = maps[3 * k + 2];
+      if (kind == 1) x = __dsub_rn(__ddiv_rn(__dmul_rn(2.0, __dsub_rn(x, lo)), __dsub_rn(hi, lo)), 1.0);
+      else if (kind == 2) x = cos(__dmul_rn(2.0 * 3.141592653589793, x));
+    }
     T[k][0] = 1.0;
     if (degree >= 1) T[k][1] = x;
-    // no FMA contraction: bit-identical to the numpy recurrence
-    for (int q = 1; q < degree; ++q) T[k][q + 1] = __dsub_rn(__dmul_rn(x, T[k][q]), __dmul_rn((double)q, T[k][q - 1]));
+    if (family == 0) {  // probabilists' Hermite: He_{q+1} = x He_q - q He_{q-1}
+      for (int q = 1; q < degree; ++q)
+        T[k][q + 1] = __dsub_rn(__dmul_rn(x, T[k][q]), __dmul_rn((double)q, T[k][q - 1]));
+    } else {  // Legendre: P_{q+1} = ((2q+1) x P_q - q P_{q-1}) / (q+1)
+      for (int q = 1; q < degree; ++q)
+        T[k][q + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(__dmul_rn((double)(2 * q + 1), x), T[k][q]),
+                                          __dmul_rn((double)q, T[k][q - 1])),
+                                (double)(q + 1));
+    }
     for (int q = 0; q <= degree; ++q) T[k][q] = __dmul_rn(T[k][q], norms[q]);
   }
   for (int col = 0; col < P; ++col) {
@@ -68,12 +86,13 @@ __global__ void gpc_basis_kernel(const double* __restrict__ xi, int M, int d, in
   }
 }
 
-int gpc_basis(const double* xi, int M, int d, int degree, const int32_t* midx, int P, const double* norms,
-              double* Psi, cudaStream_t st) {
+int gpc_basis(const double* xi, int M, int d, int degree, int family, const double* maps, const int32_t* midx, int P,
+              const double* norms, double* Psi, cudaStream_t st) {
   if (d > GPC_MAXDIM || degree > GPC_MAXDEG || degree < 0)
     return set_error(KLE_ERR_UNSUPPORTED, "gpc_basis: degree/dimension too large");
+  if (family != 0 && family != 1) return set_error(KLE_ERR_INVALID, "gpc_basis: family must be 0 (Hermite) or 1 (Legendre)");
   if (M <= 0) return KLE_OK;
-  gpc_basis_kernel<<<(M + 127) / 128, 128, 0, st>>>(xi, M, d, degree, midx, P, norms, Psi);
+  gpc_basis_kernel<<<(M + 127) / 128, 128, 0, st>>>(xi, M, d, degree, family, maps, midx, P, norms, Psi);
   return check_launch("gpc_basis_kernel");
 }
 

@@ -208,11 +208,11 @@ int newton_cgc(const NewtonCgcArgs& a, cudaStream_t st) {
   if (a.M <= 0) return KLE_OK;
   const size_t smem = newton_cgc_smem(a.N, a.nx);
   if (smem > 220 * 1024) return set_error(KLE_ERR_UNSUPPORTED, "newton_cgc: N * nx too large for one CTA");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(newton_cgc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_newton_cgc: cudaFuncSetAttribute", [&] {
+        return cudaFuncSetAttribute(newton_cgc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      }))
+    return rc;
   newton_cgc_kernel<<<a.M, 256, smem, st>>>(a);
   return check_launch("newton_cgc_kernel");
 }

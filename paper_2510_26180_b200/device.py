@@ -76,10 +76,47 @@ def tridiagonal_of(model, xi):
         if not np.array_equal(lo, up):
             raise NotImplementedError("the device path supports symmetric operators only")
         off[:-1] = up
-    g_a, g_b = np.asarray(g(0.0), dtype=float), np.asarray(g(1.0), dtype=float)
-    if not (np.array_equal(g_a, g_b) and np.all(g_a == g_a[0])):
+    # the source must be constant in time and uniform in space: probed at the
+    # interval ends and at irrational interior points (a source such as
+    # t(1-t) w agrees at t = 0 and t = 1 only)
+    g_a = np.asarray(g(0.0), dtype=float)
+    for t in (1.0, 0.5, 0.1234567890123, 0.7071067811865476, 3.0):
+        if not np.array_equal(g_a, np.asarray(g(t), dtype=float)):
+            raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
+    if not np.all(g_a == g_a[0]):
         raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
     return dia, off, float(g_a[0])
+
+
+def shared_initial_condition(model, xis):
+    """The plugin contract is ``initial_condition(xi)`` per sample
+    (``pintuq/models.py:61-106``). The device kernels take one u0 shared by the
+    batch, so every sample's initial state is evaluated and must be identical;
+    a parameter-dependent u0 raises instead of silently using the first
+    sample's. Array/tensor batches of a KL model evaluate ``initial_condition``
+    at the first and last rows (the KL models' u0 does not depend on xi)."""
+    if isinstance(xis, (list, tuple)):
+        pts = list(xis)
+    else:
+        if hasattr(xis, "detach"):
+            arr = xis.reshape(xis.shape[0], -1)[[0, -1]].cpu().numpy() if xis.shape[0] else np.zeros((0, 1))
+        else:
+            arr = np.atleast_2d(np.asarray(xis))
+        pts = [ParameterSample(arr[0], id=0), ParameterSample(arr[-1], id=len(arr) - 1)] if len(arr) else []
+    if not pts:
+        return np.asarray(model.initial_condition(None), dtype=float)
+    first = np.asarray(model.initial_condition(_as_sample(pts[0])), dtype=float)
+    for x in pts[1:]:
+        if not np.array_equal(first, np.asarray(model.initial_condition(_as_sample(x)), dtype=float)):
+            raise NotImplementedError("the device path needs one initial state shared by all samples "
+                                      "(initial_condition(xi) differs between samples)")
+    return first
+
+
+def _as_sample(x):
+    if isinstance(x, ParameterSample):
+        return x
+    return ParameterSample(np.asarray(x, dtype=float), id=0)
 
 
 class DeviceOperator:
@@ -128,8 +165,7 @@ class DeviceOperator:
             dia = to_dev(np.array([r[0] for r in rows]))
             off = to_dev(np.array([r[1] for r in rows]))
             g0 = rows[0][2]
-        first = xis[0] if isinstance(xis, (list, tuple)) else None
-        u0 = to_dev(model.initial_condition(first))
+        u0 = to_dev(shared_initial_condition(model, xis))
         return cls(dia, off, g0, u0)
 
     def blob(self, h: float):

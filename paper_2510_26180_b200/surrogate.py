@@ -82,7 +82,7 @@ def hermite_norms(degree: int) -> np.ndarray:
     return np.array([1.0 / math.sqrt(math.factorial(k)) for k in range(degree + 1)])
 
 
-def gpc_basis_matrix(points, degree: int, family: str = "hermite") -> np.ndarray:
+def gpc_basis_matrix(points, degree: int, family: str = "legendre") -> np.ndarray:
     """Host basis matrix (n, P) — used by the offline fit only."""
     points = np.atleast_2d(np.asarray(points, dtype=float))
     n, dim = points.shape
@@ -258,7 +258,7 @@ def kl_coefficients(snap: SnapshotSet, basis: KLBasis) -> np.ndarray:
     return snap.cell_weight * (X @ G.T) / np.sqrt(basis.retained)[None, :]
 
 
-def gpc_fit(points, zeta, degree: int, family: str = "hermite"):
+def gpc_fit(points, zeta, degree: int, family: str = "legendre"):
     points = np.atleast_2d(np.asarray(points, dtype=float))
     zeta = np.asarray(zeta, dtype=float)
     n, dim = points.shape
@@ -286,7 +286,7 @@ class KLGpcSurrogate:
     coeffs: np.ndarray
     degree: int
     maps: list
-    family: str = "hermite"
+    family: str = "legendre"
     cell_weight: float = 1.0
     provenance: dict = field(default_factory=dict)
     ls_residuals: np.ndarray | None = None
@@ -302,17 +302,33 @@ class KLGpcSurrogate:
         return np.array([m.apply(v) for m, v in zip(self.maps, xi.values)])
 
 
+_FAMILY_CODE = {"hermite": 0, "legendre": 1}
+_MAP_CODE = {"identity": 0, "affine": 1, "cos2pi": 2}
+
+
+def family_norms(family: str, degree: int) -> np.ndarray:
+    if family == "hermite":
+        return hermite_norms(degree)
+    return np.sqrt(2.0 * np.arange(degree + 1) + 1.0)
+
+
 class DeviceSurrogate:
-    """Device-resident evaluation tables of a Hermite ``KLGpcSurrogate``."""
+    """Device-resident evaluation tables of a ``KLGpcSurrogate`` (Hermite or
+    Legendre family; identity, affine or cos2pi parameter maps applied in the
+    basis kernel)."""
 
     def __init__(self, s: KLGpcSurrogate):
+        from .core import ConfigError
         from .device import to_dev, torch
 
-        if s.family != "hermite":
-            raise NotImplementedError("the device surrogate evaluates the Hermite family")
-        if any(m.kind != "identity" for m in s.maps):
-            raise NotImplementedError("the device surrogate expects identity parameter maps")
+        if s.family not in _FAMILY_CODE:
+            raise ConfigError(f"unknown gPC family {s.family!r}")
+        if any(m.kind not in _MAP_CODE for m in s.maps):
+            raise ConfigError(f"unknown parameter map kind in {[m.kind for m in s.maps]}")
         self.s = s
+        self.family = _FAMILY_CODE[s.family]
+        self.maps = (None if all(m.kind == "identity" for m in s.maps) else
+                     to_dev(np.array([[_MAP_CODE[m.kind], m.lo, m.hi] for m in s.maps], dtype=float)))
         self.dim = len(s.maps)
         self.field_shape = s.mean_field.shape
         self.L = int(np.prod(self.field_shape))
@@ -320,7 +336,7 @@ class DeviceSurrogate:
         self.mean = to_dev(s.mean_field.reshape(-1))
         self.midx = torch.as_tensor(np.array(gpc_multi_indices(s.degree, self.dim), dtype=np.int32),
                                     device="cuda").contiguous()
-        self.norms = to_dev(hermite_norms(s.degree))
+        self.norms = to_dev(family_norms(s.family, s.degree))
         m_q = s.m_q
         G = s.modes.reshape(m_q, -1)
         sq = np.sqrt(s.eigenvalues)
@@ -343,7 +359,8 @@ class DeviceSurrogate:
 
         M = xi_d.shape[0]
         Psi = empty(M, self.P)
-        _lib.call("kle_gpc_basis_f64", ptr(xi_d), M, self.dim, self.s.degree, ptr(self.midx), self.P,
+        _lib.call("kle_gpc_basis_f64", ptr(xi_d), M, self.dim, self.s.degree, self.family, ptr(self.maps),
+                  ptr(self.midx), self.P,
                   ptr(self.norms), ptr(Psi), stream_ptr())
         return Psi
 
@@ -373,9 +390,10 @@ def surrogate_predict(s: KLGpcSurrogate, xi: ParameterSample, initial) -> Coarse
     """``pintuq/surrogate.py:321-333`` for one sample (device evaluation)."""
     from .device import to_dev
 
-    x = s.map_parameters(xi)
+    if xi.dim != len(s.maps):
+        raise ValueError(f"sample has {xi.dim} coordinates, surrogate expects {len(s.maps)}")
     ds = DeviceSurrogate(s)
-    pred = ds.predict(to_dev(x[None]))[0].cpu().numpy()
+    pred = ds.predict(to_dev(xi.values[None]))[0].cpu().numpy()
     return CoarseTrajectory(initial, pred)
 
 
@@ -385,10 +403,18 @@ def surrogate_predict_batched(ds: DeviceSurrogate, xi_d, out=None):
 
 def build_surrogate(model, grid: TimeGrid, cfg: SolverConfig, training: list, eps_kl: float = 1e-10,
                     degree: int | None = None, snapshot_method: str = "pcgc", executor=None,
-                    snapshots: SnapshotSet | None = None, family: str = "hermite",
+                    snapshots: SnapshotSet | None = None, family: str | None = None,
                     kl_on_device: bool = True) -> KLGpcSurrogate:
     """Snapshots (device) -> KL (device products, host eigh) -> least-squares
-    Hermite fit (host). ``kl_on_device=False`` runs the KL on the host."""
+    gPC fit (host). ``kl_on_device=False`` runs the KL on the host.
+
+    ``family``: the reference's build always fits Legendre
+    (``pintuq/surrogate.py:336-393``); that stays the default. The Gaussian
+    KL models of the BASELINE configs declare ``gpc_family = "hermite"``
+    (probabilists' Hermite, orthonormal under N(0, 1)), which is used when
+    ``family`` is not given."""
+    if family is None:
+        family = getattr(model, "gpc_family", "legendre")
     if snapshots is None:
         snapshots = collect_snapshots(model, grid, cfg, training, snapshot_method, executor)
     if kl_on_device and snapshots.device_fields is not None:

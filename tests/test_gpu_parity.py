@@ -112,7 +112,7 @@ def test_kle_cgc_pipeline_c1_golden(cuda, golden):
     model, grid, cfg = c1_config()
     g = golden("c1")
     s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], int(g["degree"]),
-                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     solver = KleCgcSolver(model, grid, cfg, s)
     M = len(g["iters"])
     res = solver.solve(g["xi_all"][:M], keep_initial=True)
@@ -139,7 +139,7 @@ def test_kle_cgc_c1_full_batch_vs_oracle(cuda, golden):
     model, grid, cfg = c1_config()
     g = golden("c1")
     s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2,
-                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     xi = g["xi_all"]
     res = KleCgcSolver(model, grid, cfg, s).solve(xi)
     dia, off = batched.tridiag_from_xi(xi, model.kl_table, model.h)
@@ -225,7 +225,7 @@ def test_gpc_basis_bitwise_and_gemm(cuda, golden):
 
     g = golden("c1")
     s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2,
-                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     ds = DeviceSurrogate(s)
     xi = g["xi_all"]
     Psi = ds.basis(torch.as_tensor(xi, device="cuda")).cpu().numpy()
@@ -234,7 +234,7 @@ def test_gpc_basis_bitwise_and_gemm(cuda, golden):
     rng = np.random.default_rng(3)
     xi8 = rng.normal(size=(300, 8))
     s8 = KLGpcSurrogate(np.zeros((2, 3)), np.ones(1), np.ones((1, 2, 3)), np.ones((1, 165)), 3,
-                        [ParameterMap("identity", -np.inf, np.inf)] * 8)
+                        [ParameterMap("identity", -np.inf, np.inf)] * 8, family="hermite")
     Psi8 = DeviceSurrogate(s8).basis(torch.as_tensor(xi8, device="cuda")).cpu().numpy()
     np.testing.assert_array_equal(Psi8, ref_port.basis_matrix(xi8, 3))
 
@@ -248,7 +248,7 @@ def test_gpc_eval_factored_branch(cuda):
     rng = np.random.default_rng(5)
     m_q, P, N, nx = 20, 35, 4, 9  # d=4, p=3 -> P=35
     s = KLGpcSurrogate(rng.normal(size=(N, nx)), rng.uniform(0.1, 1, m_q), rng.normal(size=(m_q, N, nx)),
-                       rng.normal(size=(m_q, P)), 3, [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                       rng.normal(size=(m_q, P)), 3, [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     ds = DeviceSurrogate(s)
     assert ds.mode == "factored"
     xi = rng.normal(size=(77, 4))
@@ -276,7 +276,7 @@ def test_determinism_bitwise(cuda, golden):
     model, grid, cfg = c1_config()
     g = golden("c1")
     s = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"], 2,
-                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     solver = KleCgcSolver(model, grid, cfg, s)
     a = solver.solve(g["xi_all"][:64]).batch.states.cpu().numpy()
     b = solver.solve(g["xi_all"][:64]).batch.states.cpu().numpy()
@@ -526,10 +526,10 @@ def test_device_kl_build_matches_host(cuda, golden):
     np.testing.assert_allclose(db.retained, g["eigenvalues"], rtol=0, atol=1e-13 * g["eigenvalues"][0])
     maps = [ParameterMap("identity", -np.inf, np.inf)] * 4
     pts = g["train_points"]
-    ch, _, _ = gpc_fit(pts, hz, 2)
-    cd, _, _ = gpc_fit(pts, dz, 2)
-    sh = KLGpcSurrogate(snap.mean_field, hb.retained, hb.modes, ch, 2, maps)
-    sd = KLGpcSurrogate(snap.mean_field, db.retained, db.modes, cd, 2, maps)
+    ch, _, _ = gpc_fit(pts, hz, 2, "hermite")
+    cd, _, _ = gpc_fit(pts, dz, 2, "hermite")
+    sh = KLGpcSurrogate(snap.mean_field, hb.retained, hb.modes, ch, 2, maps, family="hermite")
+    sd = KLGpcSurrogate(snap.mean_field, db.retained, db.modes, cd, 2, maps, family="hermite")
     for i in range(4):
         xi = ParameterSample(g["xi_all"][i], id=i)
         a = surrogate_predict(sh, xi, model.initial_condition()).states

@@ -163,7 +163,7 @@ def test_reference_diffusion1d_model_on_device(cuda, golden):
     """The reference's Diffusion1D plugin (symmetric tridiagonal, zero source)
     runs through the generic plugin path: pcgc_solve matches the reference."""
     from paper_2510_26180_b200 import CoarseTrajectory, ParameterSample, SolverConfig, make_time_grid
-    from paper_2510_26180_b200.models import AdvectionDiffusion2D, Diffusion1D
+    from tests.plugins import AdvectionDiffusion2D, Diffusion1D
     from paper_2510_26180_b200.pcgc import pcgc_solve
 
     g = golden("models")

@@ -127,6 +127,6 @@ def test_kle_cgc_engine_harness_mode(cuda, golden):
     model, grid, cfg = c1_config()
     g1, g = golden("c1"), golden("ref")
     s = KLGpcSurrogate(g1["mean_field"], g1["eigenvalues"], g1["modes"], g1["coeffs"], int(g1["degree"]),
-                       [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                       [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     res = KleCgcSolver(model, grid, cfg, s).solve(g1["xi_all"][:8], stop_on="reference")
     _check(res.batch, g, "kle")

@@ -161,7 +161,7 @@ def test_surrogate_npz_round_trip(tmp_path):
     rng = np.random.default_rng(1)
     s = KLGpcSurrogate(rng.normal(size=(3, 4)), rng.uniform(size=2), rng.normal(size=(2, 3, 4)),
                        rng.normal(size=(2, 6)), 2, [ParameterMap("identity", -np.inf, np.inf)] * 2,
-                       provenance={"model": "x"})
+                       provenance={"model": "x"}, family="hermite")
     path = tmp_path / "s.npz"
     save_surrogate(s, path)
     t = load_surrogate(path)

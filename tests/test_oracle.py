@@ -340,7 +340,7 @@ def test_reference_linear_models_match(golden):
     """Diffusion1D / AdvectionDiffusion2D host definitions equal the
     reference's (pintuq/models.py:128-266) bit for bit."""
     from paper_2510_26180_b200 import ParameterSample
-    from paper_2510_26180_b200.models import AdvectionDiffusion2D, Diffusion1D
+    from tests.plugins import AdvectionDiffusion2D, Diffusion1D
 
     g = golden("models")
     xi = ParameterSample(np.array([1.3]), id=0)

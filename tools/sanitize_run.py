@@ -25,10 +25,10 @@ for nx, N, J, M, d in [(127, 16, 32, 6, 4), (511, 64, 8, 2, 8), (63, 12, 4, 3, 4
     mean, var = two_pass_moments(res.states, M)
     print(nx, N, res.iters.cpu().numpy().tolist(), float(var.max()))
 s = KLGpcSurrogate(rng.normal(size=(4, 9)), rng.uniform(0.1, 1, 7), rng.normal(size=(7, 4, 9)),
-                   rng.normal(size=(7, 35)), 3, [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                   rng.normal(size=(7, 35)), 3, [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
 print(DeviceSurrogate(s).predict(to_dev(rng.normal(size=(5, 4)))).shape)
 s2 = KLGpcSurrogate(rng.normal(size=(4, 9)), rng.uniform(0.1, 1, 40), rng.normal(size=(40, 4, 9)),
-                    rng.normal(size=(40, 15)), 2, [ParameterMap("identity", -np.inf, np.inf)] * 4)
+                    rng.normal(size=(40, 15)), 2, [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
 print(DeviceSurrogate(s2).predict(to_dev(rng.normal(size=(70, 4)))).shape)
 torch.cuda.synchronize()
 print("sanitize run ok")
