@@ -1,25 +1,39 @@
 #!/usr/bin/env python
-"""Benchmark: KLE-CGC solves/s (and fine-step DOF-updates/s) on the
-BASELINE config-2 workload, one process per GPU.
+"""Benchmark: KLE-CGC solves/s (and fine-step DOF-updates/s) at fixed tol,
+one process per GPU.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2|c1|c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c4|c2|c1|c3|c5|burgers|allen-cahn]
 
-A step = one complete batched KLE-CGC solve of the rank's sample shard with
-the inputs resident in HBM: coefficient field, factorisation, Hermite-gPC
+Default workload: BASELINE configs[3] (c4), the metric's own "1/2/4/8 B200"
+sweep: the config-1 problem (nx 127, N 16, J 32, d 4, Hermite p 2 on the 3^4
+Gauss-Hermite grid) over M = 1,048,576 seeded samples, STRONG-scaled: the
+global sample ids are sharded in contiguous blocks across ranks
+(moments.shard_bounds), each rank solves its block, and the mean/variance
+are combined by the two-pass NCCL allreduce. ``--config c2`` runs configs[1]
+(nx 511, N 64, J 64, d 8, p 3 on 2,048 points, M = 65,536) the same way.
+
+``--gpus N`` with N > 1 outside torchrun re-launches this script under
+``torch.distributed.run`` with N ranks (127.0.0.1 rendezvous).
+
+A step = one complete batched KLE-CGC solve of the rank's shard with the
+inputs resident in HBM: coefficient field, factorisation, Hermite-gPC
 surrogate U0 (DMMA GEMM), the PCGC outer loop to tol with per-sample
-freezing, and the two-pass mean/variance (NCCL allreduce when N > 1).
-Weak scaling: every rank solves M samples (global ids rank*M ..).
+freezing, and the two-pass mean/variance. The surrogate is built once on
+rank 0 (device snapshots, untimed) and broadcast.
 
-Rank 0 prints one JSON line.
-``--impl reference`` times the CPU reference path (the oracle's per-sample
-restatement of pintuq, scipy SuperLU/LAPACK/pocketfft — bit-identical to
-the reference) on the same config over all host cores.
+``--impl reference`` times the CPU reference path (oracle/ref_port: the
+per-sample restatement of pintuq, scipy SuperLU/LAPACK/pocketfft,
+bit-identical to the reference's goldens) on a fixed subset of the same
+config's sample ids over all host cores (one BLAS thread per worker) and
+reports it in the same metric, unit and config.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -32,13 +46,18 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # BASELINE.json configs[1]: the metric's workload on one B200
-    "c2": dict(nx=511, d=8, N=64, J=64, M=65536, degree=3, train="gauss2048", alpha=1e-3, tol=1e-8),
-    # configs[0] (CPU oracle config) and configs[3] (scaling sweep of config 1)
-    "c1": dict(nx=127, d=4, N=16, J=32, M=256, degree=2, train="gh3", alpha=1e-3, tol=1e-8),
-    "c4": dict(nx=127, d=4, N=16, J=32, M=131072, degree=2, train="gh3", alpha=1e-3, tol=1e-8),
+    # BASELINE.json configs[3]: scaling sweep of config 1 (the metric's 1/2/4/8 B200 workload)
+    "c4": dict(index=3, nx=127, d=4, N=16, J=32, M=1048576, degree=2, train="gh3", alpha=1e-3, tol=1e-8,
+               cpu_subset=4096),
+    # configs[1]: config 1 scaled up, one B200
+    "c2": dict(index=1, nx=511, d=8, N=64, J=64, M=65536, degree=3, train="gauss2048", alpha=1e-3, tol=1e-8,
+               cpu_subset=512),
+    # configs[0]: the CPU oracle config
+    "c1": dict(index=0, nx=127, d=4, N=16, J=32, M=256, degree=2, train="gh3", alpha=1e-3, tol=1e-8,
+               cpu_subset=256),
 }
 METRIC = "fine-step DOF-updates/s and KLE-CGC solves/s at fixed tol, 1/2/4/8 B200"
+UNIT = "KLE-CGC solves/s"
 FLOPS_PER_DOF = 6.0   # rhs add 1, forward FMA 2, diagonal scale 1, back-substitution FMA 2
 SEED = 2718
 
@@ -49,11 +68,11 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c3", "c5", "burgers", "allen-cahn"])
-    p.add_argument("--samples", type=int, default=0, help="c3: evaluation samples (default 296 of the config's 4096)")
+    p.add_argument("--config", default="c4", choices=sorted(CONFIGS) + ["c3", "c5", "burgers", "allen-cahn"])
+    p.add_argument("--samples", type=int, default=0,
+                   help="total samples (default: the config's M; c3: evaluation samples, default 4096)")
     p.add_argument("--train", type=int, default=1024, help="c3: surrogate training samples (config: 1024)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU work of the baseline sample")
     return p.parse_args()
 
 
@@ -62,6 +81,22 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def maybe_relaunch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on this node (one process per GPU)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def problem(cfgname):
@@ -81,8 +116,33 @@ def problem(cfgname):
     return c, model, grid, cfg, train, eval_rng
 
 
+def total_samples(args, c):
+    return args.samples or c["M"]
+
+
 def eval_samples(eval_rng, M_total, d):
+    """Eval xi = eval_rng.normal(0, 1, (M_total, d)) row-major; sample id =
+    row (pintuq/experiments.py:271-272 stream split)."""
     return eval_rng.normal(0.0, 1.0, size=(M_total, d))
+
+
+def config_dict(args, c, world):
+    """The `config` object, identical in both arms for the same invocation."""
+    M = total_samples(args, c)
+    return {"workload": f"BASELINE configs[{c['index']}] ({args.config}): nx={c['nx']}, N={c['N']}, J={c['J']}, "
+                        f"d={c['d']}, Hermite p={c['degree']}, alpha={c['alpha']}, tol={c['tol']}, M={M}",
+            "global_samples": M, "n_ranks": world, "parallelism": f"sample-sharded x{world} (strong)",
+            "l2": "inputs larger than L2 (state 8*M*N*nx bytes)"}
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------------------
@@ -102,7 +162,7 @@ class ClockSampler:
     def _run(self):
         try:
             proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                     "--format=csv,noheader,nounits", "-lms", "200"],
+                                     "--format=csv,noheader,nounits", "-lms", "100"],
                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             return
@@ -133,6 +193,42 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+def share_from_rank0(builder, rank, use_dist):
+    """Rank 0 runs ``builder()``; the result is broadcast to every rank."""
+    import torch.distributed as dist
+
+    box = [builder() if rank == 0 else None]
+    if use_dist:
+        dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
+def build_and_share_surrogate(model, grid, cfg, train, degree, rank, use_dist):
+    """Rank 0 builds the surrogate (device snapshots + KL + Hermite fit) and
+    broadcasts it; every rank evaluates the identical tables."""
+    from paper_2510_26180_b200.core import ParameterSample
+    from paper_2510_26180_b200.surrogate import build_surrogate
+
+    def build():
+        training = [ParameterSample(x, id=i) for i, x in enumerate(train)]
+        return build_surrogate(model, grid, cfg, training, eps_kl=1e-10, degree=degree, family="hermite")
+
+    t0 = time.time()
+    sur = share_from_rank0(build, rank, use_dist)
+    return sur, time.time() - t0
+
+
+def shard_inputs(args, c, eval_rng, rank, world):
+    """This rank's contiguous block of global sample ids and its xi rows
+    (all ranks draw the same global xi from the seed, then slice)."""
+    from paper_2510_26180_b200.moments import shard_bounds
+
+    M_total = total_samples(args, c)
+    lo, hi = shard_bounds(M_total, rank, world)
+    xi_all = eval_samples(eval_rng, M_total, c["d"])
+    return M_total, lo, hi, xi_all
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -140,9 +236,6 @@ def run_b200(args):
     from paper_2510_26180_b200 import _lib
     from paper_2510_26180_b200.device import DeviceOperator, empty, ptr, stream_ptr
     from paper_2510_26180_b200.engine import KleCgcSolver
-    from paper_2510_26180_b200.pcgc import build_alpha_circulant
-    from paper_2510_26180_b200.surrogate import build_surrogate
-    from paper_2510_26180_b200.core import ParameterSample
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -151,34 +244,30 @@ def run_b200(args):
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c, model, grid, cfg, train, eval_rng = problem(args.config)
-    M = c["M"]
-    t0 = time.time()
-    training = [ParameterSample(x, id=i) for i, x in enumerate(train)]
-    sur = build_surrogate(model, grid, cfg, training, eps_kl=1e-10, degree=c["degree"])
-    t_build = time.time() - t0
+    M_total, lo, hi, xi_all = shard_inputs(args, c, eval_rng, rank, world)
+    M = hi - lo
+    sur, t_build = build_and_share_surrogate(model, grid, cfg, train, c["degree"], rank, use_dist)
     solver = KleCgcSolver(model, grid, cfg, sur)
-    xi_all = eval_samples(eval_rng, M * world, c["d"])
-    xi_host = np.ascontiguousarray(xi_all[rank * M:(rank + 1) * M])
+    xi_host = np.ascontiguousarray(xi_all[lo:hi])
     xi_d = torch.as_tensor(xi_host, device="cuda")
     stream = torch.cuda.current_stream()
 
     def step(x):
         res = solver.solve(x)
-        mean, var = solver.moments(res, M_total=M * world)
+        mean, var = solver.moments(res, M_total=M_total)
         return res, mean, var
 
-    for _ in range(args.warmup):
-        res, mean, var = step(xi_d)
-    torch.cuda.synchronize()
-    if use_dist:
-        dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters_sum = 0
-    kmax = 0
-    with ClockSampler(local) as clocks:
+    def barrier():
         torch.cuda.synchronize()
         if use_dist:
             dist.barrier()
+
+    for _ in range(args.warmup):
+        res, mean, var = step(xi_d)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
         ev0.record(stream)
         for _ in range(args.steps):
             res, mean, var = step(xi_d)
@@ -186,21 +275,22 @@ def run_b200(args):
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     it = res.batch.iters
-    iters_sum = int(it.sum().item())
-    kmax = int(it.max().item())
-    status = res.batch.status.cpu().numpy()
-    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-    it_t = torch.tensor([iters_sum], device="cuda", dtype=torch.float64)
+    n_sub = min(c["cpu_subset"], M_total)
+    stats = torch.tensor([ms, float(it.sum().item()), float(it.max().item()),
+                          float((res.batch.status != 1).sum().item()),
+                          float(it[:max(0, min(n_sub - lo, M))].sum().item())], device="cuda", dtype=torch.float64)
     if use_dist:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
-    ms_max = float(ms_t.item())
-    total_iters = float(it_t.item())
+        mx = stats[[0, 2]].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats[[1, 3, 4]].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        stats = torch.stack([mx[0], sm[0], mx[1], sm[1], sm[2]])
+    ms_max, total_iters, kmax, n_bad, sub_iters = [float(v) for v in stats.tolist()]
     dof_per_iter = grid.n_coarse * grid.n_fine_per_coarse * model.nx
-    solves_per_s = M * world / (ms_max * 1e-3)
+    solves_per_s = M_total / (ms_max * 1e-3)
     dof_per_s = total_iters * dof_per_iter / (ms_max * 1e-3)
 
-    # ---- kernel-level timing of the two hot kernels (all samples active) ----
+    # ---- kernel-level timing of the hot kernels on this rank's shard (all samples active) ----
     op = DeviceOperator.from_model(model, xi_d)
     U = solver.surrogate.predict(xi_d)
     blob = op.blob(grid.deltat)
@@ -246,82 +336,79 @@ def run_b200(args):
     fgr_bytes = 16.0 * M * grid.n_coarse * model.nx   # read U, write R
     K_g = solver.surrogate.inner_dim
     gemm_tflops = 2.0 * M * K_g * grid.n_coarse * model.nx / (gemm_ms * 1e-3) / 1e12
-    avg_iters = total_iters / (M * world)
-    share_fgr = avg_iters * fgr_ms
-    share_cgc = avg_iters * cgc_ms
+    avg_iters = total_iters / M_total
+    local_ms = ms   # this rank's own step (the shares are of its own step)
+    share_fgr = float(it.double().mean().item()) * fgr_ms / local_ms
+    share_cgc = float(it.double().mean().item()) * cgc_ms / local_ms
+    del R, scratch, sfac, U, op
 
-    # ---- end to end through the public API: host xi -> device -> host moments ----
-    e2e = None
-    if world >= 1:
-        pinned = torch.from_numpy(xi_host).pin_memory()
-        host_mean = torch.empty(mean.numel(), dtype=torch.float64).pin_memory()
-        host_var = torch.empty_like(host_mean).pin_memory()
-        host_it = torch.empty(M, dtype=torch.int32).pin_memory()
-        host_st = torch.empty(M, dtype=torch.int32).pin_memory()
+    # ---- end to end through the public API: pinned host xi -> device -> host moments + counts ----
+    pinned = torch.from_numpy(xi_host).pin_memory()
+    host_mean = torch.empty(mean.numel(), dtype=torch.float64).pin_memory()
+    host_var = torch.empty_like(host_mean).pin_memory()
+    host_it = torch.empty(M, dtype=torch.int32).pin_memory()
+    host_st = torch.empty(M, dtype=torch.int32).pin_memory()
 
-        def e2e_step():
-            xd = pinned.to("cuda", non_blocking=True)
-            r2, m2, v2 = step(xd)
-            host_mean.copy_(m2.reshape(-1), non_blocking=True)
-            host_var.copy_(v2.reshape(-1), non_blocking=True)
-            host_it.copy_(r2.batch.iters, non_blocking=True)
-            host_st.copy_(r2.batch.status, non_blocking=True)
+    def e2e_step():
+        xd = pinned.to("cuda", non_blocking=True)
+        r2, m2, v2 = step(xd)
+        host_mean.copy_(m2.reshape(-1), non_blocking=True)
+        host_var.copy_(v2.reshape(-1), non_blocking=True)
+        host_it.copy_(r2.batch.iters, non_blocking=True)
+        host_st.copy_(r2.batch.status, non_blocking=True)
 
-        e2e_step()  # warm-up of the host-buffer path (untimed)
-        torch.cuda.synchronize()
-        if use_dist:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        nrep = max(1, args.steps)
-        for _ in range(nrep):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = torch.tensor([e0.elapsed_time(e1) / nrep], device="cuda", dtype=torch.float64)
-        if use_dist:
-            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": M * world / (float(e2e_ms.item()) * 1e-3), "unit": "solves/s",
-               "h2d_bytes_per_step": int(xi_host.nbytes),
-               "d2h_bytes_per_step": int(host_mean.numel() * 16 + M * 8),
-               "ms_per_step": float(e2e_ms.item())}
+    e2e_step()  # warm-up of the host-buffer path (untimed)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    nrep = max(1, args.steps)
+    for _ in range(nrep):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / nrep], device="cuda", dtype=torch.float64)
+    if use_dist:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e = {"value": M_total / (float(e2e_ms.item()) * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": int(xi_host.nbytes) * world,
+           "d2h_bytes_per_step": int(host_mean.numel() * 16 * world + M_total * 8),
+           "ms_per_step": float(e2e_ms.item())}
 
     # per step: kl_tridiag, fine_factor, gpc basis + 1-2 GEMMs, shift_factor, then per outer iteration and
     # sample pipeline (two when the batch is large, kle_capi.cu) one fgr and one CGC launch (an upper bound:
     # a pipeline stops as soon as its own samples have converged), and 2 x (2 col-sum + 1 scale) for the moments
-    pipes = 2 if (M >= 8192 and sfac is not None and os.environ.get("KLE_PCGC_PIPES", "2") != "1") else 1
+    pipes = 2 if (M >= 8192 and os.environ.get("KLE_PCGC_PIPES", "2") != "1") else 1
     launches_per_step = (1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 1
-                         + 2 * pipes * kmax + 6)
+                         + 2 * pipes * int(kmax) + 6)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_host)
+        cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_all[:n_sub])
     if rank == 0:
         fp64_peak = peaks.get("fp64_tflops")
         line = {
             "metric": METRIC,
             "value": solves_per_s,
-            "unit": "KLE-CGC solves/s",
+            "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms_max,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded N(0,1) KL coordinates, BASELINE configs; no dataset exists)",
-            "config": {"workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3}[args.config] }] ({args.config}): "
-                                   f"nx={model.nx}, N={grid.n_coarse}, J={grid.n_fine_per_coarse}, d={c['d']}, "
-                                   f"Hermite p={c['degree']}, alpha={cfg.alpha}, tol={cfg.tol}",
-                       "samples_per_gpu": M, "global_samples": M * world,
-                       "parallelism": f"sample-sharded x{world}",
-                       "l2": "inputs larger than L2 (state 8*M*N*nx bytes per rank)"},
+            "config": config_dict(args, c, world),
+            "samples_per_rank": M,
             "fine_dof_updates_per_s": dof_per_s,
             "avg_outer_iters": avg_iters,
-            "max_outer_iters": kmax,
-            "all_converged": bool(np.all(status == 1)),
+            "avg_outer_iters_cpu_subset": sub_iters / n_sub,
+            "cpu_subset_ids": [0, n_sub],
+            "max_outer_iters": int(kmax),
+            "all_converged": n_bad == 0,
             "surrogate_build_s": t_build,
-            "surrogate": {"m_q": sur.m_q, "P": solver.surrogate.P, "K_g": K_g, "mode": solver.surrogate.mode},
+            "surrogate": {"m_q": sur.m_q, "P": solver.surrogate.P, "K_g": K_g, "mode": solver.surrogate.mode,
+                          "built_on": "rank 0 (device snapshots), broadcast"},
             "roofline": {
                 "kernel": "fgr_kernel (fused J-step fine sweep + CGC rhs)",
                 "bound": "fp64",
@@ -329,12 +416,11 @@ def run_b200(args):
                 "peak": fp64_peak,
                 "unit": "TFLOP/s",
                 "frac": (fgr_tflops / fp64_peak) if fp64_peak else None,
-                "traffic": (peaks["traffic"]["fgr_kernel"]["bytes_per_sample_iteration"] * M
-                            if "traffic" in peaks else None),
+                "traffic": traffic_of(peaks, args.config, "fgr_kernel", M),
                 "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per sample-iteration "
-                                  "(profiles/r01_traffic.json) x samples per launch",
+                                  "(profiles/traffic.json) x samples per launch",
                 "peak_source": peaks.get("fp64_source"),
-                "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch",
+                "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch (M = rank shard)",
                 "hbm_frac": (fgr_bytes / (fgr_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
                 "ms_per_launch": fgr_ms,
             },
@@ -343,14 +429,13 @@ def run_b200(args):
                                "frac": cgc_gbs / peaks["hbm_gbs"], "ms_per_launch": cgc_ms,
                                "algorithmic": "24 B per (n, i) per sample: read R, read U, write U "
                                               "(+ pivots 16 (N/2+1)/N B not counted)",
-                               "path": "cluster" if sfac is not None else "on-the-fly",
-                               "traffic": (peaks["traffic"]["cgc_cluster_kernel"]["bytes_per_sample_iteration"] * M
-                                           if "traffic" in peaks and sfac is not None else None)},
+                               "path": "cluster",
+                               "traffic": traffic_of(peaks, args.config, "cgc_cluster_kernel", M)},
                 "gemm_bias_kernel": {"bound": "tensor(dmma)", "achieved": gemm_tflops,
                                      "peak": peaks.get("dmma_tflops"), "unit": "TFLOP/s",
                                      "frac": gemm_tflops / peaks["dmma_tflops"] if peaks.get("dmma_tflops") else None,
                                      "ms_per_launch": gemm_ms},
-                "step_share": {"fgr": share_fgr / ms_max, "cgc": share_cgc / ms_max},
+                "step_share": {"fgr": share_fgr, "cgc": share_cgc},
             },
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -361,6 +446,11 @@ def run_b200(args):
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def traffic_of(peaks, config, kernel, M):
+    t = peaks.get("traffic", {}).get(config, {}).get(kernel)
+    return t["bytes_per_sample_iteration"] * M if t else None
 
 
 def load_peaks():
@@ -384,8 +474,8 @@ def load_peaks():
                 out["fp64_source"] = "measured DFMA peak, profiles/r01_fp64_peaks.jsonl (tools/fp64_peaks.cu)"
             if d.get("what") == "dmma_tflops":
                 out["dmma_tflops"] = d["value"]
-    t = ROOT / "profiles" / "r01_traffic.json"
-    if t.exists():  # DRAM bytes per sample-iteration from one ncu --set full capture
+    t = ROOT / "profiles" / "traffic.json"
+    if t.exists():  # DRAM bytes per sample-iteration from one ncu --set full capture, per config
         out["traffic"] = json.loads(t.read_text())
     return out
 
@@ -398,6 +488,12 @@ _W = {}
 
 def _cpu_init(payload):
     _W.update(payload)
+    try:  # one BLAS/OpenMP thread per worker process (cores x cores threads thrash)
+        from threadpoolctl import threadpool_limits
+
+        _W["_tp"] = threadpool_limits(1)
+    except ImportError:
+        pass
 
 
 def _cpu_solve(i):
@@ -414,68 +510,87 @@ def _cpu_solve(i):
     return out["iters"]
 
 
-def cpu_baseline(args, c, model, grid, cfg, sur, xi_host):
-    """Time the reference CPU path on a bounded sample of the workload over
-    all host cores (ProcessPool, one sample per task)."""
+def _cpu_pool(payload, cores):
+    import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
 
-    cores = os.cpu_count() or 1
-    payload = dict(xi=xi_host, kl_table=model.kl_table,
-                   inv_h2=1.0 / (model.h * model.h), u0=model.initial_condition(), mean=sur.mean_field,
-                   lam=sur.eigenvalues, modes=sur.modes, coeffs=sur.coeffs, degree=sur.degree,
-                   N=grid.n_coarse, J=grid.n_fine_per_coarse, alpha=cfg.alpha, tol=cfg.tol)
-    # size the sample: one probe solve, then ~cpu_seconds of wall on `cores` workers
-    _cpu_init(payload)
-    t0 = time.time()
-    _cpu_solve(0)
-    per = time.time() - t0
-    n = int(max(cores, min(len(xi_host), cores * max(1.0, args.cpu_seconds / max(per, 1e-3)))))
-    n = min(n, len(xi_host))
-    import multiprocessing as mp
-
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
     # fork: workers inherit the surrogate tables without pickling them
-    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+    return ProcessPoolExecutor(cores, mp_context=mp.get_context("fork"), initializer=_cpu_init,
+                               initargs=(payload,))
+
+
+def _cpu_payload(c, model, grid, sur, xi_sub):
+    return dict(xi=xi_sub, kl_table=model.kl_table, inv_h2=1.0 / (model.h * model.h), u0=model.initial_condition(),
+                mean=sur.mean_field, lam=sur.eigenvalues, modes=sur.modes, coeffs=sur.coeffs, degree=sur.degree,
+                N=grid.n_coarse, J=grid.n_fine_per_coarse, alpha=c["alpha"], tol=c["tol"])
+
+
+def _cpu_record(n, wall, its, cores, c, model, grid, M_total, steps=None):
+    dof = float(np.sum(its)) * grid.n_coarse * grid.n_fine_per_coarse * model.nx
+    v = n / wall
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+            "blas_threads_per_worker": 1,
+            "sample": f"sample ids 0..{n - 1} of the {M_total} config samples"
+                      + (f" ({steps} timed chunks)" if steps else "")
+                      + ", surrogate_predict + pcgc_solve per sample (oracle/ref_port = pintuq arithmetic, scipy "
+                        f"SuperLU/LAPACK/pocketfft), {cores} processes x 1 BLAS thread, {wall:.1f} s wall",
+            "extrapolated": True,
+            "extrapolation": f"linear: the full M = {M_total} would take {M_total / v:.0f} s at this rate",
+            "subset_size": n, "avg_outer_iters_subset": float(np.mean(its)),
+            "fine_dof_updates_per_s": dof / wall}
+
+
+def cpu_baseline(args, c, model, grid, cfg, sur, xi_sub):
+    """The reference CPU path on the fixed subset of sample ids 0..n-1 over
+    all host cores (ProcessPool, one sample per task)."""
+    cores = os.cpu_count() or 1
+    n = len(xi_sub)
+    with _cpu_pool(_cpu_payload(c, model, grid, sur, xi_sub), cores) as ex:
         list(ex.map(_cpu_solve, range(min(cores, n))))  # warm the workers
         t0 = time.time()
-        its = list(ex.map(_cpu_solve, range(n)))
+        its = list(ex.map(_cpu_solve, range(n), chunksize=max(1, n // (8 * cores))))
         wall = time.time() - t0
-    dof = float(np.sum(its)) * grid.n_coarse * grid.n_fine_per_coarse * model.nx
-    return {"value": n / wall, "unit": "KLE-CGC solves/s", "cores": cores, "kind": "port",
-            "sample": f"first {n} of the {len(xi_host)} config samples, surrogate_predict + pcgc_solve "
-                      f"(oracle/ref_port = pintuq arithmetic, scipy SuperLU/LAPACK/pocketfft), "
-                      f"{cores} processes, {wall:.1f} s wall",
-            "fine_dof_updates_per_s": dof / wall, "single_core_s_per_solve": per}
+    return _cpu_record(n, wall, its, cores, c, model, grid, total_samples(args, c))
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path on the box's host cores, on
+    this arm's config/metric/unit; rank 0 only (other ranks exit 0)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     c, model, grid, cfg, train, eval_rng = problem(args.config)
-    from concurrent.futures import ProcessPoolExecutor
-
+    M_total = total_samples(args, c)
     # the reference builds its surrogate on the CPU too (collect_snapshots ->
     # kl_build -> gpc_fit); training solves run over all cores
     t0 = time.time()
     cores = os.cpu_count() or 1
     sur = _cpu_build_surrogate(model, grid, cfg, train, c["degree"], cores)
     t_build = time.time() - t0
-    xi_host = eval_samples(eval_rng, c["M"], c["d"])
-    vals = []
-    res = None
-    for s in range(args.warmup + args.steps):
-        # warm-up steps only spin up the process pool; timed steps are ~cpu_seconds/2 of CPU work
-        a2 = argparse.Namespace(**{**vars(args), "cpu_seconds": 2.0 if s < args.warmup else args.cpu_seconds / 2})
-        res = cpu_baseline(a2, c, model, grid, cfg, sur, xi_host)
-        if s >= args.warmup:
-            vals.append(res["value"])
-    v = float(np.mean(vals))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "KLE-CGC solves/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-            "config": {"workload": f"{args.config} (same as the b200 arm)", "samples_per_gpu": c["M"]},
-            "cpu_baseline": {**res, "value": v}, "surrogate_build_s": t_build,
-            "e2e": {"value": v, "unit": "KLE-CGC solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    n_sub = min(c["cpu_subset"], M_total)
+    xi_sub = eval_samples(eval_rng, M_total, c["d"])[:n_sub]
+    steps = max(1, args.steps)
+    bounds = [(n_sub * s) // steps for s in range(steps + 1)]
+    its, walls = [], []
+    with _cpu_pool(_cpu_payload(c, model, grid, sur, xi_sub), cores) as ex:
+        for _ in range(args.warmup):  # warm-up steps only spin the workers up (a few samples)
+            list(ex.map(_cpu_solve, range(min(cores, n_sub))))
+        for s in range(steps):  # each timed step = one contiguous chunk of the fixed id subset
+            ids = range(bounds[s], bounds[s + 1])
+            t1 = time.time()
+            its += list(ex.map(_cpu_solve, ids, chunksize=max(1, len(ids) // (8 * cores))))
+            walls.append(time.time() - t1)
+    wall = float(np.sum(walls))
+    rec = _cpu_record(n_sub, wall, its, cores, c, model, grid, M_total, steps)
+    line = {"impl": "reference", "metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) KL coordinates, BASELINE configs; no dataset exists)",
+            "config": config_dict(args, c, world), "avg_outer_iters_cpu_subset": rec["avg_outer_iters_subset"],
+            "cpu_subset_ids": [0, n_sub], "cpu_baseline": rec, "surrogate_build_s": t_build,
+            "e2e": {"value": rec["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -492,23 +607,20 @@ def _snap_one(args):
 
 
 def _cpu_build_surrogate(model, grid, cfg, train, degree, cores):
-    from concurrent.futures import ProcessPoolExecutor
-
     from oracle import ref_port
     from paper_2510_26180_b200.models import ParameterMap
     from paper_2510_26180_b200.surrogate import KLGpcSurrogate
 
     jobs = [(x, model.kl_table, 1.0 / (model.h * model.h), model.initial_condition(), grid.n_coarse,
              grid.n_fine_per_coarse, cfg.alpha, cfg.tol) for x in train]
-    import multiprocessing as mp
-
-    with ProcessPoolExecutor(cores, mp_context=mp.get_context("fork")) as ex:
+    with _cpu_pool({}, cores) as ex:
         fields = np.array(list(ex.map(_snap_one, jobs, chunksize=4)))
     w = model.cell_volume * grid.deltaT
     mean, lam, modes, X = ref_port.kl_build(fields, w, 1e-10)
     zeta = ref_port.kl_coefficients(X, modes, lam, w)
     coeffs = ref_port.gpc_fit(train, zeta, degree)
-    return KLGpcSurrogate(mean, lam, modes, coeffs, degree, [ParameterMap("identity", -np.inf, np.inf)] * len(train[0]), family="hermite")
+    return KLGpcSurrogate(mean, lam, modes, coeffs, degree,
+                          [ParameterMap("identity", -np.inf, np.inf)] * len(train[0]), family="hermite")
 
 
 def run_c5(args):
@@ -828,6 +940,7 @@ def run_nonlinear(args):
 
 if __name__ == "__main__":
     a = parse()
+    maybe_relaunch(a)
     if a.config in NL_CASES:
         run_nonlinear(a)
     elif a.config == "c5":

@@ -117,8 +117,9 @@ int kle_shift_factor_f64(const double* dia, const double* off, const double* lam
  *   u = diag(1/scaling) F (lambda I + dT A)^{-1} F* diag(scaling) r
  * r, u are [M][N][nx]; lam is [N] interleaved complex (re, im) =
  * build_alpha_circulant(N, alpha).eigenvalues (pintuq/pcgc.py:68-76),
- * scaling / inv_scaling its scaling and 1/scaling; imag[M] (optional)
- * receives max|Im u| per sample. sfac (optional, kle_shift_factor_f64)
+ * scaling / inv_scaling its scaling and 1/scaling; imag[M] (optional) is
+ * zeroed (every path here returns a real u via Hermitian completion; the
+ * reference's max|Im u| diagnostic is kle_imag_residue_f64). sfac (optional, kle_shift_factor_f64)
  * selects the cluster kernel; without it the pivots are formed on the fly.
  * scratch: kle_cgc_scratch_bytes(M, N, nx) bytes (the cluster path needs
  * 16*M bytes of per-sample reduction slots; the call zeroes them). scaling
@@ -127,9 +128,25 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
                        const double* dia, const double* off, const double* sfac, int M, int N, int nx, double dT,
                        double* u, double* imag, void* scratch, size_t scratch_bytes, void* stream);
 
+/* max_imag_residue of three_step_solve (pintuq/pcgc.py:170-172, accumulated
+ * per iteration at :340-342): the three-step solve done as the reference does
+ * it — all N shifted systems solved independently, u = diag(1/scaling) F q
+ * without Hermitian completion — and imag[s] = max(imag[s], max|Im u|) for
+ * every sample with status == NULL or status[s] == KLE_SAMPLE_ACTIVE. r is
+ * [M][N][nx]; load_scale == NULL means r is already alpha-scaled. A rounding-
+ * level quantity that grows with cond(V) = alpha^{-(N-1)/N}; not bit-equal to
+ * the reference's (different FFT). scratch: kle_imag_residue_scratch_bytes
+ * (<= 256 MB). kle_pcgc_solve_f64 runs it every iteration when its imag
+ * argument is non-NULL (and then uses one sample pipeline). */
+size_t kle_imag_residue_scratch_bytes(int M, int N, int nx);
+int kle_imag_residue_f64(const double* r, const double* load_scale, const double* inv_scaling, const double* lam,
+                         const double* dia, const double* off, const int32_t* status, int M, int N, int nx,
+                         double dT, double* imag, void* scratch, size_t scratch_bytes, void* stream);
+
 /* CGC update of one PCGC iteration k (pintuq/pcgc.py:331-348): U <- three_step(R)
  * in place, increment = max|U_new - U| per sample, stop test against tol,
- * status/iters updated, inc_hist[s][k-1] and imag[s] recorded, and
+ * status/iters updated, inc_hist[s][k-1] recorded (imag[s]: the on-the-fly
+ * path's Hermitian-completed residue, unused by the cluster/large paths), and
  * *active_count incremented once per still-active sample. R must already be
  * alpha-scaled (kle_fgr_f64 output). With sfac (cluster path) `scratch` holds
  * 16*M bytes of per-sample reduction slots that must be zero before the first
@@ -178,6 +195,19 @@ int kle_pcgc_solve_ref_f64(double* U, const double* u0, const double* dia, const
 int kle_err_ref_f64(const double* U, const double* ref, int M, int N, int nx, int k, int max_iters, double tol,
                     int stop_on_reference, int32_t* status, int32_t* iters, int32_t* active_count, double* err_hist,
                     double* max_err, void* stream);
+
+/* Mean-error aggregation of the experiment harness (pintuq/experiments.py:
+ * 314-334) over the error records of a reference-tracked batch: a sample is
+ * "good" when its records err_hist[s][0..iters[s]][:] ([M][max_iters+1][N],
+ * as written by kle_pcgc_solve_ref_f64) are all finite; each good sample's
+ * error vectors are padded with their last record to k_max + 1 rows and the
+ * rows are summed over the good samples in id order. Writes good[M] (0/1),
+ * counts[2] = (n_good, k_max) and sums[max_iters+1][N] for the rows 0..k_pad
+ * (k_pad < 0: this batch's own k_max; a sharded caller passes the global
+ * k_max), NaN past them. mean_vectors = sums / n_good (numpy's
+ * stack.mean(axis=0), bit for bit); mean_max_error = their row-wise max. */
+int kle_err_aggregate_f64(const double* err_hist, const int32_t* iters, int M, int N, int max_iters, int k_pad,
+                          int32_t* good, int32_t* counts, double* sums, void* stream);
 
 /* Classical parareal, the paper's comparison baseline (parareal_solve,
  * pintuq/parareal.py:100-191), for the tridiagonal models:

@@ -35,10 +35,13 @@ _SIGS = {
     "kle_cgc_update_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z,
                             _p], _i),
     "kle_pcgc_workspace_bytes": ([_i, _i, _i], _z),
+    "kle_imag_residue_scratch_bytes": ([_i, _i, _i], _z),
+    "kle_imag_residue_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _d, _p, _p, _z, _p], _i),
     "kle_pcgc_solve_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _i, _p, _p, _p, _p,
                             _p, _z, _p], _i),
     "kle_pcgc_solve_ref_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _i, _p, _i, _p,
                                 _p, _p, _p, _p, _p, _p, _z, _p], _i),
+    "kle_err_aggregate_f64": ([_p, _p, _i, _i, _i, _i, _p, _p, _p, _p], _i),
     "kle_err_ref_f64": ([_p, _p, _i, _i, _i, _i, _i, _d, _i, _p, _p, _p, _p, _p, _p], _i),
     "kle_parareal_init_f64": ([_p, _p, _p, _i, _i, _i, _d, _d, _p, _p], _i),
     "kle_parareal_step_f64": ([_p, _p, _p, _p, _p, _i, _i, _i, _d, _d, _i, _i, _d, _p, _p, _p, _p, _p], _i),

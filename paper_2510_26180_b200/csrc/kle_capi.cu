@@ -189,7 +189,7 @@ int kle_three_step_f64(const double* r, const double* scaling, const double* inv
   a.inv_scaling = inv_scaling;
   a.scratch = static_cast<double*>(scratch);
   a.scratch_doubles_per_cta = cgc_scratch_doubles_per_cta(N, nx);
-  a.imag = imag;
+  a.imag = nullptr;  // zeroed above: u is real by Hermitian completion (diagnostic: kle_imag_residue_f64)
   a.M = M;
   a.N = N;
   a.nx = nx;
@@ -244,6 +244,34 @@ int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, co
   return cgc_run(a, KLE_STREAM(stream));
 }
 
+size_t kle_imag_residue_scratch_bytes(int M, int N, int nx) { return imag_residue_scratch_bytes(M, N, nx); }
+
+int kle_imag_residue_f64(const double* R, const double* load_scale, const double* inv_scaling, const double* lam,
+                         const double* dia, const double* off, const int32_t* status, int M, int N, int nx,
+                         double dT, double* imag, void* scratch, size_t scratch_bytes, void* stream) {
+  if (M < 0 || N < 1 || nx < 1 || !imag) return set_error(KLE_ERR_INVALID, "imag_residue: bad arguments");
+  if (M == 0) return KLE_OK;
+  if (scratch_bytes < imag_residue_scratch_bytes(M, N, nx))
+    return set_error(KLE_ERR_WORKSPACE, "imag_residue: scratch too small");
+  CgcArgs a{};
+  a.R = R;
+  a.load_scale = load_scale;
+  a.dia = dia;
+  a.off = off;
+  a.lam = lam;
+  a.inv_scaling = inv_scaling;
+  a.scratch = static_cast<double*>(scratch);
+  a.status = const_cast<int32_t*>(status);
+  a.imag = imag;
+  a.M = M;
+  a.N = N;
+  a.nx = nx;
+  a.k = 1;
+  a.max_iters = 1;
+  a.dT = dT;
+  return imag_residue_run(a, KLE_STREAM(stream));
+}
+
 static size_t pcgc_scratch_part(int M, int N, int nx) {
   return cgc_cluster_supported(N, nx) ? align256(kle_shift_factor_bytes(M, N, nx)) + align256((size_t)M * 16)
                                       : kle_cgc_scratch_bytes(M, N, nx);
@@ -251,7 +279,8 @@ static size_t pcgc_scratch_part(int M, int N, int nx) {
 
 size_t kle_pcgc_workspace_bytes(int M, int N, int nx) {
   if (M <= 0 || N <= 0 || nx <= 0) return 0;
-  return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256;
+  return align256((size_t)M * N * nx * sizeof(double)) + align256(pcgc_scratch_part(M, N, nx)) + 256 +
+         align256(imag_residue_scratch_bytes(M, N, nx));
 }
 
 
@@ -285,6 +314,9 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
   void* scratch = ws;
   ws += align256(scratch_bytes);
   int32_t* counter = reinterpret_cast<int32_t*>(ws);
+  ws += 256;
+  void* imag_scratch = ws;  // the max_imag_residue diagnostic (only when imag is requested)
+  const size_t imag_scratch_bytes = imag_residue_scratch_bytes(M, N, nx);
   double* sfac = clustered ? static_cast<double*>(scratch) : nullptr;
   void* cgc_scratch = clustered ? static_cast<void*>(static_cast<char*>(scratch) + align256(kle_shift_factor_bytes(M, N, nx)))
                                 : scratch;
@@ -316,6 +348,7 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
     pipes = pipes < 1 ? 1 : (pipes > kMaxPipes ? kMaxPipes : pipes);
     if (pipes > M) pipes = M > 0 ? M : 1;
   }
+  if (imag) pipes = 1;  // the diagnostic's scratch serves one pipeline
   const FineLayoutRT lay = fine_layout(nx);
   struct Pipe {
     int m0, M, k;
@@ -365,11 +398,14 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
       cudaStreamWaitEvent(q.sc, q.fdone, 0);
     }
     cudaMemsetAsync(q.count_d, 0, sizeof(int32_t), q.sc);
+    if (imag)  // max_imag_residue (pintuq/pcgc.py:170-172, 340-342) of this iteration's three-step solve
+      KLE_TRY(kle_imag_residue_f64(R + o * N * nx, nullptr, inv_scaling, lam, dq, eq, sq, q.M, N, nx, dT, imag + o,
+                                   imag_scratch, imag_scratch_bytes, q.sc));
     const double* sf = clustered ? sfac + o * (shift_factor_doubles(1, N, nx)) : nullptr;
     void* cs = clustered ? static_cast<void*>(static_cast<char*>(cgc_scratch) + o * 16) : cgc_scratch;
     KLE_TRY(kle_cgc_update_f64(R + o * N * nx, Uq, inv_scaling, lam, dq, eq, sf, q.M, N, nx, dT, k, max_iters,
                                cgc_tol, sq, iters + o, inc_hist ? inc_hist + o * max_iters : nullptr,
-                               imag ? imag + o : nullptr, q.count_d, cs,
+                               nullptr, q.count_d, cs,
                                clustered ? (size_t)q.M * 16 : cgc_scratch_bytes, q.sc));
     if (ref)
       KLE_TRY(err_ref(Uq, ref + o * N * nx, q.M, N, nx, k, max_iters, tol, stop_ref, sq, iters + o, q.count_d,
@@ -443,6 +479,13 @@ int kle_err_ref_f64(const double* U, const double* ref, int M, int N, int nx, in
   if (!status || !iters) return set_error(KLE_ERR_INVALID, "err_ref: status and iters are required");
   return err_ref(U, ref, M, N, nx, k, max_iters, tol, stop_on_reference, status, iters, active_count, err_hist,
                  max_err, KLE_STREAM(stream));
+}
+
+int kle_err_aggregate_f64(const double* err_hist, const int32_t* iters, int M, int N, int max_iters, int k_pad,
+                          int32_t* good, int32_t* counts, double* sums, void* stream) {
+  if (M < 0 || N < 1 || max_iters < 0 || k_pad > max_iters || !err_hist || !iters || !good || !counts || !sums)
+    return set_error(KLE_ERR_INVALID, "err_aggregate: bad arguments");
+  return err_aggregate(err_hist, iters, M, N, max_iters, k_pad, good, counts, sums, KLE_STREAM(stream));
 }
 
 // ---- classical parareal (pintuq/parareal.py:100-191) ------------------------

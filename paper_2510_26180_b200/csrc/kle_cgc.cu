@@ -62,9 +62,15 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
+// a.full (the max_imag_residue diagnostic of three_step_solve, pintuq/pcgc.py:
+// 170-172): the transform keeps all N frequencies, all N shifted systems are
+// solved independently and u = diag(1/scaling) F q is formed without Hermitian
+// completion, as the reference does; the rounding asymmetry between f and N - f
+// (amplified up to cond(V) = alpha^{-(N-1)/N} by the unscaling) is what
+// max|Im u| measures. Only imag is written.
 __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2N) {
   extern __shared__ double sm[];
-  const int N = a.N, nx = a.nx, NF = N / 2 + 1;
+  const int N = a.N, nx = a.nx, NF = a.full ? N : N / 2 + 1;
   const bool pow2 = log2N >= 0;
   Cplx* tw = reinterpret_cast<Cplx*>(sm);
   Cplx* tile = tw + N;
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
         const int c = idx / N, n = idx - c * N;
         Cplx v = {0.0, 0.0};
         if (c < tc) {
-          if (n < NF) {
+          if (a.full || n < NF) {
             v = pbuf[(size_t)(c0 + c) * NF + n];
           } else {
             const Cplx w = pbuf[(size_t)(c0 + c) * NF + (N - n)];
@@ -186,6 +192,10 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
         const double u = (v.re * rsN) * isc;
         const double ui = (v.im * rsN) * isc;
         const size_t g = sb + (size_t)n * nx + c0 + c;
+        if (a.full) {
+          immax = nanmax(immax, fabs(ui));
+          continue;
+        }
         if (a.Uout) {
           if (a.U) incmax = nanmax(incmax, fabs(u - a.U[g]));
           a.Uout[g] = u;
@@ -199,6 +209,10 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
     }
     incmax = block_max(incmax, red);
     immax = block_max(immax, red);
+    if (a.full) {
+      if (threadIdx.x == 0 && a.imag) a.imag[s] = nanmax(a.imag[s], immax);
+      continue;
+    }
     if (threadIdx.x == 0) {
       if (a.inc) a.inc[s] = incmax;
       if (a.inc_hist) a.inc_hist[(size_t)s * a.max_iters + (a.k - 1)] = incmax;
@@ -248,6 +262,21 @@ size_t cgc_scratch_doubles_per_cta(int N, int nx) {
   return 4 * (size_t)nx * NF;  // p/y/q (complex) + inverse pivots (complex)
 }
 
+// The diagnostic keeps all N frequencies per sample: its slabs are twice the
+// size, so it runs on as many CTAs as fit a 256 MB scratch budget (<= 148 * 4).
+static int imag_grid(int M, int N, int nx) {
+  const size_t slab = 4 * (size_t)nx * N * sizeof(double);
+  size_t g = ((size_t)256 << 20) / (slab ? slab : 1);
+  if (g > 148 * 4) g = 148 * 4;
+  if (g < 1) g = 1;
+  return M < (int)g ? (M > 0 ? M : 1) : (int)g;
+}
+
+size_t imag_residue_scratch_bytes(int M, int N, int nx) {
+  if (M <= 0 || N <= 0 || nx <= 0) return 0;
+  return (size_t)imag_grid(M, N, nx) * 4 * (size_t)nx * N * sizeof(double);
+}
+
 int cgc_run(const CgcArgs& a, cudaStream_t st) {
   if (a.N < 1 || a.nx < 1) return set_error(KLE_ERR_INVALID, "cgc: bad dims");
   if (use_large(a.N, a.nx)) return cgc_large_run(a, st);
@@ -266,6 +295,29 @@ int cgc_run(const CgcArgs& a, cudaStream_t st) {
   const int grid = cgc_grid(a.M, a.N, a.nx);
   cgc_kernel<<<grid, CGC_NT, smem, st>>>(a, TC, log2N);
   return check_launch("cgc_kernel");
+}
+
+int imag_residue_run(const CgcArgs& a0, cudaStream_t st) {
+  if (a0.N < 1 || a0.nx < 1) return set_error(KLE_ERR_INVALID, "imag_residue: bad dims");
+  if (a0.M <= 0 || !a0.imag) return KLE_OK;
+  CgcArgs a = a0;
+  a.full = 1;
+  a.U = nullptr;
+  a.Uout = nullptr;
+  // a.status, if given, only selects the active samples (full mode never writes it)
+  int log2N = -1;
+  if ((a.N & (a.N - 1)) == 0) {
+    log2N = 0;
+    while ((1 << log2N) < a.N) ++log2N;
+  }
+  a.scratch_doubles_per_cta = 4 * (size_t)a.nx * a.N;
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_cgc(imag): cudaFuncSetAttribute", [&] {
+        return cudaFuncSetAttribute(cgc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }))
+    return rc;
+  cgc_kernel<<<imag_grid(a.M, a.N, a.nx), CGC_NT, cgc_smem_bytes(a.N), st>>>(a, tile_cols(a.N), log2N);
+  return check_launch("cgc_kernel(imag residue)");
 }
 
 }  // namespace kle

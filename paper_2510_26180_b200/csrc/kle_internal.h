@@ -154,6 +154,8 @@ struct CgcArgs {
   double* imag;             // optional [M] running max imaginary residue
   int32_t* active_count;    // optional device counter of still-active samples
   unsigned long long* red_slots;  // cluster path: [M][2] (max bits, arrival ticket), zero-initialised once
+  int full;                 // 1: imaginary-residue diagnostic (all N frequencies, no Hermitian
+                            // completion; writes only imag, never U / status)
   int M, N, nx, k, max_iters;
   double dT, tol;
 };
@@ -167,6 +169,8 @@ int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st);
 int cgc_grid(int M, int N, int nx);
 size_t cgc_scratch_doubles_per_cta(int N, int nx);
 int cgc_run(const CgcArgs& a, cudaStream_t st);
+size_t imag_residue_scratch_bytes(int M, int N, int nx);
+int imag_residue_run(const CgcArgs& a, cudaStream_t st);
 // large blocks (power-of-two N <= 1024, any nx): streaming FFT / solve / FFT kernels
 bool cgc_large_supported(int N, int nx);
 size_t cgc_large_scratch_bytes(int M, int N, int nx);
@@ -194,5 +198,8 @@ int shifted_tridiag(const double* sub, const double* dia, const double* sup, dou
                     const double* p, double* q, double* cwork, int nx, int nrhs, int32_t* status, cudaStream_t st);
 
 int axpby(const double* x, const double* y, double* out, double a, double b, size_t n, cudaStream_t st);
+
+int err_aggregate(const double* err, const int32_t* iters, int M, int N, int max_iters, int k_pad, int32_t* good,
+                  int32_t* counts, double* sums, cudaStream_t st);
 
 }  // namespace kle

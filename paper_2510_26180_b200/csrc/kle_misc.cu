@@ -292,4 +292,59 @@ int shifted_tridiag(const double* sub, const double* dia, const double* sup, dou
   return check_launch("shifted_tridiag_kernel");
 }
 
+// Harness aggregation (pintuq/experiments.py:314-334): over the "good"
+// samples (every recorded error vector finite), each sample's error vectors
+// err_hist[s][0..K_s][:] (K_s = iters[s], records past the stop are NaN) are
+// padded with their last record to k_max + 1 rows and averaged over samples.
+// The sums run over samples in id order per (k, n) entry; divided once by
+// n_good (by the caller) they are numpy's stack.mean(axis=0), bit for bit.
+__global__ void err_good_kernel(const double* __restrict__ err, const int32_t* __restrict__ iters, int M, int N,
+                                int K1, int32_t* __restrict__ good, int32_t* __restrict__ counts) {
+  const int s = blockIdx.x * blockDim.y + threadIdx.y;
+  if (s >= M) return;
+  int K = iters[s];
+  K = K < 0 ? 0 : (K >= K1 ? K1 - 1 : K);
+  const double* e = err + (size_t)s * K1 * N;
+  bool ok = true;
+  for (int j = threadIdx.x; j < (K + 1) * N; j += 32) ok = ok && isfinite(e[j]);
+  ok = __all_sync(KLE_FULL_MASK, ok);
+  if (threadIdx.x == 0) {
+    good[s] = ok ? 1 : 0;
+    if (ok) {
+      atomicAdd(&counts[0], 1);
+      atomicMax(&counts[1], K);
+    }
+  }
+}
+
+__global__ void err_sum_kernel(const double* __restrict__ err, const int32_t* __restrict__ iters,
+                               const int32_t* __restrict__ good, const int32_t* __restrict__ counts, int M, int N,
+                               int K1, int k_pad, double* __restrict__ sums) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K1 * N) return;
+  const int k = j / N, n = j - k * N;
+  const int kp = k_pad >= 0 ? k_pad : counts[1];
+  if (k > kp) {
+    sums[j] = __longlong_as_double(0x7ff8000000000000LL);
+    return;
+  }
+  double acc = 0.0;
+  for (int s = 0; s < M; ++s) {
+    if (!good[s]) continue;
+    int K = iters[s];
+    K = K < 0 ? 0 : (K >= K1 ? K1 - 1 : K);
+    acc += err[((size_t)s * K1 + (k < K ? k : K)) * N + n];
+  }
+  sums[j] = acc;
+}
+
+int err_aggregate(const double* err, const int32_t* iters, int M, int N, int max_iters, int k_pad, int32_t* good,
+                  int32_t* counts, double* sums, cudaStream_t st) {
+  const int K1 = max_iters + 1;
+  cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st);
+  if (M > 0) err_good_kernel<<<(M + 7) / 8, dim3(32, 8), 0, st>>>(err, iters, M, N, K1, good, counts);
+  err_sum_kernel<<<(K1 * N + 127) / 128, 128, 0, st>>>(err, iters, good, counts, M, N, K1, k_pad, sums);
+  return check_launch("err_aggregate");
+}
+
 }  // namespace kle

@@ -41,14 +41,17 @@ class KleCgcSolver:
         self._ws = None
 
     def solve(self, xi, keep_initial: bool = False, stop_on: str = "increment",
-              with_reference: bool = False) -> KleCgcResult:
+              with_reference: bool = False, diagnostics: bool = False) -> KleCgcResult:
         """xi: (M, d) host array or device tensor.
 
         ``stop_on="reference"`` (or ``with_reference``) computes the serial fine
         reference of every sample on the device and records the per-iteration
         errors against it, as the reference harness does for every solve
         (``_run_one_sample``, ``pintuq/experiments.py:212-235``: ``fine_reference``
-        then ``pcgc_solve(..., reference=, stop_on="reference")``)."""
+        then ``pcgc_solve(..., reference=, stop_on="reference")``); the
+        harness's mean-error tables are ``result.batch.error_summary(tol)``.
+        ``diagnostics`` records max_imag_residue per sample (an extra
+        full-spectrum three-step launch per iteration)."""
         xi_d = to_dev(xi).reshape(-1, self.model.parameter_dim)
         op = DeviceOperator.from_model(self.model, xi_d)
         reference = None
@@ -72,8 +75,12 @@ class KleCgcSolver:
             need = int(_lib.query("kle_pcgc_workspace_bytes", op.M, self.grid.n_coarse, self.model.nx))
             if self._ws.numel() < need:
                 self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
-        res = pcgc_solve_device(op, U, self.grid, self.cfg, self.tables, self._ws, reference=reference,
-                                stop_on=stop_on)
+        if isinstance(op, DeviceOperator2D):
+            res = pcgc_solve_device(op, U, self.grid, self.cfg, self.tables, self._ws, reference=reference,
+                                    stop_on=stop_on)
+        else:
+            res = pcgc_solve_device(op, U, self.grid, self.cfg, self.tables, self._ws, reference=reference,
+                                    stop_on=stop_on, diagnostics=diagnostics)
         return KleCgcResult(res, U0)
 
     @staticmethod

@@ -86,13 +86,34 @@ def shift_factors(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float
     return sfac
 
 
+def imag_residue_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float, r, prescaled=False,
+                        imag=None, status=None):
+    """max|Im u| of the reference's three-step solve (``pintuq/pcgc.py:170-172``)
+    for every sample: all N shifted systems solved independently and no
+    Hermitian completion (``kle_imag_residue_f64``), max-accumulated into
+    ``imag`` (M,). The production CGC kernels use the Hermitian symmetry and
+    return real fields, so this is a separate diagnostic launch."""
+    M, _, nx = r.shape
+    if imag is None:
+        imag = torch.zeros(M, dtype=torch.float64, device="cuda")
+    nbytes = int(_lib.query("kle_imag_residue_scratch_bytes", M, N, nx))
+    scratch = torch.empty(max(nbytes, 8), dtype=torch.uint8, device="cuda")
+    _lib.call("kle_imag_residue_f64", ptr(r.contiguous()), None if prescaled else ptr(tables.scaling),
+              ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia), ptr(op.off), ptr(status), M, N, nx, deltaT,
+              ptr(imag), ptr(scratch), nbytes, stream_ptr())
+    return imag
+
+
 def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: float, r, prescaled=False,
-                      sfac="auto"):
+                      sfac="auto", diagnostics: bool = True):
     """u = V (Lambda (x) I + dT I (x) A)^{-1} V^{-1} r for every sample;
-    r: (M, N, nx) device tensor. Returns (u, imag (M,))."""
+    r: (M, N, nx) device tensor. Returns (u, imag (M,)); ``imag`` is the
+    max_imag_residue diagnostic when ``diagnostics`` (else zeros)."""
     M, _, nx = r.shape
     u = empty(M, N, nx)
-    imag = empty(M)
+    imag = torch.zeros(M, dtype=torch.float64, device="cuda")
+    if diagnostics:
+        imag_residue_device(op, tables, N, deltaT, r, prescaled, imag)
     if isinstance(sfac, str):
         sfac = shift_factors(op, tables, N, deltaT)
     if sfac is not None:  # cluster path: per-sample reduction slots (zeroed by the call)
@@ -101,7 +122,7 @@ def three_step_device(op: DeviceOperator, tables: AlphaTables, N: int, deltaT: f
         scratch, nbytes = _cgc_scratch(M, N, nx)
     _lib.call("kle_three_step_f64", ptr(r.contiguous()), None if prescaled else ptr(tables.scaling),
               ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia), ptr(op.off), ptr(sfac), M, N, nx, deltaT,
-              ptr(u), ptr(imag), ptr(scratch), nbytes, stream_ptr())
+              ptr(u), None, ptr(scratch), nbytes, stream_ptr())
     return u, imag
 
 
@@ -267,9 +288,55 @@ class BatchResult:
     iters: "torch.Tensor"       # (M,) int32 iteration counts (len(records) - 1)
     status: "torch.Tensor"      # (M,) int32 SAMPLE_* words
     increments: "torch.Tensor"  # (M, max_iters) per-k increments, NaN past the stop
-    imag: "torch.Tensor"        # (M,) max imaginary residue
+    imag: "torch.Tensor"        # (M,) max imaginary residue (diagnostics=True), else zeros
     err_vs_ref: "torch.Tensor | None" = None  # (M, max_iters+1, N) err_n of record k (k = 0: guess), NaN past the stop
     max_err: "torch.Tensor | None" = None     # (M,) max error of the last record
+
+    def error_summary(self, tol: float, max_iters: int | None = None, group=None):
+        """The harness aggregation over this batch (``pintuq/experiments.py:
+        314-334``): ``(mean_vectors (k_max+1, N), mean_max_error (k_max+1,),
+        mean_iters)``. Error vectors of each good sample (all records finite)
+        are padded with their last record and averaged over samples on the
+        device (``kle_err_aggregate_f64``); ``mean_iters`` averages
+        ``iters_to_tol(tol)`` with unreached tolerances counted as
+        ``max_iters`` (the harness's cfg.max_iters). With a process ``group``
+        (sharded samples) the per-rank sums and counts are allreduced."""
+        if self.err_vs_ref is None:
+            raise ValueError("no reference errors were recorded")
+        import torch.distributed as dist
+
+        M, K1, N = self.err_vs_ref.shape
+        max_iters = K1 - 1 if max_iters is None else int(max_iters)
+        err = self.err_vs_ref.contiguous()
+        good = torch.empty(M, dtype=torch.int32, device="cuda")
+        counts = torch.zeros(2, dtype=torch.int32, device="cuda")
+        sums = empty(K1, N)
+
+        def aggregate(k_pad):
+            _lib.call("kle_err_aggregate_f64", ptr(err), ptr(self.iters), M, N, K1 - 1, k_pad, ptr(good),
+                      ptr(counts), ptr(sums), stream_ptr())
+
+        it = self.iters_to_tol(tol)
+        it = torch.where(it < 0, torch.full_like(it, max_iters), it).to(torch.float64)
+        sharded = group is not None or (dist.is_available() and dist.is_initialized())
+        aggregate(-1)
+        if sharded:  # pad every rank's samples to the global k_max, then sum sums and counts
+            kmax = counts[1:2].clone()
+            dist.all_reduce(kmax, op=dist.ReduceOp.MAX, group=group)
+            aggregate(int(kmax.item()))
+            stats = torch.stack([counts[0].to(torch.float64), it.sum(),
+                                 torch.tensor(float(M), device="cuda", dtype=torch.float64)])
+            dist.all_reduce(sums, group=group)
+            dist.all_reduce(stats, group=group)
+            n_good, k_max = float(stats[0].item()), int(kmax.item())
+            mean_iters = float((stats[1] / stats[2]).item()) if stats[2] > 0 else float("nan")
+        else:
+            n_good, k_max = float(counts[0].item()), int(counts[1].item())
+            mean_iters = float(it.mean().item()) if M else float("nan")
+        if n_good == 0:
+            return np.full((1, N), np.nan), np.array([np.nan]), mean_iters
+        mv = (sums[:k_max + 1] / n_good).cpu().numpy()
+        return mv, mv.max(axis=1), mean_iters
 
     def iters_to_tol(self, tol: float):
         """Per sample, the first k whose max error vs the reference is <= tol
@@ -308,12 +375,16 @@ class BatchResult:
 
 
 def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, tables: AlphaTables = None,
-                      workspace=None, reference=None, stop_on: str = "increment") -> BatchResult:
+                      workspace=None, reference=None, stop_on: str = "increment",
+                      diagnostics: bool = False) -> BatchResult:
     """The production loop: U (M, N, nx) device tensor is overwritten with the
     final states (``kle_pcgc_solve_f64``). ``reference`` (M, N, nx), e.g.
     ``fine_reference_batched``, adds the per-iteration error records of
     ``pcgc_solve(reference=...)``; ``stop_on="reference"`` stops each sample
-    at its first record with max error <= tol (``kle_pcgc_solve_ref_f64``)."""
+    at its first record with max error <= tol (``kle_pcgc_solve_ref_f64``).
+    ``diagnostics`` adds the per-iteration max_imag_residue diagnostic (an
+    extra full-spectrum three-step launch per iteration; ``imag`` is zeros
+    otherwise)."""
     from .twod import DeviceOperator2D, pcgc_solve_device2d
 
     if stop_on not in ("increment", "reference"):
@@ -336,12 +407,13 @@ def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, 
     status = torch.empty(M, dtype=torch.int32, device="cuda")
     iters = torch.empty(M, dtype=torch.int32, device="cuda")
     inc = empty(M, cfg.max_outer_iters)
-    imag = empty(M)
+    imag = torch.zeros(M, dtype=torch.float64, device="cuda")
+    imag_arg = ptr(imag) if diagnostics else None
     common = (ptr(U), ptr(op.u0), ptr(op.dia), ptr(op.off), ptr(op.blob(grid.deltat)), ptr(tables.scaling),
               ptr(tables.inv_scaling), ptr(tables.lam), M, N, nx, grid.n_fine_per_coarse, grid.t_final, cfg.alpha,
               op.g0, cfg.tol, cfg.max_outer_iters)
     if reference is None:
-        _lib.call("kle_pcgc_solve_f64", *common, ptr(status), ptr(iters), ptr(inc), ptr(imag), ptr(workspace),
+        _lib.call("kle_pcgc_solve_f64", *common, ptr(status), ptr(iters), ptr(inc), imag_arg, ptr(workspace),
                   nbytes, stream_ptr())
         return BatchResult(U, iters, status, inc, imag)
     ref = to_dev(reference).contiguous()
@@ -350,12 +422,12 @@ def pcgc_solve_device(op: DeviceOperator, U, grid: TimeGrid, cfg: SolverConfig, 
     err = empty(M, cfg.max_outer_iters + 1, N)
     me = empty(M)
     _lib.call("kle_pcgc_solve_ref_f64", *common, ptr(ref), int(stop_on == "reference"), ptr(status), ptr(iters),
-              ptr(inc), ptr(err), ptr(me), ptr(imag), ptr(workspace), nbytes, stream_ptr())
+              ptr(inc), ptr(err), ptr(me), imag_arg, ptr(workspace), nbytes, stream_ptr())
     return BatchResult(U, iters, status, inc, imag, err, me)
 
 
 def pcgc_solve_batched(model, xis, grid: TimeGrid, cfg: SolverConfig, init_states, reference=None,
-                       stop_on: str = "increment") -> BatchResult:
+                       stop_on: str = "increment", diagnostics: bool = False) -> BatchResult:
     """Batched ``pcgc_solve`` over M samples (``reference``: (M, N, nx) or
     ``"fine"`` for the batched serial fine reference of every sample)."""
     op = DeviceOperator.from_model(model, xis)
@@ -364,7 +436,7 @@ def pcgc_solve_batched(model, xis, grid: TimeGrid, cfg: SolverConfig, init_state
         from .propagators import fine_reference_batched
 
         reference = fine_reference_batched(op, grid)
-    return pcgc_solve_device(op, U, grid, cfg, reference=reference, stop_on=stop_on)
+    return pcgc_solve_device(op, U, grid, cfg, reference=reference, stop_on=stop_on, diagnostics=diagnostics)
 
 
 def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, init: CoarseTrajectory,
@@ -442,9 +514,10 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
                       None, ptr(inc), None, ptr(scratch), nbytes, stream_ptr())
         else:
             _fgr(op, tables, U, R, grid.n_fine_per_coarse, grid, cfg.alpha)
+            imag_residue_device(op, tables, N, dT, R, prescaled=True, imag=imag)
             _lib.call("kle_cgc_update_f64", ptr(R), ptr(U), ptr(tables.inv_scaling), ptr(tables.lam), ptr(op.dia),
                       ptr(op.off), ptr(sfac), 1, N, nx, dT, k, cfg.max_outer_iters, -1.0, None, None, ptr(inc),
-                      ptr(imag), None, ptr(scratch), nbytes, stream_ptr())
+                      None, None, ptr(scratch), nbytes, stream_ptr())
         host = U[0].cpu().numpy()
         increment = float(inc[0, k - 1].item())
         wall_ms = 1e3 * (time.perf_counter() - tic)

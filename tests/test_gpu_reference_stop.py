@@ -130,3 +130,50 @@ def test_kle_cgc_engine_harness_mode(cuda, golden):
                        [ParameterMap("identity", -np.inf, np.inf)] * 4, family="hermite")
     res = KleCgcSolver(model, grid, cfg, s).solve(g1["xi_all"][:8], stop_on="reference")
     _check(res.batch, g, "kle")
+
+
+def harness_aggregate(err_rows, iters_to_tol, max_iters):
+    """pintuq/experiments.py:314-334 verbatim in numpy over per-sample error
+    vectors (each (K_s+1, N), finite): pad with the last record, mean over
+    samples, row max; mean of iters_to_tol with None -> max_iters."""
+    k_max = max(ev.shape[0] for ev in err_rows)
+    stack = np.empty((len(err_rows), k_max, err_rows[0].shape[1]))
+    for i, ev in enumerate(err_rows):
+        stack[i] = np.vstack([ev, np.repeat(ev[-1:], k_max - ev.shape[0], axis=0)])
+    mv = stack.mean(axis=0)
+    its = [max_iters if t < 0 else t for t in iters_to_tol]
+    return mv, mv.max(axis=1), float(np.mean(its))
+
+
+@pytest.mark.parametrize("tag", ["kle", "rnd"])
+def test_mean_error_aggregation(cuda, golden, tag):
+    """BatchResult.error_summary (device padding + sample mean) equals the
+    harness aggregation of the same records bit for bit, and the reference's
+    own aggregation of its golden records within the record tolerance."""
+    import torch
+    from paper_2510_26180_b200.device import DeviceOperator
+    from paper_2510_26180_b200.pcgc import pcgc_solve_device
+    from paper_2510_26180_b200.propagators import fine_reference_batched
+
+    model, grid, cfg = c1_config()
+    g1, g = golden("c1"), golden("ref")
+    M = len(g[f"{tag}_iters"])
+    op = DeviceOperator.from_model(model, g1["xi_all"][:M])
+    ref = fine_reference_batched(op, grid)
+    init = g["rnd_init"] if tag == "rnd" else g1["U0"][:M]
+    U = torch.as_tensor(np.ascontiguousarray(init), device="cuda").clone()
+    res = pcgc_solve_device(op, U, grid, cfg, reference=ref, stop_on="reference")
+    mv, mme, mit = res.error_summary(cfg.tol, cfg.max_outer_iters)
+    iters = res.iters.cpu().numpy()
+    err = res.err_vs_ref.cpu().numpy()
+    own = harness_aggregate([err[i, :K + 1] for i, K in enumerate(iters)],
+                            res.iters_to_tol(cfg.tol).cpu().numpy(), cfg.max_outer_iters)
+    np.testing.assert_array_equal(mv, own[0])
+    np.testing.assert_array_equal(mme, own[1])
+    assert mit == own[2]
+    gold = harness_aggregate([g[f"{tag}_err"][i, :K + 1] for i, K in enumerate(g[f"{tag}_iters"])],
+                             g[f"{tag}_to_tol"], cfg.max_outer_iters)
+    np.testing.assert_allclose(mv, gold[0], rtol=0, atol=ATOL)
+    np.testing.assert_allclose(mme, gold[1], rtol=0, atol=ATOL)
+    assert mit == gold[2]
+    assert mv.shape[0] == int(g[f"{tag}_iters"].max()) + 1
