@@ -48,6 +48,16 @@ Outputs (np.savez_compressed):
            coarse_sweep_init (increment stop, tol 1e-8).
   c3.npz   2D model at the config-3 shape (n=127, N=32, J=16, d=10): one
            sample from coarse-sweep init (iteration count, increments, field).
+  c3b.npz  the same for eval samples 1..3.
+  c5full.npz  config 5 at full shape (nx 4095, N 1024, J 8), 2 samples x
+           alpha in {1e-1, 1e-2, 1e-4}: iteration counts, increments, imag
+           residues, final-field fingerprints.
+  c2sur.npz   config 2's surrogate built by the reference (2,048 points,
+           degree 3): KL spectrum, coefficients, U0 of 8 eval samples, and the
+           KLE-CGC of 4 of them.
+  legendre_{d1,ad}.npz / _pred.npz   the reference's own build_surrogate
+           (Legendre; affine / cos2pi maps) in its save_surrogate wire
+           format, with surrogate_predict at 6 seeded points.
 """
 from __future__ import annotations
 
@@ -486,8 +496,169 @@ def make_models():
     print(f"models done; diffusion-1d pcgc iters {it}")
 
 
+# ---------------------------------------------------------------------------
+# Full-shape goldens (round 2). The per-sample reference solves run in forked
+# worker processes over the host cores; every solve is the unmodified
+# reference's own coarse_sweep_init / pcgc_solve / surrogate_predict.
+# ---------------------------------------------------------------------------
+_G = {}
+
+
+def _pool(n=None):
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    return ProcessPoolExecutor(n or os.cpu_count(), mp_context=mp.get_context("fork"))
+
+
+def _coarse_then_pcgc(i):
+    model, grid, cfg, xi_all = _G["model"], _G["grid"], _G["cfg"], _G["xi"]
+    xi = rcore.ParameterSample(xi_all[i], id=i)
+    cs = rpar.coarse_sweep_init(model, xi, grid, cfg).states
+    return solve_one(model, grid, cfg, xi, cs)
+
+
+def _subsample(st):
+    """A committed fingerprint of a large final field: every 8th row of every
+    8th time slice, plus the per-slice sums and max norms (size-independent
+    checks of the whole field)."""
+    return st[::8, ::8].copy(), st.sum(axis=1), np.abs(st).max(axis=1)
+
+
+def make_c5full():
+    """BASELINE configs[4] at its full shape (nx 4095, N 1024, J 8): the
+    first two of the c5 bench's seeded samples, alpha in {1e-1, 1e-2, 1e-4},
+    from coarse_sweep_init: iteration counts, increments, max_imag_residue
+    and a fingerprint of the final fields (_subsample)."""
+    t0 = time.time()
+    model = RefLogNormalKL1D(nx=4095, d=4, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 1024, 8)
+    _, eval_rng, _ = rcore.RngStream(2718).split(3)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(2, 4))
+    out = {"xi": xi_all}
+    for alpha in (1e-1, 1e-2, 1e-4):
+        cfg = rcore.SolverConfig(alpha=alpha, tol=1e-8, max_outer_iters=60, seed=2718)
+        _G.update(model=model, grid=grid, cfg=cfg, xi=xi_all)
+        with _pool(2) as ex:
+            runs = list(ex.map(_coarse_then_pcgc, range(2)))
+        tag = f"a{-int(round(np.log10(alpha)))}"
+        sub = [_subsample(r[0]) for r in runs]
+        out[f"{tag}_sub"] = np.array([x[0] for x in sub])
+        out[f"{tag}_rowsum"] = np.array([x[1] for x in sub])
+        out[f"{tag}_rowmax"] = np.array([x[2] for x in sub])
+        out[f"{tag}_iters"] = np.array([r[1] for r in runs], np.int32)
+        incs = np.full((2, 60), np.nan)
+        for j, r in enumerate(runs):
+            incs[j, : len(r[2])] = r[2]
+        out[f"{tag}_incs"] = incs
+        out[f"{tag}_imag"] = np.array([r[3] for r in runs])
+        print(f"  c5full alpha {alpha:g}: iters {out[f'{tag}_iters'].tolist()} ({time.time() - t0:.0f}s)")
+    np.savez_compressed(OUT / "c5full.npz", **out)
+    print(f"c5full done in {time.time() - t0:.1f}s")
+
+
+def make_c3b():
+    """Config 3 at its full shape (n 127, N 32, J 16): eval samples 1..3 (c3.npz
+    holds sample 0), from coarse_sweep_init through the reference's SuperLU
+    paths: iteration counts, increments, final-field fingerprints."""
+    t0 = time.time()
+    n, N, J, d = 127, 32, 16, 10
+    model = RefLogNormalKL2D(n=n, d=d, sigma=0.5, ell=0.25)
+    grid = rcore.make_time_grid(1.0, N, J)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    _, eval_rng, _ = rcore.RngStream(2718).split(3)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(4, d))
+    _G.update(model=model, grid=grid, cfg=cfg, xi=xi_all)
+    with _pool(3) as ex:
+        runs = list(ex.map(_coarse_then_pcgc, [1, 2, 3]))
+    incs = np.full((3, 60), np.nan)
+    for j, r in enumerate(runs):
+        incs[j, : len(r[2])] = r[2]
+    np.savez_compressed(OUT / "c3b.npz", xi=xi_all[1:], final=np.array([r[0] for r in runs]),
+                        iters=np.array([r[1] for r in runs], np.int32), increments=incs)
+    print(f"c3b done in {time.time() - t0:.1f}s; iters {[r[1] for r in runs]}")
+
+
+def _snap(i):
+    model, grid, cfg, pts = _G["model"], _G["grid"], _G["cfg"], _G["train"]
+    xi = rcore.ParameterSample(pts[i], id=i)
+    init = rpar.coarse_sweep_init(model, xi, grid, cfg)   # collect_snapshots' `one` (surrogate.py:85-90)
+    return rpcgc.pcgc_solve(model, xi, grid, cfg, init, stop_on="increment").trajectory.states
+
+
+def _kle_one(i):
+    model, grid, cfg, s, xi_all = _G["model"], _G["grid"], _G["cfg"], _G["sur"], _G["xi"]
+    xi = rcore.ParameterSample(xi_all[i], id=i)
+    U0 = rsur.surrogate_predict(s, xi, model.initial_condition(xi)).states
+    return (U0,) + solve_one(model, grid, cfg, xi, U0)
+
+
+def make_c2sur():
+    """Config 2's own surrogate built by the reference: 2,048 seeded Gaussian
+    training points (RngStream(2718).split(3)[0]), PCGC snapshots from
+    coarse_sweep_init, snapshot KL at eps 1e-10, degree-3 Hermite least
+    squares (P = 165); then the KLE-CGC of the first 4 eval samples from its
+    surrogate_predict U0. Stores the KL spectrum, coefficients, U0 of 8 eval
+    samples and the 4 solves (the modes, 34.5 MB, are not committed)."""
+    t0 = time.time()
+    model = RefLogNormalKL1D(nx=511, d=8, sigma=0.5, ell=0.3)
+    grid = rcore.make_time_grid(1.0, 64, 64)
+    cfg = rcore.SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
+    train_rng, eval_rng, _ = rcore.RngStream(2718).split(3)
+    train = train_rng.normal(0.0, 1.0, size=(2048, 8))
+    _G.update(model=model, grid=grid, cfg=cfg, train=train)
+    with _pool() as ex:
+        fields = np.array(list(ex.map(_snap, range(len(train)), chunksize=8)))
+    print(f"  c2sur snapshots {time.time() - t0:.0f}s")
+    training = [rcore.ParameterSample(p, id=i) for i, p in enumerate(train)]
+    snap = rsur.make_snapshot_set(training, fields, model.cell_volume * grid.deltaT)
+    basis = rsur.kl_build(snap, 1e-10)
+    zeta = rsur.kl_coefficients(snap, basis)
+    coeffs, resid, deg = rsur.gpc_fit(train, zeta, 3, family="hermite")
+    s = rsur.KLGpcSurrogate(mean_field=snap.mean_field, eigenvalues=basis.retained.copy(), modes=basis.modes,
+                            coeffs=coeffs, degree=deg, maps=model.fit_maps(), family="hermite",
+                            cell_weight=snap.cell_weight)
+    xi_all = eval_rng.normal(0.0, 1.0, size=(8, 8))
+    U0 = np.array([rsur.surrogate_predict(s, rcore.ParameterSample(x, id=i), model.initial_condition(None)).states
+                   for i, x in enumerate(xi_all)])
+    _G.update(sur=s, xi=xi_all)
+    with _pool(4) as ex:
+        runs = list(ex.map(_kle_one, range(4)))
+    incs = np.full((4, 60), np.nan)
+    for j, r in enumerate(runs):
+        incs[j, : len(r[3])] = r[3]
+    np.savez_compressed(OUT / "c2sur.npz", xi=xi_all, eigenvalues=s.eigenvalues, coeffs=s.coeffs, m_q=s.m_q,
+                        degree=deg, U0=U0, final=np.array([r[1] for r in runs]),
+                        iters=np.array([r[2] for r in runs], np.int32), increments=incs,
+                        energy_ratio=basis.energy_ratio)
+    print(f"c2sur done in {time.time() - t0:.1f}s; m_q {s.m_q}; iters {[r[2] for r in runs]}")
+
+
+def make_legendre():
+    """The reference's own build_surrogate (Legendre family, the models'
+    fit_maps: affine for Diffusion1D, cos2pi for AdvectionDiffusion2D), saved
+    with the reference's save_surrogate (the wire format), and its
+    surrogate_predict at seeded evaluation points."""
+    t0 = time.time()
+    for tag, model, N, J in (("d1", rmodels.Diffusion1D(h=1.0 / 32.0), 8, 8),
+                             ("ad", rmodels.AdvectionDiffusion2D(h=1.0 / 12.0), 8, 4)):
+        grid = rcore.make_time_grid(1.0, N, J)
+        cfg = rcore.SolverConfig(alpha=0.1, tol=1e-10, max_outer_iters=60, seed=2718)
+        train_rng, eval_rng, _ = rcore.RngStream(2718).split(3)
+        training = model.sample_parameters(12, train_rng)
+        s = rsur.build_surrogate(model, grid, cfg, training, eps_kl=1e-10, degree=3)
+        rsur.save_surrogate(s, OUT / f"legendre_{tag}.npz")
+        evals = model.sample_parameters(6, eval_rng)
+        pred = np.array([rsur.surrogate_predict(s, xi, model.initial_condition(xi)).states for xi in evals])
+        np.savez_compressed(OUT / f"legendre_{tag}_pred.npz", xi=np.array([x.values for x in evals]), pred=pred,
+                            family=s.family, maps=np.array([m.kind for m in s.maps]))
+    print(f"legendre done in {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para", "nl", "models"]
+    which = sys.argv[1:] or ["c1", "c2", "c5s", "c3s", "c3", "ref", "para", "nl", "models", "legendre", "c5full",
+                             "c3b", "c2sur"]
     for w in which:
         {"c1": make_c1, "c2": make_c2, "c5s": make_c5s, "c3s": make_c3s, "c3": make_c3, "ref": make_ref,
-         "para": make_para, "nl": make_nl, "models": make_models}[w]()
+         "para": make_para, "nl": make_nl, "models": make_models, "legendre": make_legendre,
+         "c5full": make_c5full, "c3b": make_c3b, "c2sur": make_c2sur}[w]()

@@ -10,9 +10,9 @@ against the batched CPU oracle:
 - the converged iterate is a fixed point of one more correction up to tol;
 - the moments equal numpy's two-pass mean / variance of the returned fields.
 
-The surrogate is a degree-2 Hermite fit on 512 seeded training samples
-(the config's is degree 3 on 2,048; the initial guess only changes the
-iteration counts, which the oracle check covers).
+The surrogate is the config's own: a degree-3 Hermite fit on 2,048 seeded
+training samples, built on the device (compared with the reference's build
+in test_gpu_surrogate.py).
 """
 import numpy as np
 import pytest
@@ -35,8 +35,8 @@ def c2_run(cuda):
     grid = make_time_grid(1.0, 64, 64)
     cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=2718)
     train_rng, eval_rng, _ = RngStream(2718).split(3)
-    train = [ParameterSample(p, id=i) for i, p in enumerate(train_rng.normal(0.0, 1.0, size=(512, 8)))]
-    sur = build_surrogate(model, grid, cfg, train, eps_kl=1e-10, degree=2)
+    train = [ParameterSample(p, id=i) for i, p in enumerate(train_rng.normal(0.0, 1.0, size=(2048, 8)))]
+    sur = build_surrogate(model, grid, cfg, train, eps_kl=1e-10, degree=3)
     xi = eval_rng.normal(0.0, 1.0, size=(M, 8))
     solver = KleCgcSolver(model, grid, cfg, sur)
     res = solver.solve(xi, keep_initial=True)

@@ -205,3 +205,22 @@ def test_model_2d_contract():
     assert np.all(np.diff(m.kl_eigenvalues) <= 0)
     u0 = m.initial_condition()
     assert u0.shape == (81,) and abs(u0.max() - np.sin(np.pi * 0.5) ** 2) < 1e-12
+
+
+def test_legendre_host_tables_match_reference_build(golden):
+    """The reference's own build_surrogate output (Legendre family; affine and
+    cos2pi maps), read through load_surrogate (its save_surrogate wire
+    format): the host Legendre table + ParameterMap.apply reproduce its
+    surrogate_predict."""
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.surrogate import gpc_eval_basis, load_surrogate
+
+    root = Path(__file__).resolve().parent / "golden"
+    for tag in ("d1", "ad"):
+        s = load_surrogate(root / f"legendre_{tag}.npz")
+        p = golden(f"legendre_{tag}_pred")
+        for x, want in zip(p["xi"], p["pred"]):
+            psi = gpc_eval_basis(s.map_parameters(ParameterSample(x, id=0)), s.degree, s.family)
+            w = np.sqrt(s.eigenvalues) * (s.coeffs @ psi)
+            pred = s.mean_field + (w @ s.modes.reshape(s.m_q, -1)).reshape(s.mean_field.shape)
+            np.testing.assert_array_equal(pred, want)
