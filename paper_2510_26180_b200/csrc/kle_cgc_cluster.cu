@@ -318,7 +318,13 @@ struct ClShape {
 #ifndef KLE_CGC_MINB
 #define KLE_CGC_MINB 2  // 288 threads, pivots in registers: 2 CTAs/SM (measured; 1 CTA without spills is slower)
 #endif
-  static constexpr int MINB = (NT <= 160 || SP) ? 3 : KLE_CGC_MINB;
+#ifndef KLE_CGC_MINB_SP
+#define KLE_CGC_MINB_SP 3  // CTAs/SM bound for the shared-memory-pivot shapes (N = 64: 288 threads)
+#endif
+#ifndef KLE_CGC_MINB_SMALL
+#define KLE_CGC_MINB_SMALL 8  // N <= 16 (<= 96 threads): 80 registers, 8 CTAs/SM (c4: 4.88 -> 3.55 ms / 131k samples)
+#endif
+  static constexpr int MINB = NT <= 96 ? KLE_CGC_MINB_SMALL : ((NT <= 160 || SP) ? KLE_CGC_MINB_SP : KLE_CGC_MINB);
   static constexpr size_t UOLD = SP ? 0 : (size_t)N * RB;           // doubles
   static constexpr size_t PIV = SP ? (size_t)2 * NF * RB : 0;       // doubles: [NF][RB] complex, swizzled rows
   static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * N * HC + UOLD + PIV + RB + 2 + N + 2 * N +
