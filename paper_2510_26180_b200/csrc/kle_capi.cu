@@ -235,6 +235,11 @@ int kle_cgc_update_f64(const double* R, double* U, const double* inv_scaling, co
   a.max_iters = max_iters;
   a.dT = dT;
   a.tol = tol;
+  if (sfac && !imag && cgc_small_supported(N, nx)) {  // N <= 16, nx <= 128: one CTA per sample (kle_iter_small.cu)
+    IterSmallArgs ia{U, R, nullptr, nullptr, dia, off, sfac, nullptr, inv_scaling, status, iters, inc_hist,
+                     active_count, M, N, nx, 1, k, max_iters, 0.0, dT, 0.0, 0.0, tol};
+    return cgc_small_run(ia, KLE_STREAM(stream));
+  }
   if (sfac) {
     // the slots return to zero after every launch (last CTA resets the max; the
     // ticket counts modulo the cluster size), so callers zero them once
@@ -349,6 +354,9 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
     if (pipes > M) pipes = M > 0 ? M : 1;
   }
   if (imag) pipes = 1;  // the diagnostic's scratch serves one pipeline
+  // small blocks (configs 1 / 4): fused iteration kernel, unless the imag
+  // diagnostic (which reads the CGC right-hand side R from global) is on
+  const bool fused = clustered && !imag && iter_small_supported(N, nx);
   const FineLayoutRT lay = fine_layout(nx);
   struct Pipe {
     int m0, M, k;
@@ -391,6 +399,17 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
     const double* dq = dia + o * nx;
     const double* eq = off + o * nx;
     int32_t* sq = status + o;
+    if (fused) {  // the whole iteration in one kernel (kle_iter_small.cu)
+      cudaMemsetAsync(q.count_d, 0, sizeof(int32_t), q.st);
+      IterSmallArgs ia{Uq, nullptr, u0, fine_blob + o * lay.doubles, dq, eq, sfac + o * shift_factor_doubles(1, N, nx), scaling,
+                       inv_scaling, sq, iters + o, inc_hist ? inc_hist + o * max_iters : nullptr, q.count_d,
+                       q.M, N, nx, J, k, max_iters, dt, dT, g0, alpha, cgc_tol};
+      KLE_TRY(iter_small_run(ia, q.st));
+      if (q.sc != q.st) {  // the pipeline's bookkeeping (count read-back, reference errors) runs on sc
+        cudaEventRecord(q.fdone, q.st);
+        cudaStreamWaitEvent(q.sc, q.fdone, 0);
+      }
+    } else {
     KLE_TRY(kle_fgr_f64(Uq, u0, nullptr, nullptr, R + o * N * nx, fine_blob + o * lay.doubles, dq, eq, scaling, sq,
                         q.M, N, nx, J, dt, dT, g0, alpha, q.st));
     if (q.sc != q.st) {
@@ -407,6 +426,7 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
                                cgc_tol, sq, iters + o, inc_hist ? inc_hist + o * max_iters : nullptr,
                                nullptr, q.count_d, cs,
                                clustered ? (size_t)q.M * 16 : cgc_scratch_bytes, q.sc));
+    }
     if (ref)
       KLE_TRY(err_ref(Uq, ref + o * N * nx, q.M, N, nx, k, max_iters, tol, stop_ref, sq, iters + o, q.count_d,
                       err_hist ? err_hist + o * (size_t)(max_iters + 1) * N : nullptr, max_err ? max_err + o : nullptr,

@@ -20,7 +20,8 @@
 #define KLE_FINE_LAZY 0  // lazy-stitch step (kle_fine.cuh); measured slower, kept for A/B
 #endif
 #ifndef KLE_FINE_CS
-#define KLE_FINE_CS 0  // chunk products from shared memory (be_steps_cs): measured slower (5.79 vs 5.43 ms), A/B only
+#define KLE_FINE_CS 0  // chunk products from shared memory (be_steps_cs) for every variant: slower at c2
+                       // (5.79 vs 5.43 ms), A/B only; the one-warp variants (NT = 32) always use them
 #endif
 
 namespace kle {
@@ -135,16 +136,16 @@ struct FgrSmem {
   static constexpr int LD = NXP;
   static constexpr int SWZ = (MR < 16 ? MR : 16) - 1;
   __device__ __forceinline__ static int pidx(int row) { return row ^ ((row / MR) & SWZ); }
-  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8 + (KLE_FINE_CS ? 3 * NXP : 0)) * sizeof(double);
+  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8 + 3 * NXP) * sizeof(double);
 };
 
 template <int MR, int P, int R, int NT, bool PIPE>
 #ifdef KLE_FGR_MINB_ALL  // tuning override
-#define KLE_FGR_MINB(MR, R) KLE_FGR_MINB_ALL
+#define KLE_FGR_MINB(MR, R, NT) KLE_FGR_MINB_ALL
 #else
-#define KLE_FGR_MINB(MR, R) ((MR) * (R) > 32 ? 2 : 3)
+#define KLE_FGR_MINB(MR, R, NT) ((NT) == 32 ? 8 : ((MR) * (R) > 32 ? 2 : 3))
 #endif
-__global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a) {
+__global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArgs a) {
   using L = FineLayout<MR, P>;
   constexpr int SLOTS = 32 / P;
   constexpr int NC = (NT / 32) * SLOTS * R;  // subintervals per CTA
@@ -192,7 +193,10 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
     fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
     const double hg = a.dt * a.g0;
     double* cs = ee + LD + MR;  // [3][MR][P] chunk products (KLE_FINE_CS)
-    if constexpr (KLE_FINE_CS && !PIPE && !KLE_FINE_LAZY) {
+    // chunk products from shared memory: the one-warp R = 4 variant (c4: 234 registers, 8 chains per
+    // SMSP; 6.16 -> 5.17 ms per 131k-sample launch), or every variant under KLE_FINE_CS
+    constexpr bool CS = (KLE_FINE_CS || NT == 32) && !PIPE && !KLE_FINE_LAZY;
+    if constexpr (CS) {
       if (w == 0 && slot == 0) chunk_products<MR, P>(cs, fac, k, hg);
     }
     asm volatile("cp.async.wait_group 1;\n" ::);
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R)) fgr_kernel(FgrArgs a)
       }
     if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
     else if constexpr (KLE_FINE_LAZY) be_steps_lazy<MR, P, R>(x, fac, a.ffac + (size_t)s * L::DOUBLES, k, a.J, hg);
-    else if constexpr (KLE_FINE_CS) be_steps_cs<MR, P, R>(x, fac, k, a.J, cs);
+    else if constexpr (CS) be_steps_cs<MR, P, R>(x, fac, k, a.J, cs);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -363,12 +367,13 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs a) {
 // host-side dispatch
 // ---------------------------------------------------------------------------
 // PI: 0 = eager step, 128 threads; 1 = software-pipelined step; 2 = eager, 64
-// threads (finer CTA granularity: R = 3 wastes 2/66 instead of 8/72 slots at N = 64)
+// threads (finer CTA granularity: R = 3 wastes 2/66 instead of 8/72 slots at N = 64);
+// 3 = eager, 32 threads (one warp: N = 16 with R = 4)
 template <int MR, int P, int R_, int PI = 0>
 struct FineInst {
   static constexpr bool PIPE = PI == 1;
   static constexpr int R = R_;
-  static constexpr int NT = PI == 2 ? 64 : 128;
+  static constexpr int NT = PI == 3 ? 32 : (PI == 2 ? 64 : 128);
   static constexpr int NC = (NT / 32) * (32 / P) * R;
 
   static int factor(const double* dia, const double* off, double* blob, int M, int nx, double h,
@@ -400,7 +405,7 @@ struct FineVariant {
   int MR, P, R, pipe, kind = 0;  // kind 1 (shared-memory factors): `pipe` is the min CTAs/SM bound
 };
 static const FineVariant kVariants[] = {
-    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {16, 8, 2, 2},  {16, 32, 3, 2}, {32, 32, 2, 0},  // defaults
+    {1, 16, 4, 0},  {2, 16, 4, 0},  {4, 16, 4, 0},  {16, 8, 4, 3},  {16, 32, 3, 2}, {32, 32, 2, 0},  // defaults
     {8, 16, 2, 1},  {4, 32, 4, 0},  {8, 16, 4, 1},  {8, 16, 4, 0},  {16, 16, 2, 0}, {8, 32, 4, 0},
     {32, 16, 2, 0}, {16, 32, 2, 0}, {16, 32, 2, 1}, {16, 32, 4, 1}, {16, 32, 4, 0}, {4, 32, 4, 1},
     {16, 32, 3, 4, 1}, {16, 32, 3, 3, 1}, {16, 32, 2, 4, 1}, {16, 32, 4, 3, 1},  // 18..21 shared-memory factors
@@ -409,6 +414,7 @@ static const FineVariant kVariants[] = {
     {32, 16, 4, 3, 1}, {32, 16, 3, 3, 1}, {32, 16, 2, 4, 1}, {32, 16, 4, 2, 1},  // 28..31
     {16, 32, 3, 0}, {8, 16, 2, 2}, {16, 32, 2, 2},                                // 32..34
     {16, 8, 2, 0},  {16, 8, 3, 0},  {16, 8, 2, 2},  {16, 8, 3, 2},  {8, 8, 4, 0},   // 35..39 (nx <= 128)
+    {16, 8, 4, 3},  {16, 8, 2, 3},  {16, 32, 4, 3}, {16, 32, 3, 3},                 // 40..43 (one-warp CTAs)
 };
 static const int kNumDefaults = 6;
 
@@ -442,6 +448,10 @@ static const int kNumDefaults = 6;
   KLE_FINE_DISPATCH(16, 8, 3, 0, CALL)    \
   KLE_FINE_DISPATCH(16, 8, 2, 2, CALL)    \
   KLE_FINE_DISPATCH(16, 8, 3, 2, CALL)    \
+  KLE_FINE_DISPATCH(16, 8, 4, 3, CALL)    \
+  KLE_FINE_DISPATCH(16, 8, 2, 3, CALL)    \
+  KLE_FINE_DISPATCH(16, 32, 4, 3, CALL)   \
+  KLE_FINE_DISPATCH(16, 32, 3, 3, CALL)   \
   KLE_FINE_DISPATCH(8, 8, 4, 0, CALL)
 
 FineLayoutRT fine_layout(int nx) {

@@ -202,4 +202,28 @@ int axpby(const double* x, const double* y, double* out, double a, double b, siz
 int err_aggregate(const double* err, const int32_t* iters, int M, int N, int max_iters, int k_pad, int32_t* good,
                   int32_t* counts, double* sums, cudaStream_t st);
 
+// Fused PCGC iteration for small blocks (kle_iter_small.cu): fine sweeps,
+// CGC right-hand side and three-step solve of one sample per CTA.
+struct IterSmallArgs {
+  double* U;                // [M][N][nx] in: U^k, out: U^{k+1}
+  const double* R;          // CGC-only variant: [M][N][nx] alpha-scaled right-hand sides (fgr_kernel)
+  const double* u0;         // [nx]
+  const double* ffac;       // fine factor blobs (layout 16 x 8) [M][doubles]
+  const double* dia;        // [M][nx]
+  const double* off;        // [M][nx]
+  const double* sfac;       // shift pivots [M][N/2+1][nx] complex
+  const double* scaling;    // [N]
+  const double* inv_scaling;// [N]
+  int32_t* status;          // [M]
+  int32_t* iters;           // [M]
+  double* inc_hist;         // optional [M][max_iters]
+  int32_t* active_count;    // optional
+  int M, N, nx, J, k, max_iters;
+  double dt, dT, g0, alpha, tol;
+};
+bool iter_small_supported(int N, int nx);
+int iter_small_run(const IterSmallArgs& a, cudaStream_t st);
+bool cgc_small_supported(int N, int nx);
+int cgc_small_run(const IterSmallArgs& a, cudaStream_t st);
+
 }  // namespace kle

@@ -7,15 +7,16 @@ from paper_2510_26180_b200 import LogNormalKL1D, make_time_grid, _lib
 from paper_2510_26180_b200.device import DeviceOperator, AlphaTables, empty, ptr, stream_ptr
 from paper_2510_26180_b200.pcgc import build_alpha_circulant
 
-VARS = [(1, 16, 4, 0), (2, 16, 4, 0), (4, 16, 4, 0), (16, 8, 2, 2), (16, 32, 3, 2), (32, 32, 2, 0),
+VARS = [(1, 16, 4, 0), (2, 16, 4, 0), (4, 16, 4, 0), (16, 8, 4, 3), (16, 32, 3, 2), (32, 32, 2, 0),
         (8, 16, 2, 1), (4, 32, 4, 0), (8, 16, 4, 1), (8, 16, 4, 0), (16, 16, 2, 0), (8, 32, 4, 0),
         (32, 16, 2, 0), (16, 32, 2, 0), (16, 32, 2, 1), (16, 32, 4, 1), (16, 32, 4, 0), (4, 32, 4, 1),
         (16, 32, 3, 's4'), (16, 32, 3, 's3'), (16, 32, 2, 's4'), (16, 32, 4, 's3'), (8, 16, 2, 's4'), (8, 16, 4, 's4'),
         (8, 32, 4, 's4'), (32, 16, 2, 's2'), (32, 16, 1, 's3'), (16, 32, 3, 's2'),
         (32, 16, 4, 's3'), (32, 16, 3, 's3'), (32, 16, 2, 's4'), (32, 16, 4, 's2'),
         (16, 32, 3, 0), (8, 16, 2, 2), (16, 32, 2, 2), (16, 8, 2, 0), (16, 8, 3, 0), (16, 8, 2, 2), (16, 8, 3, 2),
-        (8, 8, 4, 0)]
-for nx, N, J, M in ([(511, 64, 64, 4096), (127, 16, 32, 65536)] if len(sys.argv) < 2 else [(127, 16, 32, 65536)]):
+        (8, 8, 4, 0), (16, 8, 4, 3), (16, 8, 2, 3), (16, 32, 4, 3), (16, 32, 3, 3)]
+for nx, N, J, M in ([(511, 64, 64, 4096), (127, 16, 32, 65536)] if len(sys.argv) < 2 else
+                   [(127, 16, 32, 65536)] if sys.argv[1] == 'c4' else [(511, 64, 64, 8192)]):
     model = LogNormalKL1D(nx=nx, d=4)
     grid = make_time_grid(1.0, N, J)
     xi = np.random.default_rng(0).normal(size=(M, 4))
@@ -23,7 +24,10 @@ for nx, N, J, M in ([(511, 64, 64, 4096), (127, 16, 32, 65536)] if len(sys.argv)
     U = torch.rand(M, N, nx, dtype=torch.float64, device="cuda")
     R = empty(M, N, nx)
     ref = None
+    only = [int(v) for v in sys.argv[2].split(',')] if len(sys.argv) > 2 else None
     for v, (MR, P, Rr, pipe) in enumerate(VARS):
+        if only is not None and v not in only:
+            continue
         if MR * P < nx or MR * P >= 4 * nx:
             continue
         os.environ["KLE_FINE_VARIANT"] = str(v)
