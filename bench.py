@@ -72,6 +72,8 @@ def parse():
     p.add_argument("--samples", type=int, default=0,
                    help="total samples (default: the config's M; c3: evaluation samples, default 4096)")
     p.add_argument("--train", type=int, default=1024, help="c3: surrogate training samples (config: 1024)")
+    p.add_argument("--solver", default="direct", choices=["direct", "krylov"],
+                   help="c3: banded direct factors or matrix-free PCG/COCG")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -722,6 +724,15 @@ def run_c5(args):
                                "sample": f"first {cores} samples at alpha = 0.1, coarse-sweep init, one per process "
                                          f"(oracle/ref_port: SuperLU, solve_banded, np.fft), {wall:.1f} s wall",
                                "iters": cpu_it}
+    peaks = load_peaks()
+    a4 = out["alphas"]["0.0001"]
+    out["roofline"] = {"kernel": "large-block CGC (cgcl_fwd / cgcl_solve / cgcl_inv kernels, one launch)",
+                       "bound": "hbm", "achieved": a4["cgc_compulsory_gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                       "frac": a4["cgc_compulsory_gbs"] / peaks["hbm_gbs"],
+                       "algorithmic": "24 B per (n, i) per sample-iteration (read R, read U, write U) x the chunk",
+                       "fine_sweep_fp64_frac": (a4["fgr_tflops_alg"] / peaks["fp64_tflops"]
+                                                if peaks.get("fp64_tflops") else None),
+                       "traffic": None}
     print(json.dumps(out), flush=True)
 
 
@@ -761,6 +772,7 @@ def run_c3(args):
 
     n, N, J, d = 127, 32, 16, 10
     M = args.samples or 4096
+    os.environ["KLE_2D_SOLVER"] = args.solver
     model = LogNormalKL2D(n=n, d=d, sigma=0.5, ell=0.25)
     grid = make_time_grid(1.0, N, J)
     cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60, seed=SEED)
@@ -810,6 +822,7 @@ def run_c3(args):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     dof = float(it.sum()) * N * J * model.nx
+    roof = c3_roofline(model, grid, cfg, xi_d, solver)
     cpu = None
     if not args.no_cpu_baseline:
         from concurrent.futures import ProcessPoolExecutor
@@ -845,15 +858,57 @@ def run_c3(args):
             "data": "synthetic (seeded N(0,1) KL coordinates; no dataset exists)",
             "config": {"workload": f"BASELINE configs[2] (c3): 2D 127x127 5-point, N={N}, J={J}, d={d}, "
                                    f"Hermite p=2 on {args.train} training samples, alpha={cfg.alpha}, tol={cfg.tol}; "
-                                   f"direct banded LDL^T solves (the reference's SuperLU semantics)",
+                                   + ("direct banded LDL^T solves (the reference's SuperLU semantics)"
+                                      if args.solver == "direct" else
+                                      "matrix-free Jacobi-PCG / COCG solves to relative residual 1e-13"),
                        "samples": M, "l2": "state 8*M*N*nx bytes + factors 16*17*nx*n bytes per sample > L2"},
             "fine_dof_updates_per_s": dof / (ms * 1e-3), "avg_outer_iters": float(it.mean()),
             "max_outer_iters": int(it.max()), "all_converged": bool(np.all(status == 1)),
             "surrogate_build_s": t_build, "surrogate": {"m_q": sur.m_q, "P": solver.surrogate.P},
-            "e2e": {"value": M / (e2e_ms * 1e-3), "unit": "solves/s", "h2d_bytes_per_step": int(xi_host.nbytes),
+            "e2e": {"value": M / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xi_host.nbytes),
                     "d2h_bytes_per_step": int(hm.numel() * 8), "ms_per_step": e2e_ms},
-            "clocks": clocks.summary(), "cpu_baseline": cpu}
+            "roofline": roof, "clocks": clocks.summary(), "cpu_baseline": cpu}
     print(json.dumps(line))
+
+
+def c3_roofline(model, grid, cfg, xi_d, solver):
+    """The dominant c3 kernel: the fused fine sweep + rhs of one batch
+    (direct: fine2d_tma_kernel, banded forward/backward substitutions with the
+    far parts on DMMA; krylov: cg_fine_kernel). Algorithmic work per
+    backward-Euler step and DOF: 4 n + 1 flop (n-wide banded forward and
+    backward substitutions + the D^-1 scale), x M N J nx per launch, against
+    the measured DMMA peak; HBM fraction of the factor stream beside it."""
+    import torch
+
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, empty
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant
+
+    op_all = DeviceOperator.from_model(model, xi_d)
+    B = min(op_all.M, 192)
+    op = op_all.select(0, B)
+    N, J, n, nx = grid.n_coarse, grid.n_fine_per_coarse, model.n, model.nx
+    tables = AlphaTables(build_alpha_circulant(N, cfg.alpha))
+    U = solver.surrogate.predict(xi_d[:B])
+    R = empty(B, N, nx)
+    op.fgr(U, tables, grid, cfg.alpha, R)  # warm-up (+ factor / restage, untimed)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    op.fgr(U, tables, grid, cfg.alpha, R)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    peaks = load_peaks()
+    flops = (4.0 * n + 1.0) * B * N * J * nx
+    tf = flops / (ms * 1e-3) / 1e12
+    factor_bytes = 2 * 8.0 * nx * (n + 9) * B * N * J  # the staged band chunks, streamed once per step and direction
+    return {"kernel": "fine2d_tma_kernel (banded L D L^T substitutions, DMMA far parts, TMA-streamed factors)"
+                      if op.solver == "direct" else "cg_fine_kernel (Jacobi-PCG, matrix-free 5-point)",
+            "bound": "tensor(dmma)", "achieved": tf, "peak": peaks.get("dmma_tflops"), "unit": "TFLOP/s",
+            "frac": tf / peaks["dmma_tflops"] if peaks.get("dmma_tflops") else None,
+            "algorithmic": "(4 n + 1) flop per DOF and backward-Euler step x M N J nx per launch",
+            "hbm_frac": (factor_bytes / (ms * 1e-3) / 1e9) / peaks["hbm_gbs"] if op.solver == "direct" else None,
+            "ms_per_launch": ms, "samples_per_launch": B, "traffic": None}
 
 
 # ---------------------------------------------------------------------------

@@ -277,6 +277,31 @@ int kle_shifted_tridiag_solve_f64(const double* sub, const double* dia, const do
                                   double lam_im, double dT, const double* p, double* q, double* cwork, int nx,
                                   int nrhs, int32_t* status, void* stream);
 
+/* Matrix-free Krylov 2D solvers (the alternative to the banded
+ * factors above, selected by twod.DeviceOperator2D(solver="krylov")):
+ * Jacobi-PCG for every backward-Euler step of (I + h A) (warm started from the
+ * previous step) and Jacobi-COCG for the shifted systems (lambda_f I + dT A),
+ * applied matrix-free from (dia, ex, ey), each to ||r||_2 <= rtol ||b||_2
+ * (max_its iterations at most; *its, optional, accumulates the iteration
+ * count). fgr: the fused fine sweeps + CGC right-hand side of
+ * kle_2d_fgr_staged_f64 (F_given / F_out optional); sweep: out[s][q] = J
+ * steps of size h from start[s][q] (nseg = 1); cgc: kle_2d_cgc_f64 with the
+ * COCG solves (work: kle_2d_cgc_krylov_work_doubles, zeroed before the first
+ * call). n <= 128. */
+int kle_2d_fgr_krylov_f64(const double* U, const double* u0, const double* F_given, const double* dia,
+                          const double* ex, const double* ey, const double* scaling, const int32_t* status, int M,
+                          int N, int n, int J, double dt, double dT, double g0, double alpha, double rtol,
+                          int max_its, double* R, double* F_out, long long* its, void* stream);
+int kle_2d_sweep_krylov_f64(const double* start, const double* dia, const double* ex, const double* ey, int M, int Q,
+                            int n, int J, double h, double g0, double rtol, int max_its, double* out, long long* its,
+                            void* stream);
+size_t kle_2d_cgc_krylov_work_doubles(int M, int N, int n);
+int kle_2d_cgc_krylov_f64(const double* R, const double* load_scale, double* U, double* Uout, const double* dia,
+                          const double* ex, const double* ey, const double* lam, const double* inv_scaling, int M,
+                          int N, int n, int k, int max_iters, double tol, int32_t* status, int32_t* iters,
+                          double* inc, double* inc_hist, int32_t* active_count, double dT, double rtol, int max_its,
+                          double* work, size_t work_doubles, long long* its, void* stream);
+
 /* gpc_basis_matrix (pintuq/surrogate.py:208-248) at the mapped points
  * (KLGpcSurrogate.map_parameters, ParameterMap.apply pintuq/models.py:39-45):
  * Psi[M][P] from raw xi[M][d]; family 0 = probabilists' Hermite

@@ -65,6 +65,12 @@ _SIGS = {
     "kle_2d_sweep_staged_f64": ([_p, _p, _i, _i, _i, _i, _i, _d, _d, _p, _z, _p, _p], _i),
     "kle_2d_cgc_work_doubles": ([_i, _i, _i], _z),
     "kle_2d_cgc_f64": ([_p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _p, _p, _p, _p, _p, _p, _z, _p], _i),
+    "kle_2d_fgr_krylov_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _d, _d, _i, _p, _p, _p,
+                               _p], _i),
+    "kle_2d_sweep_krylov_f64": ([_p, _p, _p, _p, _i, _i, _i, _i, _d, _d, _d, _i, _p, _p, _p], _i),
+    "kle_2d_cgc_krylov_work_doubles": ([_i, _i, _i], _z),
+    "kle_2d_cgc_krylov_f64": ([_p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _d, _p, _p, _p, _p, _p, _d,
+                               _d, _i, _p, _z, _p, _p], _i),
     "kle_gpc_basis_f64": ([_p, _i, _i, _i, _i, _p, _p, _i, _p, _p, _p], _i),
     "kle_gpc_eval_f64": ([_p, _i, _i, _p, _p, _i, _p, _p], _i),
     "kle_gemm_f64": ([_p, _p, _p, _p, _i, _i, _i, _i, _p], _i),

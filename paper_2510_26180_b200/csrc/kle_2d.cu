@@ -1023,3 +1023,62 @@ extern "C" int kle_2d_cgc_f64(const double* R, const double* load_scale, double*
                                                                 inc_hist, active_count);
   return check_launch("status2d_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Matrix-free Krylov variants (kle_2d_krylov.cu): PCG fine sweeps and COCG
+// shifted solves in place of the banded factors.
+// ---------------------------------------------------------------------------
+extern "C" int kle_2d_fgr_krylov_f64(const double* U, const double* u0, const double* F_given, const double* dia,
+                                     const double* ex, const double* ey, const double* scaling,
+                                     const int32_t* status, int M, int N, int n, int J, double dt, double dT,
+                                     double g0, double alpha, double rtol, int max_its, double* R, double* F_out,
+                                     long long* its, void* stream) {
+  if (M < 0 || N < 1 || n < 1 || n > 128 || J < 1 || !(rtol > 0) || max_its < 1)
+    return set_error(KLE_ERR_INVALID, "fgr2d_krylov: bad arguments");
+  Kry2dArgs a{U, u0, F_given, dia, ex, ey, scaling, status, F_out, R, its, M, N, n, J, max_its, 1, dt, dT, g0, alpha,
+              rtol};
+  return kry2d_fine(a, KLE2D_STREAM(stream));
+}
+
+extern "C" int kle_2d_sweep_krylov_f64(const double* start, const double* dia, const double* ex, const double* ey,
+                                       int M, int Q, int n, int J, double h, double g0, double rtol, int max_its,
+                                       double* out, long long* its, void* stream) {
+  if (M < 0 || Q < 1 || n < 1 || n > 128 || J < 1 || !(rtol > 0) || max_its < 1)
+    return set_error(KLE_ERR_INVALID, "sweep2d_krylov: bad arguments");
+  Kry2dArgs a{start, nullptr, nullptr, dia, ex, ey, nullptr, nullptr, out, nullptr, its, M, Q, n, J, max_its, 0, h,
+              0.0, g0, 0.0, rtol};
+  return kry2d_fine(a, KLE2D_STREAM(stream));
+}
+
+extern "C" size_t kle_2d_cgc_krylov_work_doubles(int M, int N, int n) {
+  return (M <= 0 || N <= 0 || n <= 0) ? 0 : 6 * (size_t)M * (N / 2 + 1) * n * n + (size_t)M;
+}
+
+extern "C" int kle_2d_cgc_krylov_f64(const double* R, const double* load_scale, double* U, double* Uout,
+                                     const double* dia, const double* ex, const double* ey, const double* lam,
+                                     const double* inv_scaling, int M, int N, int n, int k, int max_iters,
+                                     double tol, int32_t* status, int32_t* iters, double* inc, double* inc_hist,
+                                     int32_t* active_count, double dT, double rtol, int max_its, double* work,
+                                     size_t work_doubles, long long* its, void* stream) {
+  if (M < 0 || N < 2 || (N & 1) || n < 1 || n > 128 || !(rtol > 0) || max_its < 1)
+    return set_error(KLE_ERR_INVALID, "cgc2d_krylov: bad arguments (N even)");
+  if (M == 0) return KLE_OK;
+  if (work_doubles < kle_2d_cgc_krylov_work_doubles(M, N, n)) return set_error(KLE_ERR_WORKSPACE, "cgc2d_krylov: workspace");
+  const int nx = n * n, NF = N / 2 + 1;
+  cudaStream_t st = KLE2D_STREAM(stream);
+  Cplx* P = reinterpret_cast<Cplx*>(work);
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(work + 2 * (size_t)M * NF * nx);
+  Cplx* kw = reinterpret_cast<Cplx*>(work + 2 * (size_t)M * NF * nx + M);
+  const long long tot = (long long)M * nx;
+  dft_fwd_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(R, load_scale, status, M, N, nx, P);
+  if (int e = check_launch("dft_fwd_kernel")) return e;
+  if (int e = kry2d_shift_solve(P, dia, ex, ey, lam, status, M, NF, n, dT, rtol, max_its, kw, its, st)) return e;
+  const bool track = status != nullptr && U != nullptr && Uout == nullptr;
+  dft_inv_update_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(P, inv_scaling, status, M, N, nx, U, Uout,
+                                                                         track ? bits : nullptr);
+  if (int e = check_launch("dft_inv_update_kernel")) return e;
+  if (!track) return KLE_OK;
+  status2d_kernel<<<(unsigned)((M + 127) / 128), 128, 0, st>>>(bits, M, k, max_iters, tol, status, iters, inc,
+                                                                inc_hist, active_count);
+  return check_launch("status2d_kernel");
+}

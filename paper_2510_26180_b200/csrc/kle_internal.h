@@ -226,4 +226,27 @@ int iter_small_run(const IterSmallArgs& a, cudaStream_t st);
 bool cgc_small_supported(int N, int nx);
 int cgc_small_run(const IterSmallArgs& a, cudaStream_t st);
 
+// Matrix-free Krylov 2D solvers (kle_2d_krylov.cu).
+struct Kry2dArgs {
+  const double* start;      // start_from_u: the iterate U [M][Q][nx] (system q starts at u0 / U_{q-1},
+                            // and prev rows of the CGC rhs come from it); else starts [M][Q][nx]
+  const double* u0;         // [nx]
+  const double* F_given;    // optional [M][Q][nx]: skip the sweeps, rhs epilogue from these F ends
+  const double* dia;        // [M][nx]
+  const double* ex;         // [M][nx]
+  const double* ey;         // [M][nx]
+  const double* scaling;    // [Q] (rhs epilogue)
+  const int32_t* status;    // optional [M]
+  double* F_out;            // optional [M][Q][nx]
+  double* R;                // optional [M][Q][nx]: scaling_q ((I + dT A) F_q - prev_q)
+  long long* its;           // optional: total CG iterations (atomic)
+  int M, Q, n, J, max_its, start_from_u;
+  double h, dT, g0, alpha, rtol;
+};
+int kry2d_fine(const Kry2dArgs& a, cudaStream_t st);
+struct Cplx;
+int kry2d_shift_solve(Cplx* P, const double* dia, const double* ex, const double* ey, const double* lam,
+                      const int32_t* status, int M, int NF, int n, double dT, double rtol, int max_its, Cplx* work,
+                      long long* its, cudaStream_t st);
+
 }  // namespace kle

@@ -58,6 +58,20 @@ def fine_layout(nx: int):
     return MR.value, P.value, nd.value
 
 
+def constant_source(g) -> float:
+    """g0 of a source g(t) = g0 * ones that is constant in time and uniform in
+    space, else NotImplementedError. Probed at the interval ends and at
+    irrational interior points (a source such as t (1 - t) w agrees at t = 0
+    and t = 1 only)."""
+    g_a = np.asarray(g(0.0), dtype=float)
+    for t in (1.0, 0.5, 0.1234567890123, 0.7071067811865476, 3.0):
+        if not np.array_equal(g_a, np.asarray(g(t), dtype=float)):
+            raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
+    if g_a.size and not np.all(g_a == g_a.flat[0]):
+        raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
+    return float(g_a.flat[0]) if g_a.size else 0.0
+
+
 def tridiagonal_of(model, xi):
     """(dia, off, g0) of a tridiagonal plugin's operator, via its own
     ``linear_system`` (host-side model evaluation, as in the reference)."""
@@ -76,16 +90,7 @@ def tridiagonal_of(model, xi):
         if not np.array_equal(lo, up):
             raise NotImplementedError("the device path supports symmetric operators only")
         off[:-1] = up
-    # the source must be constant in time and uniform in space: probed at the
-    # interval ends and at irrational interior points (a source such as
-    # t(1-t) w agrees at t = 0 and t = 1 only)
-    g_a = np.asarray(g(0.0), dtype=float)
-    for t in (1.0, 0.5, 0.1234567890123, 0.7071067811865476, 3.0):
-        if not np.array_equal(g_a, np.asarray(g(t), dtype=float)):
-            raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
-    if not np.all(g_a == g_a[0]):
-        raise NotImplementedError("the device path needs a constant, uniform source g(t) = g0")
-    return dia, off, float(g_a[0])
+    return dia, off, constant_source(g)
 
 
 def shared_initial_condition(model, xis):

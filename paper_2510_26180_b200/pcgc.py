@@ -473,11 +473,13 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     from .twod import DeviceOperator2D
 
     is2d = isinstance(op, DeviceOperator2D)
+    krylov2d = is2d and op.solver == "krylov"
     if is2d:
         if N % 2:
             raise NotImplementedError("the 2D CGC needs an even number of subintervals")
-        fac2d = op.shifted_factors(tables, N, grid.deltaT)
-        nbytes = int(_lib.query("kle_2d_cgc_work_doubles", 1, N, op.n))
+        fac2d = None if krylov2d else op.shifted_factors(tables, N, grid.deltaT)
+        nbytes = int(_lib.query("kle_2d_cgc_krylov_work_doubles" if krylov2d else "kle_2d_cgc_work_doubles", 1, N,
+                                op.n))
         scratch = torch.zeros(max(nbytes, 1), dtype=torch.float64, device="cuda")
     else:
         sfac = shift_factors(op, tables, N, grid.deltaT)
@@ -507,7 +509,13 @@ def pcgc_solve(model, xi: ParameterSample, grid: TimeGrid, cfg: SolverConfig, in
     for k in range(1, cfg.max_outer_iters + 1):
         tic = time.perf_counter()
         # tol < 0 keeps the device from freezing the sample; the stop test is ours
-        if is2d:
+        if krylov2d:
+            from .twod import cgc_krylov
+
+            op.fgr(U, tables, grid, cfg.alpha, R, status=status)
+            cgc_krylov(op, tables, N, dT, R, U=U, k=k, max_iters=cfg.max_outer_iters, tol=-1.0, status=status,
+                       iters=iters, inc_hist=inc, work=scratch)
+        elif is2d:
             op.fgr(U, tables, grid, cfg.alpha, R, status=status)
             _lib.call("kle_2d_cgc_f64", ptr(R), None, ptr(U), None, ptr(fac2d[0]), ptr(fac2d[1]),
                       ptr(tables.inv_scaling), 1, N, op.n, k, cfg.max_outer_iters, -1.0, ptr(status), ptr(iters),

@@ -224,3 +224,27 @@ def test_legendre_host_tables_match_reference_build(golden):
             w = np.sqrt(s.eigenvalues) * (s.coeffs @ psi)
             pred = s.mean_field + (w @ s.modes.reshape(s.m_q, -1)).reshape(s.mean_field.shape)
             np.testing.assert_array_equal(pred, want)
+
+
+def test_constant_source_and_shared_initial_condition():
+    """The device path takes g(t) = g0 and one u0 per batch: a source that is
+    only constant at t = 0 and t = 1, or a parameter-dependent initial state,
+    must raise instead of being silently replaced."""
+    from paper_2510_26180_b200 import ParameterSample
+    from paper_2510_26180_b200.device import constant_source, shared_initial_condition
+
+    w = np.ones(5)
+    assert constant_source(lambda t: 2.5 * w) == 2.5
+    with pytest.raises(NotImplementedError):
+        constant_source(lambda t: t * (1.0 - t) * w)
+    with pytest.raises(NotImplementedError):
+        constant_source(lambda t: np.arange(5.0))
+
+    class M:
+        def initial_condition(self, xi):
+            return np.full(3, xi.values[0] if xi is not None else 0.0)
+
+    xs = [ParameterSample(np.array([1.0]), id=0), ParameterSample(np.array([1.0]), id=1)]
+    np.testing.assert_array_equal(shared_initial_condition(M(), xs), np.ones(3))
+    with pytest.raises(NotImplementedError):
+        shared_initial_condition(M(), xs + [ParameterSample(np.array([2.0]), id=2)])
