@@ -88,6 +88,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
 }
 
+// Cluster barrier for distributed-shared-memory exchanges only: the release is
+// restricted to this CTA's shared memory and the acquire to shared::cluster, so
+// it lowers to MEMBAR.ALL.CTA around UCGABAR instead of the MEMBAR.ALL.GPU of
+// cluster.sync() (no global-memory data crosses these barriers; the sample's
+// cross-CTA increment reduction uses its own acq_rel atomics).
+__device__ __forceinline__ void cluster_sync_smem() {
+  asm volatile(
+      "fence.release.sync_restrict::shared::cta.cluster;\n"
+      "barrier.cluster.arrive.relaxed;\n"
+      "barrier.cluster.wait;\n"
+      "fence.acquire.sync_restrict::shared::cluster.cluster;\n" ::: "memory");
+}
+
 template <int LOGN>
 __device__ __forceinline__ int brev(int n) {
   return LOGN == 0 ? 0 : (int)(__brev((unsigned)n) >> (32 - LOGN));
@@ -210,6 +223,41 @@ __device__ void fft4step(Cplx* t, const Cplx* tw) {
   __syncthreads();
 }
 
+// The same four-step FFT as fft4step for one column held in registers (N <=
+// 16): the same DFTs, twiddles and output order, so the results are bitwise
+// those of the shared-memory tile passes; one shared-memory store (forward)
+// or load (inverse) per element instead of four passes over the tile.
+template <int LOGN, int S>
+__device__ __forceinline__ void reg_fft(Cplx (&x)[1 << LOGN], const Cplx* tw) {
+  constexpr int N = 1 << LOGN;
+  constexpr int N1 = 1 << ((LOGN + 1) / 2), N2 = N / N1;
+  Cplx y[N];
+#pragma unroll
+  for (int n1 = 0; n1 < N1; ++n1) {
+    Cplx v[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) v[n2] = x[n1 + N1 * n2];
+    SmallDft<N2, S>::run(v);
+#pragma unroll
+    for (int k2 = 1; k2 < N2; ++k2) {
+      Cplx w = tw[(n1 * k2) & (N - 1)];
+      if (S > 0) w.im = -w.im;
+      v[k2] = cmul(v[k2], w);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) y[n1 + N1 * k2] = v[k2];
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < N2; ++k2) {
+    Cplx w[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) w[n1] = y[n1 + N1 * k2];
+    SmallDft<N1, S>::run(w);
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) x[k2 + N2 * k1] = w[k1];
+  }
+}
+
 // pivots 1/beta_i of (lambda_f I + dT A), f = 0..N/2, layout [s][f][i].
 // One CTA per sample: thread f runs the sequential complex recurrence
 // (factor_shifted, pintuq/pcgc.py:112-135) over the rows in chunks of SF_CH,
@@ -311,6 +359,12 @@ struct ClShape {
   static constexpr int N = 1 << LOGN, NF = N / 2 + 1, RB = CL_LANES * MR, HC = RB / 2;
   static constexpr int NT = ((NF * CL_LANES + 31) / 32) * 32;  // one 8-lane group per frequency
   static constexpr int NSTEP = NT / RB;                         // column-fixed sweeps (0: generic loop)
+#ifndef KLE_CGC_REGFFT
+#define KLE_CGC_REGFFT 0  // 1: N <= 16 column FFTs in registers, one thread per packed column (A/B:
+                          // bitwise equal, but 7.33 vs 3.39 ms per 131k c4 launch: 32 threads per CTA
+                          // serialise the loads and FFTs that 96 share in the tile passes)
+#endif
+  static constexpr bool REGFFT = LOGN <= 4 && KLE_CGC_REGFFT && NT >= RB / 2;
 #ifndef KLE_CGC_SP
 #define KLE_CGC_SP 1  // pivots in shared memory, old U re-read from global: 3 CTAs/SM at 288 threads
 #endif
@@ -359,7 +413,17 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   const int row0 = c * RB;
   CGC_T(0);
   // ---- phase 0: prefetch --------------------------------------------------
-  if constexpr (NSTEP > 0) {  // each thread keeps one column; rows n = tid/RB + m*NSTEP
+  Cplx zc[K::REGFFT ? N : 1];  // REGFFT: column tid of the packed block, rows row0+tid (re) and row0+tid+HC (im)
+  if constexpr (K::REGFFT) {
+    if (tid < HC) {
+      const int ra = row0 + tid, rb = ra + HC;
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        zc[n].re = ra < nx ? a.R[sb + (size_t)n * nx + ra] : 0.0;
+        zc[n].im = rb < nx ? a.R[sb + (size_t)n * nx + rb] : 0.0;
+      }
+    }
+  } else if constexpr (NSTEP > 0) {  // each thread keeps one column; rows n = tid/RB + m*NSTEP
     if (tid < NSTEP * RB) {
       const int col = tid % RB, row = row0 + col, ci = col % HC, part = col / HC;
       for (int n = tid / RB; n < N; n += NSTEP) {
@@ -413,14 +477,30 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   cp_async_wait_all();
   __syncthreads();
   CGC_T(1);
-  if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
-    for (int e = tid; e < N * RB; e += NT) {
-      const int n = e / RB, col = e % RB;
-      reinterpret_cast<double*>(&tile[tix<MR, HC>(n, col % HC)])[col / HC] *= a.load_scale[n];
+  if constexpr (K::REGFFT) {
+    if (tid < HC) {
+      if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          zc[n].re *= a.load_scale[n];
+          zc[n].im *= a.load_scale[n];
+        }
+      }
+      reg_fft<LOGN, -1>(zc, tw);
+#pragma unroll
+      for (int n = 0; n < N; ++n) tile[tix<MR, HC>(n, tid)] = zc[n];
     }
     __syncthreads();
+  } else {
+    if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
+      for (int e = tid; e < N * RB; e += NT) {
+        const int n = e / RB, col = e % RB;
+        reinterpret_cast<double*>(&tile[tix<MR, HC>(n, col % HC)])[col / HC] *= a.load_scale[n];
+      }
+      __syncthreads();
+    }
+    fft4step<LOGN, HC, -1, MR>(tile, tw);
   }
-  fft4step<LOGN, HC, -1, MR>(tile, tw);
   CGC_T(2);
 
   // ---- one frequency per 8-lane group: (lambda_f I + dT A) q = p_f ---------
@@ -467,7 +547,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     fwd[2 * f + 1] = B;
   }
   CGC_T(3);
-  cluster.sync();
+  cluster_sync_smem();
   CGC_T(4);
   Cplx Yc;
   {  // composite of the blocks q < c, q = k (+ 8) per lane, then a lane butterfly
@@ -523,7 +603,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     bwd[2 * f + 1] = T;
   }
   CGC_T(5);
-  cluster.sync();  // also: every thread has read its inputs from the tile
+  cluster_sync_smem();  // also: every thread has read its inputs from the tile
   CGC_T(6);
   Cplx Xc;
   {  // composite of the blocks q > c (the nearest block applied last)
@@ -552,8 +632,8 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
       y[j] = cfma(sg, Xin, y[j]);
     }
   }
-  // every CTA has done its last DSMEM read
-  asm volatile("barrier.cluster.arrive;\n" ::: "memory");
+  // every CTA has done its last DSMEM read (completed before the relaxed arrive)
+  asm volatile("fence.release.sync_restrict::shared::cta.cluster;\nbarrier.cluster.arrive.relaxed;\n" ::: "memory");
   // pack W_f = q(col) + i q(col + HC): lanes k < 4 hold the first half rows
 #pragma unroll
   for (int j = 0; j < MR; ++j) {
@@ -567,7 +647,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
   __syncthreads();
   // the pivots are dead now: stream the column's old values into their space
   // while the inverse FFT runs (each thread loads exactly what it reads later)
-  constexpr bool UPRE = K::SP && NSTEP > 0 && KLE_CGC_UPRE;
+  constexpr bool UPRE = K::SP && NSTEP > 0 && KLE_CGC_UPRE && !K::REGFFT;
   double* uold_p = reinterpret_cast<double*>(piv);  // [N][RB]
   if constexpr (UPRE) {
     if (a.U && tid < NSTEP * RB && row0 + tid % RB < nx) {
@@ -575,7 +655,7 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
       for (int n = tid / RB; n < N; n += NSTEP) cp_async8(uold_p + n * RB + col, a.U + sb + (size_t)n * nx + row0 + col);
     }
   }
-  fft4step<LOGN, HC, +1, MR>(tile, tw);
+  if constexpr (!K::REGFFT) fft4step<LOGN, HC, +1, MR>(tile, tw);
   CGC_T(7);
   // ---- update ----------------------------------------------------------------
   const double rsN = 1.0 / sqrt((double)N);
@@ -593,7 +673,37 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     }
     out[sb + (size_t)n * nx + row] = u;
   };
-  if constexpr (NSTEP > 0) {
+  if constexpr (K::REGFFT) {  // inverse column FFT in registers, then the column's two rows
+    if (tid < HC) {
+      const int ra = row0 + tid, rb = ra + HC;
+#pragma unroll
+      for (int n = 0; n < N; ++n) zc[n] = tile[tix<MR, HC>(n, tid)];
+      reg_fft<LOGN, +1>(zc, tw);
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        // the old values: each row's load precedes its store (out may alias U)
+        const double uan = (track && ra < nx) ? a.U[sb + (size_t)n * nx + ra] : 0.0;
+        const double ubn = (track && rb < nx) ? a.U[sb + (size_t)n * nx + rb] : 0.0;
+        const double u0v = (zc[n].re * rsN) * isc[n], u1v = (zc[n].im * rsN) * isc[n];
+        if (ra < nx) {
+          if (track) {
+            const double d = fabs(u0v - uan);
+            incmax = fmax(incmax, d);
+            bad |= (d != d);
+          }
+          out[sb + (size_t)n * nx + ra] = u0v;
+        }
+        if (rb < nx) {
+          if (track) {
+            const double d = fabs(u1v - ubn);
+            incmax = fmax(incmax, d);
+            bad |= (d != d);
+          }
+          out[sb + (size_t)n * nx + rb] = u1v;
+        }
+      }
+    }
+  } else if constexpr (NSTEP > 0) {
     if (tid < NSTEP * RB) {
       const int col = tid % RB, row = row0 + col;
       if (row < nx) {
@@ -644,10 +754,11 @@ __global__ void __launch_bounds__(ClShape<LOGN, MR>::NT, ClShape<LOGN, MR>::MINB
     // (and +NaN) order like their bit patterns.
     unsigned long long* slot = a.red_slots + 2 * (size_t)s;
     atomicMax(slot, (unsigned long long)__double_as_longlong(r1));
-    __threadfence();
-    const unsigned long long ticket = atomicAdd(slot + 1, 1ULL);
+    // the ticket is an acq_rel atomic: it releases this CTA's max (program order)
+    // and, for the last arriver, acquires every other CTA's (no separate fences)
+    unsigned long long ticket;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(ticket) : "l"(slot + 1), "l"(1ULL) : "memory");
     if ((ticket + 1) % (unsigned long long)CL == 0) {
-      __threadfence();
       const double inc = __longlong_as_double((long long)atomicExch(slot, 0ULL));
       if (a.inc) a.inc[s] = inc;
       if (a.inc_hist) a.inc_hist[(size_t)s * a.max_iters + (a.k - 1)] = inc;
