@@ -138,6 +138,74 @@ __device__ void fft4(Cplx* t, const Cplx* tw) {
   __syncthreads();
 }
 
+// (lambda_f I + dT A) q = p for one frequency, partitioned over an 8-lane group
+// (lane k owns rows r0 .. r0 + MR - 1, r0 = 16 k): chunk-local LDL^T passes
+// with the precomputed pivots 1/beta (piv(jj) = pivot of row r0 + jj, jj >= -1),
+// stitched by 3-stage affine lane scans (the cluster kernel's recurrences with
+// the whole system inside one group). off[jj] = dT * A[r0+jj-1][r0+jj].
+template <class PivFn>
+__device__ __forceinline__ void freq_solve(Cplx (&y)[MR], int k, const double* off, PivFn piv) {
+  auto lj = [&](int j) -> Cplx {  // l_r = dT off_{r-1} / beta_{r-1}
+    const double E = off[j];
+    const Cplx ip = piv(j - 1);
+    return {E * ip.re, E * ip.im};
+  };
+  Cplx A = {1.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const Cplx l = lj(j);
+    if (j > 0) y[j] = cfma({-l.re, -l.im}, y[j - 1], y[j]);
+    A = cneg_mul(l, A);
+  }
+  Cplx B = y[MR - 1];
+#pragma unroll
+  for (int d = 1; d < CLN; d <<= 1) {
+    const Cplx Ao = shfl_up_c(A, d), Bo = shfl_up_c(B, d);
+    if (k >= d) {
+      B = cfma(A, Bo, B);
+      A = cmul(A, Ao);
+    }
+  }
+  Cplx Be = shfl_up_c(B, 1);
+  if (k == 0) Be = {0.0, 0.0};
+  {
+    Cplx pi = {1.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      pi = cneg_mul(lj(j), pi);
+      y[j] = cmul(cfma(pi, Be, y[j]), piv(j));
+    }
+  }
+  const double En = off[MR];
+  const Cplx ibl = piv(MR - 1);
+  const Cplx lnext = {En * ibl.re, En * ibl.im};
+  Cplx S = {1.0, 0.0};
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const Cplx ln = (j == MR - 1) ? lnext : lj(j + 1);
+    if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
+    S = cneg_mul(ln, S);
+  }
+  Cplx T = y[0];
+#pragma unroll
+  for (int d = 1; d < CLN; d <<= 1) {
+    const Cplx So = shfl_down_c(S, d), To = shfl_down_c(T, d);
+    if (k + d < CLN) {
+      T = cfma(S, To, T);
+      S = cmul(S, So);
+    }
+  }
+  Cplx Te = shfl_down_c(T, 1);
+  if (k == CLN - 1) Te = {0.0, 0.0};
+  Cplx sg = {1.0, 0.0};
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const Cplx ln = (j == MR - 1) ? lnext : lj(j + 1);
+    sg = cneg_mul(ln, sg);
+    y[j] = cfma(sg, Te, y[j]);
+  }
+}
+
 template <int LOGN, bool FUSE>
 struct Shape {
   static constexpr int N = 1 << LOGN, NF = N / 2 + 1;
@@ -312,69 +380,9 @@ __global__ void __launch_bounds__(NT, FUSE ? KLE_ITS_MINB : KLE_CGS_MINB) iter_s
       if (col < HC) y[j] = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};  // (Z_f + conj Z_-f)/2
       else y[j] = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};           // (Z_f - conj Z_-f)/(2i)
     }
-    auto ibv = [&](int r) -> Cplx { return pf[pix(r)]; };
-    auto lj = [&](int j) -> Cplx {  // l_r = dT off_{r-1} / beta_{r-1}
-      const int r = r0 + j;
-      const double E = offs[r];
-      const Cplx ip = r > 0 ? ibv(r - 1) : Cplx{0.0, 0.0};
-      return {E * ip.re, E * ip.im};
-    };
-    Cplx A = {1.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < MR; ++j) {
-      const Cplx l = lj(j);
-      if (j > 0) y[j] = cfma({-l.re, -l.im}, y[j - 1], y[j]);
-      A = cneg_mul(l, A);
-    }
-    Cplx B = y[MR - 1];
-#pragma unroll
-    for (int d = 1; d < CLN; d <<= 1) {
-      const Cplx Ao = shfl_up_c(A, d), Bo = shfl_up_c(B, d);
-      if (k >= d) {
-        B = cfma(A, Bo, B);
-        A = cmul(A, Ao);
-      }
-    }
-    Cplx Be = shfl_up_c(B, 1);
-    if (k == 0) Be = {0.0, 0.0};
-    {
-      Cplx pi = {1.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < MR; ++j) {
-        pi = cneg_mul(lj(j), pi);
-        y[j] = cmul(cfma(pi, Be, y[j]), ibv(r0 + j));
-      }
-    }
-    const double En = offs[r0 + MR];
-    const Cplx ibl = ibv(r0 + MR - 1);
-    const Cplx lnext = {En * ibl.re, En * ibl.im};
-    Cplx S = {1.0, 0.0};
-#pragma unroll
-    for (int j = MR - 1; j >= 0; --j) {
-      const Cplx ln = (j == MR - 1) ? lnext : lj(j + 1);
-      if (j < MR - 1) y[j] = cfma({-ln.re, -ln.im}, y[j + 1], y[j]);
-      S = cneg_mul(ln, S);
-    }
-    Cplx T = y[0];
-#pragma unroll
-    for (int d = 1; d < CLN; d <<= 1) {
-      const Cplx So = shfl_down_c(S, d), To = shfl_down_c(T, d);
-      if (k + d < CLN) {
-        T = cfma(S, To, T);
-        S = cmul(S, So);
-      }
-    }
-    Cplx Te = shfl_down_c(T, 1);
-    if (k == CLN - 1) Te = {0.0, 0.0};
-    {
-      Cplx sg = {1.0, 0.0};
-#pragma unroll
-      for (int j = MR - 1; j >= 0; --j) {
-        const Cplx ln = (j == MR - 1) ? lnext : lj(j + 1);
-        sg = cneg_mul(ln, sg);
-        y[j] = cfma(sg, Te, y[j]);
-      }
-    }
+    freq_solve(y, k, offs + r0, [&](int jj) -> Cplx {  // pivot of row r0 + jj (jj >= -1)
+      return (r0 + jj >= 0) ? pf[pix(r0 + jj)] : Cplx{0.0, 0.0};
+    });
     __syncthreads();  // every group has read its p_f, p_{N-f} from the tile
     // pack W_f = q(col) + i q(col + HC) (and the mirror W_{N-f}): lanes k < 4 hold the first half
 #pragma unroll
@@ -439,6 +447,255 @@ __global__ void __launch_bounds__(NT, FUSE ? KLE_ITS_MINB : KLE_CGS_MINB) iter_s
   }
 }
 
+// ---------------------------------------------------------------------------
+// One WARP per sample (N = 16): the whole iteration warp-synchronous (only
+// __syncwarp), so the latency-bound FFT / shifted-solve phases of one warp
+// overlap the FP64-bound sweeps of the other warps on the SM:
+//   sweeps: 4 slots x R = 4 subintervals, 8 lanes x 16 rows each (the
+//           fgr_kernel<16, 8, 4, 32> step with shared-memory chunk products);
+//   rhs:    into the warp's packed tile [16][64];
+//   FFT:    four-step over the tile, 8 tasks per lane and pass;
+//   solve:  3 rounds of 4 frequency groups (f = 4 rho + lane / 8 <= 8), the
+//           lane's 17 pivots in registers (from global: 16 B x 17);
+//   update: lane = packed columns lane and lane + 32, old U from global.
+// ---------------------------------------------------------------------------
+namespace wv {
+constexpr int N = 16, LOGN = 4, NF = 9, R = 4;
+__device__ __forceinline__ void syncw() { __syncwarp(KLE_FULL_MASK); }
+
+// four-step FFT over the [N][HC] tile by one warp (same DFTs/twiddles/order as fft4)
+template <int S>
+__device__ void fft_warp(Cplx* t, const Cplx* tw, int lane) {
+  constexpr int N1 = 4, N2 = 4;
+  for (int task = lane; task < N1 * HC; task += 32) {
+    const int n1 = task / HC, c = task % HC;
+    Cplx v[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) v[n2] = t[tix(n1 + N1 * n2, c)];
+    Dft<N2, S>::run(v);
+#pragma unroll
+    for (int k2 = 1; k2 < N2; ++k2) {
+      Cplx w = tw[(n1 * k2) & (N - 1)];
+      if (S > 0) w.im = -w.im;
+      v[k2] = cmul(v[k2], w);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) t[tix(n1 + N1 * k2, c)] = v[k2];
+  }
+  syncw();
+  // pass 2: every lane reads all 8 of its tasks' inputs before any store (the
+  // stores permute rows: k2 + N2 k1 overwrites inputs of other tasks)
+  Cplx w[8][N1];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int task = lane + 32 * r;
+    const int k2 = task / HC, c = task % HC;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) w[r][n1] = t[tix(n1 + N1 * k2, c)];
+    Dft<N1, S>::run(w[r]);
+  }
+  syncw();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int task = lane + 32 * r;
+    const int k2 = task / HC, c = task % HC;
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) t[tix(k2 + N2 * k1, c)] = w[r][k1];
+  }
+  syncw();
+}
+}  // namespace wv
+
+struct WarpSmem {  // doubles, per warp (one warp per CTA)
+  static constexpr int O_TILE = 0;                        // [16][64] complex
+  static constexpr int O_CS = O_TILE + 2 * 16 * HC;       // [3][16][8] chunk products
+  static constexpr int O_OFS = O_CS + 3 * MR * P;         // [RB + 2]: dT * off[row - 1]
+  static constexpr int O_TW = O_OFS + RB + 2;             // [16] complex
+  static constexpr int O_ISC = O_TW + 2 * 16;             // [16]
+  static constexpr size_t BYTES = sizeof(double) * (size_t)(O_ISC + 16);
+};
+
+__global__ void __launch_bounds__(32, 8) iter_warp_kernel(IterSmallArgs a) {
+  using L = FineLayout<MR, P>;
+  constexpr int N = wv::N, NF = wv::NF, R = wv::R;
+  const int s = blockIdx.x;
+  if (a.status[s] != KLE_SAMPLE_ACTIVE) return;
+  extern __shared__ __align__(16) double sm[];
+  Cplx* tile = reinterpret_cast<Cplx*>(sm + WarpSmem::O_TILE);
+  double* cs = sm + WarpSmem::O_CS;
+  double* offs = sm + WarpSmem::O_OFS;
+  Cplx* tw = reinterpret_cast<Cplx*>(sm + WarpSmem::O_TW);
+  double* isc = sm + WarpSmem::O_ISC;
+  const int lane = threadIdx.x, k = lane & 7, slot = lane >> 3, nx = a.nx;
+  const size_t sb = (size_t)s * N * nx;
+  const double* dia = a.dia + (size_t)s * nx;
+  const double* off = a.off + (size_t)s * nx;
+
+  // ---- stage: factors, chunk products, start rows ---------------------------
+  LaneFactors<MR, P> fac;
+  fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
+  const double hg = a.dt * a.g0;
+  if (slot == 0) chunk_products<MR, P>(cs, fac, k, hg);
+  for (int e = lane; e < RB + 2; e += 32) {
+    const int row = e - 1;
+    offs[e] = (row >= 0 && row + 1 < nx) ? a.dT * off[row] : 0.0;
+  }
+  if (lane < N) {
+    double sn, c;
+    sincospi(-2.0 * (double)lane / (double)N, &sn, &c);
+    tw[lane] = {c, sn};
+    isc[lane] = a.inv_scaling[lane];
+  }
+  double x[R][MR];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int n = slot * R + r;
+    const double* src = (n == 0) ? a.u0 : a.U + sb + (size_t)(n - 1) * nx;
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      x[r][j] = row < nx ? __ldg(src + row) + hg : 0.0;
+    }
+  }
+  wv::syncw();
+  // ---- the J-step sweeps ------------------------------------------------------
+  be_steps_cs<MR, P, R>(x, fac, k, a.J, cs);
+  // ---- rhs_n = scaling_n ((I + dT A) F_n - prev_n) into the tile ---------------
+  {
+    double left[R], right[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int j = 0; j < MR; ++j) x[r][j] = (k * MR + j < nx) ? x[r][j] - hg : 0.0;
+      left[r] = __shfl_up_sync(KLE_FULL_MASK, x[r][MR - 1], 1, P);
+      right[r] = __shfl_down_sync(KLE_FULL_MASK, x[r][0], 1, P);
+      if (k == 0) left[r] = 0.0;
+      if (k == P - 1) right[r] = 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int n = slot * R + r;
+      const double sc = a.scaling[n];
+      const double pmul = (n == 0) ? a.alpha : 1.0;
+      const double* prev = a.U + sb + (size_t)(n == 0 ? N - 1 : n - 1) * nx;
+      double xl = left[r];
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = k * MR + j;
+        double rhs = 0.0;
+        const double xc = x[r][j];
+        if (row < nx) {
+          const double dj = __ldg(dia + row);
+          const double em = row > 0 ? __ldg(off + row - 1) : 0.0;
+          const double ep = row + 1 < nx ? __ldg(off + row) : 0.0;
+          const double xp = (j < MR - 1) ? x[r][j + 1] : right[r];
+          const double Ax = fma(em, xl, fma(dj, xc, ep * xp));
+          rhs = sc * (fma(a.dT, Ax, xc) - pmul * __ldg(prev + row));
+        }
+        xl = xc;
+        reinterpret_cast<double*>(&tile[tix(n, row & (HC - 1))])[row >> 6] = rhs;
+      }
+    }
+  }
+  wv::syncw();
+  wv::fft_warp<-1>(tile, tw, lane);
+  // ---- three rounds of 4 frequency groups -------------------------------------
+  const double hs = 0.5 / sqrt((double)N);
+  const int r0 = k * MR;
+#pragma unroll 1
+  for (int rho = 0; rho < 3; ++rho) {
+    const int fr = rho * 4 + slot;
+    const bool valid = fr < NF;
+    const int f = valid ? fr : NF - 1;
+    const int fm = (N - f) & (N - 1);
+    const Cplx* src = reinterpret_cast<const Cplx*>(a.sfac) + ((size_t)s * NF + f) * nx;
+    Cplx preg[MR + 1];  // pivots of rows r0 - 1 .. r0 + MR - 1
+#pragma unroll
+    for (int jj = 0; jj <= MR; ++jj) {
+      const int row = r0 + jj - 1;
+      preg[jj] = row < 0 ? Cplx{0.0, 0.0} : (row < nx ? src[row] : Cplx{1.0, 0.0});
+    }
+    Cplx y[MR];
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const int col = r0 + j;
+      const Cplx zf = tile[tix(f, col & (HC - 1))], zm = tile[tix(fm, col & (HC - 1))];
+      if (col < HC) y[j] = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};
+      else y[j] = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};
+    }
+    freq_solve(y, k, offs + r0, [&](int jj) -> Cplx { return preg[jj + 1]; });
+    wv::syncw();  // the groups have read their p_f, p_{N-f}
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      const Cplx qb = shfl_xor_c(y[j], CLN / 2);
+      if (valid && k < CLN / 2) {
+        const int col = r0 + j;
+        tile[tix(f, col)] = {y[j].re - qb.im, y[j].im + qb.re};
+        if (f > 0 && 2 * f < N) tile[tix(N - f, col)] = {y[j].re + qb.im, qb.re - y[j].im};
+      }
+    }
+    wv::syncw();
+  }
+  wv::fft_warp<+1>(tile, tw, lane);
+  // ---- update: packed columns lane and lane + 32 -------------------------------
+  const double rsN = 1.0 / sqrt((double)N);
+  double incmax = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    const int ra = c, rb = c + HC;
+#pragma unroll 4
+    for (int n = 0; n < N; ++n) {
+      const Cplx z = tile[tix(n, c)];
+      if (ra < nx) {
+        const double u = (z.re * rsN) * isc[n];
+        const double d = fabs(u - a.U[sb + (size_t)n * nx + ra]);
+        incmax = fmax(incmax, d);
+        bad |= (d != d);
+        a.U[sb + (size_t)n * nx + ra] = u;
+      }
+      if (rb < nx) {
+        const double u = (z.im * rsN) * isc[n];
+        const double d = fabs(u - a.U[sb + (size_t)n * nx + rb]);
+        incmax = fmax(incmax, d);
+        bad |= (d != d);
+        a.U[sb + (size_t)n * nx + rb] = u;
+      }
+    }
+  }
+  if (__any_sync(KLE_FULL_MASK, bad)) incmax = __longlong_as_double(0x7ff8000000000000LL);
+  incmax = warp_max(incmax);
+  if (lane == 0) {
+    const double inc = incmax;
+    if (a.inc_hist) a.inc_hist[(size_t)s * a.max_iters + (a.k - 1)] = inc;
+    int st = KLE_SAMPLE_ACTIVE;
+    if (inc <= a.tol) st = KLE_SAMPLE_CONVERGED;
+    else if (!isfinite(inc)) st = KLE_SAMPLE_NONFINITE;
+    else if (a.k >= a.max_iters) st = KLE_SAMPLE_MAXITERS;
+    if (st != KLE_SAMPLE_ACTIVE) {
+      a.status[s] = st;
+      if (a.iters) a.iters[s] = a.k;
+    } else if (a.active_count) {
+      atomicAdd(a.active_count, 1);
+    }
+  }
+}
+
+static int launch_warp(const IterSmallArgs& a, cudaStream_t st) {
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_iter_warp: cudaFuncSetAttribute", [&] {
+        const cudaError_t e = cudaFuncSetAttribute(iter_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)WarpSmem::BYTES);
+        return e != cudaSuccess ? e : cudaFuncSetAttribute(iter_warp_kernel,
+                                                           cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                           cudaSharedmemCarveoutMaxShared);
+      }))
+    return rc;
+  iter_warp_kernel<<<(unsigned)a.M, 32, WarpSmem::BYTES, st>>>(a);
+  return check_launch("iter_warp_kernel");
+}
+
 template <int LOGN, bool FUSE>
 static int launch(const IterSmallArgs& a, cudaStream_t st) {
   using K = Shape<LOGN, FUSE>;
@@ -476,11 +733,13 @@ static bool small_shape(int N, int nx) {
 }
 
 bool iter_small_supported(int N, int nx) {
-  // opt-in: KLE_FUSED=1 (read per call). Measured at c4 (131k samples): fused 104 ms per solve
-  // against 98 ms for fgr_kernel (one-warp R = 4 sweeps) + the CGC-only kernel below; the
-  // fused kernel's sweeps run R = 1 per 8-lane group
-  const char* env = getenv("KLE_FUSED");
-  return env && env[0] == '1' && small_shape(N, nx);
+  // opt-in: KLE_FUSED=1 / 2 (read per call). Measured at c4 (131k samples, one full solve):
+  // one CTA per sample 104 ms, one warp per sample 160 ms, against 96 ms for fgr_kernel
+  // (one-warp R = 4 sweeps) + the 2-CTA cluster CGC. The CTA variant sweeps with R = 1 per
+  // 8-lane group; the warp variant keeps the sweep's 255 registers allocated through its
+  // long, latency-bound single-warp CGC phase, which the other warps do not fill
+  const char* env = getenv("KLE_FUSED");  // 1: one CTA per sample; 2: one warp per sample (N = 16)
+  return env && (env[0] == '1' || env[0] == '2') && small_shape(N, nx);
 }
 
 bool cgc_small_supported(int N, int nx) {
@@ -491,7 +750,11 @@ bool cgc_small_supported(int N, int nx) {
   return env && env[0] == '1' && small_shape(N, nx);
 }
 
-int iter_small_run(const IterSmallArgs& a, cudaStream_t st) { return itsmall::dispatch<true>(a, st); }
+int iter_small_run(const IterSmallArgs& a, cudaStream_t st) {
+  const char* env = getenv("KLE_FUSED");
+  if (env && env[0] == '2' && a.N == 16) return a.M > 0 ? itsmall::launch_warp(a, st) : KLE_OK;
+  return itsmall::dispatch<true>(a, st);
+}
 int cgc_small_run(const IterSmallArgs& a, cudaStream_t st) { return itsmall::dispatch<false>(a, st); }
 
 }  // namespace kle

@@ -205,11 +205,12 @@ def test_sample_pipelines_do_not_change_results(cuda, pipes, monkeypatch):
     assert torch.equal(torch.nan_to_num(one.increments, nan=-1.0), torch.nan_to_num(many.increments, nan=-1.0))
 
 
-@pytest.mark.parametrize("env", ["KLE_FUSED", "KLE_CGC_SMALL"])
-def test_small_block_kernels_match_default_path(cuda, golden, env, monkeypatch):
-    """The one-CTA-per-sample small-block kernels (kle_iter_small.cu: the fused
-    whole-iteration kernel and its CGC-only variant, opt-in A/B paths for
-    nx <= 128, N <= 16) against the default fgr + cluster-CGC path on the
+@pytest.mark.parametrize("env,val", [("KLE_FUSED", "1"), ("KLE_FUSED", "2"), ("KLE_CGC_SMALL", "1")])
+def test_small_block_kernels_match_default_path(cuda, golden, env, val, monkeypatch):
+    """The small-block kernels (kle_iter_small.cu: the fused whole-iteration
+    kernel with one CTA or one warp per sample, and the CGC-only variant;
+    opt-in A/B paths for nx <= 128, N <= 16) against the default fgr +
+    cluster-CGC path on the
     config-1 goldens: iteration counts exact, fields within 1e-12."""
     import torch
 
@@ -221,7 +222,7 @@ def test_small_block_kernels_match_default_path(cuda, golden, env, monkeypatch):
     grid = make_time_grid(1.0, 16, 32)
     cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60)
     base = pcgc_solve_batched(model, g["xi_all"][:16], grid, cfg, g["U0"][:16])
-    monkeypatch.setenv(env, "1")
+    monkeypatch.setenv(env, val)
     alt = pcgc_solve_batched(model, g["xi_all"][:16], grid, cfg, g["U0"][:16])
     assert torch.equal(base.iters, alt.iters)
     np.testing.assert_array_equal(alt.iters.cpu().numpy(), g["iters"])

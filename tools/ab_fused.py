@@ -2,7 +2,7 @@
 separate fgr + cluster-CGC kernels (KLE_FUSED=0) on config-4 shapes: the
 batched PCGC from the config's surrogate, iteration counts, max field
 difference, and the time of one full solve per path.
-usage: python tools/ab_fused.py [M]"""
+usage: python tools/ab_fused.py [M] [modes, default 0,1]"""
 import os
 import sys
 sys.path.insert(0, ".")
@@ -23,7 +23,8 @@ sur = KLGpcSurrogate(g["mean_field"], g["eigenvalues"], g["modes"], g["coeffs"],
 xi = torch.as_tensor(RngStream(2718).split(3)[1].normal(0.0, 1.0, size=(M, 4)), device="cuda")
 solver = KleCgcSolver(model, grid, cfg, sur)
 out = {}
-for fused in ("0", "1"):
+modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1"]
+for fused in modes:
     os.environ["KLE_FUSED"] = fused
     solver.solve(xi)
     torch.cuda.synchronize()
@@ -35,8 +36,8 @@ for fused in ("0", "1"):
     out[fused] = (res.batch.states.clone(), res.batch.iters.clone(), res.batch.status.clone(), a.elapsed_time(b))
     print(f"KLE_FUSED={fused}: {out[fused][3]:.2f} ms per solve ({M / out[fused][3] * 1e3:.0f} solves/s), "
           f"mean iters {out[fused][1].double().mean().item():.4f}", flush=True)
-s0, i0, st0, _ = out["0"]
-s1, i1, st1, _ = out["1"]
+s0, i0, st0, _ = out[modes[0]]
+s1, i1, st1, _ = out[modes[-1]]
 print("iters equal:", bool(torch.equal(i0, i1)), "status equal:", bool(torch.equal(st0, st1)),
       "all converged:", bool((st1 == 1).all()))
 print("max rel field diff:", float((s0 - s1).abs().max() / s0.abs().max()))
