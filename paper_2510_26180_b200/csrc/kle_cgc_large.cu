@@ -366,6 +366,282 @@ __global__ void cgcl_status_kernel(CgcArgs a, unsigned long long* __restrict__ i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Streaming variant (N >= 256): one CTA per sample walks the rows in blocks of
+// RB = 16 (8 packed complex columns). Forward kernel: per block, the R rows are
+// loaded, the four-step FFT runs over the block's columns, and thread f (one
+// per frequency f <= N/2) unpacks p_f of the block's rows and advances the
+// forward LDL^T recurrence (pivots on the fly), writing y and 1/beta. Backward
+// kernel: blocks in reverse, thread f runs the back substitution over the
+// block's rows, the packed Hermitian spectra go into the tile, the inverse FFT
+// runs, and the block's U rows are updated. The spectrum never round-trips
+// through HBM between the FFTs and the solves: per (n, i) and iteration
+// R 8 + U 8 read, U 8 written, y and 1/beta written and read once (32 B):
+// 56 B against 88 B for the three-kernel path above. Same operations in the
+// same order per element as the three-kernel path (bitwise equal results).
+// Opt-in (KLE_CGCL_STREAM=1): measured 33.8 ms per 256-sample c5 launch against
+// 31.6 ms for the three kernels — one 135 KB-tile CTA per SM walks 256 row
+// blocks with load, FFT and recurrence phases serialised, so it is latency-
+// bound at 1.8 TB/s of (smaller) traffic where the three kernels reach 2.8.
+namespace {
+template <int LOGN>
+struct SShape {
+  static constexpr int N = 1 << LOGN, NF = N / 2 + 1;
+  static constexpr int LOG_N1 = (LOGN + 1) / 2;
+  static constexpr int N1 = 1 << LOG_N1, N2 = N / N1;
+#ifndef KLE_CGCS_CP
+#define KLE_CGCS_CP 8  // 4: 68 KB tiles, 3 CTAs/SM, measured slower (36.3 vs 33.8 ms per 256-sample launch)
+#endif
+  static constexpr int CP = KLE_CGCS_CP, RB = 2 * CP;  // complex columns / real rows per block
+  static constexpr int FT = (N1 > N2 ? N1 : N2) * CP;
+  static constexpr int FPT = 2;                      // frequencies per thread (two independent recurrences)
+  static constexpr int NS = ((NF + FPT - 1) / FPT + 31) / 32 * 32;
+  static constexpr int NT = NS > FT ? NS : FT;
+  // tile [CP][N] complex, n fastest, padded one slot per 32 (pass-2 strides) and
+  // one extra slot per column (column starts fall on distinct banks)
+  static constexpr int LD = N + N / 32 + 1;
+  static constexpr int TILE = CP * LD;
+  __device__ __forceinline__ static int idx(int n, int j) { return j * LD + n + (n >> 5); }
+};
+
+template <int LOGN, int S>
+__device__ __forceinline__ void stile_fft(Cplx* t, const Cplx* __restrict__ tw) {
+  using K = SShape<LOGN>;
+  constexpr int N = K::N, N1 = K::N1, N2 = K::N2, CP = K::CP;
+  const int tid = threadIdx.x;
+  if (tid < N1 * CP) {  // pass 1: task (n1, j), n1 fastest
+    const int n1 = tid % N1, j = tid / N1;
+    Cplx v[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) v[n2] = t[K::idx(n1 + N1 * n2, j)];
+    reg_dft<N2, S, N>(v, tw);
+#pragma unroll
+    for (int q = 0; q < N2; ++q) {
+      const int k2 = rbits<N2>(q);
+      if (k2 != 0) {
+        Cplx w = {__ldg(&tw[n1 * k2].re), __ldg(&tw[n1 * k2].im)};
+        if (S > 0) w.im = -w.im;
+        v[q] = cmul(v[q], w);
+      }
+      t[K::idx(n1 + N1 * k2, j)] = v[q];
+    }
+  }
+  __syncthreads();
+  Cplx w[N1];
+  const bool act = tid < N2 * CP;
+  const int k2 = tid % N2, j = tid / N2;  // pass 2: task (k2, j), k2 fastest
+  if (act) {
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) w[n1] = t[K::idx(n1 + N1 * k2, j)];
+    reg_dft<N1, S, N>(w, tw);
+  }
+  __syncthreads();
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < N1; ++q) t[K::idx(k2 + N2 * rbits<N1>(q), j)] = w[q];
+  }
+  __syncthreads();
+}
+}  // namespace
+
+template <int LOGN>
+__global__ void __launch_bounds__(SShape<LOGN>::NT) cgcs_fwd_kernel(CgcArgs a, int m0, const Cplx* __restrict__ tw,
+                                                                      Cplx* __restrict__ Y, Cplx* __restrict__ IB) {
+  using K = SShape<LOGN>;
+  constexpr int N = K::N, NF = K::NF, NT = K::NT, CP = K::CP, RB = K::RB;
+  const int s = m0 + blockIdx.x, sl = blockIdx.x;
+  if (a.status && a.status[s] != KLE_SAMPLE_ACTIVE) return;
+  extern __shared__ __align__(16) Cplx t[];
+  const int nx = a.nx, tid = threadIdx.x;
+  const size_t sb = (size_t)s * N * nx;
+  constexpr int FPT = K::FPT;
+  int fr[FPT];
+  bool ok[FPT];
+  Cplx lam[FPT], y[FPT], ibp[FPT];
+  Cplx* yo[FPT];
+  Cplx* ibo[FPT];
+#pragma unroll
+  for (int q = 0; q < FPT; ++q) {
+    fr[q] = tid + q * NT;
+    ok[q] = fr[q] < NF;
+    const int fq = ok[q] ? fr[q] : 0;
+    lam[q] = {a.lam[2 * fq], a.lam[2 * fq + 1]};
+    y[q] = {0.0, 0.0};
+    ibp[q] = {0.0, 0.0};
+    yo[q] = Y + (size_t)sl * nx * NF + fq;
+    ibo[q] = IB + (size_t)sl * nx * NF + fq;
+  }
+  const double dT = a.dT;
+  const double* __restrict__ dd = a.dia + (size_t)s * nx;
+  const double* __restrict__ ee = a.off + (size_t)s * nx;
+  const double hs = 0.5 / sqrt((double)N);
+  for (int c0 = 0; c0 < nx; c0 += RB) {
+    __syncthreads();  // the previous block's unpack has read the tile
+    for (int e = tid; e < N * RB; e += NT) {  // rows fastest: coalesced 128-byte row segments, all in flight
+      const int n = e / RB, col = e % RB;
+      double* dst = reinterpret_cast<double*>(&t[K::idx(n, col >> 1)]) + (col & 1);
+      if (c0 + col < nx) cp_async8(dst, a.R + sb + (size_t)n * nx + c0 + col);
+      else *dst = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    if (a.load_scale) {  // stand-alone three-step: r is not alpha-scaled yet
+      for (int e = tid; e < N * RB; e += NT) {
+        const int n = e / RB, col = e % RB;
+        reinterpret_cast<double*>(&t[K::idx(n, col >> 1)])[col & 1] *= a.load_scale[n];
+      }
+      __syncthreads();
+    }
+    stile_fft<LOGN, -1>(t, tw);
+#pragma unroll 2
+    for (int col = 0; col < RB; ++col) {
+      const int i = c0 + col;
+      if (i >= nx) break;
+      const int j = col >> 1;
+      const double Di = fma(dT, __ldg(dd + i), 0.0);
+      const double E = i > 0 ? dT * __ldg(ee + i - 1) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FPT; ++q) {
+        if (!ok[q]) continue;
+        const int f = fr[q], fm = (N - f) & (N - 1);
+        const Cplx zf = t[K::idx(f, j)], zm = t[K::idx(fm, j)];
+        Cplx pi;
+        if ((col & 1) == 0) pi = {(zf.re + zm.re) * hs, (zf.im - zm.im) * hs};
+        else pi = {(zf.im + zm.im) * hs, (zm.re - zf.re) * hs};
+        const Cplx D = {fma(dT, __ldg(dd + i), lam[q].re), lam[q].im};
+        Cplx beta = D;
+        if (i > 0) {
+          const Cplx l = {E * ibp[q].re, E * ibp[q].im};
+          beta = {fma(-l.re, E, D.re), fma(-l.im, E, D.im)};
+          y[q] = cs(pi, cmul(l, y[q]));
+        } else {
+          y[q] = pi;
+        }
+        ibp[q] = crcp(beta);
+        yo[q][(size_t)i * NF] = y[q];
+        ibo[q][(size_t)i * NF] = ibp[q];
+      }
+      (void)Di;
+    }
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(SShape<LOGN>::NT) cgcs_bwd_kernel(CgcArgs a, int m0, const Cplx* __restrict__ tw,
+                                                                      const Cplx* __restrict__ Y,
+                                                                      const Cplx* __restrict__ IB,
+                                                                      unsigned long long* __restrict__ inc_bits) {
+  using K = SShape<LOGN>;
+  constexpr int N = K::N, NF = K::NF, NT = K::NT, CP = K::CP, RB = K::RB;
+  const int s = m0 + blockIdx.x, sl = blockIdx.x;
+  if (a.status && a.status[s] != KLE_SAMPLE_ACTIVE) return;
+  extern __shared__ __align__(16) Cplx t[];
+  const int nx = a.nx, tid = threadIdx.x;
+  const size_t sb = (size_t)s * N * nx;
+  constexpr int FPT = K::FPT;
+  int fr[FPT];
+  bool ok[FPT];
+  const Cplx* yi[FPT];
+  const Cplx* ibi[FPT];
+#pragma unroll
+  for (int q = 0; q < FPT; ++q) {
+    fr[q] = tid + q * NT;
+    ok[q] = fr[q] < NF;
+    const int fq = ok[q] ? fr[q] : 0;
+    yi[q] = Y + (size_t)sl * nx * NF + fq;
+    ibi[q] = IB + (size_t)sl * nx * NF + fq;
+  }
+  const double dT = a.dT;
+  const double* __restrict__ ee = a.off + (size_t)s * nx;
+  const double rsN = 1.0 / sqrt((double)N);
+  double* __restrict__ out = a.Uout ? a.Uout : a.U;
+  const bool track = a.U != nullptr && inc_bits != nullptr;
+  double incmax = 0.0;
+  bool bad = false;
+  Cplx x[FPT];
+#pragma unroll
+  for (int q = 0; q < FPT; ++q) x[q] = {0.0, 0.0};
+  const int nb = (nx + RB - 1) / RB;
+  for (int b = nb - 1; b >= 0; --b) {
+    const int c0 = b * RB;
+    __syncthreads();  // the previous block's update has read the tile
+    // back substitution q_i = y_i / beta_i - l_{i+1} q_{i+1} over the block's rows, descending, the
+    // loads of a half-block issued together; each finished row pair (2j, 2j+1) is packed into the
+    // tile as W_f = q_2j + i q_2j+1 (and the mirror W_{N-f})
+#pragma unroll
+    for (int h = 1; h >= 0; --h) {
+      Cplx yy[FPT][CP], bb[FPT][CP];
+#pragma unroll
+      for (int q = 0; q < FPT; ++q)
+#pragma unroll
+        for (int u = 0; u < CP; ++u) {
+          const int i = c0 + h * CP + u;
+          const bool in = ok[q] && i < nx;
+          yy[q][u] = in ? yi[q][(size_t)i * NF] : Cplx{0.0, 0.0};
+          bb[q][u] = in ? ibi[q][(size_t)i * NF] : Cplx{0.0, 0.0};
+        }
+      Cplx hi[FPT];
+#pragma unroll
+      for (int u = CP - 1; u >= 0; --u) {
+        const int i = c0 + h * CP + u;
+        const double E = (i < nx - 1) ? dT * __ldg(ee + i) : 0.0;
+#pragma unroll
+        for (int q = 0; q < FPT; ++q) {
+          Cplx qi = {0.0, 0.0};
+          if (i < nx) {
+            const Cplx z = cmul(yy[q][u], bb[q][u]);
+            if (i < nx - 1) {
+              const Cplx ln = {E * bb[q][u].re, E * bb[q][u].im};
+              x[q] = cs(z, cmul(ln, x[q]));
+            } else {
+              x[q] = z;
+            }
+            qi = x[q];
+          }
+          if (u & 1) {
+            hi[q] = qi;  // row 2j+1 of the pair
+          } else if (ok[q]) {
+            const int f = fr[q], j = (h * CP + u) >> 1;
+            const Cplx qa = qi, qb = hi[q];
+            t[K::idx(f, j)] = {qa.re - qb.im, qa.im + qb.re};
+            if (f > 0 && 2 * f < N) t[K::idx(N - f, j)] = {qa.re + qb.im, qb.re - qa.im};
+          }
+        }
+      }
+    }
+    __syncthreads();
+    stile_fft<LOGN, +1>(t, tw);
+    // the old values staged in batches of UB registers: a batch's loads are in flight together and
+    // precede its stores (out may alias U)
+    constexpr int UB = 16;
+    for (int e0 = tid; e0 < N * RB; e0 += UB * NT) {
+      double old[UB];
+#pragma unroll
+      for (int r = 0; r < UB; ++r) {
+        const int e = e0 + r * NT, n = e / RB, col = e % RB;
+        old[r] = (track && e < N * RB && c0 + col < nx) ? a.U[sb + (size_t)n * nx + c0 + col] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < UB; ++r) {
+        const int e = e0 + r * NT, n = e / RB, col = e % RB;
+        if (e >= N * RB || c0 + col >= nx) continue;
+        const Cplx z = t[K::idx(n, col >> 1)];
+        const double u = (((col & 1) ? z.im : z.re) * rsN) * __ldg(a.inv_scaling + n);
+        if (track) {
+          const double d = fabs(u - old[r]);
+          incmax = fmax(incmax, d);
+          bad |= (d != d);
+        }
+        out[sb + (size_t)n * nx + c0 + col] = u;
+      }
+    }
+  }
+  if (!track) return;
+  if (__syncthreads_or(bad)) incmax = __longlong_as_double(0x7ff8000000000000LL);
+  incmax = warp_max(incmax);
+  if ((threadIdx.x & 31) == 0) atomicMax(inc_bits + s, (unsigned long long)__double_as_longlong(incmax));
+}
+
 __global__ void cgcl_twiddle_kernel(Cplx* tw, int N) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
@@ -427,6 +703,28 @@ static int run_large(const CgcArgs& a, cudaStream_t st) {
   if (two) {
     cudaEventRecord(ev[2], st);
     for (int q = 0; q < 2; ++q) cudaStreamWaitEvent(ss[q], ev[2], 0);
+  }
+  static const char* senv = getenv("KLE_CGCL_STREAM");  // 1: the streaming kernels (A/B)
+  if constexpr (LOGN >= 8) {
+    if (senv && senv[0] == '1') {
+      using S = SShape<LOGN>;
+      constexpr size_t ssm = sizeof(Cplx) * S::TILE;
+      static PerDeviceOnce sattr;
+      if (int rc = once_per_device(sattr, "kle_cgc_stream: cudaFuncSetAttribute", [&] {
+            const cudaError_t e = cudaFuncSetAttribute(cgcs_fwd_kernel<LOGN>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+            return e != cudaSuccess ? e : cudaFuncSetAttribute(cgcs_bwd_kernel<LOGN>,
+                                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+          }))
+        return rc;
+      for (int m0 = 0; m0 < a.M; m0 += MB) {
+        const int mb = a.M - m0 < MB ? a.M - m0 : MB;
+        cgcs_fwd_kernel<LOGN><<<(unsigned)mb, S::NT, ssm, st>>>(a, m0, tw, P, IB);
+        cgcs_bwd_kernel<LOGN><<<(unsigned)mb, S::NT, ssm, st>>>(a, m0, tw, P, IB, a.U ? bits : nullptr);
+      }
+      if (a.U) cgcl_status_kernel<<<(a.M + 127) / 128, 128, 0, st>>>(a, bits);
+      return check_launch("cgc_stream");
+    }
   }
   int j = 0;
   for (int m0 = 0; m0 < a.M; m0 += HB, ++j) {

@@ -228,3 +228,23 @@ def test_small_block_kernels_match_default_path(cuda, golden, env, val, monkeypa
     np.testing.assert_array_equal(alt.iters.cpu().numpy(), g["iters"])
     d = float((base.states - alt.states).abs().max() / base.states.abs().max())
     assert d <= 1e-12, d
+
+
+def test_streaming_large_cgc_is_bitwise_the_three_kernel_path(cuda, monkeypatch):
+    """The opt-in streaming large-block CGC (KLE_CGCL_STREAM=1: per-sample CTAs
+    walking row blocks, FFT + forward recurrence fused, back substitution +
+    inverse FFT + update fused) performs the same operations per element as
+    the three-kernel path: the updated U and increments are bitwise equal.
+    Run in a subprocess per setting (the switch is read once per process)."""
+    import subprocess
+    import sys
+
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    outs = []
+    for v in ("0", "1"):
+        env = dict(__import__("os").environ, KLE_CGCL_STREAM=v)
+        r = subprocess.run([sys.executable, "tools/ab_cgcl.py", "8"], capture_output=True, text=True, cwd=root,
+                           env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split("checksum")[1].strip())
+    assert outs[0] == outs[1], outs
