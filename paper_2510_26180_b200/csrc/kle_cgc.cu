@@ -51,6 +51,39 @@ __device__ void fft_tile(Cplx* t, const Cplx* tw, int N, int TC, bool inverse) {
   }
 }
 
+// Bluestein's chirp-z transform for N that is not a power of two (the
+// reference's np.fft handles every N, pintuq/pcgc.py:79-87): with the chirp
+// c_n = exp(-i pi n^2 / N),
+//   sum_n x_n exp(-2 pi i n k / N) = c_k (a * b)_k,   a_n = x_n c_n,  b_m = conj(c_m),
+// a circular convolution of length Mb = 2^ceil(log2(2N - 1)) done with radix-2
+// FFTs of size Mb (B^ = FFT(b) precomputed per CTA); the inverse sign uses the
+// conjugate chirps, whose kernel transform is conj(B^[-k]). On entry the tile
+// ([Mb][TC]) holds a in bit-reversed row order, zero padded; on exit it holds
+// Mb (a * b) in natural order. O(N log N) per column instead of the O(N^2)
+// direct sum.
+__device__ void bluestein_conv(Cplx* t, const Cplx* twM, const Cplx* Bhat, int Mb, int log2Mb, int TC,
+                               bool inverse) {
+  fft_tile(t, twM, Mb, TC, false);
+  for (int e = threadIdx.x; e < Mb * TC; e += CGC_NT) {  // pointwise product with the kernel transform
+    const int k = e / TC;
+    Cplx b = Bhat[inverse ? ((Mb - k) & (Mb - 1)) : k];
+    if (inverse) b.im = -b.im;
+    t[e] = cmul(t[e], b);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < Mb * TC; e += CGC_NT) {  // in-place bit reversal of the rows
+    const int k = e / TC, c = e - k * TC;
+    const int r = (int)(__brev((unsigned)k) >> (32 - log2Mb));
+    if (k < r) {
+      const Cplx u = t[k * TC + c];
+      t[k * TC + c] = t[r * TC + c];
+      t[r * TC + c] = u;
+    }
+  }
+  __syncthreads();
+  fft_tile(t, twM, Mb, TC, true);
+}
+
 __device__ __forceinline__ double block_max(double v, double* red) {
   v = warp_max(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -72,15 +105,49 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
   extern __shared__ double sm[];
   const int N = a.N, nx = a.nx, NF = a.full ? N : N / 2 + 1;
   const bool pow2 = log2N >= 0;
+  const bool direct = log2N == -2;  // other N whose Bluestein tables do not fit: O(N^2) direct DFT
+  const bool blue = !pow2 && !direct;
+  // non-power-of-two N: Bluestein with transforms of size Mb (tile rows)
+  int log2Mb = 0;
+  while ((1 << log2Mb) < 2 * N - 1) ++log2Mb;
+  const int Mb = blue ? (1 << log2Mb) : N, TR = Mb;
   Cplx* tw = reinterpret_cast<Cplx*>(sm);
   Cplx* tile = tw + N;
-  double* red = reinterpret_cast<double*>(tile + (size_t)N * TC);
+  Cplx* twM = tile + (size_t)TR * TC;        // [Mb] (Bluestein)
+  Cplx* chirp = twM + (blue ? Mb : 0);       // [N]
+  Cplx* Bhat = chirp + (blue ? N : 0);       // [Mb]
+  double* red = reinterpret_cast<double*>(Bhat + (blue ? Mb : 0));
   for (int j = threadIdx.x; j < N; j += CGC_NT) {
     double sn, cs;
     sincospi(-2.0 * (double)j / (double)N, &sn, &cs);
     tw[j] = {cs, sn};
   }
+  if (blue) {
+    for (int j = threadIdx.x; j < Mb; j += CGC_NT) {
+      double sn, cs;
+      sincospi(-2.0 * (double)j / (double)Mb, &sn, &cs);
+      twM[j] = {cs, sn};
+    }
+    for (int n = threadIdx.x; n < N; n += CGC_NT) {  // c_n = exp(-i pi n^2 / N), n^2 reduced mod 2N
+      double sn, cs;
+      sincospi(-(double)(((long long)n * n) % (2LL * N)) / (double)N, &sn, &cs);
+      chirp[n] = {cs, sn};
+    }
+    __syncthreads();
+    // B^ = FFT_Mb(b), b_m = conj(c_|m|) for |m| < N (circular), computed once in column 0 of the tile
+    for (int e = threadIdx.x; e < Mb * TC; e += CGC_NT) tile[e] = {0.0, 0.0};
+    __syncthreads();
+    for (int m = threadIdx.x; m < Mb; m += CGC_NT) {
+      const int d = m < N ? m : (Mb - m < N ? Mb - m : -1);
+      const Cplx v = d >= 0 ? Cplx{chirp[d].re, -chirp[d].im} : Cplx{0.0, 0.0};
+      tile[(int)(__brev((unsigned)m) >> (32 - log2Mb)) * TC] = v;
+    }
+    __syncthreads();
+    fft_tile(tile, twM, Mb, TC, false);
+    for (int k = threadIdx.x; k < Mb; k += CGC_NT) Bhat[k] = tile[k * TC];
+  }
   __syncthreads();
+  const double rMb = 1.0 / (double)Mb;
   const double rsN = 1.0 / sqrt((double)N);
   Cplx* pbuf = reinterpret_cast<Cplx*>(a.scratch + (size_t)blockIdx.x * a.scratch_doubles_per_cta);
   Cplx* ibuf = pbuf + (size_t)nx * NF;
@@ -91,6 +158,9 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
     // ---------------- phase 1: forward transform --------------------------
     for (int c0 = 0; c0 < nx; c0 += TC) {
       const int tc = min(TC, nx - c0);
+      if (blue)
+        for (int e = threadIdx.x; e < TR * TC; e += CGC_NT) tile[e] = {0.0, 0.0};
+      __syncthreads();
       for (int idx = threadIdx.x; idx < N * TC; idx += CGC_NT) {
         const int n = idx / TC, c = idx - n * TC;
         double v = 0.0;
@@ -98,17 +168,23 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
           v = a.R[sb + (size_t)n * nx + c0 + c];
           if (a.load_scale) v *= a.load_scale[n];
         }
-        const int pos = (pow2 && log2N > 0) ? (int)(__brev((unsigned)n) >> (32 - log2N)) : n;
-        tile[pos * TC + c] = {v, 0.0};
+        if (!blue) {
+          const int pos = log2N > 0 ? (int)(__brev((unsigned)n) >> (32 - log2N)) : n;
+          tile[pos * TC + c] = {v, 0.0};
+        } else {  // a_n = x_n c_n, bit-reversed over Mb rows
+          tile[(int)(__brev((unsigned)n) >> (32 - log2Mb)) * TC + c] = {v * chirp[n].re, v * chirp[n].im};
+        }
       }
       __syncthreads();
       if (pow2 && N > 1) fft_tile(tile, tw, N, TC, false);
+      if (blue) bluestein_conv(tile, twM, Bhat, Mb, log2Mb, TC, false);
       for (int idx = threadIdx.x; idx < tc * NF; idx += CGC_NT) {
         const int c = idx / NF, f = idx - c * NF;
-        Cplx v;
-        if (pow2) {
-          v = tile[f * TC + c];
-        } else {
+        Cplx v = tile[f * TC + c];
+        if (blue) {  // X_f = c_f (a * b)_f
+          v = cmul(chirp[f], v);
+          v = {v.re * rMb, v.im * rMb};
+        } else if (direct) {
           v = {0.0, 0.0};
           for (int n = 0; n < N; ++n) v = cadd(v, cmul(tile[n * TC + c], tw[(int)(((long long)n * f) % N)]));
         }
@@ -158,6 +234,9 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
     double incmax = 0.0, immax = 0.0;
     for (int c0 = 0; c0 < nx; c0 += TC) {
       const int tc = min(TC, nx - c0);
+      if (blue)
+        for (int e = threadIdx.x; e < TR * TC; e += CGC_NT) tile[e] = {0.0, 0.0};
+      __syncthreads();
       for (int idx = threadIdx.x; idx < N * TC; idx += CGC_NT) {
         const int c = idx / N, n = idx - c * N;
         Cplx v = {0.0, 0.0};
@@ -169,18 +248,24 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
             v = {w.re, -w.im};
           }
         }
-        const int pos = (pow2 && log2N > 0) ? (int)(__brev((unsigned)n) >> (32 - log2N)) : n;
-        tile[pos * TC + c] = v;
+        if (!blue) {
+          const int pos = log2N > 0 ? (int)(__brev((unsigned)n) >> (32 - log2N)) : n;
+          tile[pos * TC + c] = v;
+        } else {  // inverse sign: a_f = V_f conj(c_f)
+          tile[(int)(__brev((unsigned)n) >> (32 - log2Mb)) * TC + c] = cmul(v, Cplx{chirp[n].re, -chirp[n].im});
+        }
       }
       __syncthreads();
       if (pow2 && N > 1) fft_tile(tile, tw, N, TC, true);
+      if (blue) bluestein_conv(tile, twM, Bhat, Mb, log2Mb, TC, true);
       for (int idx = threadIdx.x; idx < N * TC; idx += CGC_NT) {
         const int n = idx / TC, c = idx - n * TC;
         if (c >= tc) continue;
-        Cplx v;
-        if (pow2) {
-          v = tile[n * TC + c];
-        } else {
+        Cplx v = tile[n * TC + c];
+        if (blue) {  // X_n = conj(c_n) (a * conj b)_n
+          v = cmul(Cplx{chirp[n].re, -chirp[n].im}, v);
+          v = {v.re * rMb, v.im * rMb};
+        } else if (direct) {
           v = {0.0, 0.0};
           for (int f = 0; f < N; ++f) {
             Cplx w = tw[(int)(((long long)n * f) % N)];
@@ -233,15 +318,46 @@ __global__ void __launch_bounds__(CGC_NT) cgc_kernel(CgcArgs a, int TC, int log2
   }
 }
 
+static bool is_pow2(int N) { return N > 0 && (N & (N - 1)) == 0; }
+
+static int bluestein_len(int N) {
+  int m = 1;
+  while (m < 2 * N - 1) m <<= 1;
+  return m;
+}
+
+// Bluestein for N that is not a power of two, unless its tables (size-Mb
+// twiddles and kernel transform, the chirp) and a one-column tile exceed the
+// shared-memory budget (N > 1024): then the direct O(N^2) DFT
+static bool use_bluestein(int N) {
+  if (is_pow2(N)) return false;
+  const size_t Mb = bluestein_len(N);
+  return (size_t)N * sizeof(Cplx) + (3 * Mb + N) * sizeof(Cplx) + 32 * sizeof(double) <= 200 * 1024;
+}
+
+static int tile_rows(int N) { return use_bluestein(N) ? bluestein_len(N) : N; }
+
 static int tile_cols(int N) {
-  int tc = 2048 / (N > 0 ? N : 1);
+  int tc = (use_bluestein(N) ? 4096 : 2048) / tile_rows(N);
   if (tc > 64) tc = 64;
   if (tc < 1) tc = 1;
   return tc;
 }
 
 static size_t cgc_smem_bytes(int N) {
-  return (size_t)N * sizeof(Cplx) + (size_t)N * tile_cols(N) * sizeof(Cplx) + 32 * sizeof(double);
+  const size_t extra = use_bluestein(N) ? (size_t)(2 * tile_rows(N) + N) * sizeof(Cplx) : 0;  // twM, chirp, B^
+  return (size_t)N * sizeof(Cplx) + (size_t)tile_rows(N) * tile_cols(N) * sizeof(Cplx) + extra +
+         32 * sizeof(double);
+}
+
+// kernel transform mode: log2 N (power of two), -1 Bluestein, -2 direct DFT
+static int transform_mode(int N) {
+  if (is_pow2(N)) {
+    int l = 0;
+    while ((1 << l) < N) ++l;
+    return l;
+  }
+  return use_bluestein(N) ? -1 : -2;
 }
 
 int cgc_grid(int M, int N, int nx) {
@@ -280,11 +396,7 @@ size_t imag_residue_scratch_bytes(int M, int N, int nx) {
 int cgc_run(const CgcArgs& a, cudaStream_t st) {
   if (a.N < 1 || a.nx < 1) return set_error(KLE_ERR_INVALID, "cgc: bad dims");
   if (use_large(a.N, a.nx)) return cgc_large_run(a, st);
-  int log2N = -1;
-  if ((a.N & (a.N - 1)) == 0) {
-    log2N = 0;
-    while ((1 << log2N) < a.N) ++log2N;
-  }
+  const int log2N = transform_mode(a.N);
   const int TC = tile_cols(a.N);
   const size_t smem = cgc_smem_bytes(a.N);
   static PerDeviceOnce attr_once;
@@ -305,11 +417,7 @@ int imag_residue_run(const CgcArgs& a0, cudaStream_t st) {
   a.U = nullptr;
   a.Uout = nullptr;
   // a.status, if given, only selects the active samples (full mode never writes it)
-  int log2N = -1;
-  if ((a.N & (a.N - 1)) == 0) {
-    log2N = 0;
-    while ((1 << log2N) < a.N) ++log2N;
-  }
+  const int log2N = transform_mode(a.N);
   a.scratch_doubles_per_cta = 4 * (size_t)a.nx * a.N;
   static PerDeviceOnce attr_once;
   if (int rc = once_per_device(attr_once, "kle_cgc(imag): cudaFuncSetAttribute", [&] {

@@ -542,3 +542,40 @@ def test_device_kl_build_matches_host(cuda, golden):
         # the least-squares fit; measured 2.2e-11 — an initial-guess difference the PCGC contracts away
         assert rel(b, a) <= 1e-10
         assert rel(b, g["U0"][i]) <= 1e-10
+
+
+@pytest.mark.parametrize("N", [24, 100, 1000, 1500])
+def test_non_power_of_two_time_fft(cuda, N):
+    """Block DFTs for any N (pintuq/pcgc.py:79-87 uses np.fft for every N): the
+    on-the-fly CGC kernel runs Bluestein's chirp-z transform through radix-2
+    FFTs of length 2^ceil(log2(2N-1)) (N <= 1024) or, beyond its table budget,
+    the direct DFT (N = 1500). three_step_solve against the oracle's np.fft +
+    banded solves, and one PCGC solve with exact iteration counts (N = 24, 100)."""
+    from paper_2510_26180_b200 import LogNormalKL1D, SolverConfig, make_time_grid
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, pcgc_solve_batched, three_step_solve
+
+    rng = np.random.default_rng(N)
+    nx, alpha = 31, 1e-2
+    dT = 1.0 / N
+    off = -rng.uniform(0.5, 1.5, nx - 1) * 4.0
+    dia = 2.0 * 4.0 + rng.uniform(0.0, 1.0, nx)
+    A = np.diag(dia) + np.diag(off, 1) + np.diag(off, -1)
+    spec = build_alpha_circulant(N, alpha)
+    r = rng.normal(size=(N, nx))
+    u, _ = three_step_solve(spec, -A, dT, r)
+    op = ref_port.SampleOperator(dia, off, np.zeros(nx))
+    want, _ = ref_port.three_step(spec.eigenvalues, spec.scaling, ref_port.shifted_solvers(op, spec.eigenvalues, dT),
+                                  r)
+    cond = alpha ** (-(N - 1) / N)
+    assert rel(u, want) <= max(1e-10, 1e-13 * cond * np.log2(N)), rel(u, want)
+    if N <= 100:
+        model = LogNormalKL1D(nx=63, d=4)
+        grid = make_time_grid(1.0, N, 4)
+        cfg = SolverConfig(alpha=1e-3, tol=1e-8, max_outer_iters=60)
+        xi = rng.normal(size=(4, 4))
+        dia2, off2 = batched.tridiag_from_xi(xi, model.kl_table, model.h)
+        U0 = batched.coarse_sweep(dia2, off2, model.initial_condition(), N, grid.deltaT)
+        res = pcgc_solve_batched(model, xi, grid, cfg, U0)
+        out = batched.pcgc(dia2, off2, model.initial_condition(), U0, N, 4, 1.0, 1e-3, 1e-8, 60)
+        np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
+        assert rel(res.states.cpu().numpy(), out["states"]) <= RTOL
