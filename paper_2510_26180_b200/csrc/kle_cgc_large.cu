@@ -498,7 +498,6 @@ __global__ void __launch_bounds__(SShape<LOGN>::NT) cgcs_fwd_kernel(CgcArgs a, i
       const int i = c0 + col;
       if (i >= nx) break;
       const int j = col >> 1;
-      const double Di = fma(dT, __ldg(dd + i), 0.0);
       const double E = i > 0 ? dT * __ldg(ee + i - 1) : 0.0;
 #pragma unroll
       for (int q = 0; q < FPT; ++q) {
@@ -521,7 +520,6 @@ __global__ void __launch_bounds__(SShape<LOGN>::NT) cgcs_fwd_kernel(CgcArgs a, i
         yo[q][(size_t)i * NF] = y[q];
         ibo[q][(size_t)i * NF] = ibp[q];
       }
-      (void)Di;
     }
   }
 }
