@@ -259,22 +259,26 @@ __device__ __forceinline__ void reg_fft(Cplx (&x)[1 << LOGN], const Cplx* tw) {
 }
 
 // pivots 1/beta_i of (lambda_f I + dT A), f = 0..N/2, layout [s][f][i].
-// One CTA per sample: thread f runs the sequential complex recurrence
-// (factor_shifted, pintuq/pcgc.py:112-135) over the rows in chunks of SF_CH,
-// staging each chunk in shared memory so the whole CTA stores it coalesced
-// (rows contiguous per frequency).
-constexpr int SF_CH = 64;
-__global__ void __launch_bounds__(128) shift_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
-                                                           const double* __restrict__ lam, int M, int NF, int nx,
-                                                           double dT, double* __restrict__ sfac) {
-  extern __shared__ __align__(16) Cplx stage[];  // [NF][SF_CH + 1]
-  const int s = blockIdx.x;
-  const int f = threadIdx.x;
-  const double* d = dia + (size_t)s * nx;
-  const double* e = off + (size_t)s * nx;
-  Cplx* out = reinterpret_cast<Cplx*>(sfac) + (size_t)s * NF * nx;
-  const bool act = f < NF;
+// Thread (sample, f) runs the sequential complex recurrence (factor_shifted,
+// pintuq/pcgc.py:112-135) over the rows in chunks of SF_CH; a CTA packs
+// SPB = 128 / NF samples (N = 16: 14 samples x 9 frequencies on 126 of its 128
+// threads, instead of one sample on 9 of 64) and stages each chunk in shared
+// memory so the whole CTA stores it coalesced (rows contiguous per frequency).
+constexpr int SF_CH = 16;
+constexpr int SF_NT = 128;
+__global__ void __launch_bounds__(SF_NT) shift_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
+                                                             const double* __restrict__ lam, int M, int NF, int nx,
+                                                             double dT, double* __restrict__ sfac) {
+  extern __shared__ __align__(16) Cplx stage[];  // [SPB][NF][SF_CH + 1]
+  const int SPB = SF_NT / NF;
+  const int sl = threadIdx.x / NF, f = threadIdx.x - sl * NF;
+  const int s0 = blockIdx.x * SPB;
+  const int s = s0 + sl;
+  const bool act = sl < SPB && s < M;
+  const double* d = dia + (size_t)(act ? s : 0) * nx;
+  const double* e = off + (size_t)(act ? s : 0) * nx;
   const Cplx lm = act ? Cplx{lam[2 * f], lam[2 * f + 1]} : Cplx{1.0, 0.0};
+  const int ns = min(SPB, M - s0);
   Cplx ib = {0.0, 0.0};
   for (int i0 = 0; i0 < nx; i0 += SF_CH) {
     const int nr = min(SF_CH, nx - i0);
@@ -288,13 +292,15 @@ __global__ void __launch_bounds__(128) shift_factor_kernel(const double* __restr
           beta.im = fma(-E * E, ib.im, beta.im);
         }
         ib = crcp(beta);
-        stage[f * (SF_CH + 1) + r] = ib;
+        stage[(sl * NF + f) * (SF_CH + 1) + r] = ib;
       }
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < NF * nr; q += blockDim.x) {
-      const int ff = q / nr, r = q % nr;
-      out[(size_t)ff * nx + i0 + r] = stage[ff * (SF_CH + 1) + r];
+    for (int q = threadIdx.x; q < ns * NF * nr; q += SF_NT) {
+      const int r = q % nr, sf = q / nr;  // sf = sample-local * NF + frequency
+      const int ss = sf / NF, ff = sf - ss * NF;
+      Cplx* out = reinterpret_cast<Cplx*>(sfac) + ((size_t)(s0 + ss) * NF + ff) * nx;
+      out[i0 + r] = stage[sf * (SF_CH + 1) + r];
     }
     __syncthreads();
   }
@@ -812,9 +818,10 @@ int shift_factor(const double* dia, const double* off, const double* lam, int M,
   const int NF = N / 2 + 1;
   const long long nth = (long long)M * NF;
   if (nth == 0) return KLE_OK;
-  if (NF > 128) return set_error(KLE_ERR_UNSUPPORTED, "shift_factor: N > 254");
-  const size_t smem = sizeof(Cplx) * (size_t)NF * (SF_CH + 1);
-  shift_factor_kernel<<<(unsigned)M, NF <= 64 ? 64 : 128, smem, st>>>(dia, off, lam, M, NF, nx, dT, sfac);
+  if (NF > SF_NT) return set_error(KLE_ERR_UNSUPPORTED, "shift_factor: N > 254");
+  const int spb = SF_NT / NF;
+  const size_t smem = sizeof(Cplx) * (size_t)spb * NF * (SF_CH + 1);
+  shift_factor_kernel<<<(unsigned)((M + spb - 1) / spb), SF_NT, smem, st>>>(dia, off, lam, M, NF, nx, dT, sfac);
   return check_launch("shift_factor_kernel");
 }
 

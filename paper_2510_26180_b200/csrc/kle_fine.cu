@@ -27,66 +27,80 @@
 namespace kle {
 
 // ---------------------------------------------------------------------------
-// Factor kernel: one thread per sample, sequential LDL^T of T = I + h A and
-// the chunk/scan tables of the partitioned solve (layout: kle_common.cuh).
+// Factor kernel: one WARP per sample (round 2; it was one thread per sample with
+// every global access uncoalesced): the operator rows are loaded coalesced into
+// shared memory, lane 0 runs the sequential LDL^T of T = I + h A, the lanes build
+// the chunk / scan tables of the partitioned solve (layout: kle_common.cuh)
+// with the same operations in the same order as before (bit-identical blob),
+// and the warp stores the blob coalesced.
 // ---------------------------------------------------------------------------
 template <int MR, int P>
-__global__ void fine_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
-                                   double* __restrict__ blob, int M, int nx, double h, double g0) {
+__global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restrict__ dia,
+                                                         const double* __restrict__ off, double* __restrict__ blob,
+                                                         int M, int nx, double h, double g0) {
   using L = FineLayout<MR, P>;
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int NXP = L::NXP;
+  extern __shared__ __align__(16) double fsm[];
+  double* b = fsm;                  // [DOUBLES] the sample's blob
+  double* dd = fsm + L::DOUBLES;    // [NXP]
+  double* ee = dd + NXP;            // [NXP]: ee[i] couples rows i, i+1
+  const int s = blockIdx.x, lane = threadIdx.x;
   if (s >= M) return;
-  const double* d = dia + (size_t)s * nx;
-  const double* e = off + (size_t)s * nx;  // e[i] couples rows i, i+1; e[nx-1] unused
-  double* b = blob + (size_t)s * L::DOUBLES;
-  // LDL^T of I + hA: l_r (row r couples to r-1), inv_r = 1/beta_r; pad rows identity
-  double beta_prev = 1.0;
-  for (int row = 0; row < L::NXP; ++row) {
-    double l = 0.0, inv = 1.0;
-    if (row < nx) {
-      const double D = fma(h, d[row], 1.0);
-      double beta = D;
-      if (row > 0) {
-        const double E = h * e[row - 1];
-        l = E / beta_prev;
-        beta = fma(-l, E, D);
-      }
-      inv = 1.0 / beta;
-      beta_prev = beta;
-    }
-    b[L::L_OFF + row] = l;
-    b[L::INV_OFF + row] = inv;
+  for (int i = lane; i < NXP; i += 32) {
+    dd[i] = i < nx ? dia[(size_t)s * nx + i] : 0.0;
+    ee[i] = i < nx ? off[(size_t)s * nx + i] : 0.0;
   }
-  // chunk products: pie_k = prod_j (-l_j) over chunk k, sigs_k = prod_j (-l_{j+1})
-  double pie[P], sigs[P];
-  for (int k = 0; k < P; ++k) {
+  __syncwarp();
+  if (lane == 0) {  // LDL^T of I + hA: l_r (row r couples to r-1), inv_r = 1/beta_r; pad rows identity
+    double beta_prev = 1.0;
+    for (int row = 0; row < NXP; ++row) {
+      double l = 0.0, inv = 1.0;
+      if (row < nx) {
+        const double D = fma(h, dd[row], 1.0);
+        double beta = D;
+        if (row > 0) {
+          const double E = h * ee[row - 1];
+          l = E / beta_prev;
+          beta = fma(-l, E, D);
+        }
+        inv = 1.0 / beta;
+        beta_prev = beta;
+      }
+      b[L::L_OFF + row] = l;
+      b[L::INV_OFF + row] = inv;
+    }
+  }
+  __syncwarp();
+  // chunk products: pie_k = prod_j (-l_j) over chunk k, sigs_k = prod_j (-l_{j+1}); staged in dd / ee
+  double* pie = dd;
+  double* sigs = ee;
+  for (int k = lane; k < P; k += 32) {
     double pi = 1.0, sg = 1.0;
     for (int j = 0; j < MR; ++j) pi *= -b[L::L_OFF + k * MR + j];
     for (int j = MR - 1; j >= 0; --j) {
       const int row = k * MR + j;
-      sg *= -((row + 1 < L::NXP) ? b[L::L_OFF + row + 1] : 0.0);
+      sg *= -((row + 1 < NXP) ? b[L::L_OFF + row + 1] : 0.0);
     }
     pie[k] = pi;
     sigs[k] = sg;
   }
-  for (int t = 0; t < L::LOGP; ++t) {
-    const int dd = 1 << t;
-    for (int k = 0; k < P; ++k) {
+  __syncwarp();
+  for (int k = lane; k < P; k += 32) {
+    for (int t = 0; t < L::LOGP; ++t) {
+      const int d = 1 << t;
       double af = 0.0, bb = 0.0;
-      if (k >= dd) {
+      if (k >= d) {
         af = 1.0;
-        for (int q = k - dd + 1; q <= k; ++q) af *= pie[q];
+        for (int q = k - d + 1; q <= k; ++q) af *= pie[q];
       }
-      if (k + dd < P) {
+      if (k + d < P) {
         bb = 1.0;
-        for (int q = k; q <= k + dd - 1; ++q) bb *= sigs[q];
+        for (int q = k; q <= k + d - 1; ++q) bb *= sigs[q];
       }
       b[L::AF_OFF + t * P + k] = af;
       b[L::BB_OFF + t * P + k] = bb;
     }
-  }
-  // lazy-stitch vectors per chunk (be_steps_lazy)
-  for (int k = 0; k < P; ++k) {
+    // lazy-stitch vectors of chunk k (be_steps_lazy)
     const double* l = b + L::L_OFF + k * MR;
     const double* inv = b + L::INV_OFF + k * MR;
     double* phi = b + L::PHI_OFF + k * MR;
@@ -112,7 +126,15 @@ __global__ void fine_factor_kernel(const double* __restrict__ dia, const double*
       sg2[j] = fma(-l[j], sg2[j - 1], sg[j]);
     }
   }
+  __syncwarp();
+  double* out = blob + (size_t)s * L::DOUBLES;
+  for (int i = lane; i < L::DOUBLES; i += 32) out[i] = b[i];
   (void)g0;
+}
+
+template <int MR, int P>
+constexpr size_t fine_factor_smem() {
+  return sizeof(double) * ((size_t)FineLayout<MR, P>::DOUBLES + 2 * (size_t)FineLayout<MR, P>::NXP);
 }
 
 // ---------------------------------------------------------------------------
@@ -378,7 +400,14 @@ struct FineInst {
 
   static int factor(const double* dia, const double* off, double* blob, int M, int nx, double h,
                     double g0, cudaStream_t st) {
-    fine_factor_kernel<MR, P><<<(M + 63) / 64, 64, 0, st>>>(dia, off, blob, M, nx, h, g0);
+    constexpr size_t smem = fine_factor_smem<MR, P>();
+    static PerDeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, "kle_fine(factor): cudaFuncSetAttribute", [&] {
+          return cudaFuncSetAttribute(fine_factor_kernel<MR, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem);
+        }))
+      return rc;
+    if (M > 0) fine_factor_kernel<MR, P><<<(unsigned)M, 32, smem, st>>>(dia, off, blob, M, nx, h, g0);
     return check_launch("fine_factor_kernel");
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {

@@ -98,25 +98,44 @@ int gpc_basis(const double* xi, int M, int d, int degree, int family, const doub
 
 // Deterministic column sums over samples: out[l] = sum_s (U[s][l] - c[l])^p,
 // p = 1 without a center, p = 2 with one (two-pass variance).
-constexpr int CS_CHUNKS = 64;
+constexpr int CS_CHUNKS = 128;
 
+// per (column l, chunk): four interleaved partial sums (samples s0 + 4 q + u go
+// to accumulator u), so four loads per thread are in flight; combined in a
+// fixed order, so the result is deterministic
 __global__ void col_sum_partial_kernel(const double* __restrict__ U, int M, int L,
                                        const double* __restrict__ center, double* __restrict__ partial) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const int chunk = blockIdx.y, nch = gridDim.y;
   const int s0 = (int)(((long long)M * chunk) / nch), s1 = (int)(((long long)M * (chunk + 1)) / nch);
-  double acc = 0.0;
-  if (center) {
-    const double c = center[l];
-    for (int s = s0; s < s1; ++s) {
-      const double v = U[(size_t)s * L + l] - c;
-      acc = fma(v, v, acc);
+  const double c = center ? center[l] : 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int s = s0;
+  for (; s + 4 <= s1; s += 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(U + (size_t)(s + u) * L + l);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (center) {
+        const double dv = v[u] - c;
+        acc[u] = fma(dv, dv, acc[u]);
+      } else {
+        acc[u] += v[u];
+      }
     }
-  } else {
-    for (int s = s0; s < s1; ++s) acc += U[(size_t)s * L + l];
   }
-  partial[(size_t)chunk * L + l] = acc;
+  for (int u = 0; s < s1; ++s, ++u) {
+    const double v = __ldg(U + (size_t)s * L + l);
+    if (center) {
+      const double dv = v - c;
+      acc[u] = fma(dv, dv, acc[u]);
+    } else {
+      acc[u] += v;
+    }
+  }
+  partial[(size_t)chunk * L + l] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 __global__ void col_sum_final_kernel(const double* __restrict__ partial, int nch, int L, double* __restrict__ out) {
