@@ -95,8 +95,14 @@ __global__ void __launch_bounds__(G_NT) gemm_bias_kernel(const double* __restric
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = n0 + wn + j * 8 + 2 * t;
-      if (col < L) C[(size_t)row * L + col] = (bias ? bias[col] : 0.0) + acc[i][j][0];
-      if (col + 1 < L) C[(size_t)row * L + col + 1] = (bias ? bias[col + 1] : 0.0) + acc[i][j][1];
+      const size_t o = (size_t)row * L + col;
+      if (col + 1 < L && (o & 1) == 0) {  // the pair as one 16-byte store: full 64-byte row segments per warp
+        const double2 bv = bias ? *reinterpret_cast<const double2*>(bias + col) : make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(C + o) = make_double2(bv.x + acc[i][j][0], bv.y + acc[i][j][1]);
+      } else {
+        if (col < L) C[o] = (bias ? bias[col] : 0.0) + acc[i][j][0];
+        if (col + 1 < L) C[o + 1] = (bias ? bias[col + 1] : 0.0) + acc[i][j][1];
+      }
     }
   }
 }
