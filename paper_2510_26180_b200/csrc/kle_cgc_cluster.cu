@@ -283,11 +283,21 @@ __global__ void __launch_bounds__(SF_NT) shift_factor_kernel(const double* __res
   for (int i0 = 0; i0 < nx; i0 += SF_CH) {
     const int nr = min(SF_CH, nx - i0);
     if (act) {
-      for (int r = 0; r < nr; ++r) {
+      // the chunk's operator rows first (all loads in flight), then the dependent recurrence
+      double dv[SF_CH], ev[SF_CH];
+#pragma unroll
+      for (int r = 0; r < SF_CH; ++r) {
         const int i = i0 + r;
-        Cplx beta = {fma(dT, __ldg(d + i), lm.re), lm.im};
+        dv[r] = r < nr ? __ldg(d + i) : 0.0;
+        ev[r] = (r < nr && i > 0) ? __ldg(e + i - 1) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < SF_CH; ++r) {
+        if (r >= nr) break;
+        const int i = i0 + r;
+        Cplx beta = {fma(dT, dv[r], lm.re), lm.im};
         if (i > 0) {
-          const double E = dT * __ldg(e + i - 1);
+          const double E = dT * ev[r];
           beta.re = fma(-E * E, ib.re, beta.re);
           beta.im = fma(-E * E, ib.im, beta.im);
         }

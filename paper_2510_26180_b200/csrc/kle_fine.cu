@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
       b[L::AF_OFF + t * P + k] = af;
       b[L::BB_OFF + t * P + k] = bb;
     }
-    // lazy-stitch vectors of chunk k (be_steps_lazy)
+    // lazy-stitch vectors of chunk k: read only by be_steps_lazy (KLE_FINE_LAZY=1 builds), so neither
+    // computed nor stored otherwise (they are two thirds of the blob)
+    if (!KLE_FINE_LAZY) continue;
     const double* l = b + L::L_OFF + k * MR;
     const double* inv = b + L::INV_OFF + k * MR;
     double* phi = b + L::PHI_OFF + k * MR;
@@ -128,7 +130,8 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
   }
   __syncwarp();
   double* out = blob + (size_t)s * L::DOUBLES;
-  for (int i = lane; i < L::DOUBLES; i += 32) out[i] = b[i];
+  const int nstore = KLE_FINE_LAZY ? L::DOUBLES : L::PHI_OFF;  // l, 1/beta and the scan multipliers
+  for (int i = lane; i < nstore; i += 32) out[i] = b[i];
   (void)g0;
 }
 
