@@ -11,6 +11,7 @@
 //   rhs_n = dT (A b_n + g) + b_n,  b_n = F_n - G(prev_n)
 //         = (I + dT A) F_n - prev_n
 // so the coarse solve of the reference collapses to one matvec.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kle_fine.cuh"
@@ -415,7 +416,9 @@ struct FineInst {
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {
     dim3 grid(a.M, (a.N + NC - 1) / NC);
-    const size_t smem = a.F_given ? 0 : FgrSmem<MR, P, NC>::BYTES;
+    size_t smem = a.F_given ? 0 : FgrSmem<MR, P, NC>::BYTES;
+    static const char* pad_env = getenv("KLE_FGR_PAD_SMEM");  // tuning: extra bytes per CTA (lowers CTAs/SM)
+    if (pad_env && smem) smem = std::min<size_t>(smem + (size_t)atoi(pad_env), 200 * 1024);
     static PerDeviceOnce attr_once;
     if (int rc = once_per_device(attr_once, "kle_fine: cudaFuncSetAttribute", [&] {
           return cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -183,10 +183,14 @@ __device__ __forceinline__ void chunk_products(double* cs, const LaneFactors<MR,
   }
 }
 
+#ifndef KLE_FGR_EXP
+#define KLE_FGR_EXP 0  // timing ablation only (wrong results): bit0 skips the carry scans, bit1 the stitch loops
+#endif
 template <int MR, int P, int R>
 __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, int J,
                                             const double* cs) {
   using L = FineLayout<MR, P>;
+  constexpr bool SCAN = !(KLE_FGR_EXP & 1), STITCH = !(KLE_FGR_EXP & 2);
   const unsigned base = (unsigned)__cvta_generic_to_shared(cs) + (unsigned)(k * sizeof(double));
   for (int it = 0; it < J; ++it) {
 #pragma unroll
@@ -196,6 +200,7 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
     double Y[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+    if constexpr (SCAN) {
 #pragma unroll
     for (int t = 0; t < L::LOGP; ++t) {
 #pragma unroll
@@ -209,6 +214,8 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
       const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
       Y[r] = (k == 0) ? 0.0 : o;
     }
+    }
+    if constexpr (STITCH)
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
       const double pi = lds_f64(base + (unsigned)((0 * MR + j) * P * sizeof(double)));
@@ -229,6 +236,7 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
     double X[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) X[r] = x[r][0];
+    if constexpr (SCAN) {
 #pragma unroll
     for (int t = 0; t < L::LOGP; ++t) {
 #pragma unroll
@@ -242,6 +250,8 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
       const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
       X[r] = (k == P - 1) ? 0.0 : o;
     }
+    }
+    if constexpr (STITCH)
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
       const double sg = lds_f64(base + (unsigned)((1 * MR + j) * P * sizeof(double)));

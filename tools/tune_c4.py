@@ -58,3 +58,15 @@ tf = timed(fgr)
 tc = timed(cgc)
 print(f"{_lib.library_path().name}: fgr {tf:.3f} ms ({6 * M * N * J * nx / tf / 1e9:.2f} TF/s) "
       f"cgc {tc:.3f} ms ({24 * M * N * nx / tc / 1e6:.0f} GB/s)  checks {Rsum:.15e} {Usum:.15e}", flush=True)
+
+if len(sys.argv) > 2 and sys.argv[2] == "jsweep":
+    # fixed cost per launch (prologue + epilogue) vs the per-step cost: t(J) = a + b J
+    ts = {}
+    for Jv in (1, 2, 8, 16, 32, 64):
+        def f(Jv=Jv):
+            _lib.call("kle_fgr_f64", ptr(U), ptr(op.u0), None, None, ptr(R), ptr(blob), ptr(op.dia), ptr(op.off),
+                      ptr(tables.scaling), None, M, N, nx, Jv, grid.deltat, grid.deltaT, 1.0, 1e-3, st)
+        ts[Jv] = timed(f)
+    b = (ts[64] - ts[16]) / 48
+    print("jsweep ms:", {k: round(v, 3) for k, v in ts.items()}, f"per-step {b:.4f} ms, fixed {ts[32] - 32 * b:.3f} ms",
+          flush=True)
