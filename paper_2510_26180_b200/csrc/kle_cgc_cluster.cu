@@ -43,15 +43,15 @@ namespace cg = cooperative_groups;
 namespace kle {
 
 #ifdef KLE_CGC_TIMING
-// debug: per-CTA phase timestamps (globaltimer ns), first 4096 CTAs
+// debug: per-CTA phase timestamps (SM clock cycles), CTAs [KLE_CGC_T0, KLE_CGC_T0 + 4096)
+#ifndef KLE_CGC_T0
+#define KLE_CGC_T0 100000
+#endif
 __device__ unsigned long long g_cgc_t[4096][10];
-#define CGC_T(i)                                                                          \
-  do {                                                                                    \
-    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                          \
-      unsigned long long t_;                                                              \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
-      g_cgc_t[blockIdx.x][i] = t_;                                                        \
-    }                                                                                     \
+#define CGC_T(i)                                                                                  \
+  do {                                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x >= KLE_CGC_T0 && blockIdx.x < KLE_CGC_T0 + 4096)           \
+      g_cgc_t[blockIdx.x - KLE_CGC_T0][i] = (unsigned long long)clock64();                        \
   } while (0)
 #else
 #define CGC_T(i) \

@@ -14,6 +14,36 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "kle_common.cuh"
+namespace kle {
+#ifdef KLE_FGR_TIMING
+// debug: per-CTA phase timestamps (SM clock), CTAs [KLE_FGR_T0, KLE_FGR_T0 + 4096)
+#ifndef KLE_FGR_T0
+#define KLE_FGR_T0 60000
+#endif
+__device__ long long g_fgr_t[4096][16];
+#define FGR_T(i)                                                                              \
+  do {                                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x >= KLE_FGR_T0 && blockIdx.x < KLE_FGR_T0 + 4096)       \
+      g_fgr_t[blockIdx.x - KLE_FGR_T0][i] = (i == 7) ? (long long)__smid() : clock64();       \
+    if (i == 7 && threadIdx.x == 0 && blockIdx.x >= KLE_FGR_T0 && blockIdx.x < KLE_FGR_T0 + 4096) {  \
+      unsigned w_;                                                                            \
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(w_));                                       \
+      g_fgr_t[blockIdx.x - KLE_FGR_T0][15] = w_;                                              \
+    }                                                                                         \
+  } while (0)
+__device__ __forceinline__ unsigned __smid() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+extern "C" int kle_debug_fgr_timing(long long* host) { return (int)cudaMemcpyFromSymbol(host, g_fgr_t, sizeof(g_fgr_t)); }
+#else
+#define FGR_T(i) \
+  do {           \
+  } while (0)
+#endif
+}  // namespace kle
 #include "kle_fine.cuh"
 #include "kle_internal.h"
 
@@ -25,7 +55,14 @@
                        // (5.79 vs 5.43 ms), A/B only; the one-warp variants (NT = 32) always use them
 #endif
 
+#ifndef KLE_FGR_LZ
+#define KLE_FGR_LZ 0  // 1: one-warp variants use the overlapped lazy-stitch step (be_steps_lz): solo warp 1,082 vs
+                      // 1,301 cycles per step, but 4.69 vs 4.67 ms per 131k c4 launch at 2 warps per sub-partition (A/B)
+#endif
+
 namespace kle {
+
+
 
 // ---------------------------------------------------------------------------
 // Factor kernel: one WARP per sample (round 2; it was one thread per sample with
@@ -162,7 +199,7 @@ struct FgrSmem {
   static constexpr int LD = NXP;
   static constexpr int SWZ = (MR < 16 ? MR : 16) - 1;
   __device__ __forceinline__ static int pidx(int row) { return row ^ ((row / MR) & SWZ); }
-  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8 + 3 * NXP) * sizeof(double);
+  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8 + 5 * NXP) * sizeof(double);
 };
 
 template <int MR, int P, int R, int NT, bool PIPE>
@@ -189,6 +226,8 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
   for (int r = 0; r < R; ++r) nl[r] = (w * SLOTS + slot) * R + r;
 
   double x[R][MR];
+  FGR_T(0);
+  FGR_T(7);
   if (a.F_given == nullptr) {
     extern __shared__ __align__(16) double sm[];
     using SM = FgrSmem<MR, P, NC>;
@@ -197,47 +236,118 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
     double* p0 = st + NC * LD;    // [LD]
     double* dd = p0 + LD;         // [LD]
     double* ee = dd + LD;         // [LD + MR]: ee[pidx(i)] couples rows i-1 and i
-    for (int ln = 0; ln < NC; ++ln) {  // no division in the index math
-      const int n = n0 + ln;
-      if (n >= N) break;
-      const double* src = (n == 0) ? a.u0 : a.U + sbase + (size_t)(n - 1) * nx;
-      for (int row = tid; row < nx; row += NT) cp_async8(st + ln * LD + SM::pidx(row), src + row);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);  // group 1: the start rows (needed first)
-    if (n0 == 0)
-      for (int row = tid; row < nx; row += NT) cp_async8(p0 + SM::pidx(row), a.U + sbase + (size_t)(N - 1) * nx + row);
-    for (int row = tid; row < nx; row += NT) {
-      cp_async8(dd + SM::pidx(row), a.dia + (size_t)s * nx + row);
-      if (row + 1 < nx) cp_async8(ee + SM::pidx(row + 1), a.off + (size_t)s * nx + row);
+    // Two prologues. FAST (one-warp CTAs, c4 / c1 shapes, where the fixed cost was 31% of a launch): the
+    // factor rows are requested first (the chunk products depend on them, the longest dependent chain), the
+    // copy loops are straight predicated LDGSTS over per-thread row slots, and the start rows come out of
+    // shared memory through unconditional volatile loads followed by selects. The compiler otherwise sinks
+    // each load under its select and serialises 64 load-use pairs behind branches: 9.9k cycles per CTA at
+    // c4 (tools/fgr_timing.py), 5.18 -> 4.56 ms per 131k-sample launch with this form. The multi-warp
+    // variants keep the original form: at c2 the prologue is 7% of a CTA's life and the step loop's
+    // register allocation is sensitive to it (10.17 ms per 8,192 samples against 10.6-11.0 with the fast form).
+    constexpr bool FAST = NT == 32;
+    constexpr int RPT = (NXP + NT - 1) / NT;
+    LaneFactors<MR, P> fac;
+    if constexpr (FAST) {
+      fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
+      int so[RPT];
+      bool rv[RPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int row = tid + i * NT;
+        rv[i] = row < nx;
+        so[i] = SM::pidx(rv[i] ? row : 0);
+      }
+      for (int ln = 0; ln < NC; ++ln) {
+        const int n = n0 + ln;
+        if (n >= N) break;
+        const double* src = ((n == 0) ? a.u0 : a.U + sbase + (size_t)(n - 1) * nx) + tid;
+        double* dst = st + ln * LD;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (rv[i]) cp_async8(dst + so[i], src + i * NT);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);  // group 1: the start rows (needed first)
+      const double* pl = a.U + sbase + (size_t)(N - 1) * nx + tid;
+      const double* dg = a.dia + (size_t)s * nx + tid;
+      const double* eg = a.off + (size_t)s * nx + tid;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int row = tid + i * NT;
+        if (rv[i]) {
+          if (n0 == 0) cp_async8(p0 + so[i], pl + i * NT);
+          cp_async8(dd + so[i], dg + i * NT);
+          if (row + 1 < nx) cp_async8(ee + SM::pidx(row + 1), eg + i * NT);
+        }
+      }
+    } else {
+      for (int ln = 0; ln < NC; ++ln) {  // no division in the index math
+        const int n = n0 + ln;
+        if (n >= N) break;
+        const double* src = (n == 0) ? a.u0 : a.U + sbase + (size_t)(n - 1) * nx;
+        for (int row = tid; row < nx; row += NT) cp_async8(st + ln * LD + SM::pidx(row), src + row);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);  // group 1: the start rows (needed first)
+      if (n0 == 0)
+        for (int row = tid; row < nx; row += NT) cp_async8(p0 + SM::pidx(row), a.U + sbase + (size_t)(N - 1) * nx + row);
+      for (int row = tid; row < nx; row += NT) {
+        cp_async8(dd + SM::pidx(row), a.dia + (size_t)s * nx + row);
+        if (row + 1 < nx) cp_async8(ee + SM::pidx(row + 1), a.off + (size_t)s * nx + row);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);  // group 2: epilogue operands
     if (tid == 0) {
       ee[0] = 0.0;
       ee[SM::pidx(nx)] = 0.0;
     }
-    LaneFactors<MR, P> fac;
-    fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
+    if constexpr (!FAST) fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
     const double hg = a.dt * a.g0;
-    double* cs = ee + LD + MR;  // [3][MR][P] chunk products (KLE_FINE_CS)
+    double* cs = ee + LD + MR;  // [3][MR][P] chunk products (KLE_FINE_CS) / [5][MR][P] lazy tables (LZ)
     // chunk products from shared memory: the one-warp R = 4 variant (c4: 234 registers, 8 chains per
     // SMSP; 6.16 -> 5.17 ms per 131k-sample launch), or every variant under KLE_FINE_CS
     constexpr bool CS = (KLE_FINE_CS || NT == 32) && !PIPE && !KLE_FINE_LAZY;
-    if constexpr (CS) {
+    constexpr bool LZ = CS && KLE_FGR_LZ;
+    if constexpr (LZ) {
+      if (w == 0 && slot == 0) lazy_tables<MR, P>(cs, fac, k, hg);
+    } else if constexpr (CS) {
       if (w == 0 && slot == 0) chunk_products<MR, P>(cs, fac, k, hg);
     }
+    FGR_T(1);
     asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
+    FGR_T(2);
+    if constexpr (FAST) {
+      // the lane's rows k MR + j sit at k MR + (j ^ (k & SWZ)); pad rows and unused slots hold garbage
+      // that the select drops
+      const int kx = k & SM::SWZ;
+      const unsigned sr0 = (unsigned)__cvta_generic_to_shared(st + nl[0] * LD + k * MR);
+      unsigned xo[MR];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+      for (int j = 0; j < MR; ++j) xo[j] = sr0 + (unsigned)((j ^ kx) * sizeof(double));
 #pragma unroll
-      for (int j = 0; j < MR; ++j) {
-        const int row = k * MR + j;
-        x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * LD + SM::pidx(row)] + hg : 0.0;
+      for (int r = 0; r < R; ++r) {
+        const int lim = (n0 + nl[r] < N) ? fac.nreal : 0;  // rows j < lim of this right-hand side are real
+#pragma unroll
+        for (int j = 0; j < MR; ++j) {
+          const double v = lds_f64(xo[j] + (unsigned)(r * LD * sizeof(double)));
+          x[r][j] = (j < lim) ? v + hg : 0.0;
+        }
       }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < MR; ++j) {
+          const int row = k * MR + j;
+          x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * LD + SM::pidx(row)] + hg : 0.0;
+        }
+    }
+    FGR_T(3);
     if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
     else if constexpr (KLE_FINE_LAZY) be_steps_lazy<MR, P, R>(x, fac, a.ffac + (size_t)s * L::DOUBLES, k, a.J, hg);
+    else if constexpr (LZ) be_steps_lz<MR, P, R>(x, fac, k, a.J, cs);
     else if constexpr (CS) be_steps_cs<MR, P, R>(x, fac, k, a.J, cs);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
+    FGR_T(4);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -299,13 +409,25 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
       }
     }
     __syncthreads();
+    FGR_T(5);
     for (int ln = 0; ln < NC; ++ln) {
       const int n = n0 + ln;
       if (n >= N) break;
       double* out = a.Rout + sbase + (size_t)n * nx;
       const double* rs = st + ln * LD;
-      for (int row = tid; row < nx; row += NT) out[row] = rs[SM::pidx(row)];
+      if constexpr (FAST) {
+        out += tid;
+        double v[RPT];  // (row slots recomputed here: keeping them live over the step loop costs registers)
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) v[i] = rs[SM::pidx(tid + i * NT < nx ? tid + i * NT : 0)];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (tid + i * NT < nx) out[i * NT] = v[i];
+      } else {
+        for (int row = tid; row < nx; row += NT) out[row] = rs[SM::pidx(row)];
+      }
     }
+    FGR_T(6);
     return;
   }
   // ---- F given (stand-alone cgc_correct): no sweep ----------------------------

@@ -7,6 +7,11 @@
 // that share the sample's factor rows (read from shared memory).
 #pragma once
 #include "kle_common.cuh"
+#ifndef FGR_T
+#define FGR_T(i) \
+  do {           \
+  } while (0)
+#endif
 
 namespace kle {
 
@@ -193,10 +198,12 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
   constexpr bool SCAN = !(KLE_FGR_EXP & 1), STITCH = !(KLE_FGR_EXP & 2);
   const unsigned base = (unsigned)__cvta_generic_to_shared(cs) + (unsigned)(k * sizeof(double));
   for (int it = 0; it < J; ++it) {
+    if (it == 1) FGR_T(8);
 #pragma unroll
     for (int j = 1; j < MR; ++j)
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+    if (it == 1) FGR_T(9);
     double Y[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
@@ -215,13 +222,16 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
       Y[r] = (k == 0) ? 0.0 : o;
     }
     }
-    if constexpr (STITCH)
+    if (it == 1) FGR_T(10);
+    if constexpr (STITCH) {
 #pragma unroll
     for (int j = 0; j < MR; ++j) {
       const double pi = lds_f64(base + (unsigned)((0 * MR + j) * P * sizeof(double)));
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r][j] = fma(pi, Y[r], x[r][j]);
     }
+    }
+    if (it == 1) FGR_T(11);
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
       const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
@@ -233,6 +243,7 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
         x[r][j] = z;
       }
     }
+    if (it == 1) FGR_T(12);
     double X[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) X[r] = x[r][0];
@@ -251,13 +262,16 @@ __device__ __forceinline__ void be_steps_cs(double (&x)[R][MR], const LaneFactor
       X[r] = (k == P - 1) ? 0.0 : o;
     }
     }
-    if constexpr (STITCH)
+    if (it == 1) FGR_T(13);
+    if constexpr (STITCH) {
 #pragma unroll
     for (int j = MR - 1; j >= 0; --j) {
       const double sg = lds_f64(base + (unsigned)((1 * MR + j) * P * sizeof(double)));
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
     }
+    }
+    if (it == 1) FGR_T(14);
   }
 }
 
@@ -447,6 +461,181 @@ __device__ __forceinline__ void be_steps_lazy(double (&x)[R][MR], const LaneFact
     const double phi = blob[L::PHI_OFF + k * MR + j], sg = blob[L::SG_OFF + k * MR + j];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r][j] = fma(X[r], sg, fma(Y[r], phi, x[r][j]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Overlapped lazy-stitch step with the R-independent row vectors in shared
+// memory (lz: [5][MR][P] = kap, phi2, sg2, phi, sg; built once per CTA by
+// lazy_tables with the operations of fine_factor_kernel's lazy block). Same
+// algebra as be_steps_lazy; the state between steps is yl = Fwd0(x). Every
+// carry scan runs in the shadow of row work that does not depend on it:
+//   A  forward scan of last(yl)            ||  xl0 = Bwd0(yl inv + kap)
+//   B  backward scan of xl0_0 + Y phi_0    ||  w = Fwd0(xl0), then w += Y phi2 (one row behind the chain)
+//   C  yl' = w + X sg2, last row first so that the next step's forward scan
+//      starts under the remaining rows
+// Five R-dependent FMAs per row and step, as in be_steps. One shuffle round
+// is consumed per SEG rows (a round's latency ~ SEG R chain FMAs).
+template <int MR, int P>
+__device__ __forceinline__ void lazy_tables(double* lz, const LaneFactors<MR, P>& f, int k, double hg) {
+  double phi[MR], sg[MR];
+  double pi = 1.0;
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    pi *= -f.l[j];
+    phi[j] = pi * f.inv[j];
+  }
+#pragma unroll
+  for (int j = MR - 2; j >= 0; --j) phi[j] = fma(-f.l[j + 1], phi[j + 1], phi[j]);
+  double g = 1.0;
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+    g *= -ln;
+    sg[j] = g;
+    lz[(0 * MR + j) * P + k] = (j < f.nreal) ? hg * (1.0 + ln) : 0.0;
+    lz[(3 * MR + j) * P + k] = phi[j];
+    lz[(4 * MR + j) * P + k] = g;
+  }
+  double p2 = phi[0], s2 = sg[0];
+  lz[(1 * MR + 0) * P + k] = p2;
+  lz[(2 * MR + 0) * P + k] = s2;
+#pragma unroll
+  for (int j = 1; j < MR; ++j) {
+    p2 = fma(-f.l[j], p2, phi[j]);
+    s2 = fma(-f.l[j], s2, sg[j]);
+    lz[(1 * MR + j) * P + k] = p2;
+    lz[(2 * MR + j) * P + k] = s2;
+  }
+}
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void be_steps_lz(double (&x)[R][MR], const LaneFactors<MR, P>& f, int k, int J,
+                                            const double* lz) {
+  using L = FineLayout<MR, P>;
+  constexpr int LOGP = L::LOGP, NS = LOGP + 1;
+  constexpr int SEG = (MR + NS - 1) / NS;  // rows per shuffle round
+  if (J <= 0) return;
+  const unsigned base = (unsigned)__cvta_generic_to_shared(lz) + (unsigned)(k * sizeof(double));
+  auto tab = [&](int t, int j) { return lds_f64(base + (unsigned)((t * MR + j) * P * sizeof(double))); };
+  double Y[R], X[R], o[R];
+  // one consumption point of a scan: st < LOGP multiplies and re-shuffles, st = LOGP takes the neighbour's value
+  auto ystep = [&](int st) {
+    if (st < LOGP) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        Y[r] = fma(f.af[st], o[r], Y[r]);  // af = 0 for k < 2^st
+        o[r] = __shfl_up_sync(KLE_FULL_MASK, Y[r], (st + 1 < LOGP) ? (1 << (st + 1)) : 1, P);
+      }
+    } else if (st == LOGP) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) Y[r] = (k == 0) ? 0.0 : o[r];
+    }
+  };
+  auto xstep = [&](int st) {
+    if (st < LOGP) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        X[r] = fma(f.bb[st], o[r], X[r]);  // bb = 0 for k + 2^st >= P
+        o[r] = __shfl_down_sync(KLE_FULL_MASK, X[r], (st + 1 < LOGP) ? (1 << (st + 1)) : 1, P);
+      }
+    } else if (st == LOGP) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) X[r] = (k == P - 1) ? 0.0 : o[r];
+    }
+  };
+  // phase A: xl0 = Bwd0(yl inv + kap) with the forward scan (round 0 already issued) consumed along the rows
+  auto phaseA = [&]() {
+#pragma unroll
+    for (int jj = 0; jj < MR; ++jj) {
+      const int j = MR - 1 - jj;
+      const double ln = (j + 1 < MR) ? f.l[j + 1] : f.lnx;
+      const double kap = tab(0, j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double z = fma(x[r][j], f.inv[j], kap);
+        if (j + 1 < MR) z = fma(-ln, x[r][j + 1], z);
+        x[r][j] = z;
+      }
+      if ((jj + 1) % SEG == 0 && (jj + 1) / SEG <= NS) ystep((jj + 1) / SEG - 1);
+    }
+#pragma unroll
+    for (int st = MR / SEG; st < NS; ++st) ystep(st);
+  };
+
+#pragma unroll
+  for (int j = 1; j < MR; ++j)
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    Y[r] = x[r][MR - 1];
+    o[r] = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
+  }
+  const double phi0 = tab(3, 0);
+  for (int it = 0; it < J - 1; ++it) {
+    phaseA();
+    // phase B
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      X[r] = fma(Y[r], phi0, x[r][0]);
+      o[r] = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
+    }
+#pragma unroll
+    for (int j = 1; j <= MR; ++j) {
+      if (j < MR) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r][j] = fma(-f.l[j], x[r][j - 1], x[r][j]);
+      }
+      const double p2 = tab(1, j - 1);  // row j - 1 has left the chain
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j - 1] = fma(Y[r], p2, x[r][j - 1]);
+      if (j % SEG == 0 && j / SEG <= NS) xstep(j / SEG - 1);
+    }
+#pragma unroll
+    for (int st = MR / SEG; st < NS; ++st) xstep(st);
+    // phase C, the last row first: it feeds round 0 of the next forward scan
+    {
+      const double s2 = tab(2, MR - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[r][MR - 1] = fma(X[r], s2, x[r][MR - 1]);
+        Y[r] = x[r][MR - 1];
+        o[r] = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);
+      }
+    }
+#pragma unroll
+    for (int j = MR - 2; j >= 0; --j) {
+      const double s2 = tab(2, j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(X[r], s2, x[r][j]);
+    }
+  }
+  // last step: materialise x' = xl0 + Y phi + X sg (the Y part runs under the backward scan)
+  phaseA();
+  {
+    const double ph = tab(3, 0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      x[r][0] = fma(Y[r], ph, x[r][0]);
+      X[r] = x[r][0];
+      o[r] = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);
+    }
+  }
+#pragma unroll
+  for (int j = 1; j < MR; ++j) {
+    const double ph = tab(3, j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r][j] = fma(Y[r], ph, x[r][j]);
+    if (j % SEG == 0 && j / SEG <= NS) xstep(j / SEG - 1);
+  }
+#pragma unroll
+  for (int st = (MR - 1) / SEG; st < NS; ++st) xstep(st);
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const double sgj = tab(4, j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r][j] = fma(X[r], sgj, x[r][j]);
   }
 }
 

@@ -50,6 +50,14 @@ def timed(fn, reps=5):
 
 fgr()
 Rsum = float(R.sum().item())
+import os
+if os.environ.get("TUNE_SAVE"):
+    torch.save(R[:4096].cpu(), os.environ["TUNE_SAVE"])
+if os.environ.get("TUNE_CMP"):
+    ref = torch.load(os.environ["TUNE_CMP"])
+    got = R[:4096].cpu()
+    print("fgr vs saved: max abs diff %.3e, max rel (to max |ref|) %.3e" % (float((got - ref).abs().max()),
+          float((got - ref).abs().max() / ref.abs().max())), flush=True)
 U.copy_(U0)
 cgc()
 Usum = float(U.sum().item())
