@@ -887,6 +887,7 @@ int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st) {
   int MR, CL, LOGN;
   if (!cluster_shape(a.N, a.nx, &MR, &CL, &LOGN)) return set_error(KLE_ERR_UNSUPPORTED, "cgc_cluster: shape");
   if (a.M <= 0) return KLE_OK;
+  if (cgc_row_supported(a.N, a.nx)) return cgc_row_run(a, sfac, st);  // same pivots, same arguments
   if (a.imag) cudaMemsetAsync(a.imag, 0, sizeof(double) * a.M, st);  // real by construction
   if (MR == 4) return dispatch_logn<4>(LOGN, a, sfac, CL, st);
   return dispatch_logn<8>(LOGN, a, sfac, CL, st);

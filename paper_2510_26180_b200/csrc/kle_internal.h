@@ -165,6 +165,10 @@ size_t shift_factor_doubles(int M, int N, int nx);
 int shift_factor(const double* dia, const double* off, const double* lam, int M, int N, int nx, double dT,
                  double* sfac, cudaStream_t st);
 int cgc_cluster_run(const CgcArgs& a, const double* sfac, cudaStream_t st);
+// small blocks (power-of-two N <= 16, nx <= 128): one CTA per sample, register FFTs (kle_cgc_row.cu);
+// cgc_cluster_run dispatches to it
+bool cgc_row_supported(int N, int nx);
+int cgc_row_run(const CgcArgs& a, const double* sfac, cudaStream_t st);
 
 int cgc_grid(int M, int N, int nx);
 size_t cgc_scratch_doubles_per_cta(int N, int nx);

@@ -61,6 +61,13 @@ if os.environ.get("TUNE_CMP"):
 U.copy_(U0)
 cgc()
 Usum = float(U.sum().item())
+if os.environ.get("TUNE_SAVE"):
+    torch.save(U[:4096].cpu(), os.environ["TUNE_SAVE"] + ".u")
+if os.environ.get("TUNE_CMP"):
+    ref = torch.load(os.environ["TUNE_CMP"] + ".u")
+    got = U[:4096].cpu()
+    print("cgc vs saved: max abs diff %.3e, max rel (to max |ref|) %.3e" % (float((got - ref).abs().max()),
+          float((got - ref).abs().max() / ref.abs().max())), flush=True)
 U.copy_(U0)
 tf = timed(fgr)
 tc = timed(cgc)
