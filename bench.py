@@ -387,6 +387,10 @@ def run_b200(args):
         cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_all[:n_sub])
     if rank == 0:
         fp64_peak = peaks.get("fp64_tflops")
+        # small blocks take the row-FFT kernel (kle_cgc_row.cu), the others the cluster kernel
+        row_path = c["N"] <= 16 and c["nx"] <= 128 and os.environ.get("KLE_CGC_ROW", "1") != "0"
+        cgc_path = "row (one CTA per sample, register FFTs)" if row_path else "cluster"
+        cgc_kernel_name = "cgc_row_kernel" if row_path else "cgc_cluster_kernel"
         line = {
             "metric": METRIC,
             "value": solves_per_s,
@@ -431,8 +435,8 @@ def run_b200(args):
                                "frac": cgc_gbs / peaks["hbm_gbs"], "ms_per_launch": cgc_ms,
                                "algorithmic": "24 B per (n, i) per sample: read R, read U, write U "
                                               "(+ pivots 16 (N/2+1)/N B not counted)",
-                               "path": "cluster",
-                               "traffic": traffic_of(peaks, args.config, "cgc_cluster_kernel", M)},
+                               "path": cgc_path,
+                               "traffic": traffic_of(peaks, args.config, cgc_kernel_name, M)},
                 "gemm_bias_kernel": {"bound": "tensor(dmma)", "achieved": gemm_tflops,
                                      "peak": peaks.get("dmma_tflops"), "unit": "TFLOP/s",
                                      "frac": gemm_tflops / peaks["dmma_tflops"] if peaks.get("dmma_tflops") else None,

@@ -199,7 +199,9 @@ struct FgrSmem {
   static constexpr int LD = NXP;
   static constexpr int SWZ = (MR < 16 ? MR : 16) - 1;
   __device__ __forceinline__ static int pidx(int row) { return row ^ ((row / MR) & SWZ); }
-  static constexpr size_t BYTES = ((size_t)(NC + 3) * LD + MR + 8 + 5 * NXP) * sizeof(double);
+  // TABS row vectors [MR][P] behind the staging: 3 chunk-product tables (be_steps_cs), 5 lazy tables
+  // (be_steps_lz), none for the register-product variants (c2: 37 KB per CTA instead of 49)
+  static constexpr size_t bytes(int tabs) { return ((size_t)(NC + 3) * LD + MR + 8 + (size_t)tabs * NXP) * sizeof(double); }
 };
 
 template <int MR, int P, int R, int NT, bool PIPE>
@@ -538,7 +540,8 @@ struct FineInst {
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {
     dim3 grid(a.M, (a.N + NC - 1) / NC);
-    size_t smem = a.F_given ? 0 : FgrSmem<MR, P, NC>::BYTES;
+    constexpr bool CS = (KLE_FINE_CS || NT == 32) && !PIPE && !KLE_FINE_LAZY;  // as in fgr_kernel
+    size_t smem = a.F_given ? 0 : FgrSmem<MR, P, NC>::bytes(CS ? (KLE_FGR_LZ ? 5 : 3) : 0);
     static const char* pad_env = getenv("KLE_FGR_PAD_SMEM");  // tuning: extra bytes per CTA (lowers CTAs/SM)
     if (pad_env && smem) smem = std::min<size_t>(smem + (size_t)atoi(pad_env), 200 * 1024);
     static PerDeviceOnce attr_once;
