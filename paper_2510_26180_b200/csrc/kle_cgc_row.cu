@@ -394,8 +394,8 @@ int launch_row(const CgcArgs& a, const double* sfac, cudaStream_t st) {
 }  // namespace
 
 bool cgc_row_supported(int N, int nx) {
-  static const char* env = getenv("KLE_CGC_ROW");  // 0: keep the cluster kernel for these shapes (A/B)
-  if (env && atoi(env) == 0) return false;
+  const char* env = getenv("KLE_CGC_ROW");  // 0: keep the cluster kernel for these shapes (A/B; read per call)
+  if (env && *env && atoi(env) == 0) return false;
   return N >= 2 && N <= 16 && (N & (N - 1)) == 0 && nx >= 1 && nx <= RW_RB;
 }
 

@@ -579,3 +579,38 @@ def test_non_power_of_two_time_fft(cuda, N):
         out = batched.pcgc(dia2, off2, model.initial_condition(), U0, N, 4, 1.0, 1e-3, 1e-8, 60)
         np.testing.assert_array_equal(res.iters.cpu().numpy(), out["iters"])
         assert rel(res.states.cpu().numpy(), out["states"]) <= RTOL
+
+
+@pytest.mark.parametrize("N,nx", [(2, 1), (2, 5), (4, 33), (8, 100), (16, 64), (16, 127), (16, 128)])
+def test_row_fft_cgc_matches_cluster_kernel_and_dense(cuda, N, nx, monkeypatch):
+    """The small-block CGC kernel (kle_cgc_row.cu: thread-per-row real FFTs in
+    registers, one CTA per sample; default for power-of-two N <= 16, nx <= 128)
+    against the cluster kernel (KLE_CGC_ROW=0) on random symmetric tridiagonal
+    operators and right-hand sides, ragged nx included, and against the dense
+    solve of (C_alpha (x) I + dT I (x) A) u = r (pintuq/pcgc.py:148-172)."""
+    import torch
+
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import build_alpha_circulant, three_step_device
+
+    rng = np.random.default_rng(1000 * N + nx)
+    M, alpha, dT = 5, 1e-3, 1.0 / N
+    off = rng.uniform(0.1, 1.0, (M, nx)) * 50.0  # A = tridiag(-off, dia, -off), SPD, stiff like the FD operator
+    off[:, -1] = 0.0
+    dia = rng.uniform(0.5, 1.5, (M, nx)) + off + np.concatenate([np.zeros((M, 1)), off[:, :-1]], axis=1)
+    op = DeviceOperator(to_dev(dia), to_dev(-off), 0.0, to_dev(np.zeros(nx)))
+    spec = build_alpha_circulant(N, alpha)
+    tables = AlphaTables(spec)
+    r = to_dev(rng.normal(size=(M, N, nx)))
+    u_row, _ = three_step_device(op, tables, N, dT, r, diagnostics=False)
+    monkeypatch.setenv("KLE_CGC_ROW", "0")
+    u_cl, _ = three_step_device(op, tables, N, dT, r, diagnostics=False)
+    monkeypatch.delenv("KLE_CGC_ROW")
+    scale = float(u_cl.abs().max())
+    assert float((u_row - u_cl).abs().max()) <= 1e-12 * scale
+    if N * nx <= 1024:
+        for s in range(M):
+            A = np.diag(dia[s]) - np.diag(off[s, :-1], 1) - np.diag(off[s, :-1], -1)
+            Mx = np.kron(spec.dense_matrix(), np.eye(nx)) + dT * np.kron(np.eye(N), A)
+            expected = np.linalg.solve(Mx, r[s].cpu().numpy().reshape(-1)).reshape(N, nx)
+            assert rel(u_row[s].cpu().numpy(), expected) <= 1e-9
