@@ -38,7 +38,8 @@ __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c
 __host__ __device__ inline int fine_blob_doubles(int MR, int P) {
   int logp = 0;
   while ((1 << logp) < P) ++logp;
-  return 6 * MR * P + 2 * logp * P;  // l, 1/beta, scan multipliers, lazy-stitch vectors
+  // l, 1/beta, scan multipliers, lazy-stitch vectors; (16, 8): the twisted two-lane tables (kle_fine_tw.cu)
+  return 6 * MR * P + 2 * logp * P + ((MR == 16 && P == 8) ? 256 : 0);
 }
 
 struct Cplx {

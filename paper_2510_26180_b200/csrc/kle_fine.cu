@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
   constexpr int NXP = MR * P;
   const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
+  if constexpr (MR == 16 && P == 8) {  // the twisted kernel took every sample it has tables for
+    if (a.tw_fallback && a.ffac[(size_t)s * L::DOUBLES + kTwFlagOff] == 0.0) return;
+  }
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
   const int nx = a.nx, N = a.N;
@@ -639,8 +642,14 @@ int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* 
                 double h, double g0, cudaStream_t st) {
   if (lay.W) return mw_factor(dia, off, blob, M, nx, h, st);
   if (lay.kind == 1) return sf_factor(lay, dia, off, blob, M, nx, h, g0, st);
-  KLE_FINE_ALL(factor(dia, off, blob, M, nx, h, g0, st))
-  return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: unsupported nx");
+  auto base = [&]() -> int {
+    KLE_FINE_ALL(factor(dia, off, blob, M, nx, h, g0, st))
+    return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: unsupported nx");
+  };
+  if (int rc = base()) return rc;
+  // the twisted two-lane tables (kle_fine_tw.cu) go into the blob's spare part
+  if (tw_supported(lay, nx)) return tw_factor(dia, off, blob, M, nx, h, g0, st);
+  return KLE_OK;
 }
 
 int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
@@ -650,6 +659,12 @@ int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
     lay.kind = 0;  // F given: no sweep, any (MR, P) register variant serves the epilogue
     lay.pipe = 0;
     lay.R = (lay.MR == 16) ? 3 : (lay.P == 32 ? 4 : 2);
+  }
+  if (!a.F_given && !a.F_out && a.Rout && tw_supported(lay, a.nx)) {
+    if (int rc = tw_fgr(a, st)) return rc;
+    FgrArgs b = a;  // samples without a scaled twisted form (flagged by tw_factor): the partitioned kernel
+    b.tw_fallback = 1;
+    KLE_FINE_ALL(fgr(b, st))
   }
   KLE_FINE_ALL(fgr(a, st))
   return set_error(KLE_ERR_UNSUPPORTED, "fgr: unsupported nx");

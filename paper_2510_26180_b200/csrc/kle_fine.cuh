@@ -29,8 +29,10 @@ struct FineLayout {
   static constexpr int PHI2_OFF = PHI_OFF + NXP;          // phi2 = Fwd0(phi)
   static constexpr int SG_OFF = PHI2_OFF + NXP;           // sg_j = prod_{i=j+1}^{MR} (-l_i)
   static constexpr int SG2_OFF = SG_OFF + NXP;            // sg2  = Fwd0(sg)
-  static constexpr int DOUBLES = 6 * NXP + 2 * LOGP * P;
+  // the (16, 8) blob carries the twisted two-lane tables (kle_fine_tw.cu) from PHI_OFF on
+  static constexpr int DOUBLES = 6 * NXP + 2 * LOGP * P + ((MR == 16 && P == 8) ? 256 : 0);
 };
+constexpr int kTwFlagOff = FineLayout<16, 8>::PHI_OFF + 640;  // per-sample "no twisted form" flag (double)
 
 // Per-lane register copy of the factor rows it owns.
 template <int MR, int P>

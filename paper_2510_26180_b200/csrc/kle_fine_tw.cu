@@ -1,0 +1,397 @@
+// Twisted-factorisation fine sweep for small systems (64 < nx <= 128; configs 1 and 4).
+//
+// Reference counterparts: propagate_fine (pintuq/propagators.py:121-145, J x splu.solve) and the
+// right-hand side of cgc_correct (pintuq/pcgc.py:175-197, 233-237), as kle_fine.cu.
+//
+// The partitioned solve of kle_fine.cu pays five FMAs per row and step plus two lane scans, because
+// every chunk has two unknown neighbours. With exactly TWO lanes per system there is no unknown
+// neighbour left: the "burn at both ends" (twisted) factorisation T = N D N^T eliminates from row 0
+// downwards in one lane and from row nx-1 upwards in the other, the two eliminations meet in a 2 x 2
+// system in the middle (one shuffle), and both lanes back-substitute outwards: the sequential Thomas
+// count and no scan. Each lane keeps its H = 64 rows of ONE right-hand side in registers (local order
+// j = 0 at the outer end .. H-1 in the middle; pad rows at the outer end), and the factor rows, which
+// are per sample, come to the 16 lane pairs of a warp (= the N = 16 subintervals of a sample at c4) as
+// broadcasts from shared memory.
+//
+// Shared-memory bandwidth is what such a kernel runs into (a broadcast 16-byte load still costs two
+// wavefronts: measured 4.65 SM-cycles per warp-row with four coefficient doubles per row against 4.0
+// for the partitioned kernel), so the recurrences are rewritten to need only TWO doubles per row:
+//
+//   * the constant source is removed by the steady state: with A x* = g0, e = x - x* obeys the
+//     homogeneous step (I + hA) e_new = e_old;
+//   * a diagonal scaling e_j = t_j w_j with t_j = nl_j t_{j-1} (t = 1 at the first real row) turns the
+//     forward multipliers into 1:
+//
+//       forward   y_j = w_j + y_{j-1}                        (DADD, no coefficient)
+//       middle    w_m = ca y_m + cb' y_m(partner)            (cb' carries the two lanes' t ratio)
+//       backward  w_j = inv_j y_j + nl_{j+1}^2 w_{j+1}       (one 16-byte load {inv_j, nl_{j+1}^2})
+//
+//     Pad rows (inv = k = 0) stay exactly 0. t decays geometrically towards the middle (0.4^63 ~ 1e-25 at
+//     c4); tw_factor_kernel flags a sample whose t leaves [1e-150, 1e150] or whose A has no positive
+//     pivots (no steady state), fgr_tw_kernel skips flagged samples and the partitioned kernel, launched
+//     right after with FgrArgs::tw_fallback, processes exactly those.
+//
+// The tables live behind the (16, 8) factor blob's scan multipliers (FineLayout::PHI_OFF .. DOUBLES), so
+// every other consumer of the blob (sweeps, classical parareal, the fused small-block kernels) keeps its
+// layout.
+#include <cstdlib>
+
+#include "kle_common.cuh"
+namespace kle {
+#define FGR_T(i) \
+  do {           \
+  } while (0)
+}
+#include "kle_fine.cuh"
+#include "kle_internal.h"
+
+#ifndef KLE_FINE_LAZY
+#define KLE_FINE_LAZY 0
+#endif
+#ifndef KLE_TW_MINB
+#define KLE_TW_MINB 8  // CTAs (= warps) per SM the register allocation is bounded for
+#endif
+
+namespace kle {
+
+namespace {
+constexpr int TW_H = 64;  // rows per lane
+// table layout (doubles), side 0 = top lane (rows ascending), side 1 = bottom lane (rows descending):
+//   A [j][side][2]     = {inv_j, k_j = nl_{j+1}^2}   (j = H-1: {ca, cb'})      at (j * 2 + side) * 2
+//   S [j][side][2]     = {x*_j, 1 / t_j}             (prologue)                at 4 H + (j * 2 + side) * 2
+//   T [j/2][side][j&1] = t_j                         (epilogue)                at 8 H + ((j/2) * 2 + side) * 2 + (j & 1)
+//   flag                                                                       at 10 H (kTwFlagOff - PHI_OFF)
+// so that a warp's 16-byte load touches 32 contiguous bytes (even lanes one half, odd lanes the other).
+constexpr int TW_DOUBLES = 10 * TW_H + 2;
+__host__ __device__ constexpr int twA(int j, int side) { return (j * 2 + side) * 2; }
+__host__ __device__ constexpr int twS(int j, int side) { return 4 * TW_H + (j * 2 + side) * 2; }
+__host__ __device__ constexpr int twT(int j, int side) { return 8 * TW_H + ((j >> 1) * 2 + side) * 2 + (j & 1); }
+constexpr int TW_FLAG = 10 * TW_H;
+
+using TwL = FineLayout<16, 8>;
+static_assert(TwL::DOUBLES - TwL::PHI_OFF >= TW_DOUBLES, "the twisted tables must fit the blob's spare part");
+static_assert((TwL::PHI_OFF % 2) == 0 && (TwL::DOUBLES % 2) == 0, "16-byte aligned tables");
+static_assert(kTwFlagOff == TwL::PHI_OFF + TW_FLAG, "flag offset shared with kle_fine.cu");
+
+__device__ __forceinline__ double2 lds_v2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cp_async8(unsigned sa, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(unsigned sa, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Tables: one warp per sample; lane 0 eliminates downwards, lane 1 upwards, lane 2 solves A x* = g0.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
+                                                       double* __restrict__ blob, int M, int nx, double h, double g0) {
+  __shared__ __align__(16) double tab[TW_DOUBLES];
+  __shared__ double dd[128], ee[128], xs[128], cw[128];
+  const int s = blockIdx.x, lane = threadIdx.x;
+  if (s >= M) return;
+  for (int i = lane; i < 128; i += 32) {
+    dd[i] = i < nx ? dia[(size_t)s * nx + i] : 0.0;
+    ee[i] = i + 1 < nx ? off[(size_t)s * nx + i] : 0.0;  // ee[i] couples rows i, i+1
+    xs[i] = 0.0;
+  }
+  __syncwarp();
+  const int mT = nx - nx / 2, mB = nx / 2;
+  double beta_last = 1.0, t_last = 1.0;
+  bool bad = false;
+  if (lane < 2) {
+    const int side = lane;
+    const int pad = TW_H - (side ? mB : mT);
+    double beta_prev = 1.0, t = 1.0, inv_prev = 0.0;
+    for (int j = 0; j < TW_H; ++j) {
+      double nl = 0.0, inv = 0.0;
+      if (j >= pad) {
+        const int row = side ? nx - 1 - (j - pad) : j - pad;
+        const double D = fma(h, dd[row], 1.0);
+        double beta = D;
+        if (j > pad) {
+          const double E = h * (side ? ee[row] : ee[row - 1]);  // coupling to the previously eliminated row
+          const double l = E / beta_prev;
+          beta = fma(-l, E, D);
+          nl = -l;
+          t *= nl;  // t_j = nl_j t_{j-1}
+        }
+        inv = 1.0 / beta;
+        beta_prev = beta;
+        bad |= !(fabs(t) >= 1e-150 && fabs(t) <= 1e150) || !(beta > 0.0);
+      }
+      // row j-1's backward coefficient is nl_j^2 (its own inv was known one trip ago)
+      if (j > 0) {
+        tab[twA(j - 1, side)] = inv_prev;
+        tab[twA(j - 1, side) + 1] = nl * nl;
+      }
+      inv_prev = inv;
+      tab[twS(j, side) + 1] = (j >= pad) ? 1.0 / t : 0.0;
+      tab[twT(j, side)] = (j >= pad) ? t : 0.0;
+    }
+    beta_last = beta_prev;
+    t_last = t;
+  } else if (lane == 2 && g0 != 0.0) {  // steady state A x* = g0 (Thomas; A must have positive pivots)
+    double bp = dd[0];
+    bad |= !(bp > 0.0);
+    cw[0] = ee[0] / bp;
+    xs[0] = g0 / bp;
+    for (int i = 1; i < nx; ++i) {
+      const double e = ee[i - 1];
+      const double b = fma(-e, cw[i - 1], dd[i]);
+      bad |= !(b > 0.0);
+      cw[i] = ee[i] / b;
+      xs[i] = fma(-e, xs[i - 1], g0) / b;
+      bp = b;
+    }
+    for (int i = nx - 2; i >= 0; --i) xs[i] = fma(-cw[i], xs[i + 1], xs[i]);
+    for (int i = 0; i < nx; ++i) bad |= !(fabs(xs[i]) <= 1e150);
+  }
+  __syncwarp();
+  // the 2 x 2 middle system [bT E; E bB] (e_p, e_q) = (yT, yB) in the scaled variables of the two lanes
+  const double bT = __shfl_sync(KLE_FULL_MASK, beta_last, 0);
+  const double bB = __shfl_sync(KLE_FULL_MASK, beta_last, 1);
+  const double tT = __shfl_sync(KLE_FULL_MASK, t_last, 0);
+  const double tB = __shfl_sync(KLE_FULL_MASK, t_last, 1);
+  if (lane < 2) {
+    const int side = lane, pad = TW_H - (side ? mB : mT);
+    const double E = h * ee[mT - 1];
+    const double idet = 1.0 / fma(bT, bB, -E * E);
+    tab[twA(TW_H - 1, side)] = (side ? bT : bB) * idet;                           // ca: own y
+    tab[twA(TW_H - 1, side) + 1] = -E * idet * (side ? tT / tB : tB / tT);        // cb': partner's y
+    bad |= !(fabs(idet) <= 1e150);
+    for (int j = 0; j < TW_H; ++j)
+      tab[twS(j, side)] = (j >= pad) ? xs[side ? nx - 1 - (j - pad) : j - pad] : 0.0;
+  }
+  const bool any_bad = __any_sync(KLE_FULL_MASK, bad);
+  if (lane == 0) {
+    tab[TW_FLAG] = any_bad ? 1.0 : 0.0;
+    tab[TW_FLAG + 1] = 0.0;
+  }
+  __syncwarp();
+  double* out = blob + (size_t)s * TwL::DOUBLES + TwL::PHI_OFF;
+  for (int i = lane; i < TW_DOUBLES; i += 32) out[i] = tab[i];
+}
+
+// ---------------------------------------------------------------------------
+// Fused F + rhs kernel: CTA = one warp = (sample, 16 subintervals); lane = 2 q + side.
+//
+// Shared memory, all in the lanes' LOCAL order (position side * H + j holds the row that lane `side`
+// keeps in x[j]), so every per-row access of the unrolled loops is a load at an immediate offset:
+//   tab [10 H + 2]      the twisted tables (above)
+//   de  [H][2][2]       {dia, coupling of local rows j-1 and j} of the operator A (epilogue)
+//   st  [17][LD]        start rows of the 16 subintervals (= prev rows of the rhs for n >= 1; the rhs rows
+//                       replace them and the warp stores them coalesced), row 16: U_{N-1} (prev of n = 0)
+// LD = 2 H + 1: the 16 lane pairs' rows fall into distinct banks.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int TW_LD = 2 * TW_H + 1;
+constexpr int TW_SMEM_DOUBLES = TW_DOUBLES + 4 * TW_H + 17 * TW_LD + 1;
+static_assert(TW_DOUBLES % 2 == 0, "16-byte copies");
+}
+
+__global__ void __launch_bounds__(32, KLE_TW_MINB) fgr_tw_kernel(FgrArgs a) {
+  constexpr int H = TW_H, LD = TW_LD;
+  const int s = blockIdx.x;
+  if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
+  const int lane = threadIdx.x, q = lane >> 1, side = lane & 1;
+  const int nx = a.nx, N = a.N;
+  const size_t sbase = (size_t)s * N * nx;
+  const int n0 = blockIdx.y * 16;
+  const int n = n0 + q;
+  const bool valid = n < N;
+  const int mT = nx - nx / 2;
+  const int padT = H - mT, padB = H - nx / 2;
+  const int pad = side ? padB : padT;
+
+  extern __shared__ __align__(16) double sm[];
+  double* tab = sm;                  // [TW_DOUBLES]
+  double* de = sm + TW_DOUBLES;      // [H][2][2]
+  double* st = de + 4 * H;           // [17][LD]
+  const unsigned tab_s = (unsigned)__cvta_generic_to_shared(tab);
+  const unsigned de_s = (unsigned)__cvta_generic_to_shared(de);
+  const unsigned st_s = (unsigned)__cvta_generic_to_shared(st);
+
+  {  // tables (16-byte copies), then the start rows and the operator (coalesced 8-byte copies)
+    const double* tg = a.ffac + (size_t)s * TwL::DOUBLES + TwL::PHI_OFF;
+#pragma unroll
+    for (int i = 0; i < (TW_DOUBLES / 2 + 31) / 32; ++i)
+      if (lane + 32 * i < TW_DOUBLES / 2) cp_async16(tab_s + (unsigned)((lane + 32 * i) * 16), tg + (lane + 32 * i) * 2);
+    bool rv[4];
+    unsigned lo[4];  // byte offset of row lane + 32 i in the local order
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = lane + 32 * i;
+      rv[i] = r < nx;
+      lo[i] = (unsigned)((r < mT ? r + padT : H + (nx - 1 - r) + padB) * sizeof(double));
+    }
+    for (int ln = 0; ln < 16; ++ln) {
+      const int nn = n0 + ln;
+      if (nn >= N) break;
+      const double* src = ((nn == 0) ? a.u0 : a.U + sbase + (size_t)(nn - 1) * nx) + lane;
+      const unsigned dst = st_s + (unsigned)(ln * LD * sizeof(double));
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (rv[i]) cp_async8(dst + lo[i], src + i * 32);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);  // group 1: what the sweep needs
+    const double* pl = a.U + sbase + (size_t)(N - 1) * nx + lane;
+    const double* dg = a.dia + (size_t)s * nx + lane;
+    const double* eg = a.off + (size_t)s * nx + lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = lane + 32 * i;
+      if (!rv[i]) continue;
+      if (n0 == 0) cp_async8(st_s + (unsigned)(16 * LD * sizeof(double)) + lo[i], pl + i * 32);
+      // de entry of local position p = side * H + j sits at ((j * 2 + side) * 2) doubles
+      const int p = (int)(lo[i] / sizeof(double));
+      const int sd = p >= H, j = p - sd * H;
+      const unsigned e = de_s + (unsigned)(((j * 2 + sd) * 2) * sizeof(double));
+      cp_async8(e, dg + i * 32);
+      // coupling to the previously eliminated (outer) row: off[r-1] in the top half, off[r] in the bottom half
+      if (sd ? (r + 1 < nx) : (r > 0)) cp_async8(e + 8, eg + i * 32 - (sd ? 0 : 1));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);  // group 2: epilogue operands
+    // entries no copy writes: the pad rows of this lane's start row (all of it for an unused lane pair),
+    // the pad entries of de and the outer coupling of the two end rows
+    const int nz = valid ? pad : H;
+    for (int j = 0; j < nz; ++j) st[q * LD + side * H + j] = 0.0;
+    if (q == 0) {
+      for (int j = 0; j <= pad; ++j) {
+        if (j < pad) de[(j * 2 + side) * 2] = 0.0;
+        de[(j * 2 + side) * 2 + 1] = 0.0;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 1;\n" ::);
+  __syncwarp();
+  if (tab[TW_FLAG] != 0.0) {  // no scaled form for this sample: the partitioned kernel takes it (tw_fallback)
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    return;
+  }
+
+  // w_j = (x_j - x*_j) / t_j
+  double x[H];
+  const unsigned xs = st_s + (unsigned)((q * LD + side * H) * sizeof(double));
+  const unsigned tS = tab_s + (unsigned)((4 * H) * sizeof(double) + side * 16);
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    const double2 sj = lds_v2(tS + (unsigned)(j * 32));
+    x[j] = (lds_f64(xs + (unsigned)(j * sizeof(double))) - sj.x) * sj.y;
+  }
+  const unsigned tA = tab_s + (unsigned)(side * 16);
+  const double2 cm = lds_v2(tA + (unsigned)((H - 1) * 32));  // {ca, cb'}
+
+#pragma unroll 1
+  for (int it = 0; it < a.J; ++it) {
+    double y = x[0];
+#pragma unroll
+    for (int j = 1; j < H; ++j) {
+      y += x[j];
+      x[j] = y;
+    }
+    const double yp = __shfl_xor_sync(KLE_FULL_MASK, y, 1);
+    double xn = fma(cm.x, y, cm.y * yp);
+    x[H - 1] = xn;
+#pragma unroll
+    for (int j = H - 2; j >= 0; --j) {
+      const double2 c = lds_v2(tA + (unsigned)(j * 32));  // {inv_j, nl_{j+1}^2}
+      xn = fma(c.y, xn, x[j] * c.x);
+      x[j] = xn;
+    }
+  }
+  {  // F_j = t_j w_j + x*_j
+    const unsigned tT = tab_s + (unsigned)((8 * H + side * 2) * sizeof(double));
+#pragma unroll
+    for (int jp = 0; jp < H / 2; ++jp) {
+      const double2 t2 = lds_v2(tT + (unsigned)(jp * 32));
+      const double2 s0 = lds_v2(tS + (unsigned)((2 * jp) * 32));
+      const double2 s1 = lds_v2(tS + (unsigned)((2 * jp + 1) * 32));
+      x[2 * jp] = fma(t2.x, x[2 * jp], s0.x);
+      x[2 * jp + 1] = fma(t2.y, x[2 * jp + 1], s1.x);
+    }
+  }
+
+  // epilogue: rhs_n = scaling_n ((I + dT A) F_n - prev_n). In local order the neighbours of row j are
+  // x[j-1] (outer; its coupling is 0 for the first real row) and x[j+1] (inner; the partner's middle
+  // row for j = H-1). Pad rows compute finite values nobody reads.
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncwarp();
+  const double xmid = __shfl_xor_sync(KLE_FULL_MASK, x[H - 1], 1);
+  const double sc = valid ? a.scaling[n] : 0.0;
+  const double pmul = (n == 0) ? a.alpha : 1.0;
+  const double emid = __ldg(a.off + (size_t)s * nx + mT - 1);  // couples the two middle rows
+  const unsigned ps = (n == 0) ? st_s + (unsigned)((16 * LD + side * H) * sizeof(double)) : xs;
+  const unsigned des = de_s + (unsigned)(side * 16);
+  double xo = 0.0;
+  double2 d0 = lds_v2(des);
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    double2 d1;
+    if (j < H - 1) d1 = lds_v2(des + (unsigned)((j + 1) * 32));
+    const double ei = (j < H - 1) ? d1.y : emid;
+    const double xc = x[j];
+    const double xi = (j < H - 1) ? x[j + 1] : xmid;
+    const double prev = lds_f64(ps + (unsigned)(j * sizeof(double)));
+    const double Ax = fma(d0.y, xo, fma(d0.x, xc, ei * xi));
+    const double rhs = fma(a.dT, Ax, xc) - pmul * prev;
+    xo = xc;
+    x[j] = sc * rhs;
+    if (j < H - 1) d0 = d1;
+  }
+  __syncwarp();  // every prev row (row 16 is shared by nobody else, but keep the reads before the writes)
+#pragma unroll
+  for (int j = 0; j < H; ++j) asm volatile("st.shared.f64 [%0], %1;" ::"r"(xs + (unsigned)(j * sizeof(double))), "d"(x[j]) : "memory");
+  __syncwarp();
+  for (int ln = 0; ln < 16; ++ln) {
+    const int nn = n0 + ln;
+    if (nn >= N) break;
+    double* out = a.Rout + sbase + (size_t)nn * nx + lane;
+    const double* rs = st + ln * LD;
+    double v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = (lane + 32 * i < nx) ? lane + 32 * i : 0;
+      v[i] = rs[r < mT ? r + padT : H + (nx - 1 - r) + padB];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < nx) out[32 * i] = v[i];
+  }
+}
+
+bool tw_supported(const FineLayoutRT& lay, int nx) {
+  if (KLE_FINE_LAZY) return false;
+  if (lay.W || lay.kind || lay.MR != 16 || lay.P != 8) return false;
+  if (nx <= TW_H || nx > 2 * TW_H) return false;
+  const char* e = getenv("KLE_FGR_TW");  // read per call (A/B in one process)
+  return !(e && *e == '0');
+}
+
+
+int tw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, double g0,
+              cudaStream_t st) {
+  if (M > 0) tw_factor_kernel<<<(unsigned)M, 32, 0, st>>>(dia, off, blob, M, nx, h, g0);
+  return check_launch("tw_factor_kernel");
+}
+
+int tw_fgr(const FgrArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)TW_SMEM_DOUBLES;
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_fine_tw: cudaFuncSetAttribute", [&] {
+        cudaError_t e = cudaFuncSetAttribute(fgr_tw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        if (e != cudaSuccess) return e;
+        return cudaFuncSetAttribute(fgr_tw_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      }))
+    return rc;
+  dim3 grid(a.M, (a.N + 15) / 16);
+  fgr_tw_kernel<<<grid, 32, smem, st>>>(a);
+  return check_launch("fgr_tw_kernel");
+}
+
+}  // namespace kle

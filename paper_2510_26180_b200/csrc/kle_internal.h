@@ -67,6 +67,7 @@ struct FgrArgs {
   const int32_t* active;  // [M] sample status (0 = active) or null
   int M, N, nx, J;
   double dt, dT, g0, alpha;
+  int tw_fallback = 0;    // 1: only the samples flagged by tw_factor (kle_fine_tw.cu); (16, 8) layout
 };
 
 struct PararealArgs {
@@ -125,6 +126,11 @@ int sf_factor(FineLayoutRT lay, const double* dia, const double* off, double* bl
               double g0, cudaStream_t st);
 int sf_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st);
 int sf_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st);
+// twisted two-lane sweep for 64 < nx <= 128 (kle_fine_tw.cu); tables in the (16, 8) blob's spare part
+bool tw_supported(const FineLayoutRT& lay, int nx);
+int tw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, double g0,
+              cudaStream_t st);
+int tw_fgr(const FgrArgs& a, cudaStream_t st);
 int mw_warps(int nx);
 int mw_blob_doubles(int nx);
 int mw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, cudaStream_t st);

@@ -614,3 +614,51 @@ def test_row_fft_cgc_matches_cluster_kernel_and_dense(cuda, N, nx, monkeypatch):
             Mx = np.kron(spec.dense_matrix(), np.eye(nx)) + dT * np.kron(np.eye(N), A)
             expected = np.linalg.solve(Mx, r[s].cpu().numpy().reshape(-1)).reshape(N, nx)
             assert rel(u_row[s].cpu().numpy(), expected) <= 1e-9
+
+
+@pytest.mark.parametrize("N,nx,J", [(16, 127, 32), (16, 128, 5), (3, 65, 2), (8, 100, 7), (20, 96, 4), (33, 127, 2)])
+def test_twisted_fine_sweep_matches_partitioned_and_dense(cuda, N, nx, J, monkeypatch):
+    """The two-lane twisted-factorisation sweep (kle_fine_tw.cu; default for
+    64 < nx <= 128) against the partitioned register kernel (KLE_FGR_TW=0) and a
+    dense evaluation of scaling_n ((I + dT A) F_n - prev_n), F_n = J backward-Euler
+    steps with a constant source (pintuq/propagators.py:121-145, pcgc.py:175-197),
+    over ragged nx, N not a multiple of 16 and samples masked by the status word."""
+    import torch
+
+    from paper_2510_26180_b200 import make_time_grid
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, empty, to_dev
+    from paper_2510_26180_b200.pcgc import _fgr, build_alpha_circulant
+
+    rng = np.random.default_rng(7000 * N + nx)
+    M, alpha, g0 = 6, 1e-3, 0.7
+    grid = make_time_grid(1.0, N, J)
+    off = rng.uniform(0.1, 1.0, (M, nx)) * 400.0
+    off[:, -1] = 0.0
+    dia = rng.uniform(0.5, 1.5, (M, nx)) + off + np.concatenate([np.zeros((M, 1)), off[:, :-1]], axis=1)
+    u0 = rng.normal(size=nx)
+    op = DeviceOperator(to_dev(dia), to_dev(-off), g0, to_dev(u0))
+    tables = AlphaTables(build_alpha_circulant(N, alpha))
+    U = to_dev(rng.normal(size=(M, N, nx)))
+    status = torch.zeros(M, dtype=torch.int32, device="cuda")
+    status[4] = 1  # a converged sample: its rhs rows must stay untouched
+    R_tw = torch.full((M, N, nx), 123.0, dtype=torch.float64, device="cuda")
+    R_pt = R_tw.clone()
+    _fgr(op, tables, U, R_tw, J, grid, alpha, status=status)
+    monkeypatch.setenv("KLE_FGR_TW", "0")
+    _fgr(op, tables, U, R_pt, J, grid, alpha, status=status)
+    monkeypatch.delenv("KLE_FGR_TW")
+    assert float((R_tw[4] - 123.0).abs().max()) == 0.0
+    scale = float(R_pt.abs().max())
+    assert float((R_tw - R_pt).abs().max()) <= 1e-12 * scale
+    sc = tables.scaling.cpu().numpy()
+    Uh = U.cpu().numpy()
+    for s in (0, 5):
+        A = np.diag(dia[s]) - np.diag(off[s, :-1], 1) - np.diag(off[s, :-1], -1)
+        T = np.eye(nx) + grid.deltat * A
+        for n in range(N):
+            x = u0 if n == 0 else Uh[s, n - 1]
+            for _ in range(J):
+                x = np.linalg.solve(T, x + grid.deltat * g0)
+            prev = alpha * Uh[s, N - 1] if n == 0 else Uh[s, n - 1]
+            want = sc[n] * (x + grid.deltaT * (A @ x) - prev)
+            assert rel(R_tw[s, n].cpu().numpy(), want) <= 1e-10
