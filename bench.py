@@ -380,8 +380,11 @@ def run_b200(args):
     # sample pipeline (two when the batch is large, kle_capi.cu) one fgr and one CGC launch (an upper bound:
     # a pipeline stops as soon as its own samples have converged), and 2 x (2 col-sum + 1 scale) for the moments
     pipes = 2 if (M >= 8192 and os.environ.get("KLE_PCGC_PIPES", "2") != "1") else 1
+    # the twisted two-lane fine sweep (kle_fine_tw.cu, 64 < nx <= 128) adds its table kernel and, per sweep,
+    # the launch of the partitioned kernel that takes the samples flagged as having no scaled form (none here)
+    tw_path = 64 < c["nx"] <= 128 and os.environ.get("KLE_FGR_TW", "1") != "0"
     launches_per_step = (1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 1
-                         + 2 * pipes * int(kmax) + 6)
+                         + 2 * pipes * int(kmax) + 6 + ((1 + pipes * int(kmax)) if tw_path else 0))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_all[:n_sub])
@@ -416,17 +419,19 @@ def run_b200(args):
             "surrogate": {"m_q": sur.m_q, "P": solver.surrogate.P, "K_g": K_g, "mode": solver.surrogate.mode,
                           "built_on": "rank 0 (device snapshots), broadcast"},
             "roofline": {
-                "kernel": "fgr_kernel (fused J-step fine sweep + CGC rhs)",
+                "kernel": ("fgr_tw_kernel (twisted two-lane J-step fine sweep + CGC rhs)" if tw_path
+                           else "fgr_kernel (fused J-step fine sweep + CGC rhs)"),
                 "bound": "fp64",
                 "achieved": fgr_tflops,
                 "peak": fp64_peak,
                 "unit": "TFLOP/s",
                 "frac": (fgr_tflops / fp64_peak) if fp64_peak else None,
-                "traffic": traffic_of(peaks, args.config, "fgr_kernel", M),
+                "traffic": traffic_of(peaks, args.config, "fgr_tw_kernel" if tw_path else "fgr_kernel", M),
                 "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per sample-iteration "
                                   "(profiles/traffic.json) x samples per launch",
                 "peak_source": peaks.get("fp64_source"),
                 "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch (M = rank shard)",
+                "executed_flop_per_dof_update": 4 if tw_path else 10,
                 "hbm_frac": (fgr_bytes / (fgr_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
                 "ms_per_launch": fgr_ms,
             },

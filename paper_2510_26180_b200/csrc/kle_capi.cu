@@ -79,7 +79,7 @@ AuxResources* aux_resources() {
   ok = ok && cudaEventCreateWithFlags(&r->ready, cudaEventDisableTiming) == cudaSuccess;
   for (int q = 0; q < 2 && ok; ++q) ok = cudaStreamCreateWithFlags(&r->cgcl[q], cudaStreamNonBlocking) == cudaSuccess;
   for (int q = 0; q < 3 && ok; ++q) ok = cudaEventCreateWithFlags(&r->cgcl_ev[q], cudaEventDisableTiming) == cudaSuccess;
-  ok = ok && cudaHostAlloc(&r->h_count, kMaxPipes * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
+  ok = ok && cudaHostAlloc(&r->h_count, (kMaxPipes + 1) * sizeof(int32_t), cudaHostAllocDefault) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     aux_destroy(r);
@@ -373,6 +373,17 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
   AuxResources* res = aux_resources();
   if (!res) return KLE_ERR_CUDA;
   int32_t* h_count = res->h_count;
+  // twisted fine sweep (kle_fine_tw.cu): count the samples its table kernel flagged as having no scaled
+  // form, so that the partitioned kernel is launched after each sweep only when there are any (one
+  // stream synchronisation per solve instead of an empty 1M-CTA launch per sweep)
+  int tw_none_flagged = 0;
+  if (!fused && tw_supported(lay, nx)) {
+    cudaMemsetAsync(counter + 8, 0, sizeof(int32_t), st);
+    KLE_TRY(tw_count_flagged(fine_blob, M, counter + 8, st));
+    cudaMemcpyAsync(&h_count[kMaxPipes], counter + 8, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return set_error(KLE_ERR_CUDA, "pcgc_solve: flag count");
+    tw_none_flagged = h_count[kMaxPipes] == 0;
+  }
   cudaEvent_t ready = res->ready;
   cudaEventRecord(ready, st);
   for (int p = 0; p < pipes; ++p) {
@@ -410,8 +421,12 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
         cudaStreamWaitEvent(q.sc, q.fdone, 0);
       }
     } else {
-    KLE_TRY(kle_fgr_f64(Uq, u0, nullptr, nullptr, R + o * N * nx, fine_blob + o * lay.doubles, dq, eq, scaling, sq,
-                        q.M, N, nx, J, dt, dT, g0, alpha, q.st));
+    {
+      FgrArgs fa{Uq, u0, nullptr, nullptr, R + o * N * nx, fine_blob + o * lay.doubles, dq, eq, scaling, sq,
+                 q.M, N, nx, J, dt, dT, g0, alpha};
+      fa.tw_none_flagged = tw_none_flagged;
+      KLE_TRY(fine_fgr(lay, fa, q.st));
+    }
     if (q.sc != q.st) {
       cudaEventRecord(q.fdone, q.st);
       cudaStreamWaitEvent(q.sc, q.fdone, 0);

@@ -65,31 +65,45 @@ namespace kle {
 
 
 // ---------------------------------------------------------------------------
-// Factor kernel: one WARP per sample (round 2; it was one thread per sample with
-// every global access uncoalesced): the operator rows are loaded coalesced into
-// shared memory, lane 0 runs the sequential LDL^T of T = I + h A, the lanes build
-// the chunk / scan tables of the partitioned solve (layout: kle_common.cuh)
-// with the same operations in the same order as before (bit-identical blob),
-// and the warp stores the blob coalesced.
+// Factor kernel: one warp builds the blobs of 32 / P samples, P lanes per sample (c4: four samples; with
+// one sample per warp the kernel, a 128-step division chain in a single lane, took 8.7 ms per 1M samples):
+// the operator rows are loaded coalesced into shared memory, lane 0 of each group runs the sequential
+// LDL^T of T = I + h A, the group's lanes build the chunk / scan tables of the partitioned solve (layout:
+// kle_common.cuh) with the same operations in the same order as the one-thread-per-sample original
+// (bit-identical blob), and the warp stores the blobs coalesced.
 // ---------------------------------------------------------------------------
+template <int MR, int P>
+struct FactorSmem {
+  using L = FineLayout<MR, P>;
+  static constexpr int SPW = 32 / P;                                  // samples per warp
+  static constexpr int BS = KLE_FINE_LAZY ? L::DOUBLES : L::PHI_OFF;  // staged (= stored) blob doubles
+  static constexpr int PER = BS + 2 * L::NXP;                         // + the operator rows
+  static constexpr size_t bytes = sizeof(double) * (size_t)SPW * PER;
+};
+
 template <int MR, int P>
 __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restrict__ dia,
                                                          const double* __restrict__ off, double* __restrict__ blob,
                                                          int M, int nx, double h, double g0) {
   using L = FineLayout<MR, P>;
+  using FS = FactorSmem<MR, P>;
   constexpr int NXP = L::NXP;
   extern __shared__ __align__(16) double fsm[];
-  double* b = fsm;                  // [DOUBLES] the sample's blob
-  double* dd = fsm + L::DOUBLES;    // [NXP]
+  const int lane = threadIdx.x, grp = lane / P, k = lane % P;
+  const int s0 = blockIdx.x * FS::SPW;
+  double* b = fsm + grp * FS::PER;  // [BS] the sample's blob
+  double* dd = b + FS::BS;          // [NXP]
   double* ee = dd + NXP;            // [NXP]: ee[i] couples rows i, i+1
-  const int s = blockIdx.x, lane = threadIdx.x;
-  if (s >= M) return;
-  for (int i = lane; i < NXP; i += 32) {
-    dd[i] = i < nx ? dia[(size_t)s * nx + i] : 0.0;
-    ee[i] = i < nx ? off[(size_t)s * nx + i] : 0.0;
+  for (int q = 0; q < FS::SPW; ++q) {
+    const int sq = s0 + q;
+    double* dq = fsm + q * FS::PER + FS::BS;
+    for (int i = lane; i < NXP; i += 32) {
+      dq[i] = (sq < M && i < nx) ? dia[(size_t)sq * nx + i] : 0.0;
+      dq[NXP + i] = (sq < M && i < nx) ? off[(size_t)sq * nx + i] : 0.0;
+    }
   }
   __syncwarp();
-  if (lane == 0) {  // LDL^T of I + hA: l_r (row r couples to r-1), inv_r = 1/beta_r; pad rows identity
+  if (k == 0) {  // LDL^T of I + hA: l_r (row r couples to r-1), inv_r = 1/beta_r; pad rows identity
     double beta_prev = 1.0;
     for (int row = 0; row < NXP; ++row) {
       double l = 0.0, inv = 1.0;
@@ -112,18 +126,19 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
   // chunk products: pie_k = prod_j (-l_j) over chunk k, sigs_k = prod_j (-l_{j+1}); staged in dd / ee
   double* pie = dd;
   double* sigs = ee;
-  for (int k = lane; k < P; k += 32) {
+  {
     double pi = 1.0, sg = 1.0;
     for (int j = 0; j < MR; ++j) pi *= -b[L::L_OFF + k * MR + j];
     for (int j = MR - 1; j >= 0; --j) {
       const int row = k * MR + j;
       sg *= -((row + 1 < NXP) ? b[L::L_OFF + row + 1] : 0.0);
     }
+    __syncwarp();  // every lane has read what it needs of dd / ee
     pie[k] = pi;
     sigs[k] = sg;
   }
   __syncwarp();
-  for (int k = lane; k < P; k += 32) {
+  {
     for (int t = 0; t < L::LOGP; ++t) {
       const int d = 1 << t;
       double af = 0.0, bb = 0.0;
@@ -140,42 +155,47 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
     }
     // lazy-stitch vectors of chunk k: read only by be_steps_lazy (KLE_FINE_LAZY=1 builds), so neither
     // computed nor stored otherwise (they are two thirds of the blob)
-    if (!KLE_FINE_LAZY) continue;
-    const double* l = b + L::L_OFF + k * MR;
-    const double* inv = b + L::INV_OFF + k * MR;
-    double* phi = b + L::PHI_OFF + k * MR;
-    double* phi2 = b + L::PHI2_OFF + k * MR;
-    double* sg = b + L::SG_OFF + k * MR;
-    double* sg2 = b + L::SG2_OFF + k * MR;
-    const double lnx = (k + 1 < P) ? b[L::L_OFF + (k + 1) * MR] : 0.0;
-    double pi = 1.0;
-    for (int j = 0; j < MR; ++j) {
-      pi *= -l[j];
-      phi[j] = pi * inv[j];
-    }
-    for (int j = MR - 2; j >= 0; --j) phi[j] = fma(-l[j + 1], phi[j + 1], phi[j]);
-    double g = 1.0;
-    for (int j = MR - 1; j >= 0; --j) {
-      g *= -((j + 1 < MR) ? l[j + 1] : lnx);
-      sg[j] = g;
-    }
-    phi2[0] = phi[0];
-    sg2[0] = sg[0];
-    for (int j = 1; j < MR; ++j) {
-      phi2[j] = fma(-l[j], phi2[j - 1], phi[j]);
-      sg2[j] = fma(-l[j], sg2[j - 1], sg[j]);
+    if (KLE_FINE_LAZY) {
+      const double* l = b + L::L_OFF + k * MR;
+      const double* inv = b + L::INV_OFF + k * MR;
+      double* phi = b + L::PHI_OFF + k * MR;
+      double* phi2 = b + L::PHI2_OFF + k * MR;
+      double* sg = b + L::SG_OFF + k * MR;
+      double* sg2 = b + L::SG2_OFF + k * MR;
+      const double lnx = (k + 1 < P) ? b[L::L_OFF + (k + 1) * MR] : 0.0;
+      double pi = 1.0;
+      for (int j = 0; j < MR; ++j) {
+        pi *= -l[j];
+        phi[j] = pi * inv[j];
+      }
+      for (int j = MR - 2; j >= 0; --j) phi[j] = fma(-l[j + 1], phi[j + 1], phi[j]);
+      double g = 1.0;
+      for (int j = MR - 1; j >= 0; --j) {
+        g *= -((j + 1 < MR) ? l[j + 1] : lnx);
+        sg[j] = g;
+      }
+      phi2[0] = phi[0];
+      sg2[0] = sg[0];
+      for (int j = 1; j < MR; ++j) {
+        phi2[j] = fma(-l[j], phi2[j - 1], phi[j]);
+        sg2[j] = fma(-l[j], sg2[j - 1], sg[j]);
+      }
     }
   }
   __syncwarp();
-  double* out = blob + (size_t)s * L::DOUBLES;
-  const int nstore = KLE_FINE_LAZY ? L::DOUBLES : L::PHI_OFF;  // l, 1/beta and the scan multipliers
-  for (int i = lane; i < nstore; i += 32) out[i] = b[i];
+  for (int q = 0; q < FS::SPW; ++q) {
+    const int sq = s0 + q;
+    if (sq >= M) break;
+    double* out = blob + (size_t)sq * L::DOUBLES;
+    const double* bq = fsm + q * FS::PER;
+    for (int i = lane; i < FS::BS; i += 32) out[i] = bq[i];  // l, 1/beta and the scan multipliers (+ lazy vectors)
+  }
   (void)g0;
 }
 
 template <int MR, int P>
 constexpr size_t fine_factor_smem() {
-  return sizeof(double) * ((size_t)FineLayout<MR, P>::DOUBLES + 2 * (size_t)FineLayout<MR, P>::NXP);
+  return FactorSmem<MR, P>::bytes;
 }
 
 // ---------------------------------------------------------------------------
@@ -538,7 +558,8 @@ struct FineInst {
                                       (int)smem);
         }))
       return rc;
-    if (M > 0) fine_factor_kernel<MR, P><<<(unsigned)M, 32, smem, st>>>(dia, off, blob, M, nx, h, g0);
+    constexpr int SPW = FactorSmem<MR, P>::SPW;
+    if (M > 0) fine_factor_kernel<MR, P><<<(unsigned)((M + SPW - 1) / SPW), 32, smem, st>>>(dia, off, blob, M, nx, h, g0);
     return check_launch("fine_factor_kernel");
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {
@@ -662,6 +683,7 @@ int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
   }
   if (!a.F_given && !a.F_out && a.Rout && tw_supported(lay, a.nx)) {
     if (int rc = tw_fgr(a, st)) return rc;
+    if (a.tw_none_flagged) return KLE_OK;
     FgrArgs b = a;  // samples without a scaled twisted form (flagged by tw_factor): the partitioned kernel
     b.tw_fallback = 1;
     KLE_FINE_ALL(fgr(b, st))

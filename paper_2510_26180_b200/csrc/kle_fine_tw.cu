@@ -34,6 +34,7 @@
 // The tables live behind the (16, 8) factor blob's scan multipliers (FineLayout::PHI_OFF .. DOUBLES), so
 // every other consumer of the blob (sweeps, classical parareal, the fused small-block kernels) keeps its
 // layout.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kle_common.cuh"
@@ -50,6 +51,9 @@ namespace kle {
 #endif
 #ifndef KLE_TW_SPLIT
 #define KLE_TW_SPLIT 2  // independent forward chains per lane
+#endif
+#ifndef KLE_TW_NCACHE
+#define KLE_TW_NCACHE 0  // rows whose backward coefficients stay in registers
 #endif
 #ifndef KLE_TW_MINB
 #define KLE_TW_MINB 8  // CTAs (= warps) per SM the register allocation is bounded for
@@ -90,95 +94,130 @@ __device__ __forceinline__ void cp_async16(unsigned sa, const void* gmem) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Tables: one warp per sample; lane 0 eliminates downwards, lane 1 upwards, lane 2 solves A x* = g0.
+// Tables. One warp builds the tables of TW_SPW = 8 samples, four lanes per sample, all running ONE
+// recurrence shape (so the warp does not diverge over the roles):
+//   role 0 / 1: twisted elimination of T = I + hA from the top / bottom end -> inv, nl^2, t;
+//   role 2 / 3: twisted Thomas solve of the steady state A x* = g0 from the top / bottom end.
+// Each lane walks its 64 rows with one division per row (the chain that bounds this kernel: a warp per
+// sample with three active lanes took 18.6 ms per 1M samples, 4% of a config-4 step); the operator rows and
+// the tables go through shared memory, so that every global access of the warp is coalesced, and 1 / t is
+// formed by all lanes after the chains.
 // ---------------------------------------------------------------------------
+namespace {
+constexpr int TW_SPW = 8;
+// per sample: the tables, (y, 1/b) of the steady-state solve, and the operator rows (staged coalesced)
+constexpr int TW_FSM = TW_DOUBLES + 2 * 2 * TW_H + 2 * 2 * TW_H;
+}
+
 __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
                                                        double* __restrict__ blob, int M, int nx, double h, double g0) {
-  __shared__ __align__(16) double tab[TW_DOUBLES];
-  __shared__ double dd[128], ee[128], xs[128], cw[128];
-  const int s = blockIdx.x, lane = threadIdx.x;
-  if (s >= M) return;
-  for (int i = lane; i < 128; i += 32) {
-    dd[i] = i < nx ? dia[(size_t)s * nx + i] : 0.0;
-    ee[i] = i + 1 < nx ? off[(size_t)s * nx + i] : 0.0;  // ee[i] couples rows i, i+1
-    xs[i] = 0.0;
+  constexpr int H = TW_H;
+  extern __shared__ __align__(16) double fsm[];
+  const int lane = threadIdx.x, ls = lane >> 2, role = lane & 3, side = role & 1;
+  const bool steady = role >= 2;
+  const int s = blockIdx.x * TW_SPW + ls;
+  const bool live = s < M;
+  double* tab = fsm + ls * TW_FSM;
+  double* scr = tab + TW_DOUBLES + side * 2 * H;  // [H][2]: y_j, 1 / b_j
+  const double* dd = tab + TW_DOUBLES + 4 * H;    // [2 H]
+  const double* ee = dd + 2 * H;                  // [2 H]: ee[i] couples rows i, i+1
+  for (int q = 0; q < TW_SPW; ++q) {
+    const int sq = blockIdx.x * TW_SPW + q;
+    double* dq = fsm + q * TW_FSM + TW_DOUBLES + 4 * H;
+    for (int i = lane; i < 2 * H; i += 32) {
+      dq[i] = (sq < M && i < nx) ? dia[(size_t)sq * nx + i] : 1.0;
+      dq[2 * H + i] = (sq < M && i + 1 < nx) ? off[(size_t)sq * nx + i] : 0.0;
+    }
   }
   __syncwarp();
   const int mT = nx - nx / 2, mB = nx / 2;
-  double beta_last = 1.0, t_last = 1.0;
+  const int pad = H - (side ? mB : mT);
+  const double hs = steady ? 1.0 : h, one = steady ? 0.0 : 1.0;
+  double ib_prev = 0.0, y_prev = 0.0, t = 1.0, beta = 1.0;
   bool bad = false;
-  if (lane < 2) {
-    const int side = lane;
-    const int pad = TW_H - (side ? mB : mT);
-    double beta_prev = 1.0, t = 1.0, inv_prev = 0.0;
-    for (int j = 0; j < TW_H; ++j) {
-      double nl = 0.0, inv = 0.0;
-      if (j >= pad) {
-        const int row = side ? nx - 1 - (j - pad) : j - pad;
-        const double D = fma(h, dd[row], 1.0);
-        double beta = D;
-        if (j > pad) {
-          const double E = h * (side ? ee[row] : ee[row - 1]);  // coupling to the previously eliminated row
-          const double l = E / beta_prev;
-          beta = fma(-l, E, D);
-          nl = -l;
-          t *= nl;  // t_j = nl_j t_{j-1}
-        }
-        inv = 1.0 / beta;
-        beta_prev = beta;
-        bad |= !(fabs(t) >= 1e-150 && fabs(t) <= 1e150) || !(beta > 0.0);
-      }
-      // row j-1's backward coefficient is nl_j^2 (its own inv was known one trip ago)
-      if (j > 0) {
-        tab[twA(j - 1, side)] = inv_prev;
+  for (int j = 0; j < H; ++j) {
+    double nl = 0.0, ib = 0.0;
+    if (j >= pad) {
+      const int row = side ? nx - 1 - (j - pad) : j - pad;
+      const double D = fma(hs, dd[row], one);
+      const double E = (j > pad) ? hs * ee[side ? row : row - 1] : 0.0;  // coupling to the row before
+      const double l = E * ib_prev;
+      beta = fma(-l, E, D);
+      ib = 1.0 / beta;
+      y_prev = fma(-l, y_prev, g0);
+      nl = -l;
+      if (j > pad) t *= nl;  // t_j = nl_j t_{j-1}
+      bad |= !(beta > 0.0) || (!steady && !(fabs(t) >= 1e-150 && fabs(t) <= 1e150));
+    }
+    if (!steady) {
+      if (j > 0) {  // row j-1: its own inv (known one trip ago) and nl_j^2
+        tab[twA(j - 1, side)] = ib_prev;
         tab[twA(j - 1, side) + 1] = nl * nl;
       }
-      inv_prev = inv;
-      tab[twS(j, side) + 1] = (j >= pad) ? 1.0 / t : 0.0;
       tab[twT(j, side)] = (j >= pad) ? t : 0.0;
+    } else {
+      scr[2 * j] = y_prev;
+      scr[2 * j + 1] = ib;
     }
-    beta_last = beta_prev;
-    t_last = t;
-  } else if (lane == 2 && g0 != 0.0) {  // steady state A x* = g0 (Thomas; A must have positive pivots)
-    double bp = dd[0];
-    bad |= !(bp > 0.0);
-    cw[0] = ee[0] / bp;
-    xs[0] = g0 / bp;
-    for (int i = 1; i < nx; ++i) {
-      const double e = ee[i - 1];
-      const double b = fma(-e, cw[i - 1], dd[i]);
-      bad |= !(b > 0.0);
-      cw[i] = ee[i] / b;
-      xs[i] = fma(-e, xs[i - 1], g0) / b;
-      bp = b;
-    }
-    for (int i = nx - 2; i >= 0; --i) xs[i] = fma(-cw[i], xs[i + 1], xs[i]);
-    for (int i = 0; i < nx; ++i) bad |= !(fabs(xs[i]) <= 1e150);
+    ib_prev = ib;
   }
+  // middle 2 x 2 systems [bT E; E bB] (x_p, x_q) = (yT, yB): of T in the scaled variables (roles 0 / 1),
+  // of A for the steady state (roles 2 / 3)
+  const int base = lane & ~3;
+  const double b_o = __shfl_sync(KLE_FULL_MASK, beta, base + (role ^ 1));  // the partner's last pivot
+  const double t_o = __shfl_sync(KLE_FULL_MASK, t, base + (role ^ 1));
+  const double y_o = __shfl_sync(KLE_FULL_MASK, y_prev, base + (role ^ 1));
+  const double E = hs * ee[mT - 1];
+  const double idet = 1.0 / fma(beta, b_o, -E * E);
+  bad |= !(fabs(idet) <= 1e150);
+  if (!steady) {
+    tab[twA(H - 1, side)] = b_o * idet;                   // ca: own y
+    tab[twA(H - 1, side) + 1] = -E * idet * (t_o / t);    // cb': partner's y
+  } else {
+    // x_mid = (b_o y - E y_o) / det, then outwards x_j = (y_j - e_{j,j+1} x_{j+1}) / b_j
+    double xn = (g0 != 0.0) ? (b_o * y_prev - E * y_o) * idet : 0.0;
+    tab[twS(H - 1, side)] = xn;
+    for (int j = H - 2; j >= 0; --j) {
+      double v = 0.0;
+      if (j >= pad && g0 != 0.0) {
+        const int row = side ? nx - 1 - (j - pad) : j - pad;
+        const double e = ee[side ? row - 1 : row];  // couples local rows j, j+1
+        v = fma(-e, xn, scr[2 * j]) * scr[2 * j + 1];
+        bad |= !(fabs(v) <= 1e150);
+      }
+      tab[twS(j, side)] = v;
+      xn = v;
+    }
+  }
+  bad = (__ballot_sync(KLE_FULL_MASK, bad && live) >> base) & 0xfu;
   __syncwarp();
-  // the 2 x 2 middle system [bT E; E bB] (e_p, e_q) = (yT, yB) in the scaled variables of the two lanes
-  const double bT = __shfl_sync(KLE_FULL_MASK, beta_last, 0);
-  const double bB = __shfl_sync(KLE_FULL_MASK, beta_last, 1);
-  const double tT = __shfl_sync(KLE_FULL_MASK, t_last, 0);
-  const double tB = __shfl_sync(KLE_FULL_MASK, t_last, 1);
-  if (lane < 2) {
-    const int side = lane, pad = TW_H - (side ? mB : mT);
-    const double E = h * ee[mT - 1];
-    const double idet = 1.0 / fma(bT, bB, -E * E);
-    tab[twA(TW_H - 1, side)] = (side ? bT : bB) * idet;                           // ca: own y
-    tab[twA(TW_H - 1, side) + 1] = -E * idet * (side ? tT / tB : tB / tT);        // cb': partner's y
-    bad |= !(fabs(idet) <= 1e150);
-    for (int j = 0; j < TW_H; ++j)
-      tab[twS(j, side)] = (j >= pad) ? xs[side ? nx - 1 - (j - pad) : j - pad] : 0.0;
-  }
-  const bool any_bad = __any_sync(KLE_FULL_MASK, bad);
-  if (lane == 0) {
-    tab[TW_FLAG] = any_bad ? 1.0 : 0.0;
+  if (role == 0) {
+    tab[TW_FLAG] = bad ? 1.0 : 0.0;
     tab[TW_FLAG + 1] = 0.0;
   }
+  // 1 / t_j by all lanes (off the chains)
+  for (int i = lane; i < TW_SPW * 2 * H; i += 32) {
+    const int sm_ = i / (2 * H), r = i % (2 * H), j = r >> 1, sd = r & 1;
+    double* tb = fsm + sm_ * TW_FSM;
+    const double tv = tb[twT(j, sd)];
+    tb[twS(j, sd) + 1] = (tv != 0.0) ? 1.0 / tv : 0.0;
+  }
   __syncwarp();
-  double* out = blob + (size_t)s * TwL::DOUBLES + TwL::PHI_OFF;
-  for (int i = lane; i < TW_DOUBLES; i += 32) out[i] = tab[i];
+  for (int q = 0; q < TW_SPW; ++q) {
+    const int sq = blockIdx.x * TW_SPW + q;
+    if (sq >= M) break;
+    double* out = blob + (size_t)sq * TwL::DOUBLES + TwL::PHI_OFF;
+    const double* tb = fsm + q * TW_FSM;
+    for (int i = lane; i < TW_DOUBLES; i += 32) out[i] = tb[i];
+  }
+}
+
+__global__ void tw_count_flagged_kernel(const double* __restrict__ blob, int M, int32_t* __restrict__ count) {
+  int n = 0;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < M; s += gridDim.x * blockDim.x)
+    n += blob[(size_t)s * TwL::DOUBLES + kTwFlagOff] != 0.0;
+  n = __reduce_add_sync(KLE_FULL_MASK, n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(count, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -290,6 +329,12 @@ __global__ void __launch_bounds__(32, KLE_TW_MINB) fgr_tw_kernel(FgrArgs a) {
   const unsigned tA = tab_s + (unsigned)(side * 16);
   const double2 cm = lds_v2(tA + (unsigned)((H - 1) * 32));  // {ca, cb'}
 
+  // the kernel is bound by shared-memory wavefronts (ncu: 87% of peak, a broadcast 16-byte load costs two):
+  // the coefficients of the first KLE_TW_NCACHE rows stay in registers over the J steps
+  constexpr int NCACHE = KLE_TW_NCACHE;
+  double2 cc[NCACHE > 0 ? NCACHE : 1];
+#pragma unroll
+  for (int j = 0; j < NCACHE; ++j) cc[j] = lds_v2(tA + (unsigned)(j * 32));
 #pragma unroll 1
   for (int it = 0; it < a.J; ++it) {
     // forward prefix sums as KLE_TW_SPLIT independent chains (a warp's step is bound by the latency of its
@@ -313,7 +358,7 @@ __global__ void __launch_bounds__(32, KLE_TW_MINB) fgr_tw_kernel(FgrArgs a) {
     x[H - 1] = xn;
 #pragma unroll
     for (int j = H - 2; j >= 0; --j) {
-      const double2 c = lds_v2(tA + (unsigned)(j * 32));  // {inv_j, nl_{j+1}^2}
+      const double2 c = (j < NCACHE) ? cc[j < NCACHE ? j : 0] : lds_v2(tA + (unsigned)(j * 32));  // {inv_j, nl_{j+1}^2}
       const double yj = (j >= SL) ? x[j] + ys[j / SL - 1] : x[j];
       xn = fma(c.y, xn, yj * c.x);
       x[j] = xn;
@@ -390,8 +435,20 @@ bool tw_supported(const FineLayoutRT& lay, int nx) {
 
 int tw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, double g0,
               cudaStream_t st) {
-  if (M > 0) tw_factor_kernel<<<(unsigned)M, 32, 0, st>>>(dia, off, blob, M, nx, h, g0);
+  constexpr size_t smem = sizeof(double) * TW_SPW * TW_FSM;
+  static PerDeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, "kle_fine_tw(factor): cudaFuncSetAttribute", [&] {
+        return cudaFuncSetAttribute(tw_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }))
+    return rc;
+  if (M > 0) tw_factor_kernel<<<(unsigned)((M + TW_SPW - 1) / TW_SPW), 32, smem, st>>>(dia, off, blob, M, nx, h, g0);
   return check_launch("tw_factor_kernel");
+}
+
+// number of samples of the batch without a scaled twisted form (flagged by tw_factor) -> *count (device, += )
+int tw_count_flagged(const double* blob, int M, int32_t* count, cudaStream_t st) {
+  if (M > 0) tw_count_flagged_kernel<<<(unsigned)std::min((M + 255) / 256, 1184), 256, 0, st>>>(blob, M, count);
+  return check_launch("tw_count_flagged_kernel");
 }
 
 int tw_fgr(const FgrArgs& a, cudaStream_t st) {

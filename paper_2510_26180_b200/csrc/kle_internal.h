@@ -68,6 +68,7 @@ struct FgrArgs {
   int M, N, nx, J;
   double dt, dT, g0, alpha;
   int tw_fallback = 0;    // 1: only the samples flagged by tw_factor (kle_fine_tw.cu); (16, 8) layout
+  int tw_none_flagged = 0;  // the caller counted the flags (tw_count_flagged): no fallback launch needed
 };
 
 struct PararealArgs {
@@ -131,6 +132,7 @@ bool tw_supported(const FineLayoutRT& lay, int nx);
 int tw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, double g0,
               cudaStream_t st);
 int tw_fgr(const FgrArgs& a, cudaStream_t st);
+int tw_count_flagged(const double* blob, int M, int32_t* count, cudaStream_t st);
 int mw_warps(int nx);
 int mw_blob_doubles(int nx);
 int mw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, cudaStream_t st);
