@@ -662,3 +662,87 @@ def test_twisted_fine_sweep_matches_partitioned_and_dense(cuda, N, nx, J, monkey
             prev = alpha * Uh[s, N - 1] if n == 0 else Uh[s, n - 1]
             want = sc[n] * (x + grid.deltaT * (A @ x) - prev)
             assert rel(R_tw[s, n].cpu().numpy(), want) <= 1e-10
+
+
+def test_twisted_fine_sweep_fallback_for_unscalable_samples(cuda, monkeypatch):
+    """Samples without a scaled twisted form — a vanishing coupling (the row scaling t
+    would be 0), an operator without positive pivots (no steady state A x* = g0) — are
+    flagged by the table kernel and taken by the partitioned kernel, inside one batch
+    with regular samples: the flagged samples equal the KLE_FGR_TW=0 run bitwise (same
+    kernel), the others within rounding; also through the batched PCGC loop, which
+    counts the flags once per solve (kle_capi.cu)."""
+    import torch
+
+    from paper_2510_26180_b200 import SolverConfig, make_time_grid
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import _fgr, build_alpha_circulant, pcgc_solve_device
+
+    rng = np.random.default_rng(99)
+    M, N, nx, J, alpha, g0 = 7, 16, 127, 8, 1e-3, 1.0
+    grid = make_time_grid(1.0, N, J)
+    off = rng.uniform(0.1, 1.0, (M, nx)) * 400.0
+    off[:, -1] = 0.0
+    dia = rng.uniform(0.5, 1.5, (M, nx)) + off + np.concatenate([np.zeros((M, 1)), off[:, :-1]], axis=1)
+    off[2, 40] = 0.0         # decoupled blocks: t = 0 beyond row 40
+    off[5, 90] = 1e-200      # t underflows
+    dia[3, :] -= 2.0 * dia[3, :].max()  # A negative definite: no positive pivots for the steady state
+    dia[3, :] *= 1e-3                  # (I + hA stays positive definite at this step size)
+    off[3, :] *= 1e-3
+    u0 = rng.normal(size=nx)
+    op = DeviceOperator(to_dev(dia), to_dev(-off), g0, to_dev(u0))
+    tables = AlphaTables(build_alpha_circulant(N, alpha))
+    U = to_dev(rng.normal(size=(M, N, nx)))
+    R_tw = torch.zeros((M, N, nx), dtype=torch.float64, device="cuda")
+    R_pt = torch.zeros_like(R_tw)
+    _fgr(op, tables, U, R_tw, J, grid, alpha)
+    monkeypatch.setenv("KLE_FGR_TW", "0")
+    _fgr(op, tables, U, R_pt, J, grid, alpha)
+    monkeypatch.delenv("KLE_FGR_TW")
+    assert torch.isfinite(R_tw).all()
+    for s in (2, 3, 5):
+        assert torch.equal(R_tw[s], R_pt[s]), s
+    for s in (0, 1, 4, 6):
+        assert float((R_tw[s] - R_pt[s]).abs().max()) <= 1e-12 * float(R_pt[s].abs().max())
+        assert not torch.equal(R_tw[s], R_pt[s])  # (the twisted kernel did run)
+    # the batched loop with flagged samples in the batch
+    cfg = SolverConfig(alpha=alpha, tol=1e-9, max_outer_iters=40)
+    keep = [0, 1, 2, 4, 5, 6]  # (sample 3's A is not a diffusion operator: PCGC need not converge for it)
+    op2 = DeviceOperator(to_dev(dia[keep]), to_dev(-off[keep]), g0, to_dev(u0))
+    U0 = to_dev(rng.normal(size=(len(keep), N, nx)))
+    res_tw = pcgc_solve_device(op2, U0.clone(), grid, cfg, tables)
+    monkeypatch.setenv("KLE_FGR_TW", "0")
+    res_pt = pcgc_solve_device(op2, U0.clone(), grid, cfg, tables)
+    monkeypatch.delenv("KLE_FGR_TW")
+    assert torch.equal(res_tw.iters, res_pt.iters)
+    assert int(res_tw.status.ne(1).sum()) == 0
+    scale = float(res_pt.states.abs().max())
+    assert float((res_tw.states - res_pt.states).abs().max()) <= 1e-10 * scale
+    for s in (2, 4):  # keep[2] = 2 and keep[4] = 5: the flagged samples, same kernels in both runs
+        assert torch.equal(res_tw.states[s], res_pt.states[s])
+
+
+def test_twisted_fine_sweep_without_source(cuda, monkeypatch):
+    """g0 = 0: no steady state (x* = 0); the twisted sweep against the partitioned one."""
+    import torch
+
+    from paper_2510_26180_b200 import make_time_grid
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import _fgr, build_alpha_circulant
+
+    rng = np.random.default_rng(5)
+    M, N, nx, J, alpha = 3, 16, 101, 6, 1e-2
+    grid = make_time_grid(0.5, N, J)
+    off = rng.uniform(0.1, 1.0, (M, nx)) * 100.0
+    off[:, -1] = 0.0
+    dia = off + np.concatenate([np.zeros((M, 1)), off[:, :-1]], axis=1)  # singular A (Neumann-like): fine when g0 = 0
+    op = DeviceOperator(to_dev(dia), to_dev(-off), 0.0, to_dev(rng.normal(size=nx)))
+    tables = AlphaTables(build_alpha_circulant(N, alpha))
+    U = to_dev(rng.normal(size=(M, N, nx)))
+    R_tw = torch.zeros((M, N, nx), dtype=torch.float64, device="cuda")
+    R_pt = torch.zeros_like(R_tw)
+    _fgr(op, tables, U, R_tw, J, grid, alpha)
+    monkeypatch.setenv("KLE_FGR_TW", "0")
+    _fgr(op, tables, U, R_pt, J, grid, alpha)
+    monkeypatch.delenv("KLE_FGR_TW")
+    assert not torch.equal(R_tw, R_pt)
+    assert float((R_tw - R_pt).abs().max()) <= 1e-12 * float(R_pt.abs().max())
