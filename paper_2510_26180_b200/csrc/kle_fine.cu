@@ -13,6 +13,7 @@
 // so the coarse solve of the reference collapses to one matvec.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kle_common.cuh"
 namespace kle {
@@ -76,7 +77,9 @@ template <int MR, int P>
 struct FactorSmem {
   using L = FineLayout<MR, P>;
   static constexpr int SPW = 32 / P;                                  // samples per warp
-  static constexpr int BS = KLE_FINE_LAZY ? L::DOUBLES : L::PHI_OFF;  // staged (= stored) blob doubles
+  // scaled partitioned sweep (be_steps_sc): P = 32 layouts carry its tables in the lazy-stitch part
+  static constexpr bool SC = !KLE_FINE_LAZY && P == 32 && L::SC_FITS;
+  static constexpr int BS = KLE_FINE_LAZY ? L::DOUBLES : (SC ? L::SC_FLAG + 1 : L::PHI_OFF);  // staged (= stored) blob doubles
   static constexpr int PER = BS + 2 * L::NXP;                         // + the operator rows
   static constexpr size_t bytes = sizeof(double) * (size_t)SPW * PER;
 };
@@ -120,6 +123,34 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
       }
       b[L::L_OFF + row] = l;
       b[L::INV_OFF + row] = inv;
+    }
+  }
+  bool sc_bad = false;
+  if constexpr (FS::SC) {
+    // steady state A x* = g0 (Thomas, one division per row; A needs positive pivots), lane 1, before dd / ee
+    // are reused; the elimination multipliers wait in the 1/t slots
+    if (k == 1) {
+      double* xs = b + L::SC_XS;
+      double* cw = b + L::SC_IT;
+      if (g0 != 0.0) {
+        double ib = 1.0 / dd[0];
+        sc_bad |= !(dd[0] > 0.0);
+        cw[0] = ee[0] * ib;
+        xs[0] = g0 * ib;
+        for (int i = 1; i < nx; ++i) {
+          const double e = ee[i - 1];
+          const double bt = fma(-e, cw[i - 1], dd[i]);
+          sc_bad |= !(bt > 0.0);
+          ib = 1.0 / bt;
+          cw[i] = ee[i] * ib;
+          xs[i] = fma(-e, xs[i - 1], g0) * ib;
+        }
+        for (int i = nx - 2; i >= 0; --i) xs[i] = fma(-cw[i], xs[i + 1], xs[i]);
+        for (int i = 0; i < nx; ++i) sc_bad |= !(fabs(xs[i]) <= 1e150);
+        for (int i = nx; i < NXP; ++i) xs[i] = 0.0;
+      } else {
+        for (int i = 0; i < NXP; ++i) xs[i] = 0.0;
+      }
     }
   }
   __syncwarp();
@@ -182,6 +213,44 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
       }
     }
   }
+  if constexpr (FS::SC) {  // tables of the scaled partitioned sweep (kle_fine.cuh: be_steps_sc)
+    __syncwarp();  // pie / sigs are consumed
+    const double* l = b + L::L_OFF + k * MR;
+    double t = 1.0, kprod = 1.0;
+    for (int j = 0; j < MR; ++j) {
+      const int row = k * MR + j;
+      if (j > 0) t = (row < nx) ? -l[j] * t : 1.0;  // pad rows: 1 (never used, must not poison q)
+      if (row < nx) sc_bad |= !(fabs(t) >= 1e-150 && fabs(t) <= 1e150);
+      b[L::SC_T + row] = t;
+      b[L::SC_IT + row] = 1.0 / t;
+      if (j + 1 < MR) kprod *= l[j + 1] * l[j + 1];
+    }
+    const double lnext = (k + 1 < P) ? b[L::L_OFF + (k + 1) * MR] : 0.0;
+    const double qk = -lnext / t;  // t = t_{k,last}
+    __syncwarp();
+    const double rho = (k > 0) ? -l[0] * b[L::SC_T + k * MR - 1] : 0.0;
+    b[L::SC_RHO + k] = rho;
+    b[L::SC_Q + k] = qk;
+    dd[k] = rho;         // forward scan multiplier of chunk k
+    ee[k] = kprod * qk;  // backward scan multiplier: sg_{k,0}
+    __syncwarp();
+    for (int tt = 0; tt < L::LOGP; ++tt) {
+      const int d = 1 << tt;
+      double af = 0.0, bb = 0.0;
+      if (k >= d) {
+        af = 1.0;
+        for (int q = k - d + 1; q <= k; ++q) af *= dd[q];
+      }
+      if (k + d < P) {
+        bb = 1.0;
+        for (int q = k; q <= k + d - 1; ++q) bb *= ee[q];
+      }
+      b[L::SC_AF + tt * P + k] = af;
+      b[L::SC_BB + tt * P + k] = bb;
+    }
+    const bool any_bad = __any_sync(KLE_FULL_MASK, sc_bad);
+    if (k == 0) b[L::SC_FLAG] = any_bad ? 1.0 : 0.0;
+  }
   __syncwarp();
   for (int q = 0; q < FS::SPW; ++q) {
     const int sq = s0 + q;
@@ -224,7 +293,7 @@ struct FgrSmem {
   static constexpr size_t bytes(int tabs) { return ((size_t)(NC + 3) * LD + MR + 8 + (size_t)tabs * NXP) * sizeof(double); }
 };
 
-template <int MR, int P, int R, int NT, bool PIPE>
+template <int MR, int P, int R, int NT, bool PIPE, bool SC = false>
 #ifdef KLE_FGR_MINB_ALL  // tuning override
 #define KLE_FGR_MINB(MR, R, NT) KLE_FGR_MINB_ALL
 #else
@@ -239,6 +308,10 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
   if constexpr (MR == 16 && P == 8) {  // the twisted kernel took every sample it has tables for
     if (a.tw_fallback && a.ffac[(size_t)s * L::DOUBLES + kTwFlagOff] == 0.0) return;
+  }
+  if constexpr (FactorSmem<MR, P>::SC) {  // scaled sweep: flagged samples go to the unscaled kernel and only those
+    const bool flagged = (SC || a.tw_fallback) && a.F_given == nullptr && a.ffac[(size_t)s * L::DOUBLES + L::SC_FLAG] != 0.0;
+    if (SC ? flagged : (a.tw_fallback && !flagged)) return;
   }
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
@@ -271,7 +344,7 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
     // register allocation is sensitive to it (10.17 ms per 8,192 samples against 10.6-11.0 with the fast form).
     constexpr bool FAST = NT == 32;
     constexpr int RPT = (NXP + NT - 1) / NT;
-    LaneFactors<MR, P> fac;
+    std::conditional_t<SC, LaneFactorsSC<MR, P>, LaneFactors<MR, P>> fac;
     if constexpr (FAST) {
       fac.load(a.ffac + (size_t)s * L::DOUBLES, k, nx);
       int so[RPT];
@@ -329,7 +402,7 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
     double* cs = ee + LD + MR;  // [3][MR][P] chunk products (KLE_FINE_CS) / [5][MR][P] lazy tables (LZ)
     // chunk products from shared memory: the one-warp R = 4 variant (c4: 234 registers, 8 chains per
     // SMSP; 6.16 -> 5.17 ms per 131k-sample launch), or every variant under KLE_FINE_CS
-    constexpr bool CS = (KLE_FINE_CS || NT == 32) && !PIPE && !KLE_FINE_LAZY;
+    constexpr bool CS = (KLE_FINE_CS || NT == 32) && !PIPE && !KLE_FINE_LAZY && !SC;
     constexpr bool LZ = CS && KLE_FGR_LZ;
     if constexpr (LZ) {
       if (w == 0 && slot == 0) lazy_tables<MR, P>(cs, fac, k, hg);
@@ -358,6 +431,17 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
         }
       }
     } else {
+      if constexpr (SC) {  // w = (x - x*) / t
+        const double* bl = a.ffac + (size_t)s * L::DOUBLES;
+#pragma unroll
+        for (int j = 0; j < MR; ++j) {
+          const int row = k * MR + j;
+          const double xs = bl[L::SC_XS + row], its = bl[L::SC_IT + row];
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            x[r][j] = (row < nx && n0 + nl[r] < N) ? (st[nl[r] * LD + SM::pidx(row)] - xs) * its : 0.0;
+        }
+      } else {
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -365,18 +449,31 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
           const int row = k * MR + j;
           x[r][j] = (row < nx && n0 + nl[r] < N) ? st[nl[r] * LD + SM::pidx(row)] + hg : 0.0;
         }
+      }
     }
     FGR_T(3);
-    if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
+    if constexpr (SC) be_steps_sc<MR, P, R>(x, fac, a.J);
+    else if constexpr (PIPE) be_steps_pipe<MR, P, R>(x, fac, k, a.J, hg);
     else if constexpr (KLE_FINE_LAZY) be_steps_lazy<MR, P, R>(x, fac, a.ffac + (size_t)s * L::DOUBLES, k, a.J, hg);
     else if constexpr (LZ) be_steps_lz<MR, P, R>(x, fac, k, a.J, cs);
     else if constexpr (CS) be_steps_cs<MR, P, R>(x, fac, k, a.J, cs);
     else be_steps<MR, P, R>(x, fac, k, a.J, hg);
     FGR_T(4);
+    if constexpr (SC) {  // F = t w + x*
+      const double* bl = a.ffac + (size_t)s * L::DOUBLES;
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const int row = k * MR + j;
+        const double xs = bl[L::SC_XS + row], ts = bl[L::SC_T + row];
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r][j] = (row < nx) ? fma(ts, x[r][j], xs) : 0.0;
+      }
+    } else {
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int j = 0; j < MR; ++j) x[r][j] = (k * MR + j < nx) ? x[r][j] - hg : 0.0;
+    }
     if (a.F_out) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -576,6 +673,23 @@ struct FineInst {
     fgr_kernel<MR, P, R, NT, PIPE><<<grid, NT, smem, st>>>(a);
     return check_launch("fgr_kernel");
   }
+  // scaled partitioned sweep (be_steps_sc), then the unscaled kernel for the samples flagged by the factor kernel
+  static int fgr_sc(const FgrArgs& a, cudaStream_t st) {
+    dim3 grid(a.M, (a.N + NC - 1) / NC);
+    const size_t smem = FgrSmem<MR, P, NC>::bytes(0);
+    static PerDeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, "kle_fine(sc): cudaFuncSetAttribute", [&] {
+          return cudaFuncSetAttribute(fgr_kernel<MR, P, R, NT, PIPE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024);
+        }))
+      return rc;
+    fgr_kernel<MR, P, R, NT, PIPE, true><<<grid, NT, smem, st>>>(a);
+    if (int rc = check_launch("fgr_kernel(sc)")) return rc;
+    if (a.tw_none_flagged) return KLE_OK;
+    FgrArgs b = a;
+    b.tw_fallback = 1;
+    return fgr(b, st);
+  }
   static int sweep(const SweepArgs& a, cudaStream_t st) {
     dim3 grid(a.M, (a.Q + NC - 1) / NC);
     sweep_kernel<MR, P, R, NT, PIPE><<<grid, NT, 0, st>>>(a);
@@ -638,6 +752,18 @@ static const int kNumDefaults = 6;
   KLE_FINE_DISPATCH(16, 32, 3, 3, CALL)   \
   KLE_FINE_DISPATCH(8, 8, 4, 0, CALL)
 
+// scaled partitioned sweep (be_steps_sc) for the (16, 32) layout (128 < nx <= 512), KLE_FGR_SC=1
+bool sc_supported(const FineLayoutRT& lay) {
+  if (KLE_FINE_LAZY || lay.W || lay.kind || lay.P != 32) return false;
+  if (!(lay.MR == 16 && lay.R == 3 && lay.pipe == 2)) return false;  // (32, 32, 2) spills with the scaled factors
+  // opt-in: measured 9.63 against 9.85 ms per 8,192-sample config-2 launch (the step loop there is bound by the
+  // latency of its carry scans, not by FP64 issue), so the unscaled step stays the default; read per call
+  const char* e = getenv("KLE_FGR_SC");
+  return e && *e == '1';
+}
+
+int sc_flag_offset(const FineLayoutRT& lay) { return FineLayout<16, 32>::SC_FLAG; }  // (the only scaled layout)
+
 FineLayoutRT fine_layout(int nx) {
   const char* env = getenv("KLE_FINE_VARIANT");
   if (env && *env) {
@@ -680,6 +806,9 @@ int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
     lay.kind = 0;  // F given: no sweep, any (MR, P) register variant serves the epilogue
     lay.pipe = 0;
     lay.R = (lay.MR == 16) ? 3 : (lay.P == 32 ? 4 : 2);
+  }
+  if (!a.F_given && sc_supported(lay)) {
+    return FineInst<16, 32, 3, 2>::fgr_sc(a, st);
   }
   if (!a.F_given && !a.F_out && a.Rout && tw_supported(lay, a.nx)) {
     if (int rc = tw_fgr(a, st)) return rc;

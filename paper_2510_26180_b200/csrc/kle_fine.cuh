@@ -29,6 +29,13 @@ struct FineLayout {
   static constexpr int PHI2_OFF = PHI_OFF + NXP;          // phi2 = Fwd0(phi)
   static constexpr int SG_OFF = PHI2_OFF + NXP;           // sg_j = prod_{i=j+1}^{MR} (-l_i)
   static constexpr int SG2_OFF = SG_OFF + NXP;            // sg2  = Fwd0(sg)
+  // Scaled partitioned sweep (be_steps_sc; P = 32 layouts), in the lazy-stitch part of the blob (unused unless
+  // KLE_FINE_LAZY): steady state x*_r, chunk-local scaling t_r and 1 / t_r (chunk-major [k][j]), then the scan
+  // multipliers of the scaled recurrences, rho_k, q_k and the per-sample "no scaled form" flag
+  static constexpr int SC_XS = PHI_OFF, SC_T = PHI2_OFF, SC_IT = SG_OFF;
+  static constexpr int SC_AF = SG2_OFF, SC_BB = SC_AF + LOGP * P, SC_RHO = SC_BB + LOGP * P, SC_Q = SC_RHO + P;
+  static constexpr int SC_FLAG = SC_Q + P;
+  static constexpr bool SC_FITS = 2 * LOGP * P + 2 * P + 1 <= NXP;
   // the (16, 8) blob carries the twisted two-lane tables (kle_fine_tw.cu) from PHI_OFF on
   static constexpr int DOUBLES = 6 * NXP + 2 * LOGP * P + ((MR == 16 && P == 8) ? 256 : 0);
 };
@@ -158,6 +165,106 @@ __device__ __forceinline__ void be_steps(double (&x)[R][MR], const LaneFactors<M
 #pragma unroll
         for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scaled partitioned step (round 2, after the twisted kernel's rewrite of the recurrences). The steady state
+// A x* = g0 removes the source (e = x - x* obeys (I + hA) e_new = e_old), and a chunk-local diagonal scaling
+// e_j = t_j w_j, t_0 = 1, t_j = (-l_j) t_{j-1}, turns the in-chunk forward multipliers into 1 and, with
+// them, every forward stitch coefficient pi_j / t_j into the same number: per step, row and right-hand side
+//   yl_j = w_j + yl_{j-1}                 (DADD, local forward = prefix sums)
+//   y_j  = yl_j + C                        (DADD, forward stitch; C = rho_k Y_{k-1}, rho_k = -l_{k,0} t_{k-1,last})
+//   z_j  = y_j inv_j                       (DMUL)
+//   wl_j = z_j + kk_j wl_{j+1}             (DFMA, local backward; kk_j = l_{j+1}^2)
+//   w_j  = wl_j + sg_j X                   (DFMA, backward stitch; sg_last = q_k = -l_{k+1,0} / t_{k,last})
+// against five three-operand DFMAs (a DFMA with three register operands issues in 3 cycles, DADD / DMUL in 2)
+// and three R-independent products per row (here one). The carry scans keep their shape (Kogge-Stone with
+// precomputed multipliers). Pad rows: inv = kk = 0, so they stay 0.
+// ---------------------------------------------------------------------------
+template <int MR, int P>
+struct LaneFactorsSC {
+  double inv[MR], kk[MR];  // kk[MR-1] unused
+  double af[FineLayout<MR, P>::LOGP], bb[FineLayout<MR, P>::LOGP];
+  double rho, q;
+  int nreal;
+
+  __device__ __forceinline__ void load(const double* __restrict__ blob, int k, int nx) {
+    using L = FineLayout<MR, P>;
+    nreal = min(MR, max(0, nx - k * MR));
+    const double2* lp = reinterpret_cast<const double2*>(blob + L::L_OFF + k * MR);
+    const double2* ip = reinterpret_cast<const double2*>(blob + L::INV_OFF + k * MR);
+    double l[MR];
+#pragma unroll
+    for (int j = 0; j < MR / 2; ++j) {
+      const double2 a = lp[j], b = ip[j];
+      l[2 * j] = a.x;
+      l[2 * j + 1] = a.y;
+      inv[2 * j] = (2 * j < nreal) ? b.x : 0.0;
+      inv[2 * j + 1] = (2 * j + 1 < nreal) ? b.y : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < MR; ++j) kk[j] = (j + 1 < MR) ? l[j + 1] * l[j + 1] : 0.0;
+#pragma unroll
+    for (int t = 0; t < L::LOGP; ++t) {
+      af[t] = blob[L::SC_AF + t * P + k];
+      bb[t] = blob[L::SC_BB + t * P + k];
+    }
+    rho = blob[L::SC_RHO + k];
+    q = blob[L::SC_Q + k];
+  }
+};
+
+template <int MR, int P, int R>
+__device__ __forceinline__ void be_steps_sc(double (&x)[R][MR], const LaneFactorsSC<MR, P>& f, int J) {
+  using L = FineLayout<MR, P>;
+  for (int it = 0; it < J; ++it) {
+#pragma unroll
+    for (int j = 1; j < MR; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] += x[r][j - 1];
+    double Y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) Y[r] = x[r][MR - 1];
+#pragma unroll
+    for (int t = 0; t < L::LOGP; ++t) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_up_sync(KLE_FULL_MASK, Y[r], 1 << t, P);
+        Y[r] = fma(f.af[t], o, Y[r]);  // af = 0 for k < 2^t
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) Y[r] = f.rho * __shfl_up_sync(KLE_FULL_MASK, Y[r], 1, P);  // rho_0 = 0
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double z = (x[r][j] + Y[r]) * f.inv[j];
+        if (j + 1 < MR) z = fma(f.kk[j], x[r][j + 1], z);
+        x[r][j] = z;
+      }
+    }
+    double X[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) X[r] = x[r][0];
+#pragma unroll
+    for (int t = 0; t < L::LOGP; ++t) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_down_sync(KLE_FULL_MASK, X[r], 1 << t, P);
+        X[r] = fma(f.bb[t], o, X[r]);  // bb = 0 for k + 2^t >= P
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) X[r] = __shfl_down_sync(KLE_FULL_MASK, X[r], 1, P);  // (q = 0 in the last chunk)
+    double sg = f.q;
+#pragma unroll
+    for (int j = MR - 1; j >= 0; --j) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r][j] = fma(sg, X[r], x[r][j]);
+      if (j > 0) sg *= f.kk[j - 1];
     }
   }
 }

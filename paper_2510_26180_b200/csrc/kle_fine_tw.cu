@@ -212,10 +212,11 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
   }
 }
 
-__global__ void tw_count_flagged_kernel(const double* __restrict__ blob, int M, int32_t* __restrict__ count) {
+__global__ void tw_count_flagged_kernel(const double* __restrict__ blob, int M, int stride, int off,
+                                        int32_t* __restrict__ count) {
   int n = 0;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < M; s += gridDim.x * blockDim.x)
-    n += blob[(size_t)s * TwL::DOUBLES + kTwFlagOff] != 0.0;
+    n += blob[(size_t)s * stride + off] != 0.0;
   n = __reduce_add_sync(KLE_FULL_MASK, n);
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(count, n);
 }
@@ -446,8 +447,13 @@ int tw_factor(const double* dia, const double* off, double* blob, int M, int nx,
 }
 
 // number of samples of the batch without a scaled twisted form (flagged by tw_factor) -> *count (device, += )
-int tw_count_flagged(const double* blob, int M, int32_t* count, cudaStream_t st) {
-  if (M > 0) tw_count_flagged_kernel<<<(unsigned)std::min((M + 255) / 256, 1184), 256, 0, st>>>(blob, M, count);
+int tw_count_flagged(const double* blob, int M, int stride, int off, int32_t* count, cudaStream_t st) {
+  if (stride == 0) {
+    stride = TwL::DOUBLES;
+    off = kTwFlagOff;
+  }
+  if (M > 0)
+    tw_count_flagged_kernel<<<(unsigned)std::min((M + 255) / 256, 1184), 256, 0, st>>>(blob, M, stride, off, count);
   return check_launch("tw_count_flagged_kernel");
 }
 

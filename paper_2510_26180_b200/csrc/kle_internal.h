@@ -129,10 +129,13 @@ int sf_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st);
 int sf_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st);
 // twisted two-lane sweep for 64 < nx <= 128 (kle_fine_tw.cu); tables in the (16, 8) blob's spare part
 bool tw_supported(const FineLayoutRT& lay, int nx);
+bool sc_supported(const FineLayoutRT& lay);  // scaled partitioned sweep (be_steps_sc), P = 32 layouts
+int sc_flag_offset(const FineLayoutRT& lay);
 int tw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, double g0,
               cudaStream_t st);
 int tw_fgr(const FgrArgs& a, cudaStream_t st);
-int tw_count_flagged(const double* blob, int M, int32_t* count, cudaStream_t st);
+// samples whose blob carries a nonzero "no scaled form" flag at blob[s * stride + off] (stride 0: the twisted tables)
+int tw_count_flagged(const double* blob, int M, int stride, int off, int32_t* count, cudaStream_t st);
 int mw_warps(int nx);
 int mw_blob_doubles(int nx);
 int mw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, cudaStream_t st);
