@@ -87,7 +87,7 @@ struct FactorSmem {
 template <int MR, int P>
 __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restrict__ dia,
                                                          const double* __restrict__ off, double* __restrict__ blob,
-                                                         int M, int nx, double h, double g0) {
+                                                         int M, int nx, double h, double g0, int sc_on) {
   using L = FineLayout<MR, P>;
   using FS = FactorSmem<MR, P>;
   constexpr int NXP = L::NXP;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
     }
   }
   bool sc_bad = false;
-  if constexpr (FS::SC) {
+  if (FS::SC && sc_on) {
     // steady state A x* = g0 (Thomas, one division per row; A needs positive pivots), lane 1, before dd / ee
     // are reused; the elimination multipliers wait in the 1/t slots
     if (k == 1) {
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
       }
     }
   }
-  if constexpr (FS::SC) {  // tables of the scaled partitioned sweep (kle_fine.cuh: be_steps_sc)
+  if (FS::SC && sc_on) {  // tables of the scaled partitioned sweep (kle_fine.cuh: be_steps_sc)
     __syncwarp();  // pie / sigs are consumed
     const double* l = b + L::L_OFF + k * MR;
     double t = 1.0, kprod = 1.0;
@@ -257,7 +257,11 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
     if (sq >= M) break;
     double* out = blob + (size_t)sq * L::DOUBLES;
     const double* bq = fsm + q * FS::PER;
-    for (int i = lane; i < FS::BS; i += 32) out[i] = bq[i];  // l, 1/beta and the scan multipliers (+ lazy vectors)
+    // l, 1/beta and the scan multipliers (+ lazy vectors / the scaled tables; without them every sample is
+    // flagged, so a later KLE_FGR_SC=1 sweep on this blob falls through to the unscaled kernel)
+    const int ns = (FS::SC && !sc_on) ? L::PHI_OFF : FS::BS;
+    for (int i = lane; i < ns; i += 32) out[i] = bq[i];
+    if (FS::SC && !sc_on && lane == 0) out[L::SC_FLAG] = 1.0;
   }
   (void)g0;
 }
@@ -656,7 +660,10 @@ struct FineInst {
         }))
       return rc;
     constexpr int SPW = FactorSmem<MR, P>::SPW;
-    if (M > 0) fine_factor_kernel<MR, P><<<(unsigned)((M + SPW - 1) / SPW), 32, smem, st>>>(dia, off, blob, M, nx, h, g0);
+    const char* e = getenv("KLE_FGR_SC");
+    const int sc_on = e && *e == '1';
+    if (M > 0)
+      fine_factor_kernel<MR, P><<<(unsigned)((M + SPW - 1) / SPW), 32, smem, st>>>(dia, off, blob, M, nx, h, g0, sc_on);
     return check_launch("fine_factor_kernel");
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {

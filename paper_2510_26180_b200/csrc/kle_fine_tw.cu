@@ -55,6 +55,9 @@ namespace kle {
 #ifndef KLE_TW_NCACHE
 #define KLE_TW_NCACHE 0  // rows whose backward coefficients stay in registers
 #endif
+#ifndef KLE_TW_PREFETCH
+#define KLE_TW_PREFETCH 0  // L2 prefetch distance in CTAs (0: off)
+#endif
 #ifndef KLE_TW_MINB
 #define KLE_TW_MINB 8  // CTAs (= warps) per SM the register allocation is bounded for
 #endif
@@ -300,6 +303,25 @@ __global__ void __launch_bounds__(32, KLE_TW_MINB) fgr_tw_kernel(FgrArgs a) {
       if (sd ? (r + 1 < nx) : (r > 0)) cp_async8(e + 8, eg + i * 32 - (sd ? 0 : 1));
     }
     asm volatile("cp.async.commit_group;\n" ::);  // group 2: epilogue operands
+#if KLE_TW_PREFETCH
+    // L2 prefetch for the CTA that takes this SM slot later (sample s + KLE_TW_PREFETCH CTAs): with 8 latency-bound
+    // warps per SM the memory phases of a CTA do not overlap the other CTAs' sweeps, so the fetch is started here
+    if (blockIdx.y == 0) {
+      const int sp = s + KLE_TW_PREFETCH;
+      if (sp < a.M) {
+        const char* pu = reinterpret_cast<const char*>(a.U + (size_t)sp * N * nx);
+        const int nl_u = (int)(((size_t)N * nx * sizeof(double) + 127) / 128);
+        for (int i = lane; i < nl_u; i += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + (size_t)i * 128));
+        const char* pt = reinterpret_cast<const char*>(a.ffac + (size_t)sp * TwL::DOUBLES + TwL::PHI_OFF);
+        for (int i = lane; i < (TW_DOUBLES * 8 + 127) / 128; i += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pt + (size_t)i * 128));
+        const char* pd = reinterpret_cast<const char*>(a.dia + (size_t)sp * nx);
+        const char* pe = reinterpret_cast<const char*>(a.off + (size_t)sp * nx);
+        if (lane < 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(pd + (size_t)lane * 128));
+        else if (lane < 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(pe + (size_t)(lane - 8) * 128));
+      }
+    }
+#endif
     // entries no copy writes: the pad rows of this lane's start row (all of it for an unused lane pair),
     // the pad entries of de and the outer coupling of the two end rows
     const int nz = valid ? pad : H;
