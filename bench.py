@@ -380,11 +380,11 @@ def run_b200(args):
     # sample pipeline (two when the batch is large, kle_capi.cu) one fgr and one CGC launch (an upper bound:
     # a pipeline stops as soon as its own samples have converged), and 2 x (2 col-sum + 1 scale) for the moments
     pipes = 2 if (M >= 8192 and os.environ.get("KLE_PCGC_PIPES", "2") != "1") else 1
-    # the twisted two-lane fine sweep (kle_fine_tw.cu, 64 < nx <= 128) adds its table kernel and, per sweep,
-    # the launch of the partitioned kernel that takes the samples flagged as having no scaled form (none here)
+    # the twisted two-lane fine sweep (kle_fine_tw.cu, 64 < nx <= 128) adds its table kernel and the count of the
+    # samples flagged as having no scaled form (none here, so the partitioned fallback kernel is never launched)
     tw_path = 64 < c["nx"] <= 128 and os.environ.get("KLE_FGR_TW", "1") != "0"
     launches_per_step = (1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 1
-                         + 2 * pipes * int(kmax) + 6 + ((1 + pipes * int(kmax)) if tw_path else 0))
+                         + 2 * pipes * int(kmax) + 6 + (2 if tw_path else 0))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_all[:n_sub])

@@ -77,7 +77,14 @@ int kle_kl_tridiag_f64(const double* xi, int M, int d, const double* kl_table, i
 
 /* _linear_factor (pintuq/propagators.py:25-34): factor I + h*A for every
  * sample into the solver blob (size M * blob_doubles); g0 is the constant
- * source value (g(t) = g0 * ones). */
+ * source value (g(t) = g0 * ones). For 64 < nx <= 128 the blob also carries
+ * the tables of the twisted two-lane sweep (kle_fine_tw.cu: twisted
+ * factorisation, row scaling, steady state A x* = g0) and a per-sample flag
+ * for samples without such a form (vanishing couplings, A without positive
+ * pivots); kle_fgr_f64 sends flagged samples through the partitioned kernel.
+ * Environment (read per call): KLE_FGR_TW=0 disables the twisted sweep,
+ * KLE_FGR_SC=1 (set when factoring AND sweeping) selects the scaled
+ * partitioned step for 128 < nx <= 512. */
 int kle_fine_factor_f64(const double* dia, const double* off, int M, int nx, double h, double g0,
                         double* blob, void* stream);
 
