@@ -383,8 +383,9 @@ def run_b200(args):
     # the twisted two-lane fine sweep (kle_fine_tw.cu, 64 < nx <= 128) adds its table kernel and the count of the
     # samples flagged as having no scaled form (none here, so the partitioned fallback kernel is never launched)
     tw_path = 64 < c["nx"] <= 128 and os.environ.get("KLE_FGR_TW", "1") != "0"
+    pw_path = 128 < c["nx"] <= 512 and os.environ.get("KLE_FGR_PW", "1") != "0"
     launches_per_step = (1 + 1 + (1 + (1 if solver.surrogate.mode == "direct" else 2)) + 1
-                         + 2 * pipes * int(kmax) + 6 + (2 if tw_path else 0))
+                         + 2 * pipes * int(kmax) + 6 + (2 if (tw_path or pw_path) else 0))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, c, model, grid, cfg, sur, xi_all[:n_sub])
@@ -420,18 +421,20 @@ def run_b200(args):
                           "built_on": "rank 0 (device snapshots), broadcast"},
             "roofline": {
                 "kernel": ("fgr_tw_kernel (twisted two-lane J-step fine sweep + CGC rhs)" if tw_path
+                           else "fgr_pw_kernel (eight-lane scaled J-step fine sweep + CGC rhs)" if pw_path
                            else "fgr_kernel (fused J-step fine sweep + CGC rhs)"),
                 "bound": "fp64",
                 "achieved": fgr_tflops,
                 "peak": fp64_peak,
                 "unit": "TFLOP/s",
                 "frac": (fgr_tflops / fp64_peak) if fp64_peak else None,
-                "traffic": traffic_of(peaks, args.config, "fgr_tw_kernel" if tw_path else "fgr_kernel", M),
+                "traffic": traffic_of(peaks, args.config,
+                                      "fgr_tw_kernel" if tw_path else "fgr_pw_kernel" if pw_path else "fgr_kernel", M),
                 "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per sample-iteration "
                                   "(profiles/traffic.json) x samples per launch",
                 "peak_source": peaks.get("fp64_source"),
                 "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch (M = rank shard)",
-                "executed_flop_per_dof_update": 4 if tw_path else 10,
+                "executed_flop_per_dof_update": 4 if tw_path else 7 if pw_path else 10,
                 "hbm_frac": (fgr_bytes / (fgr_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
                 "ms_per_launch": fgr_ms,
             },

@@ -377,10 +377,11 @@ static int pcgc_loop(double* U, const double* u0, const double* dia, const doubl
   // form, so that the partitioned kernel is launched after each sweep only when there are any (one
   // stream synchronisation per solve instead of an empty 1M-CTA launch per sweep)
   int tw_none_flagged = 0;
-  const bool sc = sc_supported(lay);
-  if (!fused && (sc || tw_supported(lay, nx))) {
+  const bool pw = pw_supported(lay, nx), sc = !pw && sc_supported(lay);
+  if (!fused && (pw || sc || tw_supported(lay, nx))) {
     cudaMemsetAsync(counter + 8, 0, sizeof(int32_t), st);
-    KLE_TRY(tw_count_flagged(fine_blob, M, sc ? lay.doubles : 0, sc ? sc_flag_offset(lay) : 0, counter + 8, st));
+    const int foff = pw ? pw_flag_offset() : (sc ? sc_flag_offset(lay) : 0);
+    KLE_TRY(tw_count_flagged(fine_blob, M, (pw || sc) ? lay.doubles : 0, foff, counter + 8, st));
     cudaMemcpyAsync(&h_count[kMaxPipes], counter + 8, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return set_error(KLE_ERR_CUDA, "pcgc_solve: flag count");
     tw_none_flagged = h_count[kMaxPipes] == 0;

@@ -78,7 +78,7 @@ struct FactorSmem {
   using L = FineLayout<MR, P>;
   static constexpr int SPW = 32 / P;                                  // samples per warp
   // scaled partitioned sweep (be_steps_sc): P = 32 layouts carry its tables in the lazy-stitch part
-  static constexpr bool SC = !KLE_FINE_LAZY && P == 32 && L::SC_FITS;
+  static constexpr bool SC = !KLE_FINE_LAZY && (P == 32 || (MR == 64 && P == 8)) && L::SC_FITS;
   static constexpr int BS = KLE_FINE_LAZY ? L::DOUBLES : (SC ? L::SC_FLAG + 1 : L::PHI_OFF);  // staged (= stored) blob doubles
   static constexpr int PER = BS + 2 * L::NXP;                         // + the operator rows
   static constexpr size_t bytes = sizeof(double) * (size_t)SPW * PER;
@@ -87,7 +87,8 @@ struct FactorSmem {
 template <int MR, int P>
 __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restrict__ dia,
                                                          const double* __restrict__ off, double* __restrict__ blob,
-                                                         int M, int nx, double h, double g0, int sc_on) {
+                                                         int M, int nx, double h, double g0, int sc_on,
+                                                         int stride, int offset) {
   using L = FineLayout<MR, P>;
   using FS = FactorSmem<MR, P>;
   constexpr int NXP = L::NXP;
@@ -222,11 +223,20 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
       if (j > 0) t = (row < nx) ? -l[j] * t : 1.0;  // pad rows: 1 (never used, must not poison q)
       if (row < nx) sc_bad |= !(fabs(t) >= 1e-150 && fabs(t) <= 1e150);
       b[L::SC_T + row] = t;
-      b[L::SC_IT + row] = 1.0 / t;
+      if (!(MR == 64 && P == 8)) b[L::SC_IT + row] = 1.0 / t;
       if (j + 1 < MR) kprod *= l[j + 1] * l[j + 1];
     }
     const double lnext = (k + 1 < P) ? b[L::L_OFF + (k + 1) * MR] : 0.0;
     const double qk = -lnext / t;  // t = t_{k,last}
+    if constexpr (MR == 64 && P == 8) {
+      // the eight-lane sweep (kle_fine_pw.cu) forms 1 / t itself and reads the backward stitch
+      // coefficients sg_j = (prod_{i=j..MR-2} l_{i+1}^2) q_k from these slots
+      double sg = qk;
+      for (int j = MR - 1; j >= 0; --j) {
+        b[L::SC_IT + k * MR + j] = sg;
+        sg *= l[j] * l[j];
+      }
+    }
     __syncwarp();
     const double rho = (k > 0) ? -l[0] * b[L::SC_T + k * MR - 1] : 0.0;
     b[L::SC_RHO + k] = rho;
@@ -248,14 +258,14 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
       b[L::SC_AF + tt * P + k] = af;
       b[L::SC_BB + tt * P + k] = bb;
     }
-    const bool any_bad = __any_sync(KLE_FULL_MASK, sc_bad);
+    const bool any_bad = ((__ballot_sync(KLE_FULL_MASK, sc_bad) >> (grp * P)) & (P == 32 ? 0xffffffffu : ((1u << P) - 1u))) != 0;
     if (k == 0) b[L::SC_FLAG] = any_bad ? 1.0 : 0.0;
   }
   __syncwarp();
   for (int q = 0; q < FS::SPW; ++q) {
     const int sq = s0 + q;
     if (sq >= M) break;
-    double* out = blob + (size_t)sq * L::DOUBLES;
+    double* out = blob + (size_t)sq * stride + offset;
     const double* bq = fsm + q * FS::PER;
     // l, 1/beta and the scan multipliers (+ lazy vectors / the scaled tables; without them every sample is
     // flagged, so a later KLE_FGR_SC=1 sweep on this blob falls through to the unscaled kernel)
@@ -310,12 +320,11 @@ __global__ void __launch_bounds__(NT, KLE_FGR_MINB(MR, R, NT)) fgr_kernel(FgrArg
   constexpr int NXP = MR * P;
   const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
-  if constexpr (MR == 16 && P == 8) {  // the twisted kernel took every sample it has tables for
-    if (a.tw_fallback && a.ffac[(size_t)s * L::DOUBLES + kTwFlagOff] == 0.0) return;
+  if (a.tw_fallback && a.F_given == nullptr) {  // only the samples the twisted / scaled / eight-lane kernel skipped
+    if (a.ffac[(size_t)s * L::DOUBLES + a.flag_off] == 0.0) return;
   }
-  if constexpr (FactorSmem<MR, P>::SC) {  // scaled sweep: flagged samples go to the unscaled kernel and only those
-    const bool flagged = (SC || a.tw_fallback) && a.F_given == nullptr && a.ffac[(size_t)s * L::DOUBLES + L::SC_FLAG] != 0.0;
-    if (SC ? flagged : (a.tw_fallback && !flagged)) return;
+  if constexpr (SC) {  // scaled step: flagged samples go to the unscaled kernel
+    if (a.ffac[(size_t)s * L::DOUBLES + L::SC_FLAG] != 0.0) return;
   }
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = lane % P, slot = lane / P;
@@ -651,7 +660,8 @@ struct FineInst {
   static constexpr int NC = (NT / 32) * (32 / P) * R;
 
   static int factor(const double* dia, const double* off, double* blob, int M, int nx, double h,
-                    double g0, cudaStream_t st) {
+                    double g0, cudaStream_t st, int force_sc = 0, int stride = FineLayout<MR, P>::DOUBLES,
+                    int offset = 0) {
     constexpr size_t smem = fine_factor_smem<MR, P>();
     static PerDeviceOnce attr_once;
     if (int rc = once_per_device(attr_once, "kle_fine(factor): cudaFuncSetAttribute", [&] {
@@ -661,9 +671,10 @@ struct FineInst {
       return rc;
     constexpr int SPW = FactorSmem<MR, P>::SPW;
     const char* e = getenv("KLE_FGR_SC");
-    const int sc_on = e && *e == '1';
+    const int sc_on = force_sc || (e && *e == '1');
     if (M > 0)
-      fine_factor_kernel<MR, P><<<(unsigned)((M + SPW - 1) / SPW), 32, smem, st>>>(dia, off, blob, M, nx, h, g0, sc_on);
+      fine_factor_kernel<MR, P><<<(unsigned)((M + SPW - 1) / SPW), 32, smem, st>>>(dia, off, blob, M, nx, h, g0, sc_on,
+                                                                                   stride, offset);
     return check_launch("fine_factor_kernel");
   }
   static int fgr(const FgrArgs& a, cudaStream_t st) {
@@ -695,6 +706,7 @@ struct FineInst {
     if (a.tw_none_flagged) return KLE_OK;
     FgrArgs b = a;
     b.tw_fallback = 1;
+    b.flag_off = FineLayout<MR, P>::SC_FLAG;
     return fgr(b, st);
   }
   static int sweep(const SweepArgs& a, cudaStream_t st) {
@@ -801,6 +813,9 @@ int fine_factor(FineLayoutRT lay, const double* dia, const double* off, double* 
     return set_error(KLE_ERR_UNSUPPORTED, "fine_factor: unsupported nx");
   };
   if (int rc = base()) return rc;
+  // the (64, 8) blob with the scaled tables of the eight-lane sweep (kle_fine_pw.cu) behind the (16, 32) blob
+  if (lay.kind == 0 && !lay.W && lay.MR == 16 && lay.P == 32 && !KLE_FINE_LAZY)
+    return FineInst<64, 8, 1, 0>::factor(dia, off, blob, M, nx, h, g0, st, 1, lay.doubles, FineLayout<16, 32>::PW_OFF);
   // the twisted two-lane tables (kle_fine_tw.cu) go into the blob's spare part
   if (tw_supported(lay, nx)) return tw_factor(dia, off, blob, M, nx, h, g0, st);
   return KLE_OK;
@@ -814,6 +829,14 @@ int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
     lay.pipe = 0;
     lay.R = (lay.MR == 16) ? 3 : (lay.P == 32 ? 4 : 2);
   }
+  if (!a.F_given && !a.F_out && a.Rout && pw_supported(lay, a.nx)) {
+    if (int rc = pw_fgr(a, st)) return rc;
+    if (a.tw_none_flagged) return KLE_OK;
+    FgrArgs b = a;  // samples without a scaled form: the partitioned kernel
+    b.tw_fallback = 1;
+    b.flag_off = pw_flag_offset();
+    KLE_FINE_ALL(fgr(b, st))
+  }
   if (!a.F_given && sc_supported(lay)) {
     return FineInst<16, 32, 3, 2>::fgr_sc(a, st);
   }
@@ -822,6 +845,7 @@ int fine_fgr(FineLayoutRT lay, const FgrArgs& a, cudaStream_t st) {
     if (a.tw_none_flagged) return KLE_OK;
     FgrArgs b = a;  // samples without a scaled twisted form (flagged by tw_factor): the partitioned kernel
     b.tw_fallback = 1;
+    b.flag_off = kTwFlagOff;
     KLE_FINE_ALL(fgr(b, st))
   }
   KLE_FINE_ALL(fgr(a, st))

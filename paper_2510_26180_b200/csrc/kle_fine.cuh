@@ -36,8 +36,11 @@ struct FineLayout {
   static constexpr int SC_AF = SG2_OFF, SC_BB = SC_AF + LOGP * P, SC_RHO = SC_BB + LOGP * P, SC_Q = SC_RHO + P;
   static constexpr int SC_FLAG = SC_Q + P;
   static constexpr bool SC_FITS = 2 * LOGP * P + 2 * P + 1 <= NXP;
-  // the (16, 8) blob carries the twisted two-lane tables (kle_fine_tw.cu) from PHI_OFF on
-  static constexpr int DOUBLES = 6 * NXP + 2 * LOGP * P + ((MR == 16 && P == 8) ? 256 : 0);
+  // the (16, 8) blob carries the twisted two-lane tables (kle_fine_tw.cu) from PHI_OFF on; the (16, 32) blob
+  // is followed by a (64, 8) blob with the scaled tables for the eight-lane sweep (kle_fine_pw.cu) at PW_OFF
+  static constexpr int PW_OFF = 6 * NXP + 2 * LOGP * P;
+  static constexpr int DOUBLES =
+      6 * NXP + 2 * LOGP * P + ((MR == 16 && P == 8) ? 256 : 0) + ((MR == 16 && P == 32) ? 6 * 512 + 48 : 0);
 };
 constexpr int kTwFlagOff = FineLayout<16, 8>::PHI_OFF + 640;  // per-sample "no twisted form" flag (double)
 

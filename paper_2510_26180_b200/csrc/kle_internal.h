@@ -67,7 +67,9 @@ struct FgrArgs {
   const int32_t* active;  // [M] sample status (0 = active) or null
   int M, N, nx, J;
   double dt, dT, g0, alpha;
-  int tw_fallback = 0;    // 1: only the samples flagged by tw_factor (kle_fine_tw.cu); (16, 8) layout
+  int tw_fallback = 0;    // 1: only the samples whose blob carries a nonzero flag at flag_off (the samples the
+                          // twisted / scaled / eight-lane kernel skipped)
+  int flag_off = 0;       // offset (doubles) of that flag in a sample's blob
   int tw_none_flagged = 0;  // the caller counted the flags (tw_count_flagged): no fallback launch needed
 };
 
@@ -131,6 +133,11 @@ int sf_sweep(FineLayoutRT lay, const SweepArgs& a, cudaStream_t st);
 bool tw_supported(const FineLayoutRT& lay, int nx);
 bool sc_supported(const FineLayoutRT& lay);  // scaled partitioned sweep (be_steps_sc), P = 32 layouts
 int sc_flag_offset(const FineLayoutRT& lay);
+// eight-lane scaled sweep for 128 < nx <= 512 (kle_fine_pw.cu): 64 rows of one right-hand side per lane,
+// coefficients from shared memory; tables = a (64, 8) blob behind the (16, 32) blob
+bool pw_supported(const FineLayoutRT& lay, int nx);
+int pw_flag_offset();
+int pw_fgr(const FgrArgs& a, cudaStream_t st);
 int tw_factor(const double* dia, const double* off, double* blob, int M, int nx, double h, double g0,
               cudaStream_t st);
 int tw_fgr(const FgrArgs& a, cudaStream_t st);

@@ -776,10 +776,12 @@ def test_scaled_partitioned_sweep_matches_unscaled_and_dense(cuda, N, nx, J, mon
     status[1] = 1
     R_sc = torch.full((M, N, nx), 123.0, dtype=torch.float64, device="cuda")
     R_un = R_sc.clone()
+    monkeypatch.setenv("KLE_FGR_PW", "0")
     monkeypatch.setenv("KLE_FGR_SC", "1")
     _fgr(op, tables, U, R_sc, J, grid, alpha, status=status)
     monkeypatch.delenv("KLE_FGR_SC")
     _fgr(op, tables, U, R_un, J, grid, alpha, status=status)
+    monkeypatch.delenv("KLE_FGR_PW")
     assert float((R_sc[1] - 123.0).abs().max()) == 0.0
     assert torch.equal(R_sc[3], R_un[3])
     scale = float(R_un.abs().max())
@@ -797,3 +799,57 @@ def test_scaled_partitioned_sweep_matches_unscaled_and_dense(cuda, N, nx, J, mon
         prev = alpha * Uh[s, N - 1] if n == 0 else Uh[s, n - 1]
         want = sc[n] * (x + grid.deltaT * (A @ x) - prev)
         assert rel(R_sc[s, n].cpu().numpy(), want) <= 1e-10
+
+
+@pytest.mark.parametrize("N,nx,J", [(64, 511, 4), (5, 300, 3), (13, 129, 2), (8, 512, 2), (40, 450, 1)])
+def test_eight_lane_scaled_sweep_matches_partitioned_and_dense(cuda, N, nx, J, monkeypatch):
+    """The eight-lane scaled sweep (kle_fine_pw.cu, the default for 128 < nx <= 512:
+    64 rows of one right-hand side per lane, coefficients from shared memory, the
+    scaled partitioned step) against the default partitioned kernel and a dense
+    evaluation of scaling_n ((I + dT A) F_n - prev_n); a masked sample stays
+    untouched and a sample without a scaled form (a vanishing coupling) comes out
+    of the partitioned kernel (KLE_FGR_PW=0) bitwise."""
+    import torch
+
+    from paper_2510_26180_b200 import make_time_grid
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import _fgr, build_alpha_circulant
+
+    rng = np.random.default_rng(11000 * N + nx)
+    M, alpha, g0 = 5, 1e-3, 0.7
+    grid = make_time_grid(1.0, N, max(J, 2))
+    off = rng.uniform(0.1, 1.0, (M, nx)) * 4000.0
+    off[:, -1] = 0.0
+    off[3, nx // 3] = 0.0
+    dia = rng.uniform(0.5, 1.5, (M, nx)) + off + np.concatenate([np.zeros((M, 1)), off[:, :-1]], axis=1)
+    u0 = rng.normal(size=nx)
+    op = DeviceOperator(to_dev(dia), to_dev(-off), g0, to_dev(u0))
+    tables = AlphaTables(build_alpha_circulant(N, alpha))
+    U = to_dev(rng.normal(size=(M, N, nx)))
+    status = torch.zeros(M, dtype=torch.int32, device="cuda")
+    status[1] = 1
+    R_pw = torch.full((M, N, nx), 123.0, dtype=torch.float64, device="cuda")
+    R_un = R_pw.clone()
+    J = max(J, 2)
+    _fgr(op, tables, U, R_pw, J, grid, alpha, status=status)
+    monkeypatch.setenv("KLE_FGR_PW", "0")
+    _fgr(op, tables, U, R_un, J, grid, alpha, status=status)
+    monkeypatch.delenv("KLE_FGR_PW")
+    assert float((R_pw[1] - 123.0).abs().max()) == 0.0
+    assert torch.equal(R_pw[3], R_un[3])
+    assert torch.isfinite(R_pw).all()
+    scale = float(R_un.abs().max())
+    assert float((R_pw - R_un).abs().max()) <= 1e-12 * scale
+    assert not torch.equal(R_pw[0], R_un[0])
+    sc = tables.scaling.cpu().numpy()
+    Uh = U.cpu().numpy()
+    s = 4
+    A = np.diag(dia[s]) - np.diag(off[s, :-1], 1) - np.diag(off[s, :-1], -1)
+    T = np.eye(nx) + grid.deltat * A
+    for n in range(0, N, max(1, N // 4)):
+        x = u0 if n == 0 else Uh[s, n - 1]
+        for _ in range(J):
+            x = np.linalg.solve(T, x + grid.deltat * g0)
+        prev = alpha * Uh[s, N - 1] if n == 0 else Uh[s, n - 1]
+        want = sc[n] * (x + grid.deltaT * (A @ x) - prev)
+        assert rel(R_pw[s, n].cpu().numpy(), want) <= 1e-10
