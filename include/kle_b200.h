@@ -82,9 +82,11 @@ int kle_kl_tridiag_f64(const double* xi, int M, int d, const double* kl_table, i
  * factorisation, row scaling, steady state A x* = g0) and a per-sample flag
  * for samples without such a form (vanishing couplings, A without positive
  * pivots); kle_fgr_f64 sends flagged samples through the partitioned kernel.
- * Environment (read per call): KLE_FGR_TW=0 disables the twisted sweep,
- * KLE_FGR_SC=1 (set when factoring AND sweeping) selects the scaled
- * partitioned step for 128 < nx <= 512. */
+ * For 128 < nx <= 512 it carries a second, (64, 8)-chunked blob with the
+ * tables of the eight-lane scaled sweep (kle_fine_pw.cu), with the same flag
+ * mechanism. Environment (read per call): KLE_FGR_TW=0 / KLE_FGR_PW=0 disable
+ * those sweeps, KLE_FGR_SC=1 (set when factoring AND sweeping) selects the
+ * scaled step of the partitioned kernel for 128 < nx <= 512. */
 int kle_fine_factor_f64(const double* dia, const double* off, int M, int nx, double h, double g0,
                         double* blob, void* stream);
 
