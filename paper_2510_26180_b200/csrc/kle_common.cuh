@@ -40,7 +40,7 @@ __host__ __device__ inline int fine_blob_doubles(int MR, int P) {
   while ((1 << logp) < P) ++logp;
   // l, 1/beta, scan multipliers, lazy-stitch vectors; (16, 8): the twisted two-lane tables (kle_fine_tw.cu)
   // (16, 32): followed by the (64, 8) blob of the eight-lane sweep (kle_fine_pw.cu)
-  return 6 * MR * P + 2 * logp * P + ((MR == 16 && P == 8) ? 256 : 0) + ((MR == 16 && P == 32) ? 6 * 512 + 48 : 0);
+  return 6 * MR * P + 2 * logp * P + ((MR == 16 && P == 8) ? 256 : 0) + ((MR == 16 && P == 32) ? 8 * 512 + 72 : 0);
 }
 
 struct Cplx {

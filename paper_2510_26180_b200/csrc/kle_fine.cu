@@ -269,9 +269,37 @@ __global__ void __launch_bounds__(32) fine_factor_kernel(const double* __restric
     const double* bq = fsm + q * FS::PER;
     // l, 1/beta and the scan multipliers (+ lazy vectors / the scaled tables; without them every sample is
     // flagged, so a later KLE_FGR_SC=1 sweep on this blob falls through to the unscaled kernel)
-    const int ns = (FS::SC && !sc_on) ? L::PHI_OFF : FS::BS;
-    for (int i = lane; i < ns; i += 32) out[i] = bq[i];
-    if (FS::SC && !sc_on && lane == 0) out[L::SC_FLAG] = 1.0;
+    if constexpr (MR == 64 && P == 8) {
+      // packed for kle_fine_pw.cu (kle_fine.cuh: kPw*): row r -> entry (j = r & 63, kq = r >> 6)
+      //   T0 {1/beta, l_{r+1}^2}   T1 {sg pairs}   T2 {x*, 1/t}   T3 {t, dia}   T4 {off[r-1] pairs}
+      for (int r = lane; r < NXP; r += 32) {
+        const int j = r & 63, kq = r >> 6, e = (j * P + kq) * 2, e2 = ((j >> 1) * P + kq) * 2 + (j & 1);
+        const bool real = r < nx;
+        const double ln1 = (j < 63 && r + 1 < nx) ? bq[L::L_OFF + r + 1] : 0.0;
+        const double tv = real ? bq[L::SC_T + r] : 0.0;
+        out[0 * NXP + e] = real ? bq[L::INV_OFF + r] : 0.0;
+        out[0 * NXP + e + 1] = ln1 * ln1;
+        out[2 * NXP + e2] = bq[L::SC_IT + r];  // sg_r
+        out[3 * NXP + e] = real ? bq[L::SC_XS + r] : 0.0;
+        out[3 * NXP + e + 1] = real ? 1.0 / tv : 0.0;
+        out[5 * NXP + e] = tv;
+        out[5 * NXP + e + 1] = real ? dia[(size_t)sq * nx + r] : 0.0;
+        out[7 * NXP + e2] = (real && r > 0) ? off[(size_t)sq * nx + r - 1] : 0.0;
+      }
+      for (int i = lane; i < 24; i += 32) {
+        out[kPwAf + i] = bq[L::SC_AF + i];
+        out[kPwBb + i] = bq[L::SC_BB + i];
+      }
+      if (lane < 8) {
+        out[kPwRho + lane] = bq[L::SC_RHO + lane];
+        out[kPwQ + lane] = bq[L::SC_Q + lane];
+      }
+      if (lane == 0) out[kPwFlag] = bq[L::SC_FLAG];
+    } else {
+      const int ns = (FS::SC && !sc_on) ? L::PHI_OFF : FS::BS;
+      for (int i = lane; i < ns; i += 32) out[i] = bq[i];
+      if (FS::SC && !sc_on && lane == 0) out[L::SC_FLAG] = 1.0;
+    }
   }
   (void)g0;
 }

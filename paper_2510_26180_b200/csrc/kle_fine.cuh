@@ -15,6 +15,12 @@
 
 namespace kle {
 
+// The eight-lane sweep's tables (kle_fine_pw.cu), packed by fine_factor_kernel<64, 8> in the kernel's shared-
+// memory order so that its prologue is a straight 16-byte copy: five tables of 16-byte entries (8 x 512
+// doubles), the scan multipliers af[3][8], bb[3][8], rho[8], q[8], the flag
+constexpr int kPwTables = 8 * 512, kPwAf = kPwTables, kPwBb = kPwAf + 24, kPwRho = kPwBb + 24, kPwQ = kPwRho + 8,
+              kPwFlag = kPwQ + 8, kPwBlobDoubles = kPwFlag + 8;
+
 template <int MR, int P>
 struct FineLayout {
   static constexpr int LOGP = ilog2c(P);
@@ -40,7 +46,7 @@ struct FineLayout {
   // is followed by a (64, 8) blob with the scaled tables for the eight-lane sweep (kle_fine_pw.cu) at PW_OFF
   static constexpr int PW_OFF = 6 * NXP + 2 * LOGP * P;
   static constexpr int DOUBLES =
-      6 * NXP + 2 * LOGP * P + ((MR == 16 && P == 8) ? 256 : 0) + ((MR == 16 && P == 32) ? 6 * 512 + 48 : 0);
+      6 * NXP + 2 * LOGP * P + ((MR == 16 && P == 8) ? 256 : 0) + ((MR == 16 && P == 32) ? kPwBlobDoubles : 0);
 };
 constexpr int kTwFlagOff = FineLayout<16, 8>::PHI_OFF + 640;  // per-sample "no twisted form" flag (double)
 

@@ -17,9 +17,10 @@
 //   w_j  = wl_j + sg_j X             (DFMA; X from the backward scan)
 // with three coefficient doubles per row (inv, kk, sg) read as 16-byte broadcast loads.
 //
-// The tables are the (64, 8) blob that fine_factor writes behind the (16, 32) blob (FineLayout::PW_OFF):
-// l, 1/beta, x*, t, 1/t, the scan multipliers and the per-sample flag for samples without a scaled form,
-// which this kernel skips and the partitioned kernel processes (FgrArgs::tw_fallback).
+// The tables are written by fine_factor_kernel<64, 8> behind the (16, 32) blob (FineLayout::PW_OFF), packed
+// in this kernel's shared-memory order (kle_fine.cuh: kPw*): {1/beta, l^2}, sg, {x*, 1/t}, {t, dia}, off, the
+// scan multipliers and the per-sample flag for samples without a scaled form, which this kernel skips and
+// the partitioned kernel processes (FgrArgs::tw_fallback).
 #include <algorithm>
 #include <cstdlib>
 
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(128, 2) fgr_pw_kernel(FgrArgs a) {
   const int s = blockIdx.x;
   if (a.active && a.active[s] != KLE_SAMPLE_ACTIVE) return;
   const double* bl = a.ffac + (size_t)s * PwOuter::DOUBLES + PwOuter::PW_OFF;  // the sample's (64, 8) blob
-  if (bl[PwL::SC_FLAG] != 0.0) return;  // no scaled form: the partitioned kernel takes it
+  if (bl[kPwFlag] != 0.0) return;  // no scaled form: the partitioned kernel takes it
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   // lane = 8 (k / 2) + 2 slot + (k & 1): a quarter-warp holds two chunks of all four systems, so that a 16-byte
   // coefficient load touches two distinct entries per quarter-warp (as in the twisted kernel, 2 shared-memory
@@ -113,38 +114,23 @@ __global__ void __launch_bounds__(128, 2) fgr_pw_kernel(FgrArgs a) {
     for (int r = tid; r < nx; r += 128) cp_async8(st_s + (unsigned)((PW_NC * LD + r + (r >> 6)) * sizeof(double)), src + r);
   }
   asm volatile("cp.async.commit_group;\n" ::);
-  // tables, row r -> entry (j = r & 63, k = r >> 6)
+  // the tables, packed by fine_factor_kernel<64, 8> in this kernel's shared-memory order (16-byte copies)
   {
-    const double* dg = a.dia + (size_t)s * nx;
-    const double* eg = a.off + (size_t)s * nx;
+    const unsigned tb0 = (unsigned)__cvta_generic_to_shared(sm);
 #pragma unroll
-    for (int it = 0; it < H * P / 128; ++it) {  // unrolled: the 4 x 7 global loads of a thread go out together
-      const int r = tid + it * 128;
-      const int j = r & 63, kq = r >> 6;
-      const bool real = r < nx;
-      const double ln1 = (j < 63 && r + 1 < nx) ? bl[PwL::L_OFF + r + 1] : 0.0;
-      double* t0 = sm + PW_T0 + (j * P + kq) * 2;
-      t0[0] = real ? bl[PwL::INV_OFF + r] : 0.0;
-      t0[1] = ln1 * ln1;
-      double* t2 = sm + PW_T2 + (j * P + kq) * 2;
-      t2[0] = real ? bl[PwL::SC_XS + r] : 0.0;
-      const double tv = real ? bl[PwL::SC_T + r] : 0.0;
-      t2[1] = real ? 1.0 / tv : 0.0;
-      double* t3 = sm + PW_T3 + (j * P + kq) * 2;
-      t3[0] = tv;
-      t3[1] = real ? dg[r] : 0.0;
-      sm[PW_T4 + ((j >> 1) * P + kq) * 2 + (j & 1)] = (real && r > 0) ? eg[r - 1] : 0.0;
-      sm[PW_T1 + ((j >> 1) * P + kq) * 2 + (j & 1)] = bl[PwL::SC_IT + r];  // sg_j (fine_factor_kernel<64, 8>)
-    }
+    for (int i = 0; i < kPwTables / 2 / 128; ++i)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tb0 + (unsigned)((tid + 128 * i) * 16)),
+                   "l"(bl + (tid + 128 * i) * 2));
   }
+  asm volatile("cp.async.commit_group;\n" ::);
   double af[PwL::LOGP], bb[PwL::LOGP];
 #pragma unroll
   for (int t = 0; t < PwL::LOGP; ++t) {
-    af[t] = bl[PwL::SC_AF + t * P + k];
-    bb[t] = bl[PwL::SC_BB + t * P + k];
+    af[t] = bl[kPwAf + t * P + k];
+    bb[t] = bl[kPwBb + t * P + k];
   }
-  const double rho = bl[PwL::SC_RHO + k];
-  asm volatile("cp.async.wait_group 1;\n" ::);
+  const double rho = bl[kPwRho + k];
+  asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
 
   // w = (x - x*) / t
@@ -274,7 +260,7 @@ bool pw_supported(const FineLayoutRT& lay, int nx) {
   return !(e && *e == '0');
 }
 
-int pw_flag_offset() { return PwOuter::PW_OFF + PwL::SC_FLAG; }
+int pw_flag_offset() { return PwOuter::PW_OFF + kPwFlag; }
 
 int pw_fgr(const FgrArgs& a, cudaStream_t st) {
   constexpr size_t smem = sizeof(double) * (size_t)PW_SMEM_DOUBLES;
