@@ -379,7 +379,8 @@ def run_b200(args):
     # per step: kl_tridiag, fine_factor, gpc basis + 1-2 GEMMs, shift_factor, then per outer iteration and
     # sample pipeline (two when the batch is large, kle_capi.cu) one fgr and one CGC launch (an upper bound:
     # a pipeline stops as soon as its own samples have converged), and 2 x (2 col-sum + 1 scale) for the moments
-    pipes = 2 if (M >= 8192 and os.environ.get("KLE_PCGC_PIPES", "2") != "1") else 1
+    tw_small = 64 < c["nx"] <= 128 and c["N"] <= 16 and os.environ.get("KLE_FGR_TW", "1") != "0"
+    pipes = int(os.environ.get("KLE_PCGC_PIPES", "1" if tw_small else "2")) if M >= 8192 else 1
     # the twisted two-lane fine sweep (kle_fine_tw.cu, 64 < nx <= 128) adds its table kernel and the count of the
     # samples flagged as having no scaled form (none here, so the partitioned fallback kernel is never launched)
     tw_path = 64 < c["nx"] <= 128 and os.environ.get("KLE_FGR_TW", "1") != "0"
