@@ -111,8 +111,11 @@ __device__ __forceinline__ void cp_async16(unsigned sa, const void* gmem) {
 // ---------------------------------------------------------------------------
 namespace {
 constexpr int TW_SPW = 8;
-// per sample: the tables, (y, 1/b) of the steady-state solve, and the operator rows (staged coalesced)
-constexpr int TW_FSM = TW_DOUBLES + 2 * 2 * TW_H + 2 * 2 * TW_H;
+// per sample: the tables (without the flag, which goes straight to global memory) and the operator rows
+// (staged coalesced); the steady-state solve keeps (y, 1/b) in the S slots that x* and 1/t take over later.
+// 896 doubles: four CTAs (32 samples) per SM
+constexpr int TW_STAGED = 10 * TW_H;
+constexpr int TW_FSM = TW_STAGED + 2 * 2 * TW_H;
 }
 
 __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict__ dia, const double* __restrict__ off,
@@ -124,12 +127,12 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
   const int s = blockIdx.x * TW_SPW + ls;
   const bool live = s < M;
   double* tab = fsm + ls * TW_FSM;
-  double* scr = tab + TW_DOUBLES + side * 2 * H;  // [H][2]: y_j, 1 / b_j
-  const double* dd = tab + TW_DOUBLES + 4 * H;    // [2 H]
+  double* scr = tab + twS(0, side);               // y_j, 1 / b_j at scr[4 j], scr[4 j + 1] (the S slots)
+  const double* dd = tab + TW_STAGED;             // [2 H]
   const double* ee = dd + 2 * H;                  // [2 H]: ee[i] couples rows i, i+1
   for (int q = 0; q < TW_SPW; ++q) {
     const int sq = blockIdx.x * TW_SPW + q;
-    double* dq = fsm + q * TW_FSM + TW_DOUBLES + 4 * H;
+    double* dq = fsm + q * TW_FSM + TW_STAGED;
     for (int i = lane; i < 2 * H; i += 32) {
       dq[i] = (sq < M && i < nx) ? dia[(size_t)sq * nx + i] : 1.0;
       dq[2 * H + i] = (sq < M && i + 1 < nx) ? off[(size_t)sq * nx + i] : 0.0;
@@ -162,8 +165,8 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
       }
       tab[twT(j, side)] = (j >= pad) ? t : 0.0;
     } else {
-      scr[2 * j] = y_prev;
-      scr[2 * j + 1] = ib;
+      scr[4 * j] = y_prev;
+      scr[4 * j + 1] = ib;
     }
     ib_prev = ib;
   }
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
       if (j >= pad && g0 != 0.0) {
         const int row = side ? nx - 1 - (j - pad) : j - pad;
         const double e = ee[side ? row - 1 : row];  // couples local rows j, j+1
-        v = fma(-e, xn, scr[2 * j]) * scr[2 * j + 1];
+        v = fma(-e, xn, scr[4 * j]) * scr[4 * j + 1];
         bad |= !(fabs(v) <= 1e150);
       }
       tab[twS(j, side)] = v;
@@ -197,9 +200,10 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
   }
   bad = (__ballot_sync(KLE_FULL_MASK, bad && live) >> base) & 0xfu;
   __syncwarp();
-  if (role == 0) {
-    tab[TW_FLAG] = bad ? 1.0 : 0.0;
-    tab[TW_FLAG + 1] = 0.0;
+  if (role == 0 && live) {
+    double* fl = blob + (size_t)s * TwL::DOUBLES + TwL::PHI_OFF + TW_FLAG;
+    fl[0] = bad ? 1.0 : 0.0;
+    fl[1] = 0.0;
   }
   // 1 / t_j by all lanes (off the chains)
   for (int i = lane; i < TW_SPW * 2 * H; i += 32) {
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
     if (sq >= M) break;
     double* out = blob + (size_t)sq * TwL::DOUBLES + TwL::PHI_OFF;
     const double* tb = fsm + q * TW_FSM;
-    for (int i = lane; i < TW_DOUBLES; i += 32) out[i] = tb[i];
+    for (int i = lane; i < TW_STAGED; i += 32) out[i] = tb[i];
   }
 }
 
