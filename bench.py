@@ -436,6 +436,15 @@ def run_b200(args):
                 "peak_source": peaks.get("fp64_source"),
                 "algorithmic": f"{FLOPS_PER_DOF:g} flop per fine DOF-update x M*N*J*nx per launch (M = rank shard)",
                 "executed_flop_per_dof_update": 4 if tw_path else 7 if pw_path else 10,
+                # the twisted / eight-lane sweeps read their factor rows as shared-memory broadcasts: ncu's
+                # shared-memory wavefront utilisation of the kernel (profiles/traffic.json), the resource that
+                # binds them beside the FP64 pipe
+                "shared_wavefronts_pct_ncu": ncu_field(peaks, args.config,
+                                                       "fgr_tw_kernel" if tw_path else "fgr_pw_kernel" if pw_path
+                                                       else "fgr_kernel", "shared_wavefronts_pct"),
+                "fp64_pipe_pct_ncu": ncu_field(peaks, args.config,
+                                               "fgr_tw_kernel" if tw_path else "fgr_pw_kernel" if pw_path
+                                               else "fgr_kernel", "fp64_pipe_pct"),
                 "hbm_frac": (fgr_bytes / (fgr_ms * 1e-3) / 1e9) / peaks["hbm_gbs"],
                 "ms_per_launch": fgr_ms,
             },
@@ -461,6 +470,10 @@ def run_b200(args):
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ncu_field(peaks, config, kernel, field):
+    return peaks.get("traffic", {}).get(config, {}).get(kernel, {}).get(field)
 
 
 def traffic_of(peaks, config, kernel, M):
