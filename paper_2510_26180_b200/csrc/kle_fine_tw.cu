@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
       y_prev = fma(-l, y_prev, g0);
       nl = -l;
       if (j > pad) t *= nl;  // t_j = nl_j t_{j-1}
-      bad |= !(beta > 0.0) || (!steady && !(fabs(t) >= 1e-150 && fabs(t) <= 1e150));
+      // (without a source there is no steady state to solve for: A may be singular then)
+      bad |= (!(beta > 0.0) && (!steady || g0 != 0.0)) || (!steady && !(fabs(t) >= 1e-150 && fabs(t) <= 1e150));
     }
     if (!steady) {
       if (j > 0) {  // row j-1: its own inv (known one trip ago) and nl_j^2
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(32) tw_factor_kernel(const double* __restrict_
   const double y_o = __shfl_sync(KLE_FULL_MASK, y_prev, base + (role ^ 1));
   const double E = hs * ee[mT - 1];
   const double idet = 1.0 / fma(beta, b_o, -E * E);
-  bad |= !(fabs(idet) <= 1e150);
+  bad |= !(fabs(idet) <= 1e150) && (!steady || g0 != 0.0);
   if (!steady) {
     tab[twA(H - 1, side)] = b_o * idet;                   // ca: own y
     tab[twA(H - 1, side) + 1] = -E * idet * (t_o / t);    // cb': partner's y

@@ -744,7 +744,8 @@ def test_twisted_fine_sweep_without_source(cuda, monkeypatch):
     monkeypatch.setenv("KLE_FGR_TW", "0")
     _fgr(op, tables, U, R_pt, J, grid, alpha)
     monkeypatch.delenv("KLE_FGR_TW")
-    assert not torch.equal(R_tw, R_pt)
+    for s in range(M):  # (the twisted kernel took every sample)
+        assert not torch.equal(R_tw[s], R_pt[s])
     assert float((R_tw - R_pt).abs().max()) <= 1e-12 * float(R_pt.abs().max())
 
 
@@ -853,3 +854,32 @@ def test_eight_lane_scaled_sweep_matches_partitioned_and_dense(cuda, N, nx, J, m
         prev = alpha * Uh[s, N - 1] if n == 0 else Uh[s, n - 1]
         want = sc[n] * (x + grid.deltaT * (A @ x) - prev)
         assert rel(R_pw[s, n].cpu().numpy(), want) <= 1e-10
+
+
+def test_eight_lane_sweep_without_source(cuda, monkeypatch):
+    """g0 = 0 with a singular (Neumann-like) A: no steady state is needed, so the
+    eight-lane sweep must still take every sample (not the fallback)."""
+    import torch
+
+    from paper_2510_26180_b200 import make_time_grid
+    from paper_2510_26180_b200.device import AlphaTables, DeviceOperator, to_dev
+    from paper_2510_26180_b200.pcgc import _fgr, build_alpha_circulant
+
+    rng = np.random.default_rng(6)
+    M, N, nx, J, alpha = 3, 20, 333, 5, 1e-2
+    grid = make_time_grid(0.5, N, J)
+    off = rng.uniform(0.1, 1.0, (M, nx)) * 1000.0
+    off[:, -1] = 0.0
+    dia = off + np.concatenate([np.zeros((M, 1)), off[:, :-1]], axis=1)
+    op = DeviceOperator(to_dev(dia), to_dev(-off), 0.0, to_dev(rng.normal(size=nx)))
+    tables = AlphaTables(build_alpha_circulant(N, alpha))
+    U = to_dev(rng.normal(size=(M, N, nx)))
+    R_pw = torch.zeros((M, N, nx), dtype=torch.float64, device="cuda")
+    R_pt = torch.zeros_like(R_pw)
+    _fgr(op, tables, U, R_pw, J, grid, alpha)
+    monkeypatch.setenv("KLE_FGR_PW", "0")
+    _fgr(op, tables, U, R_pt, J, grid, alpha)
+    monkeypatch.delenv("KLE_FGR_PW")
+    for s in range(M):
+        assert not torch.equal(R_pw[s], R_pt[s])
+    assert float((R_pw - R_pt).abs().max()) <= 1e-12 * float(R_pt.abs().max())
